@@ -1,0 +1,363 @@
+"""Benchmark: shadow-model train samples/s (+ MMD pairs/s) on B200.
+
+Workload (BASELINE.json configs[1], C2): mapping-based MMD transfer step of
+MLP 1024-512-256-10 with a 512 source + 512 target batch and 5-bandwidth
+Gaussian MMD on the 256-d hidden layer (CE + lambda*MMD, SGD), run for a
+bank of G=32 shadow models per GPU (C5's per-GPU, per-paradigm shadow
+share: 3 x 256 shadows / 8 GPUs / 3).  Weak scaling: every rank trains its
+own 32 shadows; no data-path collective (models are independent, SURVEY.md
+section 8(e)).  One step = one SGD step of all 32 models.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Prints ONE JSON line on rank 0 (contract in the task description).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+DIMS = [1024, 512, 256, 10]
+G = 32
+SRC, TGT = 512, 512
+B = SRC + TGT
+LAMBDA = 1.0
+LR = 0.01
+N_BW = 5
+# algorithmic cost
+FLOP_SRC = 2_898_944
+MMD_PAIRS = (B * (B - 1)) // 2  # 523,776 unique pairs per model per step
+MMD_FLOP_PER_PAIR = 4 * DIMS[2]  # fwd 2d + bwd 2d
+WORKLOAD = ("C2 mapping-based MMD transfer: MLP 1024-512-256-10, 512 src + 512 tgt, "
+            "5-bandwidth Gaussian MMD (lambda=1) on the 256-d hidden layer, SGD; bank of 32 "
+            "shadow models per GPU")
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("bf16_tflops"), d.get("bf16_tflops_sustained"), d.get("hbm_gbs"), "measured"
+    return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+class ClockSampler:
+    """SM clock + throttle reasons via NVML, polled every 5 ms in a thread, for
+    the duration of the `with` block (the timed region)."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.max_mhz = None
+        self._stop = threading.Event()
+
+    def __enter__(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+
+            def poll():
+                while not self._stop.is_set():
+                    try:
+                        self.samples.append(
+                            (pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+                             pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)))
+                    except Exception:
+                        pass
+                    time.sleep(0.005)
+
+            self.t = threading.Thread(target=poll, daemon=True)
+            self.t.start()
+        except Exception:
+            self.t = None
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.t:
+            self.t.join()
+
+    def summary(self):
+        sm = [s for s, _ in self.samples]
+        reasons = sorted({n for _, r in self.samples for n, bit in self.REASONS.items() if r & bit})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(sm), "source": "nvml, 5 ms poll"}
+
+
+def dist_setup(n_gpus):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ----------------------------------------------------------------------------- CPU arms
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_reference_sample(steps_per_thread=1, threads=None):
+    """Reference CPU path on the host cores: one C2 model per std::thread, each
+    running reference-Tape SGD steps (tape.hpp / optim.hpp, headers compiled
+    unmodified) + the oracle's f64 MMD injection.  Returns (samples/s, info)."""
+    import ctypes as C
+
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as po
+
+    threads = threads or cpu_threads()
+    R = po.ref()
+    dims = (C.c_int * 4)(*DIMS)
+    if R is not None:
+        secs = R.ref_bench_train(threads, 3, dims, B, SRC, steps_per_thread, LAMBDA, 1234)
+        kind = "reference"
+    else:  # oracle port (C restatement) in Python threads; ctypes drops the GIL
+        import numpy as np
+
+        def one(seed):
+            r = po.Rng(seed)
+            W, b = po.mlp_init(r, DIMS)
+            X = r.normals(B * DIMS[0]).reshape(B, DIMS[0])
+            y = np.array([r.below(10) for _ in range(B)], dtype=np.int32)
+            for _ in range(steps_per_thread):
+                _, H = po.mlp_forward(DIMS, W, b, X)
+                _, _, gs, gt = po.mmd_gaussian(H[:SRC], H[SRC:])
+                po.mlp_train_step(DIMS, W, b, X, y, lr=LR, dH=LAMBDA * np.concatenate([gs, gt]))
+
+        t0 = time.perf_counter()
+        ts = [threading.Thread(target=one, args=(s,)) for s in range(threads)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        secs = time.perf_counter() - t0
+        kind = "port"
+    samples = threads * steps_per_thread * B
+    return samples / secs, {
+        "kind": kind, "cores": threads,
+        "sample": f"{threads} C2 models x {steps_per_thread} SGD step(s) of {B} samples "
+                  f"(512 src + 512 tgt, 5-bw MMD), one model per thread",
+        "seconds": secs}
+
+
+def run_reference_arm(args, world, rank):
+    if rank != 0:
+        return
+    for _ in range(args.warmup if args.warmup < 1 else 1):
+        cpu_reference_sample(1)
+    t = []
+    for _ in range(args.steps):
+        v, info = cpu_reference_sample(1)
+        t.append(info["seconds"])
+    secs = sum(t)
+    value = args.steps * info["cores"] * B / secs
+    line = {
+        "metric": "shadow-model train samples/s", "value": value, "unit": "samples/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * secs / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": WORKLOAD + " (CPU: one model per host thread)",
+                   "global_batch": info["cores"] * B, "parallelism": "threads"},
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": info["cores"],
+                         "kind": info["kind"], "sample": info["sample"]},
+        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def run_gpu_arm(args, world, rank, local):
+    import numpy as np
+    import torch
+
+    from paper_2011_09463_b200 import api
+
+    torch.cuda.set_device(local)
+    ctx = api.Context(local)
+    bank = api.Bank(ctx, G, DIMS)
+    rng = api.Rng(20110946 + rank)
+    for g in range(G):
+        bank.init_params(g, rng)
+    gen = torch.Generator(device="cuda").manual_seed(1000 + rank)
+    X = torch.randn((G, B, DIMS[0]), device="cuda", generator=gen)
+    X[:, SRC:, :] += 0.5  # target-domain shift
+    y = torch.randint(0, DIMS[-1], (G, B), device="cuda", dtype=torch.int32, generator=gen)
+    step_kw = dict(lr=LR, src_rows=SRC, mmd_lambda=LAMBDA)
+
+    # warm-up (device-resident inputs)
+    for _ in range(max(args.warmup, 3)):
+        bank.train_step(X, y, want_loss=False, **step_kw)
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, inputs resident in HBM ----------------------------
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = ctx.launches
+    with ClockSampler(local) as clk:
+        barrier(world)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            bank.train_step(X, y, want_loss=False, **step_kw)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+    launches = ctx.launches - launches0
+    ms = max_over_ranks(e0.elapsed_time(e1), world)
+    ms_step = ms / args.steps
+    samples = world * G * B * args.steps
+    value = samples / (ms / 1000.0)
+
+    # ---- per-phase kernel timing (CUDA events on the launching stream) ---------------
+    ctx.set_timing(True)
+    for _ in range(args.steps):
+        bank.train_step(X, y, want_loss=False, **step_kw)
+    ph = ctx.phase_times()
+    ctx.set_timing(False)
+    # algorithmic flops per step, per phase (target rows are labelled, so every
+    # row pays the full 2,898,944 flop/sample of BASELINE.md's C2 source row)
+    macs = [DIMS[l] * DIMS[l + 1] for l in range(len(DIMS) - 1)]
+    phase_flop = {"fwd_gemm": 2 * G * B * sum(macs), "dx_gemm": 2 * G * B * sum(macs[1:]),
+                  "dw_gemm": 2 * G * B * sum(macs),
+                  "mmd_pairs": G * MMD_PAIRS * MMD_FLOP_PER_PAIR}
+    step_flop = G * B * FLOP_SRC
+    assert phase_flop["fwd_gemm"] + phase_flop["dx_gemm"] + phase_flop["dw_gemm"] == step_flop
+    gemm_ms = sum(ph[p][0] for p in ("fwd_gemm", "dx_gemm", "dw_gemm")) / args.steps
+    mmd_ms = ph["mmd_pairs"][0] / args.steps
+    mmd_flop = phase_flop["mmd_pairs"]
+    bf16, bf16_s, hbm, src = peaks()
+    tf32_peak = bf16 / 2.0  # dense tf32 tensor rate is half the bf16 rate
+    dominant = max(phase_flop, key=lambda p: ph[p][0])
+    dom_ms = ph[dominant][0] / args.steps  # this phase's launches per step, summed
+    achieved = phase_flop[dominant] / (dom_ms / 1000.0) / 1e12
+
+    # ---- e2e: through the C ABI with HOST buffers (H2D + loss D2H in the timed region)
+    Xh = X.cpu().pin_memory()
+    yh = y.cpu().pin_memory()
+    bank.train_step_host(Xh, yh, **step_kw)
+    torch.cuda.synchronize()
+    barrier(world)
+    t0 = time.perf_counter()
+    e0.record(stream)
+    for _ in range(args.steps):
+        bank.train_step_host(Xh, yh, want_loss=True, **step_kw)  # reads loss + mmd to host
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1), world)
+    e2e_value = world * G * B * args.steps / (e2e_ms / 1000.0)
+    h2d = G * B * DIMS[0] * 4 + G * B * 4
+    d2h = 2 * G * 8
+
+    if rank != 0:
+        return
+    cpu = None
+    if not args.no_cpu_baseline:
+        cv, info = cpu_reference_sample(1)
+        cpu = {"value": cv, "unit": "samples/s", "cores": info["cores"], "kind": info["kind"],
+               "sample": info["sample"]}
+    line = {
+        "metric": "shadow-model train samples/s",
+        "value": value,
+        "unit": "samples/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": WORKLOAD, "models_per_gpu": G, "global_batch": world * G * B,
+                   "batch_per_model": B, "dims": DIMS, "parallelism": f"shard{world}",
+                   "l2": "inputs 134 MB per step > 126 MB L2"},
+        "mmd": {"pairs_per_s": world * G * MMD_PAIRS * args.steps / (ms / 1000.0),
+                "unique_pairs_per_step": world * G * MMD_PAIRS,
+                "kernel_ms_per_step": mmd_ms,
+                "kernel_tflops": mmd_flop / (mmd_ms / 1000.0) / 1e12 if mmd_ms else None},
+        "phases_ms_per_step": {p: ph[p][0] / args.steps for p in ph},
+        "roofline": {"bound": "tensor", "kernel": dominant,
+                     "launches_per_step": ph[dominant][1] / args.steps, "achieved": achieved,
+                     "peak": tf32_peak, "unit": "TFLOP/s", "frac": achieved / tf32_peak,
+                     "traffic": None,
+                     "peak_note": f"dense tf32 = 1/2 of {src} bf16 {bf16} TFLOP/s"},
+        "step_tflops": step_flop / (ms_step / 1000.0) / 1e12,
+        "gemm_tflops": step_flop / (gemm_ms / 1000.0) / 1e12 if gemm_ms else None,
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        rank = int(os.environ.get("RANK", "0"))
+        run_reference_arm(args, world, rank)
+        return
+    world, rank, local = dist_setup(args.gpus)
+    try:
+        run_gpu_arm(args, world, rank, local)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

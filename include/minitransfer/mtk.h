@@ -1,0 +1,172 @@
+/*
+ * mtk.h -- C ABI of the B200 (sm_100a) shadow-training / MMD / membership-
+ * attack path.  Plain pointers and sizes only; no torch or C++ types.
+ *
+ * The reference (/root/reference/proj/include/minitransfer) exposes this path
+ * only as a C++ header API in namespace mt (Tape ops + optimizer_step); it has
+ * no FFI.  Each entry point below names the reference composition it replaces
+ * (file:line).  The C++ wrapper include/minitransfer/gpu.hpp maps the status
+ * codes back onto the reference exception classes (error.hpp:10-51).
+ *
+ * Conventions
+ *   - status codes (error.hpp:10-51):
+ *       0 OK, 1 ShapeError, 2 ValueError, 3 ConfigError, 4 DataError,
+ *       5 Error (internal / CUDA / non-finite).
+ *     mtk_last_error() returns the calling thread's message for the last
+ *     failing call.
+ *   - Arrays named X / y / w / logits / feats / scores / g* are DEVICE
+ *     pointers owned by the caller, unless the name ends in _host.
+ *     Host-side double arrays (parameters, metrics) are marked "host".
+ *   - Calls are stream-ordered on the context's stream and asynchronous,
+ *     except those that return host scalars (they synchronize).  Deferred
+ *     device-side errors (out-of-range label, non-finite value) are reported
+ *     by the next synchronizing call on the same context.
+ *   - Row-major fp32 on the device; f64 on the host at the parity API.
+ */
+#ifndef MINITRANSFER_MTK_H
+#define MINITRANSFER_MTK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MTK_OK 0
+#define MTK_SHAPE_ERROR 1
+#define MTK_VALUE_ERROR 2
+#define MTK_CONFIG_ERROR 3
+#define MTK_DATA_ERROR 4
+#define MTK_ERROR 5
+
+typedef struct mtk_ctx mtk_ctx;
+typedef struct mtk_bank mtk_bank;
+typedef struct mtk_rng mtk_rng;
+
+int mtk_version(void);
+const char* mtk_last_error(void);
+
+/* ---- context: one per (host thread, device); mirrors "one Tape per thread"
+ * (tape.hpp:84-85).  All work is ordered on `cuda_stream` (a cudaStream_t;
+ * NULL = the legacy default stream).                                       */
+int mtk_ctx_create(int device, void* cuda_stream, mtk_ctx** out);
+int mtk_ctx_destroy(mtk_ctx* ctx);
+int mtk_ctx_synchronize(mtk_ctx* ctx);
+/* number of kernels this library launched on ctx since creation */
+int mtk_ctx_launch_count(mtk_ctx* ctx, uint64_t* out);
+/* Optional CUDA-event timing of the bank step's phases, on the ctx stream.
+ * mtk_ctx_phase_times synchronizes and returns (then resets) the summed
+ * milliseconds and launch counts per phase, MTK_NUM_PHASES entries, in the
+ * order: fwd_gemm, ce, mmd_beta, mmd_pairs, dx_gemm, dw_gemm, bias_sgd, other */
+#define MTK_NUM_PHASES 8
+int mtk_ctx_set_timing(mtk_ctx* ctx, int on);
+int mtk_ctx_phase_times(mtk_ctx* ctx, double* ms_host, uint64_t* launches_host);
+
+/* ---- host RNG: bit-exact restatement of mt::Rng (rng.hpp:13-75) --------- */
+int mtk_rng_create(uint64_t seed, mtk_rng** out);
+int mtk_rng_destroy(mtk_rng* r);
+int mtk_rng_split(mtk_rng* parent, uint64_t stream, mtk_rng** out); /* rng.hpp:65-69 */
+uint64_t mtk_rng_next_u64(mtk_rng* r);                             /* rng.hpp:17 */
+double mtk_rng_uniform(mtk_rng* r, double lo, double hi);           /* rng.hpp:22 */
+double mtk_rng_normal(mtk_rng* r);                                  /* rng.hpp:24-37 */
+uint64_t mtk_rng_below(mtk_rng* r, uint64_t n);                     /* rng.hpp:39-46 */
+int mtk_rng_permutation(mtk_rng* r, uint64_t n, uint64_t* out_host); /* rng.hpp:58-63 */
+int mtk_rng_fill_normal(mtk_rng* r, double* out_host, uint64_t n);
+/* class-conditional Gaussians: y = below(C); x = mu[y] + N(0,I) (+ shift).
+ * X64_host (f64) and/or X32_host (fp32 copy) may be NULL.                  */
+int mtk_synth(mtk_rng* r, int C, int d, uint64_t n, const double* mu_host,
+              const double* shift_host, double* X64_host, float* X32_host, int32_t* y_host);
+
+/* ---- model bank: G independent MLPs dims[0] -> ... -> dims[n_layers], ReLU
+ * hidden layers, trained as ONE grouped step.  Replaces, per model, the Tape
+ * composition matmul (tape.hpp:225-290) -> add_bias (:204-221) -> relu
+ * (:342-352) -> ... -> cross_entropy_weighted (:475-520) -> backward
+ * (:870-886) -> optimizer_step SGD (optim.hpp:30-68).
+ * n_heads == 2 (parameter-based paradigm): a second head of the same shape
+ * as the last layer is stored as parameter matrix index n_layers; rows
+ * [0, src_rows) use head 0, rows [src_rows, B) head 1.                      */
+int mtk_bank_create(mtk_ctx* ctx, int G, int n_layers, const int* dims_host, int n_heads,
+                    mtk_bank** out);
+int mtk_bank_destroy(mtk_bank* bank);
+/* W_host[i] is [fan_in, fan_out] row-major f64, b_host[i] is [fan_out], for
+ * i in [0, n_layers + n_heads - 1).  Synchronizing.                         */
+int mtk_bank_set_params(mtk_bank* bank, int model, const double* const* W_host,
+                        const double* const* b_host);
+int mtk_bank_get_params(mtk_bank* bank, int model, double* const* W_host, double* const* b_host);
+/* SPEC.md:182 init drawn from r: W uniform(-1/sqrt(fan_in), 1/sqrt(fan_in))
+ * row-major, matrices in index order; b = 0.                                */
+int mtk_bank_init_params(mtk_bank* bank, int model, mtk_rng* r);
+/* device views of parameter matrix i: W [G, fan_in, fan_out], b [G, fan_out] */
+int mtk_bank_param_device(mtk_bank* bank, int mat, float** W, float** b);
+
+/* forward only (posterior query): X [G,B,dims[0]] ->
+ * logits [G,B,C] using head `head`; hidden_last [G,B,dims[n_layers-1]] or NULL */
+int mtk_bank_forward(mtk_bank* bank, const float* X, int B, int head, float* logits,
+                     float* hidden_last);
+
+typedef struct {
+    const float* X;     /* [G,B,dims[0]] device */
+    const int32_t* y;   /* [G,B] device, labels in [0, C) */
+    const float* w;     /* [G,B] device per-row CE weights, NULL = all 1 */
+    int B;              /* rows per model */
+    int src_rows;       /* rows [0,src_rows) = source; used by 2 heads and MMD */
+    double denom[2];    /* CE denominators head 0 / head 1; 0 selects the row count,
+                           negative is a ValueError (tape.hpp:485) */
+    double lr;          /* SGD learning rate (optim.hpp:46-48) */
+    int frozen_layers;  /* layers [0, frozen) keep bit-identical params */
+    double mmd_lambda;  /* > 0: + lambda * MMD^2(h_src, h_tgt) on the last hidden layer */
+    int mmd_nb;         /* bandwidth count (<= 8); 0 selects the 5-bandwidth default */
+    double mmd_mult[8]; /* s_b = beta * mmd_mult[b], beta detached (closed form) */
+} mtk_step;
+
+/* One SGD step for all G models.  loss_host [G] (CE part) and mmd_host [G]
+ * (MMD^2 value) are optional; passing either synchronizes.                  */
+int mtk_bank_train_step(mtk_bank* bank, const mtk_step* step, double* loss_host,
+                        double* mmd_host);
+/* Same step from HOST buffers (X_host [G,B,d0] fp32, y_host [G,B], w_host or
+ * NULL): the library stages them to the device on its stream.  Used for the
+ * end-to-end measurement; step->X/y/w are ignored.                          */
+int mtk_bank_train_step_host(mtk_bank* bank, const mtk_step* step, const float* X_host,
+                             const int32_t* y_host, const float* w_host, double* loss_host,
+                             double* mmd_host);
+/* debug/parity: keep the last step's parameter gradients (dW, db).          */
+int mtk_bank_set_keep_grads(mtk_bank* bank, int on);
+int mtk_bank_get_grads(mtk_bank* bank, int model, double* const* dW_host, double* const* db_host);
+
+/* ---- multi-bandwidth Gaussian MMD^2 (no reference
+ * code).  k(x,y) = sum_b exp(-|x-y|^2/(beta*mult[b])); beta <= 0 selects the
+ * detached closed form over [Xs;Xt].  Biased V-statistic.  gXs/gXt (device,
+ * optional) receive d MMD^2 / dX.  Synchronizing (returns host scalars).    */
+int mtk_mmd_gaussian(mtk_ctx* ctx, const float* Xs, int64_t m, const float* Xt, int64_t n, int d,
+                     const double* mult_host, int nb, double beta, double* value_host,
+                     double* beta_host, float* gXs, float* gXt);
+/* Row-sharded form for multi-GPU: only pair rows i in [row_begin, row_end)
+ * of the concatenated index space [Xs;Xt] are processed.  partial_host[3] =
+ * raw kernel sums (ss, tt, st) over those rows; gradients are written only
+ * for those rows.  beta must be given (> 0) so all shards agree.            */
+int mtk_mmd_gaussian_rows(mtk_ctx* ctx, const float* Xs, int64_t m, const float* Xt, int64_t n,
+                          int d, const double* mult_host, int nb, double beta, int64_t row_begin,
+                          int64_t row_end, double* partial_host, float* gXs, float* gXt);
+int mtk_mmd_beta(mtk_ctx* ctx, const float* Xs, int64_t m, const float* Xt, int64_t n, int d,
+                 double* beta_host);
+
+/* ---- attack stage -------------------------------------------------------- */
+/* Tape::softmax semantics (tape.hpp:433-464), fp32 out */
+int mtk_softmax(mtk_ctx* ctx, const float* logits, int64_t rows, int C, float* probs);
+/* top-k descending posteriors; with labels, one extra column = CE loss of
+ * the true label.  feats [rows, k (+1)]                                     */
+int mtk_posterior_features(mtk_ctx* ctx, const float* logits, int64_t rows, int C, int k,
+                           const int32_t* labels, float* feats);
+/* softmax probability of class `col` per row (attack score) */
+int mtk_posterior_column(mtk_ctx* ctx, const float* logits, int64_t rows, int C, int col,
+                         float* out);
+/* Mann-Whitney AUC with mid-ranks for ties + accuracy at 0.5 (either output
+ * may be NULL).  labels: 1 = member.  Synchronizing.                        */
+int mtk_auc(mtk_ctx* ctx, const float* scores, const uint8_t* labels, int64_t n,
+            double* auc_host, double* acc_host);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

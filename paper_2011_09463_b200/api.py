@@ -1,0 +1,325 @@
+"""Python host mirror of the reference interface for the shadow-training path.
+
+Names and argument meaning follow the reference's C++ API where one exists
+(``mt::Rng`` rng.hpp, the Tape ops composed by ``Bank.train_step``, SGD
+``optimizer_step`` optim.hpp) and SURVEY.md section 8(b) for the entry points
+the reference lacks (MMD, posterior features, AUC).  Every call goes through
+libmtk.so (CUDA, sm_100a) via the C ABI; torch only provides device memory
+and the stream.  Errors raise the classes in ``errors`` (error.hpp:10-51).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from . import errors
+from ._lib import MtkStep, lib
+
+_dp = C.POINTER(C.c_double)
+
+MMD_MULT = (0.25, 0.5, 1.0, 2.0, 4.0)
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if isinstance(t, torch.Tensor):
+        if not t.is_contiguous():
+            raise errors.ShapeError("tensor must be contiguous")
+        return C.c_void_p(t.data_ptr())
+    return C.c_void_p(int(t))
+
+
+def _dvec(a):
+    return (_dp * len(a))(*[x.ctypes.data_as(_dp) if x is not None else None for x in a])
+
+
+class Context:
+    """One per (thread, device); stream-ordered on torch's current stream."""
+
+    def __init__(self, device: int = 0, stream: torch.cuda.Stream | None = None):
+        self.device = device
+        torch.cuda.set_device(device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(device)
+        h = C.c_void_p()
+        errors.check(lib.mtk_ctx_create(device, C.c_void_p(self.stream.cuda_stream), C.byref(h)),
+                     "mtk_ctx_create")
+        self.h = h
+
+    def synchronize(self):
+        errors.check(lib.mtk_ctx_synchronize(self.h), "synchronize")
+
+    @property
+    def launches(self) -> int:
+        v = C.c_uint64()
+        errors.check(lib.mtk_ctx_launch_count(self.h, C.byref(v)))
+        return v.value
+
+    PHASES = ("fwd_gemm", "ce", "mmd_beta", "mmd_pairs", "dx_gemm", "dw_gemm", "bias_sgd", "other")
+
+    def set_timing(self, on: bool = True):
+        errors.check(lib.mtk_ctx_set_timing(self.h, 1 if on else 0))
+
+    def phase_times(self):
+        """{phase: (ms summed, launches)} since the last call (synchronizes)."""
+        ms = np.zeros(8)
+        n = np.zeros(8, dtype=np.uint64)
+        errors.check(lib.mtk_ctx_phase_times(self.h, ms.ctypes.data_as(_dp),
+                                             n.ctypes.data_as(C.POINTER(C.c_uint64))))
+        return {p: (float(ms[i]), int(n[i])) for i, p in enumerate(self.PHASES)}
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib.mtk_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Rng:
+    """mt::Rng (rng.hpp:13-75), host-side and bit-exact."""
+
+    def __init__(self, seed: int | None = None, _h=None):
+        if _h is not None:
+            self.h = _h
+        else:
+            h = C.c_void_p()
+            errors.check(lib.mtk_rng_create(C.c_uint64(seed & (2**64 - 1)), C.byref(h)))
+            self.h = h
+
+    def __del__(self):
+        try:
+            lib.mtk_rng_destroy(self.h)
+        except Exception:
+            pass
+
+    def next_u64(self) -> int:
+        return lib.mtk_rng_next_u64(self.h)
+
+    def uniform(self, lo: float = 0.0, hi: float = 1.0) -> float:
+        return lib.mtk_rng_uniform(self.h, lo, hi)
+
+    def normal(self) -> float:
+        return lib.mtk_rng_normal(self.h)
+
+    def below(self, n: int) -> int:
+        return lib.mtk_rng_below(self.h, n)
+
+    def permutation(self, n: int) -> np.ndarray:
+        out = np.empty(n, dtype=np.uint64)
+        errors.check(lib.mtk_rng_permutation(self.h, n, out.ctypes.data_as(C.POINTER(C.c_uint64))))
+        return out
+
+    def split(self, stream: int) -> "Rng":
+        h = C.c_void_p()
+        errors.check(lib.mtk_rng_split(self.h, stream, C.byref(h)))
+        return Rng(_h=h)
+
+    def normals(self, n: int) -> np.ndarray:
+        out = np.empty(n, dtype=np.float64)
+        errors.check(lib.mtk_rng_fill_normal(self.h, out.ctypes.data_as(_dp), n))
+        return out
+
+    def synth(self, n_classes: int, d: int, n: int, mu: np.ndarray, shift=None, f64=False):
+        """Class-conditional Gaussians; returns (X float32 [n,d], y int32 [n]) (+X f64)."""
+        mu = np.ascontiguousarray(mu, dtype=np.float64)
+        X32 = np.empty((n, d), dtype=np.float32)
+        X64 = np.empty((n, d), dtype=np.float64) if f64 else None
+        y = np.empty(n, dtype=np.int32)
+        sh = None if shift is None else np.ascontiguousarray(shift, dtype=np.float64)
+        errors.check(lib.mtk_synth(self.h, n_classes, d, n, mu.ctypes.data_as(_dp),
+                                   None if sh is None else sh.ctypes.data_as(_dp),
+                                   None if X64 is None else X64.ctypes.data_as(_dp),
+                                   C.c_void_p(X32.ctypes.data), C.c_void_p(y.ctypes.data)),
+                     "synth")
+        return (X32, y, X64) if f64 else (X32, y)
+
+
+class Bank:
+    """G independent MLPs trained as one grouped step (see mtk_bank_* in mtk.h)."""
+
+    def __init__(self, ctx: Context, G: int, dims: Sequence[int], n_heads: int = 1):
+        self.ctx, self.G, self.dims, self.n_heads = ctx, G, list(dims), n_heads
+        self.L = len(dims) - 1
+        self.n_mats = self.L + n_heads - 1
+        h = C.c_void_p()
+        d = (C.c_int * len(dims))(*dims)
+        errors.check(lib.mtk_bank_create(ctx.h, G, self.L, d, n_heads, C.byref(h)),
+                     "mtk_bank_create")
+        self.h = h
+        self._loss = np.zeros(G)
+        self._mmd = np.zeros(G)
+
+    def __del__(self):
+        try:
+            lib.mtk_bank_destroy(self.h)
+        except Exception:
+            pass
+
+    def shapes(self):
+        out = []
+        for i in range(self.n_mats):
+            l = i if i < self.L else self.L - 1
+            out.append((self.dims[l], self.dims[l + 1]))
+        return out
+
+    def set_params(self, model: int, W, b):
+        W = [np.ascontiguousarray(x, dtype=np.float64) for x in W]
+        b = [np.ascontiguousarray(x, dtype=np.float64) for x in b]
+        errors.check(lib.mtk_bank_set_params(self.h, model, _dvec(W), _dvec(b)), "set_params")
+
+    def get_params(self, model: int):
+        W = [np.empty(s) for s in self.shapes()]
+        b = [np.empty(s[1]) for s in self.shapes()]
+        errors.check(lib.mtk_bank_get_params(self.h, model, _dvec(W), _dvec(b)), "get_params")
+        return W, b
+
+    def init_params(self, model: int, rng: Rng):
+        errors.check(lib.mtk_bank_init_params(self.h, model, rng.h), "init_params")
+
+    def param_device(self, mat: int):
+        w, b = C.c_void_p(), C.c_void_p()
+        errors.check(lib.mtk_bank_param_device(self.h, mat, C.byref(w), C.byref(b)))
+        return w.value, b.value
+
+    def forward(self, X: torch.Tensor, head: int = 0, hidden: bool = False):
+        B = X.shape[1]
+        logits = torch.empty((self.G, B, self.dims[-1]), device=X.device, dtype=torch.float32)
+        hid = (torch.empty((self.G, B, self.dims[-2]), device=X.device, dtype=torch.float32)
+               if hidden and self.L > 1 else None)
+        errors.check(lib.mtk_bank_forward(self.h, _ptr(X), B, head, _ptr(logits), _ptr(hid)),
+                     "forward")
+        return (logits, hid) if hidden else logits
+
+    @staticmethod
+    def make_step(B, *, src_rows=0, denom=(0.0, 0.0), lr=0.05, frozen_layers=0, mmd_lambda=0.0,
+                  mmd_mult=None, X=None, y=None, w=None) -> MtkStep:
+        s = MtkStep()
+        s.X, s.y, s.w = _ptr(X), _ptr(y), _ptr(w)
+        s.B = B
+        s.src_rows = src_rows
+        s.denom[0], s.denom[1] = denom
+        s.lr = lr
+        s.frozen_layers = frozen_layers
+        s.mmd_lambda = mmd_lambda
+        if mmd_mult is not None:
+            s.mmd_nb = len(mmd_mult)
+            for i, v in enumerate(mmd_mult):
+                s.mmd_mult[i] = v
+        return s
+
+    def train_step(self, X, y, w=None, *, want_loss=True, **kw):
+        """One SGD step of all G models; returns (loss[G], mmd[G]) or None."""
+        B = X.shape[1]
+        s = self.make_step(B, X=X, y=y, w=w, **kw)
+        lp = self._loss.ctypes.data_as(_dp) if want_loss else None
+        mp = self._mmd.ctypes.data_as(_dp) if want_loss else None
+        errors.check(lib.mtk_bank_train_step(self.h, C.byref(s), lp, mp), "train_step")
+        return (self._loss.copy(), self._mmd.copy()) if want_loss else None
+
+    def train_step_host(self, X_host, y_host, w_host=None, *, want_loss=True, **kw):
+        """Same step from host (ideally pinned) buffers; copies inside the call."""
+        B = X_host.shape[1]
+        s = self.make_step(B, **kw)
+        lp = self._loss.ctypes.data_as(_dp) if want_loss else None
+        mp = self._mmd.ctypes.data_as(_dp) if want_loss else None
+        errors.check(lib.mtk_bank_train_step_host(self.h, C.byref(s), _ptr(X_host), _ptr(y_host),
+                                                  _ptr(w_host), lp, mp), "train_step_host")
+        return (self._loss.copy(), self._mmd.copy()) if want_loss else None
+
+    def keep_grads(self, on: bool = True):
+        errors.check(lib.mtk_bank_set_keep_grads(self.h, 1 if on else 0))
+
+    def get_grads(self, model: int):
+        W = [np.empty(s) for s in self.shapes()]
+        b = [np.empty(s[1]) for s in self.shapes()]
+        errors.check(lib.mtk_bank_get_grads(self.h, model, _dvec(W), _dvec(b)), "get_grads")
+        return W, b
+
+
+def _mult_arr(mult):
+    mult = MMD_MULT if mult is None else mult
+    return np.ascontiguousarray(mult, dtype=np.float64)
+
+
+def mmd_gaussian(ctx: Context, Xs: torch.Tensor, Xt: torch.Tensor, mult=None, beta: float = 0.0,
+                 grads: bool = True):
+    """Multi-bandwidth Gaussian MMD^2 (biased V-statistic) and d/dX (device)."""
+    m, d = Xs.shape
+    n = Xt.shape[0]
+    mu = _mult_arr(mult)
+    v, bo = C.c_double(), C.c_double()
+    gs = torch.empty_like(Xs) if grads else None
+    gt = torch.empty_like(Xt) if grads else None
+    errors.check(lib.mtk_mmd_gaussian(ctx.h, _ptr(Xs), m, _ptr(Xt), n, d, mu.ctypes.data_as(_dp),
+                                      len(mu), beta, C.byref(v), C.byref(bo), _ptr(gs), _ptr(gt)),
+                 "mmd_gaussian")
+    return v.value, bo.value, gs, gt
+
+
+def mmd_gaussian_rows(ctx: Context, Xs, Xt, beta: float, row_begin: int, row_end: int, mult=None,
+                      gXs=None, gXt=None):
+    """Row-sharded MMD: raw kernel sums (ss, tt, st) over pair rows [begin, end)."""
+    m, d = Xs.shape
+    n = Xt.shape[0]
+    mu = _mult_arr(mult)
+    part = np.zeros(3)
+    errors.check(lib.mtk_mmd_gaussian_rows(ctx.h, _ptr(Xs), m, _ptr(Xt), n, d,
+                                           mu.ctypes.data_as(_dp), len(mu), beta, row_begin,
+                                           row_end, part.ctypes.data_as(_dp), _ptr(gXs),
+                                           _ptr(gXt)), "mmd_gaussian_rows")
+    return part
+
+
+def mmd_beta(ctx: Context, Xs, Xt) -> float:
+    m, d = Xs.shape
+    out = C.c_double()
+    errors.check(lib.mtk_mmd_beta(ctx.h, _ptr(Xs), m, _ptr(Xt), Xt.shape[0], d, C.byref(out)))
+    return out.value
+
+
+def mmd_value_from_sums(sums, m: int, n: int) -> float:
+    ss, tt, st = sums
+    return ss / (m * m) + tt / (n * n) - 2.0 * st / (m * n)
+
+
+def softmax(ctx: Context, logits: torch.Tensor) -> torch.Tensor:
+    logits2 = logits.reshape(-1, logits.shape[-1])
+    out = torch.empty_like(logits2)
+    errors.check(lib.mtk_softmax(ctx.h, _ptr(logits2), logits2.shape[0], logits2.shape[1],
+                                 _ptr(out)), "softmax")
+    return out.reshape(logits.shape)
+
+
+def posterior_features(ctx: Context, logits: torch.Tensor, k: int = 3, labels=None):
+    logits2 = logits.reshape(-1, logits.shape[-1])
+    rows, Cn = logits2.shape
+    nf = k + (1 if labels is not None else 0)
+    out = torch.empty((rows, nf), device=logits.device, dtype=torch.float32)
+    lab = None if labels is None else labels.reshape(-1)
+    errors.check(lib.mtk_posterior_features(ctx.h, _ptr(logits2), rows, Cn, k, _ptr(lab),
+                                            _ptr(out)), "posterior_features")
+    return out
+
+
+def posterior_column(ctx: Context, logits: torch.Tensor, col: int = 1):
+    logits2 = logits.reshape(-1, logits.shape[-1])
+    out = torch.empty(logits2.shape[0], device=logits.device, dtype=torch.float32)
+    errors.check(lib.mtk_posterior_column(ctx.h, _ptr(logits2), logits2.shape[0],
+                                          logits2.shape[1], col, _ptr(out)), "posterior_column")
+    return out
+
+
+def auc(ctx: Context, scores: torch.Tensor, labels: torch.Tensor):
+    """(AUC with mid-ranks, accuracy at 0.5); labels uint8, 1 = member."""
+    a, acc = C.c_double(), C.c_double()
+    errors.check(lib.mtk_auc(ctx.h, _ptr(scores), _ptr(labels), scores.numel(), C.byref(a),
+                             C.byref(acc)), "auc")
+    return a.value, acc.value

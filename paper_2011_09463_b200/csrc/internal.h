@@ -1,0 +1,156 @@
+// internal.h -- shared declarations of libmtk (host side + kernel launchers).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "minitransfer/mtk.h"
+
+namespace mtk {
+
+// Exceptions carry the C-ABI status; capi.cu converts them at the boundary.
+struct Failure : std::runtime_error {
+    int status;
+    Failure(int s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+[[noreturn]] inline void fail(int s, const std::string& m) { throw Failure(s, m); }
+
+#define MTK_CUDA(call)                                                                   \
+    do {                                                                                 \
+        cudaError_t e_ = (call);                                                         \
+        if (e_ != cudaSuccess)                                                           \
+            ::mtk::fail(MTK_ERROR, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+// Device-side deferred error bits (checked at synchronizing calls).
+enum : int { kFlagNonFinite = 1, kFlagBadLabel = 2 };
+
+// Phases of the bank step, for optional CUDA-event timing (mtk_ctx_set_timing).
+enum Phase : int { kPhFwd = 0, kPhCe, kPhMmdBeta, kPhMmdPairs, kPhDx, kPhDw, kPhBias, kPhOther,
+                   kNumPhases };
+
+struct Ctx {
+    int device = 0;
+    bool timing = false;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+    std::vector<cudaEvent_t> event_pool;
+    double phase_ms[kNumPhases] = {0};
+    uint64_t phase_launches[kNumPhases] = {0};
+    cudaEvent_t take_event();
+    void collect_phases();
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int* d_flags = nullptr;          // deferred error bits
+    double* d_scratch = nullptr;     // small fp64 reduction scratch
+    size_t scratch_bytes = 0;
+    uint64_t launches = 0;
+    void* pinned = nullptr;          // host staging for small results
+    size_t pinned_bytes = 0;
+    double* scratch(size_t bytes);
+    void* pinned_buf(size_t bytes);
+    void check_flags();               // synchronizes; throws on a set flag
+};
+
+// RAII: records start/stop events around a launch group when timing is on.
+struct PhaseScope {
+    Ctx& c;
+    int ph;
+    int n;
+    cudaEvent_t a = nullptr;
+    PhaseScope(Ctx& ctx, int phase, int launches = 1);
+    ~PhaseScope();
+};
+
+// Grouped GEMM description.  Per group g:
+//   C(m,n) = sum_k A(m,k) * B(k,n)
+//   A(m,k) = A[g*a_gs + m*a_ms + k*a_ks]; B(k,n) = B[g*b_gs + k*b_ks + n*b_ns]
+// Epilogues operate on row-major outputs C[g*c_gs + m*ldc + n].
+enum class Epi : int {
+    kBias = 0,      // C = acc + bias[n]
+    kBiasRelu = 1,  // C = max(acc + bias[n], 0)
+    kMask = 2,      // C = (acc + add[m,n]) * (mask[m,n] > 0)      (dX through ReLU)
+    kSgd = 3,       // C(=W) -= lr * acc ; optionally grad_out = acc  (dW + SGD)
+};
+
+struct Gemm {
+    int G = 1, M = 0, N = 0, K = 0;
+    const float* A = nullptr;
+    long long a_gs = 0, a_ms = 0, a_ks = 0;
+    const float* B = nullptr;
+    long long b_gs = 0, b_ks = 0, b_ns = 0;
+    float* C = nullptr;
+    long long c_gs = 0, ldc = 0;
+    Epi epi = Epi::kBias;
+    const float* bias = nullptr;  // [G, N] stride bias_gs
+    long long bias_gs = 0;
+    const float* add = nullptr;   // kMask: optional addend, same layout as C
+    const float* mask = nullptr;  // kMask: mask source, same layout as C
+    float lr = 0.f;               // kSgd
+    float* grad_out = nullptr;    // kSgd: optional copy of acc, same layout as C
+    int* flags = nullptr;
+};
+
+void launch_gemm(const Gemm& g, cudaStream_t s);
+
+// Cross-entropy head (tape.hpp:475-520), rows laid out [G, B, C].
+struct CeArgs {
+    int G, B, C, src_rows;
+    const float* logits;
+    const int32_t* y;
+    const float* w;         // may be null
+    float inv_denom0, inv_denom1;  // head 0 rows [0,src_rows), head 1 the rest
+    float* dlogits;         // [G,B,C]
+    double* row_loss;       // [G,B]  w_i (lse - x_y) / denom_head
+    double* loss;           // [G]
+    int* flags;
+};
+void launch_ce(const CeArgs& a, cudaStream_t s);
+
+// Column sums + SGD on a bias: db[g,n] = sum_{rows} dZ[g, r, n]; b -= lr*db
+void launch_bias_sgd(int G, int rows, int N, const float* dZ, long long dz_gs, float* b,
+                     long long b_gs, float lr, float* grad_out, int* flags, cudaStream_t s);
+
+// MMD problem over G independent groups; group g has rows [0,m) in Xs and
+// [0,n) in Xt, both row-major with row stride d.
+struct MmdArgs {
+    int G = 1;
+    long long m = 0, n = 0;
+    int d = 0;
+    const float* Xs = nullptr;
+    long long xs_gs = 0;
+    const float* Xt = nullptr;
+    long long xt_gs = 0;
+    int nb = 5;
+    float mult[8] = {0.25f, 0.5f, 1.f, 2.f, 4.f, 0.f, 0.f, 0.f};
+    const double* beta = nullptr;   // [G] device (detached)
+    long long row_begin = 0, row_end = -1;  // concatenated-row range (all groups)
+    double* partial = nullptr;      // [G, nblocks_per_group, 3] device
+    float* gXs = nullptr;           // optional, layout as Xs, scaled by grad_scale
+    long long gs_gs = 0;
+    float* gXt = nullptr;
+    long long gt_gs = 0;
+    float grad_scale = 1.f;
+    int* flags = nullptr;
+};
+int mmd_blocks_per_group(const MmdArgs& a);
+void launch_mmd_beta(const MmdArgs& a, double* beta_out, double* scratch, cudaStream_t s);
+void launch_mmd_pairs(const MmdArgs& a, cudaStream_t s);
+// value[g] = cSS*ss + cTT*tt + cST*st from the per-block partials (fixed order)
+void launch_mmd_finish(const MmdArgs& a, double* value, double* sums3, cudaStream_t s);
+
+// attack stage
+void launch_softmax(const float* logits, long long rows, int C, float* probs, cudaStream_t s);
+void launch_features(const float* logits, long long rows, int C, int k, const int32_t* labels,
+                     float* feats, int* flags, cudaStream_t s);
+void launch_column(const float* logits, long long rows, int C, int col, float* out,
+                   cudaStream_t s);
+void auc_device(Ctx& ctx, const float* scores, const uint8_t* labels, long long n, double* auc,
+                double* acc);
+
+}  // namespace mtk
+
+struct mtk_ctx : mtk::Ctx {};

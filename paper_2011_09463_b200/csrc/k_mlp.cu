@@ -1,0 +1,211 @@
+// k_mlp.cu -- grouped MLP kernels for the shadow-model bank (SIMT fp32 path).
+//
+// Replaces, for G independent models at once, the reference loops
+//   detail::mm_acc    (tape.hpp:36-48)   forward  Z = H W      (+ add_bias, relu epilogue)
+//   detail::mm_nt_acc (tape.hpp:50-63)   backward dH = dZ W^T  (+ relu mask epilogue)
+//   detail::mm_tn_acc (tape.hpp:65-78)   backward dW = H^T dZ  (+ SGD epilogue, optim.hpp:46-48)
+// and cross_entropy_weighted (tape.hpp:475-520).  Every output element is
+// produced by exactly one thread with a fixed k order, so results are
+// bit-deterministic run to run.
+#include <cfloat>
+#include <cmath>
+
+#include "internal.h"
+
+namespace mtk {
+namespace {
+
+constexpr int BM = 128, BN = 128, BK = 8, NT = 256;
+
+__global__ void __launch_bounds__(NT) gemm_simt_kernel(Gemm p) {
+    __shared__ float As[2][BK][BM + 4];
+    __shared__ float Bs[2][BK][BN + 4];
+    const int g = blockIdx.z;
+    const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const float* A = p.A + g * p.a_gs;
+    const float* B = p.B + g * p.b_gs;
+    const bool a_k_contig = (p.a_ks == 1);
+    const bool b_n_contig = (p.b_ns == 1);
+
+    float acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+
+    float ra[4], rb[4];
+    auto load_regs = [&](int k0) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int e = tid + i * NT;
+            int mm, kk;
+            if (a_k_contig) { mm = e >> 3; kk = e & 7; } else { mm = e & (BM - 1); kk = e >> 7; }
+            const int gm = m0 + mm, gk = k0 + kk;
+            ra[i] = (gm < p.M && gk < p.K) ? __ldg(A + gm * p.a_ms + (long long)gk * p.a_ks) : 0.f;
+            int nn, kb;
+            if (b_n_contig) { nn = e & (BN - 1); kb = e >> 7; } else { nn = e >> 3; kb = e & 7; }
+            const int gn = n0 + nn, gkb = k0 + kb;
+            rb[i] = (gn < p.N && gkb < p.K) ? __ldg(B + (long long)gkb * p.b_ks + gn * p.b_ns) : 0.f;
+        }
+    };
+    auto store_smem = [&](int buf) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int e = tid + i * NT;
+            int mm, kk;
+            if (a_k_contig) { mm = e >> 3; kk = e & 7; } else { mm = e & (BM - 1); kk = e >> 7; }
+            As[buf][kk][mm] = ra[i];
+            int nn, kb;
+            if (b_n_contig) { nn = e & (BN - 1); kb = e >> 7; } else { nn = e >> 3; kb = e & 7; }
+            Bs[buf][kb][nn] = rb[i];
+        }
+    };
+
+    const int nk = (p.K + BK - 1) / BK;
+    load_regs(0);
+    store_smem(0);
+    __syncthreads();
+    for (int t = 0; t < nk; ++t) {
+        const int buf = t & 1;
+        if (t + 1 < nk) load_regs((t + 1) * BK);
+#pragma unroll
+        for (int kk = 0; kk < BK; ++kk) {
+            float a[8], b[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) a[i] = As[buf][kk][ty + 16 * i];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) b[j] = Bs[buf][kk][tx + 16 * j];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        }
+        if (t + 1 < nk) store_smem(buf ^ 1);
+        __syncthreads();
+    }
+
+    bool bad = false;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int m = m0 + ty + 16 * i;
+        if (m >= p.M) continue;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int n = n0 + tx + 16 * j;
+            if (n >= p.N) continue;
+            const long long idx = g * p.c_gs + (long long)m * p.ldc + n;
+            float v = acc[i][j];
+            switch (p.epi) {
+                case Epi::kBias:
+                    v += p.bias[g * p.bias_gs + n];
+                    p.C[idx] = v;
+                    bad |= !isfinite(v);
+                    break;
+                case Epi::kBiasRelu:
+                    v += p.bias[g * p.bias_gs + n];
+                    bad |= !isfinite(v);
+                    p.C[idx] = v > 0.f ? v : 0.f;
+                    break;
+                case Epi::kMask: {
+                    if (p.add) v = p.add[idx] + v;
+                    p.C[idx] = (p.mask[idx] > 0.f) ? v : 0.f;
+                    break;
+                }
+                case Epi::kSgd: {
+                    if (p.grad_out) p.grad_out[idx] = v;
+                    const float w = p.C[idx] - p.lr * v;
+                    bad |= !isfinite(w);
+                    p.C[idx] = w;
+                    break;
+                }
+            }
+        }
+    }
+    if (bad && p.flags) atomicOr(p.flags, kFlagNonFinite);
+}
+
+// One thread per row: softmax-CE forward + d(logits) (tape.hpp:475-520).
+__global__ void ce_kernel(CeArgs a) {
+    const long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const long long rows = (long long)a.G * a.B;
+    if (r >= rows) return;
+    const int i = (int)(r % a.B);
+    const float* x = a.logits + r * a.C;
+    float* dx = a.dlogits + r * a.C;
+    const int lab = a.y[r];
+    if (lab < 0 || lab >= a.C) {
+        atomicOr(a.flags, kFlagBadLabel);
+        for (int j = 0; j < a.C; ++j) dx[j] = 0.f;
+        a.row_loss[r] = 0.0;
+        return;
+    }
+    float mx = x[0];
+    for (int j = 1; j < a.C; ++j) mx = fmaxf(mx, x[j]);
+    float z = 0.f;
+    for (int j = 0; j < a.C; ++j) z += expf(x[j] - mx);
+    const float lse = mx + logf(z);
+    const float inv = (i < a.src_rows) ? a.inv_denom0 : a.inv_denom1;
+    const float wi = (a.w ? a.w[r] : 1.f) * inv;
+    a.row_loss[r] = (double)wi * ((double)lse - (double)x[lab]);
+    for (int j = 0; j < a.C; ++j) {
+        const float pj = expf(x[j] - lse);
+        dx[j] = wi * (pj - (j == lab ? 1.f : 0.f));
+    }
+}
+
+// Fixed-order per-model fp64 sum of the per-row losses.
+__global__ void row_sum_kernel(const double* row_loss, int B, double* loss, int* flags) {
+    __shared__ double red[256];
+    const int g = blockIdx.x;
+    double s = 0.0;
+    for (int i = threadIdx.x; i < B; i += blockDim.x) s += row_loss[(long long)g * B + i];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        loss[g] = red[0];
+        if (!isfinite(red[0])) atomicOr(flags, kFlagNonFinite);
+    }
+}
+
+// db = column sums of dZ (fixed row order), b -= lr * db.
+__global__ void bias_sgd_kernel(int G, int rows, int N, const float* dZ, long long dz_gs, float* b,
+                                long long b_gs, float lr, float* grad_out, int* flags) {
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (t >= (long long)G * N) return;
+    const int g = (int)(t / N), n = (int)(t % N);
+    const float* col = dZ + g * dz_gs + n;
+    float s = 0.f;
+    for (int r = 0; r < rows; ++r) s += col[(long long)r * N];
+    if (grad_out) grad_out[g * b_gs + n] = s;
+    const float v = b[g * b_gs + n] - lr * s;
+    if (!isfinite(v)) atomicOr(flags, kFlagNonFinite);
+    b[g * b_gs + n] = v;
+}
+
+}  // namespace
+
+void launch_gemm(const Gemm& p, cudaStream_t s) {
+    if (p.M <= 0 || p.N <= 0 || p.G <= 0) return;
+    dim3 grid((p.N + BN - 1) / BN, (p.M + BM - 1) / BM, p.G);
+    gemm_simt_kernel<<<grid, NT, 0, s>>>(p);
+}
+
+void launch_ce(const CeArgs& a, cudaStream_t s) {
+    const long long rows = (long long)a.G * a.B;
+    ce_kernel<<<(unsigned)((rows + 127) / 128), 128, 0, s>>>(a);
+    row_sum_kernel<<<a.G, 256, 0, s>>>(a.row_loss, a.B, a.loss, a.flags);
+}
+
+void launch_bias_sgd(int G, int rows, int N, const float* dZ, long long dz_gs, float* b,
+                     long long b_gs, float lr, float* grad_out, int* flags, cudaStream_t s) {
+    const long long t = (long long)G * N;
+    bias_sgd_kernel<<<(unsigned)((t + 127) / 128), 128, 0, s>>>(G, rows, N, dZ, dz_gs, b, b_gs, lr,
+                                                               grad_out, flags);
+}
+
+}  // namespace mtk

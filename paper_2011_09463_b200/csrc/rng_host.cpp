@@ -1,0 +1,125 @@
+// rng_host.cpp -- host-side bit-exact sampling for the shadow sweep.
+//
+// Restates the reference's mt::Rng (rng.hpp:13-75) on std::mt19937_64, whose
+// output sequence is fixed by the C++ standard, with the same hand-rolled
+// distributions, so every draw, permutation, member/non-member split and
+// weight initialisation is bit-identical to the reference.  Compiled with
+// -ffp-contract=off (rng.hpp:22 changes bits
+// under FMA contraction).  Sampling never runs on the device.
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <random>
+#include <string>
+
+#include "minitransfer/mtk.h"
+
+struct mtk_rng {
+    std::mt19937_64 eng;
+    bool cached = false;
+    double cache = 0.0;
+    explicit mtk_rng(uint64_t seed) : eng(seed) {}
+
+    double unit() { return static_cast<double>(eng() >> 11) * 0x1.0p-53; }  // rng.hpp:20
+    double range(double lo, double hi) {                                  // rng.hpp:22
+        const double u = unit();
+        const double width = hi - lo;
+        const double off = width * u;
+        return lo + off;
+    }
+    double gauss() {  // rng.hpp:24-37, Box-Muller pair, second value cached
+        if (cached) {
+            cached = false;
+            return cache;
+        }
+        const double u1 = 1.0 - unit();
+        const double u2 = unit();
+        const double rad = std::sqrt(-2.0 * std::log(u1));
+        const double theta = 6.28318530717958647692 * u2;
+        cache = rad * std::sin(theta);
+        cached = true;
+        return rad * std::cos(theta);
+    }
+    uint64_t bounded(uint64_t n) {  // rng.hpp:39-46, unbiased rejection
+        if (n == 0) return 0;
+        const uint64_t cut = UINT64_MAX - UINT64_MAX % n;
+        for (;;) {
+            const uint64_t x = eng();
+            if (x < cut) return x % n;
+        }
+    }
+};
+
+extern "C" void mtk_internal_set_error(const char* msg);  // capi.cu
+
+namespace {
+int set_err(int s, const char* m) {
+    mtk_internal_set_error(m);
+    return s;
+}
+}  // namespace
+
+extern "C" {
+
+int mtk_rng_create(uint64_t seed, mtk_rng** out) {
+    if (!out) return set_err(MTK_VALUE_ERROR, "mtk_rng_create: null out");
+    *out = new mtk_rng(seed);
+    return MTK_OK;
+}
+
+int mtk_rng_destroy(mtk_rng* r) {
+    delete r;
+    return MTK_OK;
+}
+
+// rng.hpp:65-69: one parent draw xor a stream constant seeds the child
+int mtk_rng_split(mtk_rng* parent, uint64_t stream, mtk_rng** out) {
+    if (!parent || !out) return set_err(MTK_VALUE_ERROR, "mtk_rng_split: null argument");
+    const uint64_t s = parent->eng() ^ (0x9e3779b97f4a7c15ULL * (stream + 1));
+    *out = new mtk_rng(s);
+    return MTK_OK;
+}
+
+uint64_t mtk_rng_next_u64(mtk_rng* r) { return r->eng(); }
+double mtk_rng_uniform(mtk_rng* r, double lo, double hi) { return r->range(lo, hi); }
+double mtk_rng_normal(mtk_rng* r) { return r->gauss(); }
+uint64_t mtk_rng_below(mtk_rng* r, uint64_t n) { return r->bounded(n); }
+
+// rng.hpp:50-63: identity then Fisher-Yates swaps from the top
+int mtk_rng_permutation(mtk_rng* r, uint64_t n, uint64_t* out) {
+    if (!r || (!out && n)) return set_err(MTK_VALUE_ERROR, "mtk_rng_permutation: null argument");
+    for (uint64_t i = 0; i < n; ++i) out[i] = i;
+    for (uint64_t top = n; top > 1; --top) {
+        const uint64_t j = r->bounded(top);
+        const uint64_t t = out[top - 1];
+        out[top - 1] = out[j];
+        out[j] = t;
+    }
+    return MTK_OK;
+}
+
+int mtk_rng_fill_normal(mtk_rng* r, double* out, uint64_t n) {
+    if (!r || (!out && n)) return set_err(MTK_VALUE_ERROR, "mtk_rng_fill_normal: null argument");
+    for (uint64_t i = 0; i < n; ++i) out[i] = r->gauss();
+    return MTK_OK;
+}
+
+int mtk_synth(mtk_rng* r, int C, int d, uint64_t n, const double* mu, const double* shift,
+              double* X64, float* X32, int32_t* y) {
+    if (!r || !mu || !y) return set_err(MTK_VALUE_ERROR, "mtk_synth: null argument");
+    if (C <= 0 || d <= 0) return set_err(MTK_SHAPE_ERROR, "mtk_synth: zero dimension");
+    for (uint64_t i = 0; i < n; ++i) {
+        const int c = static_cast<int>(r->bounded(static_cast<uint64_t>(C)));
+        y[i] = c;
+        const double* mrow = mu + static_cast<size_t>(c) * d;
+        for (int k = 0; k < d; ++k) {
+            double v = mrow[k] + r->gauss();
+            if (shift) v = v + shift[k];
+            if (X64) X64[i * d + k] = v;
+            if (X32) X32[i * d + k] = static_cast<float>(v);
+        }
+    }
+    return MTK_OK;
+}
+
+}  // extern "C"

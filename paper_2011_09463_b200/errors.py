@@ -1,0 +1,39 @@
+"""Error taxonomy of the reference (error.hpp:10-51) as Python exceptions.
+
+C-ABI status codes map onto these classes: 1 ShapeError, 2 ValueError,
+3 ConfigError, 4 DataError, 5 Error.  ``ValueError`` also derives from the
+builtin so idiomatic ``except ValueError`` keeps working.
+"""
+import builtins
+
+
+class Error(RuntimeError):
+    """mt::Error (error.hpp:10-13): base of everything the toolkit raises."""
+
+
+class ShapeError(Error):
+    """mt::ShapeError (error.hpp:16-18): tensor dimension mismatches."""
+
+
+class ValueError(Error, builtins.ValueError):  # noqa: A001 - mirrors mt::ValueError
+    """mt::ValueError (error.hpp:21-23): bad argument values."""
+
+
+class ConfigError(Error):
+    """mt::ConfigError (error.hpp:26-28): invalid configuration."""
+
+
+class DataError(Error):
+    """mt::DataError (error.hpp:31-33): problems with input data."""
+
+
+_BY_STATUS = {1: ShapeError, 2: ValueError, 3: ConfigError, 4: DataError, 5: Error}
+
+
+def check(status: int, what: str = "") -> None:
+    if status == 0:
+        return
+    from ._lib import lib
+
+    msg = lib.mtk_last_error().decode(errors="replace")
+    raise _BY_STATUS.get(status, Error)(f"{what}: {msg}" if what else msg)

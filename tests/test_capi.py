@@ -1,0 +1,99 @@
+"""CPU: the C-ABI library loads, exports every symbol include/*.h declares,
+its host-side sampling is bit-exact against the oracle / reference goldens,
+and its error paths return the reference's status classes -- all without
+launching device work (no GPU in this container)."""
+import ctypes as C
+import glob
+import os
+import re
+
+import numpy as np
+import pytest
+
+import pyoracle as po
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLD = os.path.join(ROOT, "tests", "golden")
+
+
+def declared_symbols():
+    syms = set()
+    for h in glob.glob(os.path.join(ROOT, "include", "**", "*.h"), recursive=True):
+        text = open(h).read()
+        text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+        for m in re.finditer(r"^\s*[A-Za-z_][\w\s\*]*?\b(mtk_\w+)\s*\(", text, flags=re.M):
+            syms.add(m.group(1))
+    return syms
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2011_09463_b200._lib import SIGNATURES, lib
+
+    syms = declared_symbols()
+    assert len(syms) >= 30
+    missing = [s for s in sorted(syms) if not hasattr(lib, s)]
+    assert not missing, missing
+    # and the Python binding covers all of them
+    assert syms <= set(SIGNATURES), sorted(syms - set(SIGNATURES))
+    assert lib.mtk_version() >= 100
+
+
+def test_library_is_sm100a_cuda():
+    so = os.path.join(ROOT, "paper_2011_09463_b200", "libmtk.so")
+    out = os.popen(f"cuobjdump --list-elf {so} 2>&1").read()
+    assert "sm_100a" in out
+
+
+@pytest.mark.parametrize("seed", [0, 1, 42, 20110946])
+def test_host_rng_bit_exact_vs_reference_golden(seed):
+    from paper_2011_09463_b200 import api
+
+    g = np.load(os.path.join(GOLD, "rng_ref.npz"))
+    r = api.Rng(seed)
+    assert np.array_equal([r.next_u64() for _ in range(64)], g[f"s{seed}_u64"])
+    assert np.array_equal([r.normal() for _ in range(65)], g[f"s{seed}_normal"])
+    assert np.array_equal([r.uniform(-0.3, 0.7) for _ in range(64)], g[f"s{seed}_uniform"])
+    assert np.array_equal([r.below(10) for _ in range(64)], g[f"s{seed}_below"])
+    assert np.array_equal(r.permutation(100), g[f"s{seed}_perm"])
+    c = r.split(3)
+    assert np.array_equal([c.next_u64() for _ in range(8)], g[f"s{seed}_split"])
+
+
+def test_host_rng_streams_and_synth_match_oracle():
+    from paper_2011_09463_b200 import api
+
+    root, oroot = api.Rng(20110946), po.Rng(20110946)
+    for k in range(4):
+        a, b = root.split(k), oroot.split(k)
+        assert np.array_equal(a.permutation(8192), b.permutation(8192))
+        assert np.array_equal(a.normals(1001), b.normals(1001))
+    mu = po.Rng(5).normals(10 * 13).reshape(10, 13)
+    sh = po.Rng(6).normals(13)
+    X32, y, X64 = api.Rng(9).synth(10, 13, 257, mu, sh, f64=True)
+    oX, oy = po.synth(po.Rng(9), 10, 13, 257, mu, sh)
+    assert np.array_equal(X64, oX) and np.array_equal(y, oy)
+    assert np.array_equal(X32, oX.astype(np.float32))
+
+
+def test_error_paths_without_gpu():
+    """Argument validation reports the reference's error classes."""
+    from paper_2011_09463_b200 import errors
+    from paper_2011_09463_b200._lib import lib
+
+    h = C.c_void_p()
+    st = lib.mtk_ctx_create(-1, None, C.byref(h))
+    assert st in (2, 5)  # ValueError (bad device) or Error (no CUDA driver here)
+    assert lib.mtk_last_error()
+    with pytest.raises(errors.Error):
+        errors.check(st)
+    st = lib.mtk_rng_permutation(None, 3, None)
+    assert st == 2
+    assert b"null" in lib.mtk_last_error()
+    with pytest.raises(errors.ValueError):
+        errors.check(st)
+    with pytest.raises(ValueError):  # builtin-compatible
+        errors.check(2)
+    with pytest.raises(errors.ShapeError):
+        errors.check(1)
+    with pytest.raises(errors.ConfigError):
+        errors.check(3)

@@ -1,0 +1,76 @@
+"""GPU parity of the attack stage: posteriors, top-k features, AUC."""
+import numpy as np
+import pytest
+import torch
+
+import pyoracle as po
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-30))
+
+
+def logits(rows, C, seed=1, scale=3.0):
+    r = po.Rng(seed)
+    return (scale * r.normals(rows * C)).reshape(rows, C).astype(np.float32)
+
+
+def test_softmax_matches_reference_semantics(ctx):
+    from paper_2011_09463_b200 import api
+
+    x = logits(1000, 10)
+    p = api.softmax(ctx, torch.tensor(x, device="cuda")).cpu().numpy()
+    assert rel(p, po.softmax(x.astype(np.float64))) <= 1e-5
+    assert np.abs(p.sum(1) - 1).max() < 1e-5
+    # SPEC.md:70 known answer softmax([0, ln 3]) = [0.25, 0.75]
+    kq = api.softmax(ctx, torch.tensor([[0.0, np.log(3.0)]], dtype=torch.float32, device="cuda"))
+    assert np.allclose(kq.cpu().numpy(), [[0.25, 0.75]], atol=1e-7)
+
+
+@pytest.mark.parametrize("k,with_labels", [(3, False), (3, True), (1, True), (10, False)])
+def test_features(ctx, k, with_labels):
+    from paper_2011_09463_b200 import api
+
+    x = logits(777, 10, seed=k)
+    lab = np.arange(777, dtype=np.int32) % 10 if with_labels else None
+    f = api.posterior_features(ctx, torch.tensor(x, device="cuda"), k,
+                               None if lab is None else torch.tensor(lab, device="cuda"))
+    of = po.posterior_features(x.astype(np.float64), k, lab)
+    assert rel(f.cpu().numpy(), of) <= 1e-5
+
+
+def test_posterior_column(ctx):
+    from paper_2011_09463_b200 import api
+
+    x = logits(500, 2)
+    c = api.posterior_column(ctx, torch.tensor(x, device="cuda"), 1).cpu().numpy()
+    assert rel(c, po.softmax(x.astype(np.float64))[:, 1]) <= 1e-5
+
+
+@pytest.mark.parametrize("n,ties", [(1000, False), (4096, True), (1 << 20, False), (7, True)])
+def test_auc_matches_oracle(ctx, n, ties):
+    from paper_2011_09463_b200 import api
+
+    r = po.Rng(n)
+    s = r.normals(n).astype(np.float32)
+    if ties:
+        s = np.round(s * 4) / 4
+    lab = np.array([r.below(2) for _ in range(n)], dtype=np.uint8) if n < 100000 else \
+        (r.normals(n) + 0.3 * s > 0).astype(np.uint8)
+    lab[0], lab[-1] = 1, 0
+    a, acc = api.auc(ctx, torch.tensor(s, device="cuda"), torch.tensor(lab, device="cuda"))
+    oa = po.auc(s.astype(np.float64), lab)
+    oacc = po.accuracy(s.astype(np.float64), lab, 0.5)
+    assert abs(a - oa) <= 1e-12
+    assert abs(acc - oacc) <= 1e-12
+
+
+def test_auc_errors(ctx):
+    from paper_2011_09463_b200 import api, errors
+
+    with pytest.raises(errors.ValueError):
+        api.auc(ctx, torch.zeros(10, device="cuda"), torch.ones(10, dtype=torch.uint8, device="cuda"))

@@ -1,0 +1,201 @@
+"""GPU parity of the grouped shadow-model bank against the CPU oracle.
+
+Tolerance (north_star): per-kernel fp32 outputs within 1e-5 relative,
+measured as max|gpu - oracle| / max|oracle| per tensor, on identical inputs
+(the oracle is fed the exact fp32 values the GPU sees).  Oracle steps are
+bit-identical to the reference Tape (tests/test_oracle.py).
+"""
+import numpy as np
+import pytest
+import torch
+
+import pyoracle as po
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-30))
+
+
+def make_bank(ctx, G, dims, n_heads=1, seed=11):
+    from paper_2011_09463_b200 import api
+
+    bank = api.Bank(ctx, G, dims, n_heads=n_heads)
+    rng = api.Rng(seed)
+    for g in range(G):
+        bank.init_params(g, rng)
+    return bank
+
+
+def inputs(G, B, d0, C, seed=5, shift=0.0):
+    r = po.Rng(seed)
+    X = r.normals(G * B * d0).reshape(G, B, d0).astype(np.float32)
+    X[:, B // 2:, :] += np.float32(shift)
+    y = np.array([[r.below(C) for _ in range(B)] for _ in range(G)], dtype=np.int32)
+    return X, y
+
+
+def to_dev(X, y):
+    return torch.tensor(X, device="cuda"), torch.tensor(y, device="cuda")
+
+
+def check_step(bank, X, y, *, n_heads=1, src=0, frozen=0, lam=0.0, lr=0.05, w=None):
+    dims = bank.dims
+    G = bank.G
+    before = [bank.get_params(g) for g in range(G)]
+    bank.keep_grads(True)
+    Xd, yd = to_dev(X, y)
+    wd = None if w is None else torch.tensor(w, device="cuda")
+    loss, mmd = bank.train_step(Xd, yd, wd, lr=lr, src_rows=src, frozen_layers=frozen,
+                                mmd_lambda=lam)
+    worst = 0.0
+    for g in range(G):
+        W, b = [x.copy() for x in before[g][0]], [x.copy() for x in before[g][1]]
+        Xg = X[g].astype(np.float64)
+        dH = None
+        if lam > 0:
+            _, H = po.mlp_forward(dims, W, b, Xg)
+            v, _, gs, gt = po.mmd_gaussian(H[:src], H[src:])
+            dH = lam * np.concatenate([gs, gt])
+            assert rel(mmd[g], v) <= TOL, (g, mmd[g], v)
+        lo, gW, gb = po.mlp_train_step(dims, W, b, Xg, y[g], n_heads=n_heads, frozen=frozen,
+                                       src_rows=src, lr=lr, dH=dH,
+                                       w=None if w is None else w[g].astype(np.float64),
+                                       want_grads=True)
+        assert rel(loss[g], lo) <= TOL, (g, loss[g], lo)
+        dW, db = bank.get_grads(g)
+        Wn, bn = bank.get_params(g)
+        l_lo = 0
+        for i in range(bank.n_mats):
+            lay = i if i < bank.L else bank.L - 1
+            if lay < frozen:
+                # frozen parameters must be bit-unchanged (SPEC.md finetune post-condition)
+                assert np.array_equal(Wn[i], before[g][0][i]) and np.array_equal(bn[i], before[g][1][i])
+                continue
+            e = max(rel(dW[i], gW[i]), rel(db[i], gb[i]) if np.abs(gb[i]).max() > 0 else 0.0)
+            worst = max(worst, e)
+            assert e <= TOL, (g, i, e)
+            assert rel(Wn[i], W[i]) <= TOL
+    return worst
+
+
+def test_forward_matches_oracle(ctx):
+    dims = [784, 256, 10]
+    G, B = 5, 64
+    bank = make_bank(ctx, G, dims)
+    X, _ = inputs(G, B, dims[0], dims[-1])
+    logits, hid = bank.forward(torch.tensor(X, device="cuda"), hidden=True)
+    logits, hid = logits.cpu().numpy(), hid.cpu().numpy()
+    for g in range(G):
+        W, b = bank.get_params(g)
+        lo, H = po.mlp_forward(dims, W, b, X[g].astype(np.float64))
+        assert rel(logits[g], lo) <= TOL
+        assert rel(hid[g], H) <= TOL
+
+
+def test_step_c1_shape(ctx):
+    """C1: 784-256-10, 1 target + 4 shadows, B=128."""
+    dims = [784, 256, 10]
+    bank = make_bank(ctx, 5, dims)
+    X, y = inputs(5, 128, 784, 10)
+    check_step(bank, X, y)
+
+
+def test_step_c2_shape_with_mmd(ctx):
+    """C2 architecture 1024-512-256-10, src+tgt batch, 5-bandwidth MMD injected."""
+    dims = [1024, 512, 256, 10]
+    bank = make_bank(ctx, 2, dims)
+    X, y = inputs(2, 96, 1024, 10, shift=0.5)
+    check_step(bank, X, y, src=48, lam=1.0)
+
+
+def test_step_two_heads_parameter_based(ctx):
+    dims = [784, 256, 10]
+    bank = make_bank(ctx, 3, dims, n_heads=2)
+    X, y = inputs(3, 64, 784, 10)
+    check_step(bank, X, y, n_heads=2, src=40)
+
+
+def test_step_frozen_prefix_model_based(ctx):
+    dims = [100, 64, 32, 10]
+    bank = make_bank(ctx, 2, dims)
+    X, y = inputs(2, 50, 100, 10)
+    check_step(bank, X, y, frozen=1)
+
+
+def test_step_ragged_shapes_and_weights(ctx):
+    dims = [37, 19, 3]
+    bank = make_bank(ctx, 4, dims)
+    X, y = inputs(4, 5, 37, 3)
+    w = np.array([[0.5, 0.0, 1.0, 2.0, 1.0]] * 4, dtype=np.float32)
+    check_step(bank, X, y, w=w, lr=0.3)
+
+
+def test_multi_step_trajectory(ctx):
+    dims = [64, 32, 10]
+    G = 3
+    bank = make_bank(ctx, G, dims)
+    X, y = inputs(G, 32, 64, 10)
+    Xd, yd = to_dev(X, y)
+    ref = [bank.get_params(g) for g in range(G)]
+    for _ in range(8):
+        bank.train_step(Xd, yd, lr=0.1, want_loss=False)
+        for g in range(G):
+            po.mlp_train_step(dims, ref[g][0], ref[g][1], X[g].astype(np.float64), y[g], lr=0.1)
+    for g in range(G):
+        W, b = bank.get_params(g)
+        for i in range(len(W)):
+            assert rel(W[i], ref[g][0][i]) <= 1e-4
+
+
+def test_determinism(ctx):
+    dims = [128, 64, 10]
+    X, y = inputs(2, 40, 128, 10)
+    Xd, yd = to_dev(X, y)
+    outs = []
+    for _ in range(2):
+        bank = make_bank(ctx, 2, dims, seed=3)
+        for _ in range(3):
+            bank.train_step(Xd, yd, lr=0.1, src_rows=20, mmd_lambda=0.5, want_loss=False)
+        outs.append(bank.get_params(1)[0])
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
+
+
+def test_host_step_equals_device_step(ctx):
+    dims = [64, 32, 10]
+    X, y = inputs(2, 16, 64, 10)
+    b1 = make_bank(ctx, 2, dims)
+    b2 = make_bank(ctx, 2, dims)
+    Xd, yd = to_dev(X, y)
+    l1, _ = b1.train_step(Xd, yd, lr=0.1)
+    l2, _ = b2.train_step_host(torch.tensor(X).pin_memory(), torch.tensor(y).pin_memory(), lr=0.1)
+    assert np.array_equal(l1, l2)
+    for a, b in zip(b1.get_params(1)[0], b2.get_params(1)[0]):
+        assert np.array_equal(a, b)
+
+
+def test_errors(ctx):
+    from paper_2011_09463_b200 import api, errors
+
+    with pytest.raises(errors.ShapeError):
+        api.Bank(ctx, 2, [10, 0, 3])
+    bank = make_bank(ctx, 1, [8, 4, 3])
+    X, y = inputs(1, 4, 8, 3)
+    y[0, 2] = 7
+    Xd, yd = to_dev(X, y)
+    with pytest.raises(errors.ValueError):
+        bank.train_step(Xd, yd)
+    y[0, 2] = 1
+    Xd, yd = to_dev(X, y)
+    with pytest.raises(errors.ValueError):
+        bank.train_step(Xd, yd, denom=(-1.0, 0.0))  # tape.hpp:485
+    # the context recovers: the next good call works
+    bank.train_step(Xd, yd)
+    with pytest.raises(errors.ConfigError):
+        bank.train_step(Xd, yd, frozen_layers=5)

@@ -1,0 +1,136 @@
+"""GPU parity of the multi-bandwidth Gaussian MMD kernels.
+
+Small cases: value, beta and gradients against the f64 oracle at 1e-5
+relative (max-abs / max-abs).  C4 size (65536 x 8192 x 512): size-independent
+properties -- row-sharded sums add up to the full sums bit-for-bit, the
+gradient sums to zero over all rows (antisymmetric pair terms), and a sampled
+subset of gradient rows matches the oracle.
+"""
+import numpy as np
+import pytest
+import torch
+
+import pyoracle as po
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-5
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-30))
+
+
+def sample(m, n, d, seed=3, shift=0.3):
+    r = po.Rng(seed)
+    Xs = r.normals(m * d).reshape(m, d).astype(np.float32)
+    Xt = (r.normals(n * d).reshape(n, d) + shift).astype(np.float32)
+    return Xs, Xt
+
+
+@pytest.mark.parametrize("m,n,d", [(64, 48, 32), (100, 37, 256), (5, 3, 7), (200, 200, 512),
+                                   (1, 1, 1)])
+def test_mmd_matches_oracle(ctx, m, n, d):
+    from paper_2011_09463_b200 import api
+
+    Xs, Xt = sample(m, n, d)
+    v, beta, gs, gt = api.mmd_gaussian(ctx, torch.tensor(Xs, device="cuda"),
+                                       torch.tensor(Xt, device="cuda"))
+    ov, ob, ogs, ogt = po.mmd_gaussian(Xs.astype(np.float64), Xt.astype(np.float64))
+    assert rel(beta, ob) <= 1e-9
+    assert rel(v, ov) <= TOL, (v, ov)
+    g = np.concatenate([gs.cpu().numpy(), gt.cpu().numpy()])
+    og = np.concatenate([ogs, ogt])
+    assert rel(g, og) <= TOL
+
+
+def test_mmd_explicit_beta_and_bandwidths(ctx):
+    from paper_2011_09463_b200 import api
+
+    Xs, Xt = sample(40, 30, 16)
+    mult = [0.5, 3.0]
+    v, beta, gs, gt = api.mmd_gaussian(ctx, torch.tensor(Xs, device="cuda"),
+                                       torch.tensor(Xt, device="cuda"), mult=mult, beta=7.5)
+    ov, _, ogs, ogt = po.mmd_gaussian(Xs.astype(np.float64), Xt.astype(np.float64),
+                                      mult=np.array(mult), beta=7.5)
+    assert beta == 7.5
+    assert rel(v, ov) <= TOL
+    assert rel(np.concatenate([gs.cpu(), gt.cpu()]), np.concatenate([ogs, ogt])) <= TOL
+
+
+def test_mmd_identical_samples_is_zero(ctx):
+    from paper_2011_09463_b200 import api
+
+    Xs, _ = sample(32, 1, 8)
+    t = torch.tensor(Xs, device="cuda")
+    v, _, gs, gt = api.mmd_gaussian(ctx, t, t.clone())
+    assert abs(v) < 1e-6
+    assert float((gs + gt).abs().max()) < 1e-6
+
+
+def test_mmd_translation_invariance(ctx):
+    from paper_2011_09463_b200 import api
+
+    Xs, Xt = sample(50, 40, 24)
+    a = api.mmd_gaussian(ctx, torch.tensor(Xs, device="cuda"), torch.tensor(Xt, device="cuda"))[0]
+    b = api.mmd_gaussian(ctx, torch.tensor(Xs + 2.0, device="cuda"),
+                         torch.tensor(Xt + 2.0, device="cuda"))[0]
+    assert rel(a, b) <= 1e-4
+
+
+def test_mmd_errors(ctx):
+    from paper_2011_09463_b200 import api, errors
+
+    Xs, Xt = sample(4, 4, 600)
+    with pytest.raises(errors.ShapeError):
+        api.mmd_gaussian(ctx, torch.tensor(Xs, device="cuda"), torch.tensor(Xt, device="cuda"))
+    Xs, Xt = sample(4, 4, 8)
+    with pytest.raises(errors.ValueError):
+        api.mmd_gaussian(ctx, torch.tensor(Xs, device="cuda"), torch.tensor(Xt, device="cuda"),
+                         mult=[1.0, -2.0])
+
+
+def test_mmd_c4_stress_properties(ctx):
+    """C4: m=65536, n=8192, d=512 (2.7e9 unique pairs)."""
+    from paper_2011_09463_b200 import api
+
+    m, n, d = 65536, 8192, 512
+    g = torch.Generator(device="cuda").manual_seed(0)
+    Xs = torch.randn(m, d, device="cuda", generator=g)
+    Xt = torch.randn(n, d, device="cuda", generator=g) + 0.1
+    beta = api.mmd_beta(ctx, Xs, Xt)
+    gs = torch.empty_like(Xs)
+    gt = torch.empty_like(Xt)
+    full = api.mmd_gaussian_rows(ctx, Xs, Xt, beta, 0, m + n, gXs=gs, gXt=gt)
+    # two-way row shard (as two ranks would): partial sums add up exactly
+    cut = 40000
+    gs2 = torch.empty_like(Xs)
+    gt2 = torch.empty_like(Xt)
+    p0 = api.mmd_gaussian_rows(ctx, Xs, Xt, beta, 0, cut, gXs=gs2, gXt=gt2)
+    p1 = api.mmd_gaussian_rows(ctx, Xs, Xt, beta, cut, m + n, gXs=gs2, gXt=gt2)
+    assert np.allclose(p0 + p1, full, rtol=1e-12, atol=0)
+    assert torch.equal(gs, gs2) and torch.equal(gt, gt2)
+    v = api.mmd_value_from_sums(full, m, n)
+    assert v > 0
+    # sum of all gradient rows vanishes (antisymmetric pair terms)
+    tot = torch.cat([gs, gt]).double().sum(0)
+    scale = torch.cat([gs, gt]).double().abs().sum(0).max()
+    assert float(tot.abs().max() / scale) < 1e-5
+    # sampled rows against the oracle (rows vs all columns, f64)
+    Xs_h = Xs.cpu().double().numpy()
+    Xt_h = Xt.cpu().double().numpy()
+    ob = po.mmd_beta(Xs_h, Xt_h)
+    assert rel(beta, ob) <= 1e-9
+    mult = np.array(api.MMD_MULT)
+    Z = np.concatenate([Xs_h, Xt_h])
+    rows = [0, 12345, m - 1, m, m + 4321, m + n - 1]
+    G = torch.cat([gs, gt]).cpu().double().numpy()
+    for i in rows:
+        d2 = ((Z - Z[i]) ** 2).sum(1)
+        A = sum(2.0 / (ob * q) * np.exp(-d2 / (ob * q)) for q in mult)
+        same = np.arange(m + n) < m if i < m else np.arange(m + n) >= m
+        c = np.where(same, -2.0 / (m * m) if i < m else -2.0 / (n * n), 2.0 / (m * n))
+        c[i] = 0.0
+        gi = ((c * A)[:, None] * (Z[i] - Z)).sum(0)
+        assert rel(G[i], gi) <= TOL, i

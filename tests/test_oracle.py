@@ -1,0 +1,214 @@
+"""CPU: pin the oracle (oracle/oracle.c) before trusting it.
+
+  * against the golden fixtures minted from the UNMODIFIED reference headers
+    (tests/golden/*_ref.npz; tests/make_golden.py) -- bit-exact;
+  * against the live reference shim oracle/_ref/libmtref.so when it exists
+    (random cases, bit-exact);
+  * SPEC.md known answers;
+  * MMD against an independent numpy implementation and, for its gradient,
+    the reference's own grad_check (optim.hpp:81-117) through the
+    sum(mul(h, constant(G))) injection graph;
+  * AUC against sklearn.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import pyoracle as po
+from conftest import has_ref
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def load(name):
+    return np.load(os.path.join(GOLD, name))
+
+
+# ------------------------------------------------------------------- RNG
+@pytest.mark.parametrize("seed", [0, 1, 42, 20110946])
+def test_rng_matches_reference_golden(seed):
+    g = load("rng_ref.npz")
+    r = po.Rng(seed)
+    assert np.array_equal([r.next_u64() for _ in range(64)], g[f"s{seed}_u64"])
+    assert np.array_equal([r.normal() for _ in range(65)], g[f"s{seed}_normal"])
+    assert np.array_equal([r.uniform(-0.3, 0.7) for _ in range(64)], g[f"s{seed}_uniform"])
+    assert np.array_equal([r.below(10) for _ in range(64)], g[f"s{seed}_below"])
+    assert np.array_equal(r.permutation(100), g[f"s{seed}_perm"])
+    c = r.split(3)
+    assert np.array_equal([c.next_u64() for _ in range(8)], g[f"s{seed}_split"])
+
+
+def test_rng_std_mt19937_64_known_value():
+    # the C++ standard pins the 10000th output of default-seeded mt19937_64
+    r = po.Rng(5489)
+    for _ in range(9999):
+        r.next_u64()
+    assert r.next_u64() == 9981545732273789042
+
+
+@pytest.mark.skipif(not has_ref(), reason="reference shim not built here")
+def test_rng_matches_live_reference():
+    R = po.ref()
+    for seed in (3, 77, 2**63 + 5):
+        r, h = po.Rng(seed), R.ref_rng_create(seed)
+        for _ in range(3000):
+            assert r.next_u64() == R.ref_rng_next(h)
+            assert r.normal() == R.ref_rng_normal(h)
+            assert r.below(1000003) == R.ref_rng_below(h, 1000003)
+        R.ref_rng_destroy(h)
+
+
+# ------------------------------------------------------------------- MLP
+CASES = ["plain", "inject", "frozen", "two_heads", "weighted"]
+SPECS = {
+    "plain": dict(dims=[6, 5, 4, 3], n_heads=1, frozen=0, src=0),
+    "inject": dict(dims=[6, 5, 4, 3], n_heads=1, frozen=0, src=4),
+    "frozen": dict(dims=[6, 5, 4, 3], n_heads=1, frozen=1, src=0),
+    "two_heads": dict(dims=[6, 5, 4, 3], n_heads=2, frozen=0, src=4),
+    "weighted": dict(dims=[7, 3], n_heads=1, frozen=0, src=0),
+}
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_mlp_step_matches_reference_golden(name):
+    g = load("mlp_ref.npz")
+    c = SPECS[name]
+    n_mats = len(c["dims"]) - 1 + c["n_heads"] - 1
+    W = [g[f"{name}_W{i}_before"].copy() for i in range(n_mats)]
+    b = [g[f"{name}_b{i}_before"].copy() for i in range(n_mats)]
+    dH = g[f"{name}_dH"] if f"{name}_dH" in g else None
+    w = g[f"{name}_w"] if f"{name}_w" in g else None
+    loss, gW, gb = po.mlp_train_step(c["dims"], W, b, g[f"{name}_X"], g[f"{name}_y"],
+                                     n_heads=c["n_heads"], frozen=c["frozen"], src_rows=c["src"],
+                                     lr=0.1, dH=dH, w=w,
+                                     denoms=[4.5] if name == "weighted" else None, want_grads=True)
+    assert loss == g[f"{name}_loss"][0]
+    for i in range(n_mats):
+        assert np.array_equal(W[i], g[f"{name}_W{i}_after"]), i
+        assert np.array_equal(b[i], g[f"{name}_b{i}_after"]), i
+        assert np.array_equal(gW[i], g[f"{name}_gW{i}"]), i
+        assert np.array_equal(gb[i], g[f"{name}_gb{i}"]), i
+
+
+@pytest.mark.skipif(not has_ref(), reason="reference shim not built here")
+@pytest.mark.parametrize("dims,n_heads,frozen,inject", [
+    ([30, 17, 9, 4], 1, 0, False), ([30, 17, 9, 4], 1, 0, True), ([12, 8, 5], 2, 0, False),
+    ([12, 8, 5, 5, 3], 1, 2, False), ([4, 2], 1, 0, False)])
+def test_mlp_step_matches_live_reference(dims, n_heads, frozen, inject):
+    r = po.Rng(sum(dims))
+    W, b = po.mlp_init(r, dims, n_heads)
+    W2, b2 = [x.copy() for x in W], [x.copy() for x in b]
+    B = 11
+    X = r.normals(B * dims[0]).reshape(B, dims[0])
+    y = np.array([r.below(dims[-1]) for _ in range(B)], dtype=np.int32)
+    dH = r.normals(B * dims[-2]).reshape(B, dims[-2]) if inject else None
+    for _ in range(3):
+        l1 = po.mlp_train_step(dims, W, b, X, y, n_heads=n_heads, frozen=frozen, src_rows=6,
+                               dH=dH, lr=0.2)
+        l2 = po.ref_mlp_train_step(dims, W2, b2, X, y, n_heads=n_heads, frozen=frozen,
+                                   src_rows=6, dH=dH, lr=0.2)
+        assert l1 == l2
+    for a, c in zip(W + b, W2 + b2):
+        assert np.array_equal(a, c)
+
+
+def test_spec_known_answers():
+    # matmul [[1,2],[3,4]] . [[5],[6]] = [17, 39]: one linear layer, zero bias
+    logits, _ = po.mlp_forward([2, 1], [np.array([[5.0], [6.0]])], [np.zeros(1)],
+                               np.array([[1.0, 2.0], [3.0, 4.0]]))
+    assert np.array_equal(logits[:, 0], [17.0, 39.0])
+    # uniform-logit CE over 4 classes = ln 4
+    W = [np.zeros((3, 4))]
+    b = [np.zeros(4)]
+    loss = po.mlp_train_step([3, 4], W, b, np.ones((2, 3)), np.array([0, 3], dtype=np.int32),
+                             lr=0.0)
+    assert abs(loss - 1.386294361119891) < 1e-15
+    # softmax([0, ln 3]) = [0.25, 0.75]
+    assert np.allclose(po.softmax(np.array([[0.0, np.log(3.0)]])), [[0.25, 0.75]], atol=1e-15)
+    # SGD: w=1.0, g=0.5, lr=0.1 -> 0.95: a 1x1 layer whose dW is 0.5
+    #   dlogit/dW = x, CE grad wrt logit of a 2-class... use the oracle's SGD on known grads
+    W = [np.array([[1.0, 0.0]])]
+    b = [np.zeros(2)]
+    loss, gW, _ = po.mlp_train_step([1, 2], W, b, np.array([[1.0]]), np.array([1], dtype=np.int32),
+                                    lr=0.1, want_grads=True)
+    assert abs(W[0][0, 0] - (1.0 - 0.1 * gW[0][0, 0])) == 0.0
+
+
+# ------------------------------------------------------------------- MMD
+@pytest.mark.parametrize("case", range(4))
+def test_mmd_matches_independent_numpy(case):
+    g = load("mmd_numpy.npz")
+    v, beta, gs, gt = po.mmd_gaussian(g[f"c{case}_Xs"], g[f"c{case}_Xt"])
+    assert abs(beta - g[f"c{case}_beta"][0]) <= 1e-12 * abs(beta)
+    assert abs(v - g[f"c{case}_value"][0]) <= 1e-12 * max(abs(v), 1e-3)
+    ref = np.concatenate([g[f"c{case}_gXs"], g[f"c{case}_gXt"]])
+    got = np.concatenate([gs, gt])
+    assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+def test_mmd_gradient_finite_differences():
+    r = po.Rng(9)
+    Xs = r.normals(6 * 3).reshape(6, 3)
+    Xt = r.normals(4 * 3).reshape(4, 3) + 0.5
+    v, beta, gs, gt = po.mmd_gaussian(Xs, Xt)
+    eps = 1e-6
+    for (X, G) in ((Xs, gs), (Xt, gt)):
+        for idx in [(0, 0), (2, 1), (3, 2)]:
+            old = X[idx]
+            X[idx] = old + eps
+            vp = po.mmd_gaussian(Xs, Xt, beta=beta, grads=False)[0]
+            X[idx] = old - eps
+            vm = po.mmd_gaussian(Xs, Xt, beta=beta, grads=False)[0]
+            X[idx] = old
+            assert abs((vp - vm) / (2 * eps) - G[idx]) < 1e-7
+
+
+@pytest.mark.skipif(not has_ref(), reason="reference shim not built here")
+def test_mmd_gradient_reference_grad_check():
+    """optim.hpp:87-117 grad_check over tanh-encoder params, beta frozen."""
+    R = po.ref()
+    r = po.Rng(4)
+    Xs = r.normals(6 * 4).reshape(6, 4)
+    Xt = r.normals(5 * 4).reshape(5, 4) + 0.3
+    W0 = r.uniforms(12, -0.5, 0.5)
+    b0 = np.zeros(3)
+    Wm = W0.reshape(4, 3)
+    beta = po.mmd_beta(np.tanh(Xs @ Wm), np.tanh(Xt @ Wm))
+    err = R.ref_grad_check_mmd(4, 3, po.dp(Xs), 6, po.dp(Xt), 5, po.dp(W0), po.dp(b0),
+                               po.dp(np.array(po.MMD_MULT)), 5, 1.0, beta)
+    assert err < 1e-6
+
+
+def test_mmd_beta_closed_form():
+    r = po.Rng(2)
+    Xs = r.normals(9 * 5).reshape(9, 5)
+    Xt = r.normals(4 * 5).reshape(4, 5)
+    Z = np.concatenate([Xs, Xt])
+    D = ((Z[:, None] - Z[None]) ** 2).sum(-1)
+    assert abs(po.mmd_beta(Xs, Xt) - D.sum() / (13 * 12)) < 1e-12
+
+
+# ------------------------------------------------------------------- attack stage
+@pytest.mark.parametrize("case", range(4))
+def test_auc_matches_sklearn(case):
+    g = load("auc_sklearn.npz")
+    assert abs(po.auc(g[f"c{case}_s"], g[f"c{case}_l"]) - g[f"c{case}_auc"][0]) < 1e-12
+
+
+def test_features():
+    r = po.Rng(3)
+    x = r.normals(50 * 10).reshape(50, 10)
+    f = po.posterior_features(x, 3, np.arange(50, dtype=np.int32) % 10)
+    p = np.exp(x - x.max(1, keepdims=True))
+    p /= p.sum(1, keepdims=True)
+    assert np.allclose(f[:, :3], -np.sort(-p, 1)[:, :3], atol=1e-15)
+    lse = np.log(np.exp(x - x.max(1, keepdims=True)).sum(1)) + x.max(1)
+    assert np.allclose(f[:, 3], lse - x[np.arange(50), np.arange(50) % 10], atol=1e-12)
+
+
+def test_synth_deterministic():
+    mu = np.arange(20.0).reshape(4, 5)
+    a = po.synth(po.Rng(1), 4, 5, 7, mu)
+    b = po.synth(po.Rng(1), 4, 5, 7, mu)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
