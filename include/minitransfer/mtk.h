@@ -166,6 +166,13 @@ int mtk_posterior_column(mtk_ctx* ctx, const float* logits, int64_t rows, int C,
 int mtk_auc(mtk_ctx* ctx, const float* scores, const uint8_t* labels, int64_t n,
             double* auc_host, double* acc_host);
 
+/* ---- diagnostics (tests / profiling): C[g] = A[g] * B[g] through the
+ * tcgen05 3xTF32 tensor-core GEMM used by the bank.  a_mn: A stored
+ * [G][K][M] (1) or [G][M][K] (0); b_mn: B stored [G][K][N] (1) or [G][N][K]
+ * (0); C [G][M][N] fp32.  Synchronizing.                                    */
+int mtk_diag_gemm_tf32x3(mtk_ctx* ctx, int a_mn, int b_mn, int G, int M, int N, int K,
+                         const float* A, const float* B, float* C);
+
 #ifdef __cplusplus
 }
 #endif

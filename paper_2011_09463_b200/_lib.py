@@ -83,6 +83,8 @@ SIGNATURES = {
     "mtk_posterior_features": (C.c_int, [_vp, _vp, C.c_int64, C.c_int, C.c_int, _vp, _vp]),
     "mtk_posterior_column": (C.c_int, [_vp, _vp, C.c_int64, C.c_int, C.c_int, _vp]),
     "mtk_auc": (C.c_int, [_vp, _vp, _vp, C.c_int64, _dp, _dp]),
+    "mtk_diag_gemm_tf32x3": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                       _vp, _vp, _vp]),
 }
 
 for _name, (_res, _args) in SIGNATURES.items():

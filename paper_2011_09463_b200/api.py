@@ -323,3 +323,15 @@ def auc(ctx: Context, scores: torch.Tensor, labels: torch.Tensor):
     errors.check(lib.mtk_auc(ctx.h, _ptr(scores), _ptr(labels), scores.numel(), C.byref(a),
                              C.byref(acc)), "auc")
     return a.value, acc.value
+
+
+def diag_gemm_tf32x3(ctx: Context, A: torch.Tensor, B: torch.Tensor, a_mn: bool, b_mn: bool):
+    """Diagnostics: C = A @ B on the tcgen05 3xTF32 path.  A is [G,M,K] (or
+    [G,K,M] if a_mn), B is [G,K,N] (or [G,N,K] if not b_mn); returns [G,M,N]."""
+    G = A.shape[0]
+    M, K = (A.shape[2], A.shape[1]) if a_mn else (A.shape[1], A.shape[2])
+    N = B.shape[2] if b_mn else B.shape[1]
+    C_ = torch.empty((G, M, N), device=A.device, dtype=torch.float32)
+    errors.check(lib.mtk_diag_gemm_tf32x3(ctx.h, int(a_mn), int(b_mn), G, M, N, K, _ptr(A),
+                                          _ptr(B), _ptr(C_)), "diag_gemm_tf32x3")
+    return C_

@@ -12,6 +12,7 @@
 //   [mapping]  MMD beta, pairs, finish            -> lambda * dMMD/dH_{L-1}
 //   per layer  DX gemm (+inject, *ReLU mask) then DW gemm (+SGD) + bias SGD
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -48,7 +49,8 @@ void* Ctx::pinned_buf(size_t bytes) {
 }
 
 void Ctx::check_flags() {
-    int* h = static_cast<int*>(pinned_buf(4096));
+    if (!pinned_flags) MTK_CUDA(cudaMallocHost(&pinned_flags, 64));
+    int* h = pinned_flags;
     MTK_CUDA(cudaMemcpyAsync(h, d_flags, sizeof(int), cudaMemcpyDeviceToHost, stream));
     MTK_CUDA(cudaStreamSynchronize(stream));
     const int f = *h;
@@ -506,6 +508,7 @@ int mtk_ctx_destroy(mtk_ctx* c) {
         cudaFree(c->d_flags);
         cudaFree(c->d_scratch);
         if (c->pinned) cudaFreeHost(c->pinned);
+        if (c->pinned_flags) cudaFreeHost(c->pinned_flags);
         if (c->own_stream) cudaStreamDestroy(c->stream);
         delete c;
     });
@@ -895,6 +898,49 @@ int mtk_auc(mtk_ctx* c, const float* scores, const uint8_t* labels, int64_t n, d
         need(c && scores && labels, MTK_VALUE_ERROR, "auc: null argument");
         need(n >= 1, MTK_SHAPE_ERROR, "auc: zero rows");
         auc_device(*c, scores, labels, n, auc_host, acc_host);
+        c->check_flags();
+    });
+}
+
+int mtk_diag_gemm_tf32x3(mtk_ctx* c, int a_mn, int b_mn, int G, int M, int N, int K,
+                         const float* A, const float* B, float* Cm) {
+    return guard([&] {
+        need(c && A && B && Cm, MTK_VALUE_ERROR, "diag_gemm: null argument");
+        need(G >= 1 && M >= 1 && N >= 1 && K >= 1, MTK_SHAPE_ERROR, "diag_gemm: zero dimension");
+        const size_t na = (size_t)G * M * K, nb = (size_t)G * K * N;
+        float* buf = nullptr;
+        MTK_CUDA(cudaMallocAsync(&buf, (2 * na + 2 * nb + 64) * sizeof(float), c->stream));
+        float* ahi = buf;
+        float* alo = ahi + na;
+        float* bhi = alo + na;
+        float* blo = bhi + nb;
+        launch_split(A, ahi, alo, (long long)na, c->stream);
+        launch_split(B, bhi, blo, (long long)nb, c->stream);
+        after_launch(*c, 2);
+        UmmaGemm u;
+        u.G = G;
+        u.M = M;
+        u.N = N;
+        u.K = K;
+        u.a_mn = a_mn;
+        u.b_mn = b_mn;
+        u.a_hi = ahi;
+        u.a_lo = alo;
+        u.a_rs = a_mn ? M : K;
+        u.a_gs = (long long)M * K;
+        u.b_hi = bhi;
+        u.b_lo = blo;
+        u.b_rs = b_mn ? N : K;
+        u.b_gs = (long long)K * N;
+        u.epi = Epi::kStore;
+        u.C = Cm;
+        u.c_gs = (long long)M * N;
+        u.ldc = N;
+        u.flags = c->d_flags;
+        if (getenv("MTK_UMMA_DEBUG")) u.dbg = reinterpret_cast<float*>(strtoull(getenv("MTK_UMMA_DEBUG"), nullptr, 0));
+        launch_umma(u, c->stream);
+        after_launch(*c);
+        MTK_CUDA(cudaFreeAsync(buf, c->stream));
         c->check_flags();
     });
 }

@@ -49,6 +49,7 @@ struct Ctx {
     size_t scratch_bytes = 0;
     uint64_t launches = 0;
     void* pinned = nullptr;          // host staging for small results
+    int* pinned_flags = nullptr;     // dedicated host word for check_flags()
     size_t pinned_bytes = 0;
     double* scratch(size_t bytes);
     void* pinned_buf(size_t bytes);
@@ -74,6 +75,7 @@ enum class Epi : int {
     kBiasRelu = 1,  // C = max(acc + bias[n], 0)
     kMask = 2,      // C = (acc + add[m,n]) * (mask[m,n] > 0)      (dX through ReLU)
     kSgd = 3,       // C(=W) -= lr * acc ; optionally grad_out = acc  (dW + SGD)
+    kStore = 4,     // C = acc (diagnostics)
 };
 
 struct Gemm {
@@ -95,6 +97,37 @@ struct Gemm {
 };
 
 void launch_gemm(const Gemm& g, cudaStream_t s);
+
+// tcgen05 3xTF32 grouped GEMM (k_umma.cu).  Operands are given as tf32 hi/lo
+// planes; element (r, c) of a plane sits at base[g*gs + r*rs + c], c being the
+// contiguous index: for a K-major operand r = m (or n) and c = k, for an
+// MN-major operand r = k and c = m (or n).  The epilogue writes C (fp32) and
+// its hi/lo split planes C_hi / C_lo (same layout as C).
+struct UmmaGemm {
+    int G = 1, M = 0, N = 0, K = 0;
+    int a_mn = 0, b_mn = 0;
+    const float* a_hi = nullptr;
+    const float* a_lo = nullptr;
+    long long a_rs = 0, a_gs = 0;
+    const float* b_hi = nullptr;
+    const float* b_lo = nullptr;
+    long long b_rs = 0, b_gs = 0;
+    Epi epi = Epi::kStore;
+    float* C = nullptr;
+    float* C_hi = nullptr;
+    float* C_lo = nullptr;
+    long long c_gs = 0, ldc = 0;
+    const float* bias = nullptr;
+    long long bias_gs = 0;
+    const float* add = nullptr;
+    const float* mask = nullptr;
+    float lr = 0.f;
+    float* grad_out = nullptr;
+    int* flags = nullptr;
+    float* dbg = nullptr;
+};
+void launch_umma(const UmmaGemm& u, cudaStream_t s);
+void launch_split(const float* x, float* hi, float* lo, long long n, cudaStream_t s);
 
 // Cross-entropy head (tape.hpp:475-520), rows laid out [G, B, C].
 struct CeArgs {

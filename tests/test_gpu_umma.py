@@ -1,0 +1,32 @@
+"""GPU: the tcgen05 3xTF32 grouped GEMM (k_umma.cu) against an f64 product.
+
+All four operand-major combinations the bank uses, aligned and ragged shapes
+(K not a multiple of 32, M/N not multiples of 128), G > 1.  Tolerance
+1e-5 relative (max-abs / max-abs), the north_star per-kernel bound.
+"""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-30))
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 1), (0, 0), (1, 1), (1, 0)])
+@pytest.mark.parametrize("G,M,N,K", [(1, 128, 128, 32), (2, 256, 128, 784), (3, 200, 96, 76), (2, 136, 40, 20),
+                                     (2, 1024, 512, 1024), (1, 64, 256, 512)])
+def test_umma_gemm(ctx, a_mn, b_mn, G, M, N, K):
+    from paper_2011_09463_b200 import api
+
+    g = torch.Generator().manual_seed(M + N + K)
+    A = torch.randn((G, M, K), generator=g)
+    B = torch.randn((G, K, N), generator=g)
+    ref = torch.matmul(A.double(), B.double()).numpy()
+    Ad = (A.transpose(1, 2) if a_mn else A).contiguous().cuda()
+    Bd = (B if b_mn else B.transpose(1, 2)).contiguous().cuda()
+    C = api.diag_gemm_tf32x3(ctx, Ad, Bd, bool(a_mn), bool(b_mn)).cpu().double().numpy()
+    e = rel(C, ref)
+    assert e <= 1e-5, e
