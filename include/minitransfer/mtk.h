@@ -130,6 +130,10 @@ int mtk_bank_train_step(mtk_bank* bank, const mtk_step* step, double* loss_host,
 int mtk_bank_train_step_host(mtk_bank* bank, const mtk_step* step, const float* X_host,
                              const int32_t* y_host, const float* w_host, double* loss_host,
                              double* mmd_host);
+/* which layers run their GEMMs on the tcgen05 3xTF32 path (1) vs the SIMT
+ * path (0); out_host [n_layers].  Layers with both widths >= 32 and
+ * multiples of 4 qualify (env MTK_DISABLE_TC=1 at bank creation forces SIMT). */
+int mtk_bank_tc_layers(mtk_bank* bank, int* out_host);
 /* debug/parity: keep the last step's parameter gradients (dW, db).          */
 int mtk_bank_set_keep_grads(mtk_bank* bank, int on);
 int mtk_bank_get_grads(mtk_bank* bank, int model, double* const* dW_host, double* const* db_host);

@@ -234,6 +234,12 @@ class Bank:
                                                   _ptr(w_host), lp, mp), "train_step_host")
         return (self._loss.copy(), self._mmd.copy()) if want_loss else None
 
+    def tc_layers(self):
+        """per layer: True if its GEMMs run on the tcgen05 3xTF32 path"""
+        out = (C.c_int * self.L)()
+        errors.check(lib.mtk_bank_tc_layers(self.h, out))
+        return [bool(x) for x in out]
+
     def keep_grads(self, on: bool = True):
         errors.check(lib.mtk_bank_set_keep_grads(self.h, 1 if on else 0))
 

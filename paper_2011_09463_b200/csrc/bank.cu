@@ -1,0 +1,765 @@
+// bank.cu -- the grouped shadow-model bank (C ABI mtk_bank_*).
+//
+// One bank step runs, for all G models at once, the reference composition
+//   forward : matmul -> add_bias -> relu ... -> cross_entropy_weighted
+//             (tape.hpp:225-290, 204-221, 342-352, 475-520)
+//   backward: Tape::backward reverse sweep (tape.hpp:870-886)
+//   update  : optimizer_step SGD (optim.hpp:46-48)
+// as a fixed schedule of fused kernels (no device tape):
+//   [tc layer 0] split X into tf32 hi/lo planes
+//   per layer    FWD gemm (+bias, +ReLU)             -> H[l+1] (fp32 + hi/lo)
+//   head         CE (softmax, loss, dlogits)         -> dZ_{L-1}
+//   [mapping]    MMD beta, pairs, finish             -> lambda * dMMD/dH_{L-1}
+//   per layer    DX gemm (+inject, *ReLU mask) then DW gemm (+SGD) + bias SGD
+// Layers whose in/out widths are >= 32 and multiples of 4 ("tc layers") run
+// their three GEMMs on the tcgen05 3xTF32 path (k_umma.cu); narrow layers
+// (the 10-class head, the 3-feature attack input) use the SIMT kernel.
+//
+// HBM layout per bank (row-major fp32):
+//   W[i]  [G, fan_in, fan_out] master + (tc) hi/lo planes;  b[i] [G, fan_out]
+//   H[l]  [G, B, dims[l]] post-ReLU activations + (tc) hi/lo planes
+//   dZ    two ping-pong [G, B, max dim] gradient buffers + hi/lo planes
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+using namespace mtk;
+
+namespace {
+
+struct Plane3 {
+    float* f = nullptr;   // fp32 values
+    float* hi = nullptr;  // tf32 hi plane (tensor-core operand), optional
+    float* lo = nullptr;  // tf32 lo plane, optional
+};
+
+void free3(Plane3& p, bool own_f = true) {
+    if (own_f) cudaFree(p.f);
+    cudaFree(p.hi);
+    cudaFree(p.lo);
+    p = Plane3{};
+}
+
+void alloc3(Plane3& p, size_t n, bool f, bool split) {
+    if (f) MTK_CUDA(cudaMalloc(&p.f, n * sizeof(float)));
+    if (split) {
+        MTK_CUDA(cudaMalloc(&p.hi, n * sizeof(float)));
+        MTK_CUDA(cudaMalloc(&p.lo, n * sizeof(float)));
+    }
+}
+
+}  // namespace
+
+struct mtk_bank {
+    mtk_ctx* ctx = nullptr;
+    int G = 0, L = 0, n_heads = 1, n_mats = 0;
+    std::vector<int> dims;
+    std::vector<bool> tc;  // per layer: tensor-core path
+    std::vector<Plane3> W;
+    std::vector<float*> b, gW, gb;
+    bool keep_grads = false;
+    int capB = 0;
+    Plane3 Xsp;               // hi/lo planes of the input (f borrowed per call)
+    std::vector<Plane3> H;    // H[l], l in [1, L)
+    Plane3 dZ[2];
+    float* logits = nullptr;
+    double* row_loss = nullptr;
+    double* loss = nullptr;
+    double* mmd = nullptr;
+    double* beta = nullptr;
+    float* gH = nullptr;
+    double* mmd_part = nullptr;
+    size_t mmd_part_bytes = 0;
+    float* Xs = nullptr;
+    int32_t* ys = nullptr;
+    float* ws = nullptr;
+    int stageB = 0;
+
+    int layer_of(int i) const { return i < L ? i : L - 1; }
+    int fan_in(int i) const { return dims[layer_of(i)]; }
+    int fan_out(int i) const { return dims[layer_of(i) + 1]; }
+    bool any_tc() const {
+        for (bool t : tc)
+            if (t) return true;
+        return false;
+    }
+    int maxd() const {
+        int m = 0;
+        for (int v : dims) m = std::max(m, v);
+        return m;
+    }
+
+    ~mtk_bank() {
+        for (auto& p : W) free3(p);
+        for (auto* p : b) cudaFree(p);
+        for (auto* p : gW) cudaFree(p);
+        for (auto* p : gb) cudaFree(p);
+        free_acts();
+        cudaFree(loss);
+        cudaFree(mmd);
+        cudaFree(beta);
+        cudaFree(mmd_part);
+        cudaFree(Xs);
+        cudaFree(ys);
+        cudaFree(ws);
+    }
+    void free_acts() {
+        for (auto& p : H) free3(p);
+        H.clear();
+        free3(Xsp, false);
+        free3(dZ[0]);
+        free3(dZ[1]);
+        cudaFree(logits);
+        cudaFree(row_loss);
+        cudaFree(gH);
+        logits = nullptr;
+        gH = nullptr;
+        row_loss = nullptr;
+    }
+    void ensure(int B) {
+        if (B <= capB) return;
+        MTK_CUDA(cudaStreamSynchronize(ctx->stream));
+        free_acts();
+        const size_t GB = (size_t)G * B;
+        H.assign(L, Plane3{});
+        for (int l = 1; l < L; ++l) alloc3(H[l], GB * dims[l], true, tc[l]);
+        alloc3(Xsp, GB * dims[0], false, tc[0]);
+        for (auto& z : dZ) alloc3(z, GB * maxd(), true, any_tc());
+        MTK_CUDA(cudaMalloc(&logits, GB * dims[L] * sizeof(float)));
+        MTK_CUDA(cudaMalloc(&row_loss, GB * sizeof(double)));
+        if (L > 1) MTK_CUDA(cudaMalloc(&gH, GB * dims[L - 1] * sizeof(float)));
+        capB = B;
+    }
+    void ensure_stage(int B) {
+        if (B <= stageB) return;
+        MTK_CUDA(cudaStreamSynchronize(ctx->stream));
+        cudaFree(Xs);
+        cudaFree(ys);
+        cudaFree(ws);
+        const size_t GB = (size_t)G * B;
+        MTK_CUDA(cudaMalloc(&Xs, GB * dims[0] * sizeof(float)));
+        MTK_CUDA(cudaMalloc(&ys, GB * sizeof(int32_t)));
+        MTK_CUDA(cudaMalloc(&ws, GB * sizeof(float)));
+        stageB = B;
+    }
+    // re-derive the tf32 planes of parameter matrix i from its fp32 master
+    void split_param(int i) {
+        if (!W[i].hi) return;
+        launch_split(W[i].f, W[i].hi, W[i].lo, (long long)G * fan_in(i) * fan_out(i), ctx->stream);
+        after_launch(*ctx);
+    }
+};
+
+namespace {
+
+// ---- GEMM dispatch over row range [r0, r0+rows) of every model -------------
+// FWD: out[r, n] = sum_k in[r, k] W[k, n] (+bias, ReLU)
+void gemm_fwd(mtk_bank& k, int mat, const Plane3& in, int B, int r0, int rows, const Plane3& out,
+              bool relu) {
+    Ctx& c = *k.ctx;
+    const int fi = k.fan_in(mat), fo = k.fan_out(mat);
+    if (k.tc[k.layer_of(mat)]) {
+        UmmaGemm u;
+        u.G = k.G;
+        u.M = rows;
+        u.N = fo;
+        u.K = fi;
+        u.a_mn = 0;
+        u.a_hi = in.hi + (size_t)r0 * fi;
+        u.a_lo = in.lo + (size_t)r0 * fi;
+        u.a_rs = fi;
+        u.a_gs = (long long)B * fi;
+        u.b_mn = 1;
+        u.b_hi = k.W[mat].hi;
+        u.b_lo = k.W[mat].lo;
+        u.b_rs = fo;
+        u.b_gs = (long long)fi * fo;
+        u.epi = relu ? Epi::kBiasRelu : Epi::kBias;
+        u.C = out.f + (size_t)r0 * fo;
+        u.C_hi = out.hi ? out.hi + (size_t)r0 * fo : nullptr;
+        u.C_lo = out.lo ? out.lo + (size_t)r0 * fo : nullptr;
+        u.c_gs = (long long)B * fo;
+        u.ldc = fo;
+        u.bias = k.b[mat];
+        u.bias_gs = fo;
+        u.flags = c.d_flags;
+        launch_umma(u, c.stream);
+    } else {
+        Gemm g;
+        g.G = k.G;
+        g.M = rows;
+        g.N = fo;
+        g.K = fi;
+        g.A = in.f + (size_t)r0 * fi;
+        g.a_gs = (long long)B * fi;
+        g.a_ms = fi;
+        g.a_ks = 1;
+        g.B = k.W[mat].f;
+        g.b_gs = (long long)fi * fo;
+        g.b_ks = fo;
+        g.b_ns = 1;
+        g.C = out.f + (size_t)r0 * fo;
+        g.C_hi = out.hi ? out.hi + (size_t)r0 * fo : nullptr;
+        g.C_lo = out.lo ? out.lo + (size_t)r0 * fo : nullptr;
+        g.c_gs = (long long)B * fo;
+        g.ldc = fo;
+        g.epi = relu ? Epi::kBiasRelu : Epi::kBias;
+        g.bias = k.b[mat];
+        g.bias_gs = fo;
+        g.flags = c.d_flags;
+        launch_gemm(g, c.stream);
+    }
+}
+
+// DX: out[r, p] = (sum_j dz[r, j] W[p, j] + add[r, p]) * (mask[r, p] > 0)
+void gemm_dx(mtk_bank& k, int mat, const Plane3& dz, int B, int r0, int rows, const Plane3& out,
+             const float* mask, const float* add) {
+    Ctx& c = *k.ctx;
+    const int fi = k.fan_in(mat), fo = k.fan_out(mat);
+    if (k.tc[k.layer_of(mat)]) {
+        UmmaGemm u;
+        u.G = k.G;
+        u.M = rows;
+        u.N = fi;
+        u.K = fo;
+        u.a_mn = 0;
+        u.a_hi = dz.hi + (size_t)r0 * fo;
+        u.a_lo = dz.lo + (size_t)r0 * fo;
+        u.a_rs = fo;
+        u.a_gs = (long long)B * fo;
+        u.b_mn = 0;  // B(k=j, n=p) = W[p][j]: rows p, contiguous j
+        u.b_hi = k.W[mat].hi;
+        u.b_lo = k.W[mat].lo;
+        u.b_rs = fo;
+        u.b_gs = (long long)fi * fo;
+        u.epi = Epi::kMask;
+        u.C = out.f + (size_t)r0 * fi;
+        u.C_hi = out.hi ? out.hi + (size_t)r0 * fi : nullptr;
+        u.C_lo = out.lo ? out.lo + (size_t)r0 * fi : nullptr;
+        u.c_gs = (long long)B * fi;
+        u.ldc = fi;
+        u.mask = mask + (size_t)r0 * fi;
+        u.add = add ? add + (size_t)r0 * fi : nullptr;
+        u.flags = c.d_flags;
+        launch_umma(u, c.stream);
+    } else {
+        Gemm g;
+        g.G = k.G;
+        g.M = rows;
+        g.N = fi;
+        g.K = fo;
+        g.A = dz.f + (size_t)r0 * fo;
+        g.a_gs = (long long)B * fo;
+        g.a_ms = fo;
+        g.a_ks = 1;
+        g.B = k.W[mat].f;
+        g.b_gs = (long long)fi * fo;
+        g.b_ks = 1;
+        g.b_ns = fo;
+        g.C = out.f + (size_t)r0 * fi;
+        g.C_hi = out.hi ? out.hi + (size_t)r0 * fi : nullptr;
+        g.C_lo = out.lo ? out.lo + (size_t)r0 * fi : nullptr;
+        g.c_gs = (long long)B * fi;
+        g.ldc = fi;
+        g.epi = Epi::kMask;
+        g.mask = mask + (size_t)r0 * fi;
+        g.add = add ? add + (size_t)r0 * fi : nullptr;
+        g.flags = c.d_flags;
+        launch_gemm(g, c.stream);
+    }
+}
+
+// DW + SGD: W[p, j] -= lr * sum_r in[r, p] dz[r, j]
+void gemm_dw(mtk_bank& k, int mat, const Plane3& in, const Plane3& dz, int B, int r0, int rows,
+             float lr) {
+    Ctx& c = *k.ctx;
+    const int fi = k.fan_in(mat), fo = k.fan_out(mat);
+    if (k.tc[k.layer_of(mat)]) {
+        UmmaGemm u;
+        u.G = k.G;
+        u.M = fi;
+        u.N = fo;
+        u.K = rows;
+        u.a_mn = 1;  // A(m=p, k=r) = in[r][p]
+        u.a_hi = in.hi + (size_t)r0 * fi;
+        u.a_lo = in.lo + (size_t)r0 * fi;
+        u.a_rs = fi;
+        u.a_gs = (long long)B * fi;
+        u.b_mn = 1;  // B(k=r, n=j) = dz[r][j]
+        u.b_hi = dz.hi + (size_t)r0 * fo;
+        u.b_lo = dz.lo + (size_t)r0 * fo;
+        u.b_rs = fo;
+        u.b_gs = (long long)B * fo;
+        u.epi = Epi::kSgd;
+        u.C = k.W[mat].f;
+        u.C_hi = k.W[mat].hi;
+        u.C_lo = k.W[mat].lo;
+        u.c_gs = (long long)fi * fo;
+        u.ldc = fo;
+        u.lr = lr;
+        u.grad_out = k.keep_grads ? k.gW[mat] : nullptr;
+        u.flags = c.d_flags;
+        launch_umma(u, c.stream);
+    } else {
+        Gemm g;
+        g.G = k.G;
+        g.M = fi;
+        g.N = fo;
+        g.K = rows;
+        g.A = in.f + (size_t)r0 * fi;
+        g.a_gs = (long long)B * fi;
+        g.a_ms = 1;
+        g.a_ks = fi;
+        g.B = dz.f + (size_t)r0 * fo;
+        g.b_gs = (long long)B * fo;
+        g.b_ks = fo;
+        g.b_ns = 1;
+        g.C = k.W[mat].f;
+        g.C_hi = k.W[mat].hi;
+        g.C_lo = k.W[mat].lo;
+        g.c_gs = (long long)fi * fo;
+        g.ldc = fo;
+        g.epi = Epi::kSgd;
+        g.lr = lr;
+        g.grad_out = k.keep_grads ? k.gW[mat] : nullptr;
+        g.flags = c.d_flags;
+        launch_gemm(g, c.stream);
+    }
+}
+
+Plane3 input_plane(mtk_bank& k, const float* X, int B) {
+    Plane3 in = k.Xsp;
+    in.f = const_cast<float*>(X);
+    if (k.tc[0]) {
+        PhaseScope ph(*k.ctx, kPhOther, 1);
+        launch_split(X, in.hi, in.lo, (long long)k.G * B * k.dims[0], k.ctx->stream);
+        after_launch(*k.ctx);
+    }
+    return in;
+}
+
+void run_forward(mtk_bank& k, const Plane3& X, int B, int head_all, int src_rows) {
+    Ctx& c = *k.ctx;
+    Plane3 h = X;
+    Plane3 lg;
+    lg.f = k.logits;
+    for (int l = 0; l < k.L; ++l) {
+        PhaseScope ph(c, kPhFwd, (l == k.L - 1 && head_all < 0) ? 2 : 1);
+        if (l < k.L - 1) {
+            gemm_fwd(k, l, h, B, 0, B, k.H[l + 1], true);
+            after_launch(c);
+            h = k.H[l + 1];
+        } else if (head_all >= 0) {
+            gemm_fwd(k, l + head_all, h, B, 0, B, lg, false);
+            after_launch(c);
+        } else {  // two heads split by rows
+            gemm_fwd(k, l, h, B, 0, src_rows, lg, false);
+            gemm_fwd(k, l + 1, h, B, src_rows, B - src_rows, lg, false);
+            after_launch(c, 2);
+        }
+    }
+}
+
+void train_step(mtk_bank& k, const mtk_step& s, double* loss_host, double* mmd_host) {
+    Ctx& c = *k.ctx;
+    const int B = s.B, L = k.L;
+    need(B >= 1, MTK_SHAPE_ERROR, "train_step: B must be >= 1");
+    need(s.X && s.y, MTK_VALUE_ERROR, "train_step: X and y are required");
+    need(std::isfinite(s.lr), MTK_VALUE_ERROR, "train_step: lr must be finite");
+    need(s.frozen_layers >= 0 && s.frozen_layers <= L, MTK_CONFIG_ERROR,
+         "train_step: frozen_layers out of range");
+    const bool two = k.n_heads == 2;
+    const bool use_mmd = s.mmd_lambda > 0.0;
+    if (two || use_mmd)
+        need(s.src_rows > 0 && s.src_rows < B, MTK_SHAPE_ERROR,
+             "train_step: src_rows must split the batch into two non-empty parts");
+    need(!(two && use_mmd), MTK_CONFIG_ERROR, "train_step: MMD with two heads is not supported");
+    need(!use_mmd || L >= 2, MTK_CONFIG_ERROR, "train_step: MMD needs a hidden layer");
+    const int nb = s.mmd_nb > 0 ? s.mmd_nb : 5;
+    need(nb <= 8, MTK_CONFIG_ERROR, "train_step: at most 8 MMD bandwidths");
+    need(s.denom[0] >= 0 && s.denom[1] >= 0 && !std::isnan(s.denom[0]) && !std::isnan(s.denom[1]),
+         MTK_VALUE_ERROR, "cross_entropy: denominator must be positive");
+    k.ensure(B);
+    const int src = (two || use_mmd) ? s.src_rows : B;
+    const double d0 = s.denom[0] > 0 ? s.denom[0] : (double)(two ? src : B);
+    const double d1 = s.denom[1] > 0 ? s.denom[1] : (double)(B - src);
+    const float lr = (float)s.lr;
+
+    const Plane3 X = input_plane(k, s.X, B);
+    run_forward(k, X, B, two ? -1 : 0, src);
+
+    Plane3* cur = &k.dZ[0];
+    Plane3* nxt = &k.dZ[1];
+    CeArgs ce{k.G,      B,          k.dims[L], two ? src : B, k.logits, s.y, s.w,
+              (float)(1.0 / d0), (float)(1.0 / (two ? d1 : d0)), cur->f, k.row_loss, k.loss,
+              c.d_flags};
+    {
+        PhaseScope ph(c, kPhCe, 2);
+        launch_ce(ce, c.stream);
+        after_launch(c, 2);
+        if (k.tc[L - 1]) {
+            launch_split(cur->f, cur->hi, cur->lo, (long long)k.G * B * k.dims[L], c.stream);
+            after_launch(c);
+        }
+    }
+
+    if (use_mmd) {
+        MmdArgs a;
+        a.G = k.G;
+        a.m = src;
+        a.n = B - src;
+        a.d = k.dims[L - 1];
+        a.Xs = k.H[L - 1].f;
+        a.xs_gs = (long long)B * a.d;
+        a.Xt = k.H[L - 1].f + (size_t)src * a.d;
+        a.xt_gs = a.xs_gs;
+        a.nb = nb;
+        for (int q = 0; q < 8; ++q)
+            a.mult[q] = s.mmd_nb > 0 ? (float)s.mmd_mult[q] : a.mult[q];
+        a.beta = k.beta;
+        a.gXs = k.gH;
+        a.gs_gs = a.xs_gs;
+        a.gXt = k.gH + (size_t)src * a.d;
+        a.gt_gs = a.xs_gs;
+        a.grad_scale = (float)s.mmd_lambda;
+        a.flags = c.d_flags;
+        const int nblk = mmd_blocks_per_group(a);
+        const size_t pbytes = (size_t)k.G * nblk * 3 * sizeof(double);
+        if (pbytes > k.mmd_part_bytes) {
+            MTK_CUDA(cudaStreamSynchronize(c.stream));
+            cudaFree(k.mmd_part);
+            MTK_CUDA(cudaMalloc(&k.mmd_part, pbytes));
+            k.mmd_part_bytes = pbytes;
+        }
+        a.partial = k.mmd_part;
+        const long long N = a.m + a.n;
+        double* sc = c.scratch((size_t)k.G * ((N + 255) / 256) * (a.d + 1) * sizeof(double));
+        {
+            PhaseScope ph(c, kPhMmdBeta, 2);
+            launch_mmd_beta(a, k.beta, sc, c.stream);
+            after_launch(c, 2);
+        }
+        {
+            PhaseScope ph(c, kPhMmdPairs, 1);
+            launch_mmd_pairs(a, c.stream);
+            after_launch(c, 1);
+        }
+        {
+            PhaseScope ph(c, kPhOther, 1);
+            launch_mmd_finish(a, k.mmd, nullptr, c.stream);
+            after_launch(c, 1);
+        }
+    }
+
+    // backward sweep, layer L-1 down to 0
+    for (int l = L - 1; l >= 0; --l) {
+        const bool trainable = l >= s.frozen_layers;
+        const bool need_dx = l > 0 && l > s.frozen_layers;
+        const Plane3& in = l == 0 ? X : k.H[l];
+        const float* add = (l == L - 1 && use_mmd) ? k.gH : nullptr;
+        // the DX output feeds layer l-1: only write its tf32 planes if that layer is tc
+        Plane3 out = *nxt;
+        if (l > 0 && !k.tc[l - 1]) out.hi = out.lo = nullptr;
+        const bool split = (l == L - 1 && two);
+        if (need_dx) {
+            PhaseScope ph(c, kPhDx, split ? 2 : 1);
+            if (split) {
+                gemm_dx(k, l, *cur, B, 0, src, out, k.H[l].f, nullptr);
+                gemm_dx(k, l + 1, *cur, B, src, B - src, out, k.H[l].f, nullptr);
+                after_launch(c, 2);
+            } else {
+                gemm_dx(k, l, *cur, B, 0, B, out, k.H[l].f, add);
+                after_launch(c);
+            }
+        }
+        if (trainable) {
+            const int fo = k.dims[l + 1];
+            {
+                PhaseScope ph(c, kPhDw, split ? 2 : 1);
+                if (split) {
+                    gemm_dw(k, l, in, *cur, B, 0, src, lr);
+                    gemm_dw(k, l + 1, in, *cur, B, src, B - src, lr);
+                } else {
+                    gemm_dw(k, l, in, *cur, B, 0, B, lr);
+                }
+                after_launch(c, split ? 2 : 1);
+            }
+            PhaseScope ph(c, kPhBias, split ? 2 : 1);
+            if (split) {
+                launch_bias_sgd(k.G, src, fo, cur->f, (long long)B * fo, k.b[l], fo, lr,
+                                k.keep_grads ? k.gb[l] : nullptr, c.d_flags, c.stream);
+                launch_bias_sgd(k.G, B - src, fo, cur->f + (size_t)src * fo, (long long)B * fo,
+                                k.b[l + 1], fo, lr, k.keep_grads ? k.gb[l + 1] : nullptr,
+                                c.d_flags, c.stream);
+            } else {
+                launch_bias_sgd(k.G, B, fo, cur->f, (long long)B * fo, k.b[l], fo, lr,
+                                k.keep_grads ? k.gb[l] : nullptr, c.d_flags, c.stream);
+            }
+            after_launch(c, split ? 2 : 1);
+        }
+        std::swap(cur, nxt);
+    }
+
+    if (loss_host || mmd_host) {
+        double* h = static_cast<double*>(c.pinned_buf(2 * k.G * sizeof(double) + 64));
+        if (loss_host)
+            MTK_CUDA(cudaMemcpyAsync(h, k.loss, k.G * sizeof(double), cudaMemcpyDeviceToHost,
+                                     c.stream));
+        if (mmd_host && use_mmd)
+            MTK_CUDA(cudaMemcpyAsync(h + k.G, k.mmd, k.G * sizeof(double),
+                                     cudaMemcpyDeviceToHost, c.stream));
+        c.check_flags();
+        if (loss_host) std::memcpy(loss_host, h, k.G * sizeof(double));
+        if (mmd_host) {
+            if (use_mmd)
+                std::memcpy(mmd_host, h + k.G, k.G * sizeof(double));
+            else
+                for (int g = 0; g < k.G; ++g) mmd_host[g] = 0.0;
+        }
+    }
+}
+
+void check_bank(mtk_bank* k) { need(k != nullptr, MTK_VALUE_ERROR, "null bank"); }
+void check_model(mtk_bank* k, int model) {
+    check_bank(k);
+    need(model >= 0 && model < k->G, MTK_VALUE_ERROR, "model index out of range");
+}
+
+bool tc_eligible(int fi, int fo) { return fi >= 32 && fo >= 32 && fi % 4 == 0 && fo % 4 == 0; }
+
+}  // namespace
+
+extern "C" {
+
+int mtk_bank_create(mtk_ctx* c, int G, int n_layers, const int* dims, int n_heads,
+                    mtk_bank** out) {
+    return guard([&] {
+        need(c && dims && out, MTK_VALUE_ERROR, "mtk_bank_create: null argument");
+        need(G >= 1 && n_layers >= 1, MTK_SHAPE_ERROR, "mtk_bank_create: zero dimension");
+        need(n_heads == 1 || n_heads == 2, MTK_CONFIG_ERROR, "mtk_bank_create: n_heads is 1 or 2");
+        need(n_heads == 1 || n_layers >= 2, MTK_CONFIG_ERROR,
+             "mtk_bank_create: two heads need a shared trunk");
+        for (int i = 0; i <= n_layers; ++i)
+            need(dims[i] >= 1, MTK_SHAPE_ERROR, "mtk_bank_create: zero dimension in dims");
+        MTK_CUDA(cudaSetDevice(c->device));
+        std::unique_ptr<mtk_bank> k(new mtk_bank());
+        k->ctx = c;
+        k->G = G;
+        k->L = n_layers;
+        k->n_heads = n_heads;
+        k->dims.assign(dims, dims + n_layers + 1);
+        const char* env = getenv("MTK_DISABLE_TC");
+        const bool allow_tc = !(env && env[0] == '1');
+        for (int l = 0; l < n_layers; ++l)
+            k->tc.push_back(allow_tc && tc_eligible(dims[l], dims[l + 1]));
+        k->n_mats = n_layers + n_heads - 1;
+        for (int i = 0; i < k->n_mats; ++i) {
+            const size_t nw = (size_t)G * k->fan_in(i) * k->fan_out(i);
+            Plane3 w;
+            alloc3(w, nw, true, k->tc[k->layer_of(i)]);
+            MTK_CUDA(cudaMemsetAsync(w.f, 0, nw * 4, c->stream));
+            if (w.hi) {
+                MTK_CUDA(cudaMemsetAsync(w.hi, 0, nw * 4, c->stream));
+                MTK_CUDA(cudaMemsetAsync(w.lo, 0, nw * 4, c->stream));
+            }
+            float* bb = nullptr;
+            MTK_CUDA(cudaMalloc(&bb, (size_t)G * k->fan_out(i) * sizeof(float)));
+            MTK_CUDA(cudaMemsetAsync(bb, 0, (size_t)G * k->fan_out(i) * 4, c->stream));
+            k->W.push_back(w);
+            k->b.push_back(bb);
+        }
+        MTK_CUDA(cudaMalloc(&k->loss, G * sizeof(double)));
+        MTK_CUDA(cudaMalloc(&k->mmd, G * sizeof(double)));
+        MTK_CUDA(cudaMalloc(&k->beta, G * sizeof(double)));
+        MTK_CUDA(cudaStreamSynchronize(c->stream));
+        *out = k.release();
+    });
+}
+
+int mtk_bank_destroy(mtk_bank* k) {
+    return guard([&] {
+        if (!k) return;
+        cudaStreamSynchronize(k->ctx->stream);
+        delete k;
+    });
+}
+
+int mtk_bank_set_params(mtk_bank* k, int model, const double* const* W, const double* const* b) {
+    return guard([&] {
+        check_model(k, model);
+        need(W && b, MTK_VALUE_ERROR, "set_params: null arrays");
+        std::vector<float> tmp;
+        for (int i = 0; i < k->n_mats; ++i) {
+            const size_t nw = (size_t)k->fan_in(i) * k->fan_out(i), nbias = k->fan_out(i);
+            need(W[i] && b[i], MTK_VALUE_ERROR, "set_params: null matrix");
+            tmp.assign(W[i], W[i] + nw);
+            MTK_CUDA(cudaMemcpyAsync(k->W[i].f + model * nw, tmp.data(), nw * 4,
+                                     cudaMemcpyHostToDevice, k->ctx->stream));
+            MTK_CUDA(cudaStreamSynchronize(k->ctx->stream));
+            tmp.assign(b[i], b[i] + nbias);
+            MTK_CUDA(cudaMemcpyAsync(k->b[i] + model * nbias, tmp.data(), nbias * 4,
+                                     cudaMemcpyHostToDevice, k->ctx->stream));
+            MTK_CUDA(cudaStreamSynchronize(k->ctx->stream));
+            k->split_param(i);
+        }
+        MTK_CUDA(cudaStreamSynchronize(k->ctx->stream));
+    });
+}
+
+int mtk_bank_get_params(mtk_bank* k, int model, double* const* W, double* const* b) {
+    return guard([&] {
+        check_model(k, model);
+        MTK_CUDA(cudaStreamSynchronize(k->ctx->stream));
+        std::vector<float> tmp;
+        for (int i = 0; i < k->n_mats; ++i) {
+            const size_t nw = (size_t)k->fan_in(i) * k->fan_out(i), nbias = k->fan_out(i);
+            if (W && W[i]) {
+                tmp.resize(nw);
+                MTK_CUDA(cudaMemcpy(tmp.data(), k->W[i].f + model * nw, nw * 4,
+                                    cudaMemcpyDeviceToHost));
+                for (size_t j = 0; j < nw; ++j) W[i][j] = tmp[j];
+            }
+            if (b && b[i]) {
+                tmp.resize(nbias);
+                MTK_CUDA(cudaMemcpy(tmp.data(), k->b[i] + model * nbias, nbias * 4,
+                                    cudaMemcpyDeviceToHost));
+                for (size_t j = 0; j < nbias; ++j) b[i][j] = tmp[j];
+            }
+        }
+    });
+}
+
+int mtk_bank_init_params(mtk_bank* k, int model, mtk_rng* r) {
+    return guard([&] {
+        check_model(k, model);
+        need(r != nullptr, MTK_VALUE_ERROR, "init_params: null rng");
+        std::vector<std::vector<double>> W(k->n_mats), b(k->n_mats);
+        std::vector<const double*> pw, pb;
+        for (int i = 0; i < k->n_mats; ++i) {
+            const double lim = 1.0 / std::sqrt((double)k->fan_in(i));
+            W[i].resize((size_t)k->fan_in(i) * k->fan_out(i));
+            for (double& v : W[i]) v = mtk_rng_uniform(r, -lim, lim);
+            b[i].assign(k->fan_out(i), 0.0);
+            pw.push_back(W[i].data());
+            pb.push_back(b[i].data());
+        }
+        const int st = mtk_bank_set_params(k, model, pw.data(), pb.data());
+        if (st) fail(st, last_error());
+    });
+}
+
+int mtk_bank_param_device(mtk_bank* k, int mat, float** W, float** b) {
+    return guard([&] {
+        check_bank(k);
+        need(mat >= 0 && mat < k->n_mats, MTK_VALUE_ERROR, "param_device: bad matrix index");
+        if (W) *W = k->W[mat].f;
+        if (b) *b = k->b[mat];
+    });
+}
+
+int mtk_bank_forward(mtk_bank* k, const float* X, int B, int head, float* logits,
+                     float* hidden_last) {
+    return guard([&] {
+        check_bank(k);
+        need(X && logits, MTK_VALUE_ERROR, "forward: null argument");
+        need(B >= 1, MTK_SHAPE_ERROR, "forward: B must be >= 1");
+        need(head >= 0 && head < k->n_heads, MTK_VALUE_ERROR, "forward: bad head index");
+        k->ensure(B);
+        Ctx& c = *k->ctx;
+        const Plane3 in = input_plane(*k, X, B);
+        run_forward(*k, in, B, head, 0);
+        const size_t GB = (size_t)k->G * B;
+        MTK_CUDA(cudaMemcpyAsync(logits, k->logits, GB * k->dims[k->L] * 4,
+                                 cudaMemcpyDeviceToDevice, c.stream));
+        if (hidden_last && k->L > 1)
+            MTK_CUDA(cudaMemcpyAsync(hidden_last, k->H[k->L - 1].f, GB * k->dims[k->L - 1] * 4,
+                                     cudaMemcpyDeviceToDevice, c.stream));
+    });
+}
+
+int mtk_bank_train_step(mtk_bank* k, const mtk_step* s, double* loss_host, double* mmd_host) {
+    return guard([&] {
+        check_bank(k);
+        need(s != nullptr, MTK_VALUE_ERROR, "train_step: null step");
+        train_step(*k, *s, loss_host, mmd_host);
+    });
+}
+
+int mtk_bank_train_step_host(mtk_bank* k, const mtk_step* s, const float* X_host,
+                             const int32_t* y_host, const float* w_host, double* loss_host,
+                             double* mmd_host) {
+    return guard([&] {
+        check_bank(k);
+        need(s && X_host && y_host, MTK_VALUE_ERROR, "train_step_host: null argument");
+        need(s->B >= 1, MTK_SHAPE_ERROR, "train_step_host: B must be >= 1");
+        k->ensure_stage(s->B);
+        Ctx& c = *k->ctx;
+        const size_t GB = (size_t)k->G * s->B;
+        MTK_CUDA(cudaMemcpyAsync(k->Xs, X_host, GB * k->dims[0] * 4, cudaMemcpyHostToDevice,
+                                 c.stream));
+        MTK_CUDA(cudaMemcpyAsync(k->ys, y_host, GB * 4, cudaMemcpyHostToDevice, c.stream));
+        if (w_host)
+            MTK_CUDA(cudaMemcpyAsync(k->ws, w_host, GB * 4, cudaMemcpyHostToDevice, c.stream));
+        mtk_step d = *s;
+        d.X = k->Xs;
+        d.y = k->ys;
+        d.w = w_host ? k->ws : nullptr;
+        train_step(*k, d, loss_host, mmd_host);
+    });
+}
+
+int mtk_bank_set_keep_grads(mtk_bank* k, int on) {
+    return guard([&] {
+        check_bank(k);
+        k->keep_grads = on != 0;
+        if (k->keep_grads && k->gW.empty()) {
+            for (int i = 0; i < k->n_mats; ++i) {
+                float *w = nullptr, *bb = nullptr;
+                MTK_CUDA(cudaMalloc(&w, (size_t)k->G * k->fan_in(i) * k->fan_out(i) * 4));
+                MTK_CUDA(cudaMalloc(&bb, (size_t)k->G * k->fan_out(i) * 4));
+                MTK_CUDA(cudaMemset(w, 0, (size_t)k->G * k->fan_in(i) * k->fan_out(i) * 4));
+                MTK_CUDA(cudaMemset(bb, 0, (size_t)k->G * k->fan_out(i) * 4));
+                k->gW.push_back(w);
+                k->gb.push_back(bb);
+            }
+        }
+    });
+}
+
+int mtk_bank_get_grads(mtk_bank* k, int model, double* const* dW, double* const* db) {
+    return guard([&] {
+        check_model(k, model);
+        need(!k->gW.empty(), MTK_CONFIG_ERROR, "get_grads: call mtk_bank_set_keep_grads first");
+        MTK_CUDA(cudaStreamSynchronize(k->ctx->stream));
+        std::vector<float> tmp;
+        for (int i = 0; i < k->n_mats; ++i) {
+            const size_t nw = (size_t)k->fan_in(i) * k->fan_out(i), nbias = k->fan_out(i);
+            if (dW && dW[i]) {
+                tmp.resize(nw);
+                MTK_CUDA(cudaMemcpy(tmp.data(), k->gW[i] + model * nw, nw * 4,
+                                    cudaMemcpyDeviceToHost));
+                for (size_t j = 0; j < nw; ++j) dW[i][j] = tmp[j];
+            }
+            if (db && db[i]) {
+                tmp.resize(nbias);
+                MTK_CUDA(cudaMemcpy(tmp.data(), k->gb[i] + model * nbias, nbias * 4,
+                                    cudaMemcpyDeviceToHost));
+                for (size_t j = 0; j < nbias; ++j) db[i][j] = tmp[j];
+            }
+        }
+    });
+}
+
+int mtk_bank_tc_layers(mtk_bank* k, int* out_host) {
+    return guard([&] {
+        check_bank(k);
+        need(out_host != nullptr, MTK_VALUE_ERROR, "tc_layers: null out");
+        for (int l = 0; l < k->L; ++l) out_host[l] = k->tc[l] ? 1 : 0;
+    });
+}
+
+}  // extern "C"

@@ -93,6 +93,8 @@ struct Gemm {
     const float* mask = nullptr;  // kMask: mask source, same layout as C
     float lr = 0.f;               // kSgd
     float* grad_out = nullptr;    // kSgd: optional copy of acc, same layout as C
+    float* C_hi = nullptr;        // optional tf32 split planes of the result
+    float* C_lo = nullptr;
     int* flags = nullptr;
 };
 
@@ -183,6 +185,35 @@ void launch_column(const float* logits, long long rows, int C, int col, float* o
                    cudaStream_t s);
 void auc_device(Ctx& ctx, const float* scores, const uint8_t* labels, long long n, double* auc,
                 double* acc);
+
+std::string& last_error();
+
+inline void after_launch(Ctx& c, int n = 1) {
+    c.launches += n;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) fail(MTK_ERROR, std::string("kernel launch: ") + cudaGetErrorString(e));
+}
+
+template <class F>
+inline int guard(F&& f) {
+    try {
+        f();
+        return MTK_OK;
+    } catch (const Failure& e) {
+        last_error() = e.what();
+        return e.status;
+    } catch (const std::bad_alloc&) {
+        last_error() = "host allocation failed";
+        return MTK_ERROR;
+    } catch (const std::exception& e) {
+        last_error() = e.what();
+        return MTK_ERROR;
+    }
+}
+
+inline void need(bool ok, int status, const char* msg) {
+    if (!ok) fail(status, msg);
+}
 
 }  // namespace mtk
 

@@ -11,6 +11,7 @@
 #include <cmath>
 
 #include "internal.h"
+#include "sm100.cuh"
 
 namespace mtk {
 namespace {
@@ -99,26 +100,31 @@ __global__ void __launch_bounds__(NT) gemm_simt_kernel(Gemm p) {
             switch (p.epi) {
                 case Epi::kBias:
                     v += p.bias[g * p.bias_gs + n];
-                    p.C[idx] = v;
                     bad |= !isfinite(v);
                     break;
                 case Epi::kBiasRelu:
                     v += p.bias[g * p.bias_gs + n];
                     bad |= !isfinite(v);
-                    p.C[idx] = v > 0.f ? v : 0.f;
+                    v = v > 0.f ? v : 0.f;
                     break;
-                case Epi::kMask: {
+                case Epi::kMask:
                     if (p.add) v = p.add[idx] + v;
-                    p.C[idx] = (p.mask[idx] > 0.f) ? v : 0.f;
+                    v = (p.mask[idx] > 0.f) ? v : 0.f;
                     break;
-                }
-                case Epi::kSgd: {
+                case Epi::kSgd:
                     if (p.grad_out) p.grad_out[idx] = v;
-                    const float w = p.C[idx] - p.lr * v;
-                    bad |= !isfinite(w);
-                    p.C[idx] = w;
+                    v = p.C[idx] - p.lr * v;
+                    bad |= !isfinite(v);
                     break;
-                }
+                case Epi::kStore:
+                    break;
+            }
+            p.C[idx] = v;
+            if (p.C_hi) {
+                float hi, lo;
+                sm100::split_tf32(v, hi, lo);
+                p.C_hi[idx] = hi;
+                p.C_lo[idx] = lo;
             }
         }
     }
@@ -172,19 +178,31 @@ __global__ void row_sum_kernel(const double* row_loss, int B, double* loss, int*
     }
 }
 
-// db = column sums of dZ (fixed row order), b -= lr * db.
+// db = column sums of dZ, b -= lr * db.  Block = 32 columns x 8 row groups;
+// each thread sums a strided row subset, then the 8 partials are combined in a
+// fixed order (deterministic, no atomics).
 __global__ void bias_sgd_kernel(int G, int rows, int N, const float* dZ, long long dz_gs, float* b,
                                 long long b_gs, float lr, float* grad_out, int* flags) {
-    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (t >= (long long)G * N) return;
-    const int g = (int)(t / N), n = (int)(t % N);
-    const float* col = dZ + g * dz_gs + n;
+    __shared__ float part[8][33];
+    const int g = blockIdx.y;
+    const int n = blockIdx.x * 32 + (threadIdx.x & 31);
+    const int rg = threadIdx.x >> 5;
     float s = 0.f;
-    for (int r = 0; r < rows; ++r) s += col[(long long)r * N];
-    if (grad_out) grad_out[g * b_gs + n] = s;
-    const float v = b[g * b_gs + n] - lr * s;
-    if (!isfinite(v)) atomicOr(flags, kFlagNonFinite);
-    b[g * b_gs + n] = v;
+    if (n < N) {
+        const float* col = dZ + g * dz_gs + n;
+        for (int r = rg; r < rows; r += 8) s += col[(long long)r * N];
+    }
+    part[rg][threadIdx.x & 31] = s;
+    __syncthreads();
+    if (rg == 0 && n < N) {
+        float t = 0.f;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) t += part[q][threadIdx.x];
+        if (grad_out) grad_out[g * b_gs + n] = t;
+        const float v = b[g * b_gs + n] - lr * t;
+        if (!isfinite(v)) atomicOr(flags, kFlagNonFinite);
+        b[g * b_gs + n] = v;
+    }
 }
 
 }  // namespace
@@ -203,9 +221,8 @@ void launch_ce(const CeArgs& a, cudaStream_t s) {
 
 void launch_bias_sgd(int G, int rows, int N, const float* dZ, long long dz_gs, float* b,
                      long long b_gs, float lr, float* grad_out, int* flags, cudaStream_t s) {
-    const long long t = (long long)G * N;
-    bias_sgd_kernel<<<(unsigned)((t + 127) / 128), 128, 0, s>>>(G, rows, N, dZ, dz_gs, b, b_gs, lr,
-                                                               grad_out, flags);
+    dim3 grid((N + 31) / 32, G);
+    bias_sgd_kernel<<<grid, 256, 0, s>>>(G, rows, N, dZ, dz_gs, b, b_gs, lr, grad_out, flags);
 }
 
 }  // namespace mtk
