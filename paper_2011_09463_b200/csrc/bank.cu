@@ -74,6 +74,9 @@ struct mtk_bank {
     float* gH = nullptr;
     double* mmd_part = nullptr;
     size_t mmd_part_bytes = 0;
+    void* mmd_z = nullptr;     // tf32 planes + norms of the MMD sample (tc path)
+    size_t mmd_z_bytes = 0;
+    bool tc_mmd = true;
     float* Xs = nullptr;
     int32_t* ys = nullptr;
     float* ws = nullptr;
@@ -103,6 +106,7 @@ struct mtk_bank {
         cudaFree(mmd);
         cudaFree(beta);
         cudaFree(mmd_part);
+        cudaFree(mmd_z);
         cudaFree(Xs);
         cudaFree(ys);
         cudaFree(ws);
@@ -427,6 +431,7 @@ void train_step(mtk_bank& k, const mtk_step& s, double* loss_host, double* mmd_h
         a.gt_gs = a.xs_gs;
         a.grad_scale = (float)s.mmd_lambda;
         a.flags = c.d_flags;
+        a.tc = k.tc_mmd && mmd_tc_supported(a);
         const int nblk = mmd_blocks_per_group(a);
         const size_t pbytes = (size_t)k.G * nblk * 3 * sizeof(double);
         if (pbytes > k.mmd_part_bytes) {
@@ -444,9 +449,20 @@ void train_step(mtk_bank& k, const mtk_step& s, double* loss_host, double* mmd_h
             after_launch(c, 2);
         }
         {
-            PhaseScope ph(c, kPhMmdPairs, 1);
-            launch_mmd_pairs(a, c.stream);
-            after_launch(c, 1);
+            PhaseScope ph(c, kPhMmdPairs, a.tc ? 2 : 1);
+            if (a.tc) {
+                const size_t zb = mmd_tc_scratch_bytes(a);
+                if (zb > k.mmd_z_bytes) {
+                    MTK_CUDA(cudaStreamSynchronize(c.stream));
+                    cudaFree(k.mmd_z);
+                    MTK_CUDA(cudaMalloc(&k.mmd_z, zb));
+                    k.mmd_z_bytes = zb;
+                }
+                launch_mmd_tc(a, k.mmd_z, c.stream);
+            } else {
+                launch_mmd_pairs(a, c.stream);
+            }
+            after_launch(c, a.tc ? 2 : 1);
         }
         {
             PhaseScope ph(c, kPhOther, 1);
@@ -556,6 +572,7 @@ int mtk_bank_create(mtk_ctx* c, int G, int n_layers, const int* dims, int n_head
         const bool allow_tc = !(env && env[0] == '1');
         for (int l = 0; l < n_layers; ++l)
             k->tc.push_back(allow_tc && tc_eligible(dims[l], dims[l + 1]));
+        k->tc_mmd = allow_tc;
         k->n_mats = n_layers + n_heads - 1;
         for (int i = 0; i < k->n_mats; ++i) {
             const size_t nw = (size_t)G * k->fan_in(i) * k->fan_out(i);

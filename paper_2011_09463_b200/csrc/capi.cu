@@ -193,6 +193,8 @@ static MmdArgs mmd_args(mtk_ctx* c, const float* Xs, int64_t m, const float* Xt,
         }
     }
     a.flags = c->d_flags;
+    const char* env = getenv("MTK_DISABLE_TC");
+    a.tc = !(env && env[0] == '1') && mmd_tc_supported(a);
     return a;
 }
 
@@ -234,7 +236,15 @@ static void mmd_run(mtk_ctx* c, MmdArgs& a, double beta, bool want_value, double
     }
     a.beta = beta_d;
     a.partial = part_d;
-    launch_mmd_pairs(a, c->stream);
+    if (a.tc) {
+        void* zs = nullptr;
+        MTK_CUDA(cudaMallocAsync(&zs, mmd_tc_scratch_bytes(a), c->stream));
+        launch_mmd_tc(a, zs, c->stream);
+        MTK_CUDA(cudaFreeAsync(zs, c->stream));
+        after_launch(*c, 1);
+    } else {
+        launch_mmd_pairs(a, c->stream);
+    }
     launch_mmd_finish(a, want_value ? out_d : nullptr, sums_d, c->stream);
     after_launch(*c, 2);
     double* h = static_cast<double*>(c->pinned_buf(4096));

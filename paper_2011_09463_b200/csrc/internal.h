@@ -170,8 +170,13 @@ struct MmdArgs {
     long long gt_gs = 0;
     float grad_scale = 1.f;
     int* flags = nullptr;
+    bool tc = false;                // run on the tcgen05 path (k_mmd_tc.cu)
 };
-int mmd_blocks_per_group(const MmdArgs& a);
+int mmd_blocks_per_group(const MmdArgs& a);  // partial-sum blocks (depends on a.tc)
+bool mmd_tc_supported(const MmdArgs& a);
+int mmd_tc_blocks_per_group(const MmdArgs& a);
+size_t mmd_tc_scratch_bytes(const MmdArgs& a);
+void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s);
 void launch_mmd_beta(const MmdArgs& a, double* beta_out, double* scratch, cudaStream_t s);
 void launch_mmd_pairs(const MmdArgs& a, cudaStream_t s);
 // value[g] = cSS*ss + cTT*tt + cST*st from the per-block partials (fixed order)

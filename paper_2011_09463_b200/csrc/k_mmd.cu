@@ -247,6 +247,7 @@ __global__ void mmd_finish_kernel(MmdArgs a, int nblk, double* value, double* su
 }  // namespace
 
 int mmd_blocks_per_group(const MmdArgs& a) {
+    if (a.tc) return mmd_tc_blocks_per_group(a);
     const long long N = a.m + a.n;
     const long long re = a.row_end < 0 ? N : a.row_end;
     return (int)((re - a.row_begin + TI - 1) / TI);

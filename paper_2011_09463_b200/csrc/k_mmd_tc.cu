@@ -1,0 +1,443 @@
+// k_mmd_tc.cu -- multi-bandwidth Gaussian MMD^2 + gradient on the tcgen05
+// tensor cores, FlashAttention-style (two chained 3xTF32 GEMMs per tile).
+//
+// Definition (oracle.c:orc_mmd_gaussian):
+//   d2_ij = n_i + n_j - 2 z_i.z_j          (n_i = |z_i|^2)
+//   k_ij  = sum_b exp(-d2_ij / s_b),   A_ij = sum_b (2/s_b) exp(-d2_ij / s_b)
+//   w_ij  = c_ij A_ij  (c = -2/m^2 S-S, -2/n^2 T-T, 2/(m n) cross, 0 on i = j)
+//   g_i   = sum_j w_ij (z_i - z_j) = z_i * Wsum_i - V_i,   V = W . Z
+// Per CTA: 128 rows i (M) x a 256-wide slice of V's feature dims; it streams
+// every 64-row j tile of Z:
+//   GEMM1  S[128x64]  = Z_i . Z_j^T      (TMEM cols [256,320), K = d)
+//   exp    4 epilogue warps: S -> d2 -> k, A, w; fp64 kernel sums and Wsum;
+//          w written to smem as tf32 hi/lo planes (K-major, 128-B swizzle)
+//   GEMM2  V[128xVD] += W[128x64] . Z_j[64xVD]   (TMEM cols [0,VD))
+// Operands are the tf32 hi/lo planes of Z (HBM, [G][N][d]); all products are
+// 3xTF32 (hi*hi + hi*lo + lo*hi).  One warp issues TMA, one issues MMAs.
+#include <cuda.h>
+
+#include <cmath>
+#include <cstring>
+
+#include "internal.h"
+#include "sm100.cuh"
+
+namespace mtk {
+namespace {
+
+using namespace sm100;
+
+constexpr int TI = 128, TJ = 64, KC = 32, JC = 16, VD = 256;
+constexpr int STAGES = 3;
+constexpr int G1_BYTES = 2 * (TI * KC * 4) + 2 * (TJ * KC * 4);  // 48 KB
+constexpr int G2_BYTES = 2 * (JC * VD * 4);                       // 32 KB
+constexpr int STAGE_BYTES = G1_BYTES;
+constexpr int W_PLANE = TI * TJ * 4;                              // 32 KB
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 2 * W_PLANE + 1024 + 256;
+constexpr int NUM_THREADS = 192;
+constexpr uint32_t S_COL = 256;
+
+struct MmdTcParams {
+    CUtensorMap zk_hi, zk_lo;   // K-major view: (d, N, G), box (32, 64)
+    CUtensorMap zm_hi, zm_lo;   // MN-major view: (d, N, G), box (32, 16), 32-B atom swizzle
+    const float* z_hi;          // planes, for z_i in the gradient epilogue
+    const float* z_lo;
+    const float* norms;         // [G][N]
+    const double* beta;         // [G]
+    long long m, n;
+    int d;
+    int nb;
+    float mult[8];
+    long long row_begin, row_end;
+    double* partial;            // [G][nblk][3]
+    int nblk;
+    float* gXs;
+    long long gs_gs;
+    float* gXt;
+    long long gt_gs;
+    float grad_scale;
+    int* flags;
+};
+
+__global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_constant__ MmdTcParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* wbuf = smem + STAGES * STAGE_BYTES;  // W hi plane, then lo plane
+    uint64_t* full = reinterpret_cast<uint64_t*>(wbuf + 2 * W_PLANE);
+    uint64_t* empty = full + STAGES;
+    uint64_t* s_full = empty + STAGES;
+    uint64_t* w_full = s_full + 1;
+    uint64_t* v_full = w_full + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(v_full + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = blockIdx.z;
+    const int dslice = blockIdx.y;
+    const int v0 = dslice * VD;
+    const int vd = min(VD, p.d - v0);  // feature columns of V owned here
+    const long long N = p.m + p.n;
+    const long long rb = p.row_begin, re = p.row_end;
+    const long long i0 = rb + (long long)blockIdx.x * TI;
+    const int nkc = (p.d + KC - 1) / KC;
+    const int njt = (int)((N + TJ - 1) / TJ);
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&p.zk_hi);
+        tma_prefetch(&p.zk_lo);
+        tma_prefetch(&p.zm_hi);
+        tma_prefetch(&p.zm_lo);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(s_full, 1);
+        mbar_init(w_full, 128);
+        mbar_init(v_full, 1);
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------- TMA producer ----------------
+            int st = 0;
+            for (int jt = 0; jt < njt; ++jt) {
+                const int j0 = jt * TJ;
+                for (int kc = 0; kc < nkc; ++kc, ++st) {
+                    const int s = st % STAGES;
+                    mbar_wait(&empty[s], ((st / STAGES) & 1) ^ 1);
+                    uint8_t* b = smem + s * STAGE_BYTES;
+                    mbar_expect_tx(&full[s], G1_BYTES);
+                    const int k0 = kc * KC;
+                    // Z_i (128 rows as two 64-row boxes), hi then lo; then Z_j (64 rows)
+                    tma_load_3d(b, &p.zk_hi, &full[s], k0, (int)i0, g);
+                    tma_load_3d(b + 8192, &p.zk_hi, &full[s], k0, (int)i0 + 64, g);
+                    tma_load_3d(b + 16384, &p.zk_lo, &full[s], k0, (int)i0, g);
+                    tma_load_3d(b + 24576, &p.zk_lo, &full[s], k0, (int)i0 + 64, g);
+                    tma_load_3d(b + 32768, &p.zk_hi, &full[s], k0, j0, g);
+                    tma_load_3d(b + 40960, &p.zk_lo, &full[s], k0, j0, g);
+                }
+                for (int jc = 0; jc < TJ / JC; ++jc, ++st) {
+                    const int s = st % STAGES;
+                    mbar_wait(&empty[s], ((st / STAGES) & 1) ^ 1);
+                    uint8_t* b = smem + s * STAGE_BYTES;
+                    mbar_expect_tx(&full[s], G2_BYTES);
+                    // Z_j rows [j0+16jc, +16) x dims [v0, v0+VD): VD/32 boxes per plane
+                    for (int q = 0; q < VD / 32; ++q) {
+                        tma_load_3d(b + q * 2048, &p.zm_hi, &full[s], v0 + 32 * q, j0 + JC * jc, g);
+                        tma_load_3d(b + 16384 + q * 2048, &p.zm_lo, &full[s], v0 + 32 * q,
+                                    j0 + JC * jc, g);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer ----------------
+        if (lane == 0) {
+            constexpr uint32_t id1 = idesc_tf32(TI, TJ, 0, 0);
+            constexpr uint32_t id2 = idesc_tf32(TI, VD, 0, 1);
+            const uint32_t tS = tmem + S_COL, tV = tmem;
+            const uint32_t wb = smem_u32(wbuf);
+            int st = 0;
+            for (int jt = 0; jt < njt; ++jt) {
+                for (int kc = 0; kc < nkc; ++kc, ++st) {
+                    const int s = st % STAGES;
+                    mbar_wait(&full[s], (st / STAGES) & 1);
+                    tc_fence_after();
+                    const uint32_t b = smem_u32(smem + s * STAGE_BYTES);
+#pragma unroll
+                    for (int kk = 0; kk < KC / 8; ++kk) {
+                        const uint64_t ahi = smem_desc(b + kk * 32, 16, 1024, 2);
+                        const uint64_t alo = smem_desc(b + 16384 + kk * 32, 16, 1024, 2);
+                        const uint64_t bhi = smem_desc(b + 32768 + kk * 32, 16, 1024, 2);
+                        const uint64_t blo = smem_desc(b + 40960 + kk * 32, 16, 1024, 2);
+                        mma_tf32(tS, alo, bhi, id1, (kc | kk) ? 1u : 0u);
+                        mma_tf32(tS, ahi, blo, id1, 1u);
+                        mma_tf32(tS, ahi, bhi, id1, 1u);
+                    }
+                    mma_commit(&empty[s]);
+                }
+                mma_commit(s_full);
+                mbar_wait(w_full, jt & 1);
+                tc_fence_after();
+                for (int jc = 0; jc < TJ / JC; ++jc, ++st) {
+                    const int s = st % STAGES;
+                    mbar_wait(&full[s], (st / STAGES) & 1);
+                    tc_fence_after();
+                    const uint32_t b = smem_u32(smem + s * STAGE_BYTES);
+#pragma unroll
+                    for (int h = 0; h < JC / 8; ++h) {
+                        const int kk = jc * (JC / 8) + h;  // 8-wide k step over the 64 j of W
+                        const uint32_t woff = (kk >> 2) * 16384 + (kk & 3) * 32;
+                        const uint64_t ahi = smem_desc(wb + woff, 16, 1024, 2);
+                        const uint64_t alo = smem_desc(wb + W_PLANE + woff, 16, 1024, 2);
+                        const uint64_t bhi = smem_desc(b + h * 1024, 2048, 512, 1);
+                        const uint64_t blo = smem_desc(b + 16384 + h * 1024, 2048, 512, 1);
+                        const uint32_t acc0 = (jt | jc | h) ? 1u : 0u;
+                        mma_tf32(tV, alo, bhi, id2, acc0);
+                        mma_tf32(tV, ahi, blo, id2, 1u);
+                        mma_tf32(tV, ahi, bhi, id2, 1u);
+                    }
+                    mma_commit(&empty[s]);
+                }
+            }
+            mma_commit(v_full);
+        }
+    } else {
+        // ---------------- epilogue warps: exp + weights, then the gradient ----------------
+        const int q = warp & 3;
+        const int r = 32 * q + lane;  // row within the tile == TMEM lane
+        const long long gi = i0 + r;
+        const bool row_ok = gi < re;
+        const bool si = gi < p.m;
+        const double beta = p.beta[g];
+        float nscale[8];  // -log2(e) / s_b
+        float two_inv[8];
+        for (int b = 0; b < 8; ++b) {
+            const double s = beta * (double)p.mult[b];
+            nscale[b] = b < p.nb ? (float)(-1.4426950408889634 / s) : 0.f;
+            two_inv[b] = b < p.nb ? (float)(2.0 / s) : 0.f;
+        }
+        const float cSS = (float)(-2.0 / ((double)p.m * (double)p.m));
+        const float cTT = (float)(-2.0 / ((double)p.n * (double)p.n));
+        const float cST = (float)(2.0 / ((double)p.m * (double)p.n));
+        const float* nrm = p.norms + (long long)g * N;
+        const float ni = row_ok ? nrm[gi] : 0.f;
+        double ksum[3] = {0.0, 0.0, 0.0};
+        double wsum = 0.0;
+        uint8_t* whi = wbuf;
+        uint8_t* wlo = wbuf + W_PLANE;
+        for (int jt = 0; jt < njt; ++jt) {
+            const long long j0 = (long long)jt * TJ;
+            mbar_wait(s_full, jt & 1);
+            tc_fence_after();
+#pragma unroll 1
+            for (int half = 0; half < 2; ++half) {
+                float sv[32];
+                tmem_ld_32x32(tmem + ((uint32_t)(32 * q) << 16) + S_COL + half * 32, sv);
+                float wrow[32];
+                float part = 0.f;
+                float kss = 0.f, ktt = 0.f, kst = 0.f;
+#pragma unroll
+                for (int c = 0; c < 32; ++c) {
+                    const long long gj = j0 + half * 32 + c;
+                    float wv = 0.f;
+                    if (row_ok && gj < N) {
+                        const float d2 = fmaxf(ni + nrm[gj] - 2.f * sv[c], 0.f);
+                        float kv = 0.f, A = 0.f;
+#pragma unroll
+                        for (int b = 0; b < 8; ++b) {
+                            if (b < p.nb) {
+                                const float e = exp2f(d2 * nscale[b]);
+                                kv += e;
+                                A = fmaf(two_inv[b], e, A);
+                            }
+                        }
+                        const bool sj = gj < p.m;
+                        if (si && sj) {
+                            kss += kv;
+                            wv = cSS * A;
+                        } else if (!si && !sj) {
+                            ktt += kv;
+                            wv = cTT * A;
+                        } else {
+                            if (si) kst += kv;
+                            wv = cST * A;
+                        }
+                        if (gj == gi) wv = 0.f;
+                    }
+                    wrow[c] = wv;
+                    part += wv;
+                }
+                ksum[0] += kss;
+                ksum[1] += ktt;
+                ksum[2] += kst;
+                wsum += part;
+                // store w (hi/lo) into the K-major SW128 W planes: atom `half`
+                uint8_t* rowh = whi + half * 16384 + r * 128;
+                uint8_t* rowl = wlo + half * 16384 + r * 128;
+#pragma unroll
+                for (int ch = 0; ch < 8; ++ch) {
+                    float4 h4, l4;
+                    split_tf32(wrow[4 * ch + 0], h4.x, l4.x);
+                    split_tf32(wrow[4 * ch + 1], h4.y, l4.y);
+                    split_tf32(wrow[4 * ch + 2], h4.z, l4.z);
+                    split_tf32(wrow[4 * ch + 3], h4.w, l4.w);
+                    const int pc = (ch ^ (r & 7)) * 16;
+                    *reinterpret_cast<float4*>(rowh + pc) = h4;
+                    *reinterpret_cast<float4*>(rowl + pc) = l4;
+                }
+            }
+            fence_proxy_async_smem();
+            tc_fence_before();
+            mbar_arrive(w_full);
+        }
+        // gradient rows: g_i = scale * (z_i * Wsum_i - V_i) over this CTA's feature slice
+        mbar_wait(v_full, 0);
+        tc_fence_after();
+        float* out = nullptr;
+        if (row_ok)
+            out = si ? (p.gXs ? p.gXs + g * p.gs_gs + gi * p.d : nullptr)
+                     : (p.gXt ? p.gXt + g * p.gt_gs + (gi - p.m) * p.d : nullptr);
+        const float* zh = p.z_hi + ((long long)g * N + (row_ok ? gi : 0)) * p.d;
+        const float* zl = p.z_lo + ((long long)g * N + (row_ok ? gi : 0)) * p.d;
+        bool bad = false;
+#pragma unroll 1
+        for (int cb = 0; cb < VD / 32; ++cb) {
+            float vv[32];
+            tmem_ld_32x32(tmem + ((uint32_t)(32 * q) << 16) + cb * 32, vv);
+            if (!out) continue;
+            for (int c = 0; c < 32; ++c) {
+                const int k = v0 + cb * 32 + c;
+                if (cb * 32 + c >= vd) break;
+                const double z = (double)zh[k] + (double)zl[k];
+                const float gv = (float)(((double)z * wsum - (double)vv[c]) * (double)p.grad_scale);
+                bad |= !isfinite(gv);
+                out[k] = gv;
+            }
+        }
+        if (bad) atomicOr(p.flags, kFlagNonFinite);
+        // fixed-order reduction of the kernel sums over the 128 rows (d-slice 0 only)
+        __shared__ double red[3][128];
+        const int t = threadIdx.x - 64;
+        for (int c = 0; c < 3; ++c) red[c][t] = ksum[c];
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        for (int w = 64; w > 0; w >>= 1) {
+            if (t < w)
+                for (int c = 0; c < 3; ++c) red[c][t] += red[c][t + w];
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+        }
+        if (t < 3 && dslice == 0) p.partial[((long long)g * p.nblk + blockIdx.x) * 3 + t] = red[t][0];
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc<512>(tmem);
+    }
+}
+
+// n_i = |z_i|^2 from the fp32 rows (Xs rows then Xt rows), plus the tf32
+// planes of the concatenated sample Z = [Xs; Xt].
+__global__ void mmd_prep_kernel(const float* Xs, long long xs_gs, const float* Xt, long long xt_gs,
+                                long long m, long long n, int d, float* zhi, float* zlo,
+                                float* norms) {
+    const int g = blockIdx.y;
+    const long long N = m + n;
+    const long long row = blockIdx.x * (long long)(blockDim.x / 32) + (threadIdx.x >> 5);
+    if (row >= N) return;
+    const int lane = threadIdx.x & 31;
+    const float* src = row < m ? Xs + g * xs_gs + row * d : Xt + g * xt_gs + (row - m) * d;
+    float* dh = zhi + ((long long)g * N + row) * d;
+    float* dl = zlo + ((long long)g * N + row) * d;
+    double acc = 0.0;
+    for (int k = lane; k < d; k += 32) {
+        const float x = src[k];
+        float h, l;
+        split_tf32(x, h, l);
+        dh[k] = h;
+        dl[k] = l;
+        acc += (double)x * (double)x;
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) norms[(long long)g * N + row] = (float)acc;
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encoder() {
+    static EncodeFn fn = nullptr;
+    if (!fn) {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(f);
+        if (!fn) fail(MTK_ERROR, "cuTensorMapEncodeTiled unavailable");
+    }
+    return fn;
+}
+
+CUtensorMap zmap(const float* base, long long d, long long N, long long G, int box_outer,
+                 bool mn) {
+    CUtensorMap m;
+    const cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)N, (cuuint64_t)G};
+    const cuuint64_t strides[2] = {(cuuint64_t)(d * 4), (cuuint64_t)(N * d * 4)};
+    const cuuint32_t box[3] = {32, (cuuint32_t)box_outer, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           mn ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(MTK_ERROR, "cuTensorMapEncodeTiled failed (mmd)");
+    return m;
+}
+
+}  // namespace
+
+bool mmd_tc_supported(const MmdArgs& a) { return a.d % 4 == 0 && a.d >= 4; }
+
+int mmd_tc_blocks_per_group(const MmdArgs& a) {
+    const long long N = a.m + a.n;
+    const long long re = a.row_end < 0 ? N : a.row_end;
+    return (int)((re - a.row_begin + TI - 1) / TI);
+}
+
+size_t mmd_tc_scratch_bytes(const MmdArgs& a) {
+    const long long N = a.m + a.n;
+    return (size_t)a.G * N * a.d * 2 * sizeof(float) + (size_t)a.G * N * sizeof(float) + 1024;
+}
+
+// scratch: >= mmd_tc_scratch_bytes(a); a.partial must hold [G][blocks][3]
+void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s) {
+    const long long N = a.m + a.n;
+    const long long re = a.row_end < 0 ? N : a.row_end;
+    float* zhi = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(scratch) + 255) & ~uintptr_t(255));
+    float* zlo = zhi + (size_t)a.G * N * a.d;
+    float* norms = zlo + (size_t)a.G * N * a.d;
+    dim3 pg((unsigned)((N + 7) / 8), a.G);
+    mmd_prep_kernel<<<pg, 256, 0, s>>>(a.Xs, a.xs_gs, a.Xt, a.xt_gs, a.m, a.n, a.d, zhi, zlo, norms);
+    MmdTcParams p;
+    std::memset(&p, 0, sizeof(p));
+    p.zk_hi = zmap(zhi, a.d, N, a.G, 64, false);
+    p.zk_lo = zmap(zlo, a.d, N, a.G, 64, false);
+    p.zm_hi = zmap(zhi, a.d, N, a.G, JC, true);
+    p.zm_lo = zmap(zlo, a.d, N, a.G, JC, true);
+    p.z_hi = zhi;
+    p.z_lo = zlo;
+    p.norms = norms;
+    p.beta = a.beta;
+    p.m = a.m;
+    p.n = a.n;
+    p.d = a.d;
+    p.nb = a.nb;
+    for (int b = 0; b < 8; ++b) p.mult[b] = a.mult[b] > 0 ? a.mult[b] : 1.f;
+    p.row_begin = a.row_begin;
+    p.row_end = re;
+    p.partial = a.partial;
+    p.nblk = mmd_tc_blocks_per_group(a);
+    p.gXs = a.gXs;
+    p.gs_gs = a.gs_gs;
+    p.gXt = a.gXt;
+    p.gt_gs = a.gt_gs;
+    p.grad_scale = a.grad_scale;
+    p.flags = a.flags;
+    static bool attr = false;
+    if (!attr) {
+        MTK_CUDA(cudaFuncSetAttribute(mmd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      SMEM_BYTES));
+        attr = true;
+    }
+    dim3 grid(p.nblk, (a.d + VD - 1) / VD, a.G);
+    mmd_tc_kernel<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(p);
+}
+
+}  // namespace mtk

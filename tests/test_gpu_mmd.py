@@ -82,7 +82,7 @@ def test_mmd_translation_invariance(ctx):
 def test_mmd_errors(ctx):
     from paper_2011_09463_b200 import api, errors
 
-    Xs, Xt = sample(4, 4, 600)
+    Xs, Xt = sample(4, 4, 601)  # tc path needs d % 4 == 0; SIMT path d <= 512
     with pytest.raises(errors.ShapeError):
         api.mmd_gaussian(ctx, torch.tensor(Xs, device="cuda"), torch.tensor(Xt, device="cuda"))
     Xs, Xt = sample(4, 4, 8)
@@ -134,3 +134,22 @@ def test_mmd_c4_stress_properties(ctx):
         c[i] = 0.0
         gi = ((c * A)[:, None] * (Z[i] - Z)).sum(0)
         assert rel(G[i], gi) <= TOL, i
+
+
+@pytest.mark.parametrize("m,n,d", [(300, 200, 256), (1000, 24, 512), (64, 64, 36)])
+def test_mmd_tensor_core_vs_simt(ctx, monkeypatch, m, n, d):
+    """the tcgen05 path (default) and the SIMT path agree, both vs the oracle"""
+    from paper_2011_09463_b200 import api
+
+    Xs, Xt = sample(m, n, d, seed=m)
+    out = []
+    for off in ("0", "1"):
+        monkeypatch.setenv("MTK_DISABLE_TC", off)
+        v, beta, gs, gt = api.mmd_gaussian(ctx, torch.tensor(Xs, device="cuda"),
+                                           torch.tensor(Xt, device="cuda"))
+        out.append((v, np.concatenate([gs.cpu().numpy(), gt.cpu().numpy()])))
+    ov, _, ogs, ogt = po.mmd_gaussian(Xs.astype(np.float64), Xt.astype(np.float64))
+    og = np.concatenate([ogs, ogt])
+    for v, g in out:
+        assert rel(v, ov) <= TOL
+        assert rel(g, og) <= TOL
