@@ -57,7 +57,14 @@ struct MmdTcParams {
     long long gt_gs;
     float grad_scale;
     int* flags;
+    double* vacc;               // [G][N][d] fp64 flush buffer for V, or null (short j loops)
 };
+
+// V is accumulated in fp32 TMEM for FLUSH j tiles at a time, then drained
+// into an fp64 buffer: the MMD gradient is a small difference of large
+// same-domain and cross-domain sums, and fp32 tensor-core accumulation over
+// tens of thousands of j would not hold 1e-5 (C4: m+n = 73728).
+constexpr int FLUSH = 16;
 
 __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_constant__ MmdTcParams p) {
     extern __shared__ uint8_t smem_raw[];
@@ -68,7 +75,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
     uint64_t* s_full = empty + STAGES;
     uint64_t* w_full = s_full + 1;
     uint64_t* v_full = w_full + 1;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(v_full + 1);
+    uint64_t* v_empty = v_full + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(v_empty + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = blockIdx.z;
@@ -80,6 +88,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
     const long long i0 = rb + (long long)blockIdx.x * TI;
     const int nkc = (p.d + KC - 1) / KC;
     const int njt = (int)((N + TJ - 1) / TJ);
+    const bool do_flush = p.vacc != nullptr;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&p.zk_hi);
@@ -93,6 +102,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
         mbar_init(s_full, 1);
         mbar_init(w_full, 128);
         mbar_init(v_full, 1);
+        mbar_init(v_empty, 128);
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -164,6 +174,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
                 mma_commit(s_full);
                 mbar_wait(w_full, jt & 1);
                 tc_fence_after();
+                const bool chunk_start = do_flush ? (jt % FLUSH == 0) : (jt == 0);
+                if (do_flush && jt > 0 && jt % FLUSH == 0) {
+                    mbar_wait(v_empty, ((jt / FLUSH) - 1) & 1);  // previous chunk drained
+                    tc_fence_after();
+                }
                 for (int jc = 0; jc < TJ / JC; ++jc, ++st) {
                     const int s = st % STAGES;
                     mbar_wait(&full[s], (st / STAGES) & 1);
@@ -177,13 +192,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
                         const uint64_t alo = smem_desc(wb + W_PLANE + woff, 16, 1024, 2);
                         const uint64_t bhi = smem_desc(b + h * 1024, 2048, 512, 1);
                         const uint64_t blo = smem_desc(b + 16384 + h * 1024, 2048, 512, 1);
-                        const uint32_t acc0 = (jt | jc | h) ? 1u : 0u;
+                        const uint32_t acc0 = (!chunk_start || jc || h) ? 1u : 0u;
                         mma_tf32(tV, alo, bhi, id2, acc0);
                         mma_tf32(tV, ahi, blo, id2, 1u);
                         mma_tf32(tV, ahi, bhi, id2, 1u);
                     }
                     mma_commit(&empty[s]);
                 }
+                if (do_flush && (jt + 1) % FLUSH == 0 && jt + 1 < njt) mma_commit(v_full);
             }
             mma_commit(v_full);
         }
@@ -209,6 +225,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
         const float ni = row_ok ? nrm[gi] : 0.f;
         double ksum[3] = {0.0, 0.0, 0.0};
         double wsum = 0.0;
+        int nflush = 0;
         uint8_t* whi = wbuf;
         uint8_t* wlo = wbuf + W_PLANE;
         for (int jt = 0; jt < njt; ++jt) {
@@ -275,10 +292,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
             fence_proxy_async_smem();
             tc_fence_before();
             mbar_arrive(w_full);
+            if (do_flush && (jt + 1) % FLUSH == 0 && jt + 1 < njt) {
+                // drain this chunk of V into the fp64 buffer (rows owned by this CTA)
+                mbar_wait(v_full, nflush & 1);
+                tc_fence_after();
+                double* vrow = p.vacc + ((long long)g * N + (row_ok ? gi : 0)) * p.d;
+#pragma unroll 1
+                for (int cb = 0; cb < VD / 32; ++cb) {
+                    float vv[32];
+                    tmem_ld_32x32(tmem + ((uint32_t)(32 * q) << 16) + cb * 32, vv);
+                    if (!row_ok) continue;
+                    for (int c = 0; c < 32 && cb * 32 + c < vd; ++c) {
+                        const int k = v0 + cb * 32 + c;
+                        vrow[k] = (nflush ? vrow[k] : 0.0) + (double)vv[c];
+                    }
+                }
+                tc_fence_before();
+                mbar_arrive(v_empty);
+                ++nflush;
+            }
         }
         // gradient rows: g_i = scale * (z_i * Wsum_i - V_i) over this CTA's feature slice
-        mbar_wait(v_full, 0);
+        mbar_wait(v_full, nflush & 1);
         tc_fence_after();
+        const double* vrow = (nflush && row_ok) ? p.vacc + ((long long)g * N + gi) * p.d : nullptr;
         float* out = nullptr;
         if (row_ok)
             out = si ? (p.gXs ? p.gXs + g * p.gs_gs + gi * p.d : nullptr)
@@ -295,7 +332,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
                 const int k = v0 + cb * 32 + c;
                 if (cb * 32 + c >= vd) break;
                 const double z = (double)zh[k] + (double)zl[k];
-                const float gv = (float)(((double)z * wsum - (double)vv[c]) * (double)p.grad_scale);
+                const double vt = (double)vv[c] + (vrow ? vrow[k] : 0.0);
+                const float gv = (float)((z * wsum - vt) * (double)p.grad_scale);
                 bad |= !isfinite(gv);
                 out[k] = gv;
             }
@@ -391,9 +429,17 @@ int mmd_tc_blocks_per_group(const MmdArgs& a) {
     return (int)((re - a.row_begin + TI - 1) / TI);
 }
 
+static bool needs_flush(const MmdArgs& a) {
+    const long long N = a.m + a.n;
+    const bool grads = a.gXs || a.gXt;
+    return grads && (N + TJ - 1) / TJ > FLUSH;
+}
+
 size_t mmd_tc_scratch_bytes(const MmdArgs& a) {
     const long long N = a.m + a.n;
-    return (size_t)a.G * N * a.d * 2 * sizeof(float) + (size_t)a.G * N * sizeof(float) + 1024;
+    size_t b = (size_t)a.G * N * a.d * 2 * sizeof(float) + (size_t)a.G * N * sizeof(float) + 1024;
+    if (needs_flush(a)) b += (size_t)a.G * N * a.d * sizeof(double) + 256;
+    return b;
 }
 
 // scratch: >= mmd_tc_scratch_bytes(a); a.partial must hold [G][blocks][3]
@@ -403,6 +449,10 @@ void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s) {
     float* zhi = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(scratch) + 255) & ~uintptr_t(255));
     float* zlo = zhi + (size_t)a.G * N * a.d;
     float* norms = zlo + (size_t)a.G * N * a.d;
+    double* vacc = nullptr;
+    if (needs_flush(a))
+        vacc = reinterpret_cast<double*>(
+            (reinterpret_cast<uintptr_t>(norms + (size_t)a.G * N) + 255) & ~uintptr_t(255));
     dim3 pg((unsigned)((N + 7) / 8), a.G);
     mmd_prep_kernel<<<pg, 256, 0, s>>>(a.Xs, a.xs_gs, a.Xt, a.xt_gs, a.m, a.n, a.d, zhi, zlo, norms);
     MmdTcParams p;
@@ -430,6 +480,7 @@ void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s) {
     p.gt_gs = a.gt_gs;
     p.grad_scale = a.grad_scale;
     p.flags = a.flags;
+    p.vacc = vacc;
     static bool attr = false;
     if (!attr) {
         MTK_CUDA(cudaFuncSetAttribute(mmd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -1,0 +1,283 @@
+"""Shadow-training sweep and membership-inference attack (SURVEY.md section 8
+rows a17/a18; Appendix A of SURVEY.md).
+
+The reference has no code for this stage; the definitions pinned here are:
+
+* data: class-conditional Gaussians, y = below(C), x = mu_y + N(0, I) on the
+  host RNG (rng.hpp semantics, bit-exact); the target domain adds a fixed
+  shift delta (D^S, D^T, N^S >> N^T);
+* streams: root = Rng(seed); data = root.split(0); model k (0 = target,
+  1..S = shadows) = root.split(k + 1), derived in ascending k on every rank
+  (rng.hpp:65-69: split advances the parent);
+* per model k: perm = permutation(pool) -> members = perm[:n_mem],
+  non-members = perm[n_mem:2 n_mem]; then parameter init; then
+  one permutation(n_mem) per epoch for the batch order; a
+  short last batch is padded with weight-0 duplicates;
+* paradigms:
+    model     -- pretrain on a source subset, then fine-tune on the members
+                 (optionally with a frozen prefix);
+    mapping   -- co-train on [source batch ; member batch] with CE on both and
+                 lambda * MMD^2(h_src, h_tgt) on the last hidden layer;
+    parameter -- shared trunk, a source head and a target head; each step
+                 feeds [source batch ; member batch] (rows split by head);
+* attack: top-k sorted posteriors of the target-domain head; an MLP
+  k -> 64 -> 2 trained with CE + SGD on the shadows' members (1) and
+  non-members (0); it scores the target's members / non-members -> AUC
+  (mid-rank Mann-Whitney) and accuracy at 0.5.
+
+The product path is ``GpuBackend`` (libmtk through ``api``).  The driver is
+written against a small backend interface so tests can replay it on the CPU
+oracle; nothing here imports the oracle.
+"""
+from __future__ import annotations
+
+import dataclasses
+import json
+from typing import Any
+
+import numpy as np
+
+
+@dataclasses.dataclass
+class SweepConfig:
+    paradigm: str = "model"          # model | mapping | parameter
+    dims: tuple = (784, 256, 10)
+    n_shadows: int = 4
+    pool: int = 8192                 # target-domain population
+    members: int = 2048              # per model; as many non-members
+    source_pool: int = 16384         # source-domain population (N^S >> N^T)
+    source_per_model: int = 4096     # source rows each model sees
+    batch: int = 128
+    epochs: int = 10
+    pretrain_epochs: int = 2         # model-based
+    frozen_layers: int = 0           # model-based fine-tuning
+    lr: float = 0.05
+    mmd_lambda: float = 1.0          # mapping-based
+    mu_scale: float = 0.1
+    shift_scale: float = 0.5
+    k: int = 3
+    attack_hidden: int = 64
+    attack_epochs: int = 30
+    attack_batch: int = 1024
+    attack_lr: float = 0.1
+    seed: int = 20110946
+
+    def validate(self):
+        from .errors import ConfigError
+
+        if self.paradigm not in ("model", "mapping", "parameter"):
+            raise ConfigError(f"unknown paradigm {self.paradigm!r}")
+        if 2 * self.members > self.pool:
+            raise ConfigError("members + non-members exceed the pool")
+        if self.source_per_model > self.source_pool:
+            raise ConfigError("source_per_model exceeds source_pool")
+        if len(self.dims) < 2 or (self.paradigm != "model" and len(self.dims) < 3):
+            raise ConfigError("transfer paradigms need a hidden layer")
+        if not 1 <= self.k <= self.dims[-1]:
+            raise ConfigError("k must be in [1, C]")
+
+
+# --------------------------------------------------------------------------- data
+class Population:
+    """Source and target pools drawn from the data stream (host, bit-exact)."""
+
+    def __init__(self, cfg: SweepConfig, rng_cls):
+        C, d = cfg.dims[-1], cfg.dims[0]
+        self.root = rng_cls(cfg.seed)
+        data = self.root.split(0)
+        self.mu = cfg.mu_scale * data.normals(C * d).reshape(C, d)
+        self.shift = cfg.shift_scale * data.normals(d)
+        self.Xt, self.yt = synth(data, C, d, cfg.pool, self.mu, self.shift)
+        self.Xs, self.ys = synth(data, C, d, cfg.source_pool, self.mu, None)
+
+    def model_streams(self, n_models: int):
+        # ascending k on one root: stream k+1 for model k
+        return [self.root.split(k + 1) for k in range(n_models)]
+
+
+def synth(rng, C, d, n, mu, shift):
+    out = rng.synth(C, d, n, mu, shift)
+    return out[0], out[1]
+
+
+def batches(order: np.ndarray, B: int):
+    """batch_iter semantics: consecutive slices of the seeded order; the short
+    last batch is padded with weight-0 duplicates."""
+    out = []
+    for s in range(0, len(order), B):
+        idx = order[s:s + B]
+        w = np.ones(B, dtype=np.float32)
+        if len(idx) < B:
+            pad = B - len(idx)
+            w[len(idx):] = 0.0
+            idx = np.concatenate([idx, np.repeat(idx[-1:], pad)])
+        out.append((idx.astype(np.int64), w))
+    return out
+
+
+# --------------------------------------------------------------------------- backend
+class GpuBackend:
+    """The product path: libmtk (CUDA sm_100a) through the C ABI."""
+
+    def __init__(self, device: int = 0):
+        import torch
+
+        from . import api
+
+        self.torch, self.api = torch, api
+        self.ctx = api.Context(device)
+        self.Rng = api.Rng
+        self.device = torch.device("cuda", device)
+
+    def bank(self, G, dims, n_heads=1):
+        return self.api.Bank(self.ctx, G, list(dims), n_heads=n_heads)
+
+    def init(self, bank, g, rng):
+        bank.init_params(g, rng)
+
+    def to_dev(self, a):
+        return self.torch.from_numpy(np.ascontiguousarray(a)).to(self.device)
+
+    def step(self, bank, X, y, w, **kw):
+        return bank.train_step(self.to_dev(X), self.to_dev(y), self.to_dev(w), want_loss=False,
+                               **kw)
+
+    def features(self, bank, X, head, k):
+        logits = bank.forward(self.to_dev(X), head=head)
+        return self.api.posterior_features(self.ctx, logits, k).cpu().numpy().reshape(
+            X.shape[0], X.shape[1], k)
+
+    def attack_scores(self, bank, F):
+        logits = bank.forward(self.to_dev(F[None]), head=0)
+        return self.api.posterior_column(self.ctx, logits, 1).cpu().numpy()
+
+    def auc(self, scores, labels):
+        return self.api.auc(self.ctx, self.to_dev(scores.astype(np.float32)),
+                            self.to_dev(labels.astype(np.uint8)))
+
+
+# --------------------------------------------------------------------------- training
+def train_bank(be, cfg: SweepConfig, pop: Population, streams, models: list[int]):
+    """Train the given models (indices into `streams`) as one bank.
+    Returns (bank, members[G], non_members[G])."""
+    G = len(models)
+    two = cfg.paradigm == "parameter"
+    bank = be.bank(G, cfg.dims, n_heads=2 if two else 1)
+    mem, non, src = [], [], []
+    for g, k in enumerate(models):
+        r = streams[k]
+        perm = r.permutation(cfg.pool)
+        mem.append(perm[:cfg.members])
+        non.append(perm[cfg.members:2 * cfg.members])
+        be.init(bank, g, r)
+        src.append(r.permutation(cfg.source_pool)[:cfg.source_per_model])
+    B = cfg.batch
+    d = cfg.dims[0]
+
+    def gather(X, y, idx_per_model):
+        Xb = np.stack([X[i] for i in idx_per_model])
+        yb = np.stack([y[i] for i in idx_per_model]).astype(np.int32)
+        return Xb, yb
+
+    if cfg.paradigm == "model" and cfg.pretrain_epochs > 0:
+        for _ in range(cfg.pretrain_epochs):
+            orders = [batches(streams[k].permutation(cfg.source_per_model), B) for k in models]
+            for t in range(len(orders[0])):
+                idx = [src[g][orders[g][t][0]] for g in range(G)]
+                w = np.stack([orders[g][t][1] for g in range(G)])
+                Xb, yb = gather(pop.Xs, pop.ys, idx)
+                be.step(bank, Xb, yb, w, lr=cfg.lr, denom=(float(w[0].sum()), 0.0))
+    for _ in range(cfg.epochs):
+        orders = [batches(streams[k].permutation(cfg.members), B) for k in models]
+        for t in range(len(orders[0])):
+            idx = [mem[g][orders[g][t][0]] for g in range(G)]
+            w = np.stack([orders[g][t][1] for g in range(G)])
+            Xb, yb = gather(pop.Xt, pop.yt, idx)
+            if cfg.paradigm == "model":
+                be.step(bank, Xb, yb, w, lr=cfg.lr, frozen_layers=cfg.frozen_layers,
+                        denom=(float(w[0].sum()), 0.0))
+                continue
+            # co-training: a source batch rides along with every member batch
+            sidx = [src[g][(t * B + np.arange(B)) % cfg.source_per_model] for g in range(G)]
+            Xs_, ys_ = gather(pop.Xs, pop.ys, sidx)
+            Xc = np.concatenate([Xs_, Xb], axis=1)
+            yc = np.concatenate([ys_, yb], axis=1)
+            wc = np.concatenate([np.ones_like(w), w], axis=1)
+            if cfg.paradigm == "mapping":
+                be.step(bank, Xc, yc, wc, lr=cfg.lr, src_rows=B, mmd_lambda=cfg.mmd_lambda,
+                        denom=(float(wc[0].sum()), 0.0))
+            else:
+                be.step(bank, Xc, yc, wc, lr=cfg.lr, src_rows=B,
+                        denom=(float(B), float(w[0].sum())))
+    return bank, mem, non
+
+
+def query_features(be, cfg, pop, bank, mem, non):
+    """Top-k posteriors of every model on its members and non-members:
+    returns feats [G, 2*members, k] and labels [2*members] (1 = member)."""
+    head = 1 if cfg.paradigm == "parameter" else 0
+    G = len(mem)
+    X = np.stack([np.concatenate([pop.Xt[mem[g]], pop.Xt[non[g]]]) for g in range(G)])
+    F = be.features(bank, X, head, cfg.k)
+    lab = np.concatenate([np.ones(cfg.members, np.uint8), np.zeros(cfg.members, np.uint8)])
+    return F, lab
+
+
+def train_attack(be, cfg, F_train, lab_train, rng):
+    """Attack MLP k -> hidden -> 2 with CE + SGD on shadow features."""
+    bank = be.bank(1, (cfg.k, cfg.attack_hidden, 2))
+    be.init(bank, 0, rng)
+    n = len(lab_train)
+    for _ in range(cfg.attack_epochs):
+        for idx, w in batches(rng.permutation(n), cfg.attack_batch):
+            be.step(bank, F_train[idx][None], lab_train[idx][None].astype(np.int32), w[None],
+                    lr=cfg.attack_lr, denom=(float(w.sum()), 0.0))
+    return bank
+
+
+def run_sweep(cfg: SweepConfig, be=None, *, rank: int = 0, world: int = 1,
+              all_gather=None) -> dict[str, Any]:
+    """One paradigm: train target + shadows (sharded over ranks), attack, AUC.
+
+    Models [0, 1 + n_shadows) are split into contiguous rank blocks; the
+    per-rank feature blocks are combined with ``all_gather`` (a callable
+    taking this rank's array and returning the list over ranks, e.g. a
+    torch.distributed all_gather over NCCL); with one rank it is the identity.
+    """
+    cfg.validate()
+    be = be or GpuBackend()
+    pop = Population(cfg, be.Rng)
+    M = 1 + cfg.n_shadows
+    streams = pop.model_streams(M + 1)  # last stream drives the attack model
+    lo, hi = rank * M // world, (rank + 1) * M // world
+    models = list(range(lo, hi))
+    bank, mem, non = train_bank(be, cfg, pop, streams, models)
+    F, lab = query_features(be, cfg, pop, bank, mem, non)
+    parts = all_gather(F) if all_gather else [F]
+    F_all = np.concatenate(parts, axis=0)  # [M, 2*members, k] in model order
+    F_target, F_shadow = F_all[0], F_all[1:]
+    Ftr = F_shadow.reshape(-1, cfg.k).astype(np.float32)
+    ltr = np.tile(lab, cfg.n_shadows)
+    attack = train_attack(be, cfg, Ftr, ltr, streams[M])
+    scores = be.attack_scores(attack, F_target.astype(np.float32))
+    auc, acc = be.auc(scores, lab)
+    return {"paradigm": cfg.paradigm, "auc": auc, "accuracy": acc, "models": M,
+            "rank_models": models, "n_queries": int(len(lab)),
+            "config": dataclasses.asdict(cfg)}
+
+
+def main(argv=None):
+    import argparse
+
+    ap = argparse.ArgumentParser(description="shadow-model membership-inference sweep")
+    ap.add_argument("--paradigm", default="model", choices=["model", "mapping", "parameter"])
+    ap.add_argument("--shadows", type=int, default=4)
+    ap.add_argument("--epochs", type=int, default=10)
+    ap.add_argument("--seed", type=int, default=20110946)
+    a = ap.parse_args(argv)
+    cfg = SweepConfig(paradigm=a.paradigm, n_shadows=a.shadows, epochs=a.epochs, seed=a.seed)
+    print(json.dumps(run_sweep(cfg)))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,70 @@
+"""TEST INFRASTRUCTURE: the sweep driver's backend interface implemented on the
+CPU oracle (oracle/oracle.c via pyoracle), one f64 model at a time.  Used to
+replay paper_2011_09463_b200.sweep on the CPU and compare attack AUC /
+accuracy with the GPU path (north_star: within +-0.01)."""
+import numpy as np
+
+import pyoracle as po
+
+
+class OracleRng(po.Rng):
+    def synth(self, C, d, n, mu, shift=None):
+        X, y = po.synth(self, C, d, n, mu, shift)
+        # the GPU path trains on the fp32 rounding of the same draws
+        return X.astype(np.float32), y
+
+    def split(self, stream):
+        child = OracleRng(None)
+        po.orc().orc_rng_split(self._buf, stream, child._buf)
+        return child
+
+
+class OracleBank:
+    def __init__(self, G, dims, n_heads):
+        self.G, self.dims, self.n_heads = G, list(dims), n_heads
+        self.params = [None] * G
+
+
+class OracleBackend:
+    Rng = OracleRng
+
+    def bank(self, G, dims, n_heads=1):
+        return OracleBank(G, dims, n_heads)
+
+    def init(self, bank, g, rng):
+        bank.params[g] = po.mlp_init(rng, bank.dims, bank.n_heads)
+
+    def step(self, bank, X, y, w, *, lr, src_rows=0, frozen_layers=0, mmd_lambda=0.0,
+             denom=(0.0, 0.0)):
+        X = np.asarray(X, dtype=np.float64)
+        for g in range(bank.G):
+            W, b = bank.params[g]
+            dH = None
+            if mmd_lambda > 0:
+                _, H = po.mlp_forward(bank.dims, W, b, X[g])
+                _, _, gs, gt = po.mmd_gaussian(H[:src_rows], H[src_rows:])
+                dH = mmd_lambda * np.concatenate([gs, gt])
+            B = X.shape[1]
+            if bank.n_heads == 2:
+                den = [denom[0] or src_rows, denom[1] or B - src_rows]
+            else:
+                den = [denom[0] or B]
+            po.mlp_train_step(bank.dims, W, b, X[g], y[g], n_heads=bank.n_heads,
+                              frozen=frozen_layers, src_rows=src_rows, w=w[g], denoms=den, lr=lr,
+                              dH=dH)
+
+    def features(self, bank, X, head, k):
+        out = []
+        for g in range(bank.G):
+            W, b = bank.params[g]
+            logits, _ = po.mlp_forward(bank.dims, W, b, np.asarray(X[g], dtype=np.float64), head)
+            out.append(po.posterior_features(logits, k))
+        return np.stack(out)
+
+    def attack_scores(self, bank, F):
+        W, b = bank.params[0]
+        logits, _ = po.mlp_forward(bank.dims, W, b, np.asarray(F, dtype=np.float64))
+        return po.softmax(logits)[:, 1]
+
+    def auc(self, scores, labels):
+        return po.auc(scores, labels), po.accuracy(scores, labels, 0.5)

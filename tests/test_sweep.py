@@ -1,0 +1,96 @@
+"""The shadow-training / membership-attack driver (sweep.py).
+
+CPU: the driver on the oracle backend -- determinism, bit-exact host splits,
+and rank sharding (world_size 2 over gloo gives the same result as one rank).
+GPU: the driver on the product path vs the oracle backend -- attack AUC and
+accuracy within +-0.01 (north_star end-to-end tolerance).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from oracle_backend import OracleBackend
+from paper_2011_09463_b200.sweep import Population, SweepConfig, batches, run_sweep
+
+TINY = dict(dims=(24, 16, 10), n_shadows=3, pool=512, members=96, source_pool=1024,
+            source_per_model=256, batch=32, epochs=4, pretrain_epochs=1, mu_scale=0.2,
+            attack_epochs=10, attack_batch=64)
+
+
+@pytest.mark.parametrize("paradigm", ["model", "mapping", "parameter"])
+def test_sweep_oracle_deterministic(paradigm):
+    cfg = SweepConfig(paradigm=paradigm, **TINY)
+    a = run_sweep(cfg, OracleBackend())
+    b = run_sweep(SweepConfig(paradigm=paradigm, **TINY), OracleBackend())
+    assert a["auc"] == b["auc"] and a["accuracy"] == b["accuracy"]
+    assert 0.0 <= a["auc"] <= 1.0
+
+
+def test_member_splits_and_batches_bit_exact():
+    """members / non-members / batch orders come from rng.hpp semantics"""
+    import pyoracle as po
+    from oracle_backend import OracleRng
+
+    cfg = SweepConfig(**TINY)
+    pop = Population(cfg, OracleRng)
+    st = pop.model_streams(3)
+    # re-derive by hand with the raw oracle RNG
+    root = po.Rng(cfg.seed)
+    root.split(0)
+    for k in range(3):
+        r = root.split(k + 1)
+        assert np.array_equal(r.permutation(cfg.pool), st[k].permutation(cfg.pool))
+    bs = batches(np.arange(70, dtype=np.uint64), 32)
+    assert [len(i) for i, _ in bs] == [32, 32, 32]
+    assert bs[-1][1].sum() == 6 and (bs[-1][0][6:] == 69).all()
+
+
+def _worker(rank, world, port, paradigm, out):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+    def gather(F):
+        parts = [None] * world
+        dist.all_gather_object(parts, F)
+        return parts
+
+    r = run_sweep(SweepConfig(paradigm=paradigm, **TINY), OracleBackend(), rank=rank,
+                  world=world, all_gather=gather)
+    out[rank] = (r["auc"], r["accuracy"], r["rank_models"])
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("paradigm", ["model", "parameter"])
+def test_sweep_two_ranks_gloo_matches_one(paradigm):
+    import torch.multiprocessing as mp
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(2, port, paradigm, out), nprocs=2, join=True)
+    single = run_sweep(SweepConfig(paradigm=paradigm, **TINY), OracleBackend())
+    assert out[0][:2] == out[1][:2] == (single["auc"], single["accuracy"])
+    assert out[0][2] + out[1][2] == list(range(1 + TINY["n_shadows"]))
+
+
+MID = dict(dims=(64, 32, 10), n_shadows=4, pool=2048, members=512, source_pool=4096,
+           source_per_model=1024, batch=64, epochs=6, pretrain_epochs=1, mu_scale=0.15,
+           attack_epochs=20, attack_batch=256)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("paradigm", ["model", "mapping", "parameter"])
+def test_sweep_gpu_matches_oracle_auc(paradigm):
+    from paper_2011_09463_b200.sweep import GpuBackend
+
+    g = run_sweep(SweepConfig(paradigm=paradigm, **MID), GpuBackend())
+    o = run_sweep(SweepConfig(paradigm=paradigm, **MID), OracleBackend())
+    assert abs(g["auc"] - o["auc"]) <= 0.01, (g["auc"], o["auc"])
+    assert abs(g["accuracy"] - o["accuracy"]) <= 0.01, (g["accuracy"], o["accuracy"])
