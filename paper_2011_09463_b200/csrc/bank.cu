@@ -151,9 +151,10 @@ struct mtk_bank {
         stageB = B;
     }
     // re-derive the tf32 planes of parameter matrix i from its fp32 master
-    void split_param(int i) {
+    void split_param(int i, int model) {
         if (!W[i].hi) return;
-        launch_split(W[i].f, W[i].hi, W[i].lo, (long long)G * fan_in(i) * fan_out(i), ctx->stream);
+        const size_t nw = (size_t)fan_in(i) * fan_out(i), off = (size_t)model * nw;
+        launch_split(W[i].f + off, W[i].hi + off, W[i].lo + off, (long long)nw, ctx->stream);
         after_launch(*ctx);
     }
 };
@@ -192,6 +193,27 @@ void gemm_fwd(mtk_bank& k, int mat, const Plane3& in, int B, int r0, int rows, c
         u.bias_gs = fo;
         u.flags = c.d_flags;
         launch_umma(u, c.stream);
+    } else if (head_fwd_ok(fi, fo)) {
+        HeadFwd h;
+        h.G = k.G;
+        h.rows = rows;
+        h.K = fi;
+        h.N = fo;
+        h.A = in.f + (size_t)r0 * fi;
+        h.a_gs = (long long)B * fi;
+        h.lda = fi;
+        h.W = k.W[mat].f;
+        h.w_gs = (long long)fi * fo;
+        h.bias = k.b[mat];
+        h.bias_gs = fo;
+        h.C = out.f + (size_t)r0 * fo;
+        h.C_hi = out.hi ? out.hi + (size_t)r0 * fo : nullptr;
+        h.C_lo = out.lo ? out.lo + (size_t)r0 * fo : nullptr;
+        h.c_gs = (long long)B * fo;
+        h.ldc = fo;
+        h.relu = relu ? 1 : 0;
+        h.flags = c.d_flags;
+        launch_head_fwd(h, c.stream);
     } else {
         Gemm g;
         g.G = k.G;
@@ -308,6 +330,26 @@ void gemm_dw(mtk_bank& k, int mat, const Plane3& in, const Plane3& dz, int B, in
         u.grad_out = k.keep_grads ? k.gW[mat] : nullptr;
         u.flags = c.d_flags;
         launch_umma(u, c.stream);
+    } else if (head_dw_ok(fo)) {
+        HeadDw h;
+        h.G = k.G;
+        h.rows = rows;
+        h.K = fi;
+        h.N = fo;
+        h.A = in.f + (size_t)r0 * fi;
+        h.a_gs = (long long)B * fi;
+        h.lda = fi;
+        h.dZ = dz.f + (size_t)r0 * fo;
+        h.dz_gs = (long long)B * fo;
+        h.lddz = fo;
+        h.W = k.W[mat].f;
+        h.W_hi = k.W[mat].hi;
+        h.W_lo = k.W[mat].lo;
+        h.w_gs = (long long)fi * fo;
+        h.lr = lr;
+        h.grad_out = k.keep_grads ? k.gW[mat] : nullptr;
+        h.flags = c.d_flags;
+        launch_head_dw(h, c.stream);
     } else {
         Gemm g;
         g.G = k.G;
@@ -621,7 +663,7 @@ int mtk_bank_set_params(mtk_bank* k, int model, const double* const* W, const do
             MTK_CUDA(cudaMemcpyAsync(k->b[i] + model * nbias, tmp.data(), nbias * 4,
                                      cudaMemcpyHostToDevice, k->ctx->stream));
             MTK_CUDA(cudaStreamSynchronize(k->ctx->stream));
-            k->split_param(i);
+            k->split_param(i, model);
         }
         MTK_CUDA(cudaStreamSynchronize(k->ctx->stream));
     });

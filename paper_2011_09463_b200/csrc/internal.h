@@ -131,6 +131,41 @@ struct UmmaGemm {
 void launch_umma(const UmmaGemm& u, cudaStream_t s);
 void launch_split(const float* x, float* hi, float* lo, long long n, cudaStream_t s);
 
+// Skinny layers (out width <= 32): k_head.cu
+struct HeadFwd {
+    int G = 1, rows = 0, K = 0, N = 0;
+    const float* A = nullptr;
+    long long a_gs = 0, lda = 0;
+    const float* W = nullptr;  // [G][K][N]
+    long long w_gs = 0;
+    const float* bias = nullptr;
+    long long bias_gs = 0;
+    float* C = nullptr;
+    float* C_hi = nullptr;
+    float* C_lo = nullptr;
+    long long c_gs = 0, ldc = 0;
+    int relu = 0;
+    int* flags = nullptr;
+};
+struct HeadDw {
+    int G = 1, rows = 0, K = 0, N = 0;
+    const float* A = nullptr;  // [G][rows][K] (stride lda)
+    long long a_gs = 0, lda = 0;
+    const float* dZ = nullptr; // [G][rows][N] (stride lddz)
+    long long dz_gs = 0, lddz = 0;
+    float* W = nullptr;        // [G][K][N]
+    float* W_hi = nullptr;
+    float* W_lo = nullptr;
+    long long w_gs = 0;
+    float lr = 0.f;
+    float* grad_out = nullptr;
+    int* flags = nullptr;
+};
+bool head_fwd_ok(int K, int N);
+bool head_dw_ok(int N);
+void launch_head_fwd(const HeadFwd& p, cudaStream_t s);
+void launch_head_dw(const HeadDw& p, cudaStream_t s);
+
 // Cross-entropy head (tape.hpp:475-520), rows laid out [G, B, C].
 struct CeArgs {
     int G, B, C, src_rows;

@@ -7,11 +7,12 @@
 //   w_ij  = c_ij A_ij  (c = -2/m^2 S-S, -2/n^2 T-T, 2/(m n) cross, 0 on i = j)
 //   g_i   = sum_j w_ij (z_i - z_j) = z_i * Wsum_i - V_i,   V = W . Z
 // Per CTA: 128 rows i (M) x a 256-wide slice of V's feature dims; it streams
-// every 64-row j tile of Z:
-//   GEMM1  S[128x64]  = Z_i . Z_j^T      (TMEM cols [256,320), K = d)
+// every 128-row j tile of Z:
+//   GEMM1  S[128x128] = Z_i . Z_j^T      (TMEM cols [256,384), K = d)
 //   exp    4 epilogue warps: S -> d2 -> k, A, w; fp64 kernel sums and Wsum;
-//          w written to smem as tf32 hi/lo planes (K-major, 128-B swizzle)
-//   GEMM2  V[128xVD] += W[128x64] . Z_j[64xVD]   (TMEM cols [0,VD))
+//          w is split into tf32 hi/lo and written back to TMEM (hi over S,
+//          lo in cols [384,512)) -- FlashAttention-4 style, no smem round trip
+//   GEMM2  V[128xVD] += W[128x128] . Z_j[128xVD]  (A from TMEM; cols [0,VD))
 // Operands are the tf32 hi/lo planes of Z (HBM, [G][N][d]); all products are
 // 3xTF32 (hi*hi + hi*lo + lo*hi).  One warp issues TMA, one issues MMAs.
 #include <cuda.h>
@@ -27,15 +28,15 @@ namespace {
 
 using namespace sm100;
 
-constexpr int TI = 128, TJ = 64, KC = 32, JC = 16, VD = 256;
+constexpr int TI = 128, TJ = 128, KC = 32, JC = 16, VD = 256;
 constexpr int STAGES = 3;
-constexpr int G1_BYTES = 2 * (TI * KC * 4) + 2 * (TJ * KC * 4);  // 48 KB
+constexpr int G1_BYTES = 2 * (TI * KC * 4) + 2 * (TJ * KC * 4);  // 64 KB
 constexpr int G2_BYTES = 2 * (JC * VD * 4);                       // 32 KB
 constexpr int STAGE_BYTES = G1_BYTES;
-constexpr int W_PLANE = TI * TJ * 4;                              // 32 KB
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 2 * W_PLANE + 1024 + 256;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
 constexpr int NUM_THREADS = 192;
-constexpr uint32_t S_COL = 256;
+constexpr uint32_t S_COL = 256;   // S tile, overwritten in place by the W hi plane
+constexpr uint32_t WLO_COL = 384; // W lo plane
 
 struct MmdTcParams {
     CUtensorMap zk_hi, zk_lo;   // K-major view: (d, N, G), box (32, 64)
@@ -47,6 +48,7 @@ struct MmdTcParams {
     long long m, n;
     int d;
     int nb;
+    int geo5;                   // bandwidth multipliers are {1/4, 1/2, 1, 2, 4}
     float mult[8];
     long long row_begin, row_end;
     double* partial;            // [G][nblk][3]
@@ -64,13 +66,12 @@ struct MmdTcParams {
 // into an fp64 buffer: the MMD gradient is a small difference of large
 // same-domain and cross-domain sums, and fp32 tensor-core accumulation over
 // tens of thousands of j would not hold 1e-5 (C4: m+n = 73728).
-constexpr int FLUSH = 16;
+constexpr int FLUSH = 8;
 
 __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_constant__ MmdTcParams p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* wbuf = smem + STAGES * STAGE_BYTES;  // W hi plane, then lo plane
-    uint64_t* full = reinterpret_cast<uint64_t*>(wbuf + 2 * W_PLANE);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
     uint64_t* empty = full + STAGES;
     uint64_t* s_full = empty + STAGES;
     uint64_t* w_full = s_full + 1;
@@ -123,13 +124,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
                     uint8_t* b = smem + s * STAGE_BYTES;
                     mbar_expect_tx(&full[s], G1_BYTES);
                     const int k0 = kc * KC;
-                    // Z_i (128 rows as two 64-row boxes), hi then lo; then Z_j (64 rows)
+                    // Z_i and Z_j, 128 rows each as two 64-row boxes, hi then lo planes
                     tma_load_3d(b, &p.zk_hi, &full[s], k0, (int)i0, g);
                     tma_load_3d(b + 8192, &p.zk_hi, &full[s], k0, (int)i0 + 64, g);
                     tma_load_3d(b + 16384, &p.zk_lo, &full[s], k0, (int)i0, g);
                     tma_load_3d(b + 24576, &p.zk_lo, &full[s], k0, (int)i0 + 64, g);
                     tma_load_3d(b + 32768, &p.zk_hi, &full[s], k0, j0, g);
-                    tma_load_3d(b + 40960, &p.zk_lo, &full[s], k0, j0, g);
+                    tma_load_3d(b + 40960, &p.zk_hi, &full[s], k0, j0 + 64, g);
+                    tma_load_3d(b + 49152, &p.zk_lo, &full[s], k0, j0, g);
+                    tma_load_3d(b + 57344, &p.zk_lo, &full[s], k0, j0 + 64, g);
                 }
                 for (int jc = 0; jc < TJ / JC; ++jc, ++st) {
                     const int s = st % STAGES;
@@ -150,8 +153,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
         if (lane == 0) {
             constexpr uint32_t id1 = idesc_tf32(TI, TJ, 0, 0);
             constexpr uint32_t id2 = idesc_tf32(TI, VD, 0, 1);
-            const uint32_t tS = tmem + S_COL, tV = tmem;
-            const uint32_t wb = smem_u32(wbuf);
+            const uint32_t tS = tmem + S_COL, tV = tmem, tWlo = tmem + WLO_COL;
             int st = 0;
             for (int jt = 0; jt < njt; ++jt) {
                 for (int kc = 0; kc < nkc; ++kc, ++st) {
@@ -164,7 +166,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
                         const uint64_t ahi = smem_desc(b + kk * 32, 16, 1024, 2);
                         const uint64_t alo = smem_desc(b + 16384 + kk * 32, 16, 1024, 2);
                         const uint64_t bhi = smem_desc(b + 32768 + kk * 32, 16, 1024, 2);
-                        const uint64_t blo = smem_desc(b + 40960 + kk * 32, 16, 1024, 2);
+                        const uint64_t blo = smem_desc(b + 49152 + kk * 32, 16, 1024, 2);
                         mma_tf32(tS, alo, bhi, id1, (kc | kk) ? 1u : 0u);
                         mma_tf32(tS, ahi, blo, id1, 1u);
                         mma_tf32(tS, ahi, bhi, id1, 1u);
@@ -172,7 +174,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
                     mma_commit(&empty[s]);
                 }
                 mma_commit(s_full);
-                mbar_wait(w_full, jt & 1);
+                mbar_wait(w_full, jt & 1);  // W (hi in place of S, lo beside it) is in TMEM
                 tc_fence_after();
                 const bool chunk_start = do_flush ? (jt % FLUSH == 0) : (jt == 0);
                 if (do_flush && jt > 0 && jt % FLUSH == 0) {
@@ -186,16 +188,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
                     const uint32_t b = smem_u32(smem + s * STAGE_BYTES);
 #pragma unroll
                     for (int h = 0; h < JC / 8; ++h) {
-                        const int kk = jc * (JC / 8) + h;  // 8-wide k step over the 64 j of W
-                        const uint32_t woff = (kk >> 2) * 16384 + (kk & 3) * 32;
-                        const uint64_t ahi = smem_desc(wb + woff, 16, 1024, 2);
-                        const uint64_t alo = smem_desc(wb + W_PLANE + woff, 16, 1024, 2);
+                        const uint32_t kcol = (uint32_t)(jc * JC + h * 8);  // j column of W
                         const uint64_t bhi = smem_desc(b + h * 1024, 2048, 512, 1);
                         const uint64_t blo = smem_desc(b + 16384 + h * 1024, 2048, 512, 1);
                         const uint32_t acc0 = (!chunk_start || jc || h) ? 1u : 0u;
-                        mma_tf32(tV, alo, bhi, id2, acc0);
-                        mma_tf32(tV, ahi, blo, id2, 1u);
-                        mma_tf32(tV, ahi, bhi, id2, 1u);
+                        mma_tf32_ts(tV, tWlo + kcol, bhi, id2, acc0);
+                        mma_tf32_ts(tV, tS + kcol, blo, id2, 1u);
+                        mma_tf32_ts(tV, tS + kcol, bhi, id2, 1u);
                     }
                     mma_commit(&empty[s]);
                 }
@@ -207,6 +206,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
         // ---------------- epilogue warps: exp + weights, then the gradient ----------------
         const int q = warp & 3;
         const int r = 32 * q + lane;  // row within the tile == TMEM lane
+        const uint32_t lane_base = (uint32_t)(32 * q) << 16;
         const long long gi = i0 + r;
         const bool row_ok = gi < re;
         const bool si = gi < p.m;
@@ -218,6 +218,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
             nscale[b] = b < p.nb ? (float)(-1.4426950408889634 / s) : 0.f;
             two_inv[b] = b < p.nb ? (float)(2.0 / s) : 0.f;
         }
+        const float x1 = (float)(-1.4426950408889634 / beta);  // log2 scale for s = beta
+        const float tb = (float)(2.0 / beta);
         const float cSS = (float)(-2.0 / ((double)p.m * (double)p.m));
         const float cTT = (float)(-2.0 / ((double)p.n * (double)p.n));
         const float cST = (float)(2.0 / ((double)p.m * (double)p.n));
@@ -226,32 +228,42 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
         double ksum[3] = {0.0, 0.0, 0.0};
         double wsum = 0.0;
         int nflush = 0;
-        uint8_t* whi = wbuf;
-        uint8_t* wlo = wbuf + W_PLANE;
         for (int jt = 0; jt < njt; ++jt) {
             const long long j0 = (long long)jt * TJ;
             mbar_wait(s_full, jt & 1);
             tc_fence_after();
+            float kss = 0.f, ktt = 0.f, kst = 0.f, part = 0.f;
 #pragma unroll 1
-            for (int half = 0; half < 2; ++half) {
+            for (int cb = 0; cb < TJ / 32; ++cb) {
                 float sv[32];
-                tmem_ld_32x32(tmem + ((uint32_t)(32 * q) << 16) + S_COL + half * 32, sv);
-                float wrow[32];
-                float part = 0.f;
-                float kss = 0.f, ktt = 0.f, kst = 0.f;
+                tmem_ld_32x32(tmem + lane_base + S_COL + cb * 32, sv);
+                float wlo[32];
 #pragma unroll
                 for (int c = 0; c < 32; ++c) {
-                    const long long gj = j0 + half * 32 + c;
+                    const long long gj = j0 + cb * 32 + c;
                     float wv = 0.f;
                     if (row_ok && gj < N) {
-                        const float d2 = fmaxf(ni + nrm[gj] - 2.f * sv[c], 0.f);
-                        float kv = 0.f, A = 0.f;
+                        const float d2 = fmaxf(ni + __ldg(nrm + gj) - 2.f * sv[c], 0.f);
+                        float kv, A;
+                        if (p.geo5) {
+                            // s_b = beta * {1/4,1/2,1,2,4}: two ex2, the rest by squaring
+                            const float e1 = exp2f(d2 * x1);          // s = beta
+                            const float e4 = exp2f(d2 * x1 * 0.25f);  // s = 4 beta
+                            const float e2 = e4 * e4;                 // s = 2 beta
+                            const float eh = e1 * e1;                 // s = beta/2
+                            const float eq = eh * eh;                 // s = beta/4
+                            kv = ((eq + eh) + (e1 + e2)) + e4;
+                            A = tb * ((4.f * eq + 2.f * eh) + (e1 + 0.5f * e2) + 0.25f * e4);
+                        } else {
+                            kv = 0.f;
+                            A = 0.f;
 #pragma unroll
-                        for (int b = 0; b < 8; ++b) {
-                            if (b < p.nb) {
-                                const float e = exp2f(d2 * nscale[b]);
-                                kv += e;
-                                A = fmaf(two_inv[b], e, A);
+                            for (int b = 0; b < 8; ++b) {
+                                if (b < p.nb) {
+                                    const float e = exp2f(d2 * nscale[b]);
+                                    kv += e;
+                                    A = fmaf(two_inv[b], e, A);
+                                }
                             }
                         }
                         const bool sj = gj < p.m;
@@ -267,29 +279,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
                         }
                         if (gj == gi) wv = 0.f;
                     }
-                    wrow[c] = wv;
                     part += wv;
+                    float h, l;
+                    split_tf32(wv, h, l);
+                    sv[c] = h;
+                    wlo[c] = l;
                 }
-                ksum[0] += kss;
-                ksum[1] += ktt;
-                ksum[2] += kst;
-                wsum += part;
-                // store w (hi/lo) into the K-major SW128 W planes: atom `half`
-                uint8_t* rowh = whi + half * 16384 + r * 128;
-                uint8_t* rowl = wlo + half * 16384 + r * 128;
-#pragma unroll
-                for (int ch = 0; ch < 8; ++ch) {
-                    float4 h4, l4;
-                    split_tf32(wrow[4 * ch + 0], h4.x, l4.x);
-                    split_tf32(wrow[4 * ch + 1], h4.y, l4.y);
-                    split_tf32(wrow[4 * ch + 2], h4.z, l4.z);
-                    split_tf32(wrow[4 * ch + 3], h4.w, l4.w);
-                    const int pc = (ch ^ (r & 7)) * 16;
-                    *reinterpret_cast<float4*>(rowh + pc) = h4;
-                    *reinterpret_cast<float4*>(rowl + pc) = l4;
-                }
+                // W hi overwrites the S chunk just read; W lo goes to its own columns
+                tmem_st_32x32(tmem + lane_base + S_COL + cb * 32, sv);
+                tmem_st_32x32(tmem + lane_base + WLO_COL + cb * 32, wlo);
             }
-            fence_proxy_async_smem();
+            ksum[0] += kss;
+            ksum[1] += ktt;
+            ksum[2] += kst;
+            wsum += part;
+            tmem_st_wait();
             tc_fence_before();
             mbar_arrive(w_full);
             if (do_flush && (jt + 1) % FLUSH == 0 && jt + 1 < njt) {
@@ -300,7 +304,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
 #pragma unroll 1
                 for (int cb = 0; cb < VD / 32; ++cb) {
                     float vv[32];
-                    tmem_ld_32x32(tmem + ((uint32_t)(32 * q) << 16) + cb * 32, vv);
+                    tmem_ld_32x32(tmem + lane_base + cb * 32, vv);
                     if (!row_ok) continue;
                     for (int c = 0; c < 32 && cb * 32 + c < vd; ++c) {
                         const int k = v0 + cb * 32 + c;
@@ -326,7 +330,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
 #pragma unroll 1
         for (int cb = 0; cb < VD / 32; ++cb) {
             float vv[32];
-            tmem_ld_32x32(tmem + ((uint32_t)(32 * q) << 16) + cb * 32, vv);
+            tmem_ld_32x32(tmem + lane_base + cb * 32, vv);
             if (!out) continue;
             for (int c = 0; c < 32; ++c) {
                 const int k = v0 + cb * 32 + c;
@@ -457,7 +461,7 @@ void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s) {
     mmd_prep_kernel<<<pg, 256, 0, s>>>(a.Xs, a.xs_gs, a.Xt, a.xt_gs, a.m, a.n, a.d, zhi, zlo, norms);
     MmdTcParams p;
     std::memset(&p, 0, sizeof(p));
-    p.zk_hi = zmap(zhi, a.d, N, a.G, 64, false);
+    p.zk_hi = zmap(zhi, a.d, N, a.G, 64, false);  // 64-row boxes (two per 128-row tile)
     p.zk_lo = zmap(zlo, a.d, N, a.G, 64, false);
     p.zm_hi = zmap(zhi, a.d, N, a.G, JC, true);
     p.zm_lo = zmap(zlo, a.d, N, a.G, JC, true);
@@ -470,6 +474,8 @@ void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s) {
     p.d = a.d;
     p.nb = a.nb;
     for (int b = 0; b < 8; ++b) p.mult[b] = a.mult[b] > 0 ? a.mult[b] : 1.f;
+    p.geo5 = a.nb == 5 && a.mult[0] == 0.25f && a.mult[1] == 0.5f && a.mult[2] == 1.f &&
+             a.mult[3] == 2.f && a.mult[4] == 4.f;
     p.row_begin = a.row_begin;
     p.row_end = re;
     p.partial = a.partial;
