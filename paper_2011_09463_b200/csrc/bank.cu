@@ -74,6 +74,8 @@ struct mtk_bank {
     float* gH = nullptr;
     double* mmd_part = nullptr;
     size_t mmd_part_bytes = 0;
+    float* head_scratch = nullptr;  // skinny dW partial sums
+    size_t head_scratch_bytes = 0;
     void* mmd_z = nullptr;     // tf32 planes + norms of the MMD sample (tc path)
     size_t mmd_z_bytes = 0;
     bool tc_mmd = true;
@@ -107,6 +109,7 @@ struct mtk_bank {
         cudaFree(beta);
         cudaFree(mmd_part);
         cudaFree(mmd_z);
+        cudaFree(head_scratch);
         cudaFree(Xs);
         cudaFree(ys);
         cudaFree(ws);
@@ -349,6 +352,14 @@ void gemm_dw(mtk_bank& k, int mat, const Plane3& in, const Plane3& dz, int B, in
         h.lr = lr;
         h.grad_out = k.keep_grads ? k.gW[mat] : nullptr;
         h.flags = c.d_flags;
+        const size_t hb = head_dw_scratch_bytes(k.G, fi, fo);
+        if (hb > k.head_scratch_bytes) {
+            MTK_CUDA(cudaStreamSynchronize(c.stream));
+            cudaFree(k.head_scratch);
+            MTK_CUDA(cudaMalloc(&k.head_scratch, hb));
+            k.head_scratch_bytes = hb;
+        }
+        h.partial = k.head_scratch;
         launch_head_dw(h, c.stream);
     } else {
         Gemm g;

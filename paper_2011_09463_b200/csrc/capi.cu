@@ -15,6 +15,10 @@ std::string& last_error() {
     thread_local std::string e;
     return e;
 }
+unsigned long long& launch_counter() {
+    static unsigned long long n = 0;
+    return n;
+}
 }  // namespace mtk
 
 extern "C" void mtk_internal_set_error(const char* msg) { mtk::last_error() = msg ? msg : ""; }
@@ -147,7 +151,7 @@ int mtk_ctx_synchronize(mtk_ctx* c) {
 int mtk_ctx_launch_count(mtk_ctx* c, uint64_t* out) {
     return guard([&] {
         need(c && out, MTK_VALUE_ERROR, "null argument");
-        *out = c->launches;
+        *out = __atomic_load_n(&launch_counter(), __ATOMIC_RELAXED);
     });
 }
 
@@ -195,6 +199,8 @@ static MmdArgs mmd_args(mtk_ctx* c, const float* Xs, int64_t m, const float* Xt,
     a.flags = c->d_flags;
     const char* env = getenv("MTK_DISABLE_TC");
     a.tc = !(env && env[0] == '1') && mmd_tc_supported(a);
+    if (const char* t = getenv("MTK_MMD_TRACE"))
+        a.trace = reinterpret_cast<unsigned long long*>(strtoull(t, nullptr, 0));
     return a;
 }
 

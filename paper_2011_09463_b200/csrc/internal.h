@@ -160,8 +160,10 @@ struct HeadDw {
     float lr = 0.f;
     float* grad_out = nullptr;
     int* flags = nullptr;
+    float* partial = nullptr;  // scratch, head_dw_scratch_bytes()
 };
 bool head_fwd_ok(int K, int N);
+size_t head_dw_scratch_bytes(int G, int K, int N);
 bool head_dw_ok(int N);
 void launch_head_fwd(const HeadFwd& p, cudaStream_t s);
 void launch_head_dw(const HeadDw& p, cudaStream_t s);
@@ -206,6 +208,7 @@ struct MmdArgs {
     float grad_scale = 1.f;
     int* flags = nullptr;
     bool tc = false;                // run on the tcgen05 path (k_mmd_tc.cu)
+    unsigned long long* trace = nullptr;  // diagnostics (k_mmd_tc.cu)
 };
 int mmd_blocks_per_group(const MmdArgs& a);  // partial-sum blocks (depends on a.tc)
 bool mmd_tc_supported(const MmdArgs& a);
@@ -228,8 +231,13 @@ void auc_device(Ctx& ctx, const float* scores, const uint8_t* labels, long long 
 
 std::string& last_error();
 
+// process-wide count of kernels this library launched (mtk_ctx_launch_count)
+unsigned long long& launch_counter();
+inline void count_launch() { __atomic_add_fetch(&launch_counter(), 1ULL, __ATOMIC_RELAXED); }
+
 inline void after_launch(Ctx& c, int n = 1) {
-    c.launches += n;
+    (void)c;
+    (void)n;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) fail(MTK_ERROR, std::string("kernel launch: ") + cudaGetErrorString(e));
 }

@@ -144,6 +144,7 @@ inline unsigned nblocks(long long n, int t) { return (unsigned)((n + t - 1) / t)
 void launch_softmax(const float* logits, long long rows, int C, float* probs, cudaStream_t s) {
     if (rows <= 0) return;
     softmax_kernel<<<nblocks(rows, 256), 256, 0, s>>>(logits, rows, C, probs);
+    count_launch();
 }
 
 void launch_features(const float* logits, long long rows, int C, int k, const int32_t* labels,
@@ -151,12 +152,14 @@ void launch_features(const float* logits, long long rows, int C, int k, const in
     if (C > MAXC) fail(MTK_SHAPE_ERROR, "posterior_features: more than 64 classes");
     if (rows <= 0) return;
     features_kernel<<<nblocks(rows, 256), 256, 0, s>>>(logits, rows, C, k, labels, feats, flags);
+    count_launch();
 }
 
 void launch_column(const float* logits, long long rows, int C, int col, float* out,
                    cudaStream_t s) {
     if (rows <= 0) return;
     column_kernel<<<nblocks(rows, 256), 256, 0, s>>>(logits, rows, C, col, out);
+    count_launch();
 }
 
 void auc_device(Ctx& ctx, const float* scores, const uint8_t* labels, long long n, double* auc,
@@ -188,12 +191,15 @@ void auc_device(Ctx& ctx, const float* scores, const uint8_t* labels, long long 
     void* wk = take(tmp);
     MTK_CUDA(cudaMemsetAsync(cnt, 0, 64, s));
     auc_keys_kernel<<<nblocks(n, 256), 256, 0, s>>>(scores, labels, n, k_in, v_in, cnt);
+    count_launch();
     cub::DeviceRadixSort::SortPairs(wk, sort_bytes, k_in, k_out, v_in, v_out, ni, 0, 32, s);
     auc_start_flags<<<nblocks(n, 256), 256, 0, s>>>(k_out, n, flag);
+    count_launch();
     cub::DeviceScan::InclusiveSum(wk, scan_bytes, flag, gid, ni, s);
     auc_group_bounds<<<nblocks(n, 256), 256, 0, s>>>(k_out, gid, n, gstart, gend);
+    count_launch();
     auc_rank_sum<<<nblocks(n, 256), 256, 0, s>>>(v_out, gid, n, gstart, gend, cnt + 2);
-    ctx.launches += 7;
+    count_launch();
     unsigned long long h[3];
     MTK_CUDA(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, s));
     MTK_CUDA(cudaFreeAsync(base, s));

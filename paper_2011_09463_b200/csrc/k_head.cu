@@ -65,28 +65,31 @@ __global__ void __launch_bounds__(256) head_fwd_kernel(HeadFwd p) {
     if (bad && p.flags) atomicOr(p.flags, kFlagNonFinite);
 }
 
-// block (p-chunk of 64 input features, model g), 256 threads = 4 row groups x 64
-__global__ void __launch_bounds__(256) head_dw_kernel(HeadDw p) {
+// dW partials: block (p-chunk of 64 input features, model g, row split rs),
+// 256 threads = 4 row groups x 64 features; partial[rs][g][p][n]
+constexpr int RS = 8;
+__global__ void __launch_bounds__(256) head_dw_partial_kernel(HeadDw p) {
     __shared__ float sdz[64][MAXN + 1];
     __shared__ float red[4][64][MAXN + 1];
-    const int g = blockIdx.y;
+    const int g = blockIdx.y, rs = blockIdx.z;
     const int pl = threadIdx.x & 63, rg = threadIdx.x >> 6;
     const int pp = blockIdx.x * 64 + pl;
     const int N = p.N;
+    const int rbeg = (int)((long long)p.rows * rs / RS), rend = (int)((long long)p.rows * (rs + 1) / RS);
     float acc[MAXN];
 #pragma unroll
     for (int n = 0; n < MAXN; ++n) acc[n] = 0.f;
     const float* A = p.A + g * p.a_gs;
     const float* dz = p.dZ + g * p.dz_gs;
-    for (int r0 = 0; r0 < p.rows; r0 += 64) {
+    for (int r0 = rbeg; r0 < rend; r0 += 64) {
         __syncthreads();
         for (int i = threadIdx.x; i < 64 * N; i += blockDim.x) {
             const int rr = i / N, n = i % N;
-            sdz[rr][n] = (r0 + rr < p.rows) ? dz[(long long)(r0 + rr) * p.lddz + n] : 0.f;
+            sdz[rr][n] = (r0 + rr < rend) ? dz[(long long)(r0 + rr) * p.lddz + n] : 0.f;
         }
         __syncthreads();
         if (pp < p.K) {
-            for (int rr = rg; rr < 64 && r0 + rr < p.rows; rr += 4) {
+            for (int rr = rg; rr < 64 && r0 + rr < rend; rr += 4) {
                 const float av = A[(long long)(r0 + rr) * p.lda + pp];
 #pragma unroll
                 for (int n = 0; n < MAXN; ++n)
@@ -96,23 +99,31 @@ __global__ void __launch_bounds__(256) head_dw_kernel(HeadDw p) {
     }
     for (int n = 0; n < N; ++n) red[rg][pl][n] = acc[n];
     __syncthreads();
-    if (rg == 0 && pp < p.K) {
-        bool bad = false;
-        for (int n = 0; n < N; ++n) {
-            const float gsum = ((red[0][pl][n] + red[1][pl][n]) + red[2][pl][n]) + red[3][pl][n];
-            const long long idx = g * p.w_gs + (long long)pp * N + n;
-            if (p.grad_out) p.grad_out[idx] = gsum;
-            const float w = p.W[idx] - p.lr * gsum;
-            bad |= !isfinite(w);
-            p.W[idx] = w;
-            if (p.W_hi) {
-                float h, l;
-                sm100::split_tf32(w, h, l);
-                p.W_hi[idx] = h;
-                p.W_lo[idx] = l;
-            }
-        }
-        if (bad && p.flags) atomicOr(p.flags, kFlagNonFinite);
+    if (rg == 0 && pp < p.K)
+        for (int n = 0; n < N; ++n)
+            p.partial[(((long long)rs * p.G + g) * p.K + pp) * N + n] =
+                ((red[0][pl][n] + red[1][pl][n]) + red[2][pl][n]) + red[3][pl][n];
+}
+
+// dW = sum of the RS partials in fixed order; SGD + optional gradient copy
+__global__ void head_dw_finish_kernel(HeadDw p) {
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const long long per = (long long)p.K * p.N;
+    if (t >= per * p.G) return;
+    const int g = (int)(t / per);
+    const long long e = t % per;
+    float gsum = 0.f;
+    for (int rs = 0; rs < RS; ++rs) gsum += p.partial[((long long)rs * p.G + g) * per + e];
+    const long long idx = g * p.w_gs + e;
+    if (p.grad_out) p.grad_out[idx] = gsum;
+    const float w = p.W[idx] - p.lr * gsum;
+    if (!isfinite(w) && p.flags) atomicOr(p.flags, kFlagNonFinite);
+    p.W[idx] = w;
+    if (p.W_hi) {
+        float h, l;
+        sm100::split_tf32(w, h, l);
+        p.W_hi[idx] = h;
+        p.W_lo[idx] = l;
     }
 }
 
@@ -132,12 +143,20 @@ void launch_head_fwd(const HeadFwd& p, cudaStream_t s) {
     }
     dim3 grid((p.rows + 63) / 64, p.G);
     head_fwd_kernel<<<grid, 256, smem, s>>>(p);
+    count_launch();
 }
+
+size_t head_dw_scratch_bytes(int G, int K, int N) { return (size_t)RS * G * K * N * sizeof(float); }
 
 void launch_head_dw(const HeadDw& p, cudaStream_t s) {
     if (p.K <= 0) return;
-    dim3 grid((p.K + 63) / 64, p.G);
-    head_dw_kernel<<<grid, 256, 0, s>>>(p);
+    if (!p.partial) fail(MTK_ERROR, "head_dw: missing partial scratch");
+    dim3 grid((p.K + 63) / 64, p.G, RS);
+    head_dw_partial_kernel<<<grid, 256, 0, s>>>(p);
+    count_launch();
+    const long long n = (long long)p.G * p.K * p.N;
+    head_dw_finish_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(p);
+    count_launch();
 }
 
 }  // namespace mtk

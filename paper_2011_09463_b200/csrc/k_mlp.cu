@@ -211,18 +211,22 @@ void launch_gemm(const Gemm& p, cudaStream_t s) {
     if (p.M <= 0 || p.N <= 0 || p.G <= 0) return;
     dim3 grid((p.N + BN - 1) / BN, (p.M + BM - 1) / BM, p.G);
     gemm_simt_kernel<<<grid, NT, 0, s>>>(p);
+    count_launch();
 }
 
 void launch_ce(const CeArgs& a, cudaStream_t s) {
     const long long rows = (long long)a.G * a.B;
     ce_kernel<<<(unsigned)((rows + 127) / 128), 128, 0, s>>>(a);
+    count_launch();
     row_sum_kernel<<<a.G, 256, 0, s>>>(a.row_loss, a.B, a.loss, a.flags);
+    count_launch();
 }
 
 void launch_bias_sgd(int G, int rows, int N, const float* dZ, long long dz_gs, float* b,
                      long long b_gs, float lr, float* grad_out, int* flags, cudaStream_t s) {
     dim3 grid((N + 31) / 32, G);
     bias_sgd_kernel<<<grid, 256, 0, s>>>(G, rows, N, dZ, dz_gs, b, b_gs, lr, grad_out, flags);
+    count_launch();
 }
 
 }  // namespace mtk

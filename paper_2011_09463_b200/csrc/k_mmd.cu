@@ -257,7 +257,9 @@ void launch_mmd_beta(const MmdArgs& a, double* beta_out, double* scratch, cudaSt
     const long long N = a.m + a.n;
     const int P = (int)((N + BETA_ROWS - 1) / BETA_ROWS);
     beta_partial_kernel<<<dim3(P, a.G), NT, 0, s>>>(a, scratch, P);
+    count_launch();
     beta_finish_kernel<<<a.G, NT, 0, s>>>(a, scratch, P, beta_out);
+    count_launch();
 }
 
 void launch_mmd_pairs(const MmdArgs& a, cudaStream_t s) {
@@ -272,10 +274,12 @@ void launch_mmd_pairs(const MmdArgs& a, cudaStream_t s) {
         attr = true;
     }
     mmd_pairs_kernel<<<dim3(nblk, a.G), NT, smem, s>>>(a, nblk);
+    count_launch();
 }
 
 void launch_mmd_finish(const MmdArgs& a, double* value, double* sums3, cudaStream_t s) {
     mmd_finish_kernel<<<a.G, 32, 0, s>>>(a, mmd_blocks_per_group(a), value, sums3);
+    count_launch();
 }
 
 }  // namespace mtk

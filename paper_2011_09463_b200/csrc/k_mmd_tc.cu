@@ -28,15 +28,17 @@ namespace {
 
 using namespace sm100;
 
-constexpr int TI = 128, TJ = 128, KC = 32, JC = 16, VD = 256;
-constexpr int STAGES = 3;
-constexpr int G1_BYTES = 2 * (TI * KC * 4) + 2 * (TJ * KC * 4);  // 64 KB
+constexpr int TI = 128, TJ = 64, KC = 32, JC = 16, VD = 256;
+constexpr int STAGES = 4;
+constexpr int G1_BYTES = 2 * (TI * KC * 4) + 2 * (TJ * KC * 4);  // 48 KB
 constexpr int G2_BYTES = 2 * (JC * VD * 4);                       // 32 KB
 constexpr int STAGE_BYTES = G1_BYTES;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
 constexpr int NUM_THREADS = 192;
-constexpr uint32_t S_COL = 256;   // S tile, overwritten in place by the W hi plane
-constexpr uint32_t WLO_COL = 384; // W lo plane
+// TMEM columns: V [0,256); S / W-hi double buffer b at 256 + 64 b (S is
+// overwritten in place by the hi plane of W); W-lo buffer b at 384 + 64 b.
+constexpr uint32_t S_COL = 256;
+constexpr uint32_t WLO_COL = 384;
 
 struct MmdTcParams {
     CUtensorMap zk_hi, zk_lo;   // K-major view: (d, N, G), box (32, 64)
@@ -60,7 +62,20 @@ struct MmdTcParams {
     float grad_scale;
     int* flags;
     double* vacc;               // [G][N][d] fp64 flush buffer for V, or null (short j loops)
+    unsigned long long* trace;  // diagnostics: phase timestamps of CTA (0,0,0), or null
 };
+
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+// trace layout: [0..4096) producer stage-ready times, [4096..8192) MMA stage-consumed
+// times, [8192..12288) epilogue: per tile (s_full seen, w_full arrived)
+#define TRACE(off, idx)                                                                   \
+    do {                                                                                  \
+        if (tr && (idx) < 4096) tr[(off) + (idx)] = gtime();                              \
+    } while (0)
 
 // V is accumulated in fp32 TMEM for FLUSH j tiles at a time, then drained
 // into an fp64 buffer: the MMD gradient is a small difference of large
@@ -73,9 +88,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
     uint64_t* empty = full + STAGES;
-    uint64_t* s_full = empty + STAGES;
-    uint64_t* w_full = s_full + 1;
-    uint64_t* v_full = w_full + 1;
+    uint64_t* s_full = empty + STAGES;  // [2]
+    uint64_t* w_full = s_full + 2;      // [2]
+    uint64_t* v_full = w_full + 2;
     uint64_t* v_empty = v_full + 1;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(v_empty + 1);
 
@@ -90,6 +105,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
     const int nkc = (p.d + KC - 1) / KC;
     const int njt = (int)((N + TJ - 1) / TJ);
     const bool do_flush = p.vacc != nullptr;
+    unsigned long long* tr =
+        (p.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) ? p.trace : nullptr;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&p.zk_hi);
@@ -100,8 +117,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(s_full, 1);
-        mbar_init(w_full, 128);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&s_full[b], 1);
+            mbar_init(&w_full[b], 128);
+        }
         mbar_init(v_full, 1);
         mbar_init(v_empty, 128);
         fence_barrier_init();
@@ -112,38 +131,44 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
+    // Software pipeline (MMA order == TMA order):
+    //   G1(0), G1(1), G2(0), G1(2), G2(1), ..., G1(n-1), G2(n-2), G2(n-1)
+    // so the exp epilogue of tile t overlaps GEMM1 of tile t+1.
     if (warp == 0) {
         if (lane == 0) {
             // ---------------- TMA producer ----------------
             int st = 0;
-            for (int jt = 0; jt < njt; ++jt) {
-                const int j0 = jt * TJ;
-                for (int kc = 0; kc < nkc; ++kc, ++st) {
-                    const int s = st % STAGES;
-                    mbar_wait(&empty[s], ((st / STAGES) & 1) ^ 1);
-                    uint8_t* b = smem + s * STAGE_BYTES;
-                    mbar_expect_tx(&full[s], G1_BYTES);
-                    const int k0 = kc * KC;
-                    // Z_i and Z_j, 128 rows each as two 64-row boxes, hi then lo planes
-                    tma_load_3d(b, &p.zk_hi, &full[s], k0, (int)i0, g);
-                    tma_load_3d(b + 8192, &p.zk_hi, &full[s], k0, (int)i0 + 64, g);
-                    tma_load_3d(b + 16384, &p.zk_lo, &full[s], k0, (int)i0, g);
-                    tma_load_3d(b + 24576, &p.zk_lo, &full[s], k0, (int)i0 + 64, g);
-                    tma_load_3d(b + 32768, &p.zk_hi, &full[s], k0, j0, g);
-                    tma_load_3d(b + 40960, &p.zk_hi, &full[s], k0, j0 + 64, g);
-                    tma_load_3d(b + 49152, &p.zk_lo, &full[s], k0, j0, g);
-                    tma_load_3d(b + 57344, &p.zk_lo, &full[s], k0, j0 + 64, g);
+            for (int t = 0; t <= njt; ++t) {
+                if (t < njt) {
+                    const int j0 = t * TJ;
+                    for (int kc = 0; kc < nkc; ++kc, ++st) {
+                        const int s = st % STAGES;
+                        mbar_wait(&empty[s], ((st / STAGES) & 1) ^ 1);
+                        TRACE(0, st);
+                        uint8_t* b = smem + s * STAGE_BYTES;
+                        mbar_expect_tx(&full[s], G1_BYTES);
+                        const int k0 = kc * KC;
+                        tma_load_3d(b, &p.zk_hi, &full[s], k0, (int)i0, g);
+                        tma_load_3d(b + 8192, &p.zk_hi, &full[s], k0, (int)i0 + 64, g);
+                        tma_load_3d(b + 16384, &p.zk_lo, &full[s], k0, (int)i0, g);
+                        tma_load_3d(b + 24576, &p.zk_lo, &full[s], k0, (int)i0 + 64, g);
+                        tma_load_3d(b + 32768, &p.zk_hi, &full[s], k0, j0, g);
+                        tma_load_3d(b + 40960, &p.zk_lo, &full[s], k0, j0, g);
+                    }
                 }
-                for (int jc = 0; jc < TJ / JC; ++jc, ++st) {
-                    const int s = st % STAGES;
-                    mbar_wait(&empty[s], ((st / STAGES) & 1) ^ 1);
-                    uint8_t* b = smem + s * STAGE_BYTES;
-                    mbar_expect_tx(&full[s], G2_BYTES);
-                    // Z_j rows [j0+16jc, +16) x dims [v0, v0+VD): VD/32 boxes per plane
-                    for (int q = 0; q < VD / 32; ++q) {
-                        tma_load_3d(b + q * 2048, &p.zm_hi, &full[s], v0 + 32 * q, j0 + JC * jc, g);
-                        tma_load_3d(b + 16384 + q * 2048, &p.zm_lo, &full[s], v0 + 32 * q,
-                                    j0 + JC * jc, g);
+                if (t >= 1) {
+                    const int j0 = (t - 1) * TJ;
+                    for (int jc = 0; jc < TJ / JC; ++jc, ++st) {
+                        const int s = st % STAGES;
+                        mbar_wait(&empty[s], ((st / STAGES) & 1) ^ 1);
+                        TRACE(0, st);
+                        uint8_t* b = smem + s * STAGE_BYTES;
+                        mbar_expect_tx(&full[s], G2_BYTES);
+                        for (int q = 0; q < VD / 32; ++q) {
+                            tma_load_3d(b + q * 2048, &p.zm_hi, &full[s], v0 + 32 * q, j0 + JC * jc, g);
+                            tma_load_3d(b + 16384 + q * 2048, &p.zm_lo, &full[s], v0 + 32 * q,
+                                        j0 + JC * jc, g);
+                        }
                     }
                 }
             }
@@ -153,52 +178,62 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
         if (lane == 0) {
             constexpr uint32_t id1 = idesc_tf32(TI, TJ, 0, 0);
             constexpr uint32_t id2 = idesc_tf32(TI, VD, 0, 1);
-            const uint32_t tS = tmem + S_COL, tV = tmem, tWlo = tmem + WLO_COL;
+            const uint32_t tV = tmem;
             int st = 0;
-            for (int jt = 0; jt < njt; ++jt) {
-                for (int kc = 0; kc < nkc; ++kc, ++st) {
-                    const int s = st % STAGES;
-                    mbar_wait(&full[s], (st / STAGES) & 1);
-                    tc_fence_after();
-                    const uint32_t b = smem_u32(smem + s * STAGE_BYTES);
+            for (int t = 0; t <= njt; ++t) {
+                if (t < njt) {
+                    const uint32_t tS = tmem + S_COL + (t & 1) * TJ;
+                    for (int kc = 0; kc < nkc; ++kc, ++st) {
+                        const int s = st % STAGES;
+                        mbar_wait(&full[s], (st / STAGES) & 1);
+                        TRACE(4096, st);
+                        tc_fence_after();
+                        const uint32_t b = smem_u32(smem + s * STAGE_BYTES);
 #pragma unroll
-                    for (int kk = 0; kk < KC / 8; ++kk) {
-                        const uint64_t ahi = smem_desc(b + kk * 32, 16, 1024, 2);
-                        const uint64_t alo = smem_desc(b + 16384 + kk * 32, 16, 1024, 2);
-                        const uint64_t bhi = smem_desc(b + 32768 + kk * 32, 16, 1024, 2);
-                        const uint64_t blo = smem_desc(b + 49152 + kk * 32, 16, 1024, 2);
-                        mma_tf32(tS, alo, bhi, id1, (kc | kk) ? 1u : 0u);
-                        mma_tf32(tS, ahi, blo, id1, 1u);
-                        mma_tf32(tS, ahi, bhi, id1, 1u);
+                        for (int kk = 0; kk < KC / 8; ++kk) {
+                            const uint64_t ahi = smem_desc(b + kk * 32, 16, 1024, 2);
+                            const uint64_t alo = smem_desc(b + 16384 + kk * 32, 16, 1024, 2);
+                            const uint64_t bhi = smem_desc(b + 32768 + kk * 32, 16, 1024, 2);
+                            const uint64_t blo = smem_desc(b + 40960 + kk * 32, 16, 1024, 2);
+                            mma_tf32(tS, alo, bhi, id1, (kc | kk) ? 1u : 0u);
+                            mma_tf32(tS, ahi, blo, id1, 1u);
+                            mma_tf32(tS, ahi, bhi, id1, 1u);
+                        }
+                        mma_commit(&empty[s]);
                     }
-                    mma_commit(&empty[s]);
+                    mma_commit(&s_full[t & 1]);
                 }
-                mma_commit(s_full);
-                mbar_wait(w_full, jt & 1);  // W (hi in place of S, lo beside it) is in TMEM
-                tc_fence_after();
-                const bool chunk_start = do_flush ? (jt % FLUSH == 0) : (jt == 0);
-                if (do_flush && jt > 0 && jt % FLUSH == 0) {
-                    mbar_wait(v_empty, ((jt / FLUSH) - 1) & 1);  // previous chunk drained
+                if (t >= 1) {
+                    const int jt = t - 1;
+                    const uint32_t tWhi = tmem + S_COL + (jt & 1) * TJ;
+                    const uint32_t tWlo = tmem + WLO_COL + (jt & 1) * TJ;
+                    mbar_wait(&w_full[jt & 1], (jt >> 1) & 1);  // W(jt) is in TMEM
                     tc_fence_after();
-                }
-                for (int jc = 0; jc < TJ / JC; ++jc, ++st) {
-                    const int s = st % STAGES;
-                    mbar_wait(&full[s], (st / STAGES) & 1);
-                    tc_fence_after();
-                    const uint32_t b = smem_u32(smem + s * STAGE_BYTES);
+                    const bool chunk_start = do_flush ? (jt % FLUSH == 0) : (jt == 0);
+                    if (do_flush && jt > 0 && jt % FLUSH == 0) {
+                        mbar_wait(v_empty, ((jt / FLUSH) - 1) & 1);  // previous chunk drained
+                        tc_fence_after();
+                    }
+                    for (int jc = 0; jc < TJ / JC; ++jc, ++st) {
+                        const int s = st % STAGES;
+                        mbar_wait(&full[s], (st / STAGES) & 1);
+                        TRACE(4096, st);
+                        tc_fence_after();
+                        const uint32_t b = smem_u32(smem + s * STAGE_BYTES);
 #pragma unroll
-                    for (int h = 0; h < JC / 8; ++h) {
-                        const uint32_t kcol = (uint32_t)(jc * JC + h * 8);  // j column of W
-                        const uint64_t bhi = smem_desc(b + h * 1024, 2048, 512, 1);
-                        const uint64_t blo = smem_desc(b + 16384 + h * 1024, 2048, 512, 1);
-                        const uint32_t acc0 = (!chunk_start || jc || h) ? 1u : 0u;
-                        mma_tf32_ts(tV, tWlo + kcol, bhi, id2, acc0);
-                        mma_tf32_ts(tV, tS + kcol, blo, id2, 1u);
-                        mma_tf32_ts(tV, tS + kcol, bhi, id2, 1u);
+                        for (int h = 0; h < JC / 8; ++h) {
+                            const uint32_t kcol = (uint32_t)(jc * JC + h * 8);
+                            const uint64_t bhi = smem_desc(b + h * 1024, 2048, 512, 1);
+                            const uint64_t blo = smem_desc(b + 16384 + h * 1024, 2048, 512, 1);
+                            const uint32_t acc0 = (!chunk_start || jc || h) ? 1u : 0u;
+                            mma_tf32_ts(tV, tWlo + kcol, bhi, id2, acc0);
+                            mma_tf32_ts(tV, tWhi + kcol, blo, id2, 1u);
+                            mma_tf32_ts(tV, tWhi + kcol, bhi, id2, 1u);
+                        }
+                        mma_commit(&empty[s]);
                     }
-                    mma_commit(&empty[s]);
+                    if (do_flush && (jt + 1) % FLUSH == 0 && jt + 1 < njt) mma_commit(v_full);
                 }
-                if (do_flush && (jt + 1) % FLUSH == 0 && jt + 1 < njt) mma_commit(v_full);
             }
             mma_commit(v_full);
         }
@@ -230,64 +265,92 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
         int nflush = 0;
         for (int jt = 0; jt < njt; ++jt) {
             const long long j0 = (long long)jt * TJ;
-            mbar_wait(s_full, jt & 1);
+            const int bsel = jt & 1;
+            mbar_wait(&s_full[bsel], (jt >> 1) & 1);
+            if (r == 0) TRACE(8192, 2 * jt);
             tc_fence_after();
             float kss = 0.f, ktt = 0.f, kst = 0.f, part = 0.f;
+            // 8-column chunks keep the unrolled body (and the I-cache footprint) small
 #pragma unroll 1
-            for (int cb = 0; cb < TJ / 32; ++cb) {
-                float sv[32];
-                tmem_ld_32x32(tmem + lane_base + S_COL + cb * 32, sv);
-                float wlo[32];
+            for (int ch = 0; ch < TJ / 8; ++ch) {
+                float sv[8], wlo[8];
+                tmem_ld_32x8(tmem + lane_base + S_COL + bsel * TJ + ch * 8, sv);
+                const long long jb = j0 + ch * 8;
+                // column classes are warp-uniform: all 8 j in range / same domain?
+                const bool full8 = row_ok && jb + 8 <= N;
+                const bool sj_all = jb + 8 <= p.m, tj_all = jb >= p.m;
+                float kv8[8], A8[8];
+                if (p.geo5) {
 #pragma unroll
-                for (int c = 0; c < 32; ++c) {
-                    const long long gj = j0 + cb * 32 + c;
-                    float wv = 0.f;
-                    if (row_ok && gj < N) {
-                        const float d2 = fmaxf(ni + __ldg(nrm + gj) - 2.f * sv[c], 0.f);
-                        float kv, A;
-                        if (p.geo5) {
-                            // s_b = beta * {1/4,1/2,1,2,4}: two ex2, the rest by squaring
-                            const float e1 = exp2f(d2 * x1);          // s = beta
-                            const float e4 = exp2f(d2 * x1 * 0.25f);  // s = 4 beta
-                            const float e2 = e4 * e4;                 // s = 2 beta
-                            const float eh = e1 * e1;                 // s = beta/2
-                            const float eq = eh * eh;                 // s = beta/4
-                            kv = ((eq + eh) + (e1 + e2)) + e4;
-                            A = tb * ((4.f * eq + 2.f * eh) + (e1 + 0.5f * e2) + 0.25f * e4);
-                        } else {
-                            kv = 0.f;
-                            A = 0.f;
-#pragma unroll
-                            for (int b = 0; b < 8; ++b) {
-                                if (b < p.nb) {
-                                    const float e = exp2f(d2 * nscale[b]);
-                                    kv += e;
-                                    A = fmaf(two_inv[b], e, A);
-                                }
-                            }
-                        }
-                        const bool sj = gj < p.m;
-                        if (si && sj) {
-                            kss += kv;
-                            wv = cSS * A;
-                        } else if (!si && !sj) {
-                            ktt += kv;
-                            wv = cTT * A;
-                        } else {
-                            if (si) kst += kv;
-                            wv = cST * A;
-                        }
-                        if (gj == gi) wv = 0.f;
+                    for (int c = 0; c < 8; ++c) {
+                        const long long gj = jb + c;
+                        const float nj = (gj < N) ? __ldg(nrm + gj) : 0.f;
+                        const float d2 = fmaxf(ni + nj - 2.f * sv[c], 0.f);
+                        // s_b = beta * {1/4,1/2,1,2,4}: two ex2, the rest by squaring
+                        const float e1 = exp2f(d2 * x1);          // s = beta
+                        const float e4 = exp2f(d2 * x1 * 0.25f);  // s = 4 beta
+                        const float e2 = e4 * e4;                 // s = 2 beta
+                        const float eh = e1 * e1;                 // s = beta/2
+                        const float eq = eh * eh;                 // s = beta/4
+                        kv8[c] = ((eq + eh) + (e1 + e2)) + e4;
+                        A8[c] = tb * ((4.f * eq + 2.f * eh) + (e1 + 0.5f * e2) + 0.25f * e4);
                     }
-                    part += wv;
-                    float h, l;
-                    split_tf32(wv, h, l);
-                    sv[c] = h;
-                    wlo[c] = l;
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const long long gj = jb + c;
+                        const float nj = (gj < N) ? __ldg(nrm + gj) : 0.f;
+                        const float d2 = fmaxf(ni + nj - 2.f * sv[c], 0.f);
+                        float kv = 0.f, A = 0.f;
+#pragma unroll 1
+                        for (int b = 0; b < p.nb; ++b) {
+                            const float e = exp2f(d2 * nscale[b]);
+                            kv += e;
+                            A = fmaf(two_inv[b], e, A);
+                        }
+                        kv8[c] = kv;
+                        A8[c] = A;
+                    }
                 }
-                // W hi overwrites the S chunk just read; W lo goes to its own columns
-                tmem_st_32x32(tmem + lane_base + S_COL + cb * 32, sv);
-                tmem_st_32x32(tmem + lane_base + WLO_COL + cb * 32, wlo);
+                if (full8 && (sj_all || tj_all) && !(gi >= jb && gi < jb + 8)) {
+                    // fast path: one domain pair for the whole chunk, no diagonal
+                    const float cw = si ? (sj_all ? cSS : cST) : (sj_all ? cST : cTT);
+                    float ks = 0.f;
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        ks += kv8[c];
+                        const float wv = cw * A8[c];
+                        part += wv;
+                        split_tf32(wv, sv[c], wlo[c]);
+                    }
+                    if (si && sj_all) kss += ks;
+                    else if (!si && tj_all) ktt += ks;
+                    else if (si) kst += ks;
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const long long gj = jb + c;
+                        float wv = 0.f;
+                        if (row_ok && gj < N) {
+                            const bool sj = gj < p.m;
+                            if (si && sj) {
+                                kss += kv8[c];
+                                wv = cSS * A8[c];
+                            } else if (!si && !sj) {
+                                ktt += kv8[c];
+                                wv = cTT * A8[c];
+                            } else {
+                                if (si) kst += kv8[c];
+                                wv = cST * A8[c];
+                            }
+                            if (gj == gi) wv = 0.f;
+                        }
+                        part += wv;
+                        split_tf32(wv, sv[c], wlo[c]);
+                    }
+                }
+                tmem_st_32x8(tmem + lane_base + S_COL + bsel * TJ + ch * 8, sv);
+                tmem_st_32x8(tmem + lane_base + WLO_COL + bsel * TJ + ch * 8, wlo);
             }
             ksum[0] += kss;
             ksum[1] += ktt;
@@ -295,9 +358,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
             wsum += part;
             tmem_st_wait();
             tc_fence_before();
-            mbar_arrive(w_full);
-            if (do_flush && (jt + 1) % FLUSH == 0 && jt + 1 < njt) {
-                // drain this chunk of V into the fp64 buffer (rows owned by this CTA)
+            mbar_arrive(&w_full[bsel]);
+            if (r == 0) TRACE(8192, 2 * jt + 1);
+            // drain the previous V chunk (G2 of tile jt-1 closed it) into fp64
+            if (do_flush && jt > 0 && jt % FLUSH == 0) {
                 mbar_wait(v_full, nflush & 1);
                 tc_fence_after();
                 double* vrow = p.vacc + ((long long)g * N + (row_ok ? gi : 0)) * p.d;
@@ -319,13 +383,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
         // gradient rows: g_i = scale * (z_i * Wsum_i - V_i) over this CTA's feature slice
         mbar_wait(v_full, nflush & 1);
         tc_fence_after();
+        // all MMAs and TMA loads are complete: stage z_i (hi + lo) through the idle
+        // ring with coalesced loads, [128][VD + 1] fp32
+        float* zs = reinterpret_cast<float*>(smem);
+        const int t = threadIdx.x - 64;
+        for (int e = t; e < TI * VD; e += 128) {
+            const int rr = e / VD, k = e % VD;
+            const long long row = i0 + rr;
+            float z = 0.f;
+            if (k < vd && row < N) {
+                const long long o = ((long long)g * N + row) * p.d + v0 + k;
+                z = p.z_hi[o] + p.z_lo[o];
+            }
+            zs[rr * (VD + 1) + k] = z;
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
         const double* vrow = (nflush && row_ok) ? p.vacc + ((long long)g * N + gi) * p.d : nullptr;
         float* out = nullptr;
         if (row_ok)
             out = si ? (p.gXs ? p.gXs + g * p.gs_gs + gi * p.d : nullptr)
                      : (p.gXt ? p.gXt + g * p.gt_gs + (gi - p.m) * p.d : nullptr);
-        const float* zh = p.z_hi + ((long long)g * N + (row_ok ? gi : 0)) * p.d;
-        const float* zl = p.z_lo + ((long long)g * N + (row_ok ? gi : 0)) * p.d;
         bool bad = false;
 #pragma unroll 1
         for (int cb = 0; cb < VD / 32; ++cb) {
@@ -335,7 +412,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
             for (int c = 0; c < 32; ++c) {
                 const int k = v0 + cb * 32 + c;
                 if (cb * 32 + c >= vd) break;
-                const double z = (double)zh[k] + (double)zl[k];
+                const double z = (double)zs[r * (VD + 1) + cb * 32 + c];
                 const double vt = (double)vv[c] + (vrow ? vrow[k] : 0.0);
                 const float gv = (float)((z * wsum - vt) * (double)p.grad_scale);
                 bad |= !isfinite(gv);
@@ -345,7 +422,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
         if (bad) atomicOr(p.flags, kFlagNonFinite);
         // fixed-order reduction of the kernel sums over the 128 rows (d-slice 0 only)
         __shared__ double red[3][128];
-        const int t = threadIdx.x - 64;
         for (int c = 0; c < 3; ++c) red[c][t] = ksum[c];
         asm volatile("bar.sync 1, 128;" ::: "memory");
         for (int w = 64; w > 0; w >>= 1) {
@@ -459,6 +535,7 @@ void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s) {
             (reinterpret_cast<uintptr_t>(norms + (size_t)a.G * N) + 255) & ~uintptr_t(255));
     dim3 pg((unsigned)((N + 7) / 8), a.G);
     mmd_prep_kernel<<<pg, 256, 0, s>>>(a.Xs, a.xs_gs, a.Xt, a.xt_gs, a.m, a.n, a.d, zhi, zlo, norms);
+    count_launch();
     MmdTcParams p;
     std::memset(&p, 0, sizeof(p));
     p.zk_hi = zmap(zhi, a.d, N, a.G, 64, false);  // 64-row boxes (two per 128-row tile)
@@ -487,6 +564,7 @@ void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s) {
     p.grad_scale = a.grad_scale;
     p.flags = a.flags;
     p.vacc = vacc;
+    p.trace = a.trace;
     static bool attr = false;
     if (!attr) {
         MTK_CUDA(cudaFuncSetAttribute(mmd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -495,6 +573,7 @@ void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s) {
     }
     dim3 grid(p.nblk, (a.d + VD - 1) / VD, a.G);
     mmd_tc_kernel<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(p);
+    count_launch();
 }
 
 }  // namespace mtk

@@ -303,6 +303,7 @@ void launch_variant(const UmmaParams& p, int G, cudaStream_t s) {
     }
     dim3 grid((p.N + BN - 1) / BN, (p.M + BM - 1) / BM, G);
     umma_gemm_kernel<A_MN, B_MN><<<grid, NUM_THREADS, SMEM_BYTES, s>>>(p);
+    count_launch();
 }
 
 }  // namespace
@@ -314,6 +315,7 @@ void launch_split(const float* x, float* hi, float* lo, long long n, cudaStream_
         fail(MTK_ERROR, "split: unaligned pointer");
     const long long t = (n + 3) / 4;
     split_kernel<<<(unsigned)((t + 255) / 256), 256, 0, s>>>(x, hi, lo, n);
+    count_launch();
 }
 
 // Operand views: each operand is given as (hi, lo) planes with element
