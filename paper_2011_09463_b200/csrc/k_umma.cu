@@ -18,6 +18,7 @@
 #include <cuda.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -55,6 +56,74 @@ struct UmmaParams {
     int* flags;
     float* dbg;  // diagnostics: receives stage-0 smem (64 KB) when non-null
 };
+
+// TMEM accumulator (this warp's 32 lanes = rows m0+32q.., ncols columns) ->
+// fused epilogue -> fp32 + tf32 hi/lo planes in HBM.
+__device__ __forceinline__ void epilogue_rows(const UmmaParams& p, uint32_t tmem, int q, int lane,
+                                              int g, int m0, int n0, int ncols) {
+        const int m = m0 + 32 * q + lane;
+        const bool row_ok = m < p.M;
+        const long long rowbase = (long long)g * p.c_gs + (long long)m * p.ldc;
+        bool bad = false;
+#pragma unroll 1
+        for (int c = 0; c < ncols / 32; ++c) {
+            float v[32];
+            tmem_ld_32x32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(c * 32), v);
+            const int nb = n0 + c * 32;
+            if (!row_ok || nb >= p.N) continue;
+            float xs[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const int n = nb + j;
+                const long long idx = rowbase + n;
+                float x = v[j];
+                if (n < p.N) {
+                    if (p.epi == (int)Epi::kBias || p.epi == (int)Epi::kBiasRelu) {
+                        x += p.bias[g * p.bias_gs + n];
+                        bad |= !isfinite(x);
+                        if (p.epi == (int)Epi::kBiasRelu) x = x > 0.f ? x : 0.f;
+                    } else if (p.epi == (int)Epi::kMask) {
+                        if (p.add) x = p.add[idx] + x;
+                        x = (p.mask[idx] > 0.f) ? x : 0.f;
+                    } else if (p.epi == (int)Epi::kSgd) {  // C is the fp32 master weight
+                        if (p.grad_out) p.grad_out[idx] = x;
+                        x = p.C[idx] - p.lr * x;
+                        bad |= !isfinite(x);
+                    }
+                }
+                xs[j] = x;
+            }
+            const bool vec = (nb + 32 <= p.N) && ((rowbase + nb) % 4 == 0);
+            if (vec) {
+#pragma unroll
+                for (int j = 0; j < 32; j += 4) {
+                    float4 x4 = make_float4(xs[j], xs[j + 1], xs[j + 2], xs[j + 3]);
+                    float4 h4, l4;
+                    split_tf32(x4.x, h4.x, l4.x);
+                    split_tf32(x4.y, h4.y, l4.y);
+                    split_tf32(x4.z, h4.z, l4.z);
+                    split_tf32(x4.w, h4.w, l4.w);
+                    *reinterpret_cast<float4*>(p.C + rowbase + nb + j) = x4;
+                    if (p.C_hi) {
+                        *reinterpret_cast<float4*>(p.C_hi + rowbase + nb + j) = h4;
+                        *reinterpret_cast<float4*>(p.C_lo + rowbase + nb + j) = l4;
+                    }
+                }
+            } else {
+                for (int j = 0; j < 32 && nb + j < p.N; ++j) {
+                    const long long idx = rowbase + nb + j;
+                    float hi, lo;
+                    split_tf32(xs[j], hi, lo);
+                    p.C[idx] = xs[j];
+                    if (p.C_hi) {
+                        p.C_hi[idx] = hi;
+                        p.C_lo[idx] = lo;
+                    }
+                }
+            }
+        }
+        if (bad && p.flags) atomicOr(p.flags, kFlagNonFinite);
+}
 
 template <int A_MN, int B_MN>
 __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_constant__ UmmaParams p) {
@@ -161,68 +230,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
         const int q = warp & 3;  // TMEM lane quarter this warp may access
         mbar_wait(tmem_full, 0);
         tc_fence_after();
-        const int m = m0 + 32 * q + lane;
-        const bool row_ok = m < p.M;
-        const long long rowbase = (long long)g * p.c_gs + (long long)m * p.ldc;
-        bool bad = false;
-#pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-            float v[32];
-            tmem_ld_32x32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(c * 32), v);
-            const int nb = n0 + c * 32;
-            if (!row_ok || nb >= p.N) continue;
-            float xs[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                const int n = nb + j;
-                const long long idx = rowbase + n;
-                float x = v[j];
-                if (n < p.N) {
-                    if (p.epi == (int)Epi::kBias || p.epi == (int)Epi::kBiasRelu) {
-                        x += p.bias[g * p.bias_gs + n];
-                        bad |= !isfinite(x);
-                        if (p.epi == (int)Epi::kBiasRelu) x = x > 0.f ? x : 0.f;
-                    } else if (p.epi == (int)Epi::kMask) {
-                        if (p.add) x = p.add[idx] + x;
-                        x = (p.mask[idx] > 0.f) ? x : 0.f;
-                    } else if (p.epi == (int)Epi::kSgd) {  // C is the fp32 master weight
-                        if (p.grad_out) p.grad_out[idx] = x;
-                        x = p.C[idx] - p.lr * x;
-                        bad |= !isfinite(x);
-                    }
-                }
-                xs[j] = x;
-            }
-            const bool vec = (nb + 32 <= p.N) && ((rowbase + nb) % 4 == 0);
-            if (vec) {
-#pragma unroll
-                for (int j = 0; j < 32; j += 4) {
-                    float4 x4 = make_float4(xs[j], xs[j + 1], xs[j + 2], xs[j + 3]);
-                    float4 h4, l4;
-                    split_tf32(x4.x, h4.x, l4.x);
-                    split_tf32(x4.y, h4.y, l4.y);
-                    split_tf32(x4.z, h4.z, l4.z);
-                    split_tf32(x4.w, h4.w, l4.w);
-                    *reinterpret_cast<float4*>(p.C + rowbase + nb + j) = x4;
-                    if (p.C_hi) {
-                        *reinterpret_cast<float4*>(p.C_hi + rowbase + nb + j) = h4;
-                        *reinterpret_cast<float4*>(p.C_lo + rowbase + nb + j) = l4;
-                    }
-                }
-            } else {
-                for (int j = 0; j < 32 && nb + j < p.N; ++j) {
-                    const long long idx = rowbase + nb + j;
-                    float hi, lo;
-                    split_tf32(xs[j], hi, lo);
-                    p.C[idx] = xs[j];
-                    if (p.C_hi) {
-                        p.C_hi[idx] = hi;
-                        p.C_lo[idx] = lo;
-                    }
-                }
-            }
-        }
-        if (bad && p.flags) atomicOr(p.flags, kFlagNonFinite);
+        epilogue_rows(p, tmem, q, lane, g, m0, n0, BN);
         if (p.dbg) {
             const float* sf = reinterpret_cast<const float*>(smem);
             for (int i = threadIdx.x - 64; i < STAGE_BYTES / 4; i += 128) p.dbg[i] = sf[i];
@@ -233,6 +241,130 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc<TMEM_COLS>(tmem);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2): a 2-CTA cluster computes a 256 x 256 tile.
+// Each CTA stages its 128 rows of A and its 128 columns of B (hi/lo planes);
+// the leader (rank 0) issues tcgen05.mma.cta_group::2 with M = 256, N = 256,
+// reading both CTAs' smem; each CTA's TMEM receives its 128 rows x 256 cols.
+// Per SM this halves operand bytes per MAC versus the 128 x 128 kernel.
+constexpr int BN2 = 256;
+constexpr uint32_t TMEM_COLS2 = 256;
+
+template <int A_MN, int B_MN>
+__global__ void __launch_bounds__(NUM_THREADS, 1) umma2_gemm_kernel(const __grid_constant__ UmmaParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tmem_full = empty + STAGES;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    const int g = blockIdx.z;
+    const int m0 = (blockIdx.x >> 1) * 256 + (int)rank * 128;  // this CTA's rows
+    const int n0 = blockIdx.y * BN2;                            // the pair's columns
+    const int nb0 = n0 + (int)rank * 128;                       // this CTA's B half
+    const int nk = (p.K + BK - 1) / BK;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&p.a_hi);
+        tma_prefetch(&p.a_lo);
+        tma_prefetch(&p.b_hi);
+        tma_prefetch(&p.b_lo);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 2);   // one arrival per CTA of the pair (leader's copy used)
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(tmem_full, 1);
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc_2sm<TMEM_COLS2>(tmem_slot);
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------- TMA producer (both CTAs) ----------------
+            for (int kb = 0; kb < nk; ++kb) {
+                const int s = kb % STAGES;
+                const uint32_t ph = (kb / STAGES) & 1;
+                mbar_wait(&empty[s], ph ^ 1);
+                uint8_t* st = smem + s * STAGE_BYTES;
+                const int k0 = kb * BK;
+                if (A_MN) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        tma_load_3d_2sm(st + j * 4096, &p.a_hi, &full[s], m0 + 32 * j, k0, g);
+                        tma_load_3d_2sm(st + TILE_BYTES + j * 4096, &p.a_lo, &full[s], m0 + 32 * j, k0, g);
+                    }
+                } else {
+                    tma_load_3d_2sm(st, &p.a_hi, &full[s], k0, m0, g);
+                    tma_load_3d_2sm(st + TILE_BYTES, &p.a_lo, &full[s], k0, m0, g);
+                }
+                uint8_t* sb = st + 2 * TILE_BYTES;
+                if (B_MN) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        tma_load_3d_2sm(sb + j * 4096, &p.b_hi, &full[s], nb0 + 32 * j, k0, g);
+                        tma_load_3d_2sm(sb + TILE_BYTES + j * 4096, &p.b_lo, &full[s], nb0 + 32 * j, k0, g);
+                    }
+                } else {
+                    tma_load_3d_2sm(sb, &p.b_hi, &full[s], k0, nb0, g);
+                    tma_load_3d_2sm(sb + TILE_BYTES, &p.b_lo, &full[s], k0, nb0, g);
+                }
+                // the leader expects both CTAs' bytes; the follower only arrives
+                if (rank == 0) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
+                else mbar_arrive_remote(&full[s], 0);
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer (leader CTA, one thread) ----------------
+        constexpr uint32_t idesc = idesc_tf32(256, BN2, A_MN, B_MN);
+        if (rank == 0 && lane == 0) {
+            for (int kb = 0; kb < nk; ++kb) {
+                const int s = kb % STAGES;
+                const uint32_t ph = (kb / STAGES) & 1;
+                mbar_wait(&full[s], ph);
+                tc_fence_after();
+                const uint32_t base = smem_u32(smem + s * STAGE_BYTES);
+#pragma unroll
+                for (int kk = 0; kk < BK / 8; ++kk) {
+                    const uint32_t aoff = A_MN ? kk * 1024 : kk * 32;
+                    const uint32_t boff = B_MN ? kk * 1024 : kk * 32;
+                    constexpr uint32_t a_lbo = A_MN ? 4096 : 16, b_lbo = B_MN ? 4096 : 16;
+                    constexpr uint32_t a_sbo = A_MN ? 512 : 1024, b_sbo = B_MN ? 512 : 1024;
+                    constexpr uint32_t a_lay = A_MN ? 1 : 2, b_lay = B_MN ? 1 : 2;
+                    const uint64_t ahi = smem_desc(base + aoff, a_lbo, a_sbo, a_lay);
+                    const uint64_t alo = smem_desc(base + TILE_BYTES + aoff, a_lbo, a_sbo, a_lay);
+                    const uint64_t bhi = smem_desc(base + 2 * TILE_BYTES + boff, b_lbo, b_sbo, b_lay);
+                    const uint64_t blo = smem_desc(base + 3 * TILE_BYTES + boff, b_lbo, b_sbo, b_lay);
+                    const uint32_t acc0 = (kb | kk) ? 1u : 0u;
+                    mma_tf32_2sm(tmem, alo, bhi, idesc, acc0);
+                    mma_tf32_2sm(tmem, ahi, blo, idesc, 1u);
+                    mma_tf32_2sm(tmem, ahi, bhi, idesc, 1u);
+                }
+                mma_commit_2sm(&empty[s], 0x3);  // frees this slot in both CTAs
+            }
+            mma_commit_2sm(tmem_full, 0x3);
+        }
+    } else {
+        // ---------------- epilogue (both CTAs: own 128 rows x 256 cols) ----------------
+        const int q = warp & 3;
+        mbar_wait(tmem_full, 0);
+        tc_fence_after();
+        epilogue_rows(p, tmem, q, lane, g, m0, n0, BN2);
+    }
+    tc_fence_before();
+    cluster_sync();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc_2sm<TMEM_COLS2>(tmem);
     }
 }
 
@@ -306,6 +438,39 @@ void launch_variant(const UmmaParams& p, int G, cudaStream_t s) {
     count_launch();
 }
 
+template <int A_MN, int B_MN>
+void launch_variant2(const UmmaParams& p, int G, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        MTK_CUDA(cudaFuncSetAttribute(umma2_gemm_kernel<A_MN, B_MN>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+        attr = true;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * ((p.M + 255) / 256), (p.N + BN2 - 1) / BN2, G);
+    cfg.blockDim = dim3(NUM_THREADS);
+    cfg.dynamicSmemBytes = SMEM_BYTES;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    MTK_CUDA(cudaLaunchKernelEx(&cfg, umma2_gemm_kernel<A_MN, B_MN>, p));
+    count_launch();
+}
+
+bool use_pair_kernel(const UmmaGemm& u) {
+    static int mode = -1;
+    if (mode < 0) {
+        const char* e = getenv("MTK_UMMA_PAIR");
+        mode = e ? atoi(e) : 1;
+    }
+    return mode != 0 && u.M > 128 && u.N > 128;
+}
+
 }  // namespace
 
 void launch_split(const float* x, float* hi, float* lo, long long n, cudaStream_t s) {
@@ -356,6 +521,13 @@ void launch_umma(const UmmaGemm& u, cudaStream_t s) {
     p.grad_out = u.grad_out;
     p.flags = u.flags;
     p.dbg = u.dbg;
+    if (use_pair_kernel(u)) {
+        if (!u.a_mn && u.b_mn) launch_variant2<0, 1>(p, u.G, s);
+        else if (!u.a_mn && !u.b_mn) launch_variant2<0, 0>(p, u.G, s);
+        else if (u.a_mn && u.b_mn) launch_variant2<1, 1>(p, u.G, s);
+        else launch_variant2<1, 0>(p, u.G, s);
+        return;
+    }
     if (!u.a_mn && u.b_mn) launch_variant<0, 1>(p, u.G, s);
     else if (!u.a_mn && !u.b_mn) launch_variant<0, 0>(p, u.G, s);
     else if (u.a_mn && u.b_mn) launch_variant<1, 1>(p, u.G, s);

@@ -1,6 +1,7 @@
 """GPU: the tcgen05 3xTF32 grouped GEMM (k_umma.cu) against an f64 product.
 
-All four operand-major combinations the bank uses, aligned and ragged shapes
+All four operand-major combinations the bank uses, aligned and ragged shapes,
+both the 128x128 single-CTA kernel and the 256x256 CTA-pair kernel (M, N > 128)
 (K not a multiple of 32, M/N not multiples of 128), G > 1.  Tolerance
 1e-5 relative (max-abs / max-abs), the north_star per-kernel bound.
 """
@@ -17,7 +18,8 @@ def rel(a, b):
 
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 1), (0, 0), (1, 1), (1, 0)])
 @pytest.mark.parametrize("G,M,N,K", [(1, 128, 128, 32), (2, 256, 128, 784), (3, 200, 96, 76), (2, 136, 40, 20),
-                                     (2, 1024, 512, 1024), (1, 64, 256, 512)])
+                                     (2, 1024, 512, 1024), (1, 64, 256, 512),
+                                     (2, 384, 320, 100), (3, 300, 260, 64)])
 def test_umma_gemm(ctx, a_mn, b_mn, G, M, N, K):
     from paper_2011_09463_b200 import api
 
