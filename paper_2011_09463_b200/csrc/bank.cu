@@ -6,8 +6,7 @@
 //   backward: Tape::backward reverse sweep (tape.hpp:870-886)
 //   update  : optimizer_step SGD (optim.hpp:46-48)
 // as a fixed schedule of fused kernels (no device tape):
-//   [tc layer 0] split X into tf32 hi/lo planes
-//   per layer    FWD gemm (+bias, +ReLU)             -> H[l+1] (fp32 + hi/lo)
+//   per layer    FWD gemm (+bias, +ReLU)             -> H[l+1]
 //   head         CE (softmax, loss, dlogits)         -> dZ_{L-1}
 //   [mapping]    MMD beta, pairs, finish             -> lambda * dMMD/dH_{L-1}
 //   per layer    DX gemm (+inject, *ReLU mask) then DW gemm (+SGD) + bias SGD
@@ -15,10 +14,11 @@
 // their three GEMMs on the tcgen05 3xTF32 path (k_umma.cu); narrow layers
 // (the 10-class head, the 3-feature attack input) use the SIMT kernel.
 //
-// HBM layout per bank (row-major fp32):
-//   W[i]  [G, fan_in, fan_out] master + (tc) hi/lo planes;  b[i] [G, fan_out]
-//   H[l]  [G, B, dims[l]] post-ReLU activations + (tc) hi/lo planes
-//   dZ    two ping-pong [G, B, max dim] gradient buffers + hi/lo planes
+// HBM layout per bank (row-major fp32; the tensor-core kernels split
+// operands into tf32 hi/lo on chip, so nothing else is stored):
+//   W[i]  [G, fan_in, fan_out];  b[i] [G, fan_out]
+//   H[l]  [G, B, dims[l]] post-ReLU activations (ReLU mask = H > 0)
+//   dZ    two ping-pong [G, B, max dim] gradient buffers
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -133,9 +133,8 @@ struct mtk_bank {
         free_acts();
         const size_t GB = (size_t)G * B;
         H.assign(L, Plane3{});
-        for (int l = 1; l < L; ++l) alloc3(H[l], GB * dims[l], true, tc[l]);
-        alloc3(Xsp, GB * dims[0], false, tc[0]);
-        for (auto& z : dZ) alloc3(z, GB * maxd(), true, any_tc());
+        for (int l = 1; l < L; ++l) alloc3(H[l], GB * dims[l], true, false);
+        for (auto& z : dZ) alloc3(z, GB * maxd(), true, false);
         MTK_CUDA(cudaMalloc(&logits, GB * dims[L] * sizeof(float)));
         MTK_CUDA(cudaMalloc(&row_loss, GB * sizeof(double)));
         if (L > 1) MTK_CUDA(cudaMalloc(&gH, GB * dims[L - 1] * sizeof(float)));
@@ -177,19 +176,15 @@ void gemm_fwd(mtk_bank& k, int mat, const Plane3& in, int B, int r0, int rows, c
         u.N = fo;
         u.K = fi;
         u.a_mn = 0;
-        u.a_hi = in.hi + (size_t)r0 * fi;
-        u.a_lo = in.lo + (size_t)r0 * fi;
+        u.a = in.f + (size_t)r0 * fi;
         u.a_rs = fi;
         u.a_gs = (long long)B * fi;
         u.b_mn = 1;
-        u.b_hi = k.W[mat].hi;
-        u.b_lo = k.W[mat].lo;
+        u.b = k.W[mat].f;
         u.b_rs = fo;
         u.b_gs = (long long)fi * fo;
         u.epi = relu ? Epi::kBiasRelu : Epi::kBias;
         u.C = out.f + (size_t)r0 * fo;
-        u.C_hi = out.hi ? out.hi + (size_t)r0 * fo : nullptr;
-        u.C_lo = out.lo ? out.lo + (size_t)r0 * fo : nullptr;
         u.c_gs = (long long)B * fo;
         u.ldc = fo;
         u.bias = k.b[mat];
@@ -256,19 +251,15 @@ void gemm_dx(mtk_bank& k, int mat, const Plane3& dz, int B, int r0, int rows, co
         u.N = fi;
         u.K = fo;
         u.a_mn = 0;
-        u.a_hi = dz.hi + (size_t)r0 * fo;
-        u.a_lo = dz.lo + (size_t)r0 * fo;
+        u.a = dz.f + (size_t)r0 * fo;
         u.a_rs = fo;
         u.a_gs = (long long)B * fo;
         u.b_mn = 0;  // B(k=j, n=p) = W[p][j]: rows p, contiguous j
-        u.b_hi = k.W[mat].hi;
-        u.b_lo = k.W[mat].lo;
+        u.b = k.W[mat].f;
         u.b_rs = fo;
         u.b_gs = (long long)fi * fo;
         u.epi = Epi::kMask;
         u.C = out.f + (size_t)r0 * fi;
-        u.C_hi = out.hi ? out.hi + (size_t)r0 * fi : nullptr;
-        u.C_lo = out.lo ? out.lo + (size_t)r0 * fi : nullptr;
         u.c_gs = (long long)B * fi;
         u.ldc = fi;
         u.mask = mask + (size_t)r0 * fi;
@@ -314,19 +305,15 @@ void gemm_dw(mtk_bank& k, int mat, const Plane3& in, const Plane3& dz, int B, in
         u.N = fo;
         u.K = rows;
         u.a_mn = 1;  // A(m=p, k=r) = in[r][p]
-        u.a_hi = in.hi + (size_t)r0 * fi;
-        u.a_lo = in.lo + (size_t)r0 * fi;
+        u.a = in.f + (size_t)r0 * fi;
         u.a_rs = fi;
         u.a_gs = (long long)B * fi;
         u.b_mn = 1;  // B(k=r, n=j) = dz[r][j]
-        u.b_hi = dz.hi + (size_t)r0 * fo;
-        u.b_lo = dz.lo + (size_t)r0 * fo;
+        u.b = dz.f + (size_t)r0 * fo;
         u.b_rs = fo;
         u.b_gs = (long long)B * fo;
         u.epi = Epi::kSgd;
         u.C = k.W[mat].f;
-        u.C_hi = k.W[mat].hi;
-        u.C_lo = k.W[mat].lo;
         u.c_gs = (long long)fi * fo;
         u.ldc = fo;
         u.lr = lr;
@@ -389,13 +376,9 @@ void gemm_dw(mtk_bank& k, int mat, const Plane3& in, const Plane3& dz, int B, in
 }
 
 Plane3 input_plane(mtk_bank& k, const float* X, int B) {
-    Plane3 in = k.Xsp;
+    (void)B;
+    Plane3 in;
     in.f = const_cast<float*>(X);
-    if (k.tc[0]) {
-        PhaseScope ph(*k.ctx, kPhOther, 1);
-        launch_split(X, in.hi, in.lo, (long long)k.G * B * k.dims[0], k.ctx->stream);
-        after_launch(*k.ctx);
-    }
     return in;
 }
 
@@ -458,10 +441,6 @@ void train_step(mtk_bank& k, const mtk_step& s, double* loss_host, double* mmd_h
         PhaseScope ph(c, kPhCe, 2);
         launch_ce(ce, c.stream);
         after_launch(c, 2);
-        if (k.tc[L - 1]) {
-            launch_split(cur->f, cur->hi, cur->lo, (long long)k.G * B * k.dims[L], c.stream);
-            after_launch(c);
-        }
     }
 
     if (use_mmd) {
@@ -531,8 +510,7 @@ void train_step(mtk_bank& k, const mtk_step& s, double* loss_host, double* mmd_h
         const Plane3& in = l == 0 ? X : k.H[l];
         const float* add = (l == L - 1 && use_mmd) ? k.gH : nullptr;
         // the DX output feeds layer l-1: only write its tf32 planes if that layer is tc
-        Plane3 out = *nxt;
-        if (l > 0 && !k.tc[l - 1]) out.hi = out.lo = nullptr;
+        const Plane3 out = *nxt;
         const bool split = (l == L - 1 && two);
         if (need_dx) {
             PhaseScope ph(c, kPhDx, split ? 2 : 1);
@@ -630,7 +608,7 @@ int mtk_bank_create(mtk_ctx* c, int G, int n_layers, const int* dims, int n_head
         for (int i = 0; i < k->n_mats; ++i) {
             const size_t nw = (size_t)G * k->fan_in(i) * k->fan_out(i);
             Plane3 w;
-            alloc3(w, nw, true, k->tc[k->layer_of(i)]);
+            alloc3(w, nw, true, false);
             MTK_CUDA(cudaMemsetAsync(w.f, 0, nw * 4, c->stream));
             if (w.hi) {
                 MTK_CUDA(cudaMemsetAsync(w.hi, 0, nw * 4, c->stream));
@@ -674,7 +652,6 @@ int mtk_bank_set_params(mtk_bank* k, int model, const double* const* W, const do
             MTK_CUDA(cudaMemcpyAsync(k->b[i] + model * nbias, tmp.data(), nbias * 4,
                                      cudaMemcpyHostToDevice, k->ctx->stream));
             MTK_CUDA(cudaStreamSynchronize(k->ctx->stream));
-            k->split_param(i, model);
         }
         MTK_CUDA(cudaStreamSynchronize(k->ctx->stream));
     });

@@ -343,16 +343,6 @@ int mtk_diag_gemm_tf32x3(mtk_ctx* c, int a_mn, int b_mn, int G, int M, int N, in
     return guard([&] {
         need(c && A && B && Cm, MTK_VALUE_ERROR, "diag_gemm: null argument");
         need(G >= 1 && M >= 1 && N >= 1 && K >= 1, MTK_SHAPE_ERROR, "diag_gemm: zero dimension");
-        const size_t na = (size_t)G * M * K, nb = (size_t)G * K * N;
-        float* buf = nullptr;
-        MTK_CUDA(cudaMallocAsync(&buf, (2 * na + 2 * nb + 64) * sizeof(float), c->stream));
-        float* ahi = buf;
-        float* alo = ahi + na;
-        float* bhi = alo + na;
-        float* blo = bhi + nb;
-        launch_split(A, ahi, alo, (long long)na, c->stream);
-        launch_split(B, bhi, blo, (long long)nb, c->stream);
-        after_launch(*c, 2);
         UmmaGemm u;
         u.G = G;
         u.M = M;
@@ -360,12 +350,10 @@ int mtk_diag_gemm_tf32x3(mtk_ctx* c, int a_mn, int b_mn, int G, int M, int N, in
         u.K = K;
         u.a_mn = a_mn;
         u.b_mn = b_mn;
-        u.a_hi = ahi;
-        u.a_lo = alo;
+        u.a = A;
         u.a_rs = a_mn ? M : K;
         u.a_gs = (long long)M * K;
-        u.b_hi = bhi;
-        u.b_lo = blo;
+        u.b = B;
         u.b_rs = b_mn ? N : K;
         u.b_gs = (long long)K * N;
         u.epi = Epi::kStore;
@@ -373,10 +361,8 @@ int mtk_diag_gemm_tf32x3(mtk_ctx* c, int a_mn, int b_mn, int G, int M, int N, in
         u.c_gs = (long long)M * N;
         u.ldc = N;
         u.flags = c->d_flags;
-        if (getenv("MTK_UMMA_DEBUG")) u.dbg = reinterpret_cast<float*>(strtoull(getenv("MTK_UMMA_DEBUG"), nullptr, 0));
         launch_umma(u, c->stream);
         after_launch(*c);
-        MTK_CUDA(cudaFreeAsync(buf, c->stream));
         c->check_flags();
     });
 }

@@ -100,24 +100,19 @@ struct Gemm {
 
 void launch_gemm(const Gemm& g, cudaStream_t s);
 
-// tcgen05 3xTF32 grouped GEMM (k_umma.cu).  Operands are given as tf32 hi/lo
-// planes; element (r, c) of a plane sits at base[g*gs + r*rs + c], c being the
-// contiguous index: for a K-major operand r = m (or n) and c = k, for an
-// MN-major operand r = k and c = m (or n).  The epilogue writes C (fp32) and
-// its hi/lo split planes C_hi / C_lo (same layout as C).
+// tcgen05 3xTF32 grouped GEMM (k_umma.cu).  Operands are plain fp32; element
+// (r, c) sits at base[g*gs + r*rs + c], c being the contiguous index: for a
+// K-major operand r = m (or n) and c = k, for an MN-major operand r = k and
+// c = m (or n).  Row strides must be multiples of 4 elements (TMA).
 struct UmmaGemm {
     int G = 1, M = 0, N = 0, K = 0;
     int a_mn = 0, b_mn = 0;
-    const float* a_hi = nullptr;
-    const float* a_lo = nullptr;
+    const float* a = nullptr;
     long long a_rs = 0, a_gs = 0;
-    const float* b_hi = nullptr;
-    const float* b_lo = nullptr;
+    const float* b = nullptr;
     long long b_rs = 0, b_gs = 0;
     Epi epi = Epi::kStore;
     float* C = nullptr;
-    float* C_hi = nullptr;
-    float* C_lo = nullptr;
     long long c_gs = 0, ldc = 0;
     const float* bias = nullptr;
     long long bias_gs = 0;
@@ -126,7 +121,6 @@ struct UmmaGemm {
     float lr = 0.f;
     float* grad_out = nullptr;
     int* flags = nullptr;
-    float* dbg = nullptr;
 };
 void launch_umma(const UmmaGemm& u, cudaStream_t s);
 void launch_split(const float* x, float* hi, float* lo, long long n, cudaStream_t s);

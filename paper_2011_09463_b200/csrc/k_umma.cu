@@ -1,28 +1,34 @@
-// k_umma.cu -- grouped 3xTF32 GEMM on the 5th-gen tensor cores (tcgen05 +
-// TMEM + TMA), sm_100a.
+// k_umma.cu -- grouped fp32-accurate GEMM on the 5th-gen tensor cores
+// (tcgen05 + TMEM + TMA), sm_100a.
 //
-// C[g] (M x N) = A[g] (M x K) * B[g] (K x N) for G independent models, with
-// fp32-level accuracy from three tf32 products per k step:
-//     A*B ~= A_hi*B_hi + A_hi*B_lo + A_lo*B_hi        (A = A_hi + A_lo, tf32 parts)
-// The hi/lo planes live in HBM next to every fp32 tensor that feeds a GEMM
-// (weights, activations, gradients); producers write them in their epilogues.
+// C[g] (M x N) = A[g] (M x K) * B[g] (K x N) for G independent models.
+// Operands live in HBM as plain fp32 and are staged into smem by TMA.  The
+// tf32 MMA reads an fp32 operand by truncating its low 13 mantissa bits
+// (measured: tools/umma_probe.cu), so the staged fp32 tile IS the "hi" part;
+// converter warps derive the "lo" part on chip, lo = rna_tf32(x - trunc(x)),
+// and three MMAs per k step give fp32-level products (3xTF32):
+//     A*B ~= A*B_lo + A_lo*B + A*B          (A, B read as tf32 by the MMA)
+// HBM and L2 carry 4 bytes per operand element, as for an fp32 SIMT GEMM.
 //
 // Replaces, for the bank's dense layers, the reference loops
 //   detail::mm_acc (tape.hpp:36-48)    FWD: A = H   (K-major), B = W   (N-major)
 //   detail::mm_nt_acc (tape.hpp:50-63) DX:  A = dZ  (K-major), B = W^T (K-major)
 //   detail::mm_tn_acc (tape.hpp:65-78) DW:  A = H^T (M-major), B = dZ  (N-major)
-// Tile 128 x 128 x 32, 3-stage TMA -> smem ring (128-byte swizzle), one
-// elected thread issues tcgen05.mma into a 128x128 fp32 TMEM accumulator;
-// four epilogue warps drain TMEM with tcgen05.ld and apply the fused
-// epilogue (bias/ReLU, ReLU-mask, or SGD) writing fp32 + hi + lo planes.
+// One kernel template covers both tile schemes:
+//   PAIR = false  one CTA, 128 x 128 tile (small M or N)
+//   PAIR = true   CTA pair (cta_group::2), 256 x 256 tile: each CTA stages
+//                 128 rows of A and 128 columns of B; the leader issues
+//                 M=256, N=256 MMAs over both CTAs' smem.
+// Warp roles: w0 TMA producer, w1 MMA issuer (one elected thread), w2-w5
+// epilogue (TMEM -> registers -> fused bias/ReLU | ReLU-mask | SGD -> HBM),
+// w6-w13 lo-plane converters.  3-stage ring of 64 KB stages (128-B swizzle;
+// 32-B-atom swizzle for MN-major operands, the only layout tf32 accepts).
 #include <cuda.h>
 
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
-#include <map>
 #include <mutex>
-#include <tuple>
 
 #include "internal.h"
 #include "sm100.cuh"
@@ -32,20 +38,19 @@ namespace {
 
 using namespace sm100;
 
-constexpr int BM = 128, BN = 128, BK = 32, STAGES = 3;
-constexpr int TILE_BYTES = BM * BK * 4;             // 16 KB per operand plane
-constexpr int STAGE_BYTES = 4 * TILE_BYTES;         // A_hi, A_lo, B_hi, B_lo
+constexpr int BK = 32, STAGES = 3;
+constexpr int TILE_BYTES = 128 * BK * 4;     // 16 KB: 128 rows (or cols) x 32 k
+constexpr int STAGE_BYTES = 4 * TILE_BYTES;  // A fp32, A lo, B fp32, B lo
+constexpr int LOAD_BYTES = 2 * TILE_BYTES;   // what TMA brings per stage
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-constexpr int NUM_THREADS = 192;                    // warp0 TMA, warp1 MMA, warps2-5 epilogue
-constexpr uint32_t TMEM_COLS = 128;
+constexpr int NUM_CONV_WARPS = 8;
+constexpr int NUM_THREADS = 192 + 32 * NUM_CONV_WARPS;
 
 struct UmmaParams {
-    CUtensorMap a_hi, a_lo, b_hi, b_lo;  // 3-D maps, coords (inner, outer, g)
+    CUtensorMap a, b;  // 3-D fp32 maps, coords (inner, outer, g)
     int M, N, K;
-    int epi;                             // Epi value
+    int epi;           // Epi value
     float* C;
-    float* C_hi;
-    float* C_lo;
     long long c_gs, ldc;
     const float* bias;
     long long bias_gs;
@@ -54,317 +59,264 @@ struct UmmaParams {
     float lr;
     float* grad_out;
     int* flags;
-    float* dbg;  // diagnostics: receives stage-0 smem (64 KB) when non-null
+    unsigned long long* trace;  // diagnostics: timestamps of CTA (0,0,0)
 };
 
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// TMA for one operand tile of 128 (m or n) x 32 (k) into `dst`.
+//   K-major: one box (32 k, 128 rows).   MN-major: four boxes (32 mn, 32 k).
+template <int MN>
+__device__ __forceinline__ void load_operand(uint8_t* dst, const CUtensorMap* map, uint64_t* bar,
+                                             int r0, int k0, int g) {
+    if (MN) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) tma_load_3d(dst + j * 4096, map, bar, r0 + 32 * j, k0, g);
+    } else {
+        tma_load_3d(dst, map, bar, k0, r0, g);
+    }
+}
+
+// lo = rna_tf32(x - trunc_tf32(x)) over the two fp32 tiles of a stage.  The
+// transform is elementwise, so it ignores the swizzle: lo sits at the same
+// offset in its own tile.
+__device__ __forceinline__ void convert_stage(uint8_t* st, int t) {
+    constexpr int NT = 32 * NUM_CONV_WARPS;
+#pragma unroll
+    for (int j = 0; j < 2048 / NT; ++j) {
+        const int e = t + NT * j;                // float4 index within 2 tiles
+        const int tile = e >> 10, w = e & 1023;  // 1024 float4 per 16 KB tile
+        const float4* src = reinterpret_cast<const float4*>(st + tile * 2 * TILE_BYTES) + w;
+        float4* dst = reinterpret_cast<float4*>(st + tile * 2 * TILE_BYTES + TILE_BYTES) + w;
+        const float4 x = *src;
+        float4 l;
+        l.x = tf32_rna(x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u));
+        l.y = tf32_rna(x.y - __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u));
+        l.z = tf32_rna(x.z - __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u));
+        l.w = tf32_rna(x.w - __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u));
+        *dst = l;
+    }
+}
+
+// 3 MMAs per 8-wide k step over one stage
+template <int A_MN, int B_MN, bool PAIR>
+__device__ __forceinline__ void mma_stage(uint32_t tmem, uint32_t base, uint32_t idesc, bool first) {
+    constexpr uint32_t a_lbo = A_MN ? 4096 : 16, b_lbo = B_MN ? 4096 : 16;
+    constexpr uint32_t a_sbo = A_MN ? 512 : 1024, b_sbo = B_MN ? 512 : 1024;
+    constexpr uint32_t a_lay = A_MN ? 1 : 2, b_lay = B_MN ? 1 : 2;
+#pragma unroll
+    for (int kk = 0; kk < BK / 8; ++kk) {
+        // K-major: +32 B per 8-element k step inside the 128-B swizzle row
+        // MN-major: +1024 B per 8 k rows (two 32-B-atom swizzle atoms)
+        const uint32_t aoff = A_MN ? kk * 1024 : kk * 32;
+        const uint32_t boff = B_MN ? kk * 1024 : kk * 32;
+        const uint64_t a32 = smem_desc(base + aoff, a_lbo, a_sbo, a_lay);
+        const uint64_t alo = smem_desc(base + TILE_BYTES + aoff, a_lbo, a_sbo, a_lay);
+        const uint64_t b32 = smem_desc(base + 2 * TILE_BYTES + boff, b_lbo, b_sbo, b_lay);
+        const uint64_t blo = smem_desc(base + 3 * TILE_BYTES + boff, b_lbo, b_sbo, b_lay);
+        const uint32_t acc0 = (first && kk == 0) ? 0u : 1u;
+        if (PAIR) {
+            mma_tf32_2sm(tmem, a32, blo, idesc, acc0);
+            mma_tf32_2sm(tmem, alo, b32, idesc, 1u);
+            mma_tf32_2sm(tmem, a32, b32, idesc, 1u);
+        } else {
+            mma_tf32(tmem, a32, blo, idesc, acc0);
+            mma_tf32(tmem, alo, b32, idesc, 1u);
+            mma_tf32(tmem, a32, b32, idesc, 1u);
+        }
+    }
+}
+
 // TMEM accumulator (this warp's 32 lanes = rows m0+32q.., ncols columns) ->
-// fused epilogue -> fp32 + tf32 hi/lo planes in HBM.
+// fused epilogue -> fp32 C in HBM.  Each thread owns one row.
 __device__ __forceinline__ void epilogue_rows(const UmmaParams& p, uint32_t tmem, int q, int lane,
                                               int g, int m0, int n0, int ncols) {
-        const int m = m0 + 32 * q + lane;
-        const bool row_ok = m < p.M;
-        const long long rowbase = (long long)g * p.c_gs + (long long)m * p.ldc;
-        bool bad = false;
+    const int m = m0 + 32 * q + lane;
+    const bool row_ok = m < p.M;
+    const long long rowbase = (long long)g * p.c_gs + (long long)m * p.ldc;
+    bool bad = false;
 #pragma unroll 1
-        for (int c = 0; c < ncols / 32; ++c) {
-            float v[32];
-            tmem_ld_32x32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(c * 32), v);
-            const int nb = n0 + c * 32;
-            if (!row_ok || nb >= p.N) continue;
-            float xs[32];
+    for (int c = 0; c < ncols / 32; ++c) {
+        float v[32];
+        tmem_ld_32x32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(c * 32), v);
+        const int nb = n0 + c * 32;
+        if (!row_ok || nb >= p.N) continue;
+        const bool vec = (nb + 32 <= p.N) && ((rowbase + nb) % 4 == 0);
+        if (vec) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
+            for (int j = 0; j < 32; j += 4) {
+                const long long idx = rowbase + nb + j;
+                float4 x = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                if (p.epi == (int)Epi::kBias || p.epi == (int)Epi::kBiasRelu) {
+                    const float* bp = p.bias + g * p.bias_gs + nb + j;
+                    x.x += bp[0];
+                    x.y += bp[1];
+                    x.z += bp[2];
+                    x.w += bp[3];
+                    bad |= !(isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w));
+                    if (p.epi == (int)Epi::kBiasRelu) {
+                        x.x = x.x > 0.f ? x.x : 0.f;
+                        x.y = x.y > 0.f ? x.y : 0.f;
+                        x.z = x.z > 0.f ? x.z : 0.f;
+                        x.w = x.w > 0.f ? x.w : 0.f;
+                    }
+                } else if (p.epi == (int)Epi::kMask) {
+                    if (p.add) {
+                        const float4 a = *reinterpret_cast<const float4*>(p.add + idx);
+                        x.x = a.x + x.x;
+                        x.y = a.y + x.y;
+                        x.z = a.z + x.z;
+                        x.w = a.w + x.w;
+                    }
+                    const float4 mk = *reinterpret_cast<const float4*>(p.mask + idx);
+                    x.x = mk.x > 0.f ? x.x : 0.f;
+                    x.y = mk.y > 0.f ? x.y : 0.f;
+                    x.z = mk.z > 0.f ? x.z : 0.f;
+                    x.w = mk.w > 0.f ? x.w : 0.f;
+                } else if (p.epi == (int)Epi::kSgd) {  // C is the fp32 master weight
+                    if (p.grad_out) *reinterpret_cast<float4*>(p.grad_out + idx) = x;
+                    const float4 w = *reinterpret_cast<const float4*>(p.C + idx);
+                    x.x = w.x - p.lr * x.x;
+                    x.y = w.y - p.lr * x.y;
+                    x.z = w.z - p.lr * x.z;
+                    x.w = w.w - p.lr * x.w;
+                    bad |= !(isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w));
+                }
+                *reinterpret_cast<float4*>(p.C + idx) = x;
+            }
+        } else {
+            for (int j = 0; j < 32 && nb + j < p.N; ++j) {
                 const int n = nb + j;
                 const long long idx = rowbase + n;
                 float x = v[j];
-                if (n < p.N) {
-                    if (p.epi == (int)Epi::kBias || p.epi == (int)Epi::kBiasRelu) {
-                        x += p.bias[g * p.bias_gs + n];
-                        bad |= !isfinite(x);
-                        if (p.epi == (int)Epi::kBiasRelu) x = x > 0.f ? x : 0.f;
-                    } else if (p.epi == (int)Epi::kMask) {
-                        if (p.add) x = p.add[idx] + x;
-                        x = (p.mask[idx] > 0.f) ? x : 0.f;
-                    } else if (p.epi == (int)Epi::kSgd) {  // C is the fp32 master weight
-                        if (p.grad_out) p.grad_out[idx] = x;
-                        x = p.C[idx] - p.lr * x;
-                        bad |= !isfinite(x);
-                    }
+                if (p.epi == (int)Epi::kBias || p.epi == (int)Epi::kBiasRelu) {
+                    x += p.bias[g * p.bias_gs + n];
+                    bad |= !isfinite(x);
+                    if (p.epi == (int)Epi::kBiasRelu) x = x > 0.f ? x : 0.f;
+                } else if (p.epi == (int)Epi::kMask) {
+                    if (p.add) x = p.add[idx] + x;
+                    x = (p.mask[idx] > 0.f) ? x : 0.f;
+                } else if (p.epi == (int)Epi::kSgd) {
+                    if (p.grad_out) p.grad_out[idx] = x;
+                    x = p.C[idx] - p.lr * x;
+                    bad |= !isfinite(x);
                 }
-                xs[j] = x;
-            }
-            const bool vec = (nb + 32 <= p.N) && ((rowbase + nb) % 4 == 0);
-            if (vec) {
-#pragma unroll
-                for (int j = 0; j < 32; j += 4) {
-                    float4 x4 = make_float4(xs[j], xs[j + 1], xs[j + 2], xs[j + 3]);
-                    float4 h4, l4;
-                    split_tf32(x4.x, h4.x, l4.x);
-                    split_tf32(x4.y, h4.y, l4.y);
-                    split_tf32(x4.z, h4.z, l4.z);
-                    split_tf32(x4.w, h4.w, l4.w);
-                    *reinterpret_cast<float4*>(p.C + rowbase + nb + j) = x4;
-                    if (p.C_hi) {
-                        *reinterpret_cast<float4*>(p.C_hi + rowbase + nb + j) = h4;
-                        *reinterpret_cast<float4*>(p.C_lo + rowbase + nb + j) = l4;
-                    }
-                }
-            } else {
-                for (int j = 0; j < 32 && nb + j < p.N; ++j) {
-                    const long long idx = rowbase + nb + j;
-                    float hi, lo;
-                    split_tf32(xs[j], hi, lo);
-                    p.C[idx] = xs[j];
-                    if (p.C_hi) {
-                        p.C_hi[idx] = hi;
-                        p.C_lo[idx] = lo;
-                    }
-                }
+                p.C[idx] = x;
             }
         }
-        if (bad && p.flags) atomicOr(p.flags, kFlagNonFinite);
+    }
+    if (bad && p.flags) atomicOr(p.flags, kFlagNonFinite);
 }
 
-template <int A_MN, int B_MN>
-__global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_constant__ UmmaParams p) {
+template <int A_MN, int B_MN, bool PAIR>
+__global__ void __launch_bounds__(NUM_THREADS, 1) umma_kernel(const __grid_constant__ UmmaParams p) {
+    constexpr int TN = PAIR ? 256 : 128;  // accumulator columns per CTA
+    constexpr uint32_t TMEM_COLS = PAIR ? 256 : 128;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-    uint64_t* empty = full + STAGES;
+    uint64_t* conv = full + STAGES;
+    uint64_t* empty = conv + STAGES;
     uint64_t* tmem_full = empty + STAGES;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = PAIR ? cluster_rank() : 0;
     const int g = blockIdx.z;
-    const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+    const int m0 = PAIR ? (int)(blockIdx.x >> 1) * 256 + (int)rank * 128 : (int)blockIdx.x * 128;
+    const int n0 = blockIdx.y * TN;        // accumulator columns (the pair's)
+    const int nb0 = n0 + (int)rank * 128;  // B columns staged by this CTA
     const int nk = (p.K + BK - 1) / BK;
+    unsigned long long* tr =
+        (p.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) ? p.trace : nullptr;
 
     if (warp == 0 && lane == 0) {
-        tma_prefetch(&p.a_hi);
-        tma_prefetch(&p.a_lo);
-        tma_prefetch(&p.b_hi);
-        tma_prefetch(&p.b_lo);
+        tma_prefetch(&p.a);
+        tma_prefetch(&p.b);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
+            mbar_init(&conv[s], (PAIR ? 2 : 1) * NUM_CONV_WARPS);  // one arrival per converter warp
             mbar_init(&empty[s], 1);
         }
         mbar_init(tmem_full, 1);
         fence_barrier_init();
     }
-    if (warp == 1) tmem_alloc<TMEM_COLS>(tmem_slot);
+    if (warp == 1) {
+        if (PAIR) tmem_alloc_2sm<TMEM_COLS>(tmem_slot);
+        else tmem_alloc<TMEM_COLS>(tmem_slot);
+    }
     tc_fence_before();
-    __syncthreads();
+    if (PAIR) cluster_sync();
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    if (tr && threadIdx.x == 0) tr[2002] = gtime();
 
     if (warp == 0) {
         if (lane == 0) {
             // ---------------- TMA producer ----------------
             for (int kb = 0; kb < nk; ++kb) {
                 const int s = kb % STAGES;
-                const uint32_t ph = (kb / STAGES) & 1;
-                mbar_wait(&empty[s], ph ^ 1);
+                mbar_wait(&empty[s], ((kb / STAGES) & 1) ^ 1);
+                if (tr && kb < 1000) tr[kb] = gtime();
                 uint8_t* st = smem + s * STAGE_BYTES;
-                mbar_expect_tx(&full[s], STAGE_BYTES);
-                const int k0 = kb * BK;
-                if (A_MN) {  // A(m,k) with m contiguous: 4 boxes of 32(m) x 32(k)
-#pragma unroll
-                    for (int j = 0; j < BM / 32; ++j) {
-                        tma_load_3d(st + j * 4096, &p.a_hi, &full[s], m0 + 32 * j, k0, g);
-                        tma_load_3d(st + TILE_BYTES + j * 4096, &p.a_lo, &full[s], m0 + 32 * j, k0, g);
-                    }
-                } else {     // A(m,k) with k contiguous: one box 32(k) x 128(m)
-                    tma_load_3d(st, &p.a_hi, &full[s], k0, m0, g);
-                    tma_load_3d(st + TILE_BYTES, &p.a_lo, &full[s], k0, m0, g);
-                }
-                uint8_t* sb = st + 2 * TILE_BYTES;
-                if (B_MN) {  // B(k,n) with n contiguous: 4 boxes of 32(n) x 32(k)
-#pragma unroll
-                    for (int j = 0; j < BN / 32; ++j) {
-                        tma_load_3d(sb + j * 4096, &p.b_hi, &full[s], n0 + 32 * j, k0, g);
-                        tma_load_3d(sb + TILE_BYTES + j * 4096, &p.b_lo, &full[s], n0 + 32 * j, k0, g);
-                    }
-                } else {     // B(k,n) with k contiguous: one box 32(k) x 128(n)
-                    tma_load_3d(sb, &p.b_hi, &full[s], k0, n0, g);
-                    tma_load_3d(sb + TILE_BYTES, &p.b_lo, &full[s], k0, n0, g);
-                }
-            }
-        }
-    } else if (warp == 1) {
-        // ---------------- MMA issuer (one thread) ----------------
-        constexpr uint32_t idesc = idesc_tf32(BM, BN, A_MN, B_MN);
-        if (lane == 0) {
-            for (int kb = 0; kb < nk; ++kb) {
-                const int s = kb % STAGES;
-                const uint32_t ph = (kb / STAGES) & 1;
-                mbar_wait(&full[s], ph);
-                tc_fence_after();
-                const uint32_t base = smem_u32(smem + s * STAGE_BYTES);
-#pragma unroll
-                for (int kk = 0; kk < BK / 8; ++kk) {
-                    // K-major: +32 B per 8-element k step inside the 128-B swizzle row
-                    // MN-major: +1024 B per 8 k rows (one swizzle atom)
-                    const uint32_t aoff = A_MN ? kk * 1024 : kk * 32;
-                    const uint32_t boff = B_MN ? kk * 1024 : kk * 32;
-                    // K-major: SW128, SBO = 8 rows x 128 B.  MN-major: SW128 with
-                    // 32-B atoms, LBO = 4 KB between 32-element MN boxes, SBO = 4 k
-                    // rows x 128 B.
-                    constexpr uint32_t a_lbo = A_MN ? 4096 : 16, b_lbo = B_MN ? 4096 : 16;
-                    constexpr uint32_t a_sbo = A_MN ? 512 : 1024, b_sbo = B_MN ? 512 : 1024;
-                    constexpr uint32_t a_lay = A_MN ? 1 : 2, b_lay = B_MN ? 1 : 2;
-                    const uint64_t ahi = smem_desc(base + aoff, a_lbo, a_sbo, a_lay);
-                    const uint64_t alo = smem_desc(base + TILE_BYTES + aoff, a_lbo, a_sbo, a_lay);
-                    const uint64_t bhi = smem_desc(base + 2 * TILE_BYTES + boff, b_lbo, b_sbo, b_lay);
-                    const uint64_t blo = smem_desc(base + 3 * TILE_BYTES + boff, b_lbo, b_sbo, b_lay);
-                    const uint32_t acc0 = (kb | kk) ? 1u : 0u;
-                    mma_tf32(tmem, alo, bhi, idesc, acc0);
-                    mma_tf32(tmem, ahi, blo, idesc, 1u);
-                    mma_tf32(tmem, ahi, bhi, idesc, 1u);
-                }
-                mma_commit(&empty[s]);  // frees the smem slot when these MMAs retire
-            }
-            mma_commit(tmem_full);
-        }
-    } else {
-        // ---------------- epilogue: TMEM -> registers -> HBM ----------------
-        const int q = warp & 3;  // TMEM lane quarter this warp may access
-        mbar_wait(tmem_full, 0);
-        tc_fence_after();
-        epilogue_rows(p, tmem, q, lane, g, m0, n0, BN);
-        if (p.dbg) {
-            const float* sf = reinterpret_cast<const float*>(smem);
-            for (int i = threadIdx.x - 64; i < STAGE_BYTES / 4; i += 128) p.dbg[i] = sf[i];
-        }
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 1) {
-        tc_fence_after();
-        tmem_dealloc<TMEM_COLS>(tmem);
-    }
-}
-
-// ---------------------------------------------------------------------------
-// CTA-pair variant (cta_group::2): a 2-CTA cluster computes a 256 x 256 tile.
-// Each CTA stages its 128 rows of A and its 128 columns of B (hi/lo planes);
-// the leader (rank 0) issues tcgen05.mma.cta_group::2 with M = 256, N = 256,
-// reading both CTAs' smem; each CTA's TMEM receives its 128 rows x 256 cols.
-// Per SM this halves operand bytes per MAC versus the 128 x 128 kernel.
-constexpr int BN2 = 256;
-constexpr uint32_t TMEM_COLS2 = 256;
-
-template <int A_MN, int B_MN>
-__global__ void __launch_bounds__(NUM_THREADS, 1) umma2_gemm_kernel(const __grid_constant__ UmmaParams p) {
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-    uint64_t* empty = full + STAGES;
-    uint64_t* tmem_full = empty + STAGES;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t rank = cluster_rank();
-    const int g = blockIdx.z;
-    const int m0 = (blockIdx.x >> 1) * 256 + (int)rank * 128;  // this CTA's rows
-    const int n0 = blockIdx.y * BN2;                            // the pair's columns
-    const int nb0 = n0 + (int)rank * 128;                       // this CTA's B half
-    const int nk = (p.K + BK - 1) / BK;
-
-    if (warp == 0 && lane == 0) {
-        tma_prefetch(&p.a_hi);
-        tma_prefetch(&p.a_lo);
-        tma_prefetch(&p.b_hi);
-        tma_prefetch(&p.b_lo);
-        for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 2);   // one arrival per CTA of the pair (leader's copy used)
-            mbar_init(&empty[s], 1);
-        }
-        mbar_init(tmem_full, 1);
-        fence_barrier_init();
-    }
-    if (warp == 1) tmem_alloc_2sm<TMEM_COLS2>(tmem_slot);
-    tc_fence_before();
-    cluster_sync();
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-
-    if (warp == 0) {
-        if (lane == 0) {
-            // ---------------- TMA producer (both CTAs) ----------------
-            for (int kb = 0; kb < nk; ++kb) {
-                const int s = kb % STAGES;
-                const uint32_t ph = (kb / STAGES) & 1;
-                mbar_wait(&empty[s], ph ^ 1);
-                uint8_t* st = smem + s * STAGE_BYTES;
-                const int k0 = kb * BK;
-                if (A_MN) {
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        tma_load_3d_2sm(st + j * 4096, &p.a_hi, &full[s], m0 + 32 * j, k0, g);
-                        tma_load_3d_2sm(st + TILE_BYTES + j * 4096, &p.a_lo, &full[s], m0 + 32 * j, k0, g);
-                    }
-                } else {
-                    tma_load_3d_2sm(st, &p.a_hi, &full[s], k0, m0, g);
-                    tma_load_3d_2sm(st + TILE_BYTES, &p.a_lo, &full[s], k0, m0, g);
-                }
-                uint8_t* sb = st + 2 * TILE_BYTES;
-                if (B_MN) {
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        tma_load_3d_2sm(sb + j * 4096, &p.b_hi, &full[s], nb0 + 32 * j, k0, g);
-                        tma_load_3d_2sm(sb + TILE_BYTES + j * 4096, &p.b_lo, &full[s], nb0 + 32 * j, k0, g);
-                    }
-                } else {
-                    tma_load_3d_2sm(sb, &p.b_hi, &full[s], k0, nb0, g);
-                    tma_load_3d_2sm(sb + TILE_BYTES, &p.b_lo, &full[s], k0, nb0, g);
-                }
-                // the leader expects both CTAs' bytes; the follower only arrives
-                if (rank == 0) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
-                else mbar_arrive_remote(&full[s], 0);
+                mbar_expect_tx(&full[s], LOAD_BYTES);
+                load_operand<A_MN>(st, &p.a, &full[s], m0, kb * BK, g);
+                load_operand<B_MN>(st + 2 * TILE_BYTES, &p.b, &full[s], nb0, kb * BK, g);
             }
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer (leader CTA, one thread) ----------------
-        constexpr uint32_t idesc = idesc_tf32(256, BN2, A_MN, B_MN);
+        constexpr uint32_t idesc = idesc_tf32(PAIR ? 256 : 128, TN, A_MN, B_MN);
         if (rank == 0 && lane == 0) {
             for (int kb = 0; kb < nk; ++kb) {
                 const int s = kb % STAGES;
-                const uint32_t ph = (kb / STAGES) & 1;
-                mbar_wait(&full[s], ph);
+                mbar_wait(&conv[s], (kb / STAGES) & 1);
+                if (tr && kb < 1000) tr[1000 + kb] = gtime();
                 tc_fence_after();
-                const uint32_t base = smem_u32(smem + s * STAGE_BYTES);
-#pragma unroll
-                for (int kk = 0; kk < BK / 8; ++kk) {
-                    const uint32_t aoff = A_MN ? kk * 1024 : kk * 32;
-                    const uint32_t boff = B_MN ? kk * 1024 : kk * 32;
-                    constexpr uint32_t a_lbo = A_MN ? 4096 : 16, b_lbo = B_MN ? 4096 : 16;
-                    constexpr uint32_t a_sbo = A_MN ? 512 : 1024, b_sbo = B_MN ? 512 : 1024;
-                    constexpr uint32_t a_lay = A_MN ? 1 : 2, b_lay = B_MN ? 1 : 2;
-                    const uint64_t ahi = smem_desc(base + aoff, a_lbo, a_sbo, a_lay);
-                    const uint64_t alo = smem_desc(base + TILE_BYTES + aoff, a_lbo, a_sbo, a_lay);
-                    const uint64_t bhi = smem_desc(base + 2 * TILE_BYTES + boff, b_lbo, b_sbo, b_lay);
-                    const uint64_t blo = smem_desc(base + 3 * TILE_BYTES + boff, b_lbo, b_sbo, b_lay);
-                    const uint32_t acc0 = (kb | kk) ? 1u : 0u;
-                    mma_tf32_2sm(tmem, alo, bhi, idesc, acc0);
-                    mma_tf32_2sm(tmem, ahi, blo, idesc, 1u);
-                    mma_tf32_2sm(tmem, ahi, bhi, idesc, 1u);
-                }
-                mma_commit_2sm(&empty[s], 0x3);  // frees this slot in both CTAs
+                mma_stage<A_MN, B_MN, PAIR>(tmem, smem_u32(smem + s * STAGE_BYTES), idesc, kb == 0);
+                if (PAIR) mma_commit_2sm(&empty[s], 0x3);  // frees the slot in both CTAs
+                else mma_commit(&empty[s]);
             }
-            mma_commit_2sm(tmem_full, 0x3);
+            if (PAIR) mma_commit_2sm(tmem_full, 0x3);
+            else mma_commit(tmem_full);
         }
-    } else {
-        // ---------------- epilogue (both CTAs: own 128 rows x 256 cols) ----------------
-        const int q = warp & 3;
+    } else if (warp < 6) {
+        // ---------------- epilogue: own 128 rows x TN columns ----------------
+        const int q = warp & 3;  // TMEM lane quarter this warp may access
         mbar_wait(tmem_full, 0);
+        if (tr && threadIdx.x == 64) tr[2000] = gtime();
         tc_fence_after();
-        epilogue_rows(p, tmem, q, lane, g, m0, n0, BN2);
+        epilogue_rows(p, tmem, q, lane, g, m0, n0, TN);
+        if (tr && threadIdx.x == 64) tr[2001] = gtime();
+    } else {
+        // ---------------- lo-plane converters ----------------
+        const int t = threadIdx.x - 192;
+        for (int kb = 0; kb < nk; ++kb) {
+            const int s = kb % STAGES;
+            mbar_wait(&full[s], (kb / STAGES) & 1);
+            if (tr && t == 0 && kb < 1000) tr[3000 + kb] = gtime();
+            convert_stage(smem + s * STAGE_BYTES, t);
+            fence_proxy_async_smem();  // generic-proxy stores -> tensor-core reads
+            __syncwarp();
+            if (tr && t == 0 && kb < 1000) tr[4000 + kb] = gtime();
+            if (lane == 0) {
+                if (PAIR) mbar_arrive_remote(&conv[s], 0);
+                else mbar_arrive(&conv[s]);
+            }
+        }
     }
     tc_fence_before();
-    cluster_sync();
+    if (PAIR) cluster_sync();
+    else __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc_2sm<TMEM_COLS2>(tmem);
+        if (PAIR) tmem_dealloc_2sm<TMEM_COLS>(tmem);
+        else tmem_dealloc<TMEM_COLS>(tmem);
     }
 }
 
@@ -419,47 +371,42 @@ CUtensorMap make_map(const float* base, long long inner, long long outer, long l
     CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims,
                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                            mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
-                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) fail(MTK_ERROR, "cuTensorMapEncodeTiled failed");
     return m;
 }
 
-template <int A_MN, int B_MN>
+template <int A_MN, int B_MN, bool PAIR>
 void launch_variant(const UmmaParams& p, int G, cudaStream_t s) {
     static bool attr = false;
     if (!attr) {
-        MTK_CUDA(cudaFuncSetAttribute(umma_gemm_kernel<A_MN, B_MN>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-        attr = true;
-    }
-    dim3 grid((p.N + BN - 1) / BN, (p.M + BM - 1) / BM, G);
-    umma_gemm_kernel<A_MN, B_MN><<<grid, NUM_THREADS, SMEM_BYTES, s>>>(p);
-    count_launch();
-}
-
-template <int A_MN, int B_MN>
-void launch_variant2(const UmmaParams& p, int G, cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
-        MTK_CUDA(cudaFuncSetAttribute(umma2_gemm_kernel<A_MN, B_MN>,
+        MTK_CUDA(cudaFuncSetAttribute(umma_kernel<A_MN, B_MN, PAIR>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
         attr = true;
     }
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(2 * ((p.M + 255) / 256), (p.N + BN2 - 1) / BN2, G);
+    cfg.gridDim = PAIR ? dim3(2 * ((p.M + 255) / 256), (p.N + 255) / 256, G)
+                       : dim3((p.M + 127) / 128, (p.N + 127) / 128, G);
     cfg.blockDim = dim3(NUM_THREADS);
     cfg.dynamicSmemBytes = SMEM_BYTES;
     cfg.stream = s;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.x = PAIR ? 2 : 1;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    MTK_CUDA(cudaLaunchKernelEx(&cfg, umma2_gemm_kernel<A_MN, B_MN>, p));
+    MTK_CUDA(cudaLaunchKernelEx(&cfg, umma_kernel<A_MN, B_MN, PAIR>, p));
     count_launch();
+}
+
+template <bool PAIR>
+void dispatch(const UmmaParams& p, int a_mn, int b_mn, int G, cudaStream_t s) {
+    if (!a_mn && b_mn) launch_variant<0, 1, PAIR>(p, G, s);
+    else if (!a_mn && !b_mn) launch_variant<0, 0, PAIR>(p, G, s);
+    else if (a_mn && b_mn) launch_variant<1, 1, PAIR>(p, G, s);
+    else launch_variant<1, 0, PAIR>(p, G, s);
 }
 
 bool use_pair_kernel(const UmmaGemm& u) {
@@ -483,34 +430,23 @@ void launch_split(const float* x, float* hi, float* lo, long long n, cudaStream_
     count_launch();
 }
 
-// Operand views: each operand is given as (hi, lo) planes with element
-// (r, c) at base[g*gs + r*rs + c] where c is the contiguous index.
+// Operand views: element (r, c) of an operand sits at base[g*gs + r*rs + c],
+// c the contiguous index (K-major: r = m or n, c = k; MN-major: r = k).
 void launch_umma(const UmmaGemm& u, cudaStream_t s) {
     if (u.M <= 0 || u.N <= 0 || u.G <= 0 || u.K <= 0) return;
+    const bool pair = use_pair_kernel(u);
     UmmaParams p;
     std::memset(&p, 0, sizeof(p));
     // A: K-major -> inner = K, outer = M ; MN-major -> inner = M, outer = K
-    if (u.a_mn) {
-        p.a_hi = make_map(u.a_hi, u.M, u.K, u.G, u.a_rs, u.a_gs, BK, true);
-        p.a_lo = make_map(u.a_lo, u.M, u.K, u.G, u.a_rs, u.a_gs, BK, true);
-    } else {
-        p.a_hi = make_map(u.a_hi, u.K, u.M, u.G, u.a_rs, u.a_gs, BM, false);
-        p.a_lo = make_map(u.a_lo, u.K, u.M, u.G, u.a_rs, u.a_gs, BM, false);
-    }
-    if (u.b_mn) {
-        p.b_hi = make_map(u.b_hi, u.N, u.K, u.G, u.b_rs, u.b_gs, BK, true);
-        p.b_lo = make_map(u.b_lo, u.N, u.K, u.G, u.b_rs, u.b_gs, BK, true);
-    } else {
-        p.b_hi = make_map(u.b_hi, u.K, u.N, u.G, u.b_rs, u.b_gs, BN, false);
-        p.b_lo = make_map(u.b_lo, u.K, u.N, u.G, u.b_rs, u.b_gs, BN, false);
-    }
+    p.a = u.a_mn ? make_map(u.a, u.M, u.K, u.G, u.a_rs, u.a_gs, BK, true)
+                 : make_map(u.a, u.K, u.M, u.G, u.a_rs, u.a_gs, 128, false);
+    p.b = u.b_mn ? make_map(u.b, u.N, u.K, u.G, u.b_rs, u.b_gs, BK, true)
+                 : make_map(u.b, u.K, u.N, u.G, u.b_rs, u.b_gs, 128, false);
     p.M = u.M;
     p.N = u.N;
     p.K = u.K;
     p.epi = (int)u.epi;
     p.C = u.C;
-    p.C_hi = u.C_hi;
-    p.C_lo = u.C_lo;
     p.c_gs = u.c_gs;
     p.ldc = u.ldc;
     p.bias = u.bias;
@@ -520,18 +456,10 @@ void launch_umma(const UmmaGemm& u, cudaStream_t s) {
     p.lr = u.lr;
     p.grad_out = u.grad_out;
     p.flags = u.flags;
-    p.dbg = u.dbg;
-    if (use_pair_kernel(u)) {
-        if (!u.a_mn && u.b_mn) launch_variant2<0, 1>(p, u.G, s);
-        else if (!u.a_mn && !u.b_mn) launch_variant2<0, 0>(p, u.G, s);
-        else if (u.a_mn && u.b_mn) launch_variant2<1, 1>(p, u.G, s);
-        else launch_variant2<1, 0>(p, u.G, s);
-        return;
-    }
-    if (!u.a_mn && u.b_mn) launch_variant<0, 1>(p, u.G, s);
-    else if (!u.a_mn && !u.b_mn) launch_variant<0, 0>(p, u.G, s);
-    else if (u.a_mn && u.b_mn) launch_variant<1, 1>(p, u.G, s);
-    else launch_variant<1, 0>(p, u.G, s);
+    if (const char* t = getenv("MTK_UMMA_TRACE"))
+        p.trace = reinterpret_cast<unsigned long long*>(strtoull(t, nullptr, 0));
+    if (pair) dispatch<true>(p, u.a_mn, u.b_mn, u.G, s);
+    else dispatch<false>(p, u.a_mn, u.b_mn, u.G, s);
 }
 
 }  // namespace mtk

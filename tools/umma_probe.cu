@@ -5,6 +5,8 @@
 #include <cstdlib>
 #include <cmath>
 #include <vector>
+#include <cstring>
+#include <algorithm>
 
 #include "sm100.cuh"
 
@@ -22,9 +24,9 @@ __global__ void probe(const float* A, const float* B, float* C, int mode) {
         const int r = i / 32, k = i % 32, c = k / 4, w = k % 4;
         const int pos = r * 32 + ((c ^ (r & 7)) * 4) + w;
         float a = A[i], b = B[i];
-        if (mode >= 10) {  // no swizzle: plain row-major (wrong on purpose: sanity)
-            sA[i] = a;
-            sB[i] = b;
+        if (mode == 2) {  // raw fp32 bits: what does the tf32 MMA do with the low 13 bits?
+            sA[pos] = a;
+            sB[pos] = b;
         } else {
             sA[pos] = tf32_rna(a);
             sB[pos] = tf32_rna(b);
@@ -70,20 +72,26 @@ __global__ void probe(const float* A, const float* B, float* C, int mode) {
 int main() {
     std::vector<float> A(128 * 32), B(128 * 32), C(128 * 128);
     for (int i = 0; i < 128 * 32; ++i) {
-        A[i] = (float)((i * 7) % 13) - 6.f;
-        B[i] = (float)((i * 5) % 11) - 5.f;
+        A[i] = 1.0f + (float)((i * 7919) % 8191) / 8192.0f * 0.999f;   // low mantissa bits set
+        B[i] = 1.0f + (float)((i * 104729) % 8191) / 8192.0f * 0.999f;
     }
-    std::vector<double> ref(128 * 128, 0.0);
+    auto trunc = [](float x) { uint32_t u; memcpy(&u, &x, 4); u &= 0xFFFFE000u; float y; memcpy(&y, &u, 4); return (double)y; };
+    auto rna = [](float x) { uint32_t u; memcpy(&u, &x, 4); u = (u + 0x1000u) & 0xFFFFE000u; float y; memcpy(&y, &u, 4); return (double)y; };
+    std::vector<double> ref(128 * 128, 0.0), rt(128 * 128, 0.0), rr(128 * 128, 0.0);
     for (int m = 0; m < 128; ++m)
         for (int n = 0; n < 128; ++n)
-            for (int k = 0; k < 32; ++k) ref[m * 128 + n] += (double)A[m * 32 + k] * B[n * 32 + k];
+            for (int k = 0; k < 32; ++k) {
+                ref[m * 128 + n] += (double)A[m * 32 + k] * B[n * 32 + k];
+                rt[m * 128 + n] += trunc(A[m * 32 + k]) * trunc(B[n * 32 + k]);
+                rr[m * 128 + n] += rna(A[m * 32 + k]) * rna(B[n * 32 + k]);
+            }
     float *dA, *dB, *dC;
     cudaMalloc(&dA, A.size() * 4);
     cudaMalloc(&dB, B.size() * 4);
     cudaMalloc(&dC, C.size() * 4);
     cudaMemcpy(dA, A.data(), A.size() * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(dB, B.data(), B.size() * 4, cudaMemcpyHostToDevice);
-    for (int mode : {0, 1}) {
+    for (int mode : {0, 2}) {
         cudaMemset(dC, 0, C.size() * 4);
         probe<<<1, 128>>>(dA, dB, dC, mode);
         cudaError_t e = cudaDeviceSynchronize();
@@ -93,8 +101,13 @@ int main() {
             err = std::max(err, std::fabs(C[i] - ref[i]));
             mx = std::max(mx, std::fabs(ref[i]));
         }
-        printf("mode %d: err=%s maxabs_err %.3g (ref max %.3g)  C[0..3]=%g %g %g %g ref=%g %g\n",
-               mode, cudaGetErrorString(e), err, mx, C[0], C[1], C[2], C[129], ref[0], ref[1]);
+        double et = 0, er = 0;
+        for (int i = 0; i < 128 * 128; ++i) {
+            et = std::max(et, std::fabs(C[i] - rt[i]));
+            er = std::max(er, std::fabs(C[i] - rr[i]));
+        }
+        printf("mode %d: %s |C-exact| %.3g  |C-trunc| %.3g  |C-rna| %.3g  (ref max %.3g)\n", mode,
+               cudaGetErrorString(e), err, et, er, mx);
     }
     return 0;
 }

@@ -1,0 +1,37 @@
+"""Timeline of CTA 0 of the CTA-pair GEMM (diagnostics):
+python tools/umma_trace.py G M N K a_mn b_mn"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+tr = torch.zeros(5000, dtype=torch.int64, device="cuda")
+os.environ["MTK_UMMA_TRACE"] = str(tr.data_ptr())
+from paper_2011_09463_b200 import api  # noqa: E402
+
+G, M, N, K, a_mn, b_mn = [int(x) for x in sys.argv[1:7]]
+ctx = api.Context(0)
+A = torch.randn((G, K, M) if a_mn else (G, M, K), device="cuda")
+B = torch.randn((G, K, N) if b_mn else (G, N, K), device="cuda")
+for _ in range(3):
+    tr.zero_()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    api.diag_gemm_tf32x3(ctx, A, B, bool(a_mn), bool(b_mn))
+    e1.record()
+    torch.cuda.synchronize()
+t = tr.cpu().numpy().astype(np.int64)
+t0 = t[2002]
+prod = (t[:1000][t[:1000] > 0] - t0) / 1000
+mma = (t[1000:2000][t[1000:2000] > 0] - t0) / 1000
+print(f"diag call (incl. 2 split kernels) {e0.elapsed_time(e1)*1000:.1f} us; flops {2*G*M*N*K*3/1e12:.3f} TF(tensor)")
+print("producer stage issue (us):", np.round(prod[:24], 2).tolist(), "... n =", len(prod))
+print("mma stage consume   (us):", np.round(mma[:24], 2).tolist(), "... last", np.round(mma[-1:], 2))
+cv0 = (t[3000:4000][t[3000:4000] > 0] - t0) / 1000
+cv1 = (t[4000:5000][t[4000:5000] > 0] - t0) / 1000
+print("TMA landed (conv start) (us):", np.round(cv0[:24], 2).tolist())
+print("conv done            (us):", np.round(cv1[:24], 2).tolist())
+print("epilogue start/end (us):", (t[2000] - t0) / 1000, (t[2001] - t0) / 1000)
