@@ -30,21 +30,24 @@ using namespace sm100;
 
 constexpr int TI = 128, TJ = 64, KC = 32, JC = 16, VD = 256;
 constexpr int STAGES = 4;
-constexpr int G1_BYTES = 2 * (TI * KC * 4) + 2 * (TJ * KC * 4);  // 48 KB
+constexpr int G1_BYTES = 2 * (TI * KC * 4) + 2 * (TJ * KC * 4);  // 48 KB (fp32 + lo planes)
 constexpr int G2_BYTES = 2 * (JC * VD * 4);                       // 32 KB
+constexpr int G1_LOAD = G1_BYTES / 2;                             // TMA brings the fp32 half
+constexpr int G2_LOAD = G2_BYTES / 2;
 constexpr int STAGE_BYTES = G1_BYTES;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
-constexpr int NUM_THREADS = 192;
+constexpr int CONV_WARPS = 4;
+constexpr int NUM_THREADS = 192 + 32 * CONV_WARPS;  // + lo-plane converter warps
 // TMEM columns: V [0,256); S / W-hi double buffer b at 256 + 64 b (S is
 // overwritten in place by the hi plane of W); W-lo buffer b at 384 + 64 b.
 constexpr uint32_t S_COL = 256;
 constexpr uint32_t WLO_COL = 384;
 
 struct MmdTcParams {
-    CUtensorMap zk_hi, zk_lo;   // K-major view: (d, N, G), box (32, 64)
-    CUtensorMap zm_hi, zm_lo;   // MN-major view: (d, N, G), box (32, 16), 32-B atom swizzle
-    const float* z_hi;          // planes, for z_i in the gradient epilogue
-    const float* z_lo;
+    CUtensorMap zk;             // K-major view of Z (fp32): (d, N, G), box (32, 64)
+    CUtensorMap zm;             // MN-major view: (d, N, G), box (32, 16), 32-B atom swizzle
+    const float* z;             // Z rows (fp32), for z_i in the gradient epilogue
+    long long z_rs, z_gs;       // row / group strides of z
     const float* norms;         // [G][N]
     const double* beta;         // [G]
     long long m, n;
@@ -81,13 +84,14 @@ __device__ __forceinline__ unsigned long long gtime() {
 // into an fp64 buffer: the MMD gradient is a small difference of large
 // same-domain and cross-domain sums, and fp32 tensor-core accumulation over
 // tens of thousands of j would not hold 1e-5 (C4: m+n = 73728).
-constexpr int FLUSH = 8;
+constexpr int FLUSH = 16;  // j tiles (1024 rows of Z) per fp32 V chunk
 
 __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_constant__ MmdTcParams p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-    uint64_t* empty = full + STAGES;
+    uint64_t* conv = full + STAGES;
+    uint64_t* empty = conv + STAGES;
     uint64_t* s_full = empty + STAGES;  // [2]
     uint64_t* w_full = s_full + 2;      // [2]
     uint64_t* v_full = w_full + 2;
@@ -109,12 +113,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
         (p.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) ? p.trace : nullptr;
 
     if (warp == 0 && lane == 0) {
-        tma_prefetch(&p.zk_hi);
-        tma_prefetch(&p.zk_lo);
-        tma_prefetch(&p.zm_hi);
-        tma_prefetch(&p.zm_lo);
+        tma_prefetch(&p.zk);
+        tma_prefetch(&p.zm);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
+            mbar_init(&conv[s], CONV_WARPS);
             mbar_init(&empty[s], 1);
         }
         for (int b = 0; b < 2; ++b) {
@@ -146,14 +149,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
                         mbar_wait(&empty[s], ((st / STAGES) & 1) ^ 1);
                         TRACE(0, st);
                         uint8_t* b = smem + s * STAGE_BYTES;
-                        mbar_expect_tx(&full[s], G1_BYTES);
+                        mbar_expect_tx(&full[s], G1_LOAD);
                         const int k0 = kc * KC;
-                        tma_load_3d(b, &p.zk_hi, &full[s], k0, (int)i0, g);
-                        tma_load_3d(b + 8192, &p.zk_hi, &full[s], k0, (int)i0 + 64, g);
-                        tma_load_3d(b + 16384, &p.zk_lo, &full[s], k0, (int)i0, g);
-                        tma_load_3d(b + 24576, &p.zk_lo, &full[s], k0, (int)i0 + 64, g);
-                        tma_load_3d(b + 32768, &p.zk_hi, &full[s], k0, j0, g);
-                        tma_load_3d(b + 40960, &p.zk_lo, &full[s], k0, j0, g);
+                        // fp32 Z_i (two 64-row boxes) at [0,16K), fp32 Z_j at [32K,40K);
+                        // the converters fill the lo planes at [16K,32K) and [40K,48K)
+                        tma_load_3d(b, &p.zk, &full[s], k0, (int)i0, g);
+                        tma_load_3d(b + 8192, &p.zk, &full[s], k0, (int)i0 + 64, g);
+                        tma_load_3d(b + 32768, &p.zk, &full[s], k0, j0, g);
                     }
                 }
                 if (t >= 1) {
@@ -163,12 +165,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
                         mbar_wait(&empty[s], ((st / STAGES) & 1) ^ 1);
                         TRACE(0, st);
                         uint8_t* b = smem + s * STAGE_BYTES;
-                        mbar_expect_tx(&full[s], G2_BYTES);
-                        for (int q = 0; q < VD / 32; ++q) {
-                            tma_load_3d(b + q * 2048, &p.zm_hi, &full[s], v0 + 32 * q, j0 + JC * jc, g);
-                            tma_load_3d(b + 16384 + q * 2048, &p.zm_lo, &full[s], v0 + 32 * q,
-                                        j0 + JC * jc, g);
-                        }
+                        mbar_expect_tx(&full[s], G2_LOAD);
+                        for (int q = 0; q < VD / 32; ++q)
+                            tma_load_3d(b + q * 2048, &p.zm, &full[s], v0 + 32 * q, j0 + JC * jc, g);
                     }
                 }
             }
@@ -185,7 +184,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
                     const uint32_t tS = tmem + S_COL + (t & 1) * TJ;
                     for (int kc = 0; kc < nkc; ++kc, ++st) {
                         const int s = st % STAGES;
-                        mbar_wait(&full[s], (st / STAGES) & 1);
+                        mbar_wait(&conv[s], (st / STAGES) & 1);
                         TRACE(4096, st);
                         tc_fence_after();
                         const uint32_t b = smem_u32(smem + s * STAGE_BYTES);
@@ -216,7 +215,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
                     }
                     for (int jc = 0; jc < TJ / JC; ++jc, ++st) {
                         const int s = st % STAGES;
-                        mbar_wait(&full[s], (st / STAGES) & 1);
+                        mbar_wait(&conv[s], (st / STAGES) & 1);
                         TRACE(4096, st);
                         tc_fence_after();
                         const uint32_t b = smem_u32(smem + s * STAGE_BYTES);
@@ -236,6 +235,50 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
                 }
             }
             mma_commit(v_full);
+        }
+    } else if (warp >= 6) {
+        // ---------------- lo-plane converters: same stage order as the producer ----------------
+        const int t = threadIdx.x - 192;
+        constexpr int NT = 32 * CONV_WARPS;
+        int st = 0;
+        auto convert = [&](uint8_t* b, int src, int bytes) {
+            const float4* in = reinterpret_cast<const float4*>(b + src);
+            float4* out = reinterpret_cast<float4*>(b + src + bytes);
+            for (int e = t; e < bytes / 16; e += NT) {
+                const float4 x = in[e];
+                float4 h, l;
+                split_tf32(x.x, h.x, l.x);
+                split_tf32(x.y, h.y, l.y);
+                split_tf32(x.z, h.z, l.z);
+                split_tf32(x.w, h.w, l.w);
+                const_cast<float4*>(in)[e] = h;  // hi = rna(x) in place, |lo| <= 2^-11 |x|
+                out[e] = l;
+            }
+        };
+        auto publish = [&](int s) {
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&conv[s]);
+        };
+        for (int tt = 0; tt <= njt; ++tt) {
+            if (tt < njt) {
+                for (int kc = 0; kc < nkc; ++kc, ++st) {
+                    const int s = st % STAGES;
+                    mbar_wait(&full[s], (st / STAGES) & 1);
+                    uint8_t* b = smem + s * STAGE_BYTES;
+                    convert(b, 0, 16384);      // Z_i fp32 -> lo
+                    convert(b, 32768, 8192);   // Z_j fp32 -> lo
+                    publish(s);
+                }
+            }
+            if (tt >= 1) {
+                for (int jc = 0; jc < TJ / JC; ++jc, ++st) {
+                    const int s = st % STAGES;
+                    mbar_wait(&full[s], (st / STAGES) & 1);
+                    convert(smem + s * STAGE_BYTES, 0, 16384);  // Z_j (MN-major) -> lo
+                    publish(s);
+                }
+            }
         }
     } else {
         // ---------------- epilogue warps: exp + weights, then the gradient ----------------
@@ -364,15 +407,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
             if (do_flush && jt > 0 && jt % FLUSH == 0) {
                 mbar_wait(v_full, nflush & 1);
                 tc_fence_after();
-                double* vrow = p.vacc + ((long long)g * N + (row_ok ? gi : 0)) * p.d;
+                double* vrow = p.vacc + ((long long)g * N + (row_ok ? gi : 0)) * p.d + v0;
 #pragma unroll 1
                 for (int cb = 0; cb < VD / 32; ++cb) {
                     float vv[32];
                     tmem_ld_32x32(tmem + lane_base + cb * 32, vv);
-                    if (!row_ok) continue;
-                    for (int c = 0; c < 32 && cb * 32 + c < vd; ++c) {
-                        const int k = v0 + cb * 32 + c;
-                        vrow[k] = (nflush ? vrow[k] : 0.0) + (double)vv[c];
+                    if (!row_ok || cb * 32 >= vd) continue;
+                    double2* vp = reinterpret_cast<double2*>(vrow + cb * 32);
+                    if (cb * 32 + 32 <= vd) {
+#pragma unroll
+                        for (int c = 0; c < 16; ++c) {
+                            double2 o = nflush ? vp[c] : make_double2(0.0, 0.0);
+                            o.x += (double)vv[2 * c];
+                            o.y += (double)vv[2 * c + 1];
+                            vp[c] = o;
+                        }
+                    } else {
+                        for (int c = 0; cb * 32 + c < vd; ++c)
+                            vrow[cb * 32 + c] = (nflush ? vrow[cb * 32 + c] : 0.0) + (double)vv[c];
                     }
                 }
                 tc_fence_before();
@@ -391,10 +443,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
             const int rr = e / VD, k = e % VD;
             const long long row = i0 + rr;
             float z = 0.f;
-            if (k < vd && row < N) {
-                const long long o = ((long long)g * N + row) * p.d + v0 + k;
-                z = p.z_hi[o] + p.z_lo[o];
-            }
+            if (k < vd && row < N) z = p.z[g * p.z_gs + row * p.z_rs + v0 + k];
             zs[rr * (VD + 1) + k] = z;
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -439,26 +488,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
     }
 }
 
-// n_i = |z_i|^2 from the fp32 rows (Xs rows then Xt rows), plus the tf32
-// planes of the concatenated sample Z = [Xs; Xt].
+// n_i = |z_i|^2 (fp64 accumulation) for the rows of Z = [Xs; Xt]; with `zc`
+// non-null the rows are also copied into a contiguous [G][N][d] buffer (used
+// when Xs and Xt are separate allocations).  One warp per row.
 __global__ void mmd_prep_kernel(const float* Xs, long long xs_gs, const float* Xt, long long xt_gs,
-                                long long m, long long n, int d, float* zhi, float* zlo,
-                                float* norms) {
+                                long long m, long long n, int d, float* zc, float* norms) {
     const int g = blockIdx.y;
     const long long N = m + n;
     const long long row = blockIdx.x * (long long)(blockDim.x / 32) + (threadIdx.x >> 5);
     if (row >= N) return;
     const int lane = threadIdx.x & 31;
     const float* src = row < m ? Xs + g * xs_gs + row * d : Xt + g * xt_gs + (row - m) * d;
-    float* dh = zhi + ((long long)g * N + row) * d;
-    float* dl = zlo + ((long long)g * N + row) * d;
+    float* dst = zc ? zc + ((long long)g * N + row) * d : nullptr;
     double acc = 0.0;
     for (int k = lane; k < d; k += 32) {
         const float x = src[k];
-        float h, l;
-        split_tf32(x, h, l);
-        dh[k] = h;
-        dl[k] = l;
+        if (dst) dst[k] = x;
         acc += (double)x * (double)x;
     }
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -484,11 +529,13 @@ EncodeFn encoder() {
     return fn;
 }
 
-CUtensorMap zmap(const float* base, long long d, long long N, long long G, int box_outer,
-                 bool mn) {
+CUtensorMap zmap(const float* base, long long d, long long N, long long G, long long gs,
+                 int box_outer, bool mn) {
     CUtensorMap m;
     const cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)N, (cuuint64_t)G};
-    const cuuint64_t strides[2] = {(cuuint64_t)(d * 4), (cuuint64_t)(N * d * 4)};
+    const cuuint64_t strides[2] = {(cuuint64_t)(d * 4), (cuuint64_t)(gs * 4)};
+    if ((reinterpret_cast<uintptr_t>(base) & 15) || (gs * 4) % 16)
+        fail(MTK_ERROR, "mmd: sample not 16-byte aligned for TMA");
     const cuuint32_t box[3] = {32, (cuuint32_t)box_outer, 1};
     const cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims,
@@ -515,9 +562,15 @@ static bool needs_flush(const MmdArgs& a) {
     return grads && (N + TJ - 1) / TJ > FLUSH;
 }
 
+// Xs and Xt already form one [G][N][d] block (the bank's hidden layer): no copy
+static bool contiguous(const MmdArgs& a) {
+    return a.Xt == a.Xs + a.m * a.d && a.xs_gs == a.xt_gs && (a.G == 1 || a.xs_gs >= (a.m + a.n) * a.d);
+}
+
 size_t mmd_tc_scratch_bytes(const MmdArgs& a) {
     const long long N = a.m + a.n;
-    size_t b = (size_t)a.G * N * a.d * 2 * sizeof(float) + (size_t)a.G * N * sizeof(float) + 1024;
+    size_t b = (size_t)a.G * N * sizeof(float) + 1024;
+    if (!contiguous(a)) b += (size_t)a.G * N * a.d * sizeof(float) + 256;
     if (needs_flush(a)) b += (size_t)a.G * N * a.d * sizeof(double) + 256;
     return b;
 }
@@ -526,24 +579,28 @@ size_t mmd_tc_scratch_bytes(const MmdArgs& a) {
 void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s) {
     const long long N = a.m + a.n;
     const long long re = a.row_end < 0 ? N : a.row_end;
-    float* zhi = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(scratch) + 255) & ~uintptr_t(255));
-    float* zlo = zhi + (size_t)a.G * N * a.d;
-    float* norms = zlo + (size_t)a.G * N * a.d;
-    double* vacc = nullptr;
-    if (needs_flush(a))
-        vacc = reinterpret_cast<double*>(
-            (reinterpret_cast<uintptr_t>(norms + (size_t)a.G * N) + 255) & ~uintptr_t(255));
+    uintptr_t cur = (reinterpret_cast<uintptr_t>(scratch) + 255) & ~uintptr_t(255);
+    float* norms = reinterpret_cast<float*>(cur);
+    cur = (cur + (size_t)a.G * N * sizeof(float) + 255) & ~uintptr_t(255);
+    const bool contig = contiguous(a);
+    float* zc = nullptr;
+    if (!contig) {
+        zc = reinterpret_cast<float*>(cur);
+        cur = (cur + (size_t)a.G * N * a.d * sizeof(float) + 255) & ~uintptr_t(255);
+    }
+    double* vacc = needs_flush(a) ? reinterpret_cast<double*>(cur) : nullptr;
     dim3 pg((unsigned)((N + 7) / 8), a.G);
-    mmd_prep_kernel<<<pg, 256, 0, s>>>(a.Xs, a.xs_gs, a.Xt, a.xt_gs, a.m, a.n, a.d, zhi, zlo, norms);
+    mmd_prep_kernel<<<pg, 256, 0, s>>>(a.Xs, a.xs_gs, a.Xt, a.xt_gs, a.m, a.n, a.d, zc, norms);
     count_launch();
+    const float* Z = contig ? a.Xs : zc;
+    const long long zgs = contig ? a.xs_gs : N * a.d;
     MmdTcParams p;
     std::memset(&p, 0, sizeof(p));
-    p.zk_hi = zmap(zhi, a.d, N, a.G, 64, false);  // 64-row boxes (two per 128-row tile)
-    p.zk_lo = zmap(zlo, a.d, N, a.G, 64, false);
-    p.zm_hi = zmap(zhi, a.d, N, a.G, JC, true);
-    p.zm_lo = zmap(zlo, a.d, N, a.G, JC, true);
-    p.z_hi = zhi;
-    p.z_lo = zlo;
+    p.zk = zmap(Z, a.d, N, a.G, zgs, 64, false);  // 64-row boxes (two per 128-row tile)
+    p.zm = zmap(Z, a.d, N, a.G, zgs, JC, true);
+    p.z = Z;
+    p.z_rs = a.d;
+    p.z_gs = zgs;
     p.norms = norms;
     p.beta = a.beta;
     p.m = a.m;

@@ -2,12 +2,12 @@
 // (tcgen05 + TMEM + TMA), sm_100a.
 //
 // C[g] (M x N) = A[g] (M x K) * B[g] (K x N) for G independent models.
-// Operands live in HBM as plain fp32 and are staged into smem by TMA.  The
-// tf32 MMA reads an fp32 operand by truncating its low 13 mantissa bits
-// (measured: tools/umma_probe.cu), so the staged fp32 tile IS the "hi" part;
-// converter warps derive the "lo" part on chip, lo = rna_tf32(x - trunc(x)),
+// Operands live in HBM as plain fp32 and are staged into smem by TMA.
+// Converter warps split each staged tile on chip: hi = rna_tf32(x) in place
+// and lo = rna_tf32(x - hi) in a second tile (the tf32 MMA truncates fp32
+// inputs -- measured by tools/umma_probe.cu -- so both parts are exact tf32),
 // and three MMAs per k step give fp32-level products (3xTF32):
-//     A*B ~= A*B_lo + A_lo*B + A*B          (A, B read as tf32 by the MMA)
+//     A*B ~= A_hi*B_lo + A_lo*B_hi + A_hi*B_hi      (dropped A_lo*B_lo ~ 2^-22)
 // HBM and L2 carry 4 bytes per operand element, as for an fp32 SIMT GEMM.
 //
 // Replaces, for the bank's dense layers, the reference loops
@@ -81,9 +81,9 @@ __device__ __forceinline__ void load_operand(uint8_t* dst, const CUtensorMap* ma
     }
 }
 
-// lo = rna_tf32(x - trunc_tf32(x)) over the two fp32 tiles of a stage.  The
-// transform is elementwise, so it ignores the swizzle: lo sits at the same
-// offset in its own tile.
+// hi = rna_tf32(x) (in place), lo = rna_tf32(x - hi) over the two fp32 tiles
+// of a stage.  The transform is elementwise, so it ignores the swizzle: lo
+// sits at the same offset in its own tile.
 __device__ __forceinline__ void convert_stage(uint8_t* st, int t) {
     constexpr int NT = 32 * NUM_CONV_WARPS;
 #pragma unroll
@@ -93,11 +93,12 @@ __device__ __forceinline__ void convert_stage(uint8_t* st, int t) {
         const float4* src = reinterpret_cast<const float4*>(st + tile * 2 * TILE_BYTES) + w;
         float4* dst = reinterpret_cast<float4*>(st + tile * 2 * TILE_BYTES + TILE_BYTES) + w;
         const float4 x = *src;
-        float4 l;
-        l.x = tf32_rna(x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u));
-        l.y = tf32_rna(x.y - __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u));
-        l.z = tf32_rna(x.z - __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u));
-        l.w = tf32_rna(x.w - __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u));
+        float4 h, l;
+        split_tf32(x.x, h.x, l.x);
+        split_tf32(x.y, h.y, l.y);
+        split_tf32(x.z, h.z, l.z);
+        split_tf32(x.w, h.w, l.w);
+        *const_cast<float4*>(src) = h;  // hi = rna(x) in place, |lo| <= 2^-11 |x|
         *dst = l;
     }
 }
