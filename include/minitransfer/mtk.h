@@ -131,6 +131,14 @@ int mtk_bank_train_step(mtk_bank* bank, const mtk_step* step, double* loss_host,
 int mtk_bank_train_step_host(mtk_bank* bank, const mtk_step* step, const float* X_host,
                              const int32_t* y_host, const float* w_host, double* loss_host,
                              double* mmd_host);
+/* Pipelined variant: enqueue the step (H2D copy on a library copy stream into
+ * one of two staging slots, overlapping the previous step's compute) and
+ * return without waiting.  X_host / y_host / w_host should be pinned.
+ * mtk_bank_step_result(which = 0) waits for the most recent enqueued step and
+ * returns its per-model loss / MMD (which = 1: the one before it).          */
+int mtk_bank_train_step_host_async(mtk_bank* bank, const mtk_step* step, const float* X_host,
+                                   const int32_t* y_host, const float* w_host);
+int mtk_bank_step_result(mtk_bank* bank, int which, double* loss_host, double* mmd_host);
 /* which layers run their GEMMs on the tcgen05 3xTF32 path (1) vs the SIMT
  * path (0); out_host [n_layers].  Layers with both widths >= 32 and
  * multiples of 4 qualify (env MTK_DISABLE_TC=1 at bank creation forces SIMT). */

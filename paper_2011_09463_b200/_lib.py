@@ -71,6 +71,8 @@ SIGNATURES = {
     "mtk_bank_forward": (C.c_int, [_vp, _vp, C.c_int, C.c_int, _vp, _vp]),
     "mtk_bank_train_step": (C.c_int, [_vp, C.POINTER(MtkStep), _dp, _dp]),
     "mtk_bank_train_step_host": (C.c_int, [_vp, C.POINTER(MtkStep), _vp, _vp, _vp, _dp, _dp]),
+    "mtk_bank_train_step_host_async": (C.c_int, [_vp, C.POINTER(MtkStep), _vp, _vp, _vp]),
+    "mtk_bank_step_result": (C.c_int, [_vp, C.c_int, _dp, _dp]),
     "mtk_bank_tc_layers": (C.c_int, [_vp, _ip]),
     "mtk_bank_set_keep_grads": (C.c_int, [_vp, C.c_int]),
     "mtk_bank_get_grads": (C.c_int, [_vp, C.c_int, _dpp, _dpp]),

@@ -240,6 +240,21 @@ class Bank:
         errors.check(lib.mtk_bank_tc_layers(self.h, out))
         return [bool(x) for x in out]
 
+    def train_step_host_async(self, X_host, y_host, w_host=None, **kw):
+        """Enqueue a step from pinned host buffers (copy overlaps the previous
+        step's compute); collect results with step_result()."""
+        B = X_host.shape[1]
+        s = self.make_step(B, **kw)
+        errors.check(lib.mtk_bank_train_step_host_async(self.h, C.byref(s), _ptr(X_host),
+                                                        _ptr(y_host), _ptr(w_host)),
+                     "train_step_host_async")
+
+    def step_result(self, which: int = 0):
+        """(loss[G], mmd[G]) of the last (which=0) or previous (1) async step."""
+        errors.check(lib.mtk_bank_step_result(self.h, which, self._loss.ctypes.data_as(_dp),
+                                              self._mmd.ctypes.data_as(_dp)), "step_result")
+        return self._loss.copy(), self._mmd.copy()
+
     def keep_grads(self, on: bool = True):
         errors.check(lib.mtk_bank_set_keep_grads(self.h, 1 if on else 0))
 

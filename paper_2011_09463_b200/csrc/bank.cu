@@ -83,6 +83,17 @@ struct mtk_bank {
     int32_t* ys = nullptr;
     float* ws = nullptr;
     int stageB = 0;
+    // pipelined host steps: two staging slots filled on a copy stream
+    struct Slot {
+        float* X = nullptr;
+        int32_t* y = nullptr;
+        float* w = nullptr;
+        double* res = nullptr;  // pinned [2G]: loss, mmd
+        cudaEvent_t copied = nullptr, consumed = nullptr, done = nullptr;
+        bool mmd = false;
+    } slot[2];
+    int slotB = 0, next_slot = 0, last_slot = -1;
+    cudaStream_t copy_stream = nullptr;
 
     int layer_of(int i) const { return i < L ? i : L - 1; }
     int fan_in(int i) const { return dims[layer_of(i)]; }
@@ -113,6 +124,46 @@ struct mtk_bank {
         cudaFree(Xs);
         cudaFree(ys);
         cudaFree(ws);
+        free_slots();
+        if (copy_stream) cudaStreamDestroy(copy_stream);
+        for (auto& sl : slot) {
+            if (sl.copied) cudaEventDestroy(sl.copied);
+            if (sl.consumed) cudaEventDestroy(sl.consumed);
+            if (sl.done) cudaEventDestroy(sl.done);
+            if (sl.res) cudaFreeHost(sl.res);
+        }
+    }
+    void free_slots() {
+        for (auto& sl : slot) {
+            cudaFree(sl.X);
+            cudaFree(sl.y);
+            cudaFree(sl.w);
+            sl.X = nullptr;
+            sl.y = nullptr;
+            sl.w = nullptr;
+        }
+    }
+    void ensure_slots(int B) {
+        if (!copy_stream) {
+            MTK_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+            for (auto& sl : slot) {
+                MTK_CUDA(cudaEventCreateWithFlags(&sl.copied, cudaEventDisableTiming));
+                MTK_CUDA(cudaEventCreateWithFlags(&sl.consumed, cudaEventDisableTiming));
+                MTK_CUDA(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
+                MTK_CUDA(cudaMallocHost(&sl.res, 2 * G * sizeof(double)));
+            }
+        }
+        if (B <= slotB) return;
+        MTK_CUDA(cudaStreamSynchronize(ctx->stream));
+        MTK_CUDA(cudaStreamSynchronize(copy_stream));
+        free_slots();
+        const size_t GB = (size_t)G * B;
+        for (auto& sl : slot) {
+            MTK_CUDA(cudaMalloc(&sl.X, GB * dims[0] * sizeof(float)));
+            MTK_CUDA(cudaMalloc(&sl.y, GB * sizeof(int32_t)));
+            MTK_CUDA(cudaMalloc(&sl.w, GB * sizeof(float)));
+        }
+        slotB = B;
     }
     void free_acts() {
         for (auto& p : H) free3(p);
@@ -756,6 +807,62 @@ int mtk_bank_train_step_host(mtk_bank* k, const mtk_step* s, const float* X_host
         d.y = k->ys;
         d.w = w_host ? k->ws : nullptr;
         train_step(*k, d, loss_host, mmd_host);
+    });
+}
+
+int mtk_bank_train_step_host_async(mtk_bank* k, const mtk_step* s, const float* X_host,
+                                   const int32_t* y_host, const float* w_host) {
+    return guard([&] {
+        check_bank(k);
+        need(s && X_host && y_host, MTK_VALUE_ERROR, "train_step_host_async: null argument");
+        need(s->B >= 1, MTK_SHAPE_ERROR, "train_step_host_async: B must be >= 1");
+        k->ensure_slots(s->B);
+        Ctx& c = *k->ctx;
+        auto& sl = k->slot[k->next_slot];
+        const size_t GB = (size_t)k->G * s->B;
+        // the slot's previous step must have finished reading its inputs
+        MTK_CUDA(cudaStreamWaitEvent(k->copy_stream, sl.consumed, 0));
+        MTK_CUDA(cudaMemcpyAsync(sl.X, X_host, GB * k->dims[0] * 4, cudaMemcpyHostToDevice,
+                                 k->copy_stream));
+        MTK_CUDA(cudaMemcpyAsync(sl.y, y_host, GB * 4, cudaMemcpyHostToDevice, k->copy_stream));
+        if (w_host)
+            MTK_CUDA(cudaMemcpyAsync(sl.w, w_host, GB * 4, cudaMemcpyHostToDevice, k->copy_stream));
+        MTK_CUDA(cudaEventRecord(sl.copied, k->copy_stream));
+        MTK_CUDA(cudaStreamWaitEvent(c.stream, sl.copied, 0));
+        mtk_step d = *s;
+        d.X = sl.X;
+        d.y = sl.y;
+        d.w = w_host ? sl.w : nullptr;
+        train_step(*k, d, nullptr, nullptr);
+        MTK_CUDA(cudaEventRecord(sl.consumed, c.stream));
+        MTK_CUDA(cudaMemcpyAsync(sl.res, k->loss, k->G * sizeof(double), cudaMemcpyDeviceToHost,
+                                 c.stream));
+        sl.mmd = s->mmd_lambda > 0.0;
+        if (sl.mmd)
+            MTK_CUDA(cudaMemcpyAsync(sl.res + k->G, k->mmd, k->G * sizeof(double),
+                                     cudaMemcpyDeviceToHost, c.stream));
+        MTK_CUDA(cudaEventRecord(sl.done, c.stream));
+        k->last_slot = k->next_slot;
+        k->next_slot ^= 1;
+    });
+}
+
+int mtk_bank_step_result(mtk_bank* k, int which, double* loss_host, double* mmd_host) {
+    return guard([&] {
+        check_bank(k);
+        need(k->last_slot >= 0, MTK_CONFIG_ERROR, "step_result: no asynchronous step enqueued");
+        need(which == 0 || which == 1, MTK_VALUE_ERROR, "step_result: which is 0 (last) or 1");
+        const int idx = which == 0 ? k->last_slot : (k->last_slot ^ 1);
+        auto& sl = k->slot[idx];
+        MTK_CUDA(cudaEventSynchronize(sl.done));
+        if (loss_host) std::memcpy(loss_host, sl.res, k->G * sizeof(double));
+        if (mmd_host) {
+            if (sl.mmd)
+                std::memcpy(mmd_host, sl.res + k->G, k->G * sizeof(double));
+            else
+                for (int g = 0; g < k->G; ++g) mmd_host[g] = 0.0;
+        }
+        if (which == 0) k->ctx->check_flags();
     });
 }
 

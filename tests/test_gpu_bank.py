@@ -230,3 +230,22 @@ def test_tc_and_simt_paths_agree(ctx, monkeypatch):
     assert rel(l0, l1) <= 1e-5 and rel(m0, m1) <= 1e-5
     for a, b in zip(W0, W1):
         assert rel(a, b) <= 1e-5
+
+
+def test_async_host_pipeline_matches_sync(ctx):
+    dims = [128, 64, 10]
+    X, y = inputs(2, 32, 128, 10)
+    Xh, yh = torch.tensor(X).pin_memory(), torch.tensor(y).pin_memory()
+    b1 = make_bank(ctx, 2, dims)
+    b2 = make_bank(ctx, 2, dims)
+    ref = [b1.train_step_host(Xh, yh, lr=0.1, src_rows=16, mmd_lambda=0.5) for _ in range(3)]
+    got = []
+    for k in range(3):
+        b2.train_step_host_async(Xh, yh, lr=0.1, src_rows=16, mmd_lambda=0.5)
+        if k > 0:
+            got.append(b2.step_result(1))
+    got.append(b2.step_result(0))
+    for (l1, m1), (l2, m2) in zip(ref, got):
+        assert np.array_equal(l1, l2) and np.array_equal(m1, m2)
+    for a, b in zip(b1.get_params(0)[0], b2.get_params(0)[0]):
+        assert np.array_equal(a, b)
