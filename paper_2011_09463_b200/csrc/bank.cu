@@ -317,6 +317,23 @@ void gemm_dx(mtk_bank& k, int mat, const Plane3& dz, int B, int r0, int rows, co
         u.add = add ? add + (size_t)r0 * fi : nullptr;
         u.flags = c.d_flags;
         launch_umma(u, c.stream);
+    } else if (head_dx_ok(fi, fo)) {
+        HeadDx h;
+        h.G = k.G;
+        h.rows = rows;
+        h.K = fi;
+        h.N = fo;
+        h.dZ = dz.f + (size_t)r0 * fo;
+        h.dz_gs = (long long)B * fo;
+        h.lddz = fo;
+        h.W = k.W[mat].f;
+        h.w_gs = (long long)fi * fo;
+        h.C = out.f + (size_t)r0 * fi;
+        h.c_gs = (long long)B * fi;
+        h.ldc = fi;
+        h.mask = mask + (size_t)r0 * fi;
+        h.add = add ? add + (size_t)r0 * fi : nullptr;
+        launch_head_dx(h, c.stream);
     } else {
         Gemm g;
         g.G = k.G;
@@ -524,8 +541,7 @@ void train_step(mtk_bank& k, const mtk_step& s, double* loss_host, double* mmd_h
             k.mmd_part_bytes = pbytes;
         }
         a.partial = k.mmd_part;
-        const long long N = a.m + a.n;
-        double* sc = c.scratch((size_t)k.G * ((N + 255) / 256) * (a.d + 1) * sizeof(double));
+        double* sc = c.scratch(mmd_beta_scratch_bytes(a));
         {
             PhaseScope ph(c, kPhMmdBeta, 2);
             launch_mmd_beta(a, k.beta, sc, c.stream);

@@ -208,8 +208,7 @@ int mtk_mmd_beta(mtk_ctx* c, const float* Xs, int64_t m, const float* Xt, int64_
                  double* beta_host) {
     return guard([&] {
         MmdArgs a = mmd_args(c, Xs, m, Xt, n, d, nullptr, 0);
-        const long long N = m + n;
-        const size_t part = (size_t)((N + 255) / 256) * (d + 1) * sizeof(double);
+        const size_t part = mmd_beta_scratch_bytes(a);
         double* sc = c->scratch(part + 64);
         double* beta_d = sc + part / sizeof(double);
         launch_mmd_beta(a, beta_d, sc, c->stream);
@@ -223,9 +222,8 @@ int mtk_mmd_beta(mtk_ctx* c, const float* Xs, int64_t m, const float* Xt, int64_
 
 static void mmd_run(mtk_ctx* c, MmdArgs& a, double beta, bool want_value, double* value_host,
                     double* beta_host, double* sums_host) {
-    const long long N = a.m + a.n;
     const int nblk = mmd_blocks_per_group(a);
-    const size_t part_beta = (size_t)((N + 255) / 256) * (a.d + 1) * sizeof(double);
+    const size_t part_beta = mmd_beta_scratch_bytes(a);
     const size_t part_pairs = (size_t)nblk * 3 * sizeof(double);
     const size_t bytes = part_beta + part_pairs + 64 * sizeof(double);
     double* sc = c->scratch(bytes);

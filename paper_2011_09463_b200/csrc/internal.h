@@ -156,7 +156,20 @@ struct HeadDw {
     int* flags = nullptr;
     float* partial = nullptr;  // scratch, head_dw_scratch_bytes()
 };
+struct HeadDx {
+    int G = 1, rows = 0, K = 0, N = 0;  // out [rows, K] = dZ [rows, N] . W[K, N]^T
+    const float* dZ = nullptr;
+    long long dz_gs = 0, lddz = 0;
+    const float* W = nullptr;  // [G][K][N]
+    long long w_gs = 0;
+    float* C = nullptr;
+    long long c_gs = 0, ldc = 0;
+    const float* mask = nullptr;  // same layout as C
+    const float* add = nullptr;
+};
 bool head_fwd_ok(int K, int N);
+bool head_dx_ok(int K, int N);
+void launch_head_dx(const HeadDx& p, cudaStream_t s);
 size_t head_dw_scratch_bytes(int G, int K, int N);
 bool head_dw_ok(int N);
 void launch_head_fwd(const HeadFwd& p, cudaStream_t s);
@@ -209,6 +222,7 @@ bool mmd_tc_supported(const MmdArgs& a);
 int mmd_tc_blocks_per_group(const MmdArgs& a);
 size_t mmd_tc_scratch_bytes(const MmdArgs& a);
 void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s);
+size_t mmd_beta_scratch_bytes(const MmdArgs& a);
 void launch_mmd_beta(const MmdArgs& a, double* beta_out, double* scratch, cudaStream_t s);
 void launch_mmd_pairs(const MmdArgs& a, cudaStream_t s);
 // value[g] = cSS*ss + cTT*tt + cST*st from the per-block partials (fixed order)

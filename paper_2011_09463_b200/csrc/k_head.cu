@@ -14,55 +14,87 @@ namespace {
 
 constexpr int MAXN = 32;
 
-// block: 8 warps x 8 rows each; W of model g (K x N, padded stride) in smem
+// forward: block = 64 rows of model g, 256 threads (4 per row, each owning
+// outputs n = t%4, t%4+4, ...); A and W staged through smem in 64-wide k
+// chunks with coalesced loads.
+constexpr int FR = 64, FK = 64;
 __global__ void __launch_bounds__(256) head_fwd_kernel(HeadFwd p) {
-    extern __shared__ float sW[];
+    __shared__ float sA[FR][FK + 1];
+    __shared__ float sW[FK][MAXN + 1];
     const int g = blockIdx.y;
-    const int N = p.N, K = p.K, ld = N | 1;  // odd stride: conflict-free lane-strided reads
+    const int r0 = blockIdx.x * FR;
+    const int N = p.N;
+    const int row = threadIdx.x >> 2, sub = threadIdx.x & 3;
+    const float* A = p.A + g * p.a_gs;
     const float* W = p.W + g * p.w_gs;
-    for (int i = threadIdx.x; i < K * N; i += blockDim.x) sW[(i / N) * ld + (i % N)] = W[i];
-    __syncthreads();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const float* bias = p.bias + g * p.bias_gs;
-    bool bad = false;
-    for (int rr = 0; rr < 8; ++rr) {
-        const int r = blockIdx.x * 64 + warp * 8 + rr;
-        if (r >= p.rows) break;
-        const float* a = p.A + g * p.a_gs + (long long)r * p.lda;
-        float acc[MAXN];
+    float acc[MAXN / 4];
 #pragma unroll
-        for (int n = 0; n < MAXN; ++n) acc[n] = 0.f;
-        for (int k = lane; k < K; k += 32) {
-            const float av = a[k];
-            const float* wr = sW + k * ld;
-#pragma unroll
-            for (int n = 0; n < MAXN; ++n)
-                if (n < N) acc[n] = fmaf(av, wr[n], acc[n]);
+    for (int i = 0; i < MAXN / 4; ++i) acc[i] = 0.f;
+    for (int k0 = 0; k0 < p.K; k0 += FK) {
+        const int kc = min(FK, p.K - k0);
+        __syncthreads();
+        for (int e = threadIdx.x; e < FR * FK; e += 256) {
+            const int rr = e / FK, kk = e % FK;
+            sA[rr][kk] = (r0 + rr < p.rows && kk < kc) ? A[(long long)(r0 + rr) * p.lda + k0 + kk] : 0.f;
         }
-        float mine = 0.f;
-#pragma unroll
-        for (int n = 0; n < MAXN; ++n) {
-            if (n >= N) break;
-            float v = acc[n];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            if (lane == n) mine = v;
+        for (int e = threadIdx.x; e < FK * N; e += 256) {
+            const int kk = e / N, n = e % N;
+            sW[kk][n] = kk < kc ? W[(long long)(k0 + kk) * N + n] : 0.f;
         }
-        if (lane < N) {
-            float v = mine + bias[lane];
-            bad |= !isfinite(v);
-            if (p.relu) v = v > 0.f ? v : 0.f;
-            const long long idx = g * p.c_gs + (long long)r * p.ldc + lane;
-            p.C[idx] = v;
-            if (p.C_hi) {
-                float h, l;
-                sm100::split_tf32(v, h, l);
-                p.C_hi[idx] = h;
-                p.C_lo[idx] = l;
+        __syncthreads();
+#pragma unroll 4
+        for (int kk = 0; kk < FK; ++kk) {
+            const float a = sA[row][kk];
+#pragma unroll
+            for (int i = 0; i < MAXN / 4; ++i) {
+                const int n = sub + 4 * i;
+                if (n < N) acc[i] = fmaf(a, sW[kk][n], acc[i]);
             }
         }
     }
+    const int r = r0 + row;
+    if (r >= p.rows) return;
+    bool bad = false;
+#pragma unroll
+    for (int i = 0; i < MAXN / 4; ++i) {
+        const int n = sub + 4 * i;
+        if (n >= N) break;
+        float v = acc[i] + p.bias[g * p.bias_gs + n];
+        bad |= !isfinite(v);
+        if (p.relu) v = v > 0.f ? v : 0.f;
+        p.C[g * p.c_gs + (long long)r * p.ldc + n] = v;
+    }
     if (bad && p.flags) atomicOr(p.flags, kFlagNonFinite);
+}
+
+// dX through a narrow layer: out[r, q] = (sum_j dz[r, j] W[q, j] + add[r, q]) *
+// (mask[r, q] > 0), j < N <= 32.  Block = 32 rows of model g; W (K x N) and
+// the dz rows in smem; threads stride q so mask/add/out are coalesced.
+__global__ void __launch_bounds__(256) head_dx_kernel(HeadDx p) {
+    extern __shared__ float sm[];
+    const int N = p.N, ld = N | 1;
+    float* sW = sm;                      // [K][ld]
+    float* sdz = sm + (size_t)p.K * ld;  // [32][ld]
+    const int g = blockIdx.y;
+    const int r0 = blockIdx.x * 32;
+    const float* W = p.W + g * p.w_gs;
+    for (int e = threadIdx.x; e < p.K * N; e += blockDim.x) sW[(e / N) * ld + e % N] = W[e];
+    for (int e = threadIdx.x; e < 32 * N; e += blockDim.x) {
+        const int rr = e / N, j = e % N;
+        sdz[rr * ld + j] = (r0 + rr < p.rows) ? p.dZ[g * p.dz_gs + (long long)(r0 + rr) * p.lddz + j] : 0.f;
+    }
+    __syncthreads();
+    for (int rr = 0; rr < 32 && r0 + rr < p.rows; ++rr) {
+        const long long rowb = g * p.c_gs + (long long)(r0 + rr) * p.ldc;
+        for (int q = threadIdx.x; q < p.K; q += blockDim.x) {
+            float acc = 0.f;
+#pragma unroll 8
+            for (int j = 0; j < N; ++j) acc = fmaf(sdz[rr * ld + j], sW[q * ld + j], acc);
+            const long long idx = rowb + q;
+            if (p.add) acc = p.add[idx] + acc;
+            p.C[idx] = (p.mask[idx] > 0.f) ? acc : 0.f;
+        }
+    }
 }
 
 // dW partials: block (p-chunk of 64 input features, model g, row split rs),
@@ -89,8 +121,10 @@ __global__ void __launch_bounds__(256) head_dw_partial_kernel(HeadDw p) {
         }
         __syncthreads();
         if (pp < p.K) {
-            for (int rr = rg; rr < 64 && r0 + rr < rend; rr += 4) {
-                const float av = A[(long long)(r0 + rr) * p.lda + pp];
+            const int lim = min(64, rend - r0);
+#pragma unroll 4
+            for (int rr = rg; rr < lim; rr += 4) {
+                const float av = __ldg(A + (long long)(r0 + rr) * p.lda + pp);
 #pragma unroll
                 for (int n = 0; n < MAXN; ++n)
                     if (n < N) acc[n] = fmaf(av, sdz[rr][n], acc[n]);
@@ -129,20 +163,28 @@ __global__ void head_dw_finish_kernel(HeadDw p) {
 
 }  // namespace
 
-bool head_fwd_ok(int K, int N) { return N <= MAXN && (size_t)K * (N | 1) * 4 <= 96 * 1024; }
+bool head_fwd_ok(int K, int N) { return N <= MAXN && K >= 1; }
+bool head_dx_ok(int K, int N) { return N <= MAXN && (size_t)(K + 32) * (N | 1) * 4 <= 96 * 1024; }
 bool head_dw_ok(int N) { return N <= MAXN; }
 
 void launch_head_fwd(const HeadFwd& p, cudaStream_t s) {
     if (p.rows <= 0) return;
-    const size_t smem = (size_t)p.K * (p.N | 1) * sizeof(float);
+    dim3 grid((p.rows + FR - 1) / FR, p.G);
+    head_fwd_kernel<<<grid, 256, 0, s>>>(p);
+    count_launch();
+}
+
+void launch_head_dx(const HeadDx& p, cudaStream_t s) {
+    if (p.rows <= 0) return;
+    const size_t smem = (size_t)(p.K + 32) * (p.N | 1) * sizeof(float);
     static bool attr = false;
     if (!attr) {
-        MTK_CUDA(cudaFuncSetAttribute(head_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        MTK_CUDA(cudaFuncSetAttribute(head_dx_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       96 * 1024));
         attr = true;
     }
-    dim3 grid((p.rows + 63) / 64, p.G);
-    head_fwd_kernel<<<grid, 256, smem, s>>>(p);
+    dim3 grid((p.rows + 31) / 32, p.G);
+    head_dx_kernel<<<grid, 256, smem, s>>>(p);
     count_launch();
 }
 

@@ -24,7 +24,7 @@ __device__ __forceinline__ const float* row_ptr(const MmdArgs& a, int g, long lo
 }
 
 // beta partials: block (p, g) sums rows [p*R, p*R+R) -> sum z (per dim), sum |z|^2
-constexpr int BETA_ROWS = 256;
+constexpr int BETA_ROWS = 32;
 __global__ void beta_partial_kernel(MmdArgs a, double* part, int P) {
     const int g = blockIdx.y, p = blockIdx.x;
     const long long N = a.m + a.n;
@@ -33,6 +33,7 @@ __global__ void beta_partial_kernel(MmdArgs a, double* part, int P) {
     double sq = 0.0;
     for (int k = threadIdx.x; k < a.d; k += blockDim.x) {
         double s = 0.0;
+#pragma unroll 8
         for (long long r = r0; r < r1; ++r) {
             const double v = row_ptr(a, g, r)[k];
             s += v;
@@ -251,6 +252,11 @@ int mmd_blocks_per_group(const MmdArgs& a) {
     const long long N = a.m + a.n;
     const long long re = a.row_end < 0 ? N : a.row_end;
     return (int)((re - a.row_begin + TI - 1) / TI);
+}
+
+size_t mmd_beta_scratch_bytes(const MmdArgs& a) {
+    const long long N = a.m + a.n;
+    return (size_t)a.G * ((N + BETA_ROWS - 1) / BETA_ROWS) * (a.d + 1) * sizeof(double);
 }
 
 void launch_mmd_beta(const MmdArgs& a, double* beta_out, double* scratch, cudaStream_t s) {

@@ -19,14 +19,21 @@
 //   PAIR = true   CTA pair (cta_group::2), 256 x 256 tile: each CTA stages
 //                 128 rows of A and 128 columns of B; the leader issues
 //                 M=256, N=256 MMAs over both CTAs' smem.
+// Persistent: one CTA (pair) per SM (pair), static tile striding; the TMEM
+// accumulator is double-buffered so the epilogue of tile t overlaps the
+// mainloop of tile t+1.
 // Warp roles: w0 TMA producer, w1 MMA issuer (one elected thread), w2-w5
 // epilogue (TMEM -> registers -> fused bias/ReLU | ReLU-mask | SGD -> HBM),
-// w6-w13 lo-plane converters.  3-stage ring of 64 KB stages (128-B swizzle;
-// 32-B-atom swizzle for MN-major operands, the only layout tf32 accepts).
+// w6-w13 converters.  Two rings: LS load stages (32 KB: A and B fp32 as TMA
+// wrote them, hi written back in place) and LO lo stages (32 KB: A lo, B lo),
+// so TMA runs LS stages ahead while only LO stages hold lo planes.  128-B
+// swizzle; 32-B-atom swizzle for MN-major operands (the only layout tf32
+// accepts).
 #include <cuda.h>
 
 #include <cmath>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 
@@ -38,17 +45,17 @@ namespace {
 
 using namespace sm100;
 
-constexpr int BK = 32, STAGES = 3;
+constexpr int BK = 32, LS = 5, LO = 2;
 constexpr int TILE_BYTES = 128 * BK * 4;     // 16 KB: 128 rows (or cols) x 32 k
-constexpr int STAGE_BYTES = 4 * TILE_BYTES;  // A fp32, A lo, B fp32, B lo
-constexpr int LOAD_BYTES = 2 * TILE_BYTES;   // what TMA brings per stage
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int LOAD_BYTES = 2 * TILE_BYTES;   // load stage: A fp32, B fp32 (TMA bytes)
+constexpr int LO_BYTES = 2 * TILE_BYTES;     // lo stage: A lo, B lo
+constexpr int SMEM_BYTES = LS * LOAD_BYTES + LO * LO_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 constexpr int NUM_CONV_WARPS = 8;
 constexpr int NUM_THREADS = 192 + 32 * NUM_CONV_WARPS;
 
 struct UmmaParams {
     CUtensorMap a, b;  // 3-D fp32 maps, coords (inner, outer, g)
-    int M, N, K;
+    int G, M, N, K;
     int epi;           // Epi value
     float* C;
     long long c_gs, ldc;
@@ -82,30 +89,30 @@ __device__ __forceinline__ void load_operand(uint8_t* dst, const CUtensorMap* ma
 }
 
 // hi = rna_tf32(x) (in place), lo = rna_tf32(x - hi) over the two fp32 tiles
-// of a stage.  The transform is elementwise, so it ignores the swizzle: lo
-// sits at the same offset in its own tile.
-__device__ __forceinline__ void convert_stage(uint8_t* st, int t) {
+// of a load stage.  The transform is elementwise, so it ignores the swizzle:
+// lo sits at the same offset in the lo stage.
+__device__ __forceinline__ void convert_stage(uint8_t* st, uint8_t* lo, int t) {
     constexpr int NT = 32 * NUM_CONV_WARPS;
+    const uint32_t src = smem_u32(st) + 16 * t, dst = smem_u32(lo) + 16 * t;
+    float4 x[2048 / NT];
+#pragma unroll
+    for (int j = 0; j < 2048 / NT; ++j) x[j] = lds128(src + 16 * NT * j);
 #pragma unroll
     for (int j = 0; j < 2048 / NT; ++j) {
-        const int e = t + NT * j;                // float4 index within 2 tiles
-        const int tile = e >> 10, w = e & 1023;  // 1024 float4 per 16 KB tile
-        const float4* src = reinterpret_cast<const float4*>(st + tile * 2 * TILE_BYTES) + w;
-        float4* dst = reinterpret_cast<float4*>(st + tile * 2 * TILE_BYTES + TILE_BYTES) + w;
-        const float4 x = *src;
         float4 h, l;
-        split_tf32(x.x, h.x, l.x);
-        split_tf32(x.y, h.y, l.y);
-        split_tf32(x.z, h.z, l.z);
-        split_tf32(x.w, h.w, l.w);
-        *const_cast<float4*>(src) = h;  // hi = rna(x) in place, |lo| <= 2^-11 |x|
-        *dst = l;
+        split_tf32(x[j].x, h.x, l.x);
+        split_tf32(x[j].y, h.y, l.y);
+        split_tf32(x[j].z, h.z, l.z);
+        split_tf32(x[j].w, h.w, l.w);
+        sts128(src + 16 * NT * j, h);  // hi = rna(x) in place, |lo| <= 2^-11 |x|
+        sts128(dst + 16 * NT * j, l);
     }
 }
 
 // 3 MMAs per 8-wide k step over one stage
 template <int A_MN, int B_MN, bool PAIR>
-__device__ __forceinline__ void mma_stage(uint32_t tmem, uint32_t base, uint32_t idesc, bool first) {
+__device__ __forceinline__ void mma_stage(uint32_t tmem, uint32_t base, uint32_t lo, uint32_t idesc,
+                                          bool first) {
     constexpr uint32_t a_lbo = A_MN ? 4096 : 16, b_lbo = B_MN ? 4096 : 16;
     constexpr uint32_t a_sbo = A_MN ? 512 : 1024, b_sbo = B_MN ? 512 : 1024;
     constexpr uint32_t a_lay = A_MN ? 1 : 2, b_lay = B_MN ? 1 : 2;
@@ -116,9 +123,9 @@ __device__ __forceinline__ void mma_stage(uint32_t tmem, uint32_t base, uint32_t
         const uint32_t aoff = A_MN ? kk * 1024 : kk * 32;
         const uint32_t boff = B_MN ? kk * 1024 : kk * 32;
         const uint64_t a32 = smem_desc(base + aoff, a_lbo, a_sbo, a_lay);
-        const uint64_t alo = smem_desc(base + TILE_BYTES + aoff, a_lbo, a_sbo, a_lay);
-        const uint64_t b32 = smem_desc(base + 2 * TILE_BYTES + boff, b_lbo, b_sbo, b_lay);
-        const uint64_t blo = smem_desc(base + 3 * TILE_BYTES + boff, b_lbo, b_sbo, b_lay);
+        const uint64_t alo = smem_desc(lo + aoff, a_lbo, a_sbo, a_lay);
+        const uint64_t b32 = smem_desc(base + TILE_BYTES + boff, b_lbo, b_sbo, b_lay);
+        const uint64_t blo = smem_desc(lo + TILE_BYTES + boff, b_lbo, b_sbo, b_lay);
         const uint32_t acc0 = (first && kk == 0) ? 0u : 1u;
         if (PAIR) {
             mma_tf32_2sm(tmem, a32, blo, idesc, acc0);
@@ -190,8 +197,10 @@ __device__ __forceinline__ void epilogue_rows(const UmmaParams& p, uint32_t tmem
                 *reinterpret_cast<float4*>(p.C + idx) = x;
             }
         } else {
-            for (int j = 0; j < 32 && nb + j < p.N; ++j) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
                 const int n = nb + j;
+                if (n >= p.N) break;
                 const long long idx = rowbase + n;
                 float x = v[j];
                 if (p.epi == (int)Epi::kBias || p.epi == (int)Epi::kBiasRelu) {
@@ -215,35 +224,45 @@ __device__ __forceinline__ void epilogue_rows(const UmmaParams& p, uint32_t tmem
 
 template <int A_MN, int B_MN, bool PAIR>
 __global__ void __launch_bounds__(NUM_THREADS, 1) umma_kernel(const __grid_constant__ UmmaParams p) {
-    constexpr int TN = PAIR ? 256 : 128;  // accumulator columns per CTA
-    constexpr uint32_t TMEM_COLS = PAIR ? 256 : 128;
+    constexpr int TN = PAIR ? 256 : 128;  // accumulator columns per tile
+    constexpr uint32_t TMEM_COLS = 2 * TN;  // double-buffered accumulator
+    constexpr uint32_t NCTA = PAIR ? 2 : 1;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-    uint64_t* conv = full + STAGES;
-    uint64_t* empty = conv + STAGES;
-    uint64_t* tmem_full = empty + STAGES;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+    uint8_t* lo_ring = smem + LS * LOAD_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(lo_ring + LO * LO_BYTES);
+    uint64_t* empty = full + LS;
+    uint64_t* conv = empty + LS;
+    uint64_t* lofree = conv + LO;
+    uint64_t* acc_full = lofree + LO;
+    uint64_t* acc_empty = acc_full + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = PAIR ? cluster_rank() : 0;
-    const int g = blockIdx.z;
-    const int m0 = PAIR ? (int)(blockIdx.x >> 1) * 256 + (int)rank * 128 : (int)blockIdx.x * 128;
-    const int n0 = blockIdx.y * TN;        // accumulator columns (the pair's)
-    const int nb0 = n0 + (int)rank * 128;  // B columns staged by this CTA
+    const int tiles_m = PAIR ? (p.M + 255) / 256 : (p.M + 127) / 128;
+    const int tiles_n = (p.N + TN - 1) / TN;
+    const int ntiles = tiles_m * tiles_n * p.G;
+    const int cid = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+    const int ncl = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
     const int nk = (p.K + BK - 1) / BK;
-    unsigned long long* tr =
-        (p.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) ? p.trace : nullptr;
+    unsigned long long* tr = (p.trace && blockIdx.x == 0) ? p.trace : nullptr;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&p.a);
         tma_prefetch(&p.b);
-        for (int s = 0; s < STAGES; ++s) {
+        for (int s = 0; s < LS; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&conv[s], (PAIR ? 2 : 1) * NUM_CONV_WARPS);  // one arrival per converter warp
             mbar_init(&empty[s], 1);
         }
-        mbar_init(tmem_full, 1);
+        for (int s = 0; s < LO; ++s) {
+            mbar_init(&conv[s], NCTA * NUM_CONV_WARPS);  // one arrival per converter warp
+            mbar_init(&lofree[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&acc_full[b], 1);
+            mbar_init(&acc_empty[b], NCTA * 4);  // one arrival per epilogue warp
+        }
         fence_barrier_init();
     }
     if (warp == 1) {
@@ -255,59 +274,92 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_kernel(const __grid_const
     else __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    if (tr && threadIdx.x == 0) tr[2002] = gtime();
 
     if (warp == 0) {
         if (lane == 0) {
             // ---------------- TMA producer ----------------
-            for (int kb = 0; kb < nk; ++kb) {
-                const int s = kb % STAGES;
-                mbar_wait(&empty[s], ((kb / STAGES) & 1) ^ 1);
-                if (tr && kb < 1000) tr[kb] = gtime();
-                uint8_t* st = smem + s * STAGE_BYTES;
-                mbar_expect_tx(&full[s], LOAD_BYTES);
-                load_operand<A_MN>(st, &p.a, &full[s], m0, kb * BK, g);
-                load_operand<B_MN>(st + 2 * TILE_BYTES, &p.b, &full[s], nb0, kb * BK, g);
+            uint32_t it = 0;
+            for (int t = cid; t < ntiles; t += ncl) {
+                const int nt = t % tiles_n, mt = (t / tiles_n) % tiles_m, g = t / (tiles_n * tiles_m);
+                const int m0 = PAIR ? mt * 256 + (int)rank * 128 : mt * 128;
+                const int nb0 = nt * TN + (int)rank * 128;  // B columns staged by this CTA
+                for (int kb = 0; kb < nk; ++kb, ++it) {
+                    const int s = it % LS;
+                    mbar_wait(&empty[s], ((it / LS) & 1) ^ 1);
+                    if (tr && it < 1000) tr[it] = gtime();
+                    uint8_t* st = smem + s * LOAD_BYTES;
+                    mbar_expect_tx(&full[s], LOAD_BYTES);
+                    load_operand<A_MN>(st, &p.a, &full[s], m0, kb * BK, g);
+                    load_operand<B_MN>(st + TILE_BYTES, &p.b, &full[s], nb0, kb * BK, g);
+                }
             }
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer (leader CTA, one thread) ----------------
         constexpr uint32_t idesc = idesc_tf32(PAIR ? 256 : 128, TN, A_MN, B_MN);
         if (rank == 0 && lane == 0) {
-            for (int kb = 0; kb < nk; ++kb) {
-                const int s = kb % STAGES;
-                mbar_wait(&conv[s], (kb / STAGES) & 1);
-                if (tr && kb < 1000) tr[1000 + kb] = gtime();
+            uint32_t it = 0, tl = 0;
+            for (int t = cid; t < ntiles; t += ncl, ++tl) {
+                const uint32_t b = tl & 1;
+                mbar_wait(&acc_empty[b], ((tl >> 1) & 1) ^ 1);
                 tc_fence_after();
-                mma_stage<A_MN, B_MN, PAIR>(tmem, smem_u32(smem + s * STAGE_BYTES), idesc, kb == 0);
-                if (PAIR) mma_commit_2sm(&empty[s], 0x3);  // frees the slot in both CTAs
-                else mma_commit(&empty[s]);
+                const uint32_t acc = tmem + b * TN;
+                for (int kb = 0; kb < nk; ++kb, ++it) {
+                    const int s = it % LS, l = it % LO;
+                    mbar_wait(&conv[l], (it / LO) & 1);
+                    if (tr && it < 1000) tr[1000 + it] = gtime();
+                    tc_fence_after();
+                    mma_stage<A_MN, B_MN, PAIR>(acc, smem_u32(smem + s * LOAD_BYTES),
+                                                smem_u32(lo_ring + l * LO_BYTES), idesc, kb == 0);
+                    if (PAIR) {  // frees the slots in both CTAs
+                        mma_commit_2sm(&empty[s], 0x3);
+                        mma_commit_2sm(&lofree[l], 0x3);
+                    } else {
+                        mma_commit(&empty[s]);
+                        mma_commit(&lofree[l]);
+                    }
+                }
+                if (PAIR) mma_commit_2sm(&acc_full[b], 0x3);
+                else mma_commit(&acc_full[b]);
             }
-            if (PAIR) mma_commit_2sm(tmem_full, 0x3);
-            else mma_commit(tmem_full);
         }
     } else if (warp < 6) {
         // ---------------- epilogue: own 128 rows x TN columns ----------------
         const int q = warp & 3;  // TMEM lane quarter this warp may access
-        mbar_wait(tmem_full, 0);
-        if (tr && threadIdx.x == 64) tr[2000] = gtime();
-        tc_fence_after();
-        epilogue_rows(p, tmem, q, lane, g, m0, n0, TN);
-        if (tr && threadIdx.x == 64) tr[2001] = gtime();
-    } else {
-        // ---------------- lo-plane converters ----------------
-        const int t = threadIdx.x - 192;
-        for (int kb = 0; kb < nk; ++kb) {
-            const int s = kb % STAGES;
-            mbar_wait(&full[s], (kb / STAGES) & 1);
-            if (tr && t == 0 && kb < 1000) tr[3000 + kb] = gtime();
-            convert_stage(smem + s * STAGE_BYTES, t);
-            fence_proxy_async_smem();  // generic-proxy stores -> tensor-core reads
+        uint32_t tl = 0;
+        for (int t = cid; t < ntiles; t += ncl, ++tl) {
+            const int nt = t % tiles_n, mt = (t / tiles_n) % tiles_m, g = t / (tiles_n * tiles_m);
+            const int m0 = PAIR ? mt * 256 + (int)rank * 128 : mt * 128;
+            const uint32_t b = tl & 1;
+            mbar_wait(&acc_full[b], (tl >> 1) & 1);
+            if (tr && threadIdx.x == 64 && tl < 16) tr[2000 + 2 * tl] = gtime();
+            tc_fence_after();
+            epilogue_rows(p, tmem + b * TN, q, lane, g, m0, nt * TN, TN);
+            tc_fence_before();
             __syncwarp();
-            if (tr && t == 0 && kb < 1000) tr[4000 + kb] = gtime();
+            if (tr && threadIdx.x == 64 && tl < 16) tr[2001 + 2 * tl] = gtime();
             if (lane == 0) {
-                if (PAIR) mbar_arrive_remote(&conv[s], 0);
-                else mbar_arrive(&conv[s]);
+                if (PAIR) mbar_arrive_remote(&acc_empty[b], 0);
+                else mbar_arrive(&acc_empty[b]);
+            }
+        }
+    } else {
+        // ---------------- converters ----------------
+        const int ct = threadIdx.x - 192;
+        uint32_t it = 0;
+        for (int t = cid; t < ntiles; t += ncl) {
+            for (int kb = 0; kb < nk; ++kb, ++it) {
+                const int s = it % LS, l = it % LO;
+                mbar_wait(&full[s], (it / LS) & 1);
+                mbar_wait(&lofree[l], ((it / LO) & 1) ^ 1);
+                if (tr && ct == 0 && it < 1000) tr[3000 + it] = gtime();
+                convert_stage(smem + s * LOAD_BYTES, lo_ring + l * LO_BYTES, ct);
+                fence_proxy_async_smem();  // generic-proxy stores -> tensor-core reads
+                __syncwarp();
+                if (lane == 0) {
+                    if (PAIR) mbar_arrive_remote(&conv[l], 0);
+                    else mbar_arrive(&conv[l]);
+                }
             }
         }
     }
@@ -385,9 +437,17 @@ void launch_variant(const UmmaParams& p, int G, cudaStream_t s) {
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
         attr = true;
     }
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        MTK_CUDA(cudaGetDevice(&dev));
+        MTK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const long long ntiles = PAIR ? (long long)((p.M + 255) / 256) * ((p.N + 255) / 256) * G
+                                  : (long long)((p.M + 127) / 128) * ((p.N + 127) / 128) * G;
+    const long long ncl = std::min<long long>(ntiles, PAIR ? sms / 2 : sms);
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = PAIR ? dim3(2 * ((p.M + 255) / 256), (p.N + 255) / 256, G)
-                       : dim3((p.M + 127) / 128, (p.N + 127) / 128, G);
+    cfg.gridDim = dim3((unsigned)(PAIR ? 2 * ncl : ncl), 1, 1);
     cfg.blockDim = dim3(NUM_THREADS);
     cfg.dynamicSmemBytes = SMEM_BYTES;
     cfg.stream = s;
@@ -443,6 +503,7 @@ void launch_umma(const UmmaGemm& u, cudaStream_t s) {
                  : make_map(u.a, u.K, u.M, u.G, u.a_rs, u.a_gs, 128, false);
     p.b = u.b_mn ? make_map(u.b, u.N, u.K, u.G, u.b_rs, u.b_gs, BK, true)
                  : make_map(u.b, u.K, u.N, u.G, u.b_rs, u.b_gs, 128, false);
+    p.G = u.G;
     p.M = u.M;
     p.N = u.N;
     p.K = u.K;

@@ -73,8 +73,11 @@ __device__ __forceinline__ void cluster_sync() {
 __device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t rank) {
     uint32_t remote;
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
-                 : "memory");
+    // default .release.cta semantics: a .cluster-scope release compiles to
+    // MEMBAR.ALL.GPU, which stalls the arriving warp on all its outstanding
+    // stores; the smem writes being published are ordered by the caller's
+    // fence.proxy.async (as in CUTLASS's ClusterBarrier::arrive(cta_id)).
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
 // 2-SM TMA: data lands in this CTA's smem, transaction bytes are counted on
 // the leader (rank 0) CTA's barrier at the same offset.
@@ -264,6 +267,19 @@ __device__ __forceinline__ float tf32_rna(float x) {
     uint32_t r;
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
     return __uint_as_float(r);
+}
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(a)
+                 : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, float4 v) {
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z),
+                 "f"(v.w)
+                 : "memory");
 }
 // 3xTF32 split: x ~= hi + lo, both tf32-exact
 __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {

@@ -24,14 +24,17 @@ for _ in range(3):
     e1.record()
     torch.cuda.synchronize()
 t = tr.cpu().numpy().astype(np.int64)
-t0 = t[2002]
+t0 = t[t > 0].min()
 prod = (t[:1000][t[:1000] > 0] - t0) / 1000
 mma = (t[1000:2000][t[1000:2000] > 0] - t0) / 1000
-print(f"diag call (incl. 2 split kernels) {e0.elapsed_time(e1)*1000:.1f} us; flops {2*G*M*N*K*3/1e12:.3f} TF(tensor)")
-print("producer stage issue (us):", np.round(prod[:24], 2).tolist(), "... n =", len(prod))
-print("mma stage consume   (us):", np.round(mma[:24], 2).tolist(), "... last", np.round(mma[-1:], 2))
 cv0 = (t[3000:4000][t[3000:4000] > 0] - t0) / 1000
-cv1 = (t[4000:5000][t[4000:5000] > 0] - t0) / 1000
-print("TMA landed (conv start) (us):", np.round(cv0[:24], 2).tolist())
-print("conv done            (us):", np.round(cv1[:24], 2).tolist())
-print("epilogue start/end (us):", (t[2000] - t0) / 1000, (t[2001] - t0) / 1000)
+print(f"diag call {e0.elapsed_time(e1)*1000:.1f} us; flops {2*G*M*N*K*3/1e12:.3f} TF(tensor)")
+print("producer stage issue (us):", np.round(prod[:40], 2).tolist(), "... n =", len(prod))
+print("conv start (TMA landed):", np.round(cv0[:40], 2).tolist())
+print("mma stage issue      (us):", np.round(mma[:40], 2).tolist(), "... last", np.round(mma[-1:], 2))
+d = np.diff(mma)
+print("mma per-stage median %.3f us, mean %.3f" % (np.median(d), d.mean()))
+ep = t[2000:2032]
+for i in range(16):
+    if ep[2 * i] > 0:
+        print("tile %d epilogue %.2f -> %.2f us" % (i, (ep[2 * i] - t0) / 1000, (ep[2 * i + 1] - t0) / 1000))
