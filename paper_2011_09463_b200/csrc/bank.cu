@@ -541,14 +541,16 @@ void train_step(mtk_bank& k, const mtk_step& s, double* loss_host, double* mmd_h
             k.mmd_part_bytes = pbytes;
         }
         a.partial = k.mmd_part;
-        double* sc = c.scratch(mmd_beta_scratch_bytes(a));
-        {
+        if (a.tc) {
+            a.beta_out = k.beta;  // fused into the prep pass of launch_mmd_tc
+        } else {
+            double* sc = c.scratch(mmd_beta_scratch_bytes(a));
             PhaseScope ph(c, kPhMmdBeta, 2);
             launch_mmd_beta(a, k.beta, sc, c.stream);
             after_launch(c, 2);
         }
         {
-            PhaseScope ph(c, kPhMmdPairs, a.tc ? 2 : 1);
+            PhaseScope ph(c, kPhMmdPairs, a.tc ? 3 : 1);
             if (a.tc) {
                 const size_t zb = mmd_tc_scratch_bytes(a);
                 if (zb > k.mmd_z_bytes) {
@@ -561,7 +563,7 @@ void train_step(mtk_bank& k, const mtk_step& s, double* loss_host, double* mmd_h
             } else {
                 launch_mmd_pairs(a, c.stream);
             }
-            after_launch(c, a.tc ? 2 : 1);
+            after_launch(c, a.tc ? 3 : 1);
         }
         {
             PhaseScope ph(c, kPhOther, 1);

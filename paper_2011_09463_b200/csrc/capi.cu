@@ -234,6 +234,8 @@ static void mmd_run(mtk_ctx* c, MmdArgs& a, double beta, bool want_value, double
     double* bscratch = part_d + nblk * 3;
     if (beta > 0) {
         MTK_CUDA(cudaMemcpyAsync(beta_d, &beta, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    } else if (a.tc) {
+        a.beta_out = beta_d;  // fused into the prep pass of launch_mmd_tc
     } else {
         launch_mmd_beta(a, beta_d, bscratch, c->stream);
         after_launch(*c, 2);

@@ -206,6 +206,7 @@ struct MmdArgs {
     int nb = 5;
     float mult[8] = {0.25f, 0.5f, 1.f, 2.f, 4.f, 0.f, 0.f, 0.f};
     const double* beta = nullptr;   // [G] device (detached)
+    double* beta_out = nullptr;     // tc path: compute beta here (fused into the prep pass); == beta
     long long row_begin = 0, row_end = -1;  // concatenated-row range (all groups)
     double* partial = nullptr;      // [G, nblocks_per_group, 3] device
     float* gXs = nullptr;           // optional, layout as Xs, scaled by grad_scale
@@ -224,6 +225,9 @@ size_t mmd_tc_scratch_bytes(const MmdArgs& a);
 void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s);
 size_t mmd_beta_scratch_bytes(const MmdArgs& a);
 void launch_mmd_beta(const MmdArgs& a, double* beta_out, double* scratch, cudaStream_t s);
+// beta from partials laid out as beta_partial writes them ([G][P][d+1], P = ceil(N / 32))
+void launch_mmd_beta_finish(const MmdArgs& a, const double* part, double* beta_out, cudaStream_t s);
+constexpr int kBetaRows = 32;
 void launch_mmd_pairs(const MmdArgs& a, cudaStream_t s);
 // value[g] = cSS*ss + cTT*tt + cST*st from the per-block partials (fixed order)
 void launch_mmd_finish(const MmdArgs& a, double* value, double* sums3, cudaStream_t s);

@@ -1,8 +1,12 @@
 // k_head.cu -- skinny GEMMs for narrow layers (the 10-class head, the 2-class
-// attack head): out widths <= 32 do not fill a 128-wide tile, so these run
-// as warp-per-row (forward) and thread-per-input-feature (dW + SGD) kernels.
+// attack head): output widths <= 32 do not fill a 128-wide MMA tile, so these
+// are memory-bound SIMT kernels, templated on the padded width NP (a multiple
+// of 4) so every per-output loop is fully unrolled with no dead lanes.
 //   forward  logits = H W + b          (tape.hpp:36-48 mm_acc + add_bias)
+//   dX       dH = (dZ W^T [+ add]) * (H > 0)   (tape.hpp:50-63 mm_nt_acc, :349)
 //   dW + SGD W -= lr * H^T dZ          (tape.hpp:65-78 mm_tn_acc; optim.hpp:46-48)
+// Register blocking keeps the shared-memory wavefront count per FMA low: the
+// narrow operand (W row or dZ row) is read as broadcast float4.
 // Reductions run in a fixed order (bit-deterministic).
 #include <cmath>
 
@@ -14,124 +18,192 @@ namespace {
 
 constexpr int MAXN = 32;
 
-// forward: block = 64 rows of model g, 256 threads (4 per row, each owning
-// outputs n = t%4, t%4+4, ...); A and W staged through smem in 64-wide k
-// chunks with coalesced loads.
+__device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+
+// ---- forward: block = 64 rows x 2 k-halves (128 threads); thread owns one row
+// and all NP outputs; A and W staged through smem in 64-wide k chunks.
 constexpr int FR = 64, FK = 64;
-__global__ void __launch_bounds__(256) head_fwd_kernel(HeadFwd p) {
+template <int NP>
+__global__ void __launch_bounds__(128) head_fwd_kernel(HeadFwd p) {
     __shared__ float sA[FR][FK + 1];
-    __shared__ float sW[FK][MAXN + 1];
+    __shared__ __align__(16) float sW[FK][NP];
+    __shared__ float red[FR][NP + 1];
     const int g = blockIdx.y;
     const int r0 = blockIdx.x * FR;
-    const int N = p.N;
-    const int row = threadIdx.x >> 2, sub = threadIdx.x & 3;
+    const int N = p.N, t = threadIdx.x;
+    const int row = t & (FR - 1), half = t >> 6;
     const float* A = p.A + g * p.a_gs;
     const float* W = p.W + g * p.w_gs;
-    float acc[MAXN / 4];
+    const bool vec = (p.lda % 4 == 0) && (p.K % 4 == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
+    float acc[NP];
 #pragma unroll
-    for (int i = 0; i < MAXN / 4; ++i) acc[i] = 0.f;
+    for (int n = 0; n < NP; ++n) acc[n] = 0.f;
     for (int k0 = 0; k0 < p.K; k0 += FK) {
         const int kc = min(FK, p.K - k0);
         __syncthreads();
-        for (int e = threadIdx.x; e < FR * FK; e += 256) {
-            const int rr = e / FK, kk = e % FK;
-            sA[rr][kk] = (r0 + rr < p.rows && kk < kc) ? A[(long long)(r0 + rr) * p.lda + k0 + kk] : 0.f;
+        if (vec) {
+            float4 v[FR * FK / 4 / 128];  // all loads in flight before the smem stores
+#pragma unroll
+            for (int i = 0; i < FR * FK / 4 / 128; ++i) {
+                const int e = t + 128 * i, rr = e / (FK / 4), c4 = e % (FK / 4);
+                v[i] = (r0 + rr < p.rows && 4 * c4 < kc) ? ldg4(A + (long long)(r0 + rr) * p.lda + k0 + 4 * c4)
+                                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int i = 0; i < FR * FK / 4 / 128; ++i) {
+                const int e = t + 128 * i, rr = e / (FK / 4), c4 = e % (FK / 4);
+                sA[rr][4 * c4] = v[i].x;
+                sA[rr][4 * c4 + 1] = v[i].y;
+                sA[rr][4 * c4 + 2] = v[i].z;
+                sA[rr][4 * c4 + 3] = v[i].w;
+            }
+        } else {
+            for (int e = t; e < FR * FK; e += 128) {
+                const int rr = e / FK, kk = e % FK;
+                sA[rr][kk] = (r0 + rr < p.rows && kk < kc) ? A[(long long)(r0 + rr) * p.lda + k0 + kk] : 0.f;
+            }
         }
-        for (int e = threadIdx.x; e < FK * N; e += 256) {
-            const int kk = e / N, n = e % N;
-            sW[kk][n] = kk < kc ? W[(long long)(k0 + kk) * N + n] : 0.f;
+        for (int e = t; e < FK * NP; e += 128) {
+            const int kk = e / NP, n = e % NP;
+            sW[kk][n] = (kk < kc && n < N) ? W[(long long)(k0 + kk) * N + n] : 0.f;
         }
         __syncthreads();
 #pragma unroll 4
-        for (int kk = 0; kk < FK; ++kk) {
+        for (int kk = half; kk < FK; kk += 2) {
             const float a = sA[row][kk];
 #pragma unroll
-            for (int i = 0; i < MAXN / 4; ++i) {
-                const int n = sub + 4 * i;
-                if (n < N) acc[i] = fmaf(a, sW[kk][n], acc[i]);
+            for (int n4 = 0; n4 < NP / 4; ++n4) {
+                const float4 w = *reinterpret_cast<const float4*>(&sW[kk][4 * n4]);
+                acc[4 * n4] = fmaf(a, w.x, acc[4 * n4]);
+                acc[4 * n4 + 1] = fmaf(a, w.y, acc[4 * n4 + 1]);
+                acc[4 * n4 + 2] = fmaf(a, w.z, acc[4 * n4 + 2]);
+                acc[4 * n4 + 3] = fmaf(a, w.w, acc[4 * n4 + 3]);
             }
         }
     }
-    const int r = r0 + row;
-    if (r >= p.rows) return;
-    bool bad = false;
+    if (half == 1)
 #pragma unroll
-    for (int i = 0; i < MAXN / 4; ++i) {
-        const int n = sub + 4 * i;
+        for (int n = 0; n < NP; ++n) red[row][n] = acc[n];
+    __syncthreads();
+    const int r = r0 + row;
+    if (half == 1 || r >= p.rows) return;
+    bool bad = false;
+    float* out = p.C + g * p.c_gs + (long long)r * p.ldc;
+#pragma unroll
+    for (int n = 0; n < NP; ++n) {
         if (n >= N) break;
-        float v = acc[i] + p.bias[g * p.bias_gs + n];
+        float v = (acc[n] + red[row][n]) + p.bias[g * p.bias_gs + n];
         bad |= !isfinite(v);
         if (p.relu) v = v > 0.f ? v : 0.f;
-        p.C[g * p.c_gs + (long long)r * p.ldc + n] = v;
+        out[n] = v;
+        if (p.C_hi) {
+            float h, l;
+            sm100::split_tf32(v, h, l);
+            p.C_hi[g * p.c_gs + (long long)r * p.ldc + n] = h;
+            p.C_lo[g * p.c_gs + (long long)r * p.ldc + n] = l;
+        }
     }
     if (bad && p.flags) atomicOr(p.flags, kFlagNonFinite);
 }
 
-// dX through a narrow layer: out[r, q] = (sum_j dz[r, j] W[q, j] + add[r, q]) *
-// (mask[r, q] > 0), j < N <= 32.  Block = 32 rows of model g; W (K x N) and
-// the dz rows in smem; threads stride q so mask/add/out are coalesced.
+// ---- dX: out[r, q] = (sum_j dz[r, j] W[q, j] + add[r, q]) * (mask[r, q] > 0).
+// Block = 32 rows of model g; thread owns input feature q with W[q, :] in
+// registers; dz rows are broadcast float4 reads from smem; mask/add/out are
+// coalesced over q.
+template <int NP>
 __global__ void __launch_bounds__(256) head_dx_kernel(HeadDx p) {
-    extern __shared__ float sm[];
-    const int N = p.N, ld = N | 1;
-    float* sW = sm;                      // [K][ld]
-    float* sdz = sm + (size_t)p.K * ld;  // [32][ld]
+    __shared__ __align__(16) float sdz[32][NP];
+    const int N = p.N;
     const int g = blockIdx.y;
     const int r0 = blockIdx.x * 32;
-    const float* W = p.W + g * p.w_gs;
-    for (int e = threadIdx.x; e < p.K * N; e += blockDim.x) sW[(e / N) * ld + e % N] = W[e];
-    for (int e = threadIdx.x; e < 32 * N; e += blockDim.x) {
-        const int rr = e / N, j = e % N;
-        sdz[rr * ld + j] = (r0 + rr < p.rows) ? p.dZ[g * p.dz_gs + (long long)(r0 + rr) * p.lddz + j] : 0.f;
+    const int nrows = min(32, p.rows - r0);
+    for (int e = threadIdx.x; e < 32 * NP; e += blockDim.x) {
+        const int rr = e / NP, j = e % NP;
+        sdz[rr][j] = (rr < nrows && j < N) ? p.dZ[g * p.dz_gs + (long long)(r0 + rr) * p.lddz + j] : 0.f;
     }
     __syncthreads();
-    for (int rr = 0; rr < 32 && r0 + rr < p.rows; ++rr) {
-        const long long rowb = g * p.c_gs + (long long)(r0 + rr) * p.ldc;
-        for (int q = threadIdx.x; q < p.K; q += blockDim.x) {
-            float acc = 0.f;
-#pragma unroll 8
-            for (int j = 0; j < N; ++j) acc = fmaf(sdz[rr * ld + j], sW[q * ld + j], acc);
-            const long long idx = rowb + q;
-            if (p.add) acc = p.add[idx] + acc;
-            p.C[idx] = (p.mask[idx] > 0.f) ? acc : 0.f;
+    const float* W = p.W + g * p.w_gs;
+    for (int q = threadIdx.x; q < p.K; q += blockDim.x) {
+        float w[NP];
+#pragma unroll
+        for (int j = 0; j < NP; ++j) w[j] = j < N ? W[(long long)q * N + j] : 0.f;
+        for (int rb = 0; rb < nrows; rb += 8) {
+            float mk[8], ad[8];  // all loads of the batch in flight together
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const long long idx = g * p.c_gs + (long long)(r0 + rb + i) * p.ldc + q;
+                const bool ok = rb + i < nrows;
+                mk[i] = ok ? __ldg(p.mask + idx) : 0.f;
+                ad[i] = (ok && p.add) ? __ldg(p.add + idx) : 0.f;
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                if (rb + i >= nrows) break;
+                float acc = 0.f;
+#pragma unroll
+                for (int j4 = 0; j4 < NP / 4; ++j4) {
+                    const float4 z = *reinterpret_cast<const float4*>(&sdz[rb + i][4 * j4]);
+                    acc = fmaf(z.x, w[4 * j4], acc);
+                    acc = fmaf(z.y, w[4 * j4 + 1], acc);
+                    acc = fmaf(z.z, w[4 * j4 + 2], acc);
+                    acc = fmaf(z.w, w[4 * j4 + 3], acc);
+                }
+                if (p.add) acc = ad[i] + acc;
+                p.C[g * p.c_gs + (long long)(r0 + rb + i) * p.ldc + q] = (mk[i] > 0.f) ? acc : 0.f;
+            }
         }
     }
 }
 
-// dW partials: block (p-chunk of 64 input features, model g, row split rs),
-// 256 threads = 4 row groups x 64 features; partial[rs][g][p][n]
+// ---- dW partials: block (64 features p, model g, row split rs); 4 row groups
+// of 64 threads; thread owns feature p with NP accumulators; dz rows are
+// broadcast float4 reads from smem.
 constexpr int RS = 8;
+template <int NP>
 __global__ void __launch_bounds__(256) head_dw_partial_kernel(HeadDw p) {
-    __shared__ float sdz[64][MAXN + 1];
-    __shared__ float red[4][64][MAXN + 1];
+    __shared__ __align__(16) float sdz[64][NP];
+    __shared__ float red[4][64][NP + 1];
     const int g = blockIdx.y, rs = blockIdx.z;
     const int pl = threadIdx.x & 63, rg = threadIdx.x >> 6;
     const int pp = blockIdx.x * 64 + pl;
     const int N = p.N;
     const int rbeg = (int)((long long)p.rows * rs / RS), rend = (int)((long long)p.rows * (rs + 1) / RS);
-    float acc[MAXN];
+    float acc[NP];
 #pragma unroll
-    for (int n = 0; n < MAXN; ++n) acc[n] = 0.f;
+    for (int n = 0; n < NP; ++n) acc[n] = 0.f;
     const float* A = p.A + g * p.a_gs;
     const float* dz = p.dZ + g * p.dz_gs;
     for (int r0 = rbeg; r0 < rend; r0 += 64) {
         __syncthreads();
-        for (int i = threadIdx.x; i < 64 * N; i += blockDim.x) {
-            const int rr = i / N, n = i % N;
-            sdz[rr][n] = (r0 + rr < rend) ? dz[(long long)(r0 + rr) * p.lddz + n] : 0.f;
+        for (int i = threadIdx.x; i < 64 * NP; i += blockDim.x) {
+            const int rr = i / NP, n = i % NP;
+            sdz[rr][n] = (r0 + rr < rend && n < N) ? dz[(long long)(r0 + rr) * p.lddz + n] : 0.f;
         }
         __syncthreads();
         if (pp < p.K) {
             const int lim = min(64, rend - r0);
-#pragma unroll 4
-            for (int rr = rg; rr < lim; rr += 4) {
-                const float av = __ldg(A + (long long)(r0 + rr) * p.lda + pp);
+            float av[16];  // this thread's 16 rows of the chunk, loads in flight together
 #pragma unroll
-                for (int n = 0; n < MAXN; ++n)
-                    if (n < N) acc[n] = fmaf(av, sdz[rr][n], acc[n]);
+            for (int i = 0; i < 16; ++i) {
+                const int rr = rg + 4 * i;
+                av[i] = rr < lim ? __ldg(A + (long long)(r0 + rr) * p.lda + pp) : 0.f;
+            }
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int rr = rg + 4 * i;
+#pragma unroll
+                for (int n4 = 0; n4 < NP / 4; ++n4) {
+                    const float4 z = *reinterpret_cast<const float4*>(&sdz[rr][4 * n4]);
+                    acc[4 * n4] = fmaf(av[i], z.x, acc[4 * n4]);
+                    acc[4 * n4 + 1] = fmaf(av[i], z.y, acc[4 * n4 + 1]);
+                    acc[4 * n4 + 2] = fmaf(av[i], z.z, acc[4 * n4 + 2]);
+                    acc[4 * n4 + 3] = fmaf(av[i], z.w, acc[4 * n4 + 3]);
+                }
             }
         }
     }
-    for (int n = 0; n < N; ++n) red[rg][pl][n] = acc[n];
+#pragma unroll
+    for (int n = 0; n < NP; ++n) red[rg][pl][n] = acc[n];
     __syncthreads();
     if (rg == 0 && pp < p.K)
         for (int n = 0; n < N; ++n)
@@ -161,30 +233,55 @@ __global__ void head_dw_finish_kernel(HeadDw p) {
     }
 }
 
+template <template <int> class Launch, typename P>
+void by_width(int N, const P& p, cudaStream_t s) {
+    switch ((N + 3) / 4) {
+        case 1: Launch<4>::run(p, s); break;
+        case 2: Launch<8>::run(p, s); break;
+        case 3: Launch<12>::run(p, s); break;
+        case 4: Launch<16>::run(p, s); break;
+        case 5: Launch<20>::run(p, s); break;
+        case 6: Launch<24>::run(p, s); break;
+        case 7: Launch<28>::run(p, s); break;
+        case 8: Launch<32>::run(p, s); break;
+        default: fail(MTK_ERROR, "head: output width above 32");
+    }
+}
+
+template <int NP>
+struct FwdLaunch {
+    static void run(const HeadFwd& p, cudaStream_t s) {
+        head_fwd_kernel<NP><<<dim3((p.rows + FR - 1) / FR, p.G), 128, 0, s>>>(p);
+    }
+};
+template <int NP>
+struct DxLaunch {
+    static void run(const HeadDx& p, cudaStream_t s) {
+        head_dx_kernel<NP><<<dim3((p.rows + 31) / 32, p.G), 256, 0, s>>>(p);
+    }
+};
+template <int NP>
+struct DwLaunch {
+    static void run(const HeadDw& p, cudaStream_t s) {
+        head_dw_partial_kernel<NP><<<dim3((p.K + 63) / 64, p.G, RS), 256, 0, s>>>(p);
+    }
+};
+
 }  // namespace
 
-bool head_fwd_ok(int K, int N) { return N <= MAXN && K >= 1; }
-bool head_dx_ok(int K, int N) { return N <= MAXN && (size_t)(K + 32) * (N | 1) * 4 <= 96 * 1024; }
-bool head_dw_ok(int N) { return N <= MAXN; }
+bool head_fwd_ok(int K, int N) { return N >= 1 && N <= MAXN && K >= 1; }
+bool head_dx_ok(int K, int N) { return N >= 1 && N <= MAXN && K >= 1; }
+bool head_dw_ok(int N) { return N >= 1 && N <= MAXN; }
 
 void launch_head_fwd(const HeadFwd& p, cudaStream_t s) {
     if (p.rows <= 0) return;
-    dim3 grid((p.rows + FR - 1) / FR, p.G);
-    head_fwd_kernel<<<grid, 256, 0, s>>>(p);
+    by_width<FwdLaunch>(p.N, p, s);
     count_launch();
 }
 
 void launch_head_dx(const HeadDx& p, cudaStream_t s) {
     if (p.rows <= 0) return;
-    const size_t smem = (size_t)(p.K + 32) * (p.N | 1) * sizeof(float);
-    static bool attr = false;
-    if (!attr) {
-        MTK_CUDA(cudaFuncSetAttribute(head_dx_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      96 * 1024));
-        attr = true;
-    }
-    dim3 grid((p.rows + 31) / 32, p.G);
-    head_dx_kernel<<<grid, 256, smem, s>>>(p);
+    by_width<DxLaunch>(p.N, p, s);
     count_launch();
 }
 
@@ -193,8 +290,7 @@ size_t head_dw_scratch_bytes(int G, int K, int N) { return (size_t)RS * G * K * 
 void launch_head_dw(const HeadDw& p, cudaStream_t s) {
     if (p.K <= 0) return;
     if (!p.partial) fail(MTK_ERROR, "head_dw: missing partial scratch");
-    dim3 grid((p.K + 63) / 64, p.G, RS);
-    head_dw_partial_kernel<<<grid, 256, 0, s>>>(p);
+    by_width<DwLaunch>(p.N, p, s);
     count_launch();
     const long long n = (long long)p.G * p.K * p.N;
     head_dw_finish_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(p);

@@ -178,26 +178,37 @@ __global__ void row_sum_kernel(const double* row_loss, int B, double* loss, int*
     }
 }
 
-// db = column sums of dZ, b -= lr * db.  Block = 32 columns x 8 row groups;
-// each thread sums a strided row subset, then the 8 partials are combined in a
-// fixed order (deterministic, no atomics).
-__global__ void bias_sgd_kernel(int G, int rows, int N, const float* dZ, long long dz_gs, float* b,
-                                long long b_gs, float lr, float* grad_out, int* flags) {
-    __shared__ float part[8][33];
+// db = column sums of dZ, b -= lr * db.  Block = 32 columns x 32 row groups;
+// each thread sums a strided row subset (loads batched 8 deep), then the 32
+// partials are combined in a fixed order (deterministic, no atomics).
+constexpr int BS_GROUPS = 32;
+__global__ void __launch_bounds__(32 * BS_GROUPS) bias_sgd_kernel(int G, int rows, int N, const float* dZ,
+                                                                  long long dz_gs, float* b, long long b_gs,
+                                                                  float lr, float* grad_out, int* flags) {
+    __shared__ float part[BS_GROUPS][33];
     const int g = blockIdx.y;
     const int n = blockIdx.x * 32 + (threadIdx.x & 31);
     const int rg = threadIdx.x >> 5;
     float s = 0.f;
     if (n < N) {
         const float* col = dZ + g * dz_gs + n;
-        for (int r = rg; r < rows; r += 8) s += col[(long long)r * N];
+        for (int r = rg; r < rows; r += 8 * BS_GROUPS) {
+            float v[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int rr = r + i * BS_GROUPS;
+                v[i] = rr < rows ? __ldg(col + (long long)rr * N) : 0.f;
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) s += v[i];
+        }
     }
     part[rg][threadIdx.x & 31] = s;
     __syncthreads();
     if (rg == 0 && n < N) {
         float t = 0.f;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) t += part[q][threadIdx.x];
+        for (int q = 0; q < BS_GROUPS; ++q) t += part[q][threadIdx.x];
         if (grad_out) grad_out[g * b_gs + n] = t;
         const float v = b[g * b_gs + n] - lr * t;
         if (!isfinite(v)) atomicOr(flags, kFlagNonFinite);
@@ -225,7 +236,7 @@ void launch_ce(const CeArgs& a, cudaStream_t s) {
 void launch_bias_sgd(int G, int rows, int N, const float* dZ, long long dz_gs, float* b,
                      long long b_gs, float lr, float* grad_out, int* flags, cudaStream_t s) {
     dim3 grid((N + 31) / 32, G);
-    bias_sgd_kernel<<<grid, 256, 0, s>>>(G, rows, N, dZ, dz_gs, b, b_gs, lr, grad_out, flags);
+    bias_sgd_kernel<<<grid, 32 * BS_GROUPS, 0, s>>>(G, rows, N, dZ, dz_gs, b, b_gs, lr, grad_out, flags);
     count_launch();
 }
 

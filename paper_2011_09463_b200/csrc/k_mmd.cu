@@ -24,7 +24,7 @@ __device__ __forceinline__ const float* row_ptr(const MmdArgs& a, int g, long lo
 }
 
 // beta partials: block (p, g) sums rows [p*R, p*R+R) -> sum z (per dim), sum |z|^2
-constexpr int BETA_ROWS = 32;
+constexpr int BETA_ROWS = kBetaRows;
 __global__ void beta_partial_kernel(MmdArgs a, double* part, int P) {
     const int g = blockIdx.y, p = blockIdx.x;
     const long long N = a.m + a.n;
@@ -265,6 +265,13 @@ void launch_mmd_beta(const MmdArgs& a, double* beta_out, double* scratch, cudaSt
     beta_partial_kernel<<<dim3(P, a.G), NT, 0, s>>>(a, scratch, P);
     count_launch();
     beta_finish_kernel<<<a.G, NT, 0, s>>>(a, scratch, P, beta_out);
+    count_launch();
+}
+
+void launch_mmd_beta_finish(const MmdArgs& a, const double* part, double* beta_out, cudaStream_t s) {
+    const long long N = a.m + a.n;
+    const int P = (int)((N + BETA_ROWS - 1) / BETA_ROWS);
+    beta_finish_kernel<<<a.G, NT, 0, s>>>(a, part, P, beta_out);
     count_launch();
 }
 

@@ -13,8 +13,12 @@
 //          w is split into tf32 hi/lo and written back to TMEM (hi over S,
 //          lo in cols [384,512)) -- FlashAttention-4 style, no smem round trip
 //   GEMM2  V[128xVD] += W[128x128] . Z_j[128xVD]  (A from TMEM; cols [0,VD))
-// Operands are the tf32 hi/lo planes of Z (HBM, [G][N][d]); all products are
-// 3xTF32 (hi*hi + hi*lo + lo*hi).  One warp issues TMA, one issues MMAs.
+// Operands are the tf32 hi/lo planes of Z ([G][N][d] each, written by
+// mmd_prep_kernel together with the row norms); all products are 3xTF32
+// (hi*hi + hi*lo + lo*hi).  TMA brings both planes, so the 128-B/clk shared
+// memory port carries only TMA writes and tensor-core reads (an on-chip split
+// adds a read and two writes per element and made the kernel smem-bound).
+// One warp issues TMA, one issues MMAs, four run the exp epilogue.
 #include <cuda.h>
 
 #include <cmath>
@@ -30,24 +34,21 @@ using namespace sm100;
 
 constexpr int TI = 128, TJ = 64, KC = 32, JC = 16, VD = 256;
 constexpr int STAGES = 4;
-constexpr int G1_BYTES = 2 * (TI * KC * 4) + 2 * (TJ * KC * 4);  // 48 KB (fp32 + lo planes)
+constexpr int G1_BYTES = 2 * (TI * KC * 4) + 2 * (TJ * KC * 4);  // 48 KB (hi + lo planes)
 constexpr int G2_BYTES = 2 * (JC * VD * 4);                       // 32 KB
-constexpr int G1_LOAD = G1_BYTES / 2;                             // TMA brings the fp32 half
-constexpr int G2_LOAD = G2_BYTES / 2;
 constexpr int STAGE_BYTES = G1_BYTES;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
-constexpr int CONV_WARPS = 4;
-constexpr int NUM_THREADS = 192 + 32 * CONV_WARPS;  // + lo-plane converter warps
+constexpr int NUM_THREADS = 192;
 // TMEM columns: V [0,256); S / W-hi double buffer b at 256 + 64 b (S is
 // overwritten in place by the hi plane of W); W-lo buffer b at 384 + 64 b.
 constexpr uint32_t S_COL = 256;
 constexpr uint32_t WLO_COL = 384;
 
 struct MmdTcParams {
-    CUtensorMap zk;             // K-major view of Z (fp32): (d, N, G), box (32, 64)
-    CUtensorMap zm;             // MN-major view: (d, N, G), box (32, 16), 32-B atom swizzle
-    const float* z;             // Z rows (fp32), for z_i in the gradient epilogue
-    long long z_rs, z_gs;       // row / group strides of z
+    CUtensorMap zk_hi, zk_lo;   // K-major views of the planes: (d, N, G), box (32, 64)
+    CUtensorMap zm_hi, zm_lo;   // MN-major views: (d, N, G), box (32, 16), 32-B atom swizzle
+    const float* zhi;           // [G][N][d] planes, for z_i = hi + lo in the gradient epilogue
+    const float* zlo;
     const float* norms;         // [G][N]
     const double* beta;         // [G]
     long long m, n;
@@ -90,8 +91,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-    uint64_t* conv = full + STAGES;
-    uint64_t* empty = conv + STAGES;
+    uint64_t* empty = full + STAGES;
     uint64_t* s_full = empty + STAGES;  // [2]
     uint64_t* w_full = s_full + 2;      // [2]
     uint64_t* v_full = w_full + 2;
@@ -113,11 +113,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
         (p.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) ? p.trace : nullptr;
 
     if (warp == 0 && lane == 0) {
-        tma_prefetch(&p.zk);
-        tma_prefetch(&p.zm);
+        tma_prefetch(&p.zk_hi);
+        tma_prefetch(&p.zk_lo);
+        tma_prefetch(&p.zm_hi);
+        tma_prefetch(&p.zm_lo);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&conv[s], CONV_WARPS);
             mbar_init(&empty[s], 1);
         }
         for (int b = 0; b < 2; ++b) {
@@ -149,13 +150,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
                         mbar_wait(&empty[s], ((st / STAGES) & 1) ^ 1);
                         TRACE(0, st);
                         uint8_t* b = smem + s * STAGE_BYTES;
-                        mbar_expect_tx(&full[s], G1_LOAD);
+                        mbar_expect_tx(&full[s], G1_BYTES);
                         const int k0 = kc * KC;
-                        // fp32 Z_i (two 64-row boxes) at [0,16K), fp32 Z_j at [32K,40K);
-                        // the converters fill the lo planes at [16K,32K) and [40K,48K)
-                        tma_load_3d(b, &p.zk, &full[s], k0, (int)i0, g);
-                        tma_load_3d(b + 8192, &p.zk, &full[s], k0, (int)i0 + 64, g);
-                        tma_load_3d(b + 32768, &p.zk, &full[s], k0, j0, g);
+                        // Z_i hi [0,16K) and lo [16K,32K) (two 64-row boxes each),
+                        // Z_j hi [32K,40K) and lo [40K,48K)
+                        tma_load_3d(b, &p.zk_hi, &full[s], k0, (int)i0, g);
+                        tma_load_3d(b + 8192, &p.zk_hi, &full[s], k0, (int)i0 + 64, g);
+                        tma_load_3d(b + 16384, &p.zk_lo, &full[s], k0, (int)i0, g);
+                        tma_load_3d(b + 24576, &p.zk_lo, &full[s], k0, (int)i0 + 64, g);
+                        tma_load_3d(b + 32768, &p.zk_hi, &full[s], k0, j0, g);
+                        tma_load_3d(b + 40960, &p.zk_lo, &full[s], k0, j0, g);
                     }
                 }
                 if (t >= 1) {
@@ -165,9 +169,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
                         mbar_wait(&empty[s], ((st / STAGES) & 1) ^ 1);
                         TRACE(0, st);
                         uint8_t* b = smem + s * STAGE_BYTES;
-                        mbar_expect_tx(&full[s], G2_LOAD);
-                        for (int q = 0; q < VD / 32; ++q)
-                            tma_load_3d(b + q * 2048, &p.zm, &full[s], v0 + 32 * q, j0 + JC * jc, g);
+                        mbar_expect_tx(&full[s], G2_BYTES);
+                        for (int q = 0; q < VD / 32; ++q) {
+                            tma_load_3d(b + q * 2048, &p.zm_hi, &full[s], v0 + 32 * q, j0 + JC * jc, g);
+                            tma_load_3d(b + 16384 + q * 2048, &p.zm_lo, &full[s], v0 + 32 * q,
+                                        j0 + JC * jc, g);
+                        }
                     }
                 }
             }
@@ -184,7 +191,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
                     const uint32_t tS = tmem + S_COL + (t & 1) * TJ;
                     for (int kc = 0; kc < nkc; ++kc, ++st) {
                         const int s = st % STAGES;
-                        mbar_wait(&conv[s], (st / STAGES) & 1);
+                        mbar_wait(&full[s], (st / STAGES) & 1);
                         TRACE(4096, st);
                         tc_fence_after();
                         const uint32_t b = smem_u32(smem + s * STAGE_BYTES);
@@ -215,7 +222,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
                     }
                     for (int jc = 0; jc < TJ / JC; ++jc, ++st) {
                         const int s = st % STAGES;
-                        mbar_wait(&conv[s], (st / STAGES) & 1);
+                        mbar_wait(&full[s], (st / STAGES) & 1);
                         TRACE(4096, st);
                         tc_fence_after();
                         const uint32_t b = smem_u32(smem + s * STAGE_BYTES);
@@ -235,50 +242,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
                 }
             }
             mma_commit(v_full);
-        }
-    } else if (warp >= 6) {
-        // ---------------- lo-plane converters: same stage order as the producer ----------------
-        const int t = threadIdx.x - 192;
-        constexpr int NT = 32 * CONV_WARPS;
-        int st = 0;
-        auto convert = [&](uint8_t* b, int src, int bytes) {
-            const float4* in = reinterpret_cast<const float4*>(b + src);
-            float4* out = reinterpret_cast<float4*>(b + src + bytes);
-            for (int e = t; e < bytes / 16; e += NT) {
-                const float4 x = in[e];
-                float4 h, l;
-                split_tf32(x.x, h.x, l.x);
-                split_tf32(x.y, h.y, l.y);
-                split_tf32(x.z, h.z, l.z);
-                split_tf32(x.w, h.w, l.w);
-                const_cast<float4*>(in)[e] = h;  // hi = rna(x) in place, |lo| <= 2^-11 |x|
-                out[e] = l;
-            }
-        };
-        auto publish = [&](int s) {
-            fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&conv[s]);
-        };
-        for (int tt = 0; tt <= njt; ++tt) {
-            if (tt < njt) {
-                for (int kc = 0; kc < nkc; ++kc, ++st) {
-                    const int s = st % STAGES;
-                    mbar_wait(&full[s], (st / STAGES) & 1);
-                    uint8_t* b = smem + s * STAGE_BYTES;
-                    convert(b, 0, 16384);      // Z_i fp32 -> lo
-                    convert(b, 32768, 8192);   // Z_j fp32 -> lo
-                    publish(s);
-                }
-            }
-            if (tt >= 1) {
-                for (int jc = 0; jc < TJ / JC; ++jc, ++st) {
-                    const int s = st % STAGES;
-                    mbar_wait(&full[s], (st / STAGES) & 1);
-                    convert(smem + s * STAGE_BYTES, 0, 16384);  // Z_j (MN-major) -> lo
-                    publish(s);
-                }
-            }
         }
     } else {
         // ---------------- epilogue warps: exp + weights, then the gradient ----------------
@@ -443,7 +406,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
             const int rr = e / VD, k = e % VD;
             const long long row = i0 + rr;
             float z = 0.f;
-            if (k < vd && row < N) z = p.z[g * p.z_gs + row * p.z_rs + v0 + k];
+            if (k < vd && row < N) {
+                const long long o = ((long long)g * N + row) * p.d + v0 + k;
+                z = p.zhi[o] + p.zlo[o];
+            }
             zs[rr * (VD + 1) + k] = z;
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -488,26 +454,72 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
     }
 }
 
-// n_i = |z_i|^2 (fp64 accumulation) for the rows of Z = [Xs; Xt]; with `zc`
-// non-null the rows are also copied into a contiguous [G][N][d] buffer (used
-// when Xs and Xt are separate allocations).  One warp per row.
-__global__ void mmd_prep_kernel(const float* Xs, long long xs_gs, const float* Xt, long long xt_gs,
-                                long long m, long long n, int d, float* zc, float* norms) {
+// n_i = |z_i|^2 (fp64 accumulation) and the tf32 planes hi = rna(z),
+// lo = rna(z - hi) of Z = [Xs; Xt] as [G][N][d] each.  Block = kBetaRows rows
+// (8 warps x 4 rows, one warp per row, float4; d % 4 == 0 on this path).
+// With `part` non-null it also writes the bandwidth partials of its rows in
+// beta_partial's layout: part[g][blk][c] = sum_rows z_c, part[g][blk][d] =
+// sum_rows n_i (fp64, fixed order), so beta costs no second pass over Z.
+constexpr int PREP_WARPS = 8;
+__global__ void __launch_bounds__(256) mmd_prep_kernel(const float* Xs, long long xs_gs, const float* Xt,
+                                                       long long xt_gs, long long m, long long n, int d,
+                                                       float* zhi, float* zlo, float* norms,
+                                                       double* part) {
+    extern __shared__ double colsum[];  // [PREP_WARPS][d] when part != null
+    __shared__ double nsum[PREP_WARPS];
     const int g = blockIdx.y;
     const long long N = m + n;
-    const long long row = blockIdx.x * (long long)(blockDim.x / 32) + (threadIdx.x >> 5);
-    if (row >= N) return;
-    const int lane = threadIdx.x & 31;
-    const float* src = row < m ? Xs + g * xs_gs + row * d : Xt + g * xt_gs + (row - m) * d;
-    float* dst = zc ? zc + ((long long)g * N + row) * d : nullptr;
-    double acc = 0.0;
-    for (int k = lane; k < d; k += 32) {
-        const float x = src[k];
-        if (dst) dst[k] = x;
-        acc += (double)x * (double)x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int d4 = d / 4;
+    double* cs = part ? colsum + warp * d : nullptr;
+    if (cs)
+        for (int c = lane; c < d; c += 32) cs[c] = 0.0;
+    double nacc = 0.0;
+    for (int i = 0; i < kBetaRows / PREP_WARPS; ++i) {
+        const long long row = (long long)blockIdx.x * kBetaRows + warp * (kBetaRows / PREP_WARPS) + i;
+        if (row >= N) break;
+        const float4* src = reinterpret_cast<const float4*>(row < m ? Xs + g * xs_gs + row * d
+                                                                    : Xt + g * xt_gs + (row - m) * d);
+        const long long o = ((long long)g * N + row) * d;
+        float4* hi = reinterpret_cast<float4*>(zhi + o);
+        float4* lo = reinterpret_cast<float4*>(zlo + o);
+        double acc = 0.0;
+        for (int k = lane; k < d4; k += 32) {
+            const float4 x = src[k];
+            float4 h, l;
+            split_tf32(x.x, h.x, l.x);
+            split_tf32(x.y, h.y, l.y);
+            split_tf32(x.z, h.z, l.z);
+            split_tf32(x.w, h.w, l.w);
+            hi[k] = h;
+            lo[k] = l;
+            acc += (double)x.x * (double)x.x + (double)x.y * (double)x.y;
+            acc += (double)x.z * (double)x.z + (double)x.w * (double)x.w;
+            if (cs) {  // lanes own disjoint columns: no races
+                cs[4 * k] += (double)x.x;
+                cs[4 * k + 1] += (double)x.y;
+                cs[4 * k + 2] += (double)x.z;
+                cs[4 * k + 3] += (double)x.w;
+            }
+        }
+        for (int o2 = 16; o2 > 0; o2 >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o2);
+        if (lane == 0) norms[(long long)g * N + row] = (float)acc;
+        nacc += acc;
     }
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) norms[(long long)g * N + row] = (float)acc;
+    if (!part) return;
+    if (lane == 0) nsum[warp] = nacc;
+    __syncthreads();
+    double* out = part + ((long long)g * gridDim.x + blockIdx.x) * (d + 1);
+    for (int c = threadIdx.x; c < d; c += blockDim.x) {
+        double t = 0.0;
+        for (int w = 0; w < PREP_WARPS; ++w) t += colsum[w * d + c];
+        out[c] = t;
+    }
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < PREP_WARPS; ++w) t += nsum[w];
+        out[d] = t;
+    }
 }
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -562,15 +574,11 @@ static bool needs_flush(const MmdArgs& a) {
     return grads && (N + TJ - 1) / TJ > FLUSH;
 }
 
-// Xs and Xt already form one [G][N][d] block (the bank's hidden layer): no copy
-static bool contiguous(const MmdArgs& a) {
-    return a.Xt == a.Xs + a.m * a.d && a.xs_gs == a.xt_gs && (a.G == 1 || a.xs_gs >= (a.m + a.n) * a.d);
-}
-
 size_t mmd_tc_scratch_bytes(const MmdArgs& a) {
     const long long N = a.m + a.n;
     size_t b = (size_t)a.G * N * sizeof(float) + 1024;
-    if (!contiguous(a)) b += (size_t)a.G * N * a.d * sizeof(float) + 256;
+    b += 2 * ((size_t)a.G * N * a.d * sizeof(float) + 256);
+    if (a.beta_out) b += (size_t)a.G * ((N + kBetaRows - 1) / kBetaRows) * (a.d + 1) * sizeof(double) + 256;
     if (needs_flush(a)) b += (size_t)a.G * N * a.d * sizeof(double) + 256;
     return b;
 }
@@ -582,25 +590,37 @@ void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s) {
     uintptr_t cur = (reinterpret_cast<uintptr_t>(scratch) + 255) & ~uintptr_t(255);
     float* norms = reinterpret_cast<float*>(cur);
     cur = (cur + (size_t)a.G * N * sizeof(float) + 255) & ~uintptr_t(255);
-    const bool contig = contiguous(a);
-    float* zc = nullptr;
-    if (!contig) {
-        zc = reinterpret_cast<float*>(cur);
-        cur = (cur + (size_t)a.G * N * a.d * sizeof(float) + 255) & ~uintptr_t(255);
+    float* zhi = reinterpret_cast<float*>(cur);
+    cur = (cur + (size_t)a.G * N * a.d * sizeof(float) + 255) & ~uintptr_t(255);
+    float* zlo = reinterpret_cast<float*>(cur);
+    cur = (cur + (size_t)a.G * N * a.d * sizeof(float) + 255) & ~uintptr_t(255);
+    double* vacc = nullptr;
+    if (needs_flush(a)) {
+        vacc = reinterpret_cast<double*>(cur);
+        cur = (cur + (size_t)a.G * N * a.d * sizeof(double) + 255) & ~uintptr_t(255);
     }
-    double* vacc = needs_flush(a) ? reinterpret_cast<double*>(cur) : nullptr;
-    dim3 pg((unsigned)((N + 7) / 8), a.G);
-    mmd_prep_kernel<<<pg, 256, 0, s>>>(a.Xs, a.xs_gs, a.Xt, a.xt_gs, a.m, a.n, a.d, zc, norms);
+    double* bpart = a.beta_out ? reinterpret_cast<double*>(cur) : nullptr;
+    constexpr int kFusedBetaMaxD = 512;  // colsum smem: 8 warps x d doubles
+    const bool fused_beta = bpart && a.d <= kFusedBetaMaxD;
+    if (bpart && !fused_beta) launch_mmd_beta(a, a.beta_out, bpart, s);
+    dim3 pg((unsigned)((N + kBetaRows - 1) / kBetaRows), a.G);
+    const size_t prep_smem = fused_beta ? (size_t)PREP_WARPS * a.d * sizeof(double) : 0;
+    if ((reinterpret_cast<uintptr_t>(a.Xs) | reinterpret_cast<uintptr_t>(a.Xt)) & 15 ||
+        (a.xs_gs | a.xt_gs) % 4)
+        fail(MTK_ERROR, "mmd: samples not 16-byte aligned");
+    mmd_prep_kernel<<<pg, 32 * PREP_WARPS, prep_smem, s>>>(a.Xs, a.xs_gs, a.Xt, a.xt_gs, a.m, a.n, a.d,
+                                                            zhi, zlo, norms, fused_beta ? bpart : nullptr);
     count_launch();
-    const float* Z = contig ? a.Xs : zc;
-    const long long zgs = contig ? a.xs_gs : N * a.d;
+    if (fused_beta) launch_mmd_beta_finish(a, bpart, a.beta_out, s);
+    const long long zgs = N * a.d;
     MmdTcParams p;
     std::memset(&p, 0, sizeof(p));
-    p.zk = zmap(Z, a.d, N, a.G, zgs, 64, false);  // 64-row boxes (two per 128-row tile)
-    p.zm = zmap(Z, a.d, N, a.G, zgs, JC, true);
-    p.z = Z;
-    p.z_rs = a.d;
-    p.z_gs = zgs;
+    p.zk_hi = zmap(zhi, a.d, N, a.G, zgs, 64, false);  // 64-row boxes (two per 128-row tile)
+    p.zk_lo = zmap(zlo, a.d, N, a.G, zgs, 64, false);
+    p.zm_hi = zmap(zhi, a.d, N, a.G, zgs, JC, true);
+    p.zm_lo = zmap(zlo, a.d, N, a.G, zgs, JC, true);
+    p.zhi = zhi;
+    p.zlo = zlo;
     p.norms = norms;
     p.beta = a.beta;
     p.m = a.m;
