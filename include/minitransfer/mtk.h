@@ -119,6 +119,11 @@ typedef struct {
     double mmd_lambda;  /* > 0: + lambda * MMD^2(h_src, h_tgt) on the last hidden layer */
     int mmd_nb;         /* bandwidth count (<= 8); 0 selects the 5-bandwidth default */
     double mmd_mult[8]; /* s_b = beta * mmd_mult[b], beta detached (closed form) */
+    int optimizer;      /* 0 SGD (optim.hpp:46-48), 1 Adam (optim.hpp:49-63); the bank
+                           keeps the Adam moments and step count (mtk_bank_reset_optimizer) */
+    double adam_beta1;  /* 0 selects the reference default 0.9 (optim.hpp:19) */
+    double adam_beta2;  /* 0 selects 0.999 */
+    double adam_eps;    /* 0 selects 1e-8 */
 } mtk_step;
 
 /* One SGD step for all G models.  loss_host [G] (CE part) and mmd_host [G]
@@ -143,6 +148,8 @@ int mtk_bank_step_result(mtk_bank* bank, int which, double* loss_host, double* m
  * path (0); out_host [n_layers].  Layers with both widths >= 32 and
  * multiples of 4 qualify (env MTK_DISABLE_TC=1 at bank creation forces SIMT). */
 int mtk_bank_tc_layers(mtk_bank* bank, int* out_host);
+/* zero the Adam moments and step count (a fresh mt::OptimizerState).       */
+int mtk_bank_reset_optimizer(mtk_bank* bank);
 /* debug/parity: keep the last step's parameter gradients (dW, db).          */
 int mtk_bank_set_keep_grads(mtk_bank* bank, int on);
 int mtk_bank_get_grads(mtk_bank* bank, int model, double* const* dW_host, double* const* db_host);

@@ -140,6 +140,21 @@ void orc_mm_nt_acc(const double* a, const double* b, double* c, size_t M, size_t
         }
 }
 
+/* optim.hpp:49-63: m = b1 m + (1-b1) g; v = b2 v + (1-b2) g g;
+ * w -= lr (m / bc1) / (sqrt(v / bc2) + eps), bc = 1 - beta^step.        */
+void orc_adam_update(double* w, const double* g, double* m, double* v, size_t n, double lr,
+                     double beta1, double beta2, double eps, uint64_t step) {
+    const double bc1 = 1.0 - pow(beta1, (double)step);
+    const double bc2 = 1.0 - pow(beta2, (double)step);
+    for (size_t i = 0; i < n; ++i) {
+        m[i] = beta1 * m[i] + (1.0 - beta1) * g[i];
+        v[i] = beta2 * v[i] + (1.0 - beta2) * g[i] * g[i];
+        const double mhat = m[i] / bc1;
+        const double vhat = v[i] / bc2;
+        w[i] -= lr * mhat / (sqrt(vhat) + eps);
+    }
+}
+
 void orc_mm_tn_acc(const double* a, const double* g, double* c, size_t M, size_t K, size_t N) {
     for (size_t i = 0; i < M; ++i)
         for (size_t p = 0; p < K; ++p) {

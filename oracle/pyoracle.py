@@ -88,6 +88,8 @@ def _setup_orc(L):
     L.orc_mlp_forward.argtypes = [C.c_int, _ip, C.c_int, C.POINTER(_dp), C.POINTER(_dp), _dp,
                                   C.c_int, _dp, _dp]
     L.orc_mlp_init.argtypes = [C.c_void_p, C.c_int, _ip, _ip, C.POINTER(_dp), C.POINTER(_dp)]
+    L.orc_adam_update.argtypes = [_dp, _dp, _dp, _dp, C.c_size_t, C.c_double, C.c_double,
+                                  C.c_double, C.c_double, C.c_uint64]
 
 
 def _setup_ref(L):
@@ -119,6 +121,8 @@ def _setup_ref(L):
     L.ref_bench_train.restype = C.c_double
     L.ref_bench_train.argtypes = [C.c_int, C.c_int, _ip, C.c_int, C.c_int, C.c_int, C.c_double,
                                   C.c_uint64]
+    L.ref_adam_sequence.argtypes = [_dp, _dp, C.c_size_t, C.c_int, C.c_double, C.c_double,
+                                    C.c_double, C.c_double]
 
 
 def dp(a):
@@ -221,6 +225,34 @@ def _train_step(fn, dims, W, b, X, y, *, n_heads=1, frozen=0, src_rows=0, w=None
 def mlp_train_step(dims, W, b, X, y, **kw):
     """Oracle (C restatement) SGD step; updates W/b in place."""
     return _train_step(orc().orc_mlp_train_step, dims, W, b, X, y, **kw)
+
+
+class Adam:
+    """Oracle Adam state over a list of parameter arrays (optim.hpp:13-26,
+    49-63): moments aligned with the list order, one step counter."""
+
+    def __init__(self, params, lr, beta1=0.9, beta2=0.999, eps=1e-8):
+        self.lr, self.b1, self.b2, self.eps = lr, beta1, beta2, eps
+        self.m = [np.zeros_like(p) for p in params]
+        self.v = [np.zeros_like(p) for p in params]
+        self.step = 0
+
+    def update(self, params, grads):
+        self.step += 1
+        for p, g, m, v in zip(params, grads, self.m, self.v):
+            g = np.ascontiguousarray(g, dtype=np.float64)
+            orc().orc_adam_update(dp(p), dp(g), dp(m), dp(v), p.size, self.lr, self.b1, self.b2,
+                                  self.eps, self.step)
+
+
+def ref_adam_sequence(w, grads, lr, beta1=0.9, beta2=0.999, eps=1e-8):
+    """mt::optimizer_step (Adam) applied len(grads) times to a copy of w."""
+    w = np.array(w, dtype=np.float64).ravel()
+    g = np.ascontiguousarray(np.stack([np.ravel(x) for x in grads]), dtype=np.float64)
+    st = ref().ref_adam_sequence(dp(w), dp(g), w.size, len(grads), lr, beta1, beta2, eps)
+    if st != 0:
+        raise RuntimeError(ref().ref_last_error().decode())
+    return w
 
 
 def ref_mlp_train_step(dims, W, b, X, y, **kw):

@@ -99,6 +99,30 @@ void* ref_rng_split(void* r, uint64_t stream) {
     return new mt::Rng(static_cast<mt::Rng*>(r)->split(stream));
 }
 
+// ---- Adam through mt::optimizer_step (optim.hpp:30-68) ---------------------
+// `steps` consecutive updates of one parameter with the given gradients
+// (g_seq [steps][n]); the OptimizerState persists across them.
+int ref_adam_sequence(double* w, const double* g_seq, size_t n, int steps, double lr, double beta1,
+                      double beta2, double eps) {
+    try {
+        mt::Parameter p("p", mt::Tensor({n}, std::vector<double>(w, w + n)));
+        mt::OptimizerState st = mt::OptimizerState::adam(lr);
+        st.beta1 = beta1;
+        st.beta2 = beta2;
+        st.epsilon = eps;
+        std::vector<mt::Parameter*> ps{&p};
+        for (int s = 0; s < steps; ++s) {
+            for (size_t i = 0; i < n; ++i) p.grad[i] = g_seq[(size_t)s * n + i];
+            mt::optimizer_step(st, ps);
+        }
+        for (size_t i = 0; i < n; ++i) w[i] = p.value[i];
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 5;
+    }
+}
+
 // ---- Tape MLP step: the reference composition of the path ----------------
 // Same argument meaning as orc_mlp_train_step (oracle.h).
 int ref_mlp_train_step(int L, const int* dims, int n_heads, int frozen, double* const* W,

@@ -40,6 +40,10 @@ class MtkStep(C.Structure):
         ("mmd_lambda", C.c_double),
         ("mmd_nb", C.c_int),
         ("mmd_mult", C.c_double * 8),
+        ("optimizer", C.c_int),
+        ("adam_beta1", C.c_double),
+        ("adam_beta2", C.c_double),
+        ("adam_eps", C.c_double),
     ]
 
 
@@ -48,6 +52,7 @@ SIGNATURES = {
     "mtk_last_error": (C.c_char_p, []),
     "mtk_ctx_create": (C.c_int, [C.c_int, _vp, C.POINTER(_vp)]),
     "mtk_ctx_destroy": (C.c_int, [_vp]),
+    "mtk_bank_reset_optimizer": (C.c_int, [_vp]),
     "mtk_ctx_synchronize": (C.c_int, [_vp]),
     "mtk_ctx_launch_count": (C.c_int, [_vp, _u64p]),
     "mtk_ctx_set_timing": (C.c_int, [_vp, C.c_int]),

@@ -200,13 +200,22 @@ class Bank:
 
     @staticmethod
     def make_step(B, *, src_rows=0, denom=(0.0, 0.0), lr=0.05, frozen_layers=0, mmd_lambda=0.0,
-                  mmd_mult=None, X=None, y=None, w=None) -> MtkStep:
+                  mmd_mult=None, optimizer="sgd", adam_betas=(0.0, 0.0), adam_eps=0.0,
+                  X=None, y=None, w=None) -> MtkStep:
+        """optimizer: "sgd" (optim.hpp:46-48) or "adam" (optim.hpp:49-63; the
+        bank keeps the moments, see reset_optimizer).  Zero betas / eps select
+        the reference defaults 0.9 / 0.999 / 1e-8."""
         s = MtkStep()
         s.X, s.y, s.w = _ptr(X), _ptr(y), _ptr(w)
         s.B = B
         s.src_rows = src_rows
         s.denom[0], s.denom[1] = denom
         s.lr = lr
+        if optimizer not in ("sgd", "adam"):
+            raise errors.ConfigError(f"unknown optimizer {optimizer!r}")
+        s.optimizer = 1 if optimizer == "adam" else 0
+        s.adam_beta1, s.adam_beta2 = adam_betas
+        s.adam_eps = adam_eps
         s.frozen_layers = frozen_layers
         s.mmd_lambda = mmd_lambda
         if mmd_mult is not None:
@@ -254,6 +263,10 @@ class Bank:
         errors.check(lib.mtk_bank_step_result(self.h, which, self._loss.ctypes.data_as(_dp),
                                               self._mmd.ctypes.data_as(_dp)), "step_result")
         return self._loss.copy(), self._mmd.copy()
+
+    def reset_optimizer(self):
+        """zero the Adam moments and step count (a fresh OptimizerState)"""
+        errors.check(lib.mtk_bank_reset_optimizer(self.h), "reset_optimizer")
 
     def keep_grads(self, on: bool = True):
         errors.check(lib.mtk_bank_set_keep_grads(self.h, 1 if on else 0))

@@ -61,6 +61,8 @@ struct mtk_bank {
     std::vector<bool> tc;  // per layer: tensor-core path
     std::vector<Plane3> W;
     std::vector<float*> b, gW, gb;
+    std::vector<float*> mW, vW, mb, vb;  // Adam moments (allocated on first Adam step)
+    unsigned long long adam_t = 0;       // OptimizerState::step (optim.hpp:41)
     bool keep_grads = false;
     int capB = 0;
     Plane3 Xsp;               // hi/lo planes of the input (f borrowed per call)
@@ -114,6 +116,10 @@ struct mtk_bank {
         for (auto* p : b) cudaFree(p);
         for (auto* p : gW) cudaFree(p);
         for (auto* p : gb) cudaFree(p);
+        for (auto* p : mW) cudaFree(p);
+        for (auto* p : vW) cudaFree(p);
+        for (auto* p : mb) cudaFree(p);
+        for (auto* p : vb) cudaFree(p);
         free_acts();
         cudaFree(loss);
         cudaFree(mmd);
@@ -132,6 +138,32 @@ struct mtk_bank {
             if (sl.done) cudaEventDestroy(sl.done);
             if (sl.res) cudaFreeHost(sl.res);
         }
+    }
+    void ensure_adam() {
+        if (!mW.empty()) return;
+        for (int i = 0; i < n_mats; ++i) {
+            const size_t nw = (size_t)G * fan_in(i) * fan_out(i), nb = (size_t)G * fan_out(i);
+            float *a, *b2, *c2, *d2;
+            MTK_CUDA(cudaMalloc(&a, nw * sizeof(float)));
+            MTK_CUDA(cudaMalloc(&b2, nw * sizeof(float)));
+            MTK_CUDA(cudaMalloc(&c2, nb * sizeof(float)));
+            MTK_CUDA(cudaMalloc(&d2, nb * sizeof(float)));
+            mW.push_back(a);
+            vW.push_back(b2);
+            mb.push_back(c2);
+            vb.push_back(d2);
+        }
+        reset_adam();
+    }
+    void reset_adam() {
+        for (int i = 0; i < (int)mW.size(); ++i) {
+            const size_t nw = (size_t)G * fan_in(i) * fan_out(i), nb = (size_t)G * fan_out(i);
+            MTK_CUDA(cudaMemsetAsync(mW[i], 0, nw * sizeof(float), ctx->stream));
+            MTK_CUDA(cudaMemsetAsync(vW[i], 0, nw * sizeof(float), ctx->stream));
+            MTK_CUDA(cudaMemsetAsync(mb[i], 0, nb * sizeof(float), ctx->stream));
+            MTK_CUDA(cudaMemsetAsync(vb[i], 0, nb * sizeof(float), ctx->stream));
+        }
+        adam_t = 0;
     }
     void free_slots() {
         for (auto& sl : slot) {
@@ -363,8 +395,12 @@ void gemm_dx(mtk_bank& k, int mat, const Plane3& dz, int B, int r0, int rows, co
 
 // DW + SGD: W[p, j] -= lr * sum_r in[r, p] dz[r, j]
 void gemm_dw(mtk_bank& k, int mat, const Plane3& in, const Plane3& dz, int B, int r0, int rows,
-             float lr) {
+             float lr, AdamArgs adam) {
     Ctx& c = *k.ctx;
+    if (adam.on) {
+        adam.m = k.mW[mat];
+        adam.v = k.vW[mat];
+    }
     const int fi = k.fan_in(mat), fo = k.fan_out(mat);
     if (k.tc[k.layer_of(mat)]) {
         UmmaGemm u;
@@ -385,6 +421,7 @@ void gemm_dw(mtk_bank& k, int mat, const Plane3& in, const Plane3& dz, int B, in
         u.c_gs = (long long)fi * fo;
         u.ldc = fo;
         u.lr = lr;
+        u.adam = adam;
         u.grad_out = k.keep_grads ? k.gW[mat] : nullptr;
         u.flags = c.d_flags;
         launch_umma(u, c.stream);
@@ -405,6 +442,7 @@ void gemm_dw(mtk_bank& k, int mat, const Plane3& in, const Plane3& dz, int B, in
         h.W_lo = k.W[mat].lo;
         h.w_gs = (long long)fi * fo;
         h.lr = lr;
+        h.adam = adam;
         h.grad_out = k.keep_grads ? k.gW[mat] : nullptr;
         h.flags = c.d_flags;
         const size_t hb = head_dw_scratch_bytes(k.G, fi, fo);
@@ -437,6 +475,7 @@ void gemm_dw(mtk_bank& k, int mat, const Plane3& in, const Plane3& dz, int B, in
         g.ldc = fo;
         g.epi = Epi::kSgd;
         g.lr = lr;
+        g.adam = adam;
         g.grad_out = k.keep_grads ? k.gW[mat] : nullptr;
         g.flags = c.d_flags;
         launch_gemm(g, c.stream);
@@ -496,6 +535,32 @@ void train_step(mtk_bank& k, const mtk_step& s, double* loss_host, double* mmd_h
     const double d0 = s.denom[0] > 0 ? s.denom[0] : (double)(two ? src : B);
     const double d1 = s.denom[1] > 0 ? s.denom[1] : (double)(B - src);
     const float lr = (float)s.lr;
+    need(s.optimizer == 0 || s.optimizer == 1, MTK_CONFIG_ERROR,
+         "train_step: optimizer must be 0 (SGD) or 1 (Adam)");
+    AdamArgs adam;
+    if (s.optimizer == 1) {
+        const double b1 = s.adam_beta1 > 0 ? s.adam_beta1 : 0.9;
+        const double b2 = s.adam_beta2 > 0 ? s.adam_beta2 : 0.999;
+        const double eps = s.adam_eps > 0 ? s.adam_eps : 1e-8;
+        need(b1 < 1.0 && b2 < 1.0 && std::isfinite(eps), MTK_CONFIG_ERROR,
+             "train_step: Adam betas must lie in [0, 1)");
+        k.ensure_adam();
+        k.adam_t += 1;  // optim.hpp:41, once per optimizer_step
+        adam.on = 1;
+        adam.b1 = (float)b1;
+        adam.b2 = (float)b2;
+        adam.eps = (float)eps;
+        adam.bc1 = (float)(1.0 - std::pow(b1, (double)k.adam_t));
+        adam.bc2 = (float)(1.0 - std::pow(b2, (double)k.adam_t));
+    }
+    auto bias_adam = [&](int mat) {
+        AdamArgs a = adam;
+        if (a.on) {
+            a.m = k.mb[mat];
+            a.v = k.vb[mat];
+        }
+        return a;
+    };
 
     const Plane3 X = input_plane(k, s.X, B);
     run_forward(k, X, B, two ? -1 : 0, src);
@@ -597,22 +662,22 @@ void train_step(mtk_bank& k, const mtk_step& s, double* loss_host, double* mmd_h
             {
                 PhaseScope ph(c, kPhDw, split ? 2 : 1);
                 if (split) {
-                    gemm_dw(k, l, in, *cur, B, 0, src, lr);
-                    gemm_dw(k, l + 1, in, *cur, B, src, B - src, lr);
+                    gemm_dw(k, l, in, *cur, B, 0, src, lr, adam);
+                    gemm_dw(k, l + 1, in, *cur, B, src, B - src, lr, adam);
                 } else {
-                    gemm_dw(k, l, in, *cur, B, 0, B, lr);
+                    gemm_dw(k, l, in, *cur, B, 0, B, lr, adam);
                 }
                 after_launch(c, split ? 2 : 1);
             }
             PhaseScope ph(c, kPhBias, split ? 2 : 1);
             if (split) {
-                launch_bias_sgd(k.G, src, fo, cur->f, (long long)B * fo, k.b[l], fo, lr,
+                launch_bias_sgd(k.G, src, fo, cur->f, (long long)B * fo, k.b[l], fo, lr, bias_adam(l),
                                 k.keep_grads ? k.gb[l] : nullptr, c.d_flags, c.stream);
                 launch_bias_sgd(k.G, B - src, fo, cur->f + (size_t)src * fo, (long long)B * fo,
-                                k.b[l + 1], fo, lr, k.keep_grads ? k.gb[l + 1] : nullptr,
-                                c.d_flags, c.stream);
+                                k.b[l + 1], fo, lr, bias_adam(l + 1),
+                                k.keep_grads ? k.gb[l + 1] : nullptr, c.d_flags, c.stream);
             } else {
-                launch_bias_sgd(k.G, B, fo, cur->f, (long long)B * fo, k.b[l], fo, lr,
+                launch_bias_sgd(k.G, B, fo, cur->f, (long long)B * fo, k.b[l], fo, lr, bias_adam(l),
                                 k.keep_grads ? k.gb[l] : nullptr, c.d_flags, c.stream);
             }
             after_launch(c, split ? 2 : 1);
@@ -881,6 +946,13 @@ int mtk_bank_step_result(mtk_bank* k, int which, double* loss_host, double* mmd_
                 for (int g = 0; g < k->G; ++g) mmd_host[g] = 0.0;
         }
         if (which == 0) k->ctx->check_flags();
+    });
+}
+
+int mtk_bank_reset_optimizer(mtk_bank* k) {
+    return guard([&] {
+        need(k != nullptr, MTK_VALUE_ERROR, "reset_optimizer: null bank");
+        k->reset_adam();
     });
 }
 

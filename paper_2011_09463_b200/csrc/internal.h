@@ -70,6 +70,29 @@ struct PhaseScope {
 //   C(m,n) = sum_k A(m,k) * B(k,n)
 //   A(m,k) = A[g*a_gs + m*a_ms + k*a_ks]; B(k,n) = B[g*b_gs + k*b_ks + n*b_ns]
 // Epilogues operate on row-major outputs C[g*c_gs + m*ldc + n].
+// Parameter update applied by the dW / db epilogues (optim.hpp:30-68):
+// SGD w -= lr g (:46-48), or Adam (:49-63) with moments m, v laid out like
+// the parameter and host-computed bias corrections bc1 = 1 - b1^t,
+// bc2 = 1 - b2^t (fp32 here, f64 in the reference).
+struct AdamArgs {
+    int on = 0;
+    float b1 = 0.9f, b2 = 0.999f, eps = 1e-8f, bc1 = 1.f, bc2 = 1.f;
+    float* m = nullptr;
+    float* v = nullptr;
+};
+#ifdef __CUDACC__
+__device__ __forceinline__ float param_update(float w, float g, float lr, const AdamArgs& a,
+                                              long long idx) {
+    if (!a.on) return w - lr * g;
+    const float m = a.b1 * a.m[idx] + (1.f - a.b1) * g;
+    const float v = a.b2 * a.v[idx] + (1.f - a.b2) * g * g;
+    a.m[idx] = m;
+    a.v[idx] = v;
+    const float mhat = m / a.bc1, vhat = v / a.bc2;
+    return w - lr * mhat / (sqrtf(vhat) + a.eps);
+}
+#endif
+
 enum class Epi : int {
     kBias = 0,      // C = acc + bias[n]
     kBiasRelu = 1,  // C = max(acc + bias[n], 0)
@@ -92,6 +115,7 @@ struct Gemm {
     const float* add = nullptr;   // kMask: optional addend, same layout as C
     const float* mask = nullptr;  // kMask: mask source, same layout as C
     float lr = 0.f;               // kSgd
+    AdamArgs adam;                // kSgd: Adam instead of SGD when adam.on
     float* grad_out = nullptr;    // kSgd: optional copy of acc, same layout as C
     float* C_hi = nullptr;        // optional tf32 split planes of the result
     float* C_lo = nullptr;
@@ -119,6 +143,7 @@ struct UmmaGemm {
     const float* add = nullptr;
     const float* mask = nullptr;
     float lr = 0.f;
+    AdamArgs adam;
     float* grad_out = nullptr;
     int* flags = nullptr;
 };
@@ -152,6 +177,7 @@ struct HeadDw {
     float* W_lo = nullptr;
     long long w_gs = 0;
     float lr = 0.f;
+    AdamArgs adam;
     float* grad_out = nullptr;
     int* flags = nullptr;
     float* partial = nullptr;  // scratch, head_dw_scratch_bytes()
@@ -191,7 +217,8 @@ void launch_ce(const CeArgs& a, cudaStream_t s);
 
 // Column sums + SGD on a bias: db[g,n] = sum_{rows} dZ[g, r, n]; b -= lr*db
 void launch_bias_sgd(int G, int rows, int N, const float* dZ, long long dz_gs, float* b,
-                     long long b_gs, float lr, float* grad_out, int* flags, cudaStream_t s);
+                     long long b_gs, float lr, const AdamArgs& adam, float* grad_out, int* flags,
+                     cudaStream_t s);
 
 // MMD problem over G independent groups; group g has rows [0,m) in Xs and
 // [0,n) in Xt, both row-major with row stride d.

@@ -222,7 +222,7 @@ __global__ void head_dw_finish_kernel(HeadDw p) {
     for (int rs = 0; rs < RS; ++rs) gsum += p.partial[((long long)rs * p.G + g) * per + e];
     const long long idx = g * p.w_gs + e;
     if (p.grad_out) p.grad_out[idx] = gsum;
-    const float w = p.W[idx] - p.lr * gsum;
+    const float w = param_update(p.W[idx], gsum, p.lr, p.adam, idx);
     if (!isfinite(w) && p.flags) atomicOr(p.flags, kFlagNonFinite);
     p.W[idx] = w;
     if (p.W_hi) {

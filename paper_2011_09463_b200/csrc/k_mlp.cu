@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(NT) gemm_simt_kernel(Gemm p) {
                     break;
                 case Epi::kSgd:
                     if (p.grad_out) p.grad_out[idx] = v;
-                    v = p.C[idx] - p.lr * v;
+                    v = param_update(p.C[idx], v, p.lr, p.adam, idx);
                     bad |= !isfinite(v);
                     break;
                 case Epi::kStore:
@@ -184,7 +184,8 @@ __global__ void row_sum_kernel(const double* row_loss, int B, double* loss, int*
 constexpr int BS_GROUPS = 32;
 __global__ void __launch_bounds__(32 * BS_GROUPS) bias_sgd_kernel(int G, int rows, int N, const float* dZ,
                                                                   long long dz_gs, float* b, long long b_gs,
-                                                                  float lr, float* grad_out, int* flags) {
+                                                                  float lr, AdamArgs adam, float* grad_out,
+                                                                  int* flags) {
     __shared__ float part[BS_GROUPS][33];
     const int g = blockIdx.y;
     const int n = blockIdx.x * 32 + (threadIdx.x & 31);
@@ -210,7 +211,7 @@ __global__ void __launch_bounds__(32 * BS_GROUPS) bias_sgd_kernel(int G, int row
 #pragma unroll
         for (int q = 0; q < BS_GROUPS; ++q) t += part[q][threadIdx.x];
         if (grad_out) grad_out[g * b_gs + n] = t;
-        const float v = b[g * b_gs + n] - lr * t;
+        const float v = param_update(b[g * b_gs + n], t, lr, adam, g * b_gs + n);
         if (!isfinite(v)) atomicOr(flags, kFlagNonFinite);
         b[g * b_gs + n] = v;
     }
@@ -234,9 +235,10 @@ void launch_ce(const CeArgs& a, cudaStream_t s) {
 }
 
 void launch_bias_sgd(int G, int rows, int N, const float* dZ, long long dz_gs, float* b,
-                     long long b_gs, float lr, float* grad_out, int* flags, cudaStream_t s) {
+                     long long b_gs, float lr, const AdamArgs& adam, float* grad_out, int* flags,
+                     cudaStream_t s) {
     dim3 grid((N + 31) / 32, G);
-    bias_sgd_kernel<<<grid, 32 * BS_GROUPS, 0, s>>>(G, rows, N, dZ, dz_gs, b, b_gs, lr, grad_out, flags);
+    bias_sgd_kernel<<<grid, 32 * BS_GROUPS, 0, s>>>(G, rows, N, dZ, dz_gs, b, b_gs, lr, adam, grad_out, flags);
     count_launch();
 }
 

@@ -64,6 +64,7 @@ struct UmmaParams {
     const float* add;
     const float* mask;
     float lr;
+    AdamArgs adam;
     float* grad_out;
     int* flags;
     unsigned long long* trace;  // diagnostics: timestamps of CTA (0,0,0)
@@ -188,10 +189,10 @@ __device__ __forceinline__ void epilogue_rows(const UmmaParams& p, uint32_t tmem
                 } else if (p.epi == (int)Epi::kSgd) {  // C is the fp32 master weight
                     if (p.grad_out) *reinterpret_cast<float4*>(p.grad_out + idx) = x;
                     const float4 w = *reinterpret_cast<const float4*>(p.C + idx);
-                    x.x = w.x - p.lr * x.x;
-                    x.y = w.y - p.lr * x.y;
-                    x.z = w.z - p.lr * x.z;
-                    x.w = w.w - p.lr * x.w;
+                    x.x = param_update(w.x, x.x, p.lr, p.adam, idx);
+                    x.y = param_update(w.y, x.y, p.lr, p.adam, idx + 1);
+                    x.z = param_update(w.z, x.z, p.lr, p.adam, idx + 2);
+                    x.w = param_update(w.w, x.w, p.lr, p.adam, idx + 3);
                     bad |= !(isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w));
                 }
                 *reinterpret_cast<float4*>(p.C + idx) = x;
@@ -212,7 +213,7 @@ __device__ __forceinline__ void epilogue_rows(const UmmaParams& p, uint32_t tmem
                     x = (p.mask[idx] > 0.f) ? x : 0.f;
                 } else if (p.epi == (int)Epi::kSgd) {
                     if (p.grad_out) p.grad_out[idx] = x;
-                    x = p.C[idx] - p.lr * x;
+                    x = param_update(p.C[idx], x, p.lr, p.adam, idx);
                     bad |= !isfinite(x);
                 }
                 p.C[idx] = x;
@@ -516,6 +517,7 @@ void launch_umma(const UmmaGemm& u, cudaStream_t s) {
     p.add = u.add;
     p.mask = u.mask;
     p.lr = u.lr;
+    p.adam = u.adam;
     p.grad_out = u.grad_out;
     p.flags = u.flags;
     if (const char* t = getenv("MTK_UMMA_TRACE"))

@@ -157,6 +157,54 @@ def test_multi_step_trajectory(ctx):
             assert rel(W[i], ref[g][0][i]) <= 1e-4
 
 
+@pytest.mark.parametrize("dims,n_heads,frozen", [([784, 256, 10], 1, 0), ([100, 64, 32, 10], 1, 1),
+                                                 ([64, 48, 10], 2, 0), ([37, 19, 3], 1, 0)])
+def test_adam_steps_match_oracle_update(ctx, dims, n_heads, frozen):
+    """Adam (optim.hpp:49-63) in the dW/db epilogues: three steps; each step's
+    parameters must equal the oracle Adam update (f64, its own moments) applied
+    to the step's GPU gradients (gradients themselves are pinned by the SGD
+    tests above).  Moments persist across steps; reset_optimizer restarts."""
+    G, B = 3, 40
+    bank = make_bank(ctx, G, dims, n_heads=n_heads)
+    X, y = inputs(G, B, dims[0], dims[-1])
+    Xd, yd = to_dev(X, y)
+    bank.keep_grads(True)
+    lr, betas, eps = 0.01, (0.8, 0.99), 1e-6
+    opts = None
+    for step in range(3):
+        before = [bank.get_params(g) for g in range(G)]
+        bank.train_step(Xd, yd, lr=lr, src_rows=24, frozen_layers=frozen, optimizer="adam",
+                        adam_betas=betas, adam_eps=eps, want_loss=False)
+        if opts is None:
+            opts = [po.Adam(before[g][0] + before[g][1], lr, betas[0], betas[1], eps) for g in range(G)]
+        for g in range(G):
+            W, b = [x.copy() for x in before[g][0]], [x.copy() for x in before[g][1]]
+            dW, db = bank.get_grads(g)
+            live = [i for i in range(bank.n_mats) if (i if i < bank.L else bank.L - 1) >= frozen]
+            # the oracle state steps every parameter; frozen ones get zero grads
+            # and are compared for bit-identity instead
+            grads = [dW[i] if i in live else np.zeros_like(W[i]) for i in range(len(W))] + \
+                    [db[i] if i in live else np.zeros_like(b[i]) for i in range(len(b))]
+            opts[g].update(W + b, grads)
+            Wn, bn = bank.get_params(g)
+            for i in range(bank.n_mats):
+                if i not in live:
+                    assert np.array_equal(Wn[i], before[g][0][i])
+                    continue
+                assert rel(Wn[i], W[i]) <= TOL, (step, g, i, rel(Wn[i], W[i]))
+                assert rel(bn[i], b[i]) <= TOL, (step, g, i)
+    # a fresh state: the next step is a first step again
+    bank.reset_optimizer()
+    before = bank.get_params(0)
+    bank.train_step(Xd, yd, lr=lr, src_rows=24, frozen_layers=frozen, optimizer="adam",
+                    adam_betas=betas, adam_eps=eps, want_loss=False)
+    dW, db = bank.get_grads(0)
+    i = bank.n_mats - 1
+    W = before[0][i].copy()
+    po.Adam([W], lr, betas[0], betas[1], eps).update([W], [dW[i]])
+    assert rel(bank.get_params(0)[0][i], W) <= TOL
+
+
 def test_determinism(ctx):
     dims = [128, 64, 10]
     X, y = inputs(2, 40, 128, 10)

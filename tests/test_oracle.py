@@ -135,6 +135,35 @@ def test_spec_known_answers():
     assert abs(W[0][0, 0] - (1.0 - 0.1 * gW[0][0, 0])) == 0.0
 
 
+# ------------------------------------------------------------------- Adam
+def test_adam_spec_known_answer():
+    # adam first step with g=0.2, lr=0.01 -> w decreases by lr*g/(sqrt(g^2)+eps) ~ 0.01
+    # (the survey probe measured 0.0099999995)
+    w = np.array([1.0])
+    opt = po.Adam([w], lr=0.01)
+    opt.update([w], [np.array([0.2])])
+    assert abs((1.0 - w[0]) - 0.01 * 0.2 / (0.2 + 1e-8)) < 1e-16
+    # g = 0 leaves parameters unchanged
+    w = np.array([0.5, -2.0])
+    opt = po.Adam([w], lr=0.01)
+    opt.update([w], [np.zeros(2)])
+    assert np.array_equal(w, [0.5, -2.0])
+
+
+@pytest.mark.skipif(not has_ref(), reason="reference shim not built")
+@pytest.mark.parametrize("betas", [(0.9, 0.999, 1e-8), (0.5, 0.9, 1e-3)])
+def test_adam_matches_live_reference(betas):
+    rng = np.random.default_rng(7)
+    w0 = rng.normal(size=37)
+    grads = [rng.normal(size=37) * (10.0 ** (-i)) for i in range(5)]
+    ref = po.ref_adam_sequence(w0, grads, 0.03, *betas)
+    w = w0.copy()
+    opt = po.Adam([w], 0.03, *betas)
+    for g in grads:
+        opt.update([w], [g])
+    assert np.array_equal(w, ref)
+
+
 # ------------------------------------------------------------------- MMD
 @pytest.mark.parametrize("case", range(4))
 def test_mmd_matches_independent_numpy(case):
