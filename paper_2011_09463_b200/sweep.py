@@ -52,6 +52,7 @@ class SweepConfig:
     pretrain_epochs: int = 2         # model-based
     frozen_layers: int = 0           # model-based fine-tuning
     lr: float = 0.05
+    optimizer: str = "sgd"           # sgd | adam (optim.hpp:30-68) for target/shadows
     mmd_lambda: float = 1.0          # mapping-based
     mu_scale: float = 0.1
     shift_scale: float = 0.5
@@ -60,6 +61,7 @@ class SweepConfig:
     attack_epochs: int = 30
     attack_batch: int = 1024
     attack_lr: float = 0.1
+    attack_optimizer: str = "sgd"
     seed: int = 20110946
 
     def validate(self):
@@ -75,6 +77,9 @@ class SweepConfig:
             raise ConfigError("transfer paradigms need a hidden layer")
         if not 1 <= self.k <= self.dims[-1]:
             raise ConfigError("k must be in [1, C]")
+        for o in (self.optimizer, self.attack_optimizer):
+            if o not in ("sgd", "adam"):
+                raise ConfigError(f"unknown optimizer {o!r}")
 
 
 # --------------------------------------------------------------------------- data
@@ -186,7 +191,8 @@ def train_bank(be, cfg: SweepConfig, pop: Population, streams, models: list[int]
                 idx = [src[g][orders[g][t][0]] for g in range(G)]
                 w = np.stack([orders[g][t][1] for g in range(G)])
                 Xb, yb = gather(pop.Xs, pop.ys, idx)
-                be.step(bank, Xb, yb, w, lr=cfg.lr, denom=(float(w[0].sum()), 0.0))
+                be.step(bank, Xb, yb, w, lr=cfg.lr, denom=(float(w[0].sum()), 0.0),
+                        optimizer=cfg.optimizer)
     for _ in range(cfg.epochs):
         orders = [batches(streams[k].permutation(cfg.members), B) for k in models]
         for t in range(len(orders[0])):
@@ -195,7 +201,7 @@ def train_bank(be, cfg: SweepConfig, pop: Population, streams, models: list[int]
             Xb, yb = gather(pop.Xt, pop.yt, idx)
             if cfg.paradigm == "model":
                 be.step(bank, Xb, yb, w, lr=cfg.lr, frozen_layers=cfg.frozen_layers,
-                        denom=(float(w[0].sum()), 0.0))
+                        denom=(float(w[0].sum()), 0.0), optimizer=cfg.optimizer)
                 continue
             # co-training: a source batch rides along with every member batch
             sidx = [src[g][(t * B + np.arange(B)) % cfg.source_per_model] for g in range(G)]
@@ -205,10 +211,10 @@ def train_bank(be, cfg: SweepConfig, pop: Population, streams, models: list[int]
             wc = np.concatenate([np.ones_like(w), w], axis=1)
             if cfg.paradigm == "mapping":
                 be.step(bank, Xc, yc, wc, lr=cfg.lr, src_rows=B, mmd_lambda=cfg.mmd_lambda,
-                        denom=(float(wc[0].sum()), 0.0))
+                        denom=(float(wc[0].sum()), 0.0), optimizer=cfg.optimizer)
             else:
                 be.step(bank, Xc, yc, wc, lr=cfg.lr, src_rows=B,
-                        denom=(float(B), float(w[0].sum())))
+                        denom=(float(B), float(w[0].sum())), optimizer=cfg.optimizer)
     return bank, mem, non
 
 
@@ -231,7 +237,7 @@ def train_attack(be, cfg, F_train, lab_train, rng):
     for _ in range(cfg.attack_epochs):
         for idx, w in batches(rng.permutation(n), cfg.attack_batch):
             be.step(bank, F_train[idx][None], lab_train[idx][None].astype(np.int32), w[None],
-                    lr=cfg.attack_lr, denom=(float(w.sum()), 0.0))
+                    lr=cfg.attack_lr, denom=(float(w.sum()), 0.0), optimizer=cfg.attack_optimizer)
     return bank
 
 

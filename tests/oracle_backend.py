@@ -23,6 +23,7 @@ class OracleBank:
     def __init__(self, G, dims, n_heads):
         self.G, self.dims, self.n_heads = G, list(dims), n_heads
         self.params = [None] * G
+        self.adam = [None] * G  # po.Adam per model, created on the first Adam step
 
 
 class OracleBackend:
@@ -35,7 +36,7 @@ class OracleBackend:
         bank.params[g] = po.mlp_init(rng, bank.dims, bank.n_heads)
 
     def step(self, bank, X, y, w, *, lr, src_rows=0, frozen_layers=0, mmd_lambda=0.0,
-             denom=(0.0, 0.0)):
+             denom=(0.0, 0.0), optimizer="sgd"):
         X = np.asarray(X, dtype=np.float64)
         for g in range(bank.G):
             W, b = bank.params[g]
@@ -49,9 +50,20 @@ class OracleBackend:
                 den = [denom[0] or src_rows, denom[1] or B - src_rows]
             else:
                 den = [denom[0] or B]
-            po.mlp_train_step(bank.dims, W, b, X[g], y[g], n_heads=bank.n_heads,
-                              frozen=frozen_layers, src_rows=src_rows, w=w[g], denoms=den, lr=lr,
-                              dH=dH)
+            if optimizer == "sgd":
+                po.mlp_train_step(bank.dims, W, b, X[g], y[g], n_heads=bank.n_heads,
+                                  frozen=frozen_layers, src_rows=src_rows, w=w[g], denoms=den,
+                                  lr=lr, dH=dH)
+                continue
+            # Adam: gradients of the same Tape composition (lr = 0), then
+            # optimizer_step over every parameter (frozen ones get zero grads,
+            # which leaves them and their moments unchanged)
+            _, gW, gb = po.mlp_train_step(bank.dims, W, b, X[g], y[g], n_heads=bank.n_heads,
+                                          frozen=frozen_layers, src_rows=src_rows, w=w[g],
+                                          denoms=den, lr=0.0, dH=dH, want_grads=True)
+            if bank.adam[g] is None:
+                bank.adam[g] = po.Adam(W + b, lr)
+            bank.adam[g].update(W + b, gW + gb)
 
     def features(self, bank, X, head, k):
         out = []

@@ -19,6 +19,13 @@ TINY = dict(dims=(24, 16, 10), n_shadows=3, pool=512, members=96, source_pool=10
             attack_epochs=10, attack_batch=64)
 
 
+def test_sweep_oracle_adam_runs():
+    cfg = SweepConfig(paradigm="model", optimizer="adam", attack_optimizer="adam", lr=0.01,
+                      attack_lr=0.01, **TINY)
+    a = run_sweep(cfg, OracleBackend())
+    assert 0.0 <= a["auc"] <= 1.0
+
+
 @pytest.mark.parametrize("paradigm", ["model", "mapping", "parameter"])
 def test_sweep_oracle_deterministic(paradigm):
     cfg = SweepConfig(paradigm=paradigm, **TINY)
@@ -92,5 +99,17 @@ def test_sweep_gpu_matches_oracle_auc(paradigm):
 
     g = run_sweep(SweepConfig(paradigm=paradigm, **MID), GpuBackend())
     o = run_sweep(SweepConfig(paradigm=paradigm, **MID), OracleBackend())
+    assert abs(g["auc"] - o["auc"]) <= 0.01, (g["auc"], o["auc"])
+    assert abs(g["accuracy"] - o["accuracy"]) <= 0.01, (g["accuracy"], o["accuracy"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("paradigm", ["model", "mapping"])
+def test_sweep_gpu_matches_oracle_auc_adam(paradigm):
+    from paper_2011_09463_b200.sweep import GpuBackend
+
+    kw = dict(MID, optimizer="adam", attack_optimizer="adam", lr=0.005, attack_lr=0.01)
+    g = run_sweep(SweepConfig(paradigm=paradigm, **kw), GpuBackend())
+    o = run_sweep(SweepConfig(paradigm=paradigm, **kw), OracleBackend())
     assert abs(g["auc"] - o["auc"]) <= 0.01, (g["auc"], o["auc"])
     assert abs(g["accuracy"] - o["accuracy"]) <= 0.01, (g["accuracy"], o["accuracy"])
