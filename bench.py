@@ -209,15 +209,28 @@ def run_reference_arm(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
+# the phase's main kernel in the ncu capture summaries (profile_summary.py)
+PHASE_KERNEL = {"mmd_pairs": "mmd_tc_kernel", "fwd_gemm": "umma_kernel<0, 1",
+                "dx_gemm": "umma_kernel<0, 0", "dw_gemm": "umma_kernel<1, 1"}
+
+
 def kernel_traffic(phase):
-    """DRAM bytes per step of a phase, from the committed ncu capture summary."""
-    p = os.path.join(ROOT, "profiles", "r01_kernels.json")
-    if not os.path.exists(p):
-        return None
-    with open(p) as f:
+    """DRAM read+write bytes per launch of the phase's main kernel, from the
+    newest committed ncu --set full capture summary (profiles/rNN_kernels.json).
+    Returns (bytes or None, source file)."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r[0-9]*_kernels.json")))
+    if not files:
+        return None, None
+    with open(files[-1]) as f:
         d = json.load(f)
-    ent = d.get("phases", {}).get(phase)
-    return ent.get("dram_bytes_per_step") if ent else None
+    name = PHASE_KERNEL.get(phase)
+    ks = [k for k in d.get("kernels", []) if name and name in k["name"]]
+    if not ks:
+        return None, os.path.basename(files[-1])
+    tot = sum(k.get("dram_read", 0.0) + k.get("dram_write", 0.0) for k in ks)
+    return tot / len(ks), os.path.basename(files[-1])
 
 
 # ----------------------------------------------------------------------------- GPU arm
@@ -310,7 +323,7 @@ def run_gpu_arm(args, world, rank, local):
     e2e_value = world * G * B * args.steps / (e2e_ms / 1000.0)
     h2d = G * B * DIMS[0] * 4 + G * B * 4
     d2h = 2 * G * 8
-    traffic = kernel_traffic(dominant)
+    traffic, traffic_src = kernel_traffic(dominant)
 
     if rank != 0:
         return
@@ -347,8 +360,9 @@ def run_gpu_arm(args, world, rank, local):
                      "peak_note": (f"fp32-accurate tensor peak = 3xTF32 = tf32/3 = {src} bf16 "
                                    f"{bf16} TFLOP/s / 6; frac vs plain tf32 "
                                    f"{achieved / tf32_peak:.3f}, vs bf16 {achieved / bf16:.3f}"),
-                     "traffic_note": "DRAM read+write bytes per step of the phase's kernels "
-                                     "(profiles/r01_kernels.json, one ncu --set full capture)"},
+                     "traffic_note": (f"DRAM read+write bytes per launch of "
+                                      f"{PHASE_KERNEL.get(dominant)} (profiles/{traffic_src}, "
+                                      "one ncu --set full capture)")},
         "step_tflops": step_flop / (ms_step / 1000.0) / 1e12,
         "gemm_tflops": step_flop / (gemm_ms / 1000.0) / 1e12 if gemm_ms else None,
         "cpu_baseline": cpu,

@@ -20,6 +20,7 @@
 //   H[l]  [G, B, dims[l]] post-ReLU activations (ReLU mask = H > 0)
 //   dZ    two ping-pong [G, B, max dim] gradient buffers
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -597,6 +598,8 @@ void train_step(mtk_bank& k, const mtk_step& s, double* loss_host, double* mmd_h
         a.grad_scale = (float)s.mmd_lambda;
         a.flags = c.d_flags;
         a.tc = k.tc_mmd && mmd_tc_supported(a);
+        if (const char* t = getenv("MTK_MMD_TRACE"))  // diagnostics (tools/mmd_trace.py)
+            a.trace = reinterpret_cast<unsigned long long*>(strtoull(t, nullptr, 0));
         const int nblk = mmd_blocks_per_group(a);
         const size_t pbytes = (size_t)k.G * nblk * 3 * sizeof(double);
         if (pbytes > k.mmd_part_bytes) {
@@ -608,6 +611,16 @@ void train_step(mtk_bank& k, const mtk_step& s, double* loss_host, double* mmd_h
         a.partial = k.mmd_part;
         if (a.tc) {
             a.beta_out = k.beta;  // fused into the prep pass of launch_mmd_tc
+            const size_t zb = mmd_tc_scratch_bytes(a);
+            if (zb > k.mmd_z_bytes) {
+                MTK_CUDA(cudaStreamSynchronize(c.stream));
+                cudaFree(k.mmd_z);
+                MTK_CUDA(cudaMalloc(&k.mmd_z, zb));
+                k.mmd_z_bytes = zb;
+            }
+            PhaseScope ph(c, kPhMmdBeta, 2);  // prep pass: tf32 planes, norms, beta
+            launch_mmd_tc(a, k.mmd_z, c.stream, kMmdPrep);
+            after_launch(c, 2);
         } else {
             double* sc = c.scratch(mmd_beta_scratch_bytes(a));
             PhaseScope ph(c, kPhMmdBeta, 2);
@@ -615,20 +628,10 @@ void train_step(mtk_bank& k, const mtk_step& s, double* loss_host, double* mmd_h
             after_launch(c, 2);
         }
         {
-            PhaseScope ph(c, kPhMmdPairs, a.tc ? 3 : 1);
-            if (a.tc) {
-                const size_t zb = mmd_tc_scratch_bytes(a);
-                if (zb > k.mmd_z_bytes) {
-                    MTK_CUDA(cudaStreamSynchronize(c.stream));
-                    cudaFree(k.mmd_z);
-                    MTK_CUDA(cudaMalloc(&k.mmd_z, zb));
-                    k.mmd_z_bytes = zb;
-                }
-                launch_mmd_tc(a, k.mmd_z, c.stream);
-            } else {
-                launch_mmd_pairs(a, c.stream);
-            }
-            after_launch(c, a.tc ? 3 : 1);
+            PhaseScope ph(c, kPhMmdPairs, 1);
+            if (a.tc) launch_mmd_tc(a, k.mmd_z, c.stream, kMmdPairs);
+            else launch_mmd_pairs(a, c.stream);
+            after_launch(c, 1);
         }
         {
             PhaseScope ph(c, kPhOther, 1);

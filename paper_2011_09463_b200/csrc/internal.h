@@ -249,7 +249,10 @@ int mmd_blocks_per_group(const MmdArgs& a);  // partial-sum blocks (depends on a
 bool mmd_tc_supported(const MmdArgs& a);
 int mmd_tc_blocks_per_group(const MmdArgs& a);
 size_t mmd_tc_scratch_bytes(const MmdArgs& a);
-void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s);
+// stages: 1 = prep pass (tf32 planes, norms, fused beta), 2 = the pair kernel;
+// the same scratch must be passed to both.
+constexpr int kMmdPrep = 1, kMmdPairs = 2;
+void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s, int stages = kMmdPrep | kMmdPairs);
 size_t mmd_beta_scratch_bytes(const MmdArgs& a);
 void launch_mmd_beta(const MmdArgs& a, double* beta_out, double* scratch, cudaStream_t s);
 // beta from partials laid out as beta_partial writes them ([G][P][d+1], P = ceil(N / 32))

@@ -47,8 +47,11 @@ constexpr uint32_t WLO_COL = 384;
 struct MmdTcParams {
     CUtensorMap zk_hi, zk_lo;   // K-major views of the planes: (d, N, G), box (32, 64)
     CUtensorMap zm_hi, zm_lo;   // MN-major views: (d, N, G), box (32, 16), 32-B atom swizzle
-    const float* zhi;           // [G][N][d] planes, for z_i = hi + lo in the gradient epilogue
+    const float* zhi;           // [G][N][d] planes
     const float* zlo;
+    const float* xs;            // the fp32 sample rows (z_i in the gradient epilogue)
+    const float* xt;
+    long long xs_gs, xt_gs;
     const float* norms;         // [G][N]
     const double* beta;         // [G]
     long long m, n;
@@ -111,6 +114,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
     const bool do_flush = p.vacc != nullptr;
     unsigned long long* tr =
         (p.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) ? p.trace : nullptr;
+    // per-CTA start / end / SM id at [12288 + 3 * cta] (diagnostics)
+    const long long cta_lin = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    if (p.trace && threadIdx.x == 0 && cta_lin < 4096) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        p.trace[12288 + 3 * cta_lin] = gtime();
+        p.trace[12288 + 3 * cta_lin + 2] = smid;
+    }
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&p.zk_hi);
@@ -138,8 +149,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
     // Software pipeline (MMA order == TMA order):
     //   G1(0), G1(1), G2(0), G1(2), G2(1), ..., G1(n-1), G2(n-2), G2(n-1)
     // so the exp epilogue of tile t overlaps GEMM1 of tile t+1.
+    // Producer and MMA warps run their loops converged (all 32 lanes wait on
+    // the barriers; lane 0 issues): a lone lane spinning while its siblings
+    // sit in the final __syncthreads was observed to leave the warp
+    // descheduled for ~100 us after the work was done.
     if (warp == 0) {
-        if (lane == 0) {
+        {
             // ---------------- TMA producer ----------------
             int st = 0;
             for (int t = 0; t <= njt; ++t) {
@@ -148,10 +163,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
                     for (int kc = 0; kc < nkc; ++kc, ++st) {
                         const int s = st % STAGES;
                         mbar_wait(&empty[s], ((st / STAGES) & 1) ^ 1);
-                        TRACE(0, st);
+                        if (lane == 0) TRACE(0, st);
                         uint8_t* b = smem + s * STAGE_BYTES;
-                        mbar_expect_tx(&full[s], G1_BYTES);
                         const int k0 = kc * KC;
+                        if (lane == 0) {
+                        mbar_expect_tx(&full[s], G1_BYTES);
                         // Z_i hi [0,16K) and lo [16K,32K) (two 64-row boxes each),
                         // Z_j hi [32K,40K) and lo [40K,48K)
                         tma_load_3d(b, &p.zk_hi, &full[s], k0, (int)i0, g);
@@ -160,6 +176,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
                         tma_load_3d(b + 24576, &p.zk_lo, &full[s], k0, (int)i0 + 64, g);
                         tma_load_3d(b + 32768, &p.zk_hi, &full[s], k0, j0, g);
                         tma_load_3d(b + 40960, &p.zk_lo, &full[s], k0, j0, g);
+                        }
+                        __syncwarp();
                     }
                 }
                 if (t >= 1) {
@@ -167,21 +185,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
                     for (int jc = 0; jc < TJ / JC; ++jc, ++st) {
                         const int s = st % STAGES;
                         mbar_wait(&empty[s], ((st / STAGES) & 1) ^ 1);
-                        TRACE(0, st);
                         uint8_t* b = smem + s * STAGE_BYTES;
-                        mbar_expect_tx(&full[s], G2_BYTES);
-                        for (int q = 0; q < VD / 32; ++q) {
-                            tma_load_3d(b + q * 2048, &p.zm_hi, &full[s], v0 + 32 * q, j0 + JC * jc, g);
-                            tma_load_3d(b + 16384 + q * 2048, &p.zm_lo, &full[s], v0 + 32 * q,
-                                        j0 + JC * jc, g);
+                        if (lane == 0) {
+                            TRACE(0, st);
+                            mbar_expect_tx(&full[s], G2_BYTES);
+                            for (int q = 0; q < VD / 32; ++q) {
+                                tma_load_3d(b + q * 2048, &p.zm_hi, &full[s], v0 + 32 * q, j0 + JC * jc, g);
+                                tma_load_3d(b + 16384 + q * 2048, &p.zm_lo, &full[s], v0 + 32 * q,
+                                            j0 + JC * jc, g);
+                            }
                         }
+                        __syncwarp();
                     }
                 }
             }
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer ----------------
-        if (lane == 0) {
+        {
             constexpr uint32_t id1 = idesc_tf32(TI, TJ, 0, 0);
             constexpr uint32_t id2 = idesc_tf32(TI, VD, 0, 1);
             const uint32_t tV = tmem;
@@ -192,9 +213,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
                     for (int kc = 0; kc < nkc; ++kc, ++st) {
                         const int s = st % STAGES;
                         mbar_wait(&full[s], (st / STAGES) & 1);
-                        TRACE(4096, st);
                         tc_fence_after();
                         const uint32_t b = smem_u32(smem + s * STAGE_BYTES);
+                        if (lane == 0) {
+                        TRACE(4096, st);
 #pragma unroll
                         for (int kk = 0; kk < KC / 8; ++kk) {
                             const uint64_t ahi = smem_desc(b + kk * 32, 16, 1024, 2);
@@ -206,8 +228,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
                             mma_tf32(tS, ahi, bhi, id1, 1u);
                         }
                         mma_commit(&empty[s]);
+                        }
+                        __syncwarp();
                     }
-                    mma_commit(&s_full[t & 1]);
+                    if (lane == 0) mma_commit(&s_full[t & 1]);
+                    __syncwarp();
                 }
                 if (t >= 1) {
                     const int jt = t - 1;
@@ -223,9 +248,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
                     for (int jc = 0; jc < TJ / JC; ++jc, ++st) {
                         const int s = st % STAGES;
                         mbar_wait(&full[s], (st / STAGES) & 1);
-                        TRACE(4096, st);
                         tc_fence_after();
                         const uint32_t b = smem_u32(smem + s * STAGE_BYTES);
+                        if (lane == 0) {
+                        TRACE(4096, st);
 #pragma unroll
                         for (int h = 0; h < JC / 8; ++h) {
                             const uint32_t kcol = (uint32_t)(jc * JC + h * 8);
@@ -237,11 +263,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
                             mma_tf32_ts(tV, tWhi + kcol, bhi, id2, 1u);
                         }
                         mma_commit(&empty[s]);
+                        }
+                        __syncwarp();
                     }
-                    if (do_flush && (jt + 1) % FLUSH == 0 && jt + 1 < njt) mma_commit(v_full);
+                    if (lane == 0 && do_flush && (jt + 1) % FLUSH == 0 && jt + 1 < njt) mma_commit(v_full);
+                    __syncwarp();
                 }
             }
-            mma_commit(v_full);
+            if (lane == 0) mma_commit(v_full);
+            __syncwarp();
+            if (tr && lane == 0) tr[12282] = gtime();
         }
     } else {
         // ---------------- epilogue warps: exp + weights, then the gradient ----------------
@@ -398,42 +429,72 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
         // gradient rows: g_i = scale * (z_i * Wsum_i - V_i) over this CTA's feature slice
         mbar_wait(v_full, nflush & 1);
         tc_fence_after();
-        // all MMAs and TMA loads are complete: stage z_i (hi + lo) through the idle
-        // ring with coalesced loads, [128][VD + 1] fp32
-        float* zs = reinterpret_cast<float*>(smem);
+        if (tr && r == 0) tr[12283] = gtime();  // v_full seen
+        // All MMAs and TMA loads are complete, so the ring is idle.  The fp32
+        // z_i tile streams into it with cp.async (every 16-B piece in flight
+        // at once), each thread turns its own row into g in place (V from
+        // TMEM), and the tile leaves in coalesced float4 order.
         const int t = threadIdx.x - 64;
-        for (int e = t; e < TI * VD; e += 128) {
-            const int rr = e / VD, k = e % VD;
+        constexpr int VLD = VD + 4;  // float4-aligned rows, conflict-free row-wise float4
+        constexpr int C4 = VD / 4;
+        const uint32_t zsb = smem_u32(smem);
+        for (int e = t; e < TI * C4; e += 128) {
+            const int rr = e / C4, c4 = e % C4;
             const long long row = i0 + rr;
-            float z = 0.f;
-            if (k < vd && row < N) {
-                const long long o = ((long long)g * N + row) * p.d + v0 + k;
-                z = p.zhi[o] + p.zlo[o];
-            }
-            zs[rr * (VD + 1) + k] = z;
+            if (row >= re || 4 * c4 >= vd) continue;
+            const float* zr = row < p.m ? p.xs + g * p.xs_gs + row * p.d : p.xt + g * p.xt_gs + (row - p.m) * p.d;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(zsb + (uint32_t)((rr * VLD + 4 * c4) * 4)),
+                         "l"(zr + v0 + 4 * c4)
+                         : "memory");
         }
+        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
         asm volatile("bar.sync 1, 128;" ::: "memory");
-        const double* vrow = (nflush && row_ok) ? p.vacc + ((long long)g * N + gi) * p.d : nullptr;
-        float* out = nullptr;
-        if (row_ok)
-            out = si ? (p.gXs ? p.gXs + g * p.gs_gs + gi * p.d : nullptr)
-                     : (p.gXt ? p.gXt + g * p.gt_gs + (gi - p.m) * p.d : nullptr);
+        if (tr && r == 0) tr[12284] = gtime();
         bool bad = false;
+        const double scale = (double)p.grad_scale;
+        const double* va = (nflush && row_ok) ? p.vacc + ((long long)g * N + gi) * p.d + v0 : nullptr;
 #pragma unroll 1
         for (int cb = 0; cb < VD / 32; ++cb) {
             float vv[32];
             tmem_ld_32x32(tmem + lane_base + cb * 32, vv);
-            if (!out) continue;
-            for (int c = 0; c < 32; ++c) {
-                const int k = v0 + cb * 32 + c;
-                if (cb * 32 + c >= vd) break;
-                const double z = (double)zs[r * (VD + 1) + cb * 32 + c];
-                const double vt = (double)vv[c] + (vrow ? vrow[k] : 0.0);
-                const float gv = (float)((z * wsum - vt) * (double)p.grad_scale);
-                bad |= !isfinite(gv);
-                out[k] = gv;
+            if (!row_ok || cb * 32 >= vd) continue;
+#pragma unroll
+            for (int c = 0; c < 32; c += 4) {
+                const uint32_t a4 = zsb + (uint32_t)((r * VLD + cb * 32 + c) * 4);
+                const float4 z4 = lds128(a4);
+                const float zz[4] = {z4.x, z4.y, z4.z, z4.w};
+                float gq[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const double vt = (double)vv[c + q] + (va ? va[cb * 32 + c + q] : 0.0);
+                    gq[q] = (float)(((double)zz[q] * wsum - vt) * scale);
+                    bad |= !isfinite(gq[q]);
+                }
+                sts128(a4, make_float4(gq[0], gq[1], gq[2], gq[3]));
             }
         }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (tr && r == 0) tr[12285] = gtime();
+        const bool vec_out = ((reinterpret_cast<uintptr_t>(p.gXs) | reinterpret_cast<uintptr_t>(p.gXt)) & 15) == 0 &&
+                             (p.gs_gs | p.gt_gs) % 4 == 0;
+        for (int e = t; e < TI * C4; e += 128) {
+            const int rr = e / C4, c4 = e % C4;
+            const long long row = i0 + rr;
+            if (row >= re || 4 * c4 >= vd) continue;
+            float* o = row < p.m ? (p.gXs ? p.gXs + g * p.gs_gs + row * p.d : nullptr)
+                                 : (p.gXt ? p.gXt + g * p.gt_gs + (row - p.m) * p.d : nullptr);
+            if (!o) continue;
+            const float4 g4 = lds128(zsb + (uint32_t)((rr * VLD + 4 * c4) * 4));
+            if (vec_out) {
+                *reinterpret_cast<float4*>(o + v0 + 4 * c4) = g4;
+            } else {
+                o[v0 + 4 * c4] = g4.x;
+                o[v0 + 4 * c4 + 1] = g4.y;
+                o[v0 + 4 * c4 + 2] = g4.z;
+                o[v0 + 4 * c4 + 3] = g4.w;
+            }
+        }
+        if (tr && r == 0) tr[12286] = gtime();
         if (bad) atomicOr(p.flags, kFlagNonFinite);
         // fixed-order reduction of the kernel sums over the 128 rows (d-slice 0 only)
         __shared__ double red[3][128];
@@ -445,12 +506,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
             asm volatile("bar.sync 1, 128;" ::: "memory");
         }
         if (t < 3 && dslice == 0) p.partial[((long long)g * p.nblk + blockIdx.x) * 3 + t] = red[t][0];
+        if (tr && r == 0) tr[12287] = gtime();
     }
     tc_fence_before();
     __syncthreads();
+    if (p.trace && threadIdx.x == 0 && cta_lin < 4096) p.trace[12288 + 3 * cta_lin + 1] = gtime();
     if (warp == 1) {
+        if (tr && lane == 0) tr[12281] = gtime();
         tc_fence_after();
+        if (tr && lane == 0) tr[12280] = gtime();
         tmem_dealloc<512>(tmem);
+        if (p.trace && lane == 0 && cta_lin < 4096) p.trace[12288 + 3 * cta_lin + 2] = gtime();
     }
 }
 
@@ -584,7 +650,7 @@ size_t mmd_tc_scratch_bytes(const MmdArgs& a) {
 }
 
 // scratch: >= mmd_tc_scratch_bytes(a); a.partial must hold [G][blocks][3]
-void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s) {
+void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s, int stages) {
     const long long N = a.m + a.n;
     const long long re = a.row_end < 0 ? N : a.row_end;
     uintptr_t cur = (reinterpret_cast<uintptr_t>(scratch) + 255) & ~uintptr_t(255);
@@ -602,16 +668,20 @@ void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s) {
     double* bpart = a.beta_out ? reinterpret_cast<double*>(cur) : nullptr;
     constexpr int kFusedBetaMaxD = 512;  // colsum smem: 8 warps x d doubles
     const bool fused_beta = bpart && a.d <= kFusedBetaMaxD;
-    if (bpart && !fused_beta) launch_mmd_beta(a, a.beta_out, bpart, s);
-    dim3 pg((unsigned)((N + kBetaRows - 1) / kBetaRows), a.G);
-    const size_t prep_smem = fused_beta ? (size_t)PREP_WARPS * a.d * sizeof(double) : 0;
-    if ((reinterpret_cast<uintptr_t>(a.Xs) | reinterpret_cast<uintptr_t>(a.Xt)) & 15 ||
-        (a.xs_gs | a.xt_gs) % 4)
-        fail(MTK_ERROR, "mmd: samples not 16-byte aligned");
-    mmd_prep_kernel<<<pg, 32 * PREP_WARPS, prep_smem, s>>>(a.Xs, a.xs_gs, a.Xt, a.xt_gs, a.m, a.n, a.d,
-                                                            zhi, zlo, norms, fused_beta ? bpart : nullptr);
-    count_launch();
-    if (fused_beta) launch_mmd_beta_finish(a, bpart, a.beta_out, s);
+    if (stages & kMmdPrep) {
+        if (bpart && !fused_beta) launch_mmd_beta(a, a.beta_out, bpart, s);
+        const dim3 pg((unsigned)((N + kBetaRows - 1) / kBetaRows), a.G);
+        const size_t prep_smem = fused_beta ? (size_t)PREP_WARPS * a.d * sizeof(double) : 0;
+        if ((reinterpret_cast<uintptr_t>(a.Xs) | reinterpret_cast<uintptr_t>(a.Xt)) & 15 ||
+            (a.xs_gs | a.xt_gs) % 4)
+            fail(MTK_ERROR, "mmd: samples not 16-byte aligned");
+        mmd_prep_kernel<<<pg, 32 * PREP_WARPS, prep_smem, s>>>(a.Xs, a.xs_gs, a.Xt, a.xt_gs, a.m, a.n,
+                                                                a.d, zhi, zlo, norms,
+                                                                fused_beta ? bpart : nullptr);
+        count_launch();
+        if (fused_beta) launch_mmd_beta_finish(a, bpart, a.beta_out, s);
+    }
+    if (!(stages & kMmdPairs)) return;
     const long long zgs = N * a.d;
     MmdTcParams p;
     std::memset(&p, 0, sizeof(p));
@@ -621,6 +691,10 @@ void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s) {
     p.zm_lo = zmap(zlo, a.d, N, a.G, zgs, JC, true);
     p.zhi = zhi;
     p.zlo = zlo;
+    p.xs = a.Xs;
+    p.xt = a.Xt;
+    p.xs_gs = a.xs_gs;
+    p.xt_gs = a.xt_gs;
     p.norms = norms;
     p.beta = a.beta;
     p.m = a.m;

@@ -16,7 +16,9 @@ METRICS = {
     "dram_read": "dram__bytes_read.sum",
     "dram_write": "dram__bytes_write.sum",
     "dram_pct": "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
-    "tensor_pct": "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+    "tensor_pct": "sm__ops_path_tensor_op_utchmma_src_tf32_dst_fp32_sparsity_off.sum.pct_of_peak_sustained_elapsed",
+    "smem_lsu_pct": "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+    "l2_pct": "lts__throughput.avg.pct_of_peak_sustained_elapsed",
     "sm_pct": "sm__throughput.avg.pct_of_peak_sustained_elapsed",
     "mem_pct": "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
     "regs": "launch__registers_per_thread",
@@ -30,13 +32,13 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-3, "us": 
 def phase_of(name):
     if "umma_kernel<0, 1" in name or "head_fwd" in name:
         return "fwd_gemm"
-    if "umma_kernel<0, 0" in name or "gemm_simt" in name:
+    if "umma_kernel<0, 0" in name or "gemm_simt" in name or "head_dx" in name:
         return "dx_gemm"
     if "umma_kernel<1, 1" in name or "head_dw" in name:
         return "dw_gemm"
-    if "mmd_tc" in name or "mmd_prep" in name:
+    if "mmd_tc" in name:
         return "mmd_pairs"
-    if "beta_" in name:
+    if "beta_" in name or "mmd_prep" in name:
         return "mmd_beta"
     if "ce_kernel" in name or "row_sum" in name:
         return "ce"
@@ -55,7 +57,7 @@ def main(rep, prefix):
     for r in rows[2:]:
         k = {"name": r[col["Kernel Name"]]}
         for key, metric in METRICS.items():
-            i = next((j for h, j in col.items() if h.endswith(metric)), None)
+            i = col.get(metric, next((j for h, j in col.items() if h.endswith(metric)), None))
             if i is None or not r[i]:
                 continue
             try:
@@ -83,12 +85,12 @@ def main(rep, prefix):
     with open(prefix + "_kernels.json", "w") as f:
         json.dump(out, f, indent=1)
     tot = sum(k.get("duration_us", 0) for k in kernels)
-    lines = [f"ncu --set full capture: {rep}", "one bank step, C2 x 32 models, per kernel:",
-             f"{'us':>9} {'share':>6} {'DRAM MB':>9} {'dram%':>6} {'tensor%':>8} {'SM%':>6}  kernel"]
+    lines = [f"ncu --set full capture: {rep}", "one bank step, C2 x 32 models, per kernel (tf32% = tf32 tensor-op rate vs peak):",
+             f"{'us':>9} {'share':>6} {'DRAM MB':>9} {'dram%':>6} {'tf32%':>6} {'L2%':>5} {'SM%':>6}  kernel"]
     for k in kernels:
         lines.append(f"{k.get('duration_us', 0):9.1f} {100 * k.get('duration_us', 0) / tot:5.1f}% "
                      f"{(k.get('dram_read', 0) + k.get('dram_write', 0)) / 1e6:9.1f} "
-                     f"{k.get('dram_pct', 0):6.1f} {k.get('tensor_pct', 0):8.1f} "
+                     f"{k.get('dram_pct', 0):6.1f} {k.get('tensor_pct', 0):6.1f} {k.get('l2_pct', 0):5.1f} "
                      f"{k.get('sm_pct', 0):6.1f}  {k['name'][:90]}")
     lines.append(f"{tot:9.1f}  total")
     lines.append("per phase: " + json.dumps({p: {"us": round(v["duration_us"], 1),
