@@ -64,6 +64,18 @@ struct mtk_bank {
     std::vector<float*> b, gW, gb;
     std::vector<float*> mW, vW, mb, vb;  // Adam moments (allocated on first Adam step)
     unsigned long long adam_t = 0;       // OptimizerState::step (optim.hpp:41)
+    float* adam_g = nullptr;             // gradient scratch for Adam on the GEMM paths
+    size_t adam_g_elems = 0;
+    float* adam_grad(int mat) {
+        const size_t n = (size_t)G * fan_in(mat) * fan_out(mat);
+        if (n > adam_g_elems) {
+            MTK_CUDA(cudaStreamSynchronize(ctx->stream));
+            cudaFree(adam_g);
+            MTK_CUDA(cudaMalloc(&adam_g, n * sizeof(float)));
+            adam_g_elems = n;
+        }
+        return adam_g;
+    }
     bool keep_grads = false;
     int capB = 0;
     Plane3 Xsp;               // hi/lo planes of the input (f borrowed per call)
@@ -121,6 +133,7 @@ struct mtk_bank {
         for (auto* p : vW) cudaFree(p);
         for (auto* p : mb) cudaFree(p);
         for (auto* p : vb) cudaFree(p);
+        cudaFree(adam_g);
         free_acts();
         cudaFree(loss);
         cudaFree(mmd);
@@ -398,11 +411,17 @@ void gemm_dx(mtk_bank& k, int mat, const Plane3& dz, int B, int r0, int rows, co
 void gemm_dw(mtk_bank& k, int mat, const Plane3& in, const Plane3& dz, int B, int r0, int rows,
              float lr, AdamArgs adam) {
     Ctx& c = *k.ctx;
+    const int fi = k.fan_in(mat), fo = k.fan_out(mat);
     if (adam.on) {
         adam.m = k.mW[mat];
         adam.v = k.vW[mat];
     }
-    const int fi = k.fan_in(mat), fo = k.fan_out(mat);
+    // Adam on the GEMM paths: the epilogue stores the gradient, adam_apply updates
+    const bool adam_gemm = adam.on && (k.tc[k.layer_of(mat)] || !head_dw_ok(fo));
+    float* gbuf = nullptr;
+    if (adam_gemm) {
+        gbuf = k.keep_grads ? k.gW[mat] : k.adam_grad(mat);
+    }
     if (k.tc[k.layer_of(mat)]) {
         UmmaGemm u;
         u.G = k.G;
@@ -417,15 +436,16 @@ void gemm_dw(mtk_bank& k, int mat, const Plane3& in, const Plane3& dz, int B, in
         u.b = dz.f + (size_t)r0 * fo;
         u.b_rs = fo;
         u.b_gs = (long long)B * fo;
-        u.epi = Epi::kSgd;
-        u.C = k.W[mat].f;
+        u.epi = adam_gemm ? Epi::kStore : Epi::kSgd;
+        u.C = adam_gemm ? gbuf : k.W[mat].f;
         u.c_gs = (long long)fi * fo;
         u.ldc = fo;
         u.lr = lr;
-        u.adam = adam;
-        u.grad_out = k.keep_grads ? k.gW[mat] : nullptr;
+        u.grad_out = (!adam_gemm && k.keep_grads) ? k.gW[mat] : nullptr;
         u.flags = c.d_flags;
         launch_umma(u, c.stream);
+        if (adam_gemm)
+            launch_adam_apply(k.W[mat].f, gbuf, (long long)k.G * fi * fo, lr, adam, c.d_flags, c.stream);
     } else if (head_dw_ok(fo)) {
         HeadDw h;
         h.G = k.G;
@@ -469,17 +489,18 @@ void gemm_dw(mtk_bank& k, int mat, const Plane3& in, const Plane3& dz, int B, in
         g.b_gs = (long long)B * fo;
         g.b_ks = fo;
         g.b_ns = 1;
-        g.C = k.W[mat].f;
-        g.C_hi = k.W[mat].hi;
-        g.C_lo = k.W[mat].lo;
+        g.C = adam_gemm ? gbuf : k.W[mat].f;
+        g.C_hi = adam_gemm ? nullptr : k.W[mat].hi;
+        g.C_lo = adam_gemm ? nullptr : k.W[mat].lo;
         g.c_gs = (long long)fi * fo;
         g.ldc = fo;
-        g.epi = Epi::kSgd;
+        g.epi = adam_gemm ? Epi::kStore : Epi::kSgd;
         g.lr = lr;
-        g.adam = adam;
-        g.grad_out = k.keep_grads ? k.gW[mat] : nullptr;
+        g.grad_out = (!adam_gemm && k.keep_grads) ? k.gW[mat] : nullptr;
         g.flags = c.d_flags;
         launch_gemm(g, c.stream);
+        if (adam_gemm)
+            launch_adam_apply(k.W[mat].f, gbuf, (long long)k.G * fi * fo, lr, adam, c.d_flags, c.stream);
     }
 }
 

@@ -357,6 +357,15 @@ int mtk_diag_gemm_tf32x3(mtk_ctx* c, int a_mn, int b_mn, int G, int M, int N, in
         u.b_rs = b_mn ? N : K;
         u.b_gs = (long long)K * N;
         u.epi = Epi::kStore;
+        if (const char* e = getenv("MTK_DIAG_EPI")) {  // diagnostics: epilogue variants
+            if (e[0] == 's') {  // SGD against C as the master weight, lr = 1e-3
+                u.epi = Epi::kSgd;
+                u.lr = 1e-3f;
+            } else if (e[0] == 'm') {  // ReLU mask taken from C itself
+                u.epi = Epi::kMask;
+                u.mask = Cm;
+            }
+        }
         u.C = Cm;
         u.c_gs = (long long)M * N;
         u.ldc = N;

@@ -81,6 +81,10 @@ struct AdamArgs {
     float* v = nullptr;
 };
 #ifdef __CUDACC__
+// For the simple (not unrolled) update loops: bias, skinny-head dW, adam_apply.
+// The tensor-core / SIMT GEMM epilogues do SGD only; under Adam they store the
+// gradient and launch_adam_apply updates (keeps Adam's division / sqrt slow
+// paths out of the unrolled epilogues).
 __device__ __forceinline__ float param_update(float w, float g, float lr, const AdamArgs& a,
                                               long long idx) {
     if (!a.on) return w - lr * g;
@@ -115,7 +119,6 @@ struct Gemm {
     const float* add = nullptr;   // kMask: optional addend, same layout as C
     const float* mask = nullptr;  // kMask: mask source, same layout as C
     float lr = 0.f;               // kSgd
-    AdamArgs adam;                // kSgd: Adam instead of SGD when adam.on
     float* grad_out = nullptr;    // kSgd: optional copy of acc, same layout as C
     float* C_hi = nullptr;        // optional tf32 split planes of the result
     float* C_lo = nullptr;
@@ -123,6 +126,9 @@ struct Gemm {
 };
 
 void launch_gemm(const Gemm& g, cudaStream_t s);
+// W[i] -= Adam step from grad[i], i < n (moments in a.m / a.v); non-finite -> flags
+void launch_adam_apply(float* W, const float* grad, long long n, float lr, const AdamArgs& a,
+                       int* flags, cudaStream_t s);
 
 // tcgen05 3xTF32 grouped GEMM (k_umma.cu).  Operands are plain fp32; element
 // (r, c) sits at base[g*gs + r*rs + c], c being the contiguous index: for a
@@ -143,7 +149,6 @@ struct UmmaGemm {
     const float* add = nullptr;
     const float* mask = nullptr;
     float lr = 0.f;
-    AdamArgs adam;
     float* grad_out = nullptr;
     int* flags = nullptr;
 };

@@ -8,6 +8,7 @@
 // produced by exactly one thread with a fixed k order, so results are
 // bit-deterministic run to run.
 #include <cfloat>
+#include <algorithm>
 #include <cmath>
 
 #include "internal.h"
@@ -113,7 +114,7 @@ __global__ void __launch_bounds__(NT) gemm_simt_kernel(Gemm p) {
                     break;
                 case Epi::kSgd:
                     if (p.grad_out) p.grad_out[idx] = v;
-                    v = param_update(p.C[idx], v, p.lr, p.adam, idx);
+                    v = p.C[idx] - p.lr * v;
                     bad |= !isfinite(v);
                     break;
                 case Epi::kStore:
@@ -231,6 +232,29 @@ void launch_ce(const CeArgs& a, cudaStream_t s) {
     ce_kernel<<<(unsigned)((rows + 127) / 128), 128, 0, s>>>(a);
     count_launch();
     row_sum_kernel<<<a.G, 256, 0, s>>>(a.row_loss, a.B, a.loss, a.flags);
+    count_launch();
+}
+
+namespace {
+__global__ void adam_apply_kernel(float* W, const float* grad, long long n, float lr, AdamArgs a,
+                                  int* flags) {
+    bool bad = false;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const float w = param_update(W[i], grad[i], lr, a, i);
+        bad |= !isfinite(w);
+        W[i] = w;
+    }
+    if (bad && flags) atomicOr(flags, kFlagNonFinite);
+}
+
+}  // namespace
+
+void launch_adam_apply(float* W, const float* grad, long long n, float lr, const AdamArgs& a,
+                       int* flags, cudaStream_t s) {
+    if (n <= 0) return;
+    const long long blocks = std::min<long long>((n + 255) / 256, 148LL * 16);
+    adam_apply_kernel<<<(unsigned)blocks, 256, 0, s>>>(W, grad, n, lr, a, flags);
     count_launch();
 }
 

@@ -3,11 +3,15 @@
 //
 // C[g] (M x N) = A[g] (M x K) * B[g] (K x N) for G independent models.
 // Operands live in HBM as plain fp32 and are staged into smem by TMA.
-// Converter warps split each staged tile on chip: hi = rna_tf32(x) in place
-// and lo = rna_tf32(x - hi) in a second tile (the tf32 MMA truncates fp32
-// inputs -- measured by tools/umma_probe.cu -- so both parts are exact tf32),
-// and three MMAs per k step give fp32-level products (3xTF32):
-//     A*B ~= A_hi*B_lo + A_lo*B_hi + A_hi*B_hi      (dropped A_lo*B_lo ~ 2^-22)
+// The tf32 MMA truncates fp32 inputs (measured by tools/umma_probe.cu), so
+// the staged fp32 tile itself serves as hi = trunc_tf32(x); converter warps
+// add lo = rna_tf32(x - hi) (x - hi is exact) in a second tile, and three MMAs
+// per k step give fp32-level products (3xTF32):
+//     A*B ~= A_hi*B_lo + A_lo*B_hi + A_hi*B_hi      (dropped A_lo*B_lo < 2^-20)
+// Truncated hi doubles the dropped term against rna hi (still ~1e-7 of
+// max|C| on the bank's operands); it saves the in-place hi write-back, a
+// seventh of the stage's shared-memory traffic, which bounds this kernel.
+// (The MMD kernel keeps rna hi: its d^2 = n_i + n_j - 2 z_i.z_j cancels.)
 // HBM and L2 carry 4 bytes per operand element, as for an fp32 SIMT GEMM.
 //
 // Replaces, for the bank's dense layers, the reference loops
@@ -25,7 +29,7 @@
 // Warp roles: w0 TMA producer, w1 MMA issuer (one elected thread), w2-w5
 // epilogue (TMEM -> registers -> fused bias/ReLU | ReLU-mask | SGD -> HBM),
 // w6-w13 converters.  Two rings: LS load stages (32 KB: A and B fp32 as TMA
-// wrote them, hi written back in place) and LO lo stages (32 KB: A lo, B lo),
+// wrote them = the hi operands) and LO lo stages (32 KB: A lo, B lo),
 // so TMA runs LS stages ahead while only LO stages hold lo planes.  128-B
 // swizzle; 32-B-atom swizzle for MN-major operands (the only layout tf32
 // accepts).
@@ -45,11 +49,13 @@ namespace {
 
 using namespace sm100;
 
-constexpr int BK = 32, LS = 5, LO = 2;
+constexpr int BK = 32, LS = 4, LO = 2;
 constexpr int TILE_BYTES = 128 * BK * 4;     // 16 KB: 128 rows (or cols) x 32 k
 constexpr int LOAD_BYTES = 2 * TILE_BYTES;   // load stage: A fp32, B fp32 (TMA bytes)
 constexpr int LO_BYTES = 2 * TILE_BYTES;     // lo stage: A lo, B lo
-constexpr int SMEM_BYTES = LS * LOAD_BYTES + LO * LO_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int EPI_LD = 36;                          // transpose tile row stride (floats)
+constexpr int EPI_BYTES = 4 * 32 * EPI_LD * 4;      // one 32 x 32 tile per epilogue warp
+constexpr int SMEM_BYTES = LS * LOAD_BYTES + LO * LO_BYTES + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 constexpr int NUM_CONV_WARPS = 8;
 constexpr int NUM_THREADS = 192 + 32 * NUM_CONV_WARPS;
 
@@ -64,7 +70,6 @@ struct UmmaParams {
     const float* add;
     const float* mask;
     float lr;
-    AdamArgs adam;
     float* grad_out;
     int* flags;
     unsigned long long* trace;  // diagnostics: timestamps of CTA (0,0,0)
@@ -89,9 +94,9 @@ __device__ __forceinline__ void load_operand(uint8_t* dst, const CUtensorMap* ma
     }
 }
 
-// hi = rna_tf32(x) (in place), lo = rna_tf32(x - hi) over the two fp32 tiles
-// of a load stage.  The transform is elementwise, so it ignores the swizzle:
-// lo sits at the same offset in the lo stage.
+// lo = rna_tf32(x - trunc_tf32(x)) over the two fp32 tiles of a load stage
+// (the tiles stay untouched as the hi operands).  The transform is
+// elementwise, so it ignores the swizzle: lo sits at the same offset.
 __device__ __forceinline__ void convert_stage(uint8_t* st, uint8_t* lo, int t) {
     constexpr int NT = 32 * NUM_CONV_WARPS;
     const uint32_t src = smem_u32(st) + 16 * t, dst = smem_u32(lo) + 16 * t;
@@ -100,12 +105,11 @@ __device__ __forceinline__ void convert_stage(uint8_t* st, uint8_t* lo, int t) {
     for (int j = 0; j < 2048 / NT; ++j) x[j] = lds128(src + 16 * NT * j);
 #pragma unroll
     for (int j = 0; j < 2048 / NT; ++j) {
-        float4 h, l;
-        split_tf32(x[j].x, h.x, l.x);
-        split_tf32(x[j].y, h.y, l.y);
-        split_tf32(x[j].z, h.z, l.z);
-        split_tf32(x[j].w, h.w, l.w);
-        sts128(src + 16 * NT * j, h);  // hi = rna(x) in place, |lo| <= 2^-11 |x|
+        float4 l;
+        l.x = tf32_rna(x[j].x - tf32_trunc(x[j].x));
+        l.y = tf32_rna(x[j].y - tf32_trunc(x[j].y));
+        l.z = tf32_rna(x[j].z - tf32_trunc(x[j].z));
+        l.w = tf32_rna(x[j].w - tf32_trunc(x[j].w));
         sts128(dst + 16 * NT * j, l);
     }
 }
@@ -141,86 +145,137 @@ __device__ __forceinline__ void mma_stage(uint32_t tmem, uint32_t base, uint32_t
 }
 
 // TMEM accumulator (this warp's 32 lanes = rows m0+32q.., ncols columns) ->
-// fused epilogue -> fp32 C in HBM.  Each thread owns one row.
-__device__ __forceinline__ void epilogue_rows(const UmmaParams& p, uint32_t tmem, int q, int lane,
-                                              int g, int m0, int n0, int ncols) {
-    const int m = m0 + 32 * q + lane;
-    const bool row_ok = m < p.M;
-    const long long rowbase = (long long)g * p.c_gs + (long long)m * p.ldc;
+// fused epilogue -> fp32 C in HBM.  Per 32 x 32 chunk the warp transposes
+// through smem (thread = row after tcgen05.ld; then 8 threads x float4 per
+// row, 4 rows per instruction), so each global access instruction touches
+// four 128-B row segments instead of 32 rows' 16-B pieces; all operand loads
+// of a chunk (bias | mask, add | master weight) are in flight together.
+__device__ __forceinline__ void epilogue_tile(const UmmaParams& p, uint32_t tmem, int q, int lane,
+                                              int g, int m0, int n0, int ncols, uint32_t sb) {
+    const int epi = p.epi;
+    const int mw = m0 + 32 * q;       // first row of this warp
+    const int c4 = lane & 7;          // float4 column within the chunk
+    const int r0 = lane >> 3;         // row offset 0..3 (+4 i)
     bool bad = false;
 #pragma unroll 1
     for (int c = 0; c < ncols / 32; ++c) {
-        float v[32];
-        tmem_ld_32x32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(c * 32), v);
         const int nb = n0 + c * 32;
-        if (!row_ok || nb >= p.N) continue;
-        const bool vec = (nb + 32 <= p.N) && ((rowbase + nb) % 4 == 0);
-        if (vec) {
+        if (nb >= p.N) break;  // warp-uniform
+        const int n = nb + 4 * c4;
+        const bool full4 = n + 4 <= p.N;
+        float4 o1[8], o2[8];
 #pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-                const long long idx = rowbase + nb + j;
-                float4 x = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-                if (p.epi == (int)Epi::kBias || p.epi == (int)Epi::kBiasRelu) {
-                    const float* bp = p.bias + g * p.bias_gs + nb + j;
-                    x.x += bp[0];
-                    x.y += bp[1];
-                    x.z += bp[2];
-                    x.w += bp[3];
-                    bad |= !(isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w));
-                    if (p.epi == (int)Epi::kBiasRelu) {
-                        x.x = x.x > 0.f ? x.x : 0.f;
-                        x.y = x.y > 0.f ? x.y : 0.f;
-                        x.z = x.z > 0.f ? x.z : 0.f;
-                        x.w = x.w > 0.f ? x.w : 0.f;
-                    }
-                } else if (p.epi == (int)Epi::kMask) {
-                    if (p.add) {
-                        const float4 a = *reinterpret_cast<const float4*>(p.add + idx);
-                        x.x = a.x + x.x;
-                        x.y = a.y + x.y;
-                        x.z = a.z + x.z;
-                        x.w = a.w + x.w;
-                    }
-                    const float4 mk = *reinterpret_cast<const float4*>(p.mask + idx);
-                    x.x = mk.x > 0.f ? x.x : 0.f;
-                    x.y = mk.y > 0.f ? x.y : 0.f;
-                    x.z = mk.z > 0.f ? x.z : 0.f;
-                    x.w = mk.w > 0.f ? x.w : 0.f;
-                } else if (p.epi == (int)Epi::kSgd) {  // C is the fp32 master weight
-                    if (p.grad_out) *reinterpret_cast<float4*>(p.grad_out + idx) = x;
-                    const float4 w = *reinterpret_cast<const float4*>(p.C + idx);
-                    x.x = param_update(w.x, x.x, p.lr, p.adam, idx);
-                    x.y = param_update(w.y, x.y, p.lr, p.adam, idx + 1);
-                    x.z = param_update(w.z, x.z, p.lr, p.adam, idx + 2);
-                    x.w = param_update(w.w, x.w, p.lr, p.adam, idx + 3);
-                    bad |= !(isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w));
+        for (int i = 0; i < 8; ++i) {
+            const int m = mw + r0 + 4 * i;
+            const long long idx = (long long)g * p.c_gs + (long long)m * p.ldc + n;
+            o1[i] = o2[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (m < p.M && full4) {
+                if (epi == (int)Epi::kMask) {
+                    o1[i] = *reinterpret_cast<const float4*>(p.mask + idx);
+                    if (p.add) o2[i] = *reinterpret_cast<const float4*>(p.add + idx);
+                } else if (epi == (int)Epi::kSgd) {
+                    o1[i] = *reinterpret_cast<const float4*>(p.C + idx);
                 }
-                *reinterpret_cast<float4*>(p.C + idx) = x;
-            }
-        } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                const int n = nb + j;
-                if (n >= p.N) break;
-                const long long idx = rowbase + n;
-                float x = v[j];
-                if (p.epi == (int)Epi::kBias || p.epi == (int)Epi::kBiasRelu) {
-                    x += p.bias[g * p.bias_gs + n];
-                    bad |= !isfinite(x);
-                    if (p.epi == (int)Epi::kBiasRelu) x = x > 0.f ? x : 0.f;
-                } else if (p.epi == (int)Epi::kMask) {
-                    if (p.add) x = p.add[idx] + x;
-                    x = (p.mask[idx] > 0.f) ? x : 0.f;
-                } else if (p.epi == (int)Epi::kSgd) {
-                    if (p.grad_out) p.grad_out[idx] = x;
-                    x = param_update(p.C[idx], x, p.lr, p.adam, idx);
-                    bad |= !isfinite(x);
-                }
-                p.C[idx] = x;
             }
         }
+        float4 bias = make_float4(0.f, 0.f, 0.f, 0.f);
+        if ((epi == (int)Epi::kBias || epi == (int)Epi::kBiasRelu) && full4)
+            bias = *reinterpret_cast<const float4*>(p.bias + g * p.bias_gs + n);
+        float v[32];
+        tmem_ld_32x32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(c * 32), v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            sts128(sb + (uint32_t)((lane * EPI_LD + 4 * j) * 4),
+                   make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int r = r0 + 4 * i, m = mw + r;
+            if (m >= p.M) continue;
+            const long long idx = (long long)g * p.c_gs + (long long)m * p.ldc + n;
+            float4 x = lds128(sb + (uint32_t)((r * EPI_LD + 4 * c4) * 4));
+            if (!full4) {  // ragged right edge: scalar tail
+                const float xs[4] = {x.x, x.y, x.z, x.w};
+                for (int e = 0; e < 4 && n + e < p.N; ++e) {
+                    float y = xs[e];
+                    const long long ie = idx + e;
+                    if (epi == (int)Epi::kBias || epi == (int)Epi::kBiasRelu) {
+                        y += p.bias[g * p.bias_gs + n + e];
+                        bad |= !isfinite(y);
+                        if (epi == (int)Epi::kBiasRelu) y = y > 0.f ? y : 0.f;
+                    } else if (epi == (int)Epi::kMask) {
+                        if (p.add) y = p.add[ie] + y;
+                        y = (p.mask[ie] > 0.f) ? y : 0.f;
+                    } else if (epi == (int)Epi::kSgd) {
+                        if (p.grad_out) p.grad_out[ie] = y;
+                        y = p.C[ie] - p.lr * y;
+                        bad |= !isfinite(y);
+                    }
+                    p.C[ie] = y;
+                }
+                continue;
+            }
+            if (epi == (int)Epi::kBias || epi == (int)Epi::kBiasRelu) {
+                x.x += bias.x;
+                x.y += bias.y;
+                x.z += bias.z;
+                x.w += bias.w;
+                bad |= !(isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w));
+                if (epi == (int)Epi::kBiasRelu) {
+                    x.x = x.x > 0.f ? x.x : 0.f;
+                    x.y = x.y > 0.f ? x.y : 0.f;
+                    x.z = x.z > 0.f ? x.z : 0.f;
+                    x.w = x.w > 0.f ? x.w : 0.f;
+                }
+            } else if (epi == (int)Epi::kMask) {
+                if (p.add) {
+                    x.x = o2[i].x + x.x;
+                    x.y = o2[i].y + x.y;
+                    x.z = o2[i].z + x.z;
+                    x.w = o2[i].w + x.w;
+                }
+                x.x = o1[i].x > 0.f ? x.x : 0.f;
+                x.y = o1[i].y > 0.f ? x.y : 0.f;
+                x.z = o1[i].z > 0.f ? x.z : 0.f;
+                x.w = o1[i].w > 0.f ? x.w : 0.f;
+            } else if (epi == (int)Epi::kSgd) {  // C is the fp32 master weight
+                if (p.grad_out) *reinterpret_cast<float4*>(p.grad_out + idx) = x;
+                x.x = o1[i].x - p.lr * x.x;
+                x.y = o1[i].y - p.lr * x.y;
+                x.z = o1[i].z - p.lr * x.z;
+                x.w = o1[i].w - p.lr * x.w;
+                bad |= !(isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w));
+            }
+            *reinterpret_cast<float4*>(p.C + idx) = x;
+        }
+        __syncwarp();
     }
     if (bad && p.flags) atomicOr(p.flags, kFlagNonFinite);
+}
+
+// L2 prefetch of the global operands the epilogue of a tile will read (its
+// 128 rows of the master weight, or the ReLU mask and addend), issued by the
+// producer warp a few stages before the tile's mainloop ends.
+__device__ __forceinline__ void prefetch_epilogue_rows(const UmmaParams& p, int g, int m0, int n0,
+                                                       int ncols, int lane) {
+    const float* src[2] = {nullptr, nullptr};
+    if (p.epi == (int)Epi::kSgd) src[0] = p.C;
+    else if (p.epi == (int)Epi::kMask) { src[0] = p.mask; src[1] = p.add; }
+    if (!src[0]) return;
+    const int n1 = min(n0 + ncols, p.N);
+    if (n1 <= n0) return;
+    const uint32_t bytes = (uint32_t)(n1 - n0) * 4;
+    if (bytes % 16) return;
+    for (int rr = lane; rr < 128; rr += 32) {
+        const int m = m0 + rr;
+        if (m >= p.M) break;
+        for (int i = 0; i < 2; ++i) {
+            if (!src[i]) continue;
+            const float* a = src[i] + (long long)g * p.c_gs + (long long)m * p.ldc + n0;
+            if (reinterpret_cast<uintptr_t>(a) & 15) continue;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(bytes) : "memory");
+        }
+    }
 }
 
 template <int A_MN, int B_MN, bool PAIR>
@@ -231,7 +286,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_kernel(const __grid_const
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* lo_ring = smem + LS * LOAD_BYTES;
-    uint64_t* full = reinterpret_cast<uint64_t*>(lo_ring + LO * LO_BYTES);
+    uint8_t* epi_smem = lo_ring + LO * LO_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(lo_ring + LO * LO_BYTES + EPI_BYTES);
     uint64_t* empty = full + LS;
     uint64_t* conv = empty + LS;
     uint64_t* lofree = conv + LO;
@@ -248,6 +304,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_kernel(const __grid_const
     const int ncl = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
     const int nk = (p.K + BK - 1) / BK;
     unsigned long long* tr = (p.trace && blockIdx.x == 0) ? p.trace : nullptr;
+    if (p.trace && threadIdx.x == 0 && blockIdx.x < 400) p.trace[4000 + 2 * blockIdx.x] = gtime();
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&p.a);
@@ -276,8 +333,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_kernel(const __grid_const
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
+    // Producer and MMA warps run their loops converged (all lanes wait, lane 0
+    // issues); see k_mmd_tc.cu for the divergent-lane stall this avoids.
     if (warp == 0) {
-        if (lane == 0) {
+        {
             // ---------------- TMA producer ----------------
             uint32_t it = 0;
             for (int t = cid; t < ntiles; t += ncl) {
@@ -286,19 +345,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_kernel(const __grid_const
                 const int nb0 = nt * TN + (int)rank * 128;  // B columns staged by this CTA
                 for (int kb = 0; kb < nk; ++kb, ++it) {
                     const int s = it % LS;
+                    if (kb == (nk > 8 ? nk - 8 : 0)) prefetch_epilogue_rows(p, g, m0, nt * TN, TN, lane);
                     mbar_wait(&empty[s], ((it / LS) & 1) ^ 1);
-                    if (tr && it < 1000) tr[it] = gtime();
                     uint8_t* st = smem + s * LOAD_BYTES;
-                    mbar_expect_tx(&full[s], LOAD_BYTES);
-                    load_operand<A_MN>(st, &p.a, &full[s], m0, kb * BK, g);
-                    load_operand<B_MN>(st + TILE_BYTES, &p.b, &full[s], nb0, kb * BK, g);
+                    if (lane == 0) {
+                        if (tr && it < 1000) tr[it] = gtime();
+                        mbar_expect_tx(&full[s], LOAD_BYTES);
+                        load_operand<A_MN>(st, &p.a, &full[s], m0, kb * BK, g);
+                        load_operand<B_MN>(st + TILE_BYTES, &p.b, &full[s], nb0, kb * BK, g);
+                    }
+                    __syncwarp();
                 }
             }
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer (leader CTA, one thread) ----------------
         constexpr uint32_t idesc = idesc_tf32(PAIR ? 256 : 128, TN, A_MN, B_MN);
-        if (rank == 0 && lane == 0) {
+        if (rank == 0) {
             uint32_t it = 0, tl = 0;
             for (int t = cid; t < ntiles; t += ncl, ++tl) {
                 const uint32_t b = tl & 1;
@@ -308,20 +371,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_kernel(const __grid_const
                 for (int kb = 0; kb < nk; ++kb, ++it) {
                     const int s = it % LS, l = it % LO;
                     mbar_wait(&conv[l], (it / LO) & 1);
-                    if (tr && it < 1000) tr[1000 + it] = gtime();
                     tc_fence_after();
-                    mma_stage<A_MN, B_MN, PAIR>(acc, smem_u32(smem + s * LOAD_BYTES),
-                                                smem_u32(lo_ring + l * LO_BYTES), idesc, kb == 0);
-                    if (PAIR) {  // frees the slots in both CTAs
-                        mma_commit_2sm(&empty[s], 0x3);
-                        mma_commit_2sm(&lofree[l], 0x3);
-                    } else {
-                        mma_commit(&empty[s]);
-                        mma_commit(&lofree[l]);
+                    if (lane == 0) {
+                        if (tr && it < 1000) tr[1000 + it] = gtime();
+                        mma_stage<A_MN, B_MN, PAIR>(acc, smem_u32(smem + s * LOAD_BYTES),
+                                                    smem_u32(lo_ring + l * LO_BYTES), idesc, kb == 0);
+                        if (PAIR) {  // frees the slots in both CTAs
+                            mma_commit_2sm(&empty[s], 0x3);
+                            mma_commit_2sm(&lofree[l], 0x3);
+                        } else {
+                            mma_commit(&empty[s]);
+                            mma_commit(&lofree[l]);
+                        }
                     }
+                    __syncwarp();
                 }
-                if (PAIR) mma_commit_2sm(&acc_full[b], 0x3);
-                else mma_commit(&acc_full[b]);
+                if (lane == 0) {
+                    if (PAIR) mma_commit_2sm(&acc_full[b], 0x3);
+                    else mma_commit(&acc_full[b]);
+                }
+                __syncwarp();
             }
         }
     } else if (warp < 6) {
@@ -335,7 +404,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_kernel(const __grid_const
             mbar_wait(&acc_full[b], (tl >> 1) & 1);
             if (tr && threadIdx.x == 64 && tl < 16) tr[2000 + 2 * tl] = gtime();
             tc_fence_after();
-            epilogue_rows(p, tmem + b * TN, q, lane, g, m0, nt * TN, TN);
+            epilogue_tile(p, tmem + b * TN, q, lane, g, m0, nt * TN, TN,
+                          smem_u32(epi_smem) + (uint32_t)(q * 32 * EPI_LD * 4));
             tc_fence_before();
             __syncwarp();
             if (tr && threadIdx.x == 64 && tl < 16) tr[2001 + 2 * tl] = gtime();
@@ -367,6 +437,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_kernel(const __grid_const
     tc_fence_before();
     if (PAIR) cluster_sync();
     else __syncthreads();
+    if (tr && threadIdx.x == 32) tr[2040] = gtime();
+    if (p.trace && threadIdx.x == 32 && blockIdx.x < 400) p.trace[4001 + 2 * blockIdx.x] = gtime();
     if (warp == 1) {
         tc_fence_after();
         if (PAIR) tmem_dealloc_2sm<TMEM_COLS>(tmem);
@@ -517,7 +589,6 @@ void launch_umma(const UmmaGemm& u, cudaStream_t s) {
     p.add = u.add;
     p.mask = u.mask;
     p.lr = u.lr;
-    p.adam = u.adam;
     p.grad_out = u.grad_out;
     p.flags = u.flags;
     if (const char* t = getenv("MTK_UMMA_TRACE"))

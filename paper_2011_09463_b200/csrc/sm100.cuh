@@ -281,6 +281,10 @@ __device__ __forceinline__ void sts128(uint32_t a, float4 v) {
                  "f"(v.w)
                  : "memory");
 }
+// what the tf32 MMA reads from an fp32 operand: the low 13 mantissa bits dropped
+__device__ __forceinline__ float tf32_trunc(float x) {
+    return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+}
 // 3xTF32 split: x ~= hi + lo, both tf32-exact
 __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
     hi = tf32_rna(x);
