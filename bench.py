@@ -209,15 +209,10 @@ def run_reference_arm(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
-# the phase's main kernel in the ncu capture summaries (profile_summary.py)
-PHASE_KERNEL = {"mmd_pairs": "mmd_tc_kernel", "fwd_gemm": "umma_kernel<0, 1",
-                "dx_gemm": "umma_kernel<0, 0", "dw_gemm": "umma_kernel<1, 1"}
-
-
 def kernel_traffic(phase):
-    """DRAM read+write bytes per launch of the phase's main kernel, from the
-    newest committed ncu --set full capture summary (profiles/rNN_kernels.json).
-    Returns (bytes or None, source file)."""
+    """DRAM read+write bytes per step of a phase's kernels (the same launches
+    `achieved` is timed over), from the newest committed ncu --set full capture
+    summary (profiles/rNN_kernels.json).  Returns (bytes or None, source file)."""
     import glob
 
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r[0-9]*_kernels.json")))
@@ -225,12 +220,8 @@ def kernel_traffic(phase):
         return None, None
     with open(files[-1]) as f:
         d = json.load(f)
-    name = PHASE_KERNEL.get(phase)
-    ks = [k for k in d.get("kernels", []) if name and name in k["name"]]
-    if not ks:
-        return None, os.path.basename(files[-1])
-    tot = sum(k.get("dram_read", 0.0) + k.get("dram_write", 0.0) for k in ks)
-    return tot / len(ks), os.path.basename(files[-1])
+    ent = d.get("phases", {}).get(phase)
+    return (ent.get("dram_bytes_per_step") if ent else None), os.path.basename(files[-1])
 
 
 # ----------------------------------------------------------------------------- GPU arm
@@ -360,9 +351,9 @@ def run_gpu_arm(args, world, rank, local):
                      "peak_note": (f"fp32-accurate tensor peak = 3xTF32 = tf32/3 = {src} bf16 "
                                    f"{bf16} TFLOP/s / 6; frac vs plain tf32 "
                                    f"{achieved / tf32_peak:.3f}, vs bf16 {achieved / bf16:.3f}"),
-                     "traffic_note": (f"DRAM read+write bytes per launch of "
-                                      f"{PHASE_KERNEL.get(dominant)} (profiles/{traffic_src}, "
-                                      "one ncu --set full capture)")},
+                     "traffic_note": (f"DRAM read+write bytes per step of the {dominant} "
+                                      f"phase's {ph[dominant][1] / args.steps:.0f} launch(es), "
+                                      f"profiles/{traffic_src} (one ncu --set full capture)")},
         "step_tflops": step_flop / (ms_step / 1000.0) / 1e12,
         "gemm_tflops": step_flop / (gemm_ms / 1000.0) / 1e12 if gemm_ms else None,
         "cpu_baseline": cpu,
