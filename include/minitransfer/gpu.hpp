@@ -154,6 +154,8 @@ class Bank {
         check(mtk_bank_train_step(h_, &s, loss.data(), mmd ? mmd->data() : nullptr), "train_step");
         return loss;
     }
+    // a fresh Adam state (OptimizerState, optim.hpp:13-26): zero moments, step 0
+    void reset_optimizer() { check(mtk_bank_reset_optimizer(h_), "reset_optimizer"); }
     void forward(const float* X, int B, float* logits, int head = 0, float* hidden = nullptr) {
         check(mtk_bank_forward(h_, X, B, head, logits, hidden), "forward");
     }
