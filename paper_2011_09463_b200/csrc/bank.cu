@@ -87,6 +87,7 @@ struct mtk_bank {
     double* mmd = nullptr;
     double* beta = nullptr;
     float* gH = nullptr;
+    float* colsum = nullptr;  // [G][ceil(B/32)][max dim] bias-gradient partials from the DX epilogues
     double* mmd_part = nullptr;
     size_t mmd_part_bytes = 0;
     float* head_scratch = nullptr;  // skinny dW partial sums
@@ -220,6 +221,8 @@ struct mtk_bank {
         cudaFree(logits);
         cudaFree(row_loss);
         cudaFree(gH);
+        cudaFree(colsum);
+        colsum = nullptr;
         logits = nullptr;
         gH = nullptr;
         row_loss = nullptr;
@@ -235,6 +238,7 @@ struct mtk_bank {
         MTK_CUDA(cudaMalloc(&logits, GB * dims[L] * sizeof(float)));
         MTK_CUDA(cudaMalloc(&row_loss, GB * sizeof(double)));
         if (L > 1) MTK_CUDA(cudaMalloc(&gH, GB * dims[L - 1] * sizeof(float)));
+        MTK_CUDA(cudaMalloc(&colsum, (size_t)G * ((B + 31) / 32) * maxd() * sizeof(float)));
         capB = B;
     }
     void ensure_stage(int B) {
@@ -337,8 +341,10 @@ void gemm_fwd(mtk_bank& k, int mat, const Plane3& in, int B, int r0, int rows, c
 }
 
 // DX: out[r, p] = (sum_j dz[r, j] W[p, j] + add[r, p]) * (mask[r, p] > 0)
-void gemm_dx(mtk_bank& k, int mat, const Plane3& dz, int B, int r0, int rows, const Plane3& out,
-             const float* mask, const float* add) {
+// returns true when `colsum` received the per-32-row-block column sums of out
+// (the next layer's bias gradient), false when the caller must reduce it
+bool gemm_dx(mtk_bank& k, int mat, const Plane3& dz, int B, int r0, int rows, const Plane3& out,
+             const float* mask, const float* add, float* colsum = nullptr) {
     Ctx& c = *k.ctx;
     const int fi = k.fan_in(mat), fo = k.fan_out(mat);
     if (k.tc[k.layer_of(mat)]) {
@@ -361,8 +367,10 @@ void gemm_dx(mtk_bank& k, int mat, const Plane3& dz, int B, int r0, int rows, co
         u.ldc = fi;
         u.mask = mask + (size_t)r0 * fi;
         u.add = add ? add + (size_t)r0 * fi : nullptr;
+        u.colsum = colsum;
         u.flags = c.d_flags;
         launch_umma(u, c.stream);
+        return colsum != nullptr;
     } else if (head_dx_ok(fi, fo)) {
         HeadDx h;
         h.G = k.G;
@@ -379,7 +387,9 @@ void gemm_dx(mtk_bank& k, int mat, const Plane3& dz, int B, int r0, int rows, co
         h.ldc = fi;
         h.mask = mask + (size_t)r0 * fi;
         h.add = add ? add + (size_t)r0 * fi : nullptr;
+        h.colsum = colsum;
         launch_head_dx(h, c.stream);
+        return colsum != nullptr;
     } else {
         Gemm g;
         g.G = k.G;
@@ -404,6 +414,7 @@ void gemm_dx(mtk_bank& k, int mat, const Plane3& dz, int B, int r0, int rows, co
         g.add = add ? add + (size_t)r0 * fi : nullptr;
         g.flags = c.d_flags;
         launch_gemm(g, c.stream);
+        return false;
     }
 }
 
@@ -661,7 +672,10 @@ void train_step(mtk_bank& k, const mtk_step& s, double* loss_host, double* mmd_h
         }
     }
 
-    // backward sweep, layer L-1 down to 0
+    // backward sweep, layer L-1 down to 0.  A DX launch also reduces its
+    // output's columns per 32-row block when the layer below is trainable,
+    // so that layer's bias update needs no second pass over dZ.
+    bool colsum_ready = false;
     for (int l = L - 1; l >= 0; --l) {
         const bool trainable = l >= s.frozen_layers;
         const bool need_dx = l > 0 && l > s.frozen_layers;
@@ -670,31 +684,14 @@ void train_step(mtk_bank& k, const mtk_step& s, double* loss_host, double* mmd_h
         // the DX output feeds layer l-1: only write its tf32 planes if that layer is tc
         const Plane3 out = *nxt;
         const bool split = (l == L - 1 && two);
-        if (need_dx) {
-            PhaseScope ph(c, kPhDx, split ? 2 : 1);
-            if (split) {
-                gemm_dx(k, l, *cur, B, 0, src, out, k.H[l].f, nullptr);
-                gemm_dx(k, l + 1, *cur, B, src, B - src, out, k.H[l].f, nullptr);
-                after_launch(c, 2);
-            } else {
-                gemm_dx(k, l, *cur, B, 0, B, out, k.H[l].f, add);
-                after_launch(c);
-            }
-        }
-        if (trainable) {
+        bool next_colsum = false;
+        if (trainable) {  // bias first: the DX below overwrites k.colsum
             const int fo = k.dims[l + 1];
-            {
-                PhaseScope ph(c, kPhDw, split ? 2 : 1);
-                if (split) {
-                    gemm_dw(k, l, in, *cur, B, 0, src, lr, adam);
-                    gemm_dw(k, l + 1, in, *cur, B, src, B - src, lr, adam);
-                } else {
-                    gemm_dw(k, l, in, *cur, B, 0, B, lr, adam);
-                }
-                after_launch(c, split ? 2 : 1);
-            }
             PhaseScope ph(c, kPhBias, split ? 2 : 1);
-            if (split) {
+            if (colsum_ready && !split) {
+                launch_bias_from_partials(k.G, (B + 31) / 32, fo, k.colsum, k.b[l], lr, bias_adam(l),
+                                          k.keep_grads ? k.gb[l] : nullptr, c.d_flags, c.stream);
+            } else if (split) {
                 launch_bias_sgd(k.G, src, fo, cur->f, (long long)B * fo, k.b[l], fo, lr, bias_adam(l),
                                 k.keep_grads ? k.gb[l] : nullptr, c.d_flags, c.stream);
                 launch_bias_sgd(k.G, B - src, fo, cur->f + (size_t)src * fo, (long long)B * fo,
@@ -706,6 +703,34 @@ void train_step(mtk_bank& k, const mtk_step& s, double* loss_host, double* mmd_h
             }
             after_launch(c, split ? 2 : 1);
         }
+        if (need_dx) {
+            PhaseScope ph(c, kPhDx, split ? 2 : 1);
+            if (split) {
+                gemm_dx(k, l, *cur, B, 0, src, out, k.H[l].f, nullptr);
+                gemm_dx(k, l + 1, *cur, B, src, B - src, out, k.H[l].f, nullptr);
+                after_launch(c, 2);
+            } else {
+                static const bool no_colsum = getenv("MTK_NO_COLSUM") != nullptr;  // A/B diagnostics
+                const bool below_trainable = l - 1 >= s.frozen_layers && !no_colsum;
+                const bool have = gemm_dx(k, l, *cur, B, 0, B, out, k.H[l].f, add,
+                                          below_trainable ? k.colsum : nullptr);
+                after_launch(c);
+                next_colsum = have;
+            }
+        }
+        if (trainable) {
+            {
+                PhaseScope ph(c, kPhDw, split ? 2 : 1);
+                if (split) {
+                    gemm_dw(k, l, in, *cur, B, 0, src, lr, adam);
+                    gemm_dw(k, l + 1, in, *cur, B, src, B - src, lr, adam);
+                } else {
+                    gemm_dw(k, l, in, *cur, B, 0, B, lr, adam);
+                }
+                after_launch(c, split ? 2 : 1);
+            }
+        }
+        colsum_ready = next_colsum;
         std::swap(cur, nxt);
     }
 

@@ -150,6 +150,7 @@ struct UmmaGemm {
     const float* mask = nullptr;
     float lr = 0.f;
     float* grad_out = nullptr;
+    float* colsum = nullptr;  // kMask: per-32-row-block column sums [G][ceil(M/32)][N]
     int* flags = nullptr;
 };
 void launch_umma(const UmmaGemm& u, cudaStream_t s);
@@ -197,6 +198,7 @@ struct HeadDx {
     long long c_gs = 0, ldc = 0;
     const float* mask = nullptr;  // same layout as C
     const float* add = nullptr;
+    float* colsum = nullptr;      // per-32-row-block column sums [G][ceil(rows/32)][K], or null
 };
 bool head_fwd_ok(int K, int N);
 bool head_dx_ok(int K, int N);
@@ -221,6 +223,9 @@ struct CeArgs {
 void launch_ce(const CeArgs& a, cudaStream_t s);
 
 // Column sums + SGD on a bias: db[g,n] = sum_{rows} dZ[g, r, n]; b -= lr*db
+// bias update from per-row-block column partials [G][nrb][N] (fixed order)
+void launch_bias_from_partials(int G, int nrb, int N, const float* partial, float* b, float lr,
+                               const AdamArgs& adam, float* grad_out, int* flags, cudaStream_t s);
 void launch_bias_sgd(int G, int rows, int N, const float* dZ, long long dz_gs, float* b,
                      long long b_gs, float lr, const AdamArgs& adam, float* grad_out, int* flags,
                      cudaStream_t s);

@@ -124,6 +124,7 @@ __global__ void __launch_bounds__(256) head_dx_kernel(HeadDx p) {
     __syncthreads();
     const float* W = p.W + g * p.w_gs;
     for (int q = threadIdx.x; q < p.K; q += blockDim.x) {
+        float csum = 0.f;  // column sum of this block's 32 rows (bias gradient partial)
         float w[NP];
 #pragma unroll
         for (int j = 0; j < NP; ++j) w[j] = j < N ? W[(long long)q * N + j] : 0.f;
@@ -149,9 +150,12 @@ __global__ void __launch_bounds__(256) head_dx_kernel(HeadDx p) {
                     acc = fmaf(z.w, w[4 * j4 + 3], acc);
                 }
                 if (p.add) acc = ad[i] + acc;
-                p.C[g * p.c_gs + (long long)(r0 + rb + i) * p.ldc + q] = (mk[i] > 0.f) ? acc : 0.f;
+                const float outv = (mk[i] > 0.f) ? acc : 0.f;
+                p.C[g * p.c_gs + (long long)(r0 + rb + i) * p.ldc + q] = outv;
+                csum += outv;
             }
         }
+        if (p.colsum) p.colsum[((long long)g * gridDim.x + blockIdx.x) * p.K + q] = csum;
     }
 }
 

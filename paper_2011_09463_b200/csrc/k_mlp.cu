@@ -258,6 +258,29 @@ void launch_adam_apply(float* W, const float* grad, long long n, float lr, const
     count_launch();
 }
 
+namespace {
+__global__ void bias_from_partials_kernel(int G, int nrb, int N, const float* partial, float* b,
+                                          float lr, AdamArgs adam, float* grad_out, int* flags) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= G * N) return;
+    const int g = t / N, n = t % N;
+    float s = 0.f;
+    for (int rb = 0; rb < nrb; ++rb) s += partial[((long long)g * nrb + rb) * N + n];
+    if (grad_out) grad_out[t] = s;
+    const float v = param_update(b[t], s, lr, adam, t);
+    if (!isfinite(v)) atomicOr(flags, kFlagNonFinite);
+    b[t] = v;
+}
+}  // namespace
+
+void launch_bias_from_partials(int G, int nrb, int N, const float* partial, float* b, float lr,
+                               const AdamArgs& adam, float* grad_out, int* flags, cudaStream_t s) {
+    const int n = G * N;
+    bias_from_partials_kernel<<<(n + 255) / 256, 256, 0, s>>>(G, nrb, N, partial, b, lr, adam, grad_out,
+                                                               flags);
+    count_launch();
+}
+
 void launch_bias_sgd(int G, int rows, int N, const float* dZ, long long dz_gs, float* b,
                      long long b_gs, float lr, const AdamArgs& adam, float* grad_out, int* flags,
                      cudaStream_t s) {

@@ -71,6 +71,7 @@ struct UmmaParams {
     const float* mask;
     float lr;
     float* grad_out;
+    float* colsum;     // kMask: per-32-row-block column sums of C, [G][ceil(M/32)][N], or null
     int* flags;
     unsigned long long* trace;  // diagnostics: timestamps of CTA (0,0,0)
 };
@@ -188,6 +189,7 @@ __device__ __forceinline__ void epilogue_tile(const UmmaParams& p, uint32_t tmem
             sts128(sb + (uint32_t)((lane * EPI_LD + 4 * j) * 4),
                    make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
         __syncwarp();
+        float4 cs = make_float4(0.f, 0.f, 0.f, 0.f);  // this thread's rows of 4 columns
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             const int r = r0 + 4 * i, m = mw + r;
@@ -206,6 +208,10 @@ __device__ __forceinline__ void epilogue_tile(const UmmaParams& p, uint32_t tmem
                     } else if (epi == (int)Epi::kMask) {
                         if (p.add) y = p.add[ie] + y;
                         y = (p.mask[ie] > 0.f) ? y : 0.f;
+                        if (e == 0) cs.x += y;
+                        else if (e == 1) cs.y += y;
+                        else if (e == 2) cs.z += y;
+                        else cs.w += y;
                     } else if (epi == (int)Epi::kSgd) {
                         if (p.grad_out) p.grad_out[ie] = y;
                         y = p.C[ie] - p.lr * y;
@@ -238,6 +244,10 @@ __device__ __forceinline__ void epilogue_tile(const UmmaParams& p, uint32_t tmem
                 x.y = o1[i].y > 0.f ? x.y : 0.f;
                 x.z = o1[i].z > 0.f ? x.z : 0.f;
                 x.w = o1[i].w > 0.f ? x.w : 0.f;
+                cs.x += x.x;
+                cs.y += x.y;
+                cs.z += x.z;
+                cs.w += x.w;
             } else if (epi == (int)Epi::kSgd) {  // C is the fp32 master weight
                 if (p.grad_out) *reinterpret_cast<float4*>(p.grad_out + idx) = x;
                 x.x = o1[i].x - p.lr * x.x;
@@ -247,6 +257,21 @@ __device__ __forceinline__ void epilogue_tile(const UmmaParams& p, uint32_t tmem
                 bad |= !(isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w));
             }
             *reinterpret_cast<float4*>(p.C + idx) = x;
+        }
+        if (p.colsum) {  // fixed-order reduction of the warp's 32 rows (lanes differ in r0)
+#pragma unroll
+            for (int o = 8; o <= 16; o <<= 1) {
+                cs.x += __shfl_xor_sync(0xffffffffu, cs.x, o);
+                cs.y += __shfl_xor_sync(0xffffffffu, cs.y, o);
+                cs.z += __shfl_xor_sync(0xffffffffu, cs.z, o);
+                cs.w += __shfl_xor_sync(0xffffffffu, cs.w, o);
+            }
+            if (r0 == 0 && mw < p.M) {
+                const int nrb = (p.M + 31) / 32;
+                float* o = p.colsum + ((long long)g * nrb + mw / 32) * p.N + n;
+                const float cv[4] = {cs.x, cs.y, cs.z, cs.w};
+                for (int e = 0; e < 4 && n + e < p.N; ++e) o[e] = cv[e];
+            }
         }
         __syncwarp();
     }
@@ -590,6 +615,7 @@ void launch_umma(const UmmaGemm& u, cudaStream_t s) {
     p.mask = u.mask;
     p.lr = u.lr;
     p.grad_out = u.grad_out;
+    p.colsum = u.colsum;
     p.flags = u.flags;
     if (const char* t = getenv("MTK_UMMA_TRACE"))
         p.trace = reinterpret_cast<unsigned long long*>(strtoull(t, nullptr, 0));
