@@ -88,6 +88,7 @@ struct mtk_bank {
     double* beta = nullptr;
     float* gH = nullptr;
     float* colsum = nullptr;  // [G][ceil(B/32)][max dim] bias-gradient partials from the DX epilogues
+    double* loss_part = nullptr;  // [G][ceil(B/32)] CE loss partials
     double* mmd_part = nullptr;
     size_t mmd_part_bytes = 0;
     float* head_scratch = nullptr;  // skinny dW partial sums
@@ -223,6 +224,8 @@ struct mtk_bank {
         cudaFree(gH);
         cudaFree(colsum);
         colsum = nullptr;
+        cudaFree(loss_part);
+        loss_part = nullptr;
         logits = nullptr;
         gH = nullptr;
         row_loss = nullptr;
@@ -239,6 +242,7 @@ struct mtk_bank {
         MTK_CUDA(cudaMalloc(&row_loss, GB * sizeof(double)));
         if (L > 1) MTK_CUDA(cudaMalloc(&gH, GB * dims[L - 1] * sizeof(float)));
         MTK_CUDA(cudaMalloc(&colsum, (size_t)G * ((B + 31) / 32) * maxd() * sizeof(float)));
+        MTK_CUDA(cudaMalloc(&loss_part, (size_t)G * ((B + 31) / 32) * sizeof(double)));
         capB = B;
     }
     void ensure_stage(int B) {
@@ -602,7 +606,10 @@ void train_step(mtk_bank& k, const mtk_step& s, double* loss_host, double* mmd_h
     Plane3* nxt = &k.dZ[1];
     CeArgs ce{k.G,      B,          k.dims[L], two ? src : B, k.logits, s.y, s.w,
               (float)(1.0 / d0), (float)(1.0 / (two ? d1 : d0)), cur->f, k.row_loss, k.loss,
-              c.d_flags};
+              c.d_flags, k.loss_part};
+    // the head's bias gradient comes out of the CE kernel as column partials
+    static const bool no_colsum = getenv("MTK_NO_COLSUM") != nullptr;  // A/B diagnostics
+    ce.colsum = (!two && L - 1 >= s.frozen_layers && !no_colsum) ? k.colsum : nullptr;
     {
         PhaseScope ph(c, kPhCe, 2);
         launch_ce(ce, c.stream);
@@ -675,7 +682,7 @@ void train_step(mtk_bank& k, const mtk_step& s, double* loss_host, double* mmd_h
     // backward sweep, layer L-1 down to 0.  A DX launch also reduces its
     // output's columns per 32-row block when the layer below is trainable,
     // so that layer's bias update needs no second pass over dZ.
-    bool colsum_ready = false;
+    bool colsum_ready = ce.colsum != nullptr;
     for (int l = L - 1; l >= 0; --l) {
         const bool trainable = l >= s.frozen_layers;
         const bool need_dx = l > 0 && l > s.frozen_layers;
@@ -710,7 +717,6 @@ void train_step(mtk_bank& k, const mtk_step& s, double* loss_host, double* mmd_h
                 gemm_dx(k, l + 1, *cur, B, src, B - src, out, k.H[l].f, nullptr);
                 after_launch(c, 2);
             } else {
-                static const bool no_colsum = getenv("MTK_NO_COLSUM") != nullptr;  // A/B diagnostics
                 const bool below_trainable = l - 1 >= s.frozen_layers && !no_colsum;
                 const bool have = gemm_dx(k, l, *cur, B, 0, B, out, k.H[l].f, add,
                                           below_trainable ? k.colsum : nullptr);

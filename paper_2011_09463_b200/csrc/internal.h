@@ -219,6 +219,8 @@ struct CeArgs {
     double* row_loss;       // [G,B]  w_i (lse - x_y) / denom_head
     double* loss;           // [G]
     int* flags;
+    double* loss_part;      // [G][ceil(B/32)] scratch
+    float* colsum = nullptr;  // optional [G][ceil(B/32)][C] dlogits column partials
 };
 void launch_ce(const CeArgs& a, cudaStream_t s);
 

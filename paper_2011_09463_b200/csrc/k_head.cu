@@ -63,9 +63,19 @@ __global__ void __launch_bounds__(128) head_fwd_kernel(HeadFwd p) {
                 sA[rr][kk] = (r0 + rr < p.rows && kk < kc) ? A[(long long)(r0 + rr) * p.lda + k0 + kk] : 0.f;
             }
         }
-        for (int e = t; e < FK * NP; e += 128) {
-            const int kk = e / NP, n = e % NP;
-            sW[kk][n] = (kk < kc && n < N) ? W[(long long)(k0 + kk) * N + n] : 0.f;
+        {
+            constexpr int PER = (FK * NP + 127) / 128;
+            float wv[PER];  // loads in flight together, then the smem stores
+#pragma unroll
+            for (int i = 0; i < PER; ++i) {
+                const int e = t + 128 * i, kk = e / NP, n = e % NP;
+                wv[i] = (e < FK * NP && kk < kc && n < N) ? __ldg(W + (long long)(k0 + kk) * N + n) : 0.f;
+            }
+#pragma unroll
+            for (int i = 0; i < PER; ++i) {
+                const int e = t + 128 * i;
+                if (e < FK * NP) sW[e / NP][e % NP] = wv[i];
+            }
         }
         __syncthreads();
 #pragma unroll 4
@@ -117,9 +127,20 @@ __global__ void __launch_bounds__(256) head_dx_kernel(HeadDx p) {
     const int g = blockIdx.y;
     const int r0 = blockIdx.x * 32;
     const int nrows = min(32, p.rows - r0);
-    for (int e = threadIdx.x; e < 32 * NP; e += blockDim.x) {
-        const int rr = e / NP, j = e % NP;
-        sdz[rr][j] = (rr < nrows && j < N) ? p.dZ[g * p.dz_gs + (long long)(r0 + rr) * p.lddz + j] : 0.f;
+    {
+        constexpr int PER = (32 * NP + 255) / 256;
+        float zv[PER];
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int e = threadIdx.x + 256 * i, rr = e / NP, j = e % NP;
+            zv[i] = (e < 32 * NP && rr < nrows && j < N)
+                        ? __ldg(p.dZ + g * p.dz_gs + (long long)(r0 + rr) * p.lddz + j) : 0.f;
+        }
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int e = threadIdx.x + 256 * i;
+            if (e < 32 * NP) sdz[e / NP][e % NP] = zv[i];
+        }
     }
     __syncthreads();
     const float* W = p.W + g * p.w_gs;
@@ -179,9 +200,19 @@ __global__ void __launch_bounds__(256) head_dw_partial_kernel(HeadDw p) {
     const float* dz = p.dZ + g * p.dz_gs;
     for (int r0 = rbeg; r0 < rend; r0 += 64) {
         __syncthreads();
-        for (int i = threadIdx.x; i < 64 * NP; i += blockDim.x) {
-            const int rr = i / NP, n = i % NP;
-            sdz[rr][n] = (r0 + rr < rend && n < N) ? dz[(long long)(r0 + rr) * p.lddz + n] : 0.f;
+        {
+            constexpr int PER = (64 * NP + 255) / 256;
+            float zv[PER];
+#pragma unroll
+            for (int i = 0; i < PER; ++i) {
+                const int e = threadIdx.x + 256 * i, rr = e / NP, n = e % NP;
+                zv[i] = (e < 64 * NP && r0 + rr < rend && n < N) ? __ldg(dz + (long long)(r0 + rr) * p.lddz + n) : 0.f;
+            }
+#pragma unroll
+            for (int i = 0; i < PER; ++i) {
+                const int e = threadIdx.x + 256 * i;
+                if (e < 64 * NP) sdz[e / NP][e % NP] = zv[i];
+            }
         }
         __syncthreads();
         if (pp < p.K) {

@@ -133,50 +133,67 @@ __global__ void __launch_bounds__(NT) gemm_simt_kernel(Gemm p) {
 }
 
 // One thread per row: softmax-CE forward + d(logits) (tape.hpp:475-520).
-__global__ void ce_kernel(CeArgs a) {
-    const long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    const long long rows = (long long)a.G * a.B;
-    if (r >= rows) return;
-    const int i = (int)(r % a.B);
-    const float* x = a.logits + r * a.C;
-    float* dx = a.dlogits + r * a.C;
-    const int lab = a.y[r];
-    if (lab < 0 || lab >= a.C) {
-        atomicOr(a.flags, kFlagBadLabel);
-        for (int j = 0; j < a.C; ++j) dx[j] = 0.f;
-        a.row_loss[r] = 0.0;
-        return;
+// Softmax-CE over one model's rows (tape.hpp:475-520): block = 256 rows of
+// model blockIdx.y, one thread per row; dlogits = w_i/denom (P - onehot).
+// Per warp (32 rows) it also reduces, in a fixed butterfly order, the row
+// losses (fp64) into loss_part[g][blk32] and -- with colsum set -- the dlogits
+// columns into colsum[g][blk32][C] (the head's bias gradient partials).
+__global__ void __launch_bounds__(256) ce_kernel(CeArgs a) {
+    const int g = blockIdx.y;
+    const int i = blockIdx.x * 256 + threadIdx.x;  // row within the model
+    const int lane = threadIdx.x & 31;
+    const int blk = i >> 5;                        // 32-row block
+    const int nblk = (a.B + 31) / 32;
+    const bool active = i < a.B;
+    const long long r = (long long)g * a.B + i;
+    double rl = 0.0;
+    float dx[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) dx[j] = 0.f;
+    if (active) {
+        const float* x = a.logits + r * a.C;
+        const int lab = a.y[r];
+        if (lab < 0 || lab >= a.C) {
+            atomicOr(a.flags, kFlagBadLabel);
+        } else {
+            float mx = x[0];
+            for (int j = 1; j < a.C; ++j) mx = fmaxf(mx, x[j]);
+            float z = 0.f;
+            for (int j = 0; j < a.C; ++j) z += expf(x[j] - mx);
+            const float lse = mx + logf(z);
+            const float inv = (i < a.src_rows) ? a.inv_denom0 : a.inv_denom1;
+            const float wi = (a.w ? a.w[r] : 1.f) * inv;
+            rl = (double)wi * ((double)lse - (double)x[lab]);
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if (j < a.C) dx[j] = wi * (expf(x[j] - lse) - (j == lab ? 1.f : 0.f));
+        }
+        float* d = a.dlogits + r * a.C;
+        for (int j = 0; j < a.C; ++j) d[j] = dx[j];
+        a.row_loss[r] = rl;
     }
-    float mx = x[0];
-    for (int j = 1; j < a.C; ++j) mx = fmaxf(mx, x[j]);
-    float z = 0.f;
-    for (int j = 0; j < a.C; ++j) z += expf(x[j] - mx);
-    const float lse = mx + logf(z);
-    const float inv = (i < a.src_rows) ? a.inv_denom0 : a.inv_denom1;
-    const float wi = (a.w ? a.w[r] : 1.f) * inv;
-    a.row_loss[r] = (double)wi * ((double)lse - (double)x[lab]);
-    for (int j = 0; j < a.C; ++j) {
-        const float pj = expf(x[j] - lse);
-        dx[j] = wi * (pj - (j == lab ? 1.f : 0.f));
+    // warp partials (inactive rows contribute zeros)
+    for (int o = 16; o > 0; o >>= 1) rl += __shfl_xor_sync(0xffffffffu, rl, o);
+    if (lane == 0 && blk < nblk) a.loss_part[(long long)g * nblk + blk] = rl;
+    if (a.colsum) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            if (j >= a.C) break;
+            float v = dx[j];
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0 && blk < nblk) a.colsum[((long long)g * nblk + blk) * a.C + j] = v;
+        }
     }
 }
 
-// Fixed-order per-model fp64 sum of the per-row losses.
-__global__ void row_sum_kernel(const double* row_loss, int B, double* loss, int* flags) {
-    __shared__ double red[256];
-    const int g = blockIdx.x;
+// loss[g] = sum of the 32-row partials in order
+__global__ void ce_loss_kernel(const double* loss_part, int G, int nblk, double* loss, int* flags) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= G) return;
     double s = 0.0;
-    for (int i = threadIdx.x; i < B; i += blockDim.x) s += row_loss[(long long)g * B + i];
-    red[threadIdx.x] = s;
-    __syncthreads();
-    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        loss[g] = red[0];
-        if (!isfinite(red[0])) atomicOr(flags, kFlagNonFinite);
-    }
+    for (int b = 0; b < nblk; ++b) s += loss_part[(long long)g * nblk + b];
+    loss[g] = s;
+    if (!isfinite(s)) atomicOr(flags, kFlagNonFinite);
 }
 
 // db = column sums of dZ, b -= lr * db.  Block = 32 columns x 32 row groups;
@@ -228,10 +245,10 @@ void launch_gemm(const Gemm& p, cudaStream_t s) {
 }
 
 void launch_ce(const CeArgs& a, cudaStream_t s) {
-    const long long rows = (long long)a.G * a.B;
-    ce_kernel<<<(unsigned)((rows + 127) / 128), 128, 0, s>>>(a);
+    if (a.C > 32) fail(MTK_SHAPE_ERROR, "cross_entropy: more than 32 classes");
+    ce_kernel<<<dim3((a.B + 255) / 256, a.G), 256, 0, s>>>(a);
     count_launch();
-    row_sum_kernel<<<a.G, 256, 0, s>>>(a.row_loss, a.B, a.loss, a.flags);
+    ce_loss_kernel<<<(a.G + 127) / 128, 128, 0, s>>>(a.loss_part, a.G, (a.B + 31) / 32, a.loss, a.flags);
     count_launch();
 }
 
