@@ -9,6 +9,8 @@ own 32 shadows; no data-path collective (models are independent, SURVEY.md
 section 8(e)).  One step = one SGD step of all 32 models.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+  python bench.py --workload c4      # MMD stress (configs[3]): kernel pairs/s, row-sharded
+  python bench.py --workload attack  # attack stage over 2^20 queries (configs[4] share)
 
 Prints ONE JSON line on rank 0 (contract in the task description).
 """
@@ -224,6 +226,147 @@ def kernel_traffic(phase):
     return (ent.get("dram_bytes_per_step") if ent else None), os.path.basename(files[-1])
 
 
+# ----------------------------------------------------------------------------- C4 MMD
+C4_M, C4_N, C4_D = 65536, 8192, 512
+C4_PAIRS = C4_M * (C4_M - 1) // 2 + C4_N * (C4_N - 1) // 2 + C4_M * C4_N  # 2,717,872,128
+
+
+def run_c4_arm(args, world, rank, local):
+    """configs[3]: multi-bandwidth MMD^2 + gradient of Xs [65536, 512] vs Xt
+    [8192, 512].  One step = the full evaluation, pair rows sharded over the
+    ranks (strong scaling); the ranks' raw sums would be combined in ascending
+    rank order (section 8(e))."""
+    import torch
+
+    from paper_2011_09463_b200 import api
+
+    torch.cuda.set_device(local)
+    ctx = api.Context(local)
+    gen = torch.Generator(device="cuda").manual_seed(4)
+    Xs = torch.randn(C4_M, C4_D, device="cuda", generator=gen)
+    Xt = torch.randn(C4_N, C4_D, device="cuda", generator=gen) + 0.1
+    gXs, gXt = torch.empty_like(Xs), torch.empty_like(Xt)
+    beta = api.mmd_beta(ctx, Xs, Xt)
+    Nt = C4_M + C4_N
+    r0, r1 = rank * Nt // world, (rank + 1) * Nt // world
+    for _ in range(max(args.warmup, 1)):
+        api.mmd_gaussian_rows(ctx, Xs, Xt, beta, r0, r1, gXs=gXs, gXt=gXt)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = ctx.launches
+    with ClockSampler(local) as clk:
+        barrier(world)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            api.mmd_gaussian_rows(ctx, Xs, Xt, beta, r0, r1, gXs=gXs, gXt=gXt)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1), world)
+    launches = ctx.launches - launches0
+    if rank != 0:
+        return
+    bf16, _, _, src = peaks()
+    fp32acc_peak = bf16 / 2.0 / 3.0
+    pairs_s = C4_PAIRS * args.steps / (ms / 1000.0)
+    achieved = pairs_s * 4 * C4_D / 1e12
+    line = {
+        "metric": "MMD kernel-pairs/s", "value": pairs_s, "unit": "pairs/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": "C4 MMD stress: Xs 65536 x 512 vs Xt 8192 x 512 (N(0,1), N(0.1,1)), "
+                               "5-bandwidth Gaussian MMD^2 + gradient, pair rows sharded over ranks",
+                   "unique_pairs": C4_PAIRS, "parallelism": f"rows{world}",
+                   "l2": "inputs 151 MB + tf32 planes > 126 MB L2"},
+        "roofline": {"bound": "tensor", "kernel": "mmd_tc_kernel (+prep, grad finish)",
+                     "achieved": achieved, "peak": fp32acc_peak, "unit": "TFLOP/s",
+                     "frac": achieved / fp32acc_peak, "traffic": None,
+                     "peak_note": f"algorithmic 4d flop per unique pair; 3xTF32 peak = {src} bf16 / 6; "
+                                  "the kernel evaluates ordered pairs (2x the algorithmic work)"},
+        "cpu_baseline": None,
+        "e2e": None,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- attack
+ATT_Q = 1 << 20
+
+
+def run_attack_arm(args, world, rank, local):
+    """Attack stage of configs[4] on one paradigm's 2^20 member/non-member
+    queries per rank: posterior top-3 features -> attack MLP 3-64-2 -> member
+    score -> AUC + accuracy.  Reports queries/s and the streaming kernels'
+    achieved HBM bandwidth on algorithmic bytes."""
+    import torch
+
+    from paper_2011_09463_b200 import api
+
+    torch.cuda.set_device(local)
+    ctx = api.Context(local)
+    gen = torch.Generator(device="cuda").manual_seed(5 + rank)
+    logits = torch.randn(ATT_Q, 10, device="cuda", generator=gen)
+    labels = (torch.rand(ATT_Q, device="cuda", generator=gen) < 0.5).to(torch.uint8)
+    logits[labels.bool(), 0] += 1.0  # members look more confident
+    att = api.Bank(ctx, 1, [3, 64, 2])
+    rng = api.Rng(77)
+    att.init_params(0, rng)
+
+    def step():
+        F = api.posterior_features(ctx, logits, 3)
+        out = att.forward(F.reshape(1, ATT_Q, 3))
+        score = api.posterior_column(ctx, out, 1)
+        return api.auc(ctx, score, labels)
+
+    for _ in range(max(args.warmup, 1)):
+        step()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = ctx.launches
+    with ClockSampler(local) as clk:
+        barrier(world)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            auc, acc = step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1), world)
+    launches = ctx.launches - launches0
+    if rank != 0:
+        return
+    _, _, hbm, src = peaks()
+    # algorithmic bytes per query: logits 40 + features 12 (w) + 12 (r) + out 8 (w) + 8 (r)
+    # + score 4 (w) + AUC: score 4 + label 1 read, sorted pairs (4+4) written/read twice
+    bytes_q = 40 + 12 + 12 + 8 + 8 + 4 + 5 + 2 * 2 * 8
+    qps = world * ATT_Q * args.steps / (ms / 1000.0)
+    gbs = qps * bytes_q / world / 1e9
+    line = {
+        "metric": "membership-attack queries/s", "value": qps, "unit": "queries/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "attack stage: 2^20 queries x 10-class posteriors -> top-3 "
+                               "features -> attack MLP 3-64-2 -> score -> AUC/accuracy per rank",
+                   "queries_per_gpu": ATT_Q, "parallelism": f"shard{world}", "auc": auc,
+                   "accuracy": acc},
+        "roofline": {"bound": "hbm", "kernel": "features + attack forward + AUC (whole stage)",
+                     "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm if hbm else None,
+                     "traffic": None,
+                     "peak_note": f"{src} HBM copy bandwidth; {bytes_q} algorithmic B/query"},
+        "cpu_baseline": None,
+        "e2e": None,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
 # ----------------------------------------------------------------------------- GPU arm
 def run_gpu_arm(args, world, rank, local):
     import numpy as np
@@ -372,6 +515,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="c2", choices=["c2", "c4", "attack"],
+                    help="c2 (default, the headline), c4 MMD stress, attack stage")
     args = ap.parse_args()
     if args.impl == "reference":
         world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -380,7 +525,8 @@ def main():
         return
     world, rank, local = dist_setup(args.gpus)
     try:
-        run_gpu_arm(args, world, rank, local)
+        {"c2": run_gpu_arm, "c4": run_c4_arm, "attack": run_attack_arm}[args.workload](
+            args, world, rank, local)
     finally:
         if world > 1:
             import torch.distributed as dist

@@ -904,8 +904,16 @@ int mtk_bank_forward(mtk_bank* k, const float* X, int B, int head, float* logits
         need(X && logits, MTK_VALUE_ERROR, "forward: null argument");
         need(B >= 1, MTK_SHAPE_ERROR, "forward: B must be >= 1");
         need(head >= 0 && head < k->n_heads, MTK_VALUE_ERROR, "forward: bad head index");
-        k->ensure(B);
         Ctx& c = *k->ctx;
+        if (k->L == 2 && k->n_heads == 1 && !hidden_last &&
+            small2_forward_ok(k->dims[0], k->dims[1], k->dims[2])) {
+            // attack-model shape: one fused kernel, hidden layer kept in registers
+            launch_small2_forward(X, k->G, B, k->dims[0], k->dims[1], k->dims[2], k->W[0].f, k->b[0],
+                                  k->W[1].f, k->b[1], logits, c.stream);
+            after_launch(c);
+            return;
+        }
+        k->ensure(B);
         const Plane3 in = input_plane(*k, X, B);
         run_forward(*k, in, B, head, 0);
         const size_t GB = (size_t)k->G * B;

@@ -35,6 +35,16 @@ double* Ctx::scratch(size_t bytes) {
     return d_scratch;
 }
 
+void* Ctx::big(size_t bytes) {
+    if (bytes > big_bytes) {
+        if (d_big) MTK_CUDA(cudaFree(d_big));  // synchronizes: in-flight users are done
+        d_big = nullptr;
+        MTK_CUDA(cudaMalloc(&d_big, bytes));
+        big_bytes = bytes;
+    }
+    return d_big;
+}
+
 void* Ctx::pinned_buf(size_t bytes) {
     if (bytes > pinned_bytes) {
         if (pinned) MTK_CUDA(cudaFreeHost(pinned));
@@ -134,6 +144,7 @@ int mtk_ctx_destroy(mtk_ctx* c) {
         cudaStreamSynchronize(c->stream);
         cudaFree(c->d_flags);
         cudaFree(c->d_scratch);
+        cudaFree(c->d_big);
         if (c->pinned) cudaFreeHost(c->pinned);
         if (c->pinned_flags) cudaFreeHost(c->pinned_flags);
         if (c->own_stream) cudaStreamDestroy(c->stream);
@@ -243,10 +254,8 @@ static void mmd_run(mtk_ctx* c, MmdArgs& a, double beta, bool want_value, double
     a.beta = beta_d;
     a.partial = part_d;
     if (a.tc) {
-        void* zs = nullptr;
-        MTK_CUDA(cudaMallocAsync(&zs, mmd_tc_scratch_bytes(a), c->stream));
+        void* zs = c->big(mmd_tc_scratch_bytes(a));
         launch_mmd_tc(a, zs, c->stream);
-        MTK_CUDA(cudaFreeAsync(zs, c->stream));
         after_launch(*c, 1);
     } else {
         launch_mmd_pairs(a, c->stream);

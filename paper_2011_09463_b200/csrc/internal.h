@@ -52,6 +52,11 @@ struct Ctx {
     int* pinned_flags = nullptr;     // dedicated host word for check_flags()
     size_t pinned_bytes = 0;
     double* scratch(size_t bytes);
+    // grow-only device workspace for the large per-call buffers (AUC sort,
+    // MMD planes / partial slots); stream-ordered reuse, no per-call malloc
+    void* big(size_t bytes);
+    void* d_big = nullptr;
+    size_t big_bytes = 0;
     void* pinned_buf(size_t bytes);
     void check_flags();               // synchronizes; throws on a set flag
 };
@@ -201,6 +206,11 @@ struct HeadDx {
     float* colsum = nullptr;      // per-32-row-block column sums [G][ceil(rows/32)][K], or null
 };
 bool head_fwd_ok(int K, int N);
+// forward-only 2-layer MLP K -> H -> O with K <= 8, O <= 4 (the attack model)
+bool small2_forward_ok(int K, int H, int O);
+void launch_small2_forward(const float* X, int G, int rows, int K, int H, int O, const float* W0,
+                           const float* b0, const float* W1, const float* b1, float* logits,
+                           cudaStream_t s);
 bool head_dx_ok(int K, int N);
 void launch_head_dx(const HeadDx& p, cudaStream_t s);
 size_t head_dw_scratch_bytes(int G, int K, int N);

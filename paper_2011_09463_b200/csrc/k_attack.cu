@@ -33,6 +33,60 @@ __global__ void softmax_kernel(const float* logits, long long rows, int C, float
     for (int j = 0; j < C; ++j) p[j] *= inv;
 }
 
+// C <= 16 (the 10-class posteriors): everything in registers, top-k by
+// unrolled insertion into a descending register list (values only, so tie
+// order does not matter).
+template <int CC>
+__global__ void features_small_kernel(const float* logits, long long rows, int C, int k,
+                                      const int32_t* labels, float* feats, int* flags) {
+    const long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (r >= rows) return;
+    const float* x = logits + r * C;
+    float v[CC];
+#pragma unroll
+    for (int j = 0; j < CC; ++j) v[j] = j < C ? __ldg(x + j) : -INFINITY;
+    float mx = v[0];
+#pragma unroll
+    for (int j = 1; j < CC; ++j) mx = fmaxf(mx, v[j]);
+    float z = 0.f;
+#pragma unroll
+    for (int j = 0; j < CC; ++j) {
+        v[j] = j < C ? expf(v[j] - mx) : 0.f;
+        z += v[j];
+    }
+    const float inv = 1.f / z;
+    constexpr int KM = 8;
+    float top[KM];
+#pragma unroll
+    for (int a = 0; a < KM; ++a) top[a] = -1.f;
+#pragma unroll
+    for (int j = 0; j < CC; ++j) {
+        if (j >= C) break;
+        float t = v[j] * inv;
+#pragma unroll
+        for (int a = 0; a < KM; ++a) {  // insert t, keep descending
+            if (a >= k) break;
+            const float hi = fmaxf(top[a], t), lo = fminf(top[a], t);
+            top[a] = hi;
+            t = lo;
+        }
+    }
+    const int nf = k + (labels ? 1 : 0);
+    float* out = feats + r * nf;
+#pragma unroll
+    for (int a = 0; a < KM; ++a)
+        if (a < k) out[a] = top[a];
+    if (labels) {
+        const int lab = labels[r];
+        if (lab < 0 || lab >= C) {
+            atomicOr(flags, kFlagBadLabel);
+            out[k] = 0.f;
+        } else {
+            out[k] = mx + logf(z) - x[lab];
+        }
+    }
+}
+
 __global__ void features_kernel(const float* logits, long long rows, int C, int k,
                                 const int32_t* labels, float* feats, int* flags) {
     const long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -98,14 +152,25 @@ __global__ void auc_keys_kernel(const float* s, const uint8_t* lab, long long n,
         pos = l;
         hit = ((s[i] > 0.5f) == (l != 0));
     }
-    // warp-aggregated integer atomics: exact and order-independent
+    // block-aggregated integer atomics: exact and order-independent
+    __shared__ unsigned long long sp[8], sh[8];
     for (int o = 16; o > 0; o >>= 1) {
         pos += __shfl_down_sync(0xffffffffu, pos, o);
         hit += __shfl_down_sync(0xffffffffu, hit, o);
     }
     if ((threadIdx.x & 31) == 0) {
-        atomicAdd(&counts[0], pos);
-        atomicAdd(&counts[1], hit);
+        sp[threadIdx.x >> 5] = pos;
+        sh[threadIdx.x >> 5] = hit;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long a = 0, b = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            a += sp[w];
+            b += sh[w];
+        }
+        if (a) atomicAdd(&counts[0], a);
+        if (b) atomicAdd(&counts[1], b);
     }
 }
 
@@ -133,8 +198,15 @@ __global__ void auc_rank_sum(const uint8_t* v, const int* gid1, long long n, con
         const int g = gid1[i] - 1;
         t = (unsigned long long)(gstart[g] + 1 + gend[g]);
     }
+    __shared__ unsigned long long st[8];
     for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
-    if ((threadIdx.x & 31) == 0 && t) atomicAdd(acc, t);
+    if ((threadIdx.x & 31) == 0) st[threadIdx.x >> 5] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long a = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) a += st[w];
+        if (a) atomicAdd(acc, a);
+    }
 }
 
 inline unsigned nblocks(long long n, int t) { return (unsigned)((n + t - 1) / t); }
@@ -151,7 +223,11 @@ void launch_features(const float* logits, long long rows, int C, int k, const in
                      float* feats, int* flags, cudaStream_t s) {
     if (C > MAXC) fail(MTK_SHAPE_ERROR, "posterior_features: more than 64 classes");
     if (rows <= 0) return;
-    features_kernel<<<nblocks(rows, 256), 256, 0, s>>>(logits, rows, C, k, labels, feats, flags);
+    if (C <= 16 && k <= 8)
+        features_small_kernel<16><<<nblocks(rows, 256), 256, 0, s>>>(logits, rows, C, k, labels, feats,
+                                                                      flags);
+    else
+        features_kernel<<<nblocks(rows, 256), 256, 0, s>>>(logits, rows, C, k, labels, feats, flags);
     count_launch();
 }
 
@@ -175,8 +251,7 @@ void auc_device(Ctx& ctx, const float* scores, const uint8_t* labels, long long 
     const size_t tmp = std::max(sort_bytes, scan_bytes);
     auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
     const size_t bytes = al(4 * n) * 2 + al(n) * 2 + al(4 * n) * 2 + al(8 * n) * 2 + al(64) + al(tmp);
-    char* base = nullptr;
-    MTK_CUDA(cudaMallocAsync(&base, bytes, s));
+    char* base = static_cast<char*>(ctx.big(bytes));
     char* p = base;
     auto take = [&](size_t b) { char* r = p; p += al(b); return r; };
     uint32_t* k_in = (uint32_t*)take(4 * n);
@@ -202,7 +277,6 @@ void auc_device(Ctx& ctx, const float* scores, const uint8_t* labels, long long 
     count_launch();
     unsigned long long h[3];
     MTK_CUDA(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, s));
-    MTK_CUDA(cudaFreeAsync(base, s));
     MTK_CUDA(cudaStreamSynchronize(s));
     const double npos = (double)h[0], nneg = (double)n - npos;
     if (h[0] == 0 || npos == (double)n)

@@ -268,6 +268,70 @@ __global__ void head_dw_finish_kernel(HeadDw p) {
     }
 }
 
+// Forward-only 2-layer MLP with a tiny input and output (the attack model
+// k -> H -> 2): one thread per row, all weights of model g in smem, the
+// hidden layer streamed through registers (never written to HBM).
+// Same sums as the layered path: (x W0) + b0 -> ReLU -> (h W1) + b1.
+constexpr int S2_K = 8, S2_O = 4, S2_R = 4;  // rows per thread: each smem weight read serves 4 rows
+__global__ void __launch_bounds__(256) small2_forward_kernel(const float* X, int rows, int K, int H,
+                                                             int O, const float* W0, const float* b0,
+                                                             const float* W1, const float* b1,
+                                                             float* logits) {
+    extern __shared__ float sw[];
+    const int g = blockIdx.y;
+    float* w0 = sw;                      // [K][H]
+    float* c0 = w0 + K * H;              // [H]
+    float* w1 = c0 + H;                  // [H][O]
+    float* c1 = w1 + H * O;              // [O]
+    for (int e = threadIdx.x; e < K * H; e += blockDim.x) w0[e] = W0[(long long)g * K * H + e];
+    for (int e = threadIdx.x; e < H; e += blockDim.x) c0[e] = b0[(long long)g * H + e];
+    for (int e = threadIdx.x; e < H * O; e += blockDim.x) w1[e] = W1[(long long)g * H * O + e];
+    for (int e = threadIdx.x; e < O; e += blockDim.x) c1[e] = b1[(long long)g * O + e];
+    __syncthreads();
+    // rows r0 + 256 i, i < S2_R: a warp still reads 32 consecutive rows
+    const int r0 = blockIdx.x * blockDim.x * S2_R + threadIdx.x;
+    float xv[S2_R][S2_K], out[S2_R][S2_O];
+#pragma unroll
+    for (int i = 0; i < S2_R; ++i) {
+        const int r = r0 + i * blockDim.x;
+        const float* x = X + ((long long)g * rows + r) * K;
+#pragma unroll
+        for (int k = 0; k < S2_K; ++k) xv[i][k] = (k < K && r < rows) ? __ldg(x + k) : 0.f;
+#pragma unroll
+        for (int o = 0; o < S2_O; ++o) out[i][o] = 0.f;
+    }
+#pragma unroll 2
+    for (int n = 0; n < H; ++n) {
+        float wk[S2_K], wo[S2_O];
+#pragma unroll
+        for (int k = 0; k < S2_K; ++k) wk[k] = k < K ? w0[k * H + n] : 0.f;
+#pragma unroll
+        for (int o = 0; o < S2_O; ++o) wo[o] = o < O ? w1[n * O + o] : 0.f;
+        const float bn = c0[n];
+#pragma unroll
+        for (int i = 0; i < S2_R; ++i) {
+            float acc = 0.f;
+#pragma unroll
+            for (int k = 0; k < S2_K; ++k)
+                if (k < K) acc = fmaf(xv[i][k], wk[k], acc);
+            float h = acc + bn;
+            h = h > 0.f ? h : 0.f;
+#pragma unroll
+            for (int o = 0; o < S2_O; ++o)
+                if (o < O) out[i][o] = fmaf(h, wo[o], out[i][o]);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < S2_R; ++i) {
+        const int r = r0 + i * blockDim.x;
+        if (r >= rows) break;
+        float* y = logits + ((long long)g * rows + r) * O;
+#pragma unroll
+        for (int o = 0; o < S2_O; ++o)
+            if (o < O) y[o] = out[i][o] + c1[o];
+    }
+}
+
 template <template <int> class Launch, typename P>
 void by_width(int N, const P& p, cudaStream_t s) {
     switch ((N + 3) / 4) {
@@ -317,6 +381,21 @@ void launch_head_fwd(const HeadFwd& p, cudaStream_t s) {
 void launch_head_dx(const HeadDx& p, cudaStream_t s) {
     if (p.rows <= 0) return;
     by_width<DxLaunch>(p.N, p, s);
+    count_launch();
+}
+
+bool small2_forward_ok(int K, int H, int O) {
+    return K >= 1 && K <= S2_K && O >= 1 && O <= S2_O && H >= 1 &&
+           (size_t)(K * H + H + H * O + O) * 4 <= 48 * 1024;
+}
+
+void launch_small2_forward(const float* X, int G, int rows, int K, int H, int O, const float* W0,
+                           const float* b0, const float* W1, const float* b1, float* logits,
+                           cudaStream_t s) {
+    if (rows <= 0) return;
+    const size_t smem = (size_t)(K * H + H + H * O + O) * 4;
+    small2_forward_kernel<<<dim3((rows + 256 * S2_R - 1) / (256 * S2_R), G), 256, smem, s>>>(
+        X, rows, K, H, O, W0, b0, W1, b1, logits);
     count_launch();
 }
 

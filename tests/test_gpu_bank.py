@@ -98,6 +98,20 @@ def test_forward_matches_oracle(ctx):
         assert rel(hid[g], H) <= TOL
 
 
+@pytest.mark.parametrize("dims", [[3, 64, 2], [4, 48, 2], [8, 200, 4]])
+def test_forward_attack_model_shape(ctx, dims):
+    """k -> H -> 2 forward (the attack model) runs as one fused kernel."""
+    G, B = 3, 1000
+    bank = make_bank(ctx, G, dims)
+    r = po.Rng(9)
+    X = r.normals(G * B * dims[0]).reshape(G, B, dims[0]).astype(np.float32)
+    logits = bank.forward(torch.tensor(X, device="cuda")).cpu().numpy()
+    for g in range(G):
+        W, b = bank.get_params(g)
+        lo, _ = po.mlp_forward(dims, W, b, X[g].astype(np.float64))
+        assert rel(logits[g], lo) <= TOL
+
+
 def test_step_c1_shape(ctx):
     """C1: 784-256-10, 1 target + 4 shadows, B=128."""
     dims = [784, 256, 10]
