@@ -61,7 +61,9 @@ constexpr int NUM_THREADS = 192 + 32 * NUM_CONV_WARPS;
 
 struct UmmaParams {
     CUtensorMap a, b;  // 3-D fp32 maps, coords (inner, outer, g)
+    CUtensorMap b64;   // K-major B with 64-row boxes (half tiles)
     int G, M, N, K;
+    int nfull, nhalf;  // work items: nfull full tiles, then nhalf half tiles (N / 2)
     int epi;           // Epi value
     float* C;
     long long c_gs, ldc;
@@ -86,13 +88,32 @@ __device__ __forceinline__ unsigned long long gtime() {
 //   K-major: one box (32 k, 128 rows).   MN-major: four boxes (32 mn, 32 k).
 template <int MN>
 __device__ __forceinline__ void load_operand(uint8_t* dst, const CUtensorMap* map, uint64_t* bar,
-                                             int r0, int k0, int g) {
+                                             int r0, int k0, int g, int rows = 128) {
     if (MN) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) tma_load_3d(dst + j * 4096, map, bar, r0 + 32 * j, k0, g);
+        for (int j = 0; j < rows / 32; ++j) tma_load_3d(dst + j * 4096, map, bar, r0 + 32 * j, k0, g);
     } else {
-        tma_load_3d(dst, map, bar, k0, r0, g);
+        tma_load_3d(dst, map, bar, k0, r0, g);  // the map's box carries the row count
     }
+}
+
+// work item w -> tile coordinates; items [0, nfull) are full tiles, the rest
+// split the last partial wave's tiles into two N halves (half = 0 / 1)
+struct Item {
+    int g, mt, nt, half;  // half = -1 for a full tile
+};
+__device__ __forceinline__ Item decode_item(const UmmaParams& p, int w, int tiles_m, int tiles_n) {
+    int t = w, half = -1;
+    if (w >= p.nfull) {
+        const int h = w - p.nfull;
+        t = p.nfull + (h >> 1);
+        half = h & 1;
+    }
+    Item it;
+    it.nt = t % tiles_n;
+    it.mt = (t / tiles_n) % tiles_m;
+    it.g = t / (tiles_n * tiles_m);
+    it.half = half;
+    return it;
 }
 
 // lo = rna_tf32(x - trunc_tf32(x)) over the two fp32 tiles of a load stage
@@ -324,7 +345,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_kernel(const __grid_const
     const uint32_t rank = PAIR ? cluster_rank() : 0;
     const int tiles_m = PAIR ? (p.M + 255) / 256 : (p.M + 127) / 128;
     const int tiles_n = (p.N + TN - 1) / TN;
-    const int ntiles = tiles_m * tiles_n * p.G;
+    const int nitems = p.nfull + p.nhalf;
     const int cid = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
     const int ncl = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
     const int nk = (p.K + BK - 1) / BK;
@@ -334,6 +355,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_kernel(const __grid_const
     if (warp == 0 && lane == 0) {
         tma_prefetch(&p.a);
         tma_prefetch(&p.b);
+        if (p.nhalf && !B_MN) tma_prefetch(&p.b64);
         for (int s = 0; s < LS; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
@@ -364,20 +386,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_kernel(const __grid_const
         {
             // ---------------- TMA producer ----------------
             uint32_t it = 0;
-            for (int t = cid; t < ntiles; t += ncl) {
-                const int nt = t % tiles_n, mt = (t / tiles_n) % tiles_m, g = t / (tiles_n * tiles_m);
-                const int m0 = PAIR ? mt * 256 + (int)rank * 128 : mt * 128;
-                const int nb0 = nt * TN + (int)rank * 128;  // B columns staged by this CTA
+            for (int w = cid; w < nitems; w += ncl) {
+                const Item im = decode_item(p, w, tiles_m, tiles_n);
+                const int g = im.g;
+                const int m0 = PAIR ? im.mt * 256 + (int)rank * 128 : im.mt * 128;
+                const int ncols = im.half < 0 ? TN : TN / 2;
+                const int n0 = im.nt * TN + (im.half > 0 ? TN / 2 : 0);
+                const int brows = ncols / (int)NCTA;          // B columns staged by this CTA
+                const int nb0 = n0 + (int)rank * brows;
+                const uint32_t bytes = TILE_BYTES + (uint32_t)brows * BK * 4;
+                const CUtensorMap* bmap = (im.half >= 0 && !B_MN) ? &p.b64 : &p.b;
                 for (int kb = 0; kb < nk; ++kb, ++it) {
                     const int s = it % LS;
-                    if (kb == (nk > 8 ? nk - 8 : 0)) prefetch_epilogue_rows(p, g, m0, nt * TN, TN, lane);
+                    if (kb == (nk > 8 ? nk - 8 : 0)) prefetch_epilogue_rows(p, g, m0, n0, ncols, lane);
                     mbar_wait(&empty[s], ((it / LS) & 1) ^ 1);
                     uint8_t* st = smem + s * LOAD_BYTES;
                     if (lane == 0) {
                         if (tr && it < 1000) tr[it] = gtime();
-                        mbar_expect_tx(&full[s], LOAD_BYTES);
+                        mbar_expect_tx(&full[s], bytes);
                         load_operand<A_MN>(st, &p.a, &full[s], m0, kb * BK, g);
-                        load_operand<B_MN>(st + TILE_BYTES, &p.b, &full[s], nb0, kb * BK, g);
+                        load_operand<B_MN>(st + TILE_BYTES, bmap, &full[s], nb0, kb * BK, g, brows);
                     }
                     __syncwarp();
                 }
@@ -385,10 +413,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_kernel(const __grid_const
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer (leader CTA, one thread) ----------------
-        constexpr uint32_t idesc = idesc_tf32(PAIR ? 256 : 128, TN, A_MN, B_MN);
+        constexpr uint32_t idesc_full = idesc_tf32(PAIR ? 256 : 128, TN, A_MN, B_MN);
+        constexpr uint32_t idesc_half = idesc_tf32(PAIR ? 256 : 128, TN / 2, A_MN, B_MN);
         if (rank == 0) {
             uint32_t it = 0, tl = 0;
-            for (int t = cid; t < ntiles; t += ncl, ++tl) {
+            for (int w = cid; w < nitems; w += ncl, ++tl) {
+                const uint32_t idesc = w < p.nfull ? idesc_full : idesc_half;
                 const uint32_t b = tl & 1;
                 mbar_wait(&acc_empty[b], ((tl >> 1) & 1) ^ 1);
                 tc_fence_after();
@@ -422,14 +452,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_kernel(const __grid_const
         // ---------------- epilogue: own 128 rows x TN columns ----------------
         const int q = warp & 3;  // TMEM lane quarter this warp may access
         uint32_t tl = 0;
-        for (int t = cid; t < ntiles; t += ncl, ++tl) {
-            const int nt = t % tiles_n, mt = (t / tiles_n) % tiles_m, g = t / (tiles_n * tiles_m);
-            const int m0 = PAIR ? mt * 256 + (int)rank * 128 : mt * 128;
+        for (int w = cid; w < nitems; w += ncl, ++tl) {
+            const Item im = decode_item(p, w, tiles_m, tiles_n);
+            const int g = im.g;
+            const int m0 = PAIR ? im.mt * 256 + (int)rank * 128 : im.mt * 128;
+            const int ncols = im.half < 0 ? TN : TN / 2;
+            const int n0 = im.nt * TN + (im.half > 0 ? TN / 2 : 0);
             const uint32_t b = tl & 1;
             mbar_wait(&acc_full[b], (tl >> 1) & 1);
             if (tr && threadIdx.x == 64 && tl < 16) tr[2000 + 2 * tl] = gtime();
             tc_fence_after();
-            epilogue_tile(p, tmem + b * TN, q, lane, g, m0, nt * TN, TN,
+            epilogue_tile(p, tmem + b * TN, q, lane, g, m0, n0, ncols,
                           smem_u32(epi_smem) + (uint32_t)(q * 32 * EPI_LD * 4));
             tc_fence_before();
             __syncwarp();
@@ -443,7 +476,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_kernel(const __grid_const
         // ---------------- converters ----------------
         const int ct = threadIdx.x - 192;
         uint32_t it = 0;
-        for (int t = cid; t < ntiles; t += ncl) {
+        for (int w = cid; w < nitems; w += ncl) {
             for (int kb = 0; kb < nk; ++kb, ++it) {
                 const int s = it % LS, l = it % LO;
                 mbar_wait(&full[s], (it / LS) & 1);
@@ -527,8 +560,17 @@ CUtensorMap make_map(const float* base, long long inner, long long outer, long l
     return m;
 }
 
+bool disable_half_tiles() {
+    static int mode = -1;
+    if (mode < 0) {
+        const char* e = getenv("MTK_UMMA_NO_HALF");  // A/B diagnostics
+        mode = e ? 1 : 0;
+    }
+    return mode == 1;
+}
+
 template <int A_MN, int B_MN, bool PAIR>
-void launch_variant(const UmmaParams& p, int G, cudaStream_t s) {
+void launch_variant(UmmaParams p, int G, cudaStream_t s) {
     static bool attr = false;
     if (!attr) {
         MTK_CUDA(cudaFuncSetAttribute(umma_kernel<A_MN, B_MN, PAIR>,
@@ -544,6 +586,14 @@ void launch_variant(const UmmaParams& p, int G, cudaStream_t s) {
     const long long ntiles = PAIR ? (long long)((p.M + 255) / 256) * ((p.N + 255) / 256) * G
                                   : (long long)((p.M + 127) / 128) * ((p.N + 127) / 128) * G;
     const long long ncl = std::min<long long>(ntiles, PAIR ? sms / 2 : sms);
+    // split the last partial wave into N halves when they fit in one wave
+    p.nfull = (int)ntiles;
+    p.nhalf = 0;
+    const long long rem = ntiles % ncl;
+    if (PAIR && ntiles > ncl && rem > 0 && 2 * rem <= ncl && !disable_half_tiles()) {
+        p.nfull = (int)(ntiles - rem);
+        p.nhalf = (int)(2 * rem);
+    }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)(PAIR ? 2 * ncl : ncl), 1, 1);
     cfg.blockDim = dim3(NUM_THREADS);
@@ -601,6 +651,7 @@ void launch_umma(const UmmaGemm& u, cudaStream_t s) {
                  : make_map(u.a, u.K, u.M, u.G, u.a_rs, u.a_gs, 128, false);
     p.b = u.b_mn ? make_map(u.b, u.N, u.K, u.G, u.b_rs, u.b_gs, BK, true)
                  : make_map(u.b, u.K, u.N, u.G, u.b_rs, u.b_gs, 128, false);
+    if (!u.b_mn) p.b64 = make_map(u.b, u.K, u.N, u.G, u.b_rs, u.b_gs, 64, false);
     p.G = u.G;
     p.M = u.M;
     p.N = u.N;

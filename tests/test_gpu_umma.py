@@ -32,3 +32,21 @@ def test_umma_gemm(ctx, a_mn, b_mn, G, M, N, K):
     C = api.diag_gemm_tf32x3(ctx, Ad, Bd, bool(a_mn), bool(b_mn)).cpu().double().numpy()
     e = rel(C, ref)
     assert e <= 1e-5, e
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 1), (0, 0), (1, 1), (1, 0)])
+@pytest.mark.parametrize("G,M,N,K", [(32, 1024, 512, 64), (20, 512, 392, 100), (40, 300, 300, 36)])
+def test_umma_gemm_half_tiles(ctx, a_mn, b_mn, G, M, N, K):
+    """Tile counts whose last partial wave is split into N halves (256 x 128
+    pair tiles), including ragged M / N edges inside the halves."""
+    from paper_2011_09463_b200 import api
+
+    g = torch.Generator(device="cuda").manual_seed(G + M + N + K)
+    A = torch.randn((G, M, K), device="cuda", generator=g)
+    B = torch.randn((G, K, N), device="cuda", generator=g)
+    ref = torch.matmul(A.double(), B.double())
+    Ad = (A.transpose(1, 2) if a_mn else A).contiguous()
+    Bd = (B if b_mn else B.transpose(1, 2)).contiguous()
+    C = api.diag_gemm_tf32x3(ctx, Ad, Bd, bool(a_mn), bool(b_mn)).double()
+    e = float((C - ref).abs().max() / ref.abs().max())
+    assert e <= 1e-5, e
