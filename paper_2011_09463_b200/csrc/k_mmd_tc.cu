@@ -22,6 +22,7 @@
 #include <cuda.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "internal.h"
@@ -33,16 +34,34 @@ namespace {
 using namespace sm100;
 
 constexpr int TI = 128, TJ = 64, KC = 32, JC = 16, VD = 256;
-constexpr int STAGES = 4;
+// Two smem plans (template RES):
+//   RES = false  4-stage ring of 48 KB: G1 stages bring Z_i hi+lo and Z_j hi+lo
+//   RES = true   (d <= 256) Z_i hi stays resident (128 KB, loaded once) and a
+//                3-stage ring of 32 KB brings Z_i lo + Z_j hi+lo -- a quarter
+//                less L2 -> smem traffic per j tile
 constexpr int G1_BYTES = 2 * (TI * KC * 4) + 2 * (TJ * KC * 4);  // 48 KB (hi + lo planes)
+constexpr int G1R_BYTES = (TI * KC * 4) + 2 * (TJ * KC * 4);     // 32 KB (Z_i lo + Z_j hi/lo)
 constexpr int G2_BYTES = 2 * (JC * VD * 4);                       // 32 KB
-constexpr int STAGE_BYTES = G1_BYTES;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr int RES_BYTES = TI * VD * 4;                            // resident Z_i hi (d <= 256)
+template <bool RES>
+struct Plan {
+    static constexpr int STAGES = RES ? 3 : 4;
+    static constexpr int STAGE_BYTES = RES ? G1R_BYTES : G1_BYTES;
+    static constexpr int RING_OFF = RES ? RES_BYTES : 0;
+    static constexpr int SMEM_BYTES = RING_OFF + STAGES * STAGE_BYTES + 1024 + 256;
+};
+static_assert(Plan<true>::SMEM_BYTES <= 232448, "resident plan exceeds smem");
 constexpr int NUM_THREADS = 192;
 // TMEM columns: V [0,256); S / W-hi double buffer b at 256 + 64 b (S is
 // overwritten in place by the hi plane of W); W-lo buffer b at 384 + 64 b.
+// TMEM columns: V [0,256); S/W buffer b at 256 + 128 b.  GEMM1 runs as
+//   [S_lo | S_hh] (128 cols) = Z_i_hi . [Z_j_lo | Z_j_hi]^T   (one N=128 MMA)
+//   S_hh += Z_i_lo . Z_j_hi^T                                  (N=64, cols 64..127)
+// so Z_i_hi is read once per k step instead of twice (GEMM1 is bound by the
+// A-operand smem reads at N=64); S = S_lo + S_hh.  The epilogue then writes
+// W's tf32 hi over cols [0,64) and lo over [64,128) of the same buffer.
 constexpr uint32_t S_COL = 256;
-constexpr uint32_t WLO_COL = 384;
+constexpr uint32_t SBUF = 128;
 
 struct MmdTcParams {
     CUtensorMap zk_hi, zk_lo;   // K-major views of the planes: (d, N, G), box (32, 64)
@@ -90,16 +109,21 @@ __device__ __forceinline__ unsigned long long gtime() {
 // tens of thousands of j would not hold 1e-5 (C4: m+n = 73728).
 constexpr int FLUSH = 16;  // j tiles (1024 rows of Z) per fp32 V chunk
 
+template <bool RES>
 __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_constant__ MmdTcParams p) {
+    constexpr int STAGES = Plan<RES>::STAGES, STAGE_BYTES = Plan<RES>::STAGE_BYTES;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* smem0 = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* res = smem0;                          // resident Z_i hi (RES)
+    uint8_t* smem = smem0 + Plan<RES>::RING_OFF;   // the stage ring
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
     uint64_t* empty = full + STAGES;
     uint64_t* s_full = empty + STAGES;  // [2]
     uint64_t* w_full = s_full + 2;      // [2]
     uint64_t* v_full = w_full + 2;
     uint64_t* v_empty = v_full + 1;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(v_empty + 1);
+    uint64_t* res_full = v_empty + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(res_full + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = blockIdx.z;
@@ -138,6 +162,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
         }
         mbar_init(v_full, 1);
         mbar_init(v_empty, 128);
+        mbar_init(res_full, 1);
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -156,6 +181,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
     if (warp == 0) {
         {
             // ---------------- TMA producer ----------------
+            if (RES && lane == 0) {  // resident Z_i hi: kc chunk at kc * 16 KB (two 64-row boxes)
+                mbar_expect_tx(res_full, (uint32_t)(nkc * 2 * 8192));
+                for (int kc = 0; kc < nkc; ++kc) {
+                    tma_load_3d(res + kc * 16384, &p.zk_hi, res_full, kc * KC, (int)i0, g);
+                    tma_load_3d(res + kc * 16384 + 8192, &p.zk_hi, res_full, kc * KC, (int)i0 + 64, g);
+                }
+            }
+            __syncwarp();
             int st = 0;
             for (int t = 0; t <= njt; ++t) {
                 if (t < njt) {
@@ -167,15 +200,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
                         uint8_t* b = smem + s * STAGE_BYTES;
                         const int k0 = kc * KC;
                         if (lane == 0) {
-                        mbar_expect_tx(&full[s], G1_BYTES);
-                        // Z_i hi [0,16K) and lo [16K,32K) (two 64-row boxes each),
-                        // Z_j hi [32K,40K) and lo [40K,48K)
-                        tma_load_3d(b, &p.zk_hi, &full[s], k0, (int)i0, g);
-                        tma_load_3d(b + 8192, &p.zk_hi, &full[s], k0, (int)i0 + 64, g);
-                        tma_load_3d(b + 16384, &p.zk_lo, &full[s], k0, (int)i0, g);
-                        tma_load_3d(b + 24576, &p.zk_lo, &full[s], k0, (int)i0 + 64, g);
-                        tma_load_3d(b + 32768, &p.zk_hi, &full[s], k0, j0, g);
-                        tma_load_3d(b + 40960, &p.zk_lo, &full[s], k0, j0, g);
+                            if (RES) {
+                                // Z_i lo [0,16K) (two 64-row boxes), Z_j lo [16K,24K), hi [24K,32K)
+                                mbar_expect_tx(&full[s], G1R_BYTES);
+                                tma_load_3d(b, &p.zk_lo, &full[s], k0, (int)i0, g);
+                                tma_load_3d(b + 8192, &p.zk_lo, &full[s], k0, (int)i0 + 64, g);
+                                tma_load_3d(b + 16384, &p.zk_lo, &full[s], k0, j0, g);
+                                tma_load_3d(b + 24576, &p.zk_hi, &full[s], k0, j0, g);
+                            } else {
+                                // Z_i hi [0,16K) and lo [16K,32K) (two 64-row boxes each),
+                                // Z_j lo [32K,40K) and hi [40K,48K)
+                                mbar_expect_tx(&full[s], G1_BYTES);
+                                tma_load_3d(b, &p.zk_hi, &full[s], k0, (int)i0, g);
+                                tma_load_3d(b + 8192, &p.zk_hi, &full[s], k0, (int)i0 + 64, g);
+                                tma_load_3d(b + 16384, &p.zk_lo, &full[s], k0, (int)i0, g);
+                                tma_load_3d(b + 24576, &p.zk_lo, &full[s], k0, (int)i0 + 64, g);
+                                tma_load_3d(b + 32768, &p.zk_lo, &full[s], k0, j0, g);
+                                tma_load_3d(b + 40960, &p.zk_hi, &full[s], k0, j0, g);
+                            }
                         }
                         __syncwarp();
                     }
@@ -204,12 +246,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
         // ---------------- MMA issuer ----------------
         {
             constexpr uint32_t id1 = idesc_tf32(TI, TJ, 0, 0);
+            constexpr uint32_t id1w = idesc_tf32(TI, 2 * TJ, 0, 0);
             constexpr uint32_t id2 = idesc_tf32(TI, VD, 0, 1);
             const uint32_t tV = tmem;
+            const uint32_t rbase = smem_u32(res);
+            if (RES) {
+                mbar_wait(res_full, 0);
+                tc_fence_after();
+            }
             int st = 0;
             for (int t = 0; t <= njt; ++t) {
                 if (t < njt) {
-                    const uint32_t tS = tmem + S_COL + (t & 1) * TJ;
+                    const uint32_t tS = tmem + S_COL + (t & 1) * SBUF;
                     for (int kc = 0; kc < nkc; ++kc, ++st) {
                         const int s = st % STAGES;
                         mbar_wait(&full[s], (st / STAGES) & 1);
@@ -219,13 +267,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
                         TRACE(4096, st);
 #pragma unroll
                         for (int kk = 0; kk < KC / 8; ++kk) {
-                            const uint64_t ahi = smem_desc(b + kk * 32, 16, 1024, 2);
-                            const uint64_t alo = smem_desc(b + 16384 + kk * 32, 16, 1024, 2);
-                            const uint64_t bhi = smem_desc(b + 32768 + kk * 32, 16, 1024, 2);
-                            const uint64_t blo = smem_desc(b + 40960 + kk * 32, 16, 1024, 2);
-                            mma_tf32(tS, alo, bhi, id1, (kc | kk) ? 1u : 0u);
-                            mma_tf32(tS, ahi, blo, id1, 1u);
-                            mma_tf32(tS, ahi, bhi, id1, 1u);
+                            const uint64_t ahi = RES ? smem_desc(rbase + kc * 16384 + kk * 32, 16, 1024, 2)
+                                                     : smem_desc(b + kk * 32, 16, 1024, 2);
+                            const uint64_t alo = smem_desc(b + (RES ? 0 : 16384) + kk * 32, 16, 1024, 2);
+                            // 128 rows: Z_j lo (64) then Z_j hi (64)
+                            const uint64_t blh = smem_desc(b + (RES ? 16384 : 32768) + kk * 32, 16, 1024, 2);
+                            const uint64_t bhi = smem_desc(b + (RES ? 24576 : 40960) + kk * 32, 16, 1024, 2);
+                            mma_tf32(tS, ahi, blh, id1w, (kc | kk) ? 1u : 0u);
+                            mma_tf32(tS + TJ, alo, bhi, id1, 1u);
                         }
                         mma_commit(&empty[s]);
                         }
@@ -236,8 +285,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
                 }
                 if (t >= 1) {
                     const int jt = t - 1;
-                    const uint32_t tWhi = tmem + S_COL + (jt & 1) * TJ;
-                    const uint32_t tWlo = tmem + WLO_COL + (jt & 1) * TJ;
+                    const uint32_t tWhi = tmem + S_COL + (jt & 1) * SBUF;
+                    const uint32_t tWlo = tWhi + TJ;
                     mbar_wait(&w_full[jt & 1], (jt >> 1) & 1);  // W(jt) is in TMEM
                     tc_fence_after();
                     const bool chunk_start = do_flush ? (jt % FLUSH == 0) : (jt == 0);
@@ -311,7 +360,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
 #pragma unroll 1
             for (int ch = 0; ch < TJ / 8; ++ch) {
                 float sv[8], wlo[8];
-                tmem_ld_32x8(tmem + lane_base + S_COL + bsel * TJ + ch * 8, sv);
+                {
+                    float sh[8];
+                    tmem_ld_32x8(tmem + lane_base + S_COL + bsel * SBUF + ch * 8, sv);
+                    tmem_ld_32x8(tmem + lane_base + S_COL + bsel * SBUF + TJ + ch * 8, sh);
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) sv[c] += sh[c];  // S = S_lo + S_hh
+                }
                 const long long jb = j0 + ch * 8;
                 // column classes are warp-uniform: all 8 j in range / same domain?
                 const bool full8 = row_ok && jb + 8 <= N;
@@ -386,8 +441,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
                         split_tf32(wv, sv[c], wlo[c]);
                     }
                 }
-                tmem_st_32x8(tmem + lane_base + S_COL + bsel * TJ + ch * 8, sv);
-                tmem_st_32x8(tmem + lane_base + WLO_COL + bsel * TJ + ch * 8, wlo);
+                tmem_st_32x8(tmem + lane_base + S_COL + bsel * SBUF + ch * 8, sv);
+                tmem_st_32x8(tmem + lane_base + S_COL + bsel * SBUF + TJ + ch * 8, wlo);
             }
             ksum[0] += kss;
             ksum[1] += ktt;
@@ -437,7 +492,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
         const int t = threadIdx.x - 64;
         constexpr int VLD = VD + 4;  // float4-aligned rows, conflict-free row-wise float4
         constexpr int C4 = VD / 4;
-        const uint32_t zsb = smem_u32(smem);
+        static_assert(TI * VLD * 4 <= Plan<true>::RING_OFF + Plan<true>::STAGES * Plan<true>::STAGE_BYTES &&
+                          TI * VLD * 4 <= Plan<false>::STAGES * Plan<false>::STAGE_BYTES,
+                      "finish tile exceeds the idle smem");
+        const uint32_t zsb = smem_u32(smem0);
         for (int e = t; e < TI * C4; e += 128) {
             const int rr = e / C4, c4 = e % C4;
             const long long row = i0 + rr;
@@ -497,7 +555,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) mmd_tc_kernel(const __grid_con
         if (tr && r == 0) tr[12286] = gtime();
         if (bad) atomicOr(p.flags, kFlagNonFinite);
         // fixed-order reduction of the kernel sums over the 128 rows (d-slice 0 only)
-        __shared__ double red[3][128];
+        // (dynamic smem past the finish tile: the whole ring is idle by now)
+        double(*red)[128] = reinterpret_cast<double(*)[128]>(smem0 + ((TI * VLD * 4 + 1023) & ~1023));
         for (int c = 0; c < 3; ++c) red[c][t] = ksum[c];
         asm volatile("bar.sync 1, 128;" ::: "memory");
         for (int w = 64; w > 0; w >>= 1) {
@@ -718,12 +777,20 @@ void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s, int stages) 
     p.trace = a.trace;
     static bool attr = false;
     if (!attr) {
-        MTK_CUDA(cudaFuncSetAttribute(mmd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      SMEM_BYTES));
+        MTK_CUDA(cudaFuncSetAttribute(mmd_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      Plan<true>::SMEM_BYTES));
+        MTK_CUDA(cudaFuncSetAttribute(mmd_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      Plan<false>::SMEM_BYTES));
         attr = true;
     }
     dim3 grid(p.nblk, (a.d + VD - 1) / VD, a.G);
-    mmd_tc_kernel<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(p);
+    // the resident-Z_i-hi plan measured ~1.5% slower than the 4-stage ring
+    // (GEMM1 is bound by operand reads, not by the TMA stream); opt-in only
+    static const bool use_res = getenv("MTK_MMD_RES") != nullptr;
+    if (a.d <= VD && use_res)
+        mmd_tc_kernel<true><<<grid, NUM_THREADS, Plan<true>::SMEM_BYTES, s>>>(p);
+    else
+        mmd_tc_kernel<false><<<grid, NUM_THREADS, Plan<false>::SMEM_BYTES, s>>>(p);
     count_launch();
 }
 

@@ -20,6 +20,26 @@ for _ in range(2):
     api.mmd_gaussian(ctx, Xs, Xt)
 t = tr.cpu().numpy().astype(np.int64)
 t0 = min(x for x in t if x > 0)
+def stage_types(njt, nkc=8, n2=4):
+    ty = []
+    for tt in range(njt + 1):
+        if tt < njt:
+            ty += ["G1"] * nkc
+        if tt >= 1:
+            ty += ["G2"] * n2
+    return ty
+
+
+def split_gaps(name, arr, njt, nkc):
+    arr = arr[arr > 0]
+    ty = stage_types(njt, nkc)[: len(arr)]
+    dd = np.diff(arr) / 1000
+    for kind in ("G1", "G2"):
+        v = [dd[i] for i in range(len(dd)) if ty[i] == kind]
+        if v:
+            print(f"   {name} {kind}: {len(v)} stages, mean {np.mean(v):.3f} us, median {np.median(v):.3f}")
+
+
 def show(name, arr):
     arr = arr[arr > 0] - t0
     print(name, len(arr), "events; first 40 (us):", np.round(arr[:40] / 1000, 2).tolist())
@@ -27,6 +47,7 @@ def show(name, arr):
         print("   span", (arr.max() - arr.min()) / 1000, "us; mean gap", np.diff(arr).mean() / 1000, "us")
 show("producer stage-issue", t[:4096])
 show("mma stage-consume", t[4096:8192])
+split_gaps("mma consume", t[4096:8192], (N + 63) // 64, (d + 31) // 32)
 ep = t[8192:12288]
 show("epilogue s_full seen / w arrived", ep)
 
@@ -48,6 +69,7 @@ if len(sys.argv) > 3:  # full bank step (G models) for CTA (0,0,0) under load
     print(f"---- bank step, G={G}")
     show("producer stage-issue", t[:4096])
     show("mma stage-consume", t[4096:8192])
+    split_gaps("mma consume", t[4096:8192], (N + 63) // 64, (d + 31) // 32)
     show("epilogue s_full seen / w arrived", t[8192:12288])
     c = t[12288:].reshape(-1, 3)
     c = c[c[:, 0] > 0]
