@@ -32,26 +32,17 @@ using namespace mtk;
 
 namespace {
 
+// one device fp32 array (kept as a struct so the layer plumbing stays typed)
 struct Plane3 {
-    float* f = nullptr;   // fp32 values
-    float* hi = nullptr;  // tf32 hi plane (tensor-core operand), optional
-    float* lo = nullptr;  // tf32 lo plane, optional
+    float* f = nullptr;
 };
 
 void free3(Plane3& p, bool own_f = true) {
     if (own_f) cudaFree(p.f);
-    cudaFree(p.hi);
-    cudaFree(p.lo);
     p = Plane3{};
 }
 
-void alloc3(Plane3& p, size_t n, bool f, bool split) {
-    if (f) MTK_CUDA(cudaMalloc(&p.f, n * sizeof(float)));
-    if (split) {
-        MTK_CUDA(cudaMalloc(&p.hi, n * sizeof(float)));
-        MTK_CUDA(cudaMalloc(&p.lo, n * sizeof(float)));
-    }
-}
+void alloc3(Plane3& p, size_t n) { MTK_CUDA(cudaMalloc(&p.f, n * sizeof(float))); }
 
 }  // namespace
 
@@ -78,7 +69,6 @@ struct mtk_bank {
     }
     bool keep_grads = false;
     int capB = 0;
-    Plane3 Xsp;               // hi/lo planes of the input (f borrowed per call)
     std::vector<Plane3> H;    // H[l], l in [1, L)
     Plane3 dZ[2];
     float* logits = nullptr;
@@ -216,7 +206,6 @@ struct mtk_bank {
     void free_acts() {
         for (auto& p : H) free3(p);
         H.clear();
-        free3(Xsp, false);
         free3(dZ[0]);
         free3(dZ[1]);
         cudaFree(logits);
@@ -236,8 +225,8 @@ struct mtk_bank {
         free_acts();
         const size_t GB = (size_t)G * B;
         H.assign(L, Plane3{});
-        for (int l = 1; l < L; ++l) alloc3(H[l], GB * dims[l], true, false);
-        for (auto& z : dZ) alloc3(z, GB * maxd(), true, false);
+        for (int l = 1; l < L; ++l) alloc3(H[l], GB * dims[l]);
+        for (auto& z : dZ) alloc3(z, GB * maxd());
         MTK_CUDA(cudaMalloc(&logits, GB * dims[L] * sizeof(float)));
         MTK_CUDA(cudaMalloc(&row_loss, GB * sizeof(double)));
         if (L > 1) MTK_CUDA(cudaMalloc(&gH, GB * dims[L - 1] * sizeof(float)));
@@ -256,13 +245,6 @@ struct mtk_bank {
         MTK_CUDA(cudaMalloc(&ys, GB * sizeof(int32_t)));
         MTK_CUDA(cudaMalloc(&ws, GB * sizeof(float)));
         stageB = B;
-    }
-    // re-derive the tf32 planes of parameter matrix i from its fp32 master
-    void split_param(int i, int model) {
-        if (!W[i].hi) return;
-        const size_t nw = (size_t)fan_in(i) * fan_out(i), off = (size_t)model * nw;
-        launch_split(W[i].f + off, W[i].hi + off, W[i].lo + off, (long long)nw, ctx->stream);
-        after_launch(*ctx);
     }
 };
 
@@ -310,8 +292,6 @@ void gemm_fwd(mtk_bank& k, int mat, const Plane3& in, int B, int r0, int rows, c
         h.bias = k.b[mat];
         h.bias_gs = fo;
         h.C = out.f + (size_t)r0 * fo;
-        h.C_hi = out.hi ? out.hi + (size_t)r0 * fo : nullptr;
-        h.C_lo = out.lo ? out.lo + (size_t)r0 * fo : nullptr;
         h.c_gs = (long long)B * fo;
         h.ldc = fo;
         h.relu = relu ? 1 : 0;
@@ -332,8 +312,6 @@ void gemm_fwd(mtk_bank& k, int mat, const Plane3& in, int B, int r0, int rows, c
         g.b_ks = fo;
         g.b_ns = 1;
         g.C = out.f + (size_t)r0 * fo;
-        g.C_hi = out.hi ? out.hi + (size_t)r0 * fo : nullptr;
-        g.C_lo = out.lo ? out.lo + (size_t)r0 * fo : nullptr;
         g.c_gs = (long long)B * fo;
         g.ldc = fo;
         g.epi = relu ? Epi::kBiasRelu : Epi::kBias;
@@ -409,8 +387,6 @@ bool gemm_dx(mtk_bank& k, int mat, const Plane3& dz, int B, int r0, int rows, co
         g.b_ks = 1;
         g.b_ns = fo;
         g.C = out.f + (size_t)r0 * fi;
-        g.C_hi = out.hi ? out.hi + (size_t)r0 * fi : nullptr;
-        g.C_lo = out.lo ? out.lo + (size_t)r0 * fi : nullptr;
         g.c_gs = (long long)B * fi;
         g.ldc = fi;
         g.epi = Epi::kMask;
@@ -474,8 +450,6 @@ void gemm_dw(mtk_bank& k, int mat, const Plane3& in, const Plane3& dz, int B, in
         h.dz_gs = (long long)B * fo;
         h.lddz = fo;
         h.W = k.W[mat].f;
-        h.W_hi = k.W[mat].hi;
-        h.W_lo = k.W[mat].lo;
         h.w_gs = (long long)fi * fo;
         h.lr = lr;
         h.adam = adam;
@@ -505,8 +479,6 @@ void gemm_dw(mtk_bank& k, int mat, const Plane3& in, const Plane3& dz, int B, in
         g.b_ks = fo;
         g.b_ns = 1;
         g.C = adam_gemm ? gbuf : k.W[mat].f;
-        g.C_hi = adam_gemm ? nullptr : k.W[mat].hi;
-        g.C_lo = adam_gemm ? nullptr : k.W[mat].lo;
         g.c_gs = (long long)fi * fo;
         g.ldc = fo;
         g.epi = adam_gemm ? Epi::kStore : Epi::kSgd;
@@ -797,12 +769,8 @@ int mtk_bank_create(mtk_ctx* c, int G, int n_layers, const int* dims, int n_head
         for (int i = 0; i < k->n_mats; ++i) {
             const size_t nw = (size_t)G * k->fan_in(i) * k->fan_out(i);
             Plane3 w;
-            alloc3(w, nw, true, false);
+            alloc3(w, nw);
             MTK_CUDA(cudaMemsetAsync(w.f, 0, nw * 4, c->stream));
-            if (w.hi) {
-                MTK_CUDA(cudaMemsetAsync(w.hi, 0, nw * 4, c->stream));
-                MTK_CUDA(cudaMemsetAsync(w.lo, 0, nw * 4, c->stream));
-            }
             float* bb = nullptr;
             MTK_CUDA(cudaMalloc(&bb, (size_t)G * k->fan_out(i) * sizeof(float)));
             MTK_CUDA(cudaMemsetAsync(bb, 0, (size_t)G * k->fan_out(i) * 4, c->stream));

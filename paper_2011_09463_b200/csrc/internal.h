@@ -125,8 +125,6 @@ struct Gemm {
     const float* mask = nullptr;  // kMask: mask source, same layout as C
     float lr = 0.f;               // kSgd
     float* grad_out = nullptr;    // kSgd: optional copy of acc, same layout as C
-    float* C_hi = nullptr;        // optional tf32 split planes of the result
-    float* C_lo = nullptr;
     int* flags = nullptr;
 };
 
@@ -159,7 +157,6 @@ struct UmmaGemm {
     int* flags = nullptr;
 };
 void launch_umma(const UmmaGemm& u, cudaStream_t s);
-void launch_split(const float* x, float* hi, float* lo, long long n, cudaStream_t s);
 
 // Skinny layers (out width <= 32): k_head.cu
 struct HeadFwd {
@@ -171,8 +168,6 @@ struct HeadFwd {
     const float* bias = nullptr;
     long long bias_gs = 0;
     float* C = nullptr;
-    float* C_hi = nullptr;
-    float* C_lo = nullptr;
     long long c_gs = 0, ldc = 0;
     int relu = 0;
     int* flags = nullptr;
@@ -184,8 +179,6 @@ struct HeadDw {
     const float* dZ = nullptr; // [G][rows][N] (stride lddz)
     long long dz_gs = 0, lddz = 0;
     float* W = nullptr;        // [G][K][N]
-    float* W_hi = nullptr;
-    float* W_lo = nullptr;
     long long w_gs = 0;
     float lr = 0.f;
     AdamArgs adam;

@@ -106,12 +106,6 @@ __global__ void __launch_bounds__(128) head_fwd_kernel(HeadFwd p) {
         bad |= !isfinite(v);
         if (p.relu) v = v > 0.f ? v : 0.f;
         out[n] = v;
-        if (p.C_hi) {
-            float h, l;
-            sm100::split_tf32(v, h, l);
-            p.C_hi[g * p.c_gs + (long long)r * p.ldc + n] = h;
-            p.C_lo[g * p.c_gs + (long long)r * p.ldc + n] = l;
-        }
     }
     if (bad && p.flags) atomicOr(p.flags, kFlagNonFinite);
 }
@@ -260,12 +254,6 @@ __global__ void head_dw_finish_kernel(HeadDw p) {
     const float w = param_update(p.W[idx], gsum, p.lr, p.adam, idx);
     if (!isfinite(w) && p.flags) atomicOr(p.flags, kFlagNonFinite);
     p.W[idx] = w;
-    if (p.W_hi) {
-        float h, l;
-        sm100::split_tf32(w, h, l);
-        p.W_hi[idx] = h;
-        p.W_lo[idx] = l;
-    }
 }
 
 // Forward-only 2-layer MLP with a tiny input and output (the attack model

@@ -121,12 +121,6 @@ __global__ void __launch_bounds__(NT) gemm_simt_kernel(Gemm p) {
                     break;
             }
             p.C[idx] = v;
-            if (p.C_hi) {
-                float hi, lo;
-                sm100::split_tf32(v, hi, lo);
-                p.C_hi[idx] = hi;
-                p.C_lo[idx] = lo;
-            }
         }
     }
     if (bad && p.flags) atomicOr(p.flags, kFlagNonFinite);

@@ -504,22 +504,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_kernel(const __grid_const
     }
 }
 
-__global__ void split_kernel(const float* __restrict__ x, float* __restrict__ hi,
-                             float* __restrict__ lo, long long n) {
-    const long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 4;
-    if (i + 3 < n) {
-        const float4 v = *reinterpret_cast<const float4*>(x + i);
-        float4 h, l;
-        split_tf32(v.x, h.x, l.x);
-        split_tf32(v.y, h.y, l.y);
-        split_tf32(v.z, h.z, l.z);
-        split_tf32(v.w, h.w, l.w);
-        *reinterpret_cast<float4*>(hi + i) = h;
-        *reinterpret_cast<float4*>(lo + i) = l;
-    } else {
-        for (long long j = i; j < n; ++j) split_tf32(x[j], hi[j], lo[j]);
-    }
-}
 
 // ---- host: tensor-map encoding through the driver entry point -------------
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -629,15 +613,6 @@ bool use_pair_kernel(const UmmaGemm& u) {
 
 }  // namespace
 
-void launch_split(const float* x, float* hi, float* lo, long long n, cudaStream_t s) {
-    if (n <= 0) return;
-    if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(hi) |
-         reinterpret_cast<uintptr_t>(lo)) & 15)
-        fail(MTK_ERROR, "split: unaligned pointer");
-    const long long t = (n + 3) / 4;
-    split_kernel<<<(unsigned)((t + 255) / 256), 256, 0, s>>>(x, hi, lo, n);
-    count_launch();
-}
 
 // Operand views: element (r, c) of an operand sits at base[g*gs + r*rs + c],
 // c the contiguous index (K-major: r = m or n, c = k; MN-major: r = k).
