@@ -276,6 +276,7 @@ __global__ void bias_from_partials_kernel(int G, int nrb, int N, const float* pa
     if (t >= G * N) return;
     const int g = t / N, n = t % N;
     float s = 0.f;
+#pragma unroll 8
     for (int rb = 0; rb < nrb; ++rb) s += partial[((long long)g * nrb + rb) * N + n];
     if (grad_out) grad_out[t] = s;
     const float v = param_update(b[t], s, lr, adam, t);

@@ -57,10 +57,14 @@ __global__ void beta_finish_kernel(MmdArgs a, const double* part, int P, double*
     double ss = 0.0;
     for (int k = threadIdx.x; k < a.d; k += NT) {
         double s = 0.0;
+#pragma unroll 8
         for (int p = 0; p < P; ++p) s += part[((long long)g * P + p) * (a.d + 1) + k];
         ss += s * s;
     }
     red[threadIdx.x] = ss;
+    // the row-norm partials, loaded in parallel, summed in order by thread 0
+    __shared__ double np[NT];
+    for (int p = threadIdx.x; p < min(P, NT); p += NT) np[p] = part[((long long)g * P + p) * (a.d + 1) + a.d];
     __syncthreads();
     for (int w = NT / 2; w > 0; w >>= 1) {
         if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
@@ -68,7 +72,7 @@ __global__ void beta_finish_kernel(MmdArgs a, const double* part, int P, double*
     }
     if (threadIdx.x == 0) {
         double s2 = 0.0;
-        for (int p = 0; p < P; ++p) s2 += part[((long long)g * P + p) * (a.d + 1) + a.d];
+        for (int p = 0; p < P; ++p) s2 += p < NT ? np[p] : part[((long long)g * P + p) * (a.d + 1) + a.d];
         const double N = (double)(a.m + a.n);
         beta[g] = (2.0 * N * s2 - 2.0 * red[0]) / (N * N - N);
     }

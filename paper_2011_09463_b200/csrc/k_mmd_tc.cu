@@ -599,37 +599,68 @@ __global__ void __launch_bounds__(256) mmd_prep_kernel(const float* Xs, long lon
     double* cs = part ? colsum + warp * d : nullptr;
     if (cs)
         for (int c = lane; c < d; c += 32) cs[c] = 0.0;
-    double nacc = 0.0;
-    for (int i = 0; i < kBetaRows / PREP_WARPS; ++i) {
-        const long long row = (long long)blockIdx.x * kBetaRows + warp * (kBetaRows / PREP_WARPS) + i;
-        if (row >= N) break;
-        const float4* src = reinterpret_cast<const float4*>(row < m ? Xs + g * xs_gs + row * d
-                                                                    : Xt + g * xt_gs + (row - m) * d);
-        const long long o = ((long long)g * N + row) * d;
-        float4* hi = reinterpret_cast<float4*>(zhi + o);
-        float4* lo = reinterpret_cast<float4*>(zlo + o);
-        double acc = 0.0;
-        for (int k = lane; k < d4; k += 32) {
-            const float4 x = src[k];
+    // the warp's 4 rows advance together (their loads in flight at once);
+    // per row and per column the summation order is unchanged (k ascending,
+    // rows ascending)
+    constexpr int R = kBetaRows / PREP_WARPS;
+    const float4* src[R];
+    float4* hi[R];
+    float4* lo[R];
+    bool ok[R];
+    double acc[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+        const long long row = (long long)blockIdx.x * kBetaRows + warp * R + i;
+        ok[i] = row < N;
+        const long long rr = ok[i] ? row : 0;
+        src[i] = reinterpret_cast<const float4*>(rr < m ? Xs + g * xs_gs + rr * d : Xt + g * xt_gs + (rr - m) * d);
+        const long long o = ((long long)g * N + rr) * d;
+        hi[i] = reinterpret_cast<float4*>(zhi + o);
+        lo[i] = reinterpret_cast<float4*>(zlo + o);
+        acc[i] = 0.0;
+    }
+    for (int k = lane; k < d4; k += 32) {
+        float4 x[R];
+#pragma unroll
+        for (int i = 0; i < R; ++i) x[i] = ok[i] ? src[i][k] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            if (!ok[i]) continue;
             float4 h, l;
-            split_tf32(x.x, h.x, l.x);
-            split_tf32(x.y, h.y, l.y);
-            split_tf32(x.z, h.z, l.z);
-            split_tf32(x.w, h.w, l.w);
-            hi[k] = h;
-            lo[k] = l;
-            acc += (double)x.x * (double)x.x + (double)x.y * (double)x.y;
-            acc += (double)x.z * (double)x.z + (double)x.w * (double)x.w;
-            if (cs) {  // lanes own disjoint columns: no races
-                cs[4 * k] += (double)x.x;
-                cs[4 * k + 1] += (double)x.y;
-                cs[4 * k + 2] += (double)x.z;
-                cs[4 * k + 3] += (double)x.w;
-            }
+            split_tf32(x[i].x, h.x, l.x);
+            split_tf32(x[i].y, h.y, l.y);
+            split_tf32(x[i].z, h.z, l.z);
+            split_tf32(x[i].w, h.w, l.w);
+            hi[i][k] = h;
+            lo[i][k] = l;
+            acc[i] += (double)x[i].x * (double)x[i].x + (double)x[i].y * (double)x[i].y;
+            acc[i] += (double)x[i].z * (double)x[i].z + (double)x[i].w * (double)x[i].w;
         }
-        for (int o2 = 16; o2 > 0; o2 >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o2);
-        if (lane == 0) norms[(long long)g * N + row] = (float)acc;
-        nacc += acc;
+        if (cs) {  // lanes own disjoint columns: no races
+            double c0 = cs[4 * k], c1 = cs[4 * k + 1], c2 = cs[4 * k + 2], c3 = cs[4 * k + 3];
+#pragma unroll
+            for (int i = 0; i < R; ++i) {
+                if (!ok[i]) continue;
+                c0 += (double)x[i].x;
+                c1 += (double)x[i].y;
+                c2 += (double)x[i].z;
+                c3 += (double)x[i].w;
+            }
+            cs[4 * k] = c0;
+            cs[4 * k + 1] = c1;
+            cs[4 * k + 2] = c2;
+            cs[4 * k + 3] = c3;
+        }
+    }
+    double nacc = 0.0;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+        double a2 = acc[i];
+        for (int o2 = 16; o2 > 0; o2 >>= 1) a2 += __shfl_xor_sync(0xffffffffu, a2, o2);
+        if (ok[i]) {
+            if (lane == 0) norms[(long long)g * N + (long long)blockIdx.x * kBetaRows + warp * R + i] = (float)a2;
+            nacc += a2;
+        }
     }
     if (!part) return;
     if (lane == 0) nsum[warp] = nacc;
