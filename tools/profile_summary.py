@@ -40,9 +40,9 @@ def phase_of(name):
         return "mmd_pairs"
     if "beta_" in name or "mmd_prep" in name:
         return "mmd_beta"
-    if "ce_kernel" in name or "row_sum" in name:
+    if "ce_kernel" in name or "row_sum" in name or "ce_loss" in name:
         return "ce"
-    if "bias_sgd" in name:
+    if "bias_sgd" in name or "bias_from_partials" in name:
         return "bias_sgd"
     return "other"
 
