@@ -370,6 +370,8 @@ int mtk_diag_gemm_tf32x3(mtk_ctx* c, int a_mn, int b_mn, int G, int M, int N, in
             if (e[0] == 's') {  // SGD against C as the master weight, lr = 1e-3
                 u.epi = Epi::kSgd;
                 u.lr = 1e-3f;
+            } else if (e[0] == 'n') {  // epilogue reads TMEM, writes nothing
+                u.epi = Epi::kNone;
             } else if (e[0] == 'm') {  // ReLU mask taken from C itself
                 u.epi = Epi::kMask;
                 u.mask = Cm;

@@ -108,6 +108,7 @@ enum class Epi : int {
     kMask = 2,      // C = (acc + add[m,n]) * (mask[m,n] > 0)      (dX through ReLU)
     kSgd = 3,       // C(=W) -= lr * acc ; optionally grad_out = acc  (dW + SGD)
     kStore = 4,     // C = acc (diagnostics)
+    kNone = 5,      // no output (diagnostics: epilogue without global traffic)
 };
 
 struct Gemm {

@@ -49,15 +49,15 @@ namespace {
 
 using namespace sm100;
 
-constexpr int BK = 32, LS = 4, LO = 2;
+constexpr int BK = 32, LS = 5, LO = 2;
 constexpr int TILE_BYTES = 128 * BK * 4;     // 16 KB: 128 rows (or cols) x 32 k
 constexpr int LOAD_BYTES = 2 * TILE_BYTES;   // load stage: A fp32, B fp32 (TMA bytes)
 constexpr int LO_BYTES = 2 * TILE_BYTES;     // lo stage: A lo, B lo
-constexpr int EPI_LD = 36;                          // transpose tile row stride (floats)
-constexpr int EPI_BYTES = 4 * 32 * EPI_LD * 4;      // one 32 x 32 tile per epilogue warp
-constexpr int SMEM_BYTES = LS * LOAD_BYTES + LO * LO_BYTES + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-constexpr int NUM_CONV_WARPS = 8;
-constexpr int NUM_THREADS = 192 + 32 * NUM_CONV_WARPS;
+constexpr int SMEM_BYTES = LS * LOAD_BYTES + LO * LO_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int NUM_EPI_WARPS = 8;   // two per TMEM lane quarter, each half the columns
+constexpr int NUM_CONV_WARPS = 4;
+constexpr int EPI_W0 = 2, CONV_W0 = EPI_W0 + NUM_EPI_WARPS;
+constexpr int NUM_THREADS = 32 * (CONV_W0 + NUM_CONV_WARPS);
 
 struct UmmaParams {
     CUtensorMap a, b;  // 3-D fp32 maps, coords (inner, outer, g)
@@ -166,135 +166,131 @@ __device__ __forceinline__ void mma_stage(uint32_t tmem, uint32_t base, uint32_t
     }
 }
 
-// TMEM accumulator (this warp's 32 lanes = rows m0+32q.., ncols columns) ->
-// fused epilogue -> fp32 C in HBM.  Per 32 x 32 chunk the warp transposes
-// through smem (thread = row after tcgen05.ld; then 8 threads x float4 per
-// row, 4 rows per instruction), so each global access instruction touches
-// four 128-B row segments instead of 32 rows' 16-B pieces; all operand loads
-// of a chunk (bias | mask, add | master weight) are in flight together.
-__device__ __forceinline__ void epilogue_tile(const UmmaParams& p, uint32_t tmem, int q, int lane,
-                                              int g, int m0, int n0, int ncols, uint32_t sb) {
+// 32 column values per lane (lane = row) -> lane j holds the sum over the
+// warp's 32 rows of column j.  Five butterfly steps, fixed order.
+__device__ __forceinline__ float column_sums_32(float (&v)[32], int lane) {
+#pragma unroll
+    for (int k = 16; k >= 1; k >>= 1) {
+        const bool up = (lane & k) != 0;
+#pragma unroll
+        for (int j = 0; j < k; ++j) {
+            const float send = up ? v[j] : v[j + k];
+            const float keep = up ? v[j + k] : v[j];
+            v[j] = keep + __shfl_xor_sync(0xffffffffu, send, k);
+        }
+    }
+    return v[0];
+}
+
+// TMEM accumulator -> fused epilogue -> fp32 C in HBM.  Thread = row (TMEM
+// lane); this warp covers the 32-column chunks [c0, c1).  Per chunk every
+// global operand load (bias | mask, add | master weight) is issued before the
+// TMEM read, so a chunk costs one memory round trip.  No shared memory: the
+// mainloop running on the other accumulator saturates the smem port.
+__device__ __forceinline__ void epilogue_rows(const UmmaParams& p, uint32_t tmem, int q, int lane,
+                                              int g, int m0, int n0, int c0, int c1) {
+    const int mw = m0 + 32 * q;
+    const int m = mw + lane;
+    const bool row_ok = m < p.M;
+    const long long rowbase = (long long)g * p.c_gs + (long long)m * p.ldc;
     const int epi = p.epi;
-    const int mw = m0 + 32 * q;       // first row of this warp
-    const int c4 = lane & 7;          // float4 column within the chunk
-    const int r0 = lane >> 3;         // row offset 0..3 (+4 i)
     bool bad = false;
 #pragma unroll 1
-    for (int c = 0; c < ncols / 32; ++c) {
+    for (int c = c0; c < c1; ++c) {
         const int nb = n0 + c * 32;
         if (nb >= p.N) break;  // warp-uniform
-        const int n = nb + 4 * c4;
-        const bool full4 = n + 4 <= p.N;
-        float4 o1[8], o2[8];
+        const bool vec = row_ok && (nb + 32 <= p.N) && ((rowbase + nb) % 4 == 0);
+        float4 o1[8], o2[8];  // prefetched operands of this chunk
+        if (vec) {
+            const float* s1 = nullptr;
+            const float* s2 = nullptr;
+            if (epi == (int)Epi::kBias || epi == (int)Epi::kBiasRelu) s1 = p.bias + g * p.bias_gs + nb;
+            else if (epi == (int)Epi::kMask) { s1 = p.mask + rowbase + nb; s2 = p.add ? p.add + rowbase + nb : nullptr; }
+            else if (epi == (int)Epi::kSgd) s1 = p.C + rowbase + nb;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int m = mw + r0 + 4 * i;
-            const long long idx = (long long)g * p.c_gs + (long long)m * p.ldc + n;
-            o1[i] = o2[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (m < p.M && full4) {
-                if (epi == (int)Epi::kMask) {
-                    o1[i] = *reinterpret_cast<const float4*>(p.mask + idx);
-                    if (p.add) o2[i] = *reinterpret_cast<const float4*>(p.add + idx);
-                } else if (epi == (int)Epi::kSgd) {
-                    o1[i] = *reinterpret_cast<const float4*>(p.C + idx);
-                }
+            for (int j = 0; j < 8; ++j) {
+                o1[j] = s1 ? *reinterpret_cast<const float4*>(s1 + 4 * j) : make_float4(0.f, 0.f, 0.f, 0.f);
+                o2[j] = s2 ? *reinterpret_cast<const float4*>(s2 + 4 * j) : make_float4(0.f, 0.f, 0.f, 0.f);
             }
         }
-        float4 bias = make_float4(0.f, 0.f, 0.f, 0.f);
-        if ((epi == (int)Epi::kBias || epi == (int)Epi::kBiasRelu) && full4)
-            bias = *reinterpret_cast<const float4*>(p.bias + g * p.bias_gs + n);
         float v[32];
         tmem_ld_32x32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(c * 32), v);
+        if (vec) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-            sts128(sb + (uint32_t)((lane * EPI_LD + 4 * j) * 4),
-                   make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
-        __syncwarp();
-        float4 cs = make_float4(0.f, 0.f, 0.f, 0.f);  // this thread's rows of 4 columns
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int r = r0 + 4 * i, m = mw + r;
-            if (m >= p.M) continue;
-            const long long idx = (long long)g * p.c_gs + (long long)m * p.ldc + n;
-            float4 x = lds128(sb + (uint32_t)((r * EPI_LD + 4 * c4) * 4));
-            if (!full4) {  // ragged right edge: scalar tail
-                const float xs[4] = {x.x, x.y, x.z, x.w};
-                for (int e = 0; e < 4 && n + e < p.N; ++e) {
-                    float y = xs[e];
-                    const long long ie = idx + e;
-                    if (epi == (int)Epi::kBias || epi == (int)Epi::kBiasRelu) {
-                        y += p.bias[g * p.bias_gs + n + e];
-                        bad |= !isfinite(y);
-                        if (epi == (int)Epi::kBiasRelu) y = y > 0.f ? y : 0.f;
-                    } else if (epi == (int)Epi::kMask) {
-                        if (p.add) y = p.add[ie] + y;
-                        y = (p.mask[ie] > 0.f) ? y : 0.f;
-                        if (e == 0) cs.x += y;
-                        else if (e == 1) cs.y += y;
-                        else if (e == 2) cs.z += y;
-                        else cs.w += y;
-                    } else if (epi == (int)Epi::kSgd) {
-                        if (p.grad_out) p.grad_out[ie] = y;
-                        y = p.C[ie] - p.lr * y;
-                        bad |= !isfinite(y);
+            for (int j = 0; j < 8; ++j) {
+                const long long idx = rowbase + nb + 4 * j;
+                float4 x = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                if (epi == (int)Epi::kBias || epi == (int)Epi::kBiasRelu) {
+                    x.x += o1[j].x;
+                    x.y += o1[j].y;
+                    x.z += o1[j].z;
+                    x.w += o1[j].w;
+                    bad |= !(isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w));
+                    if (epi == (int)Epi::kBiasRelu) {
+                        x.x = x.x > 0.f ? x.x : 0.f;
+                        x.y = x.y > 0.f ? x.y : 0.f;
+                        x.z = x.z > 0.f ? x.z : 0.f;
+                        x.w = x.w > 0.f ? x.w : 0.f;
                     }
-                    p.C[ie] = y;
+                } else if (epi == (int)Epi::kMask) {
+                    if (p.add) {
+                        x.x = o2[j].x + x.x;
+                        x.y = o2[j].y + x.y;
+                        x.z = o2[j].z + x.z;
+                        x.w = o2[j].w + x.w;
+                    }
+                    x.x = o1[j].x > 0.f ? x.x : 0.f;
+                    x.y = o1[j].y > 0.f ? x.y : 0.f;
+                    x.z = o1[j].z > 0.f ? x.z : 0.f;
+                    x.w = o1[j].w > 0.f ? x.w : 0.f;
+                } else if (epi == (int)Epi::kSgd) {  // C is the fp32 master weight
+                    if (p.grad_out) *reinterpret_cast<float4*>(p.grad_out + idx) = x;
+                    x.x = o1[j].x - p.lr * x.x;
+                    x.y = o1[j].y - p.lr * x.y;
+                    x.z = o1[j].z - p.lr * x.z;
+                    x.w = o1[j].w - p.lr * x.w;
+                    bad |= !(isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w));
                 }
-                continue;
+                if (epi != (int)Epi::kNone) *reinterpret_cast<float4*>(p.C + idx) = x;
+                v[4 * j] = x.x;  // kept for the column sums
+                v[4 * j + 1] = x.y;
+                v[4 * j + 2] = x.z;
+                v[4 * j + 3] = x.w;
             }
-            if (epi == (int)Epi::kBias || epi == (int)Epi::kBiasRelu) {
-                x.x += bias.x;
-                x.y += bias.y;
-                x.z += bias.z;
-                x.w += bias.w;
-                bad |= !(isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w));
-                if (epi == (int)Epi::kBiasRelu) {
-                    x.x = x.x > 0.f ? x.x : 0.f;
-                    x.y = x.y > 0.f ? x.y : 0.f;
-                    x.z = x.z > 0.f ? x.z : 0.f;
-                    x.w = x.w > 0.f ? x.w : 0.f;
-                }
-            } else if (epi == (int)Epi::kMask) {
-                if (p.add) {
-                    x.x = o2[i].x + x.x;
-                    x.y = o2[i].y + x.y;
-                    x.z = o2[i].z + x.z;
-                    x.w = o2[i].w + x.w;
-                }
-                x.x = o1[i].x > 0.f ? x.x : 0.f;
-                x.y = o1[i].y > 0.f ? x.y : 0.f;
-                x.z = o1[i].z > 0.f ? x.z : 0.f;
-                x.w = o1[i].w > 0.f ? x.w : 0.f;
-                cs.x += x.x;
-                cs.y += x.y;
-                cs.z += x.z;
-                cs.w += x.w;
-            } else if (epi == (int)Epi::kSgd) {  // C is the fp32 master weight
-                if (p.grad_out) *reinterpret_cast<float4*>(p.grad_out + idx) = x;
-                x.x = o1[i].x - p.lr * x.x;
-                x.y = o1[i].y - p.lr * x.y;
-                x.z = o1[i].z - p.lr * x.z;
-                x.w = o1[i].w - p.lr * x.w;
-                bad |= !(isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w));
-            }
-            *reinterpret_cast<float4*>(p.C + idx) = x;
-        }
-        if (p.colsum) {  // fixed-order reduction of the warp's 32 rows (lanes differ in r0)
+        } else {
 #pragma unroll
-            for (int o = 8; o <= 16; o <<= 1) {
-                cs.x += __shfl_xor_sync(0xffffffffu, cs.x, o);
-                cs.y += __shfl_xor_sync(0xffffffffu, cs.y, o);
-                cs.z += __shfl_xor_sync(0xffffffffu, cs.z, o);
-                cs.w += __shfl_xor_sync(0xffffffffu, cs.w, o);
-            }
-            if (r0 == 0 && mw < p.M) {
-                const int nrb = (p.M + 31) / 32;
-                float* o = p.colsum + ((long long)g * nrb + mw / 32) * p.N + n;
-                const float cv[4] = {cs.x, cs.y, cs.z, cs.w};
-                for (int e = 0; e < 4 && n + e < p.N; ++e) o[e] = cv[e];
+            for (int j = 0; j < 32; ++j) {
+                const int n = nb + j;
+                float x = v[j];
+                if (row_ok && n < p.N) {
+                    const long long idx = rowbase + n;
+                    if (epi == (int)Epi::kBias || epi == (int)Epi::kBiasRelu) {
+                        x += p.bias[g * p.bias_gs + n];
+                        bad |= !isfinite(x);
+                        if (epi == (int)Epi::kBiasRelu) x = x > 0.f ? x : 0.f;
+                    } else if (epi == (int)Epi::kMask) {
+                        if (p.add) x = p.add[idx] + x;
+                        x = (p.mask[idx] > 0.f) ? x : 0.f;
+                    } else if (epi == (int)Epi::kSgd) {
+                        if (p.grad_out) p.grad_out[idx] = x;
+                        x = p.C[idx] - p.lr * x;
+                        bad |= !isfinite(x);
+                    }
+                    if (epi != (int)Epi::kNone) p.C[idx] = x;
+                } else {
+                    x = 0.f;
+                }
+                v[j] = x;
             }
         }
-        __syncwarp();
+        if (p.colsum && epi == (int)Epi::kMask && mw < p.M) {
+            // per-32-row-block column sums of the stored values (next layer's db)
+            const float cs = column_sums_32(v, lane);
+            if (nb + lane < p.N) {
+                const int nrb = (p.M + 31) / 32;
+                p.colsum[((long long)g * nrb + mw / 32) * p.N + nb + lane] = cs;
+            }
+        }
     }
     if (bad && p.flags) atomicOr(p.flags, kFlagNonFinite);
 }
@@ -332,8 +328,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_kernel(const __grid_const
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* lo_ring = smem + LS * LOAD_BYTES;
-    uint8_t* epi_smem = lo_ring + LO * LO_BYTES;
-    uint64_t* full = reinterpret_cast<uint64_t*>(lo_ring + LO * LO_BYTES + EPI_BYTES);
+    uint64_t* full = reinterpret_cast<uint64_t*>(lo_ring + LO * LO_BYTES);
     uint64_t* empty = full + LS;
     uint64_t* conv = empty + LS;
     uint64_t* lofree = conv + LO;
@@ -366,7 +361,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_kernel(const __grid_const
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&acc_full[b], 1);
-            mbar_init(&acc_empty[b], NCTA * 4);  // one arrival per epilogue warp
+            mbar_init(&acc_empty[b], NCTA * NUM_EPI_WARPS);  // one arrival per epilogue warp
         }
         fence_barrier_init();
     }
@@ -448,9 +443,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_kernel(const __grid_const
                 __syncwarp();
             }
         }
-    } else if (warp < 6) {
+    } else if (warp < CONV_W0) {
         // ---------------- epilogue: own 128 rows x TN columns ----------------
         const int q = warp & 3;  // TMEM lane quarter this warp may access
+        const int hsel = (warp - EPI_W0) >> 2;  // which half of the tile's columns
         uint32_t tl = 0;
         for (int w = cid; w < nitems; w += ncl, ++tl) {
             const Item im = decode_item(p, w, tiles_m, tiles_n);
@@ -462,8 +458,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_kernel(const __grid_const
             mbar_wait(&acc_full[b], (tl >> 1) & 1);
             if (tr && threadIdx.x == 64 && tl < 16) tr[2000 + 2 * tl] = gtime();
             tc_fence_after();
-            epilogue_tile(p, tmem + b * TN, q, lane, g, m0, n0, ncols,
-                          smem_u32(epi_smem) + (uint32_t)(q * 32 * EPI_LD * 4));
+            const int nch = ncols / 32;
+            epilogue_rows(p, tmem + b * TN, q, lane, g, m0, n0, hsel * (nch / 2), (hsel + 1) * (nch / 2));
             tc_fence_before();
             __syncwarp();
             if (tr && threadIdx.x == 64 && tl < 16) tr[2001 + 2 * tl] = gtime();
@@ -474,7 +470,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_kernel(const __grid_const
         }
     } else {
         // ---------------- converters ----------------
-        const int ct = threadIdx.x - 192;
+        const int ct = threadIdx.x - 32 * CONV_W0;
         uint32_t it = 0;
         for (int w = cid; w < nitems; w += ncl) {
             for (int kb = 0; kb < nk; ++kb, ++it) {
