@@ -150,6 +150,24 @@ int mtk_bank_step_result(mtk_bank* bank, int which, double* loss_host, double* m
 int mtk_bank_tc_layers(mtk_bank* bank, int* out_host);
 /* zero the Adam moments and step count (a fresh mt::OptimizerState).       */
 int mtk_bank_reset_optimizer(mtk_bank* bank);
+/* nsteps training steps without host round trips: step s gathers its batch
+ * X[g, r] = X_pool[idx[s, g, r]] (and labels) on the device, then runs
+ * mtk_bank_train_step with `tmpl` (B, lr, options), w = w + s*G*B (or NULL)
+ * and denom[0] = denom0_host[s] (or tmpl's).  X_pool [pool_rows, dims[0]],
+ * y_pool [pool_rows], idx (int64) [nsteps, G, B], w [nsteps, G, B] on the
+ * device.  Synchronizing (reports bad labels / indices / non-finite).       */
+int mtk_bank_train_epoch(mtk_bank* bank, const mtk_step* tmpl, const float* X_pool,
+                         const int32_t* y_pool, int64_t pool_rows, const int64_t* idx,
+                         const float* w, const double* denom0_host, int nsteps);
+
+/* Batch assembly on the device (the sweep driver's batch_iter gather,
+ * SPEC.md:605-613): out[g, row0 + r, :] = src[idx[g * nb + r], :] for
+ * g < G, r < nb; src [src_rows, d] and idx (int64) [G, nb] on the device,
+ * out has out_rows rows per model.  4-byte elements are copied bitwise, so
+ * int32 labels use the same call with d = 1.  Bad indices -> ValueError at
+ * the next synchronizing call.                                              */
+int mtk_gather_rows(mtk_ctx* ctx, const void* src, int64_t src_rows, int d, const int64_t* idx,
+                    int G, int nb, void* out, int out_rows, int row0);
 /* debug/parity: keep the last step's parameter gradients (dW, db).          */
 int mtk_bank_set_keep_grads(mtk_bank* bank, int on);
 int mtk_bank_get_grads(mtk_bank* bank, int model, double* const* dW_host, double* const* db_host);

@@ -264,6 +264,24 @@ class Bank:
                                               self._mmd.ctypes.data_as(_dp)), "step_result")
         return self._loss.copy(), self._mmd.copy()
 
+    def train_epoch(self, X_pool, y_pool, idx, w=None, denom0=None, **kw):
+        """idx.shape[0] steps, each gathering X_pool[idx[s]] / y_pool[idx[s]] on
+        the device (idx int64 [steps, G, B]); w [steps, G, B] or None; denom0
+        per-step head-0 denominators (host) or None (kw's denom)."""
+        steps, G, B = idx.shape
+        if G != self.G:
+            raise errors.ShapeError(f"train_epoch: idx has {G} models, bank has {self.G}")
+        s = self.make_step(B, **kw)
+        dn = None
+        if denom0 is not None:
+            dn = np.ascontiguousarray(denom0, dtype=np.float64)
+            if dn.shape != (steps,):
+                raise errors.ShapeError("train_epoch: denom0 needs one value per step")
+        errors.check(lib.mtk_bank_train_epoch(self.h, C.byref(s), _ptr(X_pool), _ptr(y_pool),
+                                              X_pool.shape[0], _ptr(idx), _ptr(w),
+                                              dn.ctypes.data_as(_dp) if dn is not None else None,
+                                              steps), "train_epoch")
+
     def reset_optimizer(self):
         """zero the Adam moments and step count (a fresh OptimizerState)"""
         errors.check(lib.mtk_bank_reset_optimizer(self.h), "reset_optimizer")
@@ -322,6 +340,23 @@ def mmd_beta(ctx: Context, Xs, Xt) -> float:
 def mmd_value_from_sums(sums, m: int, n: int) -> float:
     ss, tt, st = sums
     return ss / (m * m) + tt / (n * n) - 2.0 * st / (m * n)
+
+
+def gather_rows(ctx: Context, src: torch.Tensor, idx: torch.Tensor, out: torch.Tensor = None,
+                row0: int = 0) -> torch.Tensor:
+    """out[g, row0 + r] = src[idx[g, r]] on the device (batch assembly).
+    src [rows, d] (float32 or int32), idx int64 [G, nb]; out [G, out_rows, d]
+    (allocated [G, nb, d] when None)."""
+    src2 = src.reshape(src.shape[0], -1)
+    G, nb = idx.shape
+    d = src2.shape[1]
+    if out is None:
+        out = torch.empty((G, nb) + tuple(src.shape[1:]), device=src.device, dtype=src.dtype)
+    if src.element_size() != 4 or out.element_size() != 4:
+        raise errors.ShapeError("gather_rows: 4-byte elements only")
+    errors.check(lib.mtk_gather_rows(ctx.h, _ptr(src2), src2.shape[0], d, _ptr(idx), G, nb,
+                                     _ptr(out), out.shape[1], row0), "gather_rows")
+    return out
 
 
 def softmax(ctx: Context, logits: torch.Tensor) -> torch.Tensor:

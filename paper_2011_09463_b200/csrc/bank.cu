@@ -408,7 +408,7 @@ void gemm_dw(mtk_bank& k, int mat, const Plane3& in, const Plane3& dz, int B, in
         adam.v = k.vW[mat];
     }
     // Adam on the GEMM paths: the epilogue stores the gradient, adam_apply updates
-    const bool adam_gemm = adam.on && (k.tc[k.layer_of(mat)] || !head_dw_ok(fo));
+    const bool adam_gemm = adam.on && (k.tc[k.layer_of(mat)] || (!head_dw_ok(fo) && !head_dw_ok(fi)));
     float* gbuf = nullptr;
     if (adam_gemm) {
         gbuf = k.keep_grads ? k.gW[mat] : k.adam_grad(mat);
@@ -437,18 +437,23 @@ void gemm_dw(mtk_bank& k, int mat, const Plane3& in, const Plane3& dz, int B, in
         launch_umma(u, c.stream);
         if (adam_gemm)
             launch_adam_apply(k.W[mat].f, gbuf, (long long)k.G * fi * fo, lr, adam, c.d_flags, c.stream);
-    } else if (head_dw_ok(fo)) {
+    } else if (head_dw_ok(fo) || head_dw_ok(fi)) {
+        // narrow output (the heads): reduce over rows with the fo-wide dZ as the
+        // register-blocked operand; narrow input (the attack model's k -> H
+        // layer): the same kernel on the transposed product dW^T = dZ^T X
+        const bool tr = !head_dw_ok(fo);
         HeadDw h;
         h.G = k.G;
         h.rows = rows;
-        h.K = fi;
-        h.N = fo;
-        h.A = in.f + (size_t)r0 * fi;
-        h.a_gs = (long long)B * fi;
-        h.lda = fi;
-        h.dZ = dz.f + (size_t)r0 * fo;
-        h.dz_gs = (long long)B * fo;
-        h.lddz = fo;
+        h.K = tr ? fo : fi;
+        h.N = tr ? fi : fo;
+        h.A = tr ? dz.f + (size_t)r0 * fo : in.f + (size_t)r0 * fi;
+        h.a_gs = (long long)B * (tr ? fo : fi);
+        h.lda = tr ? fo : fi;
+        h.dZ = tr ? in.f + (size_t)r0 * fi : dz.f + (size_t)r0 * fo;
+        h.dz_gs = (long long)B * (tr ? fi : fo);
+        h.lddz = tr ? fi : fo;
+        h.trans = tr ? 1 : 0;
         h.W = k.W[mat].f;
         h.w_gs = (long long)fi * fo;
         h.lr = lr;
@@ -898,6 +903,36 @@ int mtk_bank_train_step(mtk_bank* k, const mtk_step* s, double* loss_host, doubl
         check_bank(k);
         need(s != nullptr, MTK_VALUE_ERROR, "train_step: null step");
         train_step(*k, *s, loss_host, mmd_host);
+    });
+}
+
+int mtk_bank_train_epoch(mtk_bank* k, const mtk_step* tmpl, const float* X_pool, const int32_t* y_pool,
+                         int64_t pool_rows, const int64_t* idx, const float* w, const double* denom0,
+                         int nsteps) {
+    return guard([&] {
+        check_bank(k);
+        need(tmpl && X_pool && y_pool && idx, MTK_VALUE_ERROR, "train_epoch: null argument");
+        need(nsteps >= 0 && tmpl->B >= 1 && pool_rows >= 1, MTK_SHAPE_ERROR, "train_epoch: bad shape");
+        k->ensure_stage(tmpl->B);
+        Ctx& c = *k->ctx;
+        const int B = tmpl->B, G = k->G;
+        for (int s = 0; s < nsteps; ++s) {
+            const int64_t* ix = idx + (size_t)s * G * B;
+            launch_gather_rows(reinterpret_cast<const uint32_t*>(X_pool), pool_rows, k->dims[0],
+                               reinterpret_cast<const long long*>(ix), G, B,
+                               reinterpret_cast<uint32_t*>(k->Xs), B, 0, c.d_flags, c.stream);
+            launch_gather_rows(reinterpret_cast<const uint32_t*>(y_pool), pool_rows, 1,
+                               reinterpret_cast<const long long*>(ix), G, B,
+                               reinterpret_cast<uint32_t*>(k->ys), B, 0, c.d_flags, c.stream);
+            after_launch(c, 2);
+            mtk_step st = *tmpl;
+            st.X = k->Xs;
+            st.y = k->ys;
+            st.w = w ? w + (size_t)s * G * B : nullptr;
+            if (denom0) st.denom[0] = denom0[s];
+            train_step(*k, st, nullptr, nullptr);
+        }
+        c.check_flags();
     });
 }
 

@@ -65,6 +65,7 @@ void Ctx::check_flags() {
         MTK_CUDA(cudaMemsetAsync(d_flags, 0, sizeof(int), stream));
         MTK_CUDA(cudaStreamSynchronize(stream));
         if (f & kFlagBadLabel) fail(MTK_VALUE_ERROR, "label out of range [0, C)");
+        if (f & kFlagBadIndex) fail(MTK_VALUE_ERROR, "gather_rows: index out of range");
         fail(MTK_ERROR, "non-finite values produced on the device");
     }
 }
@@ -306,6 +307,19 @@ int mtk_mmd_gaussian_rows(mtk_ctx* c, const float* Xs, int64_t m, const float* X
 }
 
 // ---- attack stage ----------------------------------------------------------
+int mtk_gather_rows(mtk_ctx* c, const void* src, int64_t src_rows, int d, const int64_t* idx, int G,
+                    int nb, void* out, int out_rows, int row0) {
+    return guard([&] {
+        need(c && src && idx && out, MTK_VALUE_ERROR, "gather_rows: null argument");
+        need(d >= 1 && G >= 0 && nb >= 0 && src_rows >= 1, MTK_SHAPE_ERROR, "gather_rows: bad shape");
+        need(row0 >= 0 && row0 + nb <= out_rows, MTK_SHAPE_ERROR, "gather_rows: rows exceed out_rows");
+        launch_gather_rows(static_cast<const uint32_t*>(src), src_rows, d,
+                           reinterpret_cast<const long long*>(idx), G, nb, static_cast<uint32_t*>(out),
+                           out_rows, row0, c->d_flags, c->stream);
+        after_launch(*c);
+    });
+}
+
 int mtk_softmax(mtk_ctx* c, const float* logits, int64_t rows, int C, float* probs) {
     return guard([&] {
         need(c && logits && probs, MTK_VALUE_ERROR, "softmax: null argument");

@@ -27,7 +27,7 @@ struct Failure : std::runtime_error {
     } while (0)
 
 // Device-side deferred error bits (checked at synchronizing calls).
-enum : int { kFlagNonFinite = 1, kFlagBadLabel = 2 };
+enum : int { kFlagNonFinite = 1, kFlagBadLabel = 2, kFlagBadIndex = 4 };
 
 // Phases of the bank step, for optional CUDA-event timing (mtk_ctx_set_timing).
 enum Phase : int { kPhFwd = 0, kPhCe, kPhMmdBeta, kPhMmdPairs, kPhDx, kPhDw, kPhBias, kPhOther,
@@ -179,8 +179,9 @@ struct HeadDw {
     long long a_gs = 0, lda = 0;
     const float* dZ = nullptr; // [G][rows][N] (stride lddz)
     long long dz_gs = 0, lddz = 0;
-    float* W = nullptr;        // [G][K][N]
+    float* W = nullptr;        // [G][K][N]  ([G][N][K] with trans)
     long long w_gs = 0;
+    int trans = 0;             // W^T layout: the narrow operand is the layer input
     float lr = 0.f;
     AdamArgs adam;
     float* grad_out = nullptr;
@@ -279,6 +280,8 @@ void launch_mmd_pairs(const MmdArgs& a, cudaStream_t s);
 void launch_mmd_finish(const MmdArgs& a, double* value, double* sums3, cudaStream_t s);
 
 // attack stage
+void launch_gather_rows(const uint32_t* src, long long src_rows, int d, const long long* idx, int G,
+                        int nb, uint32_t* out, int out_rows, int row0, int* flags, cudaStream_t s);
 void launch_softmax(const float* logits, long long rows, int C, float* probs, cudaStream_t s);
 void launch_features(const float* logits, long long rows, int C, int k, const int32_t* labels,
                      float* feats, int* flags, cudaStream_t s);

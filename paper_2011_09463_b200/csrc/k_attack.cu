@@ -211,7 +211,38 @@ __global__ void auc_rank_sum(const uint8_t* v, const int* gid1, long long n, con
 
 inline unsigned nblocks(long long n, int t) { return (unsigned)((n + t - 1) / t); }
 
+// one warp per output row: a row-contiguous copy (16-B vectors when aligned)
+__global__ void gather_rows_kernel(const uint32_t* src, long long src_rows, int d, const long long* idx,
+                                   int G, int nb, uint32_t* out, int out_rows, int row0, int* flags) {
+    const long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= (long long)G * nb) return;
+    const int g = (int)(w / nb), r = (int)(w % nb);
+    const long long s = idx[w];
+    if (s < 0 || s >= src_rows) {
+        if (lane == 0) atomicOr(flags, kFlagBadIndex);
+        return;
+    }
+    const uint32_t* a = src + s * d;
+    uint32_t* o = out + ((long long)g * out_rows + row0 + r) * d;
+    if ((d & 3) == 0 && ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(o)) & 15) == 0) {
+        for (int k = lane; k < d / 4; k += 32)
+            reinterpret_cast<uint4*>(o)[k] = __ldg(reinterpret_cast<const uint4*>(a) + k);
+    } else {
+        for (int k = lane; k < d; k += 32) o[k] = __ldg(a + k);
+    }
+}
+
 }  // namespace
+
+void launch_gather_rows(const uint32_t* src, long long src_rows, int d, const long long* idx, int G,
+                        int nb, uint32_t* out, int out_rows, int row0, int* flags, cudaStream_t s) {
+    const long long rows = (long long)G * nb;
+    if (rows <= 0) return;
+    gather_rows_kernel<<<nblocks(rows * 32, 256), 256, 0, s>>>(src, src_rows, d, idx, G, nb, out, out_rows,
+                                                                 row0, flags);
+    count_launch();
+}
 
 void launch_softmax(const float* logits, long long rows, int C, float* probs, cudaStream_t s) {
     if (rows <= 0) return;

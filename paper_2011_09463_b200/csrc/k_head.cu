@@ -249,7 +249,7 @@ __global__ void head_dw_finish_kernel(HeadDw p) {
     const long long e = t % per;
     float gsum = 0.f;
     for (int rs = 0; rs < RS; ++rs) gsum += p.partial[((long long)rs * p.G + g) * per + e];
-    const long long idx = g * p.w_gs + e;
+    const long long idx = g * p.w_gs + (p.trans ? (e % p.N) * p.K + e / p.N : e);
     if (p.grad_out) p.grad_out[idx] = gsum;
     const float w = param_update(p.W[idx], gsum, p.lr, p.adam, idx);
     if (!isfinite(w) && p.flags) atomicOr(p.flags, kFlagNonFinite);

@@ -105,6 +105,14 @@ def synth(rng, C, d, n, mu, shift):
     return out[0], out[1]
 
 
+def host_gather(parts):
+    """[(X_pool, y_pool, idx[G][nb]), ...] -> X [G, sum nb, d], y [G, sum nb] (rows
+    concatenated in part order)."""
+    Xs = [np.stack([X[i] for i in idx]) for X, _, idx in parts]
+    ys = [np.stack([y[i] for i in idx]).astype(np.int32) for _, y, idx in parts]
+    return np.concatenate(Xs, axis=1), np.concatenate(ys, axis=1)
+
+
 def batches(order: np.ndarray, B: int):
     """batch_iter semantics: consecutive slices of the seeded order; the short
     last batch is padded with weight-0 duplicates."""
@@ -141,7 +149,41 @@ class GpuBackend:
         bank.init_params(g, rng)
 
     def to_dev(self, a):
+        if isinstance(a, self.torch.Tensor):
+            return a
         return self.torch.from_numpy(np.ascontiguousarray(a)).to(self.device)
+
+    def _pool(self, X, y):
+        if not hasattr(self, "_pools"):
+            self._pools = {}
+        key = (id(X), id(y))
+        if key not in self._pools:
+            self._pools[key] = (X, y, self.to_dev(np.ascontiguousarray(X, dtype=np.float32)),
+                                self.to_dev(np.ascontiguousarray(y, dtype=np.int32)))
+        return self._pools[key][2], self._pools[key][3]
+
+    def train_epoch(self, bank, X, y, idx, w, denom0, **kw):
+        Xd, yd = self._pool(X, y)
+        bank.train_epoch(Xd, yd, self.to_dev(np.ascontiguousarray(idx, dtype=np.int64)),
+                         self.to_dev(np.ascontiguousarray(w, dtype=np.float32)), denom0, **kw)
+
+    def gather(self, parts):
+        """Batch assembly on the device: parts = [(X_pool, y_pool, idx[G][nb]), ...]
+        concatenated along rows; pools are uploaded once (mtk_gather_rows)."""
+        torch = self.torch
+        G = len(parts[0][2])
+        rows = sum(len(p[2][0]) for p in parts)
+        d = parts[0][0].shape[1]
+        Xo = torch.empty((G, rows, d), device=self.device, dtype=torch.float32)
+        yo = torch.empty((G, rows), device=self.device, dtype=torch.int32)
+        r0 = 0
+        for X, y, idx in parts:
+            Xd, yd = self._pool(X, y)
+            ix = self.to_dev(np.ascontiguousarray(np.stack(idx), dtype=np.int64))
+            self.api.gather_rows(self.ctx, Xd, ix, Xo, r0)
+            self.api.gather_rows(self.ctx, yd, ix, yo.view(G, rows, 1), r0)
+            r0 += ix.shape[1]
+        return Xo, yo
 
     def step(self, bank, X, y, w, **kw):
         return bank.train_step(self.to_dev(X), self.to_dev(y), self.to_dev(w), want_loss=False,
@@ -179,10 +221,10 @@ def train_bank(be, cfg: SweepConfig, pop: Population, streams, models: list[int]
     B = cfg.batch
     d = cfg.dims[0]
 
+    gather_parts = getattr(be, "gather", None) or host_gather
+
     def gather(X, y, idx_per_model):
-        Xb = np.stack([X[i] for i in idx_per_model])
-        yb = np.stack([y[i] for i in idx_per_model]).astype(np.int32)
-        return Xb, yb
+        return gather_parts([(X, y, idx_per_model)])
 
     if cfg.paradigm == "model" and cfg.pretrain_epochs > 0:
         for _ in range(cfg.pretrain_epochs):
@@ -198,16 +240,14 @@ def train_bank(be, cfg: SweepConfig, pop: Population, streams, models: list[int]
         for t in range(len(orders[0])):
             idx = [mem[g][orders[g][t][0]] for g in range(G)]
             w = np.stack([orders[g][t][1] for g in range(G)])
-            Xb, yb = gather(pop.Xt, pop.yt, idx)
             if cfg.paradigm == "model":
+                Xb, yb = gather(pop.Xt, pop.yt, idx)
                 be.step(bank, Xb, yb, w, lr=cfg.lr, frozen_layers=cfg.frozen_layers,
                         denom=(float(w[0].sum()), 0.0), optimizer=cfg.optimizer)
                 continue
             # co-training: a source batch rides along with every member batch
             sidx = [src[g][(t * B + np.arange(B)) % cfg.source_per_model] for g in range(G)]
-            Xs_, ys_ = gather(pop.Xs, pop.ys, sidx)
-            Xc = np.concatenate([Xs_, Xb], axis=1)
-            yc = np.concatenate([ys_, yb], axis=1)
+            Xc, yc = gather_parts([(pop.Xs, pop.ys, sidx), (pop.Xt, pop.yt, idx)])
             wc = np.concatenate([np.ones_like(w), w], axis=1)
             if cfg.paradigm == "mapping":
                 be.step(bank, Xc, yc, wc, lr=cfg.lr, src_rows=B, mmd_lambda=cfg.mmd_lambda,
@@ -234,8 +274,18 @@ def train_attack(be, cfg, F_train, lab_train, rng):
     bank = be.bank(1, (cfg.k, cfg.attack_hidden, 2))
     be.init(bank, 0, rng)
     n = len(lab_train)
+    lab32 = np.ascontiguousarray(lab_train, dtype=np.int32)
+    epoch_fn = getattr(be, "train_epoch", None)
     for _ in range(cfg.attack_epochs):
-        for idx, w in batches(rng.permutation(n), cfg.attack_batch):
+        bl = batches(rng.permutation(n), cfg.attack_batch)
+        if epoch_fn is not None:  # the whole epoch in one library call
+            idx = np.stack([b[0] for b in bl])[:, None, :]
+            w = np.stack([b[1] for b in bl])[:, None, :]
+            epoch_fn(bank, F_train, lab32, idx, w,
+                     [float(b[1].sum()) for b in bl], lr=cfg.attack_lr,
+                     optimizer=cfg.attack_optimizer)
+            continue
+        for idx, w in bl:
             be.step(bank, F_train[idx][None], lab_train[idx][None].astype(np.int32), w[None],
                     lr=cfg.attack_lr, denom=(float(w.sum()), 0.0), optimizer=cfg.attack_optimizer)
     return bank

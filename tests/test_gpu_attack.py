@@ -74,3 +74,25 @@ def test_auc_errors(ctx):
 
     with pytest.raises(errors.ValueError):
         api.auc(ctx, torch.zeros(10, device="cuda"), torch.ones(10, dtype=torch.uint8, device="cuda"))
+
+
+def test_gather_rows_matches_indexing(ctx):
+    """mtk_gather_rows: device batch assembly (bitwise copies, row offsets)."""
+    from paper_2011_09463_b200 import api, errors
+
+    g = torch.Generator().manual_seed(3)
+    X = torch.randn(500, 37, generator=g).cuda()
+    y = torch.randint(0, 10, (500,), generator=g, dtype=torch.int32).cuda()
+    idx = torch.randint(0, 500, (4, 9), generator=g, dtype=torch.int64).cuda()
+    out = torch.zeros(4, 20, 37, device="cuda")
+    api.gather_rows(ctx, X, idx, out, row0=5)
+    assert torch.equal(out[:, 5:14], X[idx])
+    assert torch.equal(out[:, :5], torch.zeros_like(out[:, :5]))
+    yo = torch.zeros(4, 9, 1, device="cuda", dtype=torch.int32)
+    api.gather_rows(ctx, y, idx, yo)
+    assert torch.equal(yo[..., 0], y[idx])
+    bad = idx.clone()
+    bad[1, 2] = 500
+    api.gather_rows(ctx, X, bad, out, row0=5)
+    with pytest.raises(errors.ValueError):
+        ctx.synchronize()

@@ -154,6 +154,15 @@ def test_step_ragged_shapes_and_weights(ctx):
     check_step(bank, X, y, w=w, lr=0.3)
 
 
+def test_step_narrow_input_layer(ctx):
+    """fan_in <= 32 < fan_out (the attack model's k -> 64 layer): dW runs as the
+    transposed skinny reduction."""
+    dims = [5, 48, 3]
+    bank = make_bank(ctx, 3, dims)
+    X, y = inputs(3, 300, 5, 3)
+    check_step(bank, X, y, lr=0.2)
+
+
 def test_multi_step_trajectory(ctx):
     dims = [64, 32, 10]
     G = 3
@@ -172,7 +181,8 @@ def test_multi_step_trajectory(ctx):
 
 
 @pytest.mark.parametrize("dims,n_heads,frozen", [([784, 256, 10], 1, 0), ([100, 64, 32, 10], 1, 1),
-                                                 ([64, 48, 10], 2, 0), ([37, 19, 3], 1, 0)])
+                                                 ([64, 48, 10], 2, 0), ([37, 19, 3], 1, 0),
+                                                 ([3, 64, 2], 1, 0)])
 def test_adam_steps_match_oracle_update(ctx, dims, n_heads, frozen):
     """Adam (optim.hpp:49-63) in the dW/db epilogues: three steps; each step's
     parameters must equal the oracle Adam update (f64, its own moments) applied
