@@ -190,7 +190,8 @@ class GpuBackend:
                                **kw)
 
     def features(self, bank, X, head, k):
-        logits = bank.forward(self.to_dev(X), head=head)
+        X = self.to_dev(X)
+        logits = bank.forward(X, head=head)
         return self.api.posterior_features(self.ctx, logits, k).cpu().numpy().reshape(
             X.shape[0], X.shape[1], k)
 
@@ -263,7 +264,8 @@ def query_features(be, cfg, pop, bank, mem, non):
     returns feats [G, 2*members, k] and labels [2*members] (1 = member)."""
     head = 1 if cfg.paradigm == "parameter" else 0
     G = len(mem)
-    X = np.stack([np.concatenate([pop.Xt[mem[g]], pop.Xt[non[g]]]) for g in range(G)])
+    gather_parts = getattr(be, "gather", None) or host_gather
+    X, _ = gather_parts([(pop.Xt, pop.yt, [np.concatenate([mem[g], non[g]]) for g in range(G)])])
     F = be.features(bank, X, head, cfg.k)
     lab = np.concatenate([np.ones(cfg.members, np.uint8), np.zeros(cfg.members, np.uint8)])
     return F, lab
