@@ -38,6 +38,18 @@ struct ConfigError : Error {
 struct DataError : Error {
     using Error::Error;
 };
+struct CheckpointError : DataError {
+    using DataError::DataError;
+};
+struct VersionError : CheckpointError {
+    using CheckpointError::CheckpointError;
+};
+struct DigestError : CheckpointError {
+    using CheckpointError::CheckpointError;
+};
+struct TruncatedError : CheckpointError {
+    using CheckpointError::CheckpointError;
+};
 }  // namespace mt
 #define MT_GPU_HAVE_REFERENCE 0
 #endif
@@ -54,6 +66,10 @@ namespace gpu {
         case MTK_VALUE_ERROR: throw ValueError(msg);
         case MTK_CONFIG_ERROR: throw ConfigError(msg);
         case MTK_DATA_ERROR: throw DataError(msg);
+        case MTK_CHECKPOINT_ERROR: throw CheckpointError(msg);
+        case MTK_VERSION_ERROR: throw VersionError(msg);
+        case MTK_DIGEST_ERROR: throw DigestError(msg);
+        case MTK_TRUNCATED_ERROR: throw TruncatedError(msg);
         default: throw Error(msg);
     }
 }
@@ -154,6 +170,8 @@ class Bank {
         check(mtk_bank_train_step(h_, &s, loss.data(), mmd ? mmd->data() : nullptr), "train_step");
         return loss;
     }
+    // checkpoint / resume: bit-exact, Adam state included
+    void save(const std::string& path) { check(mtk_bank_save(h_, path.c_str()), "save"); }
     // a fresh Adam state (OptimizerState, optim.hpp:13-26): zero moments, step 0
     void reset_optimizer() { check(mtk_bank_reset_optimizer(h_), "reset_optimizer"); }
     void forward(const float* X, int B, float* logits, int head = 0, float* hidden = nullptr) {

@@ -39,6 +39,12 @@ extern "C" {
 #define MTK_CONFIG_ERROR 3
 #define MTK_DATA_ERROR 4
 #define MTK_ERROR 5
+/* checkpoint load failures (error.hpp:34-46: CheckpointError and its
+ * VersionError / DigestError / TruncatedError subclasses of DataError)      */
+#define MTK_CHECKPOINT_ERROR 6
+#define MTK_VERSION_ERROR 7
+#define MTK_DIGEST_ERROR 8
+#define MTK_TRUNCATED_ERROR 9
 
 typedef struct mtk_ctx mtk_ctx;
 typedef struct mtk_bank mtk_bank;
@@ -150,6 +156,21 @@ int mtk_bank_step_result(mtk_bank* bank, int which, double* loss_host, double* m
 int mtk_bank_tc_layers(mtk_bank* bank, int* out_host);
 /* zero the Adam moments and step count (a fresh mt::OptimizerState).       */
 int mtk_bank_reset_optimizer(mtk_bank* bank);
+
+/* ---- bank checkpoint / resume ------
+ * Text header (magic, format_version, config, payload size, SHA-256 of the
+ * payload) followed by length-prefixed named little-endian fp32 tensors:
+ * W<i>, b<i> per matrix and, once Adam has run, its moments m/v and step.
+ * load(save(bank)) is bit-exact, so training resumes identically.  Load
+ * errors: VersionError (names both versions), DigestError, TruncatedError,
+ * CheckpointError (malformed).                                             */
+int mtk_bank_save(mtk_bank* bank, const char* path);
+/* configuration of a bank (e.g. one made by mtk_bank_load); dims_out may be
+ * NULL (else n_layers + 1 entries), any other pointer may be NULL.          */
+int mtk_bank_info(mtk_bank* bank, int* G, int* n_layers, int* dims_out, int* n_heads);
+int mtk_bank_load(mtk_ctx* ctx, const char* path, mtk_bank** out);
+/* FIPS 180-4 SHA-256 of `len` bytes (host), 32 bytes out.                  */
+int mtk_sha256(const void* data, size_t len, uint8_t* out32);
 /* nsteps training steps without host round trips: step s gathers its batch
  * X[g, r] = X_pool[idx[s, g, r]] (and labels) on the device, then runs
  * mtk_bank_train_step with `tmpl` (B, lr, options), w = w + s*G*B (or NULL)

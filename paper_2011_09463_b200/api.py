@@ -157,6 +157,28 @@ class Bank:
         self._loss = np.zeros(G)
         self._mmd = np.zeros(G)
 
+    @classmethod
+    def load(cls, ctx: Context, path: str) -> "Bank":
+        """A bank restored from a checkpoint written by save() (bit-exact)."""
+        h = C.c_void_p()
+        errors.check(lib.mtk_bank_load(ctx.h, str(path).encode(), C.byref(h)), "load")
+        G, L, heads = C.c_int(), C.c_int(), C.c_int()
+        errors.check(lib.mtk_bank_info(h, C.byref(G), C.byref(L), None, C.byref(heads)))
+        dims = (C.c_int * (L.value + 1))()
+        errors.check(lib.mtk_bank_info(h, None, None, dims, None))
+        self = cls.__new__(cls)
+        self.ctx, self.G, self.dims, self.n_heads = ctx, G.value, list(dims), heads.value
+        self.L = L.value
+        self.n_mats = self.L + self.n_heads - 1
+        self.h = h
+        self._loss = np.zeros(self.G)
+        self._mmd = np.zeros(self.G)
+        return self
+
+    def save(self, path: str):
+        """Checkpoint parameters (and Adam state) to `path`."""
+        errors.check(lib.mtk_bank_save(self.h, str(path).encode()), "save")
+
     def __del__(self):
         try:
             lib.mtk_bank_destroy(self.h)
@@ -340,6 +362,14 @@ def mmd_beta(ctx: Context, Xs, Xt) -> float:
 def mmd_value_from_sums(sums, m: int, n: int) -> float:
     ss, tt, st = sums
     return ss / (m * m) + tt / (n * n) - 2.0 * st / (m * n)
+
+
+def sha256(data: bytes) -> bytes:
+    """FIPS 180-4 SHA-256 (the checkpoint digest)."""
+    out = (C.c_uint8 * 32)()
+    buf = C.create_string_buffer(bytes(data), len(data))
+    errors.check(lib.mtk_sha256(buf, len(data), out))
+    return bytes(out)
 
 
 def gather_rows(ctx: Context, src: torch.Tensor, idx: torch.Tensor, out: torch.Tensor = None,

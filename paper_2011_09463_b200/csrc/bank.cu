@@ -1073,3 +1073,236 @@ int mtk_bank_tc_layers(mtk_bank* k, int* out_host) {
 }
 
 }  // extern "C"
+
+// ---- checkpoint / resume ---------------------------------------------------
+namespace {
+
+constexpr int kCkptVersion = 1;
+const char kCkptMagic[] = "MTKBANK";
+
+std::string hex32(const uint8_t* d) {
+    static const char* x = "0123456789abcdef";
+    std::string s;
+    for (int i = 0; i < 32; ++i) {
+        s += x[d[i] >> 4];
+        s += x[d[i] & 15];
+    }
+    return s;
+}
+
+void put_u32(std::string& o, uint32_t v) {
+    for (int i = 0; i < 4; ++i) o += (char)((v >> (8 * i)) & 0xff);
+}
+void put_u64(std::string& o, uint64_t v) {
+    for (int i = 0; i < 8; ++i) o += (char)((v >> (8 * i)) & 0xff);
+}
+// little-endian fp32 record: name, rank, dims, byte count, data
+void put_tensor(std::string& o, const std::string& name, const std::vector<uint64_t>& shape,
+                const std::vector<float>& v) {
+    put_u32(o, (uint32_t)name.size());
+    o += name;
+    put_u32(o, (uint32_t)shape.size());
+    for (uint64_t d : shape) put_u64(o, d);
+    put_u64(o, (uint64_t)v.size() * 4);
+    for (float f : v) {
+        uint32_t u;
+        std::memcpy(&u, &f, 4);
+        put_u32(o, u);
+    }
+}
+
+struct Reader {
+    const std::string& s;
+    size_t pos;
+    uint32_t u32() {
+        need(pos + 4 <= s.size(), MTK_CHECKPOINT_ERROR, "checkpoint: record overruns the payload");
+        uint32_t v = 0;
+        for (int i = 0; i < 4; ++i) v |= (uint32_t)(uint8_t)s[pos + i] << (8 * i);
+        pos += 4;
+        return v;
+    }
+    uint64_t u64() {
+        const uint64_t lo = u32(), hi = u32();
+        return lo | (hi << 32);
+    }
+    // the next record, which must be `name` with `shape`
+    void tensor(const std::string& name, const std::vector<uint64_t>& shape, std::vector<float>& out) {
+        const uint32_t nl = u32();
+        need(pos + nl <= s.size(), MTK_CHECKPOINT_ERROR, "checkpoint: record overruns the payload");
+        const std::string got = s.substr(pos, nl);
+        pos += nl;
+        need(got == name, MTK_CHECKPOINT_ERROR, "checkpoint: expected tensor " + name + ", found " + got);
+        const uint32_t rank = u32();
+        need(rank == shape.size(), MTK_CHECKPOINT_ERROR, "checkpoint: rank mismatch for " + name);
+        size_t n = 1;
+        for (uint64_t d : shape) {
+            need(u64() == d, MTK_CHECKPOINT_ERROR, "checkpoint: shape mismatch for " + name);
+            n *= d;
+        }
+        need(u64() == n * 4, MTK_CHECKPOINT_ERROR, "checkpoint: byte count mismatch for " + name);
+        out.resize(n);
+        for (size_t i = 0; i < n; ++i) {
+            const uint32_t u = u32();
+            std::memcpy(&out[i], &u, 4);
+        }
+    }
+};
+
+std::vector<float> d2h(const float* d, size_t n, cudaStream_t s) {
+    std::vector<float> h(n);
+    MTK_CUDA(cudaMemcpyAsync(h.data(), d, n * 4, cudaMemcpyDeviceToHost, s));
+    MTK_CUDA(cudaStreamSynchronize(s));
+    return h;
+}
+
+}  // namespace
+
+int mtk_bank_save(mtk_bank* k, const char* path) {
+    return guard([&] {
+        check_bank(k);
+        need(path != nullptr, MTK_VALUE_ERROR, "save: null path");
+        Ctx& c = *k->ctx;
+        c.check_flags();
+        std::string pay;
+        const bool adam = !k->mW.empty();
+        for (int i = 0; i < k->n_mats; ++i) {
+            const uint64_t G = k->G, fi = k->fan_in(i), fo = k->fan_out(i);
+            const std::string n = std::to_string(i);
+            put_tensor(pay, "W" + n, {G, fi, fo}, d2h(k->W[i].f, G * fi * fo, c.stream));
+            put_tensor(pay, "b" + n, {G, fo}, d2h(k->b[i], G * fo, c.stream));
+            if (adam) {
+                put_tensor(pay, "mW" + n, {G, fi, fo}, d2h(k->mW[i], G * fi * fo, c.stream));
+                put_tensor(pay, "vW" + n, {G, fi, fo}, d2h(k->vW[i], G * fi * fo, c.stream));
+                put_tensor(pay, "mb" + n, {G, fo}, d2h(k->mb[i], G * fo, c.stream));
+                put_tensor(pay, "vb" + n, {G, fo}, d2h(k->vb[i], G * fo, c.stream));
+            }
+        }
+        uint8_t dg[32];
+        sha256(pay.data(), pay.size(), dg);
+        std::string hdr = std::string(kCkptMagic) + " " + std::to_string(kCkptVersion) + "\n";
+        hdr += "G " + std::to_string(k->G) + "\n";
+        hdr += "dims";
+        for (int v : k->dims) hdr += " " + std::to_string(v);
+        hdr += "\nheads " + std::to_string(k->n_heads) + "\n";
+        hdr += "adam " + std::to_string(adam ? 1 : 0) + " " + std::to_string(k->adam_t) + "\n";
+        hdr += "payload " + std::to_string(pay.size()) + "\n";
+        hdr += "sha256 " + hex32(dg) + "\n\n";
+        FILE* f = std::fopen(path, "wb");
+        need(f != nullptr, MTK_DATA_ERROR, std::string("save: cannot open ") + path);
+        const bool ok = std::fwrite(hdr.data(), 1, hdr.size(), f) == hdr.size() &&
+                        std::fwrite(pay.data(), 1, pay.size(), f) == pay.size();
+        std::fclose(f);
+        need(ok, MTK_DATA_ERROR, std::string("save: write failed for ") + path);
+    });
+}
+
+int mtk_bank_load(mtk_ctx* c, const char* path, mtk_bank** out) {
+    return guard([&] {
+        need(c && path && out, MTK_VALUE_ERROR, "load: null argument");
+        *out = nullptr;
+        FILE* f = std::fopen(path, "rb");
+        need(f != nullptr, MTK_DATA_ERROR, std::string("load: cannot open ") + path);
+        std::string all;
+        char buf[1 << 16];
+        size_t got;
+        while ((got = std::fread(buf, 1, sizeof(buf), f)) > 0) all.append(buf, got);
+        std::fclose(f);
+        const size_t he = all.find("\n\n");
+        need(he != std::string::npos, MTK_TRUNCATED_ERROR, "checkpoint: truncated header");
+        std::vector<std::string> lines;
+        for (size_t p = 0; p < he;) {
+            const size_t e = all.find('\n', p);
+            lines.push_back(all.substr(p, (e == std::string::npos || e > he ? he : e) - p));
+            p = (e == std::string::npos) ? he : e + 1;
+        }
+        auto words = [](const std::string& l) {
+            std::vector<std::string> w;
+            size_t p = 0;
+            while (p < l.size()) {
+                const size_t e = l.find(' ', p);
+                const size_t q = e == std::string::npos ? l.size() : e;
+                if (q > p) w.push_back(l.substr(p, q - p));
+                p = q + 1;
+            }
+            return w;
+        };
+        need(!lines.empty(), MTK_CHECKPOINT_ERROR, "checkpoint: empty header");
+        auto l0 = words(lines[0]);
+        need(l0.size() == 2 && l0[0] == kCkptMagic, MTK_CHECKPOINT_ERROR, "checkpoint: not a bank checkpoint");
+        const int ver = std::atoi(l0[1].c_str());
+        need(ver == kCkptVersion, MTK_VERSION_ERROR,
+             "checkpoint: format_version " + l0[1] + " in file, this library reads version " +
+                 std::to_string(kCkptVersion));
+        int G = 0, heads = 0, adam = 0;
+        unsigned long long adam_t = 0, paybytes = 0;
+        std::vector<int> dims;
+        std::string digest;
+        for (size_t i = 1; i < lines.size(); ++i) {
+            auto w = words(lines[i]);
+            if (w.empty()) continue;
+            if (w[0] == "G" && w.size() == 2) G = std::atoi(w[1].c_str());
+            else if (w[0] == "dims")
+                for (size_t j = 1; j < w.size(); ++j) dims.push_back(std::atoi(w[j].c_str()));
+            else if (w[0] == "heads" && w.size() == 2) heads = std::atoi(w[1].c_str());
+            else if (w[0] == "adam" && w.size() == 3) {
+                adam = std::atoi(w[1].c_str());
+                adam_t = std::strtoull(w[2].c_str(), nullptr, 10);
+            } else if (w[0] == "payload" && w.size() == 2) paybytes = std::strtoull(w[1].c_str(), nullptr, 10);
+            else if (w[0] == "sha256" && w.size() == 2) digest = w[1];
+        }
+        need(G >= 1 && dims.size() >= 2 && (heads == 1 || heads == 2) && digest.size() == 64,
+             MTK_CHECKPOINT_ERROR, "checkpoint: malformed header");
+        const std::string pay = all.substr(he + 2);
+        need(pay.size() >= paybytes, MTK_TRUNCATED_ERROR,
+             "checkpoint: truncated payload (" + std::to_string(pay.size()) + " of " +
+                 std::to_string(paybytes) + " bytes)");
+        need(pay.size() == paybytes, MTK_CHECKPOINT_ERROR, "checkpoint: trailing bytes after the payload");
+        uint8_t dg[32];
+        sha256(pay.data(), pay.size(), dg);
+        need(hex32(dg) == digest, MTK_DIGEST_ERROR, "checkpoint: payload SHA-256 mismatch");
+        mtk_bank* k = nullptr;
+        const int st = mtk_bank_create(c, G, (int)dims.size() - 1, dims.data(), heads, &k);
+        if (st != MTK_OK) fail(st, mtk_last_error());
+        std::unique_ptr<mtk_bank> own(k);
+        Reader rd{pay, 0};
+        std::vector<float> v;
+        Ctx& cx = *k->ctx;
+        auto h2d = [&](float* d) {
+            MTK_CUDA(cudaMemcpyAsync(d, v.data(), v.size() * 4, cudaMemcpyHostToDevice, cx.stream));
+            MTK_CUDA(cudaStreamSynchronize(cx.stream));
+        };
+        if (adam) k->ensure_adam();
+        for (int i = 0; i < k->n_mats; ++i) {
+            const uint64_t g = k->G, fi = k->fan_in(i), fo = k->fan_out(i);
+            const std::string n = std::to_string(i);
+            rd.tensor("W" + n, {g, fi, fo}, v);
+            h2d(k->W[i].f);
+            rd.tensor("b" + n, {g, fo}, v);
+            h2d(k->b[i]);
+            if (adam) {
+                rd.tensor("mW" + n, {g, fi, fo}, v);
+                h2d(k->mW[i]);
+                rd.tensor("vW" + n, {g, fi, fo}, v);
+                h2d(k->vW[i]);
+                rd.tensor("mb" + n, {g, fo}, v);
+                h2d(k->mb[i]);
+                rd.tensor("vb" + n, {g, fo}, v);
+                h2d(k->vb[i]);
+            }
+        }
+        need(rd.pos == pay.size(), MTK_CHECKPOINT_ERROR, "checkpoint: unexpected records after the last tensor");
+        k->adam_t = adam_t;
+        *out = own.release();
+    });
+}
+
+int mtk_bank_info(mtk_bank* k, int* G, int* n_layers, int* dims_out, int* n_heads) {
+    return guard([&] {
+        check_bank(k);
+        if (G) *G = k->G;
+        if (n_layers) *n_layers = k->L;
+        if (dims_out)
+            for (size_t i = 0; i < k->dims.size(); ++i) dims_out[i] = k->dims[i];
+        if (n_heads) *n_heads = k->n_heads;
+    });
+}

@@ -18,6 +18,7 @@ struct Failure : std::runtime_error {
     Failure(int s, const std::string& m) : std::runtime_error(m), status(s) {}
 };
 [[noreturn]] inline void fail(int s, const std::string& m) { throw Failure(s, m); }
+void sha256(const void* data, size_t len, uint8_t out[32]);
 
 #define MTK_CUDA(call)                                                                   \
     do {                                                                                 \
@@ -321,6 +322,9 @@ inline int guard(F&& f) {
 }
 
 inline void need(bool ok, int status, const char* msg) {
+    if (!ok) fail(status, msg);
+}
+inline void need(bool ok, int status, const std::string& msg) {
     if (!ok) fail(status, msg);
 }
 

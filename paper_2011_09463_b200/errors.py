@@ -1,7 +1,8 @@
 """Error taxonomy of the reference (error.hpp:10-51) as Python exceptions.
 
 C-ABI status codes map onto these classes: 1 ShapeError, 2 ValueError,
-3 ConfigError, 4 DataError, 5 Error.  ``ValueError`` also derives from the
+3 ConfigError, 4 DataError, 5 Error, 6 CheckpointError, 7 VersionError,
+8 DigestError, 9 TruncatedError.  ``ValueError`` also derives from the
 builtin so idiomatic ``except ValueError`` keeps working.
 """
 import builtins
@@ -27,7 +28,24 @@ class DataError(Error):
     """mt::DataError (error.hpp:31-33): problems with input data."""
 
 
-_BY_STATUS = {1: ShapeError, 2: ValueError, 3: ConfigError, 4: DataError, 5: Error}
+class CheckpointError(DataError):
+    """mt::CheckpointError (error.hpp:34-37): checkpoint load failures."""
+
+
+class VersionError(CheckpointError):
+    """mt::VersionError (error.hpp:38-40): unsupported format_version."""
+
+
+class DigestError(CheckpointError):
+    """mt::DigestError (error.hpp:41-43): payload SHA-256 mismatch."""
+
+
+class TruncatedError(CheckpointError):
+    """mt::TruncatedError (error.hpp:44-46): file shorter than its header says."""
+
+
+_BY_STATUS = {1: ShapeError, 2: ValueError, 3: ConfigError, 4: DataError, 5: Error,
+              6: CheckpointError, 7: VersionError, 8: DigestError, 9: TruncatedError}
 
 
 def check(status: int, what: str = "") -> None:
