@@ -324,18 +324,154 @@ def run_sweep(cfg: SweepConfig, be=None, *, rank: int = 0, world: int = 1,
             "config": dataclasses.asdict(cfg)}
 
 
-def main(argv=None):
+# --------------------------------------------------------------------------- config / report
+# Strict-JSON sweep configuration, metrics report and exit codes (SURVEY.md
+# 8(f) f4, after SPEC.md:656-665, 686-697): unknown keys are rejected with a
+# nearest-name suggestion, every violation is reported (not just the first),
+# the resolved config (defaults injected) is echoed, and the report carries a
+# digest of the resolved config.  Exit codes: 0 ok, 2 config, 3 data, 4 other.
+REPORT_VERSION = 1
+
+
+def _edit_distance(a: str, b: str) -> int:
+    d = list(range(len(b) + 1))
+    for i, ca in enumerate(a, 1):
+        prev, d[0] = d[0], i
+        for j, cb in enumerate(b, 1):
+            prev, d[j] = d[j], min(d[j] + 1, d[j - 1] + 1, prev + (ca != cb))
+    return d[-1]
+
+
+def resolve_config(doc: dict) -> SweepConfig:
+    """Strictly validate a JSON document into a SweepConfig (raises
+    ConfigError listing every violation)."""
+    from .errors import ConfigError
+
+    if not isinstance(doc, dict):
+        raise ConfigError("sweep config: the document must be a JSON object")
+    fields = {f.name: f for f in dataclasses.fields(SweepConfig)}
+    errs = []
+    for k in doc:
+        if k not in fields:
+            near = min(fields, key=lambda f: _edit_distance(k, f))
+            errs.append(f"unknown key {k!r} (did you mean {near!r}?)")
+    kw = {}
+    for name, f in fields.items():
+        if name not in doc:
+            continue
+        v = doc[name]
+        default = f.default
+        if isinstance(default, bool) or not isinstance(default, (int, float, str, tuple)):
+            kw[name] = v
+            continue
+        if isinstance(default, tuple):
+            if not (isinstance(v, list) and all(isinstance(x, int) and not isinstance(x, bool) for x in v)):
+                errs.append(f"{name}: expected a list of integers")
+                continue
+            kw[name] = tuple(v)
+        elif isinstance(default, str):
+            if not isinstance(v, str):
+                errs.append(f"{name}: expected a string")
+                continue
+            kw[name] = v
+        elif isinstance(default, int):
+            if not (isinstance(v, int) and not isinstance(v, bool)):
+                errs.append(f"{name}: expected an integer")
+                continue
+            kw[name] = v
+        else:
+            if not isinstance(v, (int, float)) or isinstance(v, bool):
+                errs.append(f"{name}: expected a number")
+                continue
+            kw[name] = float(v)
+    cfg = None
+    if not errs:
+        cfg = SweepConfig(**kw)
+        try:
+            cfg.validate()
+        except ConfigError as e:
+            errs.append(str(e))
+    if errs:
+        raise ConfigError("sweep config: " + "; ".join(errs))
+    return cfg
+
+
+def resolved_dict(cfg: SweepConfig) -> dict:
+    return {k: list(v) if isinstance(v, tuple) else v for k, v in dataclasses.asdict(cfg).items()}
+
+
+def config_digest(cfg: SweepConfig) -> str:
+    import hashlib
+
+    canon = json.dumps(resolved_dict(cfg), sort_keys=True, separators=(",", ":"))
+    return hashlib.sha256(canon.encode()).hexdigest()
+
+
+def metrics_report(cfg: SweepConfig, result: dict, seconds: float) -> dict:
+    """Deterministic fields first; only `wall_clock_seconds` varies between runs."""
+    return {"report_version": REPORT_VERSION, "paradigm": cfg.paradigm,
+            "auc": result["auc"], "accuracy": result["accuracy"], "models": result["models"],
+            "n_queries": result["n_queries"], "config_digest": config_digest(cfg),
+            "wall_clock_seconds": seconds}
+
+
+EXIT_OK, EXIT_CONFIG, EXIT_DATA, EXIT_INTERNAL = 0, 2, 3, 4
+
+
+def main(argv=None) -> int:
+    """python -m paper_2011_09463_b200.sweep --config cfg.json [--output DIR]
+    (or the quick flags); prints the metrics report; returns the exit code."""
     import argparse
+    import os
+    import sys
+    import time
+
+    from .errors import ConfigError, DataError
 
     ap = argparse.ArgumentParser(description="shadow-model membership-inference sweep")
-    ap.add_argument("--paradigm", default="model", choices=["model", "mapping", "parameter"])
-    ap.add_argument("--shadows", type=int, default=4)
-    ap.add_argument("--epochs", type=int, default=10)
-    ap.add_argument("--seed", type=int, default=20110946)
+    ap.add_argument("--config", help="strict JSON SweepConfig document")
+    ap.add_argument("--output", help="directory for metrics.json and resolved_config.json")
+    ap.add_argument("--paradigm", choices=["model", "mapping", "parameter"])
+    ap.add_argument("--shadows", type=int)
+    ap.add_argument("--epochs", type=int)
+    ap.add_argument("--seed", type=int)
     a = ap.parse_args(argv)
-    cfg = SweepConfig(paradigm=a.paradigm, n_shadows=a.shadows, epochs=a.epochs, seed=a.seed)
-    print(json.dumps(run_sweep(cfg)))
+    try:
+        doc = {}
+        if a.config:
+            try:
+                with open(a.config) as f:
+                    doc = json.load(f)
+            except OSError as e:
+                raise DataError(f"sweep config: cannot read {a.config}: {e}") from e
+            except json.JSONDecodeError as e:
+                raise ConfigError(f"sweep config: not valid JSON: {e}") from e
+        for flag, key in (("paradigm", "paradigm"), ("shadows", "n_shadows"), ("epochs", "epochs"),
+                          ("seed", "seed")):
+            if getattr(a, flag) is not None:  # flag > file > default
+                doc[key] = getattr(a, flag)
+        cfg = resolve_config(doc)
+        t0 = time.perf_counter()
+        result = run_sweep(cfg)
+        report = metrics_report(cfg, result, time.perf_counter() - t0)
+        if a.output:
+            os.makedirs(a.output, exist_ok=True)
+            with open(os.path.join(a.output, "resolved_config.json"), "w") as f:
+                json.dump(resolved_dict(cfg), f, indent=1, sort_keys=True)
+            with open(os.path.join(a.output, "metrics.json"), "w") as f:
+                json.dump(report, f, indent=1)
+        print(json.dumps(report))
+        return EXIT_OK
+    except ConfigError as e:
+        print(f"config error: {e}", file=sys.stderr)
+        return EXIT_CONFIG
+    except DataError as e:
+        print(f"data error: {e}", file=sys.stderr)
+        return EXIT_DATA
+    except Exception as e:  # noqa: BLE001 - internal invariant violation
+        print(f"internal error: {type(e).__name__}: {e}", file=sys.stderr)
+        return EXIT_INTERNAL
 
 
 if __name__ == "__main__":
-    main()
+    raise SystemExit(main())

@@ -113,3 +113,43 @@ def test_sweep_gpu_matches_oracle_auc_adam(paradigm):
     o = run_sweep(SweepConfig(paradigm=paradigm, **kw), OracleBackend())
     assert abs(g["auc"] - o["auc"]) <= 0.01, (g["auc"], o["auc"])
     assert abs(g["accuracy"] - o["accuracy"]) <= 0.01, (g["accuracy"], o["accuracy"])
+
+
+# ----------------------------------------------------------- strict config (8(f) f4)
+def test_resolve_config_strict_and_aggregated():
+    from paper_2011_09463_b200.errors import ConfigError
+    from paper_2011_09463_b200.sweep import SweepConfig, config_digest, resolve_config, resolved_dict
+
+    cfg = resolve_config({"paradigm": "mapping", "n_shadows": 3})
+    assert cfg.paradigm == "mapping" and cfg.n_shadows == 3
+    assert resolved_dict(cfg)["epochs"] == SweepConfig().epochs  # defaults echoed
+    assert config_digest(cfg) == config_digest(resolve_config({"paradigm": "mapping", "n_shadows": 3}))
+    with pytest.raises(ConfigError, match="epcohs.*did you mean 'epochs'.*lr: expected a number"):
+        resolve_config({"epcohs": 3, "lr": "fast"})
+    with pytest.raises(ConfigError, match="unknown paradigm"):
+        resolve_config({"paradigm": "magic"})
+
+
+def test_sweep_main_exit_codes(tmp_path, monkeypatch):
+    from paper_2011_09463_b200 import sweep as sw
+
+    bad = tmp_path / "bad.json"
+    bad.write_text('{"shadows": 2}')
+    assert sw.main(["--config", str(bad)]) == sw.EXIT_CONFIG
+    assert sw.main(["--config", str(tmp_path / "missing.json")]) == sw.EXIT_DATA
+    broken = tmp_path / "broken.json"
+    broken.write_text("{not json")
+    assert sw.main(["--config", str(broken)]) == sw.EXIT_CONFIG
+    # a run on the oracle backend: report written, deterministic except wall clock
+    ok = tmp_path / "ok.json"
+    import json as _json
+    ok.write_text(_json.dumps(dict(TINY, paradigm="model")))
+    monkeypatch.setattr(sw, "run_sweep", lambda cfg: run_sweep(cfg, OracleBackend()))
+    out = tmp_path / "out"
+    assert sw.main(["--config", str(ok), "--output", str(out)]) == sw.EXIT_OK
+    r1 = _json.loads((out / "metrics.json").read_text())
+    assert sw.main(["--config", str(ok), "--output", str(out)]) == sw.EXIT_OK
+    r2 = _json.loads((out / "metrics.json").read_text())
+    r1.pop("wall_clock_seconds"), r2.pop("wall_clock_seconds")
+    assert r1 == r2 and 0.0 <= r1["auc"] <= 1.0
+    assert _json.loads((out / "resolved_config.json").read_text())["paradigm"] == "model"
