@@ -193,6 +193,31 @@ int mtk_gather_rows(mtk_ctx* ctx, const void* src, int64_t src_rows, int d, cons
 int mtk_bank_set_keep_grads(mtk_bank* bank, int on);
 int mtk_bank_get_grads(mtk_bank* bank, int model, double* const* dW_host, double* const* db_host);
 
+/* ---- data-parallel training of a replicated bank (dp_step).
+ * The gradient ARENA is one flat fp32 array: for each parameter matrix i in
+ * index order, dW_i [G, fan_in, fan_out] then db_i [G, fan_out], each
+ * segment starting at a multiple of 32 floats (the size is one too, so
+ * arenas stacked back to back stay 128-byte aligned).                      */
+int mtk_bank_grad_size(mtk_bank* bank, int64_t* n_floats);
+/* Forward + backward of `step` on this worker's shard (CE weights / denom as
+ * in step: a shard of a global batch uses denom = its global_rows / n so the
+ * mean-reduction algebra stays exact, tape.hpp:466-468) writing the gradients
+ * to `grads` (device arena, 128-byte aligned).  Parameters and optimizer state are unchanged;
+ * frozen matrices report zeros.  step->lr / optimizer are ignored here.     */
+int mtk_bank_compute_grads(mtk_bank* bank, const mtk_step* step, float* grads, double* loss_host,
+                           double* mmd_host);
+/* The aggregation + one optimizer step: per element
+ * g = ((parts[0] + parts[1]) + ... + parts[n-1]) / n in ascending worker
+ * order (fixed, so every replica computes the same bits), then
+ * SGD / Adam per step->optimizer on every non-frozen parameter.  parts:
+ * device, n_parts arenas part_stride floats apart (an all-gather output).  */
+int mtk_bank_dp_apply(mtk_bank* bank, const mtk_step* step, const float* parts, int n_parts,
+                      int64_t part_stride);
+/* Order-independent 64-bit hash of every parameter's bits (all models):
+ * equal on bit-identical replicas; compared across workers before a step
+ * ("replica divergence detected before step").  Synchronizing. */
+int mtk_bank_fingerprint(mtk_bank* bank, uint64_t* out_host);
+
 /* ---- multi-bandwidth Gaussian MMD^2 (no reference
  * code).  k(x,y) = sum_b exp(-|x-y|^2/(beta*mult[b])); beta <= 0 selects the
  * detached closed form over [Xs;Xt].  Biased V-statistic.  gXs/gXt (device,

@@ -37,6 +37,16 @@ def _dvec(a):
     return (_dp * len(a))(*[x.ctypes.data_as(_dp) if x is not None else None for x in a])
 
 
+class _CudaArray:
+    def __init__(self, ptr, shape):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<f4",
+                                         "data": (int(ptr), False), "version": 3}
+
+
+def _device_view(ptr, shape, device):
+    return torch.as_tensor(_CudaArray(ptr, shape), device=device)
+
+
 class Context:
     """One per (thread, device); stream-ordered on torch's current stream."""
 
@@ -211,6 +221,18 @@ class Bank:
         errors.check(lib.mtk_bank_param_device(self.h, mat, C.byref(w), C.byref(b)))
         return w.value, b.value
 
+    def param_tensors(self):
+        """zero-copy torch views [W_0, b_0, W_1, b_1, ...] of the device
+        parameters (W_i [G, fan_in, fan_out], b_i [G, fan_out]); used to
+        broadcast a replica's initial parameters (dp.DataParallel)."""
+        dev = torch.device("cuda", self.ctx.device)
+        out = []
+        for i, (fi, fo) in enumerate(self.shapes()):
+            w, b = self.param_device(i)
+            out.append(_device_view(w, (self.G, fi, fo), dev))
+            out.append(_device_view(b, (self.G, fo), dev))
+        return out
+
     def forward(self, X: torch.Tensor, head: int = 0, hidden: bool = False):
         B = X.shape[1]
         logits = torch.empty((self.G, B, self.dims[-1]), device=X.device, dtype=torch.float32)
@@ -307,6 +329,45 @@ class Bank:
     def reset_optimizer(self):
         """zero the Adam moments and step count (a fresh OptimizerState)"""
         errors.check(lib.mtk_bank_reset_optimizer(self.h), "reset_optimizer")
+
+    # ---- data-parallel replicas (dp_step, SPEC.md:605-642; see dp.py) ----
+    def grad_size(self) -> int:
+        """floats in the gradient arena (per matrix: dW [G,fi,fo] then db [G,fo])"""
+        n = C.c_int64()
+        errors.check(lib.mtk_bank_grad_size(self.h, C.byref(n)), "grad_size")
+        return n.value
+
+    def compute_grads(self, X, y, w=None, out: torch.Tensor = None, *, want_loss=True, **kw):
+        """Forward + backward of this shard into a device gradient arena
+        (parameters and optimizer state unchanged); returns (arena, loss, mmd)."""
+        n = self.grad_size()
+        if out is None:
+            out = torch.empty(n, dtype=torch.float32, device=X.device)
+        if out.dtype != torch.float32 or not out.is_contiguous() or out.numel() < n:
+            raise errors.ShapeError(f"compute_grads: out must be contiguous fp32 with >= {n} floats")
+        s = self.make_step(X.shape[1], X=X, y=y, w=w, **kw)
+        lp = self._loss.ctypes.data_as(_dp) if want_loss else None
+        mp = self._mmd.ctypes.data_as(_dp) if want_loss else None
+        errors.check(lib.mtk_bank_compute_grads(self.h, C.byref(s), _ptr(out), lp, mp),
+                     "compute_grads")
+        return out, (self._loss.copy() if want_loss else None), (self._mmd.copy() if want_loss else None)
+
+    def dp_apply(self, parts: torch.Tensor, **kw):
+        """parts [n_workers, >= grad_size] fp32 device: g = ordered mean over
+        workers (ascending), then one optimizer step (make_step options)."""
+        if parts.dim() != 2 or parts.dtype != torch.float32 or parts.stride(1) != 1:
+            raise errors.ShapeError("dp_apply: parts must be [n_workers, arena] fp32, row-contiguous")
+        if parts.shape[1] < self.grad_size():
+            raise errors.ShapeError("dp_apply: parts rows are shorter than the gradient arena")
+        s = self.make_step(1, **kw)
+        errors.check(lib.mtk_bank_dp_apply(self.h, C.byref(s), _ptr(parts), parts.shape[0],
+                                           parts.stride(0)), "dp_apply")
+
+    def fingerprint(self) -> int:
+        """order-independent 64-bit hash of all parameter bits"""
+        v = C.c_uint64()
+        errors.check(lib.mtk_bank_fingerprint(self.h, C.byref(v)), "fingerprint")
+        return v.value
 
     def keep_grads(self, on: bool = True):
         errors.check(lib.mtk_bank_set_keep_grads(self.h, 1 if on else 0))

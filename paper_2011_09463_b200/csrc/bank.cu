@@ -1064,6 +1064,169 @@ int mtk_bank_get_grads(mtk_bank* k, int model, double* const* dW, double* const*
     });
 }
 
+// ---- data-parallel training of a replicated bank --------
+
+namespace {
+
+int layer_of(const mtk_bank& k, int mat) { return mat < k.L ? mat : k.L - 1; }
+
+// the gradient-arena layout: per matrix i, dW_i then db_i, every segment
+// starting on a 128-byte boundary (the GEMM epilogues store 16-byte vectors)
+constexpr long long kArenaAlign = 32;  // floats
+long long arena_round(long long n) { return (n + kArenaAlign - 1) / kArenaAlign * kArenaAlign; }
+
+std::vector<DpSegment> arena_segments(mtk_bank& k, int frozen_layers, bool adam) {
+    std::vector<DpSegment> v;
+    long long off = 0;
+    for (int i = 0; i < k.n_mats; ++i) {
+        const int fz = layer_of(k, i) < frozen_layers;
+        DpSegment w, b;
+        w.p = k.W[i].f;
+        w.n = (long long)k.G * k.fan_in(i) * k.fan_out(i);
+        w.off = off;
+        w.frozen = fz;
+        off = arena_round(off + w.n);
+        b.p = k.b[i];
+        b.n = (long long)k.G * k.fan_out(i);
+        b.off = off;
+        b.frozen = fz;
+        off = arena_round(off + b.n);
+        if (adam) {
+            w.m = k.mW[i];
+            w.v = k.vW[i];
+            b.m = k.mb[i];
+            b.v = k.vb[i];
+        }
+        v.push_back(w);
+        v.push_back(b);
+    }
+    return v;
+}
+
+long long arena_floats(mtk_bank& k) {
+    const auto v = arena_segments(k, 0, false);
+    return v.empty() ? 0 : arena_round(v.back().off + v.back().n);
+}
+
+std::vector<DpSegments> segment_chunks(const std::vector<DpSegment>& v) {
+    std::vector<DpSegments> out;
+    for (size_t i = 0; i < v.size(); i += kMaxDpSegments) {
+        DpSegments s;
+        for (size_t j = i; j < v.size() && j < i + kMaxDpSegments; ++j) s.s[s.count++] = v[j];
+        out.push_back(s);
+    }
+    return out;
+}
+
+}  // namespace
+
+int mtk_bank_grad_size(mtk_bank* k, int64_t* n_floats) {
+    return guard([&] {
+        check_bank(k);
+        need(n_floats != nullptr, MTK_VALUE_ERROR, "grad_size: null out");
+        *n_floats = arena_floats(*k);
+    });
+}
+
+int mtk_bank_compute_grads(mtk_bank* k, const mtk_step* s, float* grads, double* loss_host,
+                           double* mmd_host) {
+    return guard([&] {
+        check_bank(k);
+        need(s != nullptr && grads != nullptr, MTK_VALUE_ERROR, "compute_grads: null argument");
+        need(((uintptr_t)grads & 127) == 0, MTK_VALUE_ERROR,
+             "compute_grads: the gradient arena must be 128-byte aligned");
+        need(s->frozen_layers >= 0 && s->frozen_layers <= k->L, MTK_CONFIG_ERROR,
+             "train_step: frozen_layers out of range");
+        // the step's own forward/backward with lr = 0 under SGD: every update
+        // is w - 0*g = w (bit-identical parameters, no optimizer state
+        // touched) while the keep-grads outputs land in the caller's arena
+        const std::vector<DpSegment> segs = arena_segments(*k, s->frozen_layers, false);
+        std::vector<float*> saved_w, saved_b;
+        saved_w.swap(k->gW);
+        saved_b.swap(k->gb);
+        const bool saved_keep = k->keep_grads;
+        for (int i = 0; i < k->n_mats; ++i) {
+            k->gW.push_back(grads + segs[2 * i].off);
+            k->gb.push_back(grads + segs[2 * i + 1].off);
+        }
+        k->keep_grads = true;
+        struct Restore {
+            mtk_bank* k;
+            std::vector<float*>& w;
+            std::vector<float*>& b;
+            bool keep;
+            ~Restore() {
+                k->gW.swap(w);
+                k->gb.swap(b);
+                k->keep_grads = keep;
+            }
+        } restore{k, saved_w, saved_b, saved_keep};
+        for (const DpSegment& sg : segs)  // frozen matrices report zero gradients
+            if (sg.frozen)
+                MTK_CUDA(cudaMemsetAsync(grads + sg.off, 0, sg.n * sizeof(float), k->ctx->stream));
+        mtk_step g = *s;
+        g.lr = 0.0;
+        g.optimizer = 0;
+        train_step(*k, g, loss_host, mmd_host);
+    });
+}
+
+int mtk_bank_dp_apply(mtk_bank* k, const mtk_step* s, const float* parts, int n_parts,
+                      int64_t part_stride) {
+    return guard([&] {
+        check_bank(k);
+        need(s != nullptr && parts != nullptr, MTK_VALUE_ERROR, "dp_apply: null argument");
+        need(n_parts >= 1, MTK_CONFIG_ERROR, "dp_apply: n_workers must be >= 1");
+        need(part_stride >= arena_floats(*k) || n_parts == 1, MTK_SHAPE_ERROR,
+             "dp_apply: part_stride is smaller than the gradient arena");
+        need(((uintptr_t)parts & 15) == 0, MTK_VALUE_ERROR, "dp_apply: parts must be 16-byte aligned");
+        need(std::isfinite(s->lr), MTK_VALUE_ERROR, "train_step: lr must be finite");
+        need(s->frozen_layers >= 0 && s->frozen_layers <= k->L, MTK_CONFIG_ERROR,
+             "train_step: frozen_layers out of range");
+        need(s->optimizer == 0 || s->optimizer == 1, MTK_CONFIG_ERROR,
+             "train_step: optimizer must be 0 (SGD) or 1 (Adam)");
+        AdamArgs adam;
+        if (s->optimizer == 1) {
+            const double b1 = s->adam_beta1 > 0 ? s->adam_beta1 : 0.9;
+            const double b2 = s->adam_beta2 > 0 ? s->adam_beta2 : 0.999;
+            const double eps = s->adam_eps > 0 ? s->adam_eps : 1e-8;
+            need(b1 < 1.0 && b2 < 1.0 && std::isfinite(eps), MTK_CONFIG_ERROR,
+                 "train_step: Adam betas must lie in [0, 1)");
+            k->ensure_adam();
+            k->adam_t += 1;  // one optimizer_step per dp_step (optim.hpp:41)
+            adam.on = 1;
+            adam.b1 = (float)b1;
+            adam.b2 = (float)b2;
+            adam.eps = (float)eps;
+            adam.bc1 = (float)(1.0 - std::pow(b1, (double)k->adam_t));
+            adam.bc2 = (float)(1.0 - std::pow(b2, (double)k->adam_t));
+        }
+        Ctx& c = *k->ctx;
+        const auto segs = arena_segments(*k, s->frozen_layers, adam.on != 0);
+        for (const DpSegments& ch : segment_chunks(segs))
+            launch_dp_reduce_apply(ch, parts, n_parts, (long long)part_stride, (float)s->lr, adam,
+                                   c.d_flags, c.stream);
+        after_launch(c);
+    });
+}
+
+int mtk_bank_fingerprint(mtk_bank* k, uint64_t* out_host) {
+    return guard([&] {
+        check_bank(k);
+        need(out_host != nullptr, MTK_VALUE_ERROR, "fingerprint: null out");
+        Ctx& c = *k->ctx;
+        auto* d = reinterpret_cast<unsigned long long*>(c.scratch(sizeof(unsigned long long)));
+        MTK_CUDA(cudaMemsetAsync(d, 0, sizeof(unsigned long long), c.stream));
+        for (const DpSegments& ch : segment_chunks(arena_segments(*k, 0, false)))
+            launch_fingerprint(ch, d, c.stream);
+        after_launch(c);
+        auto* h = static_cast<unsigned long long*>(c.pinned_buf(sizeof(unsigned long long)));
+        MTK_CUDA(cudaMemcpyAsync(h, d, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c.stream));
+        MTK_CUDA(cudaStreamSynchronize(c.stream));
+        *out_host = *h;
+    });
+}
+
 int mtk_bank_tc_layers(mtk_bank* k, int* out_host) {
     return guard([&] {
         check_bank(k);

@@ -91,9 +91,13 @@ struct AdamArgs {
 // The tensor-core / SIMT GEMM epilogues do SGD only; under Adam they store the
 // gradient and launch_adam_apply updates (keeps Adam's division / sqrt slow
 // paths out of the unrolled epilogues).
+// SGD w - lr*g as one explicit fused multiply-add, so every update site (GEMM
+// epilogues, bias kernels, dp_apply) rounds identically whatever nvcc's
+// contraction choices are.
+__device__ __forceinline__ float sgd_update(float w, float g, float lr) { return __fmaf_rn(-lr, g, w); }
 __device__ __forceinline__ float param_update(float w, float g, float lr, const AdamArgs& a,
                                               long long idx) {
-    if (!a.on) return w - lr * g;
+    if (!a.on) return sgd_update(w, g, lr);
     const float m = a.b1 * a.m[idx] + (1.f - a.b1) * g;
     const float v = a.b2 * a.v[idx] + (1.f - a.b2) * g * g;
     a.m[idx] = m;
@@ -134,6 +138,27 @@ void launch_gemm(const Gemm& g, cudaStream_t s);
 // W[i] -= Adam step from grad[i], i < n (moments in a.m / a.v); non-finite -> flags
 void launch_adam_apply(float* W, const float* grad, long long n, float lr, const AdamArgs& a,
                        int* flags, cudaStream_t s);
+
+// data-parallel step (k_dp.cu): one segment per parameter array (W_i, b_i)
+// of a bank, at float offset `off` of the gradient arena.
+struct DpSegment {
+    float* p = nullptr;  // parameters (device)
+    float* m = nullptr;  // Adam moments (or null)
+    float* v = nullptr;
+    long long off = 0, n = 0;
+    int frozen = 0;
+};
+constexpr int kMaxDpSegments = 40;
+struct DpSegments {
+    DpSegment s[kMaxDpSegments];
+    int count = 0;
+};
+// p_seg = optimizer_step(p_seg, (sum_{r ascending} parts[r*stride + off + j]) / n)
+void launch_dp_reduce_apply(const DpSegments& segs, const float* parts, int n_parts,
+                            long long part_stride, float lr, const AdamArgs& adam, int* flags,
+                            cudaStream_t s);
+// *out += order-independent 64-bit hash of every segment's parameter bits
+void launch_fingerprint(const DpSegments& segs, unsigned long long* out, cudaStream_t s);
 
 // tcgen05 3xTF32 grouped GEMM (k_umma.cu).  Operands are plain fp32; element
 // (r, c) sits at base[g*gs + r*rs + c], c being the contiguous index: for a

@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(NT) gemm_simt_kernel(Gemm p) {
                     break;
                 case Epi::kSgd:
                     if (p.grad_out) p.grad_out[idx] = v;
-                    v = p.C[idx] - p.lr * v;
+                    v = sgd_update(p.C[idx], v, p.lr);
                     bad |= !isfinite(v);
                     break;
                 case Epi::kStore:

@@ -245,10 +245,10 @@ __device__ __forceinline__ void epilogue_rows(const UmmaParams& p, uint32_t tmem
                     x.w = o1[j].w > 0.f ? x.w : 0.f;
                 } else if (epi == (int)Epi::kSgd) {  // C is the fp32 master weight
                     if (p.grad_out) *reinterpret_cast<float4*>(p.grad_out + idx) = x;
-                    x.x = o1[j].x - p.lr * x.x;
-                    x.y = o1[j].y - p.lr * x.y;
-                    x.z = o1[j].z - p.lr * x.z;
-                    x.w = o1[j].w - p.lr * x.w;
+                    x.x = sgd_update(o1[j].x, x.x, p.lr);
+                    x.y = sgd_update(o1[j].y, x.y, p.lr);
+                    x.z = sgd_update(o1[j].z, x.z, p.lr);
+                    x.w = sgd_update(o1[j].w, x.w, p.lr);
                     bad |= !(isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w));
                 }
                 if (epi != (int)Epi::kNone) *reinterpret_cast<float4*>(p.C + idx) = x;
@@ -273,7 +273,7 @@ __device__ __forceinline__ void epilogue_rows(const UmmaParams& p, uint32_t tmem
                         x = (p.mask[idx] > 0.f) ? x : 0.f;
                     } else if (epi == (int)Epi::kSgd) {
                         if (p.grad_out) p.grad_out[idx] = x;
-                        x = p.C[idx] - p.lr * x;
+                        x = sgd_update(p.C[idx], x, p.lr);
                         bad |= !isfinite(x);
                     }
                     if (epi != (int)Epi::kNone) p.C[idx] = x;

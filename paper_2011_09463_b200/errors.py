@@ -44,6 +44,12 @@ class TruncatedError(CheckpointError):
     """mt::TruncatedError (error.hpp:44-46): file shorter than its header says."""
 
 
+class ConsistencyError(Error):
+    """dp_step's "replica divergence detected before step -> consistency
+    error"; error.hpp has no dedicated class, so it derives
+    from mt::Error.  Raised host-side by dp.DataParallel."""
+
+
 _BY_STATUS = {1: ShapeError, 2: ValueError, 3: ConfigError, 4: DataError, 5: Error,
               6: CheckpointError, 7: VersionError, 8: DigestError, 9: TruncatedError}
 

@@ -80,3 +80,74 @@ class OracleBackend:
 
     def auc(self, scores, labels):
         return po.auc(scores, labels), po.accuracy(scores, labels, 0.5)
+
+
+class OracleReplica:
+    """TEST INFRASTRUCTURE: one f64 oracle model behind the replica interface
+    paper_2011_09463_b200.dp.DataParallel drives (G = 1, single head), so the
+    dp_step plumbing (sharding, gather, ascending-order mean, replica check)
+    runs over gloo on the CPU against single-process full-batch training."""
+
+    import torch as _torch
+
+    grad_dtype = _torch.float64
+    device = _torch.device("cpu")
+
+    def __init__(self, dims, W, b):
+        self.dims = list(dims)
+        self.W = [np.array(x, dtype=np.float64) for x in W]
+        self.b = [np.array(x, dtype=np.float64) for x in b]
+        self.adam = None
+
+    def grad_size(self):
+        return sum(w.size + b.size for w, b in zip(self.W, self.b))
+
+    def compute_grads(self, X, y, w, out, denom, *, lr=0.0, optimizer="sgd", frozen_layers=0,
+                      **_):
+        X = np.asarray(X, dtype=np.float64)[0]
+        y = np.asarray(y)[0]
+        wv = None if w is None else np.asarray(w, dtype=np.float64)[0]
+        loss, gW, gb = po.mlp_train_step(self.dims, self.W, self.b, X, y, frozen=frozen_layers,
+                                         w=wv, denoms=[denom[0]], lr=0.0, want_grads=True)
+        flat = np.concatenate([np.concatenate([a.ravel(), c.ravel()]) for a, c in zip(gW, gb)])
+        out.copy_(self._torch.from_numpy(flat))
+        return np.array([loss])
+
+    def apply(self, parts, *, lr=0.05, optimizer="sgd", frozen_layers=0, **_):
+        P = parts.numpy()
+        acc = P[0].copy()
+        for r in range(1, P.shape[0]):  # ascending worker order
+            acc = acc + P[r]
+        g = acc / P.shape[0]
+        off = 0
+        gW, gb = [], []
+        for Wi, bi in zip(self.W, self.b):
+            gW.append(g[off:off + Wi.size].reshape(Wi.shape))
+            off += Wi.size
+            gb.append(g[off:off + bi.size])
+            off += bi.size
+        L = len(self.dims) - 1
+        if optimizer == "adam":
+            if self.adam is None:
+                self.adam = po.Adam(self.W + self.b, lr)
+            self.adam.update(self.W + self.b, gW + gb)
+            return
+        for i in range(L):
+            if i < frozen_layers:
+                continue
+            self.W[i] -= lr * gW[i]
+            self.b[i] -= lr * gb[i]
+
+    def fingerprint(self):
+        import hashlib
+
+        h = hashlib.sha256()
+        for a in self.W + self.b:
+            h.update(a.tobytes())
+        return int.from_bytes(h.digest()[:8], "little")
+
+    def param_tensors(self):
+        out = []
+        for Wi, bi in zip(self.W, self.b):
+            out += [self._torch.from_numpy(Wi), self._torch.from_numpy(bi)]
+        return out
