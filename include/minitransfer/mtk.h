@@ -85,6 +85,25 @@ int mtk_rng_fill_normal(mtk_rng* r, double* out_host, uint64_t n);
 int mtk_synth(mtk_rng* r, int C, int d, uint64_t n, const double* mu_host,
               const double* shift_host, double* X64_host, float* X32_host, int32_t* y_host);
 
+/* ---- counter-based synthetic data on the DEVICE.  Not
+ * mt::Rng: a stateless Philox4x64-10 stream keyed by {seed, stream}, so a
+ * pool of any size is generated in parallel straight into HBM.  Contract
+ * (restated by oracle/oracle.c orc_synth_counter):
+ *   normals: element e of a row-major [n, d] matrix <- counter {e/4,0,0,0};
+ *     words (w0,w1) -> elements 4i, 4i+1, (w2,w3) -> 4i+2, 4i+3, Box-Muller
+ *     with u1 = ((wa >> 40) + 1) 2^-24, u2 = (wb >> 40) 2^-24 (fp32 math);
+ *   labels: row i <- word i%4 of counter {i/4,1,0,0}, y = (w * C) >> 64;
+ *   X[i,k] = (mu[y_i,k] + z[i*d+k]) (+ shift[k]).
+ * Raw words and labels are bit-exact against the oracle; normals agree to a
+ * few fp32 ulps (libm vs device transcendental rounding).                  */
+int mtk_philox4x64_fill(mtk_ctx* ctx, uint64_t seed, uint64_t stream, uint64_t ctr0, uint64_t ctr1,
+                        int64_t nblocks, uint64_t* out); /* out[4i..4i+3] = philox({ctr0+i,ctr1,0,0}) */
+int mtk_counter_normals(mtk_ctx* ctx, uint64_t seed, uint64_t stream, int64_t first, int64_t count,
+                        float* out);                      /* elements [first, first+count) */
+/* mu [C, d] and shift [d] (or NULL) fp32 device; X [n, d] fp32, y [n] int32 device */
+int mtk_synth_counter(mtk_ctx* ctx, uint64_t seed, uint64_t stream, int C, int d, int64_t n,
+                      const float* mu, const float* shift, float* X, int32_t* y);
+
 /* ---- model bank: G independent MLPs dims[0] -> ... -> dims[n_layers], ReLU
  * hidden layers, trained as ONE grouped step.  Replaces, per model, the Tape
  * composition matmul (tape.hpp:225-290) -> add_bias (:204-221) -> relu

@@ -609,3 +609,77 @@ void orc_synth(orc_rng* r, int C, int d, size_t n, const double* mu, const doubl
         }
     }
 }
+
+/* ======================================================================= */
+/* Counter-based generator -- see oracle.h             */
+/* ======================================================================= */
+static uint64_t mulhilo64(uint64_t a, uint64_t b, uint64_t* hi) {
+    const unsigned __int128 p = (unsigned __int128)a * b;
+    *hi = (uint64_t)(p >> 64);
+    return (uint64_t)p;
+}
+
+void orc_philox4x64(const uint64_t ctr[4], const uint64_t key[2], uint64_t out[4]) {
+    uint64_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3];
+    uint64_t k0 = key[0], k1 = key[1];
+    for (int r = 0; r < 10; ++r) {
+        uint64_t hi0, hi1;
+        const uint64_t lo0 = mulhilo64(0xD2E7470EE14C6C93ULL, c0, &hi0);
+        const uint64_t lo1 = mulhilo64(0xCA5A826395121157ULL, c2, &hi1);
+        const uint64_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+        c0 = n0;
+        c1 = lo1;
+        c2 = n2;
+        c3 = lo0;
+        k0 += 0x9E3779B97F4A7C15ULL;
+        k1 += 0xBB67AE8584CAA73BULL;
+    }
+    out[0] = c0;
+    out[1] = c1;
+    out[2] = c2;
+    out[3] = c3;
+}
+
+static void box_muller(uint64_t wa, uint64_t wb, double* za, double* zb) {
+    const double u1 = (double)((wa >> 40) + 1) * 0x1p-24;
+    const double u2 = (double)(wb >> 40) * 0x1p-24;
+    const double r = sqrt(-2.0 * log(u1));
+    const double t = 2.0 * 3.14159265358979323846 * u2;
+    *za = r * cos(t);
+    *zb = r * sin(t);
+}
+
+void orc_counter_normals(uint64_t seed, uint64_t stream, size_t first, size_t count, double* z) {
+    const uint64_t key[2] = {seed, stream};
+    for (size_t e = first; e < first + count;) {
+        const uint64_t ctr[4] = {(uint64_t)(e / 4), 0, 0, 0};
+        uint64_t w[4];
+        double v[4];
+        orc_philox4x64(ctr, key, w);
+        box_muller(w[0], w[1], &v[0], &v[1]);
+        box_muller(w[2], w[3], &v[2], &v[3]);
+        for (size_t j = e % 4; j < 4 && e < first + count; ++j, ++e) z[e - first] = v[j];
+    }
+}
+
+void orc_synth_counter(uint64_t seed, uint64_t stream, int C, int d, size_t n, const double* mu,
+                       const double* shift, double* X, int32_t* y) {
+    const uint64_t key[2] = {seed, stream};
+    for (size_t i = 0; i < n; ++i) {
+        const uint64_t ctr[4] = {(uint64_t)(i / 4), 1, 0, 0};
+        uint64_t w[4], hi;
+        orc_philox4x64(ctr, key, w);
+        (void)mulhilo64(w[i % 4], (uint64_t)C, &hi);
+        y[i] = (int32_t)hi;
+    }
+    orc_counter_normals(seed, stream, 0, n * (size_t)d, X);
+    for (size_t i = 0; i < n; ++i) {
+        const double* m = mu + (size_t)y[i] * (size_t)d;
+        double* x = X + i * (size_t)d;
+        for (int k = 0; k < d; ++k) {
+            double v = m[k] + x[k];
+            if (shift) v = v + shift[k];
+            x[k] = v;
+        }
+    }
+}

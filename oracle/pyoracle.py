@@ -82,6 +82,10 @@ def _setup_orc(L):
     L.orc_accuracy.restype = C.c_double
     L.orc_accuracy.argtypes = [_dp, _u8p, C.c_size_t, C.c_double]
     L.orc_synth.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_size_t, _dp, _dp, _dp, _i32p]
+    L.orc_philox4x64.argtypes = [C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+    L.orc_counter_normals.argtypes = [C.c_uint64, C.c_uint64, C.c_size_t, C.c_size_t, _dp]
+    L.orc_synth_counter.argtypes = [C.c_uint64, C.c_uint64, C.c_int, C.c_int, C.c_size_t, _dp, _dp,
+                                    _dp, _i32p]
     step_args = [C.c_int, _ip, C.c_int, C.c_int, C.POINTER(_dp), C.POINTER(_dp), _dp, C.c_int,
                  C.c_int, _i32p, _dp, _dp, C.c_double, _dp, _dp, C.POINTER(_dp), C.POINTER(_dp)]
     L.orc_mlp_train_step.argtypes = step_args
@@ -351,4 +355,29 @@ def synth(rng: Rng, C_, d, n, mu, shift=None):
     mu = np.ascontiguousarray(mu, dtype=np.float64)
     sh = None if shift is None else np.ascontiguousarray(shift, dtype=np.float64)
     orc().orc_synth(rng._buf, C_, d, n, dp(mu), dp(sh), dp(X), y.ctypes.data_as(_i32p))
+    return X, y
+
+
+def philox4x64(ctr, key):
+    """Philox4x64-10 bijection (oracle.h): 4 counter words, 2 key words -> 4 words."""
+    c = (C.c_uint64 * 4)(*[int(x) & (2**64 - 1) for x in ctr])
+    k = (C.c_uint64 * 2)(*[int(x) & (2**64 - 1) for x in key])
+    o = (C.c_uint64 * 4)()
+    orc().orc_philox4x64(c, k, o)
+    return [int(x) for x in o]
+
+
+def counter_normals(seed, stream, first, count):
+    z = np.empty(count)
+    orc().orc_counter_normals(seed, stream, first, count, dp(z))
+    return z
+
+
+def synth_counter(seed, stream, C_, d, n, mu, shift=None):
+    """Counter-based class-conditional Gaussians (oracle.h); f64 X, int32 y."""
+    X = np.empty((n, d))
+    y = np.empty(n, dtype=np.int32)
+    mu = np.ascontiguousarray(mu, dtype=np.float64)
+    sh = None if shift is None else np.ascontiguousarray(shift, dtype=np.float64)
+    orc().orc_synth_counter(seed, stream, C_, d, n, dp(mu), dp(sh), dp(X), y.ctypes.data_as(_i32p))
     return X, y

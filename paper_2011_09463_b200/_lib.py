@@ -57,6 +57,11 @@ SIGNATURES = {
     "mtk_bank_load": (C.c_int, [_vp, C.c_char_p, C.POINTER(_vp)]),
     "mtk_bank_info": (C.c_int, [_vp, _ip, _ip, _ip, _ip]),
     "mtk_sha256": (C.c_int, [_vp, C.c_size_t, _vp]),
+    "mtk_philox4x64_fill": (C.c_int, [_vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
+                                      C.c_int64, _vp]),
+    "mtk_counter_normals": (C.c_int, [_vp, C.c_uint64, C.c_uint64, C.c_int64, C.c_int64, _vp]),
+    "mtk_synth_counter": (C.c_int, [_vp, C.c_uint64, C.c_uint64, C.c_int, C.c_int, C.c_int64, _vp,
+                                    _vp, _vp, _vp]),
     "mtk_bank_grad_size": (C.c_int, [_vp, C.POINTER(C.c_int64)]),
     "mtk_bank_compute_grads": (C.c_int, [_vp, C.POINTER(MtkStep), _vp, _dp, _dp]),
     "mtk_bank_dp_apply": (C.c_int, [_vp, C.POINTER(MtkStep), _vp, C.c_int, C.c_int64]),

@@ -450,6 +450,42 @@ def gather_rows(ctx: Context, src: torch.Tensor, idx: torch.Tensor, out: torch.T
     return out
 
 
+# ---- counter-based synthetic data on the device (mtk.h) ----
+_U64 = 2**64 - 1
+
+
+def philox4x64_fill(ctx: Context, seed: int, stream: int, nblocks: int, ctr0: int = 0,
+                    ctr1: int = 0) -> torch.Tensor:
+    """raw Philox4x64-10 words: out[i] = philox({ctr0 + i, ctr1, 0, 0}, {seed, stream}),
+    as an int64 tensor [nblocks, 4] (bit pattern of the uint64 words)."""
+    out = torch.empty((nblocks, 4), dtype=torch.int64, device=torch.device("cuda", ctx.device))
+    errors.check(lib.mtk_philox4x64_fill(ctx.h, seed & _U64, stream & _U64, ctr0 & _U64,
+                                         ctr1 & _U64, nblocks, _ptr(out)), "philox4x64_fill")
+    return out
+
+
+def counter_normals(ctx: Context, seed: int, stream: int, first: int, count: int) -> torch.Tensor:
+    out = torch.empty(count, dtype=torch.float32, device=torch.device("cuda", ctx.device))
+    errors.check(lib.mtk_counter_normals(ctx.h, seed & _U64, stream & _U64, first, count,
+                                         _ptr(out)), "counter_normals")
+    return out
+
+
+def synth_counter(ctx: Context, seed: int, stream: int, n: int, mu: torch.Tensor,
+                  shift: torch.Tensor = None):
+    """X [n, d] fp32, y [n] int32 on the device: y from the label counter
+    space, X = mu[y] + N(0, I) (+ shift) (mtk_synth_counter)."""
+    C, d = mu.shape
+    dev = torch.device("cuda", ctx.device)
+    mu = mu.to(dev, torch.float32).contiguous()
+    sh = None if shift is None else shift.to(dev, torch.float32).contiguous()
+    X = torch.empty((n, d), dtype=torch.float32, device=dev)
+    y = torch.empty(n, dtype=torch.int32, device=dev)
+    errors.check(lib.mtk_synth_counter(ctx.h, seed & _U64, stream & _U64, C, d, n, _ptr(mu),
+                                       _ptr(sh), _ptr(X), _ptr(y)), "synth_counter")
+    return X, y
+
+
 def softmax(ctx: Context, logits: torch.Tensor) -> torch.Tensor:
     logits2 = logits.reshape(-1, logits.shape[-1])
     out = torch.empty_like(logits2)

@@ -320,6 +320,36 @@ int mtk_gather_rows(mtk_ctx* c, const void* src, int64_t src_rows, int d, const 
     });
 }
 
+int mtk_philox4x64_fill(mtk_ctx* c, uint64_t seed, uint64_t stream, uint64_t ctr0, uint64_t ctr1,
+                        int64_t nblocks, uint64_t* out) {
+    return guard([&] {
+        need(c && (out || nblocks == 0), MTK_VALUE_ERROR, "philox: null argument");
+        need(nblocks >= 0, MTK_SHAPE_ERROR, "philox: negative block count");
+        launch_philox_fill(seed, stream, ctr0, ctr1, nblocks, out, c->stream);
+        after_launch(*c);
+    });
+}
+
+int mtk_counter_normals(mtk_ctx* c, uint64_t seed, uint64_t stream, int64_t first, int64_t count,
+                        float* out) {
+    return guard([&] {
+        need(c && (out || count == 0), MTK_VALUE_ERROR, "counter_normals: null argument");
+        need(first >= 0 && count >= 0, MTK_SHAPE_ERROR, "counter_normals: negative range");
+        launch_counter_normals(seed, stream, first, count, out, c->stream);
+        after_launch(*c);
+    });
+}
+
+int mtk_synth_counter(mtk_ctx* c, uint64_t seed, uint64_t stream, int C, int d, int64_t n,
+                      const float* mu, const float* shift, float* X, int32_t* y) {
+    return guard([&] {
+        need(c && mu && X && y, MTK_VALUE_ERROR, "synth_counter: null argument");
+        need(C >= 1 && d >= 1 && n >= 1, MTK_SHAPE_ERROR, "synth_counter: zero dimension");
+        launch_synth_counter(seed, stream, C, d, n, mu, shift, X, y, c->stream);
+        after_launch(*c);
+    });
+}
+
 int mtk_softmax(mtk_ctx* c, const float* logits, int64_t rows, int C, float* probs) {
     return guard([&] {
         need(c && logits && probs, MTK_VALUE_ERROR, "softmax: null argument");

@@ -160,6 +160,15 @@ void launch_dp_reduce_apply(const DpSegments& segs, const float* parts, int n_pa
 // *out += order-independent 64-bit hash of every segment's parameter bits
 void launch_fingerprint(const DpSegments& segs, unsigned long long* out, cudaStream_t s);
 
+// counter-based synthetic data (k_rng.cu; contract in mtk.h / oracle.h)
+void launch_philox_fill(uint64_t seed, uint64_t stream, uint64_t c0, uint64_t c1, long long nblocks,
+                        uint64_t* out, cudaStream_t s);
+void launch_counter_normals(uint64_t seed, uint64_t stream, long long first, long long count,
+                            float* out, cudaStream_t s);
+void launch_synth_counter(uint64_t seed, uint64_t stream, int C, int d, long long n,
+                          const float* mu, const float* shift, float* X, int32_t* y,
+                          cudaStream_t s);
+
 // tcgen05 3xTF32 grouped GEMM (k_umma.cu).  Operands are plain fp32; element
 // (r, c) sits at base[g*gs + r*rs + c], c being the contiguous index: for a
 // K-major operand r = m (or n) and c = k, for an MN-major operand r = k and

@@ -6,6 +6,12 @@ The reference has no code for this stage; the definitions pinned here are:
 * data: class-conditional Gaussians, y = below(C), x = mu_y + N(0, I) on the
   host RNG (rng.hpp semantics, bit-exact); the target domain adds a fixed
   shift delta (PAPER.md:17-23: D^S, D^T, N^S >> N^T);
+* data_rng = "counter": mu / shift as above, but the
+  two pools come from the device counter-based generator (mtk_synth_counter:
+  Philox4x64-10 keyed {seed, 1} for the target pool, {seed, 2} for the
+  source pool), generated straight into HBM -- the host Box-Muller stream is
+  the C5 wall-clock floor otherwise.  A different (documented) stream, so
+  "counter" results differ from "host" ones; the oracle backend restates it;
 * streams: root = Rng(seed); data = root.split(0); model k (0 = target,
   1..S = shadows) = root.split(k + 1), derived in ascending k on every rank
   (rng.hpp:65-69: split advances the parent);
@@ -62,6 +68,7 @@ class SweepConfig:
     attack_batch: int = 1024
     attack_lr: float = 0.1
     attack_optimizer: str = "sgd"
+    data_rng: str = "host"           # host (mt::Rng, bit-exact) | counter (device Philox)
     seed: int = 20110946
 
     def validate(self):
@@ -80,18 +87,30 @@ class SweepConfig:
         for o in (self.optimizer, self.attack_optimizer):
             if o not in ("sgd", "adam"):
                 raise ConfigError(f"unknown optimizer {o!r}")
+        if self.data_rng not in ("host", "counter"):
+            raise ConfigError(f"unknown data_rng {self.data_rng!r} (host | counter)")
 
 
 # --------------------------------------------------------------------------- data
 class Population:
-    """Source and target pools drawn from the data stream (host, bit-exact)."""
+    """Source and target pools: drawn from the host data stream (bit-exact
+    mt::Rng), or with data_rng = "counter" by the backend's counter-based
+    generator (device pools for the GPU backend)."""
 
-    def __init__(self, cfg: SweepConfig, rng_cls):
+    def __init__(self, cfg: SweepConfig, rng_cls, synth_counter=None):
+        from .errors import ConfigError
+
         C, d = cfg.dims[-1], cfg.dims[0]
         self.root = rng_cls(cfg.seed)
         data = self.root.split(0)
         self.mu = cfg.mu_scale * data.normals(C * d).reshape(C, d)
         self.shift = cfg.shift_scale * data.normals(d)
+        if cfg.data_rng == "counter":
+            if synth_counter is None:
+                raise ConfigError("data_rng 'counter' needs a backend with synth_counter")
+            self.Xt, self.yt = synth_counter(cfg.seed, 1, cfg.pool, self.mu, self.shift)
+            self.Xs, self.ys = synth_counter(cfg.seed, 2, cfg.source_pool, self.mu, None)
+            return
         self.Xt, self.yt = synth(data, C, d, cfg.pool, self.mu, self.shift)
         self.Xs, self.ys = synth(data, C, d, cfg.source_pool, self.mu, None)
 
@@ -153,7 +172,15 @@ class GpuBackend:
             return a
         return self.torch.from_numpy(np.ascontiguousarray(a)).to(self.device)
 
+    def synth_counter(self, seed, stream, n, mu, shift):
+        """pool generated on the device (mtk_synth_counter); stays in HBM"""
+        torch = self.torch
+        return self.api.synth_counter(self.ctx, seed, stream, n, torch.from_numpy(np.asarray(mu)),
+                                      None if shift is None else torch.from_numpy(np.asarray(shift)))
+
     def _pool(self, X, y):
+        if isinstance(X, self.torch.Tensor):  # device-born pool (data_rng = "counter")
+            return X, y
         if not hasattr(self, "_pools"):
             self._pools = {}
         key = (id(X), id(y))
@@ -304,7 +331,7 @@ def run_sweep(cfg: SweepConfig, be=None, *, rank: int = 0, world: int = 1,
     """
     cfg.validate()
     be = be or GpuBackend()
-    pop = Population(cfg, be.Rng)
+    pop = Population(cfg, be.Rng, getattr(be, "synth_counter", None))
     M = 1 + cfg.n_shadows
     streams = pop.model_streams(M + 1)  # last stream drives the attack model
     lo, hi = rank * M // world, (rank + 1) * M // world

@@ -35,6 +35,14 @@ class OracleBackend:
     def init(self, bank, g, rng):
         bank.params[g] = po.mlp_init(rng, bank.dims, bank.n_heads)
 
+    def synth_counter(self, seed, stream, n, mu, shift):
+        # the device generator's contract (oracle.c orc_synth_counter); the GPU
+        # path builds its pools from fp32 mu / shift, so round them the same way
+        mu32 = np.asarray(mu, dtype=np.float32).astype(np.float64)
+        sh32 = None if shift is None else np.asarray(shift, dtype=np.float32).astype(np.float64)
+        X, y = po.synth_counter(seed, stream, mu32.shape[0], mu32.shape[1], n, mu32, sh32)
+        return X.astype(np.float32), y
+
     def step(self, bank, X, y, w, *, lr, src_rows=0, frozen_layers=0, mmd_lambda=0.0,
              denom=(0.0, 0.0), optimizer="sgd"):
         X = np.asarray(X, dtype=np.float64)

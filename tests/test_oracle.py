@@ -241,3 +241,43 @@ def test_synth_deterministic():
     a = po.synth(po.Rng(1), 4, 5, 7, mu)
     b = po.synth(po.Rng(1), 4, 5, 7, mu)
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+# ---- counter-based generator ------------------------------
+
+def test_philox4x64_known_answer_and_numpy():
+    # Random123 known-answer vector for philox4x64_R(10), ctr = key = 0
+    assert po.philox4x64([0, 0, 0, 0], [0, 0]) == [0x16554D9ECA36314C, 0xDB20FE9D672D0FDC,
+                                                   0xD7E772CEE186176B, 0x7E68B68AEC7BA23B]
+    # numpy's Philox (4x64, 10 rounds) increments the counter before each block
+    rs = np.random.default_rng(5)
+    for _ in range(20):
+        ctr = [int(x) for x in rs.integers(0, 2**63, 4)]
+        key = [int(x) for x in rs.integers(0, 2**63, 2)]
+        bg = np.random.Philox(counter=[ctr[0] - 1 if ctr[0] else 0] + ctr[1:], key=key)
+        if ctr[0] == 0:
+            continue
+        assert [int(x) for x in bg.random_raw(4)] == po.philox4x64(ctr, key)
+
+
+def test_counter_normals_statistics_and_slicing():
+    z = po.counter_normals(11, 3, 0, 400_000)
+    assert abs(z.mean()) < 0.01 and abs(z.var() - 1.0) < 0.01
+    assert np.abs(z).max() < 5.8  # u1 >= 2^-24 bounds |z| by sqrt(2 ln 2^24)
+    # any window of the stream is the same numbers (counter-based)
+    assert np.array_equal(po.counter_normals(11, 3, 1001, 37), z[1001:1038])
+    assert not np.array_equal(po.counter_normals(11, 4, 0, 64), z[:64])
+
+
+def test_synth_counter_labels_and_composition():
+    C, d, n = 10, 6, 5000
+    mu = np.arange(C * d, dtype=np.float64).reshape(C, d)
+    sh = np.linspace(-1, 1, d)
+    X, y = po.synth_counter(7, 1, C, d, n, mu, sh)
+    assert y.min() >= 0 and y.max() < C
+    counts = np.bincount(y, minlength=C)
+    assert counts.min() > 0.8 * n / C
+    z = po.counter_normals(7, 1, 0, n * d).reshape(n, d)
+    assert np.array_equal(X, (mu[y] + z) + sh)
+    X2, y2 = po.synth_counter(7, 1, C, d, n, mu, sh)
+    assert np.array_equal(X, X2) and np.array_equal(y, y2)

@@ -115,6 +115,37 @@ def test_sweep_gpu_matches_oracle_auc_adam(paradigm):
     assert abs(g["accuracy"] - o["accuracy"]) <= 0.01, (g["accuracy"], o["accuracy"])
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("paradigm", ["model", "mapping"])
+def test_sweep_gpu_counter_data_matches_oracle_auc(paradigm):
+    # device-born pools (8(f) f3) vs the oracle restatement of the same stream
+    from paper_2011_09463_b200.sweep import GpuBackend
+
+    g = run_sweep(SweepConfig(paradigm=paradigm, data_rng="counter", **MID), GpuBackend())
+    o = run_sweep(SweepConfig(paradigm=paradigm, data_rng="counter", **MID), OracleBackend())
+    assert abs(g["auc"] - o["auc"]) <= 0.01, (g["auc"], o["auc"])
+    assert abs(g["accuracy"] - o["accuracy"]) <= 0.01, (g["accuracy"], o["accuracy"])
+
+
+def test_sweep_oracle_counter_data():
+    from oracle_backend import OracleRng
+
+    from paper_2011_09463_b200.errors import ConfigError
+
+    cfg = SweepConfig(paradigm="model", data_rng="counter", **TINY)
+    a = run_sweep(cfg, OracleBackend())
+    b = run_sweep(SweepConfig(paradigm="model", data_rng="counter", **TINY), OracleBackend())
+    assert a["auc"] == b["auc"] and 0.0 <= a["auc"] <= 1.0
+    pc = Population(cfg, OracleRng, OracleBackend().synth_counter)
+    ph = Population(SweepConfig(paradigm="model", **TINY), OracleRng)
+    assert np.array_equal(pc.mu, ph.mu)  # mu / shift still come from the host stream
+    assert pc.Xt.shape == ph.Xt.shape and not np.array_equal(pc.Xt, ph.Xt)
+    with pytest.raises(ConfigError):
+        Population(cfg, OracleRng)
+    with pytest.raises(ConfigError):
+        SweepConfig(data_rng="philox").validate()
+
+
 # ----------------------------------------------------------- strict config (8(f) f4)
 def test_resolve_config_strict_and_aggregated():
     from paper_2011_09463_b200.errors import ConfigError
