@@ -114,6 +114,7 @@ enum class Epi : int {
     kSgd = 3,       // C(=W) -= lr * acc ; optionally grad_out = acc  (dW + SGD)
     kStore = 4,     // C = acc (diagnostics)
     kNone = 5,      // no output (diagnostics: epilogue without global traffic)
+    kMmdGrad = 6,   // C = scale * (add[m,n] * rowvec[m] - acc)   (MMD gradient from V = W.Z)
 };
 
 struct Gemm {
@@ -190,6 +191,8 @@ struct UmmaGemm {
     float lr = 0.f;
     float* grad_out = nullptr;
     float* colsum = nullptr;  // kMask: per-32-row-block column sums [G][ceil(M/32)][N]
+    const float* rowvec = nullptr;  // kMmdGrad: per-row scalar [G][M]
+    float scale = 1.f;              // kMmdGrad
     int* flags = nullptr;
 };
 void launch_umma(const UmmaGemm& u, cudaStream_t s);

@@ -21,6 +21,7 @@
 // One warp issues TMA, one issues MMAs, four run the exp epilogue.
 #include <cuda.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -678,6 +679,432 @@ __global__ void __launch_bounds__(256) mmd_prep_kernel(const float* Xs, long lon
     }
 }
 
+// ---------------------------------------------------------------------------
+// Materialised-W path (bank steps with gradients, N = m + n small enough that
+// W [G][N][N] fits the scratch budget).  The kernel matrix is symmetric, so
+// pass 1 visits each unordered 128 x 128 tile pair (I <= J) ONCE:
+//   S_IJ = Z_I . Z_J^T      (3xTF32 on the rna planes: one N=256 MMA over
+//                            [Z_J lo | Z_J hi] plus an N=128 Z_I lo . Z_J hi)
+//   exp epilogue -> w_ij, written to W at (i, j) and, for I < J, at (j, i)
+//   (the transposed store is coalesced: lanes are consecutive i);
+//   per-tile partials: row sums of w (rows of I), column sums (rows of J),
+//   the three kernel sums with the pair multiplicities of the V-statistic.
+// Then V = W . Z is a plain grouped 3xTF32 GEMM (umma_kernel) whose epilogue
+// forms g = scale * (z * Wsum - V) (Epi::kMmdGrad).  GEMM1 work is halved
+// against the fused kernel, which evaluates every ordered pair.
+constexpr int WT = 128;
+constexpr int W_STAGES = 2;
+constexpr int W_STAGE_BYTES = 4 * (WT * KC * 4);  // Z_I hi, Z_I lo, Z_J lo, Z_J hi: 64 KB
+constexpr int W_TILE_LD = 33;  // per-warp 32 x 32 transpose tile, padded (conflict-free)
+constexpr int W_SMEM_BYTES = W_STAGES * W_STAGE_BYTES + 1024 + 256 + 16 * 32 * W_TILE_LD * 4;
+static_assert(W_SMEM_BYTES <= 232448, "mmd_w_kernel smem");
+constexpr int W_EPI_WARPS = 16;  // 4 per TMEM lane quarter, 32 columns each
+constexpr int W_THREADS = 64 + 32 * W_EPI_WARPS;
+
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+struct MmdWParams {
+    CUtensorMap zk_hi, zk_lo;  // K-major (d, N, G), 64-row boxes
+    const float* norms;        // [G][N]
+    const double* beta;        // [G]
+    long long m, n;
+    int d, nb, geo5;
+    float mult[8];
+    int T, npairs, G;
+    float* W;                  // [G][N][N]
+    float* rpart;              // [G][T][T][4][WT]: row sums of block (I, J), per column quarter
+    float* cpart;              // [G][T][T][4][WT]: column sums of block (I, J) (I < J), per row quarter
+    double* kpart;             // [G][npairs][W_EPI_WARPS][3]: kernel sums per epilogue warp
+    int* flags;
+    int diag;                  // diagnostics (MTK_MMDW_DIAG): 1 = epilogue only arrives, 2 = no MMAs
+};
+
+__device__ __forceinline__ void pair_of(int p, int T, int& I, int& J) {
+    I = 0;
+    while (p >= T - I) {
+        p -= T - I;
+        ++I;
+    }
+    J = I + p;
+}
+
+// 8 column values per lane (lane = row) -> the sum over the warp's 32 rows
+// of column ((lane>>4)&1)*4 + ((lane>>3)&1)*2 + ((lane>>2)&1), complete on
+// lanes with (lane & 3) == 0.  Fixed butterfly order (deterministic).
+__device__ __forceinline__ float column_sums_8(const float (&v)[8], int lane) {
+    float a[4], b[2];
+    const bool u16 = lane & 16, u8 = lane & 8, u4 = lane & 4;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const float send = u16 ? v[c] : v[c + 4];
+        const float keep = u16 ? v[c + 4] : v[c];
+        a[c] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        const float send = u8 ? a[c] : a[c + 2];
+        const float keep = u8 ? a[c + 2] : a[c];
+        b[c] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    float x;
+    {
+        const float send = u4 ? b[0] : b[1];
+        const float keep = u4 ? b[1] : b[0];
+        x = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    x += __shfl_xor_sync(0xffffffffu, x, 2);
+    x += __shfl_xor_sync(0xffffffffu, x, 1);
+    return x;
+}
+
+__global__ void __launch_bounds__(W_THREADS, 1) mmd_w_kernel(const __grid_constant__ MmdWParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + W_STAGES * W_STAGE_BYTES);
+    uint64_t* empty = full + W_STAGES;
+    uint64_t* acc_full = empty + W_STAGES;  // [2]
+    uint64_t* acc_empty = acc_full + 2;     // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+    float* wtile = reinterpret_cast<float*>(smem + W_STAGES * W_STAGE_BYTES + 256);  // [16][32][33]
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long N = p.m + p.n;
+    const int nkc = (p.d + KC - 1) / KC;
+    const int total = p.G * p.npairs;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&p.zk_hi);
+        tma_prefetch(&p.zk_lo);
+        for (int s = 0; s < W_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&acc_full[b], 1);
+            mbar_init(&acc_empty[b], 32 * W_EPI_WARPS);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------- TMA producer ----------------
+        int st = 0;
+        for (int item = blockIdx.x; item < total; item += gridDim.x) {
+            const int g = item / p.npairs;
+            int I, J;
+            pair_of(item % p.npairs, p.T, I, J);
+            const int i0 = I * WT, j0 = J * WT;
+            for (int kc = 0; kc < nkc; ++kc, ++st) {
+                const int s = st % W_STAGES;
+                mbar_wait(&empty[s], ((st / W_STAGES) & 1) ^ 1);
+                if (lane == 0) {
+                    uint8_t* b = smem + s * W_STAGE_BYTES;
+                    const int k0 = kc * KC;
+                    mbar_expect_tx(&full[s], W_STAGE_BYTES);
+                    tma_load_3d(b, &p.zk_hi, &full[s], k0, i0, g);
+                    tma_load_3d(b + 8192, &p.zk_hi, &full[s], k0, i0 + 64, g);
+                    tma_load_3d(b + 16384, &p.zk_lo, &full[s], k0, i0, g);
+                    tma_load_3d(b + 24576, &p.zk_lo, &full[s], k0, i0 + 64, g);
+                    tma_load_3d(b + 32768, &p.zk_lo, &full[s], k0, j0, g);
+                    tma_load_3d(b + 40960, &p.zk_lo, &full[s], k0, j0 + 64, g);
+                    tma_load_3d(b + 49152, &p.zk_hi, &full[s], k0, j0, g);
+                    tma_load_3d(b + 57344, &p.zk_hi, &full[s], k0, j0 + 64, g);
+                }
+                __syncwarp();
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer ----------------
+        constexpr uint32_t idw = idesc_tf32(WT, 2 * WT, 0, 0);
+        constexpr uint32_t idn = idesc_tf32(WT, WT, 0, 0);
+        int st = 0, lt = 0;
+        for (int item = blockIdx.x; item < total; item += gridDim.x, ++lt) {
+            const int buf = lt & 1;
+            const uint32_t tS = tmem + buf * 256;
+            mbar_wait(&acc_empty[buf], ((lt >> 1) & 1) ^ 1);
+            tc_fence_after();
+            for (int kc = 0; kc < nkc; ++kc, ++st) {
+                const int s = st % W_STAGES;
+                mbar_wait(&full[s], (st / W_STAGES) & 1);
+                tc_fence_after();
+                const uint32_t b = smem_u32(smem + s * W_STAGE_BYTES);
+                if (lane == 0) {
+#pragma unroll
+                    for (int kk = 0; kk < KC / 8; ++kk) {
+                        if (p.diag == 2) break;
+                        const uint64_t ahi = smem_desc(b + kk * 32, 16, 1024, 2);
+                        const uint64_t alo = smem_desc(b + 16384 + kk * 32, 16, 1024, 2);
+                        const uint64_t blh = smem_desc(b + 32768 + kk * 32, 16, 1024, 2);  // lo 128 | hi 128
+                        const uint64_t bhi = smem_desc(b + 49152 + kk * 32, 16, 1024, 2);
+                        mma_tf32(tS, ahi, blh, idw, (kc | kk) ? 1u : 0u);
+                        mma_tf32(tS + WT, alo, bhi, idn, 1u);
+                    }
+                    mma_commit(&empty[s]);
+                }
+                __syncwarp();
+            }
+            if (lane == 0) mma_commit(&acc_full[buf]);
+            __syncwarp();
+        }
+    } else {
+        // ---------------- epilogue: exp -> w, stores, partials ----------------
+        // 16 warps: warp w covers TMEM lane quarter q = w % 4 (rows 32q..32q+31)
+        // and column quarter h (32 columns); four warps share each scheduler.
+        // Partials go straight to global memory (no block barriers); the
+        // wsum kernel combines them in a fixed order.
+        const int q = warp & 3, h = (warp - 2) >> 2;
+        const int r = 32 * q + lane;
+        const int ew = warp - 2;
+        float* tw = wtile + ew * 32 * W_TILE_LD;
+        const uint32_t lane_base = (uint32_t)(32 * q) << 16;
+        const float cSS = (float)(-2.0 / ((double)p.m * (double)p.m));
+        const float cTT = (float)(-2.0 / ((double)p.n * (double)p.n));
+        const float cST = (float)(2.0 / ((double)p.m * (double)p.n));
+        int lt = 0;
+        bool bad = false;
+        for (int item = blockIdx.x; item < total; item += gridDim.x, ++lt) {
+            const int g = item / p.npairs;
+            const int pidx = item % p.npairs;
+            int I, J;
+            pair_of(pidx, p.T, I, J);
+            const bool diag = I == J;
+            const long long gi = (long long)I * WT + r;
+            const bool row_ok = gi < N;
+            const bool si = gi < p.m;
+            const double beta = p.beta[g];
+            const float x1 = (float)(-1.4426950408889634 / beta);
+            const float tb = (float)(2.0 / beta);
+            float nscale[8], two_inv[8];
+            if (!p.geo5) {  // general bandwidth set: per-bandwidth scales
+#pragma unroll
+                for (int b = 0; b < 8; ++b) {
+                    const double sb = beta * (double)p.mult[b];
+                    nscale[b] = b < p.nb ? (float)(-1.4426950408889634 / sb) : 0.f;
+                    two_inv[b] = b < p.nb ? (float)(2.0 / sb) : 0.f;
+                }
+            }
+            const float* nrm = p.norms + (long long)g * N;
+            const float ni = row_ok ? nrm[gi] : 0.f;
+            float* Wg = p.W + (long long)g * N * N;
+            const int buf = lt & 1;
+            mbar_wait(&acc_full[buf], (lt >> 1) & 1);
+            tc_fence_after();
+            float kss = 0.f, ktt = 0.f, kst = 0.f, rowp = 0.f;
+            const float mo = diag ? 1.f : 2.f;  // an off-diagonal unordered pair stands for two
+#pragma unroll 1
+            for (int ch = 4 * h; ch < 4 * h + 4; ++ch) {
+                if (p.diag == 1) break;
+                float sv[8];
+                {
+                    float sh[8];
+                    tmem_ld_32x8(tmem + lane_base + buf * 256 + ch * 8, sv);
+                    tmem_ld_32x8(tmem + lane_base + buf * 256 + WT + ch * 8, sh);
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) sv[c] += sh[c];
+                }
+                const long long jb = (long long)J * WT + ch * 8;
+                const bool full8 = jb + 8 <= N;
+                float nj[8];
+                if (full8) {
+                    const float4 a = __ldg(reinterpret_cast<const float4*>(nrm + jb));
+                    const float4 b = __ldg(reinterpret_cast<const float4*>(nrm + jb + 4));
+                    nj[0] = a.x; nj[1] = a.y; nj[2] = a.z; nj[3] = a.w;
+                    nj[4] = b.x; nj[5] = b.y; nj[6] = b.z; nj[7] = b.w;
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) nj[c] = jb + c < N ? __ldg(nrm + jb + c) : 0.f;
+                }
+                float kv8[8], A8[8];
+                if (p.geo5) {
+                    // packed fp32x2 arithmetic (FFMA2 / FMUL2 / FADD2), two columns per op
+                    const float2 ni2 = make_float2(ni, ni), m2 = make_float2(-2.f, -2.f);
+                    const float2 x1v = make_float2(x1, x1), x4v = make_float2(0.25f * x1, 0.25f * x1);
+                    const float2 c4 = make_float2(4.f, 4.f), c2 = make_float2(2.f, 2.f);
+                    const float2 ch5 = make_float2(0.5f, 0.5f), cq = make_float2(0.25f, 0.25f);
+                    const float2 tbv = make_float2(tb, tb);
+#pragma unroll
+                    for (int c = 0; c < 8; c += 2) {
+                        float2 d = __ffma2_rn(m2, make_float2(sv[c], sv[c + 1]),
+                                              __fadd2_rn(ni2, make_float2(nj[c], nj[c + 1])));
+                        d.x = fmaxf(d.x, 0.f);
+                        d.y = fmaxf(d.y, 0.f);
+                        const float2 a1 = __fmul2_rn(d, x1v), a4 = __fmul2_rn(d, x4v);
+                        const float2 e1 = make_float2(ex2_approx(a1.x), ex2_approx(a1.y));
+                        const float2 e4 = make_float2(ex2_approx(a4.x), ex2_approx(a4.y));
+                        const float2 e2 = __fmul2_rn(e4, e4);
+                        const float2 eh = __fmul2_rn(e1, e1);
+                        const float2 eq = __fmul2_rn(eh, eh);
+                        const float2 kv = __fadd2_rn(__fadd2_rn(__fadd2_rn(eq, eh), __fadd2_rn(e1, e2)), e4);
+                        const float2 u = __ffma2_rn(c4, eq, __fmul2_rn(c2, eh));
+                        const float2 v = __ffma2_rn(ch5, e2, e1);
+                        const float2 A = __fmul2_rn(tbv, __ffma2_rn(cq, e4, __fadd2_rn(u, v)));
+                        kv8[c] = kv.x;
+                        kv8[c + 1] = kv.y;
+                        A8[c] = A.x;
+                        A8[c + 1] = A.y;
+                    }
+                } else {
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    const float d2 = fmaxf(ni + nj[c] - 2.f * sv[c], 0.f);
+                    {
+                        float kv = 0.f, A = 0.f;
+#pragma unroll
+                        for (int b = 0; b < 8; ++b) {
+                            if (b >= p.nb) break;
+                            const float e = exp2f(d2 * nscale[b]);
+                            kv += e;
+                            A = fmaf(two_inv[b], e, A);
+                        }
+                        kv8[c] = kv;
+                        A8[c] = A;
+                    }
+                }
+                }
+                float wv[8];
+                const bool sj_all = jb + 8 <= p.m, tj_all = jb >= p.m;
+                if (row_ok && full8 && (sj_all || tj_all) && !(diag && gi >= jb && gi < jb + 8)) {
+                    // one domain pair for the whole chunk, no diagonal element
+                    const float cw = si ? (sj_all ? cSS : cST) : (sj_all ? cST : cTT);
+                    float ks = 0.f;
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        ks += kv8[c];
+                        wv[c] = cw * A8[c];
+                        rowp += wv[c];
+                    }
+                    if (si == sj_all) {  // same domain
+                        if (si) kss += mo * ks;
+                        else ktt += mo * ks;
+                    } else if (!diag || si) {
+                        kst += ks;  // a mixed unordered pair counts once, as (s, t)
+                    }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const long long gj = jb + c;
+                        float w = 0.f;
+                        if (row_ok && gj < N) {
+                            const bool sj = gj < p.m;
+                            if (si && sj) {
+                                kss += mo * kv8[c];
+                                w = cSS * A8[c];
+                            } else if (!si && !sj) {
+                                ktt += mo * kv8[c];
+                                w = cTT * A8[c];
+                            } else {
+                                if (!diag || si) kst += kv8[c];
+                                w = cST * A8[c];
+                            }
+                            if (gj == gi) w = 0.f;
+                        }
+                        wv[c] = w;
+                        rowp += w;
+                    }
+                }
+                // (i, j) goes through the warp's smem tile (row = lane) and leaves
+                // as coalesced 128-B row segments after the last chunk
+#pragma unroll
+                for (int c = 0; c < 8; ++c) tw[lane * W_TILE_LD + (ch - 4 * h) * 8 + c] = wv[c];
+                if (!diag) {
+                    // (j, i): lanes are consecutive i -> one 128-B row segment per store
+                    float* dt = Wg + jb * N + gi;
+                    if (p.diag == 3 || p.diag == 4) {
+                    } else if (row_ok && full8) {
+#pragma unroll
+                        for (int c = 0; c < 8; ++c) dt[c * N] = wv[c];
+                    } else if (row_ok) {
+                        for (int c = 0; c < 8 && jb + c < N; ++c) dt[c * N] = wv[c];
+                    }
+                    const float cs = column_sums_8(wv, lane);
+                    if ((lane & 3) == 0)
+                        p.cpart[((((long long)g * p.T + I) * p.T + J) * 4 + q) * WT + ch * 8 +
+                                ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1)] = cs;
+                }
+            }
+            bad |= !isfinite(rowp);
+            tc_fence_before();
+            mbar_arrive(&acc_empty[buf]);
+            __syncwarp();
+            if (p.diag != 3 && p.diag != 5) {
+                const long long jc = (long long)J * WT + 32 * h + lane;
+                const long long r0 = (long long)I * WT + 32 * q;
+                if (jc < N)
+#pragma unroll 8
+                    for (int rr = 0; rr < 32; ++rr)
+                        if (r0 + rr < N) Wg[(r0 + rr) * N + jc] = tw[rr * W_TILE_LD + lane];
+            }
+            __syncwarp();
+
+            p.rpart[((((long long)g * p.T + I) * p.T + J) * 4 + h) * WT + r] = rowp;
+            // this warp's kernel sums: fixed butterfly over the 32 rows, fp64
+            double kd[3] = {(double)kss, (double)ktt, (double)kst};
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) kd[c] += __shfl_xor_sync(0xffffffffu, kd[c], o);
+            if (lane < 3) {
+                const double v = lane == 0 ? kd[0] : (lane == 1 ? kd[1] : kd[2]);
+                p.kpart[(((long long)g * p.npairs + pidx) * W_EPI_WARPS + ew) * 3 + lane] = v;
+            }
+        }
+        if (bad && p.flags) atomicOr(p.flags, kFlagNonFinite);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc<512>(tmem);
+    }
+}
+
+// Wsum_i = sum over column blocks J of block (R, J)'s row sums, R = i / WT:
+// for J >= R the four column-quarter row sums of pair (R, J), for J < R the
+// four row-quarter column sums of pair (J, R) -- fixed order, fp64.  Also the
+// kernel-sum partials per 128-row block in the fused kernel's layout:
+// partial[g][I][c] = sum_{J >= I} sum_w kpart[g][pair(I, J)][w][c].
+__global__ void mmd_wsum_kernel(const float* rpart, const float* cpart, const double* kpart, int G,
+                                long long N, int T, int npairs, float* wsum, double* partial) {
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (t < (long long)G * N) {
+        const int g = (int)(t / N);
+        const long long i = t % N;
+        const int R = (int)(i / WT), r = (int)(i % WT);
+        double s = 0.0;
+#pragma unroll 4
+        for (int J = 0; J < T; ++J) {
+            const float* src = J >= R ? rpart + ((((long long)g * T + R) * T + J) * 4) * WT
+                                      : cpart + ((((long long)g * T + J) * T + R) * 4) * WT;
+            s += (double)(((src[r] + src[WT + r]) + src[2 * WT + r]) + src[3 * WT + r]);
+        }
+        wsum[t] = (float)s;
+    }
+    if (t < (long long)G * T * 3) {
+        const int g = (int)(t / (3 * T)), I = (int)((t / 3) % T), c = (int)(t % 3);
+        int base = 0;
+        for (int k = 0; k < I; ++k) base += T - k;
+        double s = 0.0;
+        for (int J = I; J < T; ++J) {
+            const double* kp = kpart + ((long long)g * npairs + base + (J - I)) * W_EPI_WARPS * 3 + c;
+            double v[W_EPI_WARPS];  // all loads in flight, then the fixed-order sum
+#pragma unroll
+            for (int w = 0; w < W_EPI_WARPS; ++w) v[w] = kp[w * 3];
+#pragma unroll
+            for (int w = 0; w < W_EPI_WARPS; ++w) s += v[w];
+        }
+        partial[((long long)g * T + I) * 3 + c] = s;
+    }
+}
+
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                               const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                               const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -724,6 +1151,49 @@ int mmd_tc_blocks_per_group(const MmdArgs& a) {
     return (int)((re - a.row_begin + TI - 1) / TI);
 }
 
+// the materialised-W path (mmd_w_kernel + a grouped GEMM): bank-shaped calls
+// with gradients whose samples and gradients are each one contiguous
+// [G][m+n][d] block and whose W fits the budget; MTK_MMD_FUSED=1 forces the
+// fused kernel (A/B)
+static bool w_path(const MmdArgs& a) {
+    static const bool fused = getenv("MTK_MMD_FUSED") != nullptr;
+    const long long N = a.m + a.n;
+    if (fused || !a.gXs || !a.gXt || a.m <= 0 || a.n <= 0) return false;
+    if (a.row_begin != 0 || (a.row_end >= 0 && a.row_end != N)) return false;
+    if (a.d % 4 || a.d < 32 || N % 4) return false;
+    if (a.Xt != a.Xs + a.m * a.d || a.xt_gs != a.xs_gs || a.xs_gs < N * a.d) return false;
+    if (a.gXt != a.gXs + a.m * a.d || a.gt_gs != a.gs_gs || a.gs_gs != a.xs_gs) return false;
+    return (double)a.G * N * N * 4.0 <= 2.0 * 1024 * 1024 * 1024;
+}
+
+struct WLayout {
+    float* W;
+    float* rpart;
+    float* cpart;
+    double* kpart;
+    float* wsum;
+    size_t bytes;
+};
+static WLayout w_layout(const MmdArgs& a, uintptr_t base) {
+    const long long N = a.m + a.n;
+    const int T = (int)((N + WT - 1) / WT), np = T * (T + 1) / 2;
+    WLayout L;
+    uintptr_t cur = (base + 255) & ~uintptr_t(255);
+    const uintptr_t start = cur;
+    L.W = reinterpret_cast<float*>(cur);
+    cur = (cur + (size_t)a.G * N * N * 4 + 255) & ~uintptr_t(255);
+    L.rpart = reinterpret_cast<float*>(cur);
+    cur = (cur + (size_t)a.G * T * T * 4 * WT * 4 + 255) & ~uintptr_t(255);
+    L.cpart = reinterpret_cast<float*>(cur);
+    cur = (cur + (size_t)a.G * T * T * 4 * WT * 4 + 255) & ~uintptr_t(255);
+    L.kpart = reinterpret_cast<double*>(cur);
+    cur = (cur + (size_t)a.G * np * W_EPI_WARPS * 3 * 8 + 255) & ~uintptr_t(255);
+    L.wsum = reinterpret_cast<float*>(cur);
+    cur = (cur + (size_t)a.G * N * 4 + 255) & ~uintptr_t(255);
+    L.bytes = cur - start + 256;
+    return L;
+}
+
 static bool needs_flush(const MmdArgs& a) {
     const long long N = a.m + a.n;
     const bool grads = a.gXs || a.gXt;
@@ -736,6 +1206,7 @@ size_t mmd_tc_scratch_bytes(const MmdArgs& a) {
     b += 2 * ((size_t)a.G * N * a.d * sizeof(float) + 256);
     if (a.beta_out) b += (size_t)a.G * ((N + kBetaRows - 1) / kBetaRows) * (a.d + 1) * sizeof(double) + 256;
     if (needs_flush(a)) b += (size_t)a.G * N * a.d * sizeof(double) + 256;
+    if (w_path(a)) b += w_layout(a, 0).bytes + 256;
     return b;
 }
 
@@ -756,6 +1227,8 @@ void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s, int stages) 
         cur = (cur + (size_t)a.G * N * a.d * sizeof(double) + 255) & ~uintptr_t(255);
     }
     double* bpart = a.beta_out ? reinterpret_cast<double*>(cur) : nullptr;
+    if (bpart) cur = (cur + (size_t)a.G * ((N + kBetaRows - 1) / kBetaRows) * (a.d + 1) * sizeof(double) + 255) &
+                     ~uintptr_t(255);
     constexpr int kFusedBetaMaxD = 512;  // colsum smem: 8 warps x d doubles
     const bool fused_beta = bpart && a.d <= kFusedBetaMaxD;
     if (stages & kMmdPrep) {
@@ -773,6 +1246,70 @@ void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s, int stages) 
     }
     if (!(stages & kMmdPairs)) return;
     const long long zgs = N * a.d;
+    if (w_path(a)) {
+        const WLayout L = w_layout(a, cur);
+        const int T = (int)((N + WT - 1) / WT), np = T * (T + 1) / 2;
+        MmdWParams w;
+        std::memset(&w, 0, sizeof(w));
+        w.zk_hi = zmap(zhi, a.d, N, a.G, zgs, 64, false);
+        w.zk_lo = zmap(zlo, a.d, N, a.G, zgs, 64, false);
+        w.norms = norms;
+        w.beta = a.beta;
+        w.m = a.m;
+        w.n = a.n;
+        w.d = a.d;
+        w.nb = a.nb;
+        for (int b = 0; b < 8; ++b) w.mult[b] = a.mult[b] > 0 ? a.mult[b] : 1.f;
+        w.geo5 = a.nb == 5 && a.mult[0] == 0.25f && a.mult[1] == 0.5f && a.mult[2] == 1.f &&
+                 a.mult[3] == 2.f && a.mult[4] == 4.f;
+        w.T = T;
+        w.npairs = np;
+        w.G = a.G;
+        w.W = L.W;
+        w.rpart = L.rpart;
+        w.cpart = L.cpart;
+        w.kpart = L.kpart;
+        w.flags = a.flags;
+        if (const char* e = getenv("MTK_MMDW_DIAG")) w.diag = atoi(e);
+        static bool wattr = false;
+        if (!wattr) {
+            MTK_CUDA(cudaFuncSetAttribute(mmd_w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          W_SMEM_BYTES));
+            wattr = true;
+        }
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+        const int items = a.G * np;
+        mmd_w_kernel<<<std::min(items, sms), W_THREADS, W_SMEM_BYTES, s>>>(w);
+        count_launch();
+        const long long nt = std::max((long long)a.G * N, (long long)a.G * T * 3);
+        mmd_wsum_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, s>>>(L.rpart, L.cpart, L.kpart, a.G, N, T,
+                                                                     np, L.wsum, a.partial);
+        count_launch();
+        UmmaGemm u;
+        u.G = a.G;
+        u.M = (int)N;
+        u.N = a.d;
+        u.K = (int)N;
+        u.a_mn = 0;
+        u.a = L.W;
+        u.a_rs = N;
+        u.a_gs = N * N;
+        u.b_mn = 1;
+        u.b = a.Xs;
+        u.b_rs = a.d;
+        u.b_gs = a.xs_gs;
+        u.epi = Epi::kMmdGrad;
+        u.C = a.gXs;
+        u.c_gs = a.gs_gs;
+        u.ldc = a.d;
+        u.add = a.Xs;
+        u.rowvec = L.wsum;
+        u.scale = a.grad_scale;
+        u.flags = a.flags;
+        launch_umma(u, s);
+        return;
+    }
     MmdTcParams p;
     std::memset(&p, 0, sizeof(p));
     p.zk_hi = zmap(zhi, a.d, N, a.G, zgs, 64, false);  // 64-row boxes (two per 128-row tile)

@@ -74,6 +74,8 @@ struct UmmaParams {
     float lr;
     float* grad_out;
     float* colsum;     // kMask: per-32-row-block column sums of C, [G][ceil(M/32)][N], or null
+    const float* rowvec;  // kMmdGrad: [G][M]
+    float scale;          // kMmdGrad
     int* flags;
     unsigned long long* trace;  // diagnostics: timestamps of CTA (0,0,0)
 };
@@ -207,6 +209,7 @@ __device__ __forceinline__ void epilogue_rows(const UmmaParams& p, uint32_t tmem
             if (epi == (int)Epi::kBias || epi == (int)Epi::kBiasRelu) s1 = p.bias + g * p.bias_gs + nb;
             else if (epi == (int)Epi::kMask) { s1 = p.mask + rowbase + nb; s2 = p.add ? p.add + rowbase + nb : nullptr; }
             else if (epi == (int)Epi::kSgd) s1 = p.C + rowbase + nb;
+            else if (epi == (int)Epi::kMmdGrad) s1 = p.add + rowbase + nb;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 o1[j] = s1 ? *reinterpret_cast<const float4*>(s1 + 4 * j) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -243,6 +246,13 @@ __device__ __forceinline__ void epilogue_rows(const UmmaParams& p, uint32_t tmem
                     x.y = o1[j].y > 0.f ? x.y : 0.f;
                     x.z = o1[j].z > 0.f ? x.z : 0.f;
                     x.w = o1[j].w > 0.f ? x.w : 0.f;
+                } else if (epi == (int)Epi::kMmdGrad) {  // o1 = z row, rowvec = Wsum
+                    const float rv = p.rowvec[(long long)g * p.M + m];
+                    x.x = p.scale * fmaf(o1[j].x, rv, -x.x);
+                    x.y = p.scale * fmaf(o1[j].y, rv, -x.y);
+                    x.z = p.scale * fmaf(o1[j].z, rv, -x.z);
+                    x.w = p.scale * fmaf(o1[j].w, rv, -x.w);
+                    bad |= !(isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w));
                 } else if (epi == (int)Epi::kSgd) {  // C is the fp32 master weight
                     if (p.grad_out) *reinterpret_cast<float4*>(p.grad_out + idx) = x;
                     x.x = sgd_update(o1[j].x, x.x, p.lr);
@@ -271,6 +281,9 @@ __device__ __forceinline__ void epilogue_rows(const UmmaParams& p, uint32_t tmem
                     } else if (epi == (int)Epi::kMask) {
                         if (p.add) x = p.add[idx] + x;
                         x = (p.mask[idx] > 0.f) ? x : 0.f;
+                    } else if (epi == (int)Epi::kMmdGrad) {
+                        x = p.scale * fmaf(p.add[idx], p.rowvec[(long long)g * p.M + m], -x);
+                        bad |= !isfinite(x);
                     } else if (epi == (int)Epi::kSgd) {
                         if (p.grad_out) p.grad_out[idx] = x;
                         x = sgd_update(p.C[idx], x, p.lr);
@@ -303,6 +316,7 @@ __device__ __forceinline__ void prefetch_epilogue_rows(const UmmaParams& p, int 
     const float* src[2] = {nullptr, nullptr};
     if (p.epi == (int)Epi::kSgd) src[0] = p.C;
     else if (p.epi == (int)Epi::kMask) { src[0] = p.mask; src[1] = p.add; }
+    else if (p.epi == (int)Epi::kMmdGrad) src[0] = p.add;
     if (!src[0]) return;
     const int n1 = min(n0 + ncols, p.N);
     if (n1 <= n0) return;
@@ -638,6 +652,8 @@ void launch_umma(const UmmaGemm& u, cudaStream_t s) {
     p.lr = u.lr;
     p.grad_out = u.grad_out;
     p.colsum = u.colsum;
+    p.rowvec = u.rowvec;
+    p.scale = u.scale;
     p.flags = u.flags;
     if (const char* t = getenv("MTK_UMMA_TRACE"))
         p.trace = reinterpret_cast<unsigned long long*>(strtoull(t, nullptr, 0));
