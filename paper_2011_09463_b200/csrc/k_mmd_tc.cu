@@ -1156,7 +1156,8 @@ int mmd_tc_blocks_per_group(const MmdArgs& a) {
 // [G][m+n][d] block and whose W fits the budget; MTK_MMD_FUSED=1 forces the
 // fused kernel (A/B)
 static bool w_path(const MmdArgs& a) {
-    static const bool fused = getenv("MTK_MMD_FUSED") != nullptr;
+    const char* fe = getenv("MTK_MMD_FUSED");
+    const bool fused = fe && fe[0] == '1';
     const long long N = a.m + a.n;
     if (fused || !a.gXs || !a.gXt || a.m <= 0 || a.n <= 0) return false;
     if (a.row_begin != 0 || (a.row_end >= 0 && a.row_end != N)) return false;

@@ -132,6 +132,27 @@ def test_step_c2_shape_with_mmd(ctx):
     check_step(bank, X, y, src=48, lam=1.0, tol=2e-5)
 
 
+@pytest.mark.parametrize("B,src,dims", [(300, 140, [96, 64, 10]), (1024, 512, [1024, 512, 256, 10]),
+                                        (260, 100, [64, 48, 7])])
+def test_mmd_materialised_w_path_matches_fused(ctx, monkeypatch, B, src, dims):
+    """The bank's MMD runs on the materialised-W path (each unordered tile
+    pair once + a GEMM for V) unless MTK_MMD_FUSED=1; both must give the same
+    step (ragged tiles: N = 300 / 260 is not a multiple of 128)."""
+    X, y = inputs(3, B, dims[0], dims[-1], shift=0.4)
+    Xd, yd = to_dev(X, y)
+    res = []
+    for fused in ("0", "1"):
+        monkeypatch.setenv("MTK_MMD_FUSED", fused)
+        bank = make_bank(ctx, 3, dims, seed=5)
+        bank.keep_grads(True)
+        loss, mmd = bank.train_step(Xd, yd, lr=0.05, src_rows=src, mmd_lambda=0.8)
+        res.append((loss, mmd, bank.get_grads(2)[0]))
+    (l0, m0, g0), (l1, m1, g1) = res
+    assert rel(l0, l1) <= 1e-6 and rel(m0, m1) <= 1e-5, (m0, m1)
+    for a, b in zip(g0, g1):
+        assert rel(a, b) <= 2e-5
+
+
 def test_step_two_heads_parameter_based(ctx):
     dims = [784, 256, 10]
     bank = make_bank(ctx, 3, dims, n_heads=2)
