@@ -1069,13 +1069,20 @@ __global__ void __launch_bounds__(W_THREADS, 1) mmd_w_kernel(const __grid_consta
 
 // Wsum_i = sum over column blocks J of block (R, J)'s row sums, R = i / WT:
 // for J >= R the four column-quarter row sums of pair (R, J), for J < R the
-// four row-quarter column sums of pair (J, R) -- fixed order, fp64.  Also the
-// kernel-sum partials per 128-row block in the fused kernel's layout:
-// partial[g][I][c] = sum_{J >= I} sum_w kpart[g][pair(I, J)][w][c].
-__global__ void mmd_wsum_kernel(const float* rpart, const float* cpart, const double* kpart, int G,
-                                long long N, int T, int npairs, float* wsum, double* partial) {
-    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (t < (long long)G * N) {
+// four row-quarter column sums of pair (J, R) -- fixed order, fp64.  Blocks
+// past the Wsum range each take one (g, I) and form the kernel-sum partials
+// in the fused kernel's layout: partial[g][I][c] = sum_{J >= I} sum_w
+// kpart[g][pair(I, J)][w][c] (every load in flight, then fixed-order sums).
+constexpr int WSUM_THREADS = 256;
+__global__ void __launch_bounds__(WSUM_THREADS) mmd_wsum_kernel(const float* rpart, const float* cpart,
+                                                                const double* kpart, int G, long long N,
+                                                                int T, int npairs, float* wsum,
+                                                                double* partial) {
+    __shared__ double jsum[3][WSUM_THREADS / 3 + 1];
+    const long long nbw = ((long long)G * N + WSUM_THREADS - 1) / WSUM_THREADS;
+    if (blockIdx.x < nbw) {
+        const long long t = blockIdx.x * (long long)WSUM_THREADS + threadIdx.x;
+        if (t >= (long long)G * N) return;
         const int g = (int)(t / N);
         const long long i = t % N;
         const int R = (int)(i / WT), r = (int)(i % WT);
@@ -1087,22 +1094,34 @@ __global__ void mmd_wsum_kernel(const float* rpart, const float* cpart, const do
             s += (double)(((src[r] + src[WT + r]) + src[2 * WT + r]) + src[3 * WT + r]);
         }
         wsum[t] = (float)s;
+        return;
     }
-    if (t < (long long)G * T * 3) {
-        const int g = (int)(t / (3 * T)), I = (int)((t / 3) % T), c = (int)(t % 3);
-        int base = 0;
-        for (int k = 0; k < I; ++k) base += T - k;
-        double s = 0.0;
-        for (int J = I; J < T; ++J) {
-            const double* kp = kpart + ((long long)g * npairs + base + (J - I)) * W_EPI_WARPS * 3 + c;
-            double v[W_EPI_WARPS];  // all loads in flight, then the fixed-order sum
+    const int gi = (int)(blockIdx.x - nbw), g = gi / T, I = gi % T;
+    int base = 0;
+    for (int k = 0; k < I; ++k) base += T - k;
+    const int nJ = T - I;
+    double total[3] = {0.0, 0.0, 0.0};
+    // chunks of up to WSUM_THREADS / 3 column blocks: thread (c, jj) sums the
+    // 16 warp partials of pair (I, I + j0 + jj), then threads c < 3 add the
+    // chunk in ascending J
+    for (int j0 = 0; j0 < nJ; j0 += WSUM_THREADS / 3) {
+        const int c = threadIdx.x / (WSUM_THREADS / 3), jj = threadIdx.x % (WSUM_THREADS / 3);
+        if (c < 3 && j0 + jj < nJ) {
+            const double* kp = kpart + ((long long)g * npairs + base + j0 + jj) * W_EPI_WARPS * 3 + c;
+            double v[W_EPI_WARPS];
 #pragma unroll
             for (int w = 0; w < W_EPI_WARPS; ++w) v[w] = kp[w * 3];
+            double a = 0.0;
 #pragma unroll
-            for (int w = 0; w < W_EPI_WARPS; ++w) s += v[w];
+            for (int w = 0; w < W_EPI_WARPS; ++w) a += v[w];
+            jsum[c][jj] = a;
         }
-        partial[((long long)g * T + I) * 3 + c] = s;
+        __syncthreads();
+        if (threadIdx.x < 3)
+            for (int jj2 = 0; jj2 < WSUM_THREADS / 3 && j0 + jj2 < nJ; ++jj2) total[threadIdx.x] += jsum[threadIdx.x][jj2];
+        __syncthreads();
     }
+    if (threadIdx.x < 3) partial[((long long)g * T + I) * 3 + threadIdx.x] = total[threadIdx.x];
 }
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -1283,9 +1302,9 @@ void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s, int stages) 
         const int items = a.G * np;
         mmd_w_kernel<<<std::min(items, sms), W_THREADS, W_SMEM_BYTES, s>>>(w);
         count_launch();
-        const long long nt = std::max((long long)a.G * N, (long long)a.G * T * 3);
-        mmd_wsum_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, s>>>(L.rpart, L.cpart, L.kpart, a.G, N, T,
-                                                                     np, L.wsum, a.partial);
+        const long long nbw = ((long long)a.G * N + WSUM_THREADS - 1) / WSUM_THREADS;
+        mmd_wsum_kernel<<<(unsigned)(nbw + (long long)a.G * T), WSUM_THREADS, 0, s>>>(
+            L.rpart, L.cpart, L.kpart, a.G, N, T, np, L.wsum, a.partial);
         count_launch();
         UmmaGemm u;
         u.G = a.G;

@@ -29,7 +29,9 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-3, "us": 
          "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
 
 
-def phase_of(name):
+def phase_of(name, in_mmd=False):
+    if in_mmd or "mmd_w_kernel" in name or "mmd_wsum" in name:
+        return "mmd_pairs"  # the materialised-W path: pass 1, Wsum, V = W.Z GEMM
     if "umma_kernel<0, 1" in name or "head_fwd" in name:
         return "fwd_gemm"
     if "umma_kernel<0, 0" in name or "gemm_simt" in name or "head_dx" in name:
@@ -54,6 +56,7 @@ def main(rep, prefix):
     hdr, units = rows[0], rows[1]
     col = {h: i for i, h in enumerate(hdr)}
     kernels = []
+    in_mmd = False
     for r in rows[2:]:
         k = {"name": r[col["Kernel Name"]]}
         for key, metric in METRICS.items():
@@ -70,7 +73,11 @@ def main(rep, prefix):
             if key == "duration_us":
                 v *= SCALE.get(u, 1)
             k[key] = v
-        k["phase"] = phase_of(k["name"])
+        if "mmd_w_kernel" in k["name"]:
+            in_mmd = True
+        if "mmd_finish" in k["name"]:
+            in_mmd = False
+        k["phase"] = phase_of(k["name"], in_mmd)
         kernels.append(k)
     phases = {}
     for k in kernels:
