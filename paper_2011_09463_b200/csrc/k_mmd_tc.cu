@@ -696,7 +696,8 @@ constexpr int WT = 128;
 constexpr int W_STAGES = 2;
 constexpr int W_STAGE_BYTES = 4 * (WT * KC * 4);  // Z_I hi, Z_I lo, Z_J lo, Z_J hi: 64 KB
 constexpr int W_TILE_LD = 33;  // per-warp 32 x 32 transpose tile, padded (conflict-free)
-constexpr int W_SMEM_BYTES = W_STAGES * W_STAGE_BYTES + 1024 + 256 + 16 * 32 * W_TILE_LD * 4;
+constexpr int W_MAX_G_TAB = 2048;  // per-group exp scales kept in smem
+constexpr int W_SMEM_BYTES = W_STAGES * W_STAGE_BYTES + 1024 + 256 + 16 * 32 * W_TILE_LD * 4 + W_MAX_G_TAB * 8;
 static_assert(W_SMEM_BYTES <= 232448, "mmd_w_kernel smem");
 constexpr int W_EPI_WARPS = 16;  // 4 per TMEM lane quarter, 32 columns each
 constexpr int W_THREADS = 64 + 32 * W_EPI_WARPS;
@@ -770,6 +771,7 @@ __global__ void __launch_bounds__(W_THREADS, 1) mmd_w_kernel(const __grid_consta
     uint64_t* acc_empty = acc_full + 2;     // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
     float* wtile = reinterpret_cast<float*>(smem + W_STAGES * W_STAGE_BYTES + 256);  // [16][32][33]
+    float2* gtab = reinterpret_cast<float2*>(wtile + 16 * 32 * W_TILE_LD);            // [G]: (x1, tb)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long N = p.m + p.n;
@@ -790,6 +792,10 @@ __global__ void __launch_bounds__(W_THREADS, 1) mmd_w_kernel(const __grid_consta
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc<512>(tmem_slot);
+    for (int g = threadIdx.x; g < p.G && g < W_MAX_G_TAB; g += blockDim.x) {
+        const double beta = p.beta[g];
+        gtab[g] = make_float2((float)(-1.4426950408889634 / beta), (float)(2.0 / beta));
+    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -877,14 +883,21 @@ __global__ void __launch_bounds__(W_THREADS, 1) mmd_w_kernel(const __grid_consta
             int I, J;
             pair_of(pidx, p.T, I, J);
             const bool diag = I == J;
-            const long long gi = (long long)I * WT + r;
+            const int gi = I * WT + r;
             const bool row_ok = gi < N;
             const bool si = gi < p.m;
-            const double beta = p.beta[g];
-            const float x1 = (float)(-1.4426950408889634 / beta);
-            const float tb = (float)(2.0 / beta);
+            float x1, tb;
+            if (g < W_MAX_G_TAB) {
+                const float2 xt = gtab[g];
+                x1 = xt.x;
+                tb = xt.y;
+            } else {
+                x1 = (float)(-1.4426950408889634 / p.beta[g]);
+                tb = (float)(2.0 / p.beta[g]);
+            }
             float nscale[8], two_inv[8];
             if (!p.geo5) {  // general bandwidth set: per-bandwidth scales
+                const double beta = p.beta[g];
 #pragma unroll
                 for (int b = 0; b < 8; ++b) {
                     const double sb = beta * (double)p.mult[b];
@@ -909,9 +922,13 @@ __global__ void __launch_bounds__(W_THREADS, 1) mmd_w_kernel(const __grid_consta
                     tmem_ld_32x8(tmem + lane_base + buf * 256 + ch * 8, sv);
                     tmem_ld_32x8(tmem + lane_base + buf * 256 + WT + ch * 8, sh);
 #pragma unroll
-                    for (int c = 0; c < 8; ++c) sv[c] += sh[c];
+                    for (int c = 0; c < 8; c += 2) {
+                        const float2 t2 = __fadd2_rn(make_float2(sv[c], sv[c + 1]), make_float2(sh[c], sh[c + 1]));
+                        sv[c] = t2.x;
+                        sv[c + 1] = t2.y;
+                    }
                 }
-                const long long jb = (long long)J * WT + ch * 8;
+                const int jb = J * WT + ch * 8;  // N^2 < 2^31 on this path: 32-bit offsets
                 const bool full8 = jb + 8 <= N;
                 float nj[8];
                 if (full8) {
@@ -975,13 +992,18 @@ __global__ void __launch_bounds__(W_THREADS, 1) mmd_w_kernel(const __grid_consta
                 if (row_ok && full8 && (sj_all || tj_all) && !(diag && gi >= jb && gi < jb + 8)) {
                     // one domain pair for the whole chunk, no diagonal element
                     const float cw = si ? (sj_all ? cSS : cST) : (sj_all ? cST : cTT);
-                    float ks = 0.f;
+                    const float2 cw2 = make_float2(cw, cw);
+                    float2 ks2 = make_float2(0.f, 0.f), rp2 = make_float2(0.f, 0.f);
 #pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        ks += kv8[c];
-                        wv[c] = cw * A8[c];
-                        rowp += wv[c];
+                    for (int c = 0; c < 8; c += 2) {
+                        ks2 = __fadd2_rn(ks2, make_float2(kv8[c], kv8[c + 1]));
+                        const float2 w2 = __fmul2_rn(cw2, make_float2(A8[c], A8[c + 1]));
+                        wv[c] = w2.x;
+                        wv[c + 1] = w2.y;
+                        rp2 = __fadd2_rn(rp2, w2);
                     }
+                    const float ks = ks2.x + ks2.y;
+                    rowp += rp2.x + rp2.y;
                     if (si == sj_all) {  // same domain
                         if (si) kss += mo * ks;
                         else ktt += mo * ks;
@@ -991,7 +1013,7 @@ __global__ void __launch_bounds__(W_THREADS, 1) mmd_w_kernel(const __grid_consta
                 } else {
 #pragma unroll
                     for (int c = 0; c < 8; ++c) {
-                        const long long gj = jb + c;
+                        const int gj = jb + c;
                         float w = 0.f;
                         if (row_ok && gj < N) {
                             const bool sj = gj < p.m;
@@ -1017,11 +1039,14 @@ __global__ void __launch_bounds__(W_THREADS, 1) mmd_w_kernel(const __grid_consta
                 for (int c = 0; c < 8; ++c) tw[lane * W_TILE_LD + (ch - 4 * h) * 8 + c] = wv[c];
                 if (!diag) {
                     // (j, i): lanes are consecutive i -> one 128-B row segment per store
-                    float* dt = Wg + jb * N + gi;
+                    float* dt = Wg + ((unsigned)jb * (unsigned)N + (unsigned)gi);
                     if (p.diag == 3 || p.diag == 4) {
                     } else if (row_ok && full8) {
 #pragma unroll
-                        for (int c = 0; c < 8; ++c) dt[c * N] = wv[c];
+                        for (int c = 0; c < 8; ++c) {
+                            *dt = wv[c];
+                            dt += N;
+                        }
                     } else if (row_ok) {
                         for (int c = 0; c < 8 && jb + c < N; ++c) dt[c * N] = wv[c];
                     }
@@ -1036,12 +1061,17 @@ __global__ void __launch_bounds__(W_THREADS, 1) mmd_w_kernel(const __grid_consta
             mbar_arrive(&acc_empty[buf]);
             __syncwarp();
             if (p.diag != 3 && p.diag != 5) {
-                const long long jc = (long long)J * WT + 32 * h + lane;
-                const long long r0 = (long long)I * WT + 32 * q;
-                if (jc < N)
+                const int jc = J * WT + 32 * h + lane;
+                const int r0 = I * WT + 32 * q;
+                const int nr = min(32, (int)N - r0);
+                if (jc < N) {
+                    float* dst = Wg + ((unsigned)r0 * (unsigned)N + (unsigned)jc);
 #pragma unroll 8
-                    for (int rr = 0; rr < 32; ++rr)
-                        if (r0 + rr < N) Wg[(r0 + rr) * N + jc] = tw[rr * W_TILE_LD + lane];
+                    for (int rr = 0; rr < nr; ++rr) {
+                        *dst = tw[rr * W_TILE_LD + lane];
+                        dst += N;
+                    }
+                }
             }
             __syncwarp();
 
