@@ -57,8 +57,16 @@ __global__ void beta_finish_kernel(MmdArgs a, const double* part, int P, double*
     double ss = 0.0;
     for (int k = threadIdx.x; k < a.d; k += NT) {
         double s = 0.0;
-#pragma unroll 8
-        for (int p = 0; p < P; ++p) s += part[((long long)g * P + p) * (a.d + 1) + k];
+        const double* src = part + (long long)g * P * (a.d + 1) + k;
+        int p = 0;
+        for (; p + 16 <= P; p += 16) {  // 16 loads in flight, then the fixed-order sum
+            double v[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) v[q] = src[(long long)(p + q) * (a.d + 1)];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) s += v[q];
+        }
+        for (; p < P; ++p) s += src[(long long)p * (a.d + 1)];
         ss += s * s;
     }
     red[threadIdx.x] = ss;
