@@ -593,6 +593,7 @@ void train_step(mtk_bank& k, const mtk_step& s, double* loss_host, double* mmd_h
         after_launch(c, 2);
     }
 
+    bool head_fused = false, head_fused_colsum = false;
     if (use_mmd) {
         MmdArgs a;
         a.G = k.G;
@@ -614,6 +615,38 @@ void train_step(mtk_bank& k, const mtk_step& s, double* loss_host, double* mmd_h
         a.grad_scale = (float)s.mmd_lambda;
         a.flags = c.d_flags;
         a.tc = k.tc_mmd && mmd_tc_supported(a);
+        // The head's DX (dZ of the last hidden layer = (lambda*g + dlogits W^T) * (h > 0))
+        // is fused into the MMD gradient GEMM (an extra K block + the masked
+        // epilogue) when that GEMM runs (materialised-W path) and the head is skinny.
+        const char* nhf = getenv("MTK_NO_HEAD_FUSE");  // A/B (read per call)
+        const bool no_head_fuse = nhf && nhf[0] == '1';
+        const int hl = L - 1;
+        if (a.tc && !two && !no_head_fuse && hl > 0 && hl > s.frozen_layers && !k.tc[k.layer_of(hl)] &&
+            head_dx_ok(k.fan_in(hl), k.fan_out(hl))) {
+            const int fi = k.fan_in(hl), fo = k.fan_out(hl);
+            a.hd_dz = cur->f;
+            a.hd_dz_gs = (long long)B * fo;
+            a.hd_n = fo;
+            a.hd_W = k.W[hl].f;
+            a.hd_w_gs = (long long)fi * fo;
+            a.hd_out = nxt->f;
+            a.hd_colsum = (hl - 1 >= s.frozen_layers && !no_colsum) ? k.colsum : nullptr;
+            if (!mmd_head_fusable(a)) a.hd_n = 0;
+        }
+        if (a.hd_n > 0) {
+            const int fo = a.hd_n;
+            head_fused = true;
+            head_fused_colsum = a.hd_colsum != nullptr;
+            // the head's bias update first: the fused DX overwrites k.colsum
+            PhaseScope ph(c, kPhBias, 1);
+            if (ce.colsum)
+                launch_bias_from_partials(k.G, (B + 31) / 32, fo, k.colsum, k.b[hl], lr, bias_adam(hl),
+                                          k.keep_grads ? k.gb[hl] : nullptr, c.d_flags, c.stream);
+            else
+                launch_bias_sgd(k.G, B, fo, cur->f, (long long)B * fo, k.b[hl], fo, lr, bias_adam(hl),
+                                k.keep_grads ? k.gb[hl] : nullptr, c.d_flags, c.stream);
+            after_launch(c, 1);
+        }
         if (const char* t = getenv("MTK_MMD_TRACE"))  // diagnostics (tools/mmd_trace.py)
             a.trace = reinterpret_cast<unsigned long long*>(strtoull(t, nullptr, 0));
         const int nblk = mmd_blocks_per_group(a);
@@ -669,7 +702,9 @@ void train_step(mtk_bank& k, const mtk_step& s, double* loss_host, double* mmd_h
         const Plane3 out = *nxt;
         const bool split = (l == L - 1 && two);
         bool next_colsum = false;
-        if (trainable) {  // bias first: the DX below overwrites k.colsum
+        const bool fused_here = head_fused && l == L - 1;  // bias + DX done with the MMD
+        if (fused_here) next_colsum = head_fused_colsum;
+        if (trainable && !fused_here) {  // bias first: the DX below overwrites k.colsum
             const int fo = k.dims[l + 1];
             PhaseScope ph(c, kPhBias, split ? 2 : 1);
             if (colsum_ready && !split) {
@@ -687,7 +722,7 @@ void train_step(mtk_bank& k, const mtk_step& s, double* loss_host, double* mmd_h
             }
             after_launch(c, split ? 2 : 1);
         }
-        if (need_dx) {
+        if (need_dx && !fused_here) {
             PhaseScope ph(c, kPhDx, split ? 2 : 1);
             if (split) {
                 gemm_dx(k, l, *cur, B, 0, src, out, k.H[l].f, nullptr);

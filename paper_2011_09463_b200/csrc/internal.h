@@ -193,6 +193,12 @@ struct UmmaGemm {
     float* colsum = nullptr;  // kMask: per-32-row-block column sums [G][ceil(M/32)][N]
     const float* rowvec = nullptr;  // kMmdGrad: per-row scalar [G][M]
     float scale = 1.f;              // kMmdGrad
+    int zmask = 0;                  // kMmdGrad: C *= (add > 0) (the fused head DX)
+    // optional second B operand: rows k >= ksplit of B are rows k - ksplit of b2
+    // (N-major B only; ksplit % 32 == 0)
+    const float* b2 = nullptr;
+    long long b2_rs = 0, b2_gs = 0;
+    int ksplit = 0;
     int* flags = nullptr;
 };
 void launch_umma(const UmmaGemm& u, cudaStream_t s);
@@ -296,6 +302,17 @@ struct MmdArgs {
     float* gXt = nullptr;
     long long gt_gs = 0;
     float grad_scale = 1.f;
+    // optional (materialised-W path only, mmd_head_fusable): fuse the head layer's DX
+    // into the gradient GEMM (an extra K block + the epilogue).  hd_out[r, p] = (grad_scale * g[r, p] +
+    // sum_j hd_dz[r, j] hd_W[p, j]) * (z[r, p] > 0), laid out as gXs; gXs/gXt are
+    // then not written.  hd_colsum (or null) gets per-32-row-block column sums.
+    const float* hd_dz = nullptr;   // [G][m+n][hd_n]
+    long long hd_dz_gs = 0;
+    const float* hd_W = nullptr;    // [G][d][hd_n]
+    long long hd_w_gs = 0;
+    int hd_n = 0;                   // <= 32
+    float* hd_out = nullptr;
+    float* hd_colsum = nullptr;
     int* flags = nullptr;
     bool tc = false;                // run on the tcgen05 path (k_mmd_tc.cu)
     unsigned long long* trace = nullptr;  // diagnostics (k_mmd_tc.cu)
@@ -304,6 +321,9 @@ int mmd_blocks_per_group(const MmdArgs& a);  // partial-sum blocks (depends on a
 bool mmd_tc_supported(const MmdArgs& a);
 int mmd_tc_blocks_per_group(const MmdArgs& a);
 size_t mmd_tc_scratch_bytes(const MmdArgs& a);
+// true when launch_mmd_tc fuses the head DX described by a.hd_* (materialised-W
+// path, hd_n <= 32, (m + n) % 32 == 0)
+bool mmd_head_fusable(const MmdArgs& a);
 // stages: 1 = prep pass (tf32 planes, norms, fused beta), 2 = the pair kernel;
 // the same scratch must be passed to both.
 constexpr int kMmdPrep = 1, kMmdPairs = 2;

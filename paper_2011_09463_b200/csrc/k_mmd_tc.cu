@@ -716,7 +716,8 @@ struct MmdWParams {
     int d, nb, geo5;
     float mult[8];
     int T, npairs, G;
-    float* W;                  // [G][N][N]
+    float* W;                  // [G][N][ldw]
+    long long ldw;             // row stride of W (N, or N + 32 with the head block)
     float* rpart;              // [G][T][T][4][WT]: row sums of block (I, J), per column quarter
     float* cpart;              // [G][T][T][4][WT]: column sums of block (I, J) (I < J), per row quarter
     double* kpart;             // [G][npairs][W_EPI_WARPS][3]: kernel sums per epilogue warp
@@ -907,7 +908,8 @@ __global__ void __launch_bounds__(W_THREADS, 1) mmd_w_kernel(const __grid_consta
             }
             const float* nrm = p.norms + (long long)g * N;
             const float ni = row_ok ? nrm[gi] : 0.f;
-            float* Wg = p.W + (long long)g * N * N;
+            float* Wg = p.W + (long long)g * N * p.ldw;
+            const unsigned ldw = (unsigned)p.ldw;
             const int buf = lt & 1;
             mbar_wait(&acc_full[buf], (lt >> 1) & 1);
             tc_fence_after();
@@ -1039,16 +1041,16 @@ __global__ void __launch_bounds__(W_THREADS, 1) mmd_w_kernel(const __grid_consta
                 for (int c = 0; c < 8; ++c) tw[lane * W_TILE_LD + (ch - 4 * h) * 8 + c] = wv[c];
                 if (!diag) {
                     // (j, i): lanes are consecutive i -> one 128-B row segment per store
-                    float* dt = Wg + ((unsigned)jb * (unsigned)N + (unsigned)gi);
+                    float* dt = Wg + ((unsigned)jb * ldw + (unsigned)gi);
                     if (p.diag == 3 || p.diag == 4) {
                     } else if (row_ok && full8) {
 #pragma unroll
                         for (int c = 0; c < 8; ++c) {
                             *dt = wv[c];
-                            dt += N;
+                            dt += ldw;
                         }
                     } else if (row_ok) {
-                        for (int c = 0; c < 8 && jb + c < N; ++c) dt[c * N] = wv[c];
+                        for (int c = 0; c < 8 && jb + c < N; ++c) dt[c * ldw] = wv[c];
                     }
                     const float cs = column_sums_8(wv, lane);
                     if ((lane & 3) == 0)
@@ -1065,11 +1067,11 @@ __global__ void __launch_bounds__(W_THREADS, 1) mmd_w_kernel(const __grid_consta
                 const int r0 = I * WT + 32 * q;
                 const int nr = min(32, (int)N - r0);
                 if (jc < N) {
-                    float* dst = Wg + ((unsigned)r0 * (unsigned)N + (unsigned)jc);
+                    float* dst = Wg + ((unsigned)r0 * ldw + (unsigned)jc);
 #pragma unroll 8
                     for (int rr = 0; rr < nr; ++rr) {
                         *dst = tw[rr * W_TILE_LD + lane];
-                        dst += N;
+                        dst += ldw;
                     }
                 }
             }
@@ -1104,17 +1106,54 @@ __global__ void __launch_bounds__(W_THREADS, 1) mmd_w_kernel(const __grid_consta
 // in the fused kernel's layout: partial[g][I][c] = sum_{J >= I} sum_w
 // kpart[g][pair(I, J)][w][c] (every load in flight, then fixed-order sums).
 constexpr int WSUM_THREADS = 256;
+// The fused head DX (MmdArgs::hd_*) rides on the V = W.Z GEMM as 32 extra K
+// columns: A = [W | dZ_head 0], B = [Z ; -W_head^T / lambda 0], so the GEMM's
+// kMmdGrad epilogue lambda * (z * Wsum - acc) gives lambda * g + dZ_head W_head^T.
+constexpr int kHeadK = 32;
+
+struct WsumHead {  // the fused head DX's extra K block (hn = 0: none)
+    int hn, d;
+    const float* dz;   // [G][N][hn]
+    long long dz_gs;
+    const float* Wh;   // [G][d][hn]
+    long long wh_gs;
+    float scale;       // lambda
+    float* W;          // [G][N][ldw]: columns N .. N + kHeadK
+    long long ldw;
+    float* bx;         // [G][kHeadK][d]
+};
 __global__ void __launch_bounds__(WSUM_THREADS) mmd_wsum_kernel(const float* rpart, const float* cpart,
                                                                 const double* kpart, int G, long long N,
                                                                 int T, int npairs, float* wsum,
-                                                                double* partial) {
+                                                                double* partial, WsumHead h) {
     __shared__ double jsum[3][WSUM_THREADS / 3 + 1];
     const long long nbw = ((long long)G * N + WSUM_THREADS - 1) / WSUM_THREADS;
+    if (blockIdx.x >= nbw + (long long)G * T) {  // head block B rows: -W_head^T / lambda
+        const long long e = (blockIdx.x - nbw - (long long)G * T) * WSUM_THREADS + threadIdx.x;
+        const long long per = (long long)kHeadK * h.d;
+        if (e >= G * per) return;
+        const int g = (int)(e / per), j = (int)(e % per / h.d), n = (int)(e % h.d);
+        h.bx[e] = j < h.hn ? __fdiv_rn(-h.Wh[g * h.wh_gs + (long long)n * h.hn + j], h.scale) : 0.f;
+        return;
+    }
     if (blockIdx.x < nbw) {
         const long long t = blockIdx.x * (long long)WSUM_THREADS + threadIdx.x;
         if (t >= (long long)G * N) return;
         const int g = (int)(t / N);
         const long long i = t % N;
+        if (h.hn) {  // head block A columns of row i: dZ_head[i, :], zero past hn
+            const float* z = h.dz + g * h.dz_gs + i * h.hn;
+            float4* dst = reinterpret_cast<float4*>(h.W + ((long long)g * N + i) * h.ldw + N);
+#pragma unroll
+            for (int c = 0; c < kHeadK / 4; ++c) {
+                float4 v;
+                v.x = 4 * c < h.hn ? z[4 * c] : 0.f;
+                v.y = 4 * c + 1 < h.hn ? z[4 * c + 1] : 0.f;
+                v.z = 4 * c + 2 < h.hn ? z[4 * c + 2] : 0.f;
+                v.w = 4 * c + 3 < h.hn ? z[4 * c + 3] : 0.f;
+                dst[c] = v;
+            }
+        }
         const int R = (int)(i / WT), r = (int)(i % WT);
         double s = 0.0;
 #pragma unroll 4
@@ -1216,7 +1255,15 @@ static bool w_path(const MmdArgs& a) {
     return (double)a.G * N * N * 4.0 <= 2.0 * 1024 * 1024 * 1024;
 }
 
+static bool head_block(const MmdArgs& a) {
+    return a.hd_n > 0 && a.hd_n <= kHeadK && (a.m + a.n) % 32 == 0;
+}
+
+bool mmd_head_fusable(const MmdArgs& a) { return w_path(a) && head_block(a); }
+
 struct WLayout {
+    long long ldw;  // row stride of W: N, or N + kHeadK with the head block
+    float* bx;      // [G][kHeadK][d]: -W_head^T / lambda, zero rows past hd_n
     float* W;
     float* rpart;
     float* cpart;
@@ -1230,8 +1277,11 @@ static WLayout w_layout(const MmdArgs& a, uintptr_t base) {
     WLayout L;
     uintptr_t cur = (base + 255) & ~uintptr_t(255);
     const uintptr_t start = cur;
+    L.ldw = N + (head_block(a) ? kHeadK : 0);
     L.W = reinterpret_cast<float*>(cur);
-    cur = (cur + (size_t)a.G * N * N * 4 + 255) & ~uintptr_t(255);
+    cur = (cur + (size_t)a.G * N * L.ldw * 4 + 255) & ~uintptr_t(255);
+    L.bx = reinterpret_cast<float*>(cur);
+    if (head_block(a)) cur = (cur + (size_t)a.G * kHeadK * a.d * 4 + 255) & ~uintptr_t(255);
     L.rpart = reinterpret_cast<float*>(cur);
     cur = (cur + (size_t)a.G * T * T * 4 * WT * 4 + 255) & ~uintptr_t(255);
     L.cpart = reinterpret_cast<float*>(cur);
@@ -1316,6 +1366,7 @@ void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s, int stages) 
         w.npairs = np;
         w.G = a.G;
         w.W = L.W;
+        w.ldw = L.ldw;
         w.rpart = L.rpart;
         w.cpart = L.cpart;
         w.kpart = L.kpart;
@@ -1333,8 +1384,27 @@ void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s, int stages) 
         mmd_w_kernel<<<std::min(items, sms), W_THREADS, W_SMEM_BYTES, s>>>(w);
         count_launch();
         const long long nbw = ((long long)a.G * N + WSUM_THREADS - 1) / WSUM_THREADS;
-        mmd_wsum_kernel<<<(unsigned)(nbw + (long long)a.G * T), WSUM_THREADS, 0, s>>>(
-            L.rpart, L.cpart, L.kpart, a.G, N, T, np, L.wsum, a.partial);
+        const bool head = head_block(a);
+        WsumHead h;
+        std::memset(&h, 0, sizeof(h));
+        long long nbx = 0;
+        if (head) {
+            if (!a.hd_out || !a.hd_dz || !a.hd_W || a.grad_scale == 0.f)
+                fail(MTK_ERROR, "mmd: incomplete fused head DX arguments");
+            h.hn = a.hd_n;
+            h.d = a.d;
+            h.dz = a.hd_dz;
+            h.dz_gs = a.hd_dz_gs;
+            h.Wh = a.hd_W;
+            h.wh_gs = a.hd_w_gs;
+            h.scale = a.grad_scale;
+            h.W = L.W;
+            h.ldw = L.ldw;
+            h.bx = L.bx;
+            nbx = ((long long)a.G * kHeadK * a.d + WSUM_THREADS - 1) / WSUM_THREADS;
+        }
+        mmd_wsum_kernel<<<(unsigned)(nbw + (long long)a.G * T + nbx), WSUM_THREADS, 0, s>>>(
+            L.rpart, L.cpart, L.kpart, a.G, N, T, np, L.wsum, a.partial, h);
         count_launch();
         UmmaGemm u;
         u.G = a.G;
@@ -1343,8 +1413,8 @@ void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s, int stages) 
         u.K = (int)N;
         u.a_mn = 0;
         u.a = L.W;
-        u.a_rs = N;
-        u.a_gs = N * N;
+        u.a_rs = L.ldw;
+        u.a_gs = N * L.ldw;
         u.b_mn = 1;
         u.b = a.Xs;
         u.b_rs = a.d;
@@ -1352,6 +1422,16 @@ void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s, int stages) 
         u.epi = Epi::kMmdGrad;
         u.C = a.gXs;
         u.c_gs = a.gs_gs;
+        if (head) {  // fused head DX: K gains the head block; the epilogue writes the layer's dZ
+            u.K = (int)N + kHeadK;
+            u.b2 = L.bx;
+            u.b2_rs = a.d;
+            u.b2_gs = (long long)kHeadK * a.d;
+            u.ksplit = (int)N;
+            u.C = a.hd_out;
+            u.zmask = 1;
+            u.colsum = a.hd_colsum;
+        }
         u.ldc = a.d;
         u.add = a.Xs;
         u.rowvec = L.wsum;

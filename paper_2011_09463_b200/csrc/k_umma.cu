@@ -76,6 +76,9 @@ struct UmmaParams {
     float* colsum;     // kMask: per-32-row-block column sums of C, [G][ceil(M/32)][N], or null
     const float* rowvec;  // kMmdGrad: [G][M]
     float scale;          // kMmdGrad
+    int zmask;            // kMmdGrad: C *= (add > 0) (the fused head DX)
+    CUtensorMap b2;       // B rows k >= ksplit come from here (row k - ksplit); ksplit % 32 == 0
+    int ksplit;           // K if there is no second B operand
     int* flags;
     unsigned long long* trace;  // diagnostics: timestamps of CTA (0,0,0)
 };
@@ -253,6 +256,12 @@ __device__ __forceinline__ void epilogue_rows(const UmmaParams& p, uint32_t tmem
                     x.z = p.scale * fmaf(o1[j].z, rv, -x.z);
                     x.w = p.scale * fmaf(o1[j].w, rv, -x.w);
                     bad |= !(isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w));
+                    if (p.zmask) {  // fused head DX: the ReLU mask of z (= h, tape.hpp:349)
+                        x.x = o1[j].x > 0.f ? x.x : 0.f;
+                        x.y = o1[j].y > 0.f ? x.y : 0.f;
+                        x.z = o1[j].z > 0.f ? x.z : 0.f;
+                        x.w = o1[j].w > 0.f ? x.w : 0.f;
+                    }
                 } else if (epi == (int)Epi::kSgd) {  // C is the fp32 master weight
                     if (p.grad_out) *reinterpret_cast<float4*>(p.grad_out + idx) = x;
                     x.x = sgd_update(o1[j].x, x.x, p.lr);
@@ -282,8 +291,10 @@ __device__ __forceinline__ void epilogue_rows(const UmmaParams& p, uint32_t tmem
                         if (p.add) x = p.add[idx] + x;
                         x = (p.mask[idx] > 0.f) ? x : 0.f;
                     } else if (epi == (int)Epi::kMmdGrad) {
-                        x = p.scale * fmaf(p.add[idx], p.rowvec[(long long)g * p.M + m], -x);
+                        const float z = p.add[idx];
+                        x = p.scale * fmaf(z, p.rowvec[(long long)g * p.M + m], -x);
                         bad |= !isfinite(x);
+                        if (p.zmask) x = z > 0.f ? x : 0.f;
                     } else if (epi == (int)Epi::kSgd) {
                         if (p.grad_out) p.grad_out[idx] = x;
                         x = sgd_update(p.C[idx], x, p.lr);
@@ -296,7 +307,7 @@ __device__ __forceinline__ void epilogue_rows(const UmmaParams& p, uint32_t tmem
                 v[j] = x;
             }
         }
-        if (p.colsum && epi == (int)Epi::kMask && mw < p.M) {
+        if (p.colsum && (epi == (int)Epi::kMask || epi == (int)Epi::kMmdGrad) && mw < p.M) {
             // per-32-row-block column sums of the stored values (next layer's db)
             const float cs = column_sums_32(v, lane);
             if (nb + lane < p.N) {
@@ -364,6 +375,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_kernel(const __grid_const
     if (warp == 0 && lane == 0) {
         tma_prefetch(&p.a);
         tma_prefetch(&p.b);
+        if (p.ksplit < p.K) tma_prefetch(&p.b2);
         if (p.nhalf && !B_MN) tma_prefetch(&p.b64);
         for (int s = 0; s < LS; ++s) {
             mbar_init(&full[s], 1);
@@ -414,7 +426,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_kernel(const __grid_const
                         if (tr && it < 1000) tr[it] = gtime();
                         mbar_expect_tx(&full[s], bytes);
                         load_operand<A_MN>(st, &p.a, &full[s], m0, kb * BK, g);
-                        load_operand<B_MN>(st + TILE_BYTES, bmap, &full[s], nb0, kb * BK, g, brows);
+                        if (kb * BK < p.ksplit)
+                            load_operand<B_MN>(st + TILE_BYTES, bmap, &full[s], nb0, kb * BK, g, brows);
+                        else  // the second B operand (p.b2, N-major)
+                            load_operand<B_MN>(st + TILE_BYTES, &p.b2, &full[s], nb0, kb * BK - p.ksplit, g, brows);
                     }
                     __syncwarp();
                 }
@@ -654,6 +669,14 @@ void launch_umma(const UmmaGemm& u, cudaStream_t s) {
     p.colsum = u.colsum;
     p.rowvec = u.rowvec;
     p.scale = u.scale;
+    p.zmask = u.zmask;
+    p.ksplit = u.K;
+    if (u.b2) {  // K = [0, ksplit) from b, [ksplit, K) from b2 (same major-ness)
+        if (u.ksplit <= 0 || u.ksplit % BK || u.ksplit >= u.K || u.b_mn != 1)
+            fail(MTK_ERROR, "umma: split B needs an N-major B and ksplit % 32 == 0 inside K");
+        p.ksplit = u.ksplit;
+        p.b2 = make_map(u.b2, u.N, u.K - u.ksplit, u.G, u.b2_rs, u.b2_gs, BK, true);
+    }
     p.flags = u.flags;
     if (const char* t = getenv("MTK_UMMA_TRACE"))
         p.trace = reinterpret_cast<unsigned long long*>(strtoull(t, nullptr, 0));

@@ -153,6 +153,41 @@ def test_mmd_materialised_w_path_matches_fused(ctx, monkeypatch, B, src, dims):
         assert rel(a, b) <= 2e-5
 
 
+@pytest.mark.parametrize("B,src,dims,frozen,fused", [
+    (320, 140, [96, 64, 10], 0, True), (1024, 512, [1024, 512, 256, 10], 0, True),
+    (224, 90, [100, 64, 32, 10], 1, True), (96, 40, [64, 32, 2], 0, True), (256, 100, [64, 48, 20], 0, True),
+    (300, 140, [96, 64, 10], 0, False)])  # B % 32 != 0: separate head DX launch
+def test_head_dx_fused_into_mmd_gradient_gemm(ctx, monkeypatch, B, src, dims, frozen, fused):
+    """With MMD on the materialised-W path and a skinny head, the head's DX
+    ((lambda g + dlogits W_head^T) * (h > 0)) rides on the V = W.Z GEMM as an
+    extra K block instead of a separate head_dx launch (MTK_NO_HEAD_FUSE=1):
+    one launch fewer, same step to fp32 rounding (3xTF32 head product)."""
+    G = 3
+    X, y = inputs(G, B, dims[0], dims[-1], shift=0.4)
+    Xd, yd = to_dev(X, y)
+    res = []
+    for off in ("0", "1"):
+        monkeypatch.setenv("MTK_NO_HEAD_FUSE", off)
+        bank = make_bank(ctx, G, dims, seed=9)
+        bank.keep_grads(True)
+        torch.cuda.synchronize()
+        n0 = ctx.launches
+        loss, mmd = bank.train_step(Xd, yd, lr=0.05, src_rows=src, mmd_lambda=0.7, frozen_layers=frozen)
+        res.append((loss.copy(), mmd.copy(), [bank.get_grads(g) for g in range(G)],
+                    [bank.get_params(g) for g in range(G)], ctx.launches - n0))
+    (l0, m0, g0, p0, n0), (l1, m1, g1, p1, n1) = res
+    assert n0 == n1 - (1 if fused else 0), (n0, n1)
+    assert np.array_equal(l0, l1) and np.array_equal(m0, m1)
+    L = len(dims) - 1
+    for g in range(G):
+        for i in range(frozen, L):
+            for k in (0, 1):  # dW, db
+                assert rel(g0[g][k][i], g1[g][k][i]) <= 2e-6, (g, i, k)
+                assert rel(p0[g][k][i], p1[g][k][i]) <= 2e-6, (g, i, k)
+            if i == L - 1 or not fused:
+                assert np.array_equal(g0[g][0][i], g1[g][0][i]), (g, i)  # the head's own dW
+
+
 def test_step_two_heads_parameter_based(ctx):
     dims = [784, 256, 10]
     bank = make_bank(ctx, 3, dims, n_heads=2)
