@@ -65,8 +65,11 @@ int mtk_ctx_launch_count(mtk_ctx* ctx, uint64_t* out);
 /* Optional CUDA-event timing of the bank step's phases, on the ctx stream.
  * mtk_ctx_phase_times synchronizes and returns (then resets) the summed
  * milliseconds and launch counts per phase, MTK_NUM_PHASES entries, in the
- * order: fwd_gemm, ce, mmd_beta, mmd_pairs, dx_gemm, dw_gemm, bias_sgd, other */
-#define MTK_NUM_PHASES 8
+ * order: fwd_gemm, ce, mmd_beta, mmd_pairs, dx_gemm, dw_gemm, bias_sgd, other,
+ * side_stream.  side_stream is the wall time of the launch groups on the ctx's
+ * side stream (MMD prep pass, bias updates, skinny head dW), which overlap
+ * the main-stream phases, waiting included. */
+#define MTK_NUM_PHASES 9
 int mtk_ctx_set_timing(mtk_ctx* ctx, int on);
 int mtk_ctx_phase_times(mtk_ctx* ctx, double* ms_host, uint64_t* launches_host);
 

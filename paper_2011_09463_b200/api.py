@@ -68,15 +68,18 @@ class Context:
         errors.check(lib.mtk_ctx_launch_count(self.h, C.byref(v)))
         return v.value
 
-    PHASES = ("fwd_gemm", "ce", "mmd_beta", "mmd_pairs", "dx_gemm", "dw_gemm", "bias_sgd", "other")
+    # side_stream: wall time of the side-stream groups (MMD prep, bias updates,
+    # head dW); they overlap the main-stream phases
+    PHASES = ("fwd_gemm", "ce", "mmd_beta", "mmd_pairs", "dx_gemm", "dw_gemm", "bias_sgd", "other",
+              "side_stream")
 
     def set_timing(self, on: bool = True):
         errors.check(lib.mtk_ctx_set_timing(self.h, 1 if on else 0))
 
     def phase_times(self):
         """{phase: (ms summed, launches)} since the last call (synchronizes)."""
-        ms = np.zeros(8)
-        n = np.zeros(8, dtype=np.uint64)
+        ms = np.zeros(len(self.PHASES))
+        n = np.zeros(len(self.PHASES), dtype=np.uint64)
         errors.check(lib.mtk_ctx_phase_times(self.h, ms.ctypes.data_as(_dp),
                                              n.ctypes.data_as(C.POINTER(C.c_uint64))))
         return {p: (float(ms[i]), int(n[i])) for i, p in enumerate(self.PHASES)}

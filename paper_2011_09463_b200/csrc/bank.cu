@@ -20,6 +20,7 @@
 //   H[l]  [G, B, dims[l]] post-ReLU activations (ReLU mask = H > 0)
 //   dZ    two ping-pong [G, B, max dim] gradient buffers
 #include <cmath>
+#include <functional>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -77,7 +78,11 @@ struct mtk_bank {
     double* mmd = nullptr;
     double* beta = nullptr;
     float* gH = nullptr;
-    float* colsum = nullptr;  // [G][ceil(B/32)][max dim] bias-gradient partials from the DX epilogues
+    // [G][ceil(B/32)][max dim] bias-gradient partials: layer j's from the
+    // producer of its dZ (CE, a DX epilogue, the fused MMD gradient GEMM) in
+    // colsum[j % 3], so a bias update on the side stream can lag two layers
+    float* colsum[3] = {nullptr, nullptr, nullptr};
+    Plane3 dlog;              // dlogits [G][B][C] (own buffer: the side-stream head dW reads it late)
     double* loss_part = nullptr;  // [G][ceil(B/32)] CE loss partials
     double* mmd_part = nullptr;
     size_t mmd_part_bytes = 0;
@@ -211,8 +216,11 @@ struct mtk_bank {
         cudaFree(logits);
         cudaFree(row_loss);
         cudaFree(gH);
-        cudaFree(colsum);
-        colsum = nullptr;
+        for (auto& cs : colsum) {
+            cudaFree(cs);
+            cs = nullptr;
+        }
+        free3(dlog);
         cudaFree(loss_part);
         loss_part = nullptr;
         logits = nullptr;
@@ -230,7 +238,8 @@ struct mtk_bank {
         MTK_CUDA(cudaMalloc(&logits, GB * dims[L] * sizeof(float)));
         MTK_CUDA(cudaMalloc(&row_loss, GB * sizeof(double)));
         if (L > 1) MTK_CUDA(cudaMalloc(&gH, GB * dims[L - 1] * sizeof(float)));
-        MTK_CUDA(cudaMalloc(&colsum, (size_t)G * ((B + 31) / 32) * maxd() * sizeof(float)));
+        for (auto& cs : colsum) MTK_CUDA(cudaMalloc(&cs, (size_t)G * ((B + 31) / 32) * maxd() * sizeof(float)));
+        alloc3(dlog, GB * dims[L]);
         MTK_CUDA(cudaMalloc(&loss_part, (size_t)G * ((B + 31) / 32) * sizeof(double)));
         capB = B;
     }
@@ -400,8 +409,9 @@ bool gemm_dx(mtk_bank& k, int mat, const Plane3& dz, int B, int r0, int rows, co
 
 // DW + SGD: W[p, j] -= lr * sum_r in[r, p] dz[r, j]
 void gemm_dw(mtk_bank& k, int mat, const Plane3& in, const Plane3& dz, int B, int r0, int rows,
-             float lr, AdamArgs adam) {
+             float lr, AdamArgs adam, cudaStream_t st = nullptr) {
     Ctx& c = *k.ctx;
+    if (!st) st = c.stream;
     const int fi = k.fan_in(mat), fo = k.fan_out(mat);
     if (adam.on) {
         adam.m = k.mW[mat];
@@ -434,9 +444,9 @@ void gemm_dw(mtk_bank& k, int mat, const Plane3& in, const Plane3& dz, int B, in
         u.lr = lr;
         u.grad_out = (!adam_gemm && k.keep_grads) ? k.gW[mat] : nullptr;
         u.flags = c.d_flags;
-        launch_umma(u, c.stream);
+        launch_umma(u, st);
         if (adam_gemm)
-            launch_adam_apply(k.W[mat].f, gbuf, (long long)k.G * fi * fo, lr, adam, c.d_flags, c.stream);
+            launch_adam_apply(k.W[mat].f, gbuf, (long long)k.G * fi * fo, lr, adam, c.d_flags, st);
     } else if (head_dw_ok(fo) || head_dw_ok(fi)) {
         // narrow output (the heads): reduce over rows with the fo-wide dZ as the
         // register-blocked operand; narrow input (the attack model's k -> H
@@ -462,13 +472,14 @@ void gemm_dw(mtk_bank& k, int mat, const Plane3& in, const Plane3& dz, int B, in
         h.flags = c.d_flags;
         const size_t hb = head_dw_scratch_bytes(k.G, fi, fo);
         if (hb > k.head_scratch_bytes) {
+            MTK_CUDA(cudaStreamSynchronize(st));  // (the side stream's own prior work)
             MTK_CUDA(cudaStreamSynchronize(c.stream));
             cudaFree(k.head_scratch);
             MTK_CUDA(cudaMalloc(&k.head_scratch, hb));
             k.head_scratch_bytes = hb;
         }
         h.partial = k.head_scratch;
-        launch_head_dw(h, c.stream);
+        launch_head_dw(h, st);
     } else {
         Gemm g;
         g.G = k.G;
@@ -490,9 +501,9 @@ void gemm_dw(mtk_bank& k, int mat, const Plane3& in, const Plane3& dz, int B, in
         g.lr = lr;
         g.grad_out = (!adam_gemm && k.keep_grads) ? k.gW[mat] : nullptr;
         g.flags = c.d_flags;
-        launch_gemm(g, c.stream);
+        launch_gemm(g, st);
         if (adam_gemm)
-            launch_adam_apply(k.W[mat].f, gbuf, (long long)k.G * fi * fo, lr, adam, c.d_flags, c.stream);
+            launch_adam_apply(k.W[mat].f, gbuf, (long long)k.G * fi * fo, lr, adam, c.d_flags, st);
     }
 }
 
@@ -503,7 +514,9 @@ Plane3 input_plane(mtk_bank& k, const float* X, int B) {
     return in;
 }
 
-void run_forward(mtk_bank& k, const Plane3& X, int B, int head_all, int src_rows) {
+// after_hidden (optional) runs once the last hidden layer's forward is enqueued
+void run_forward(mtk_bank& k, const Plane3& X, int B, int head_all, int src_rows,
+                 const std::function<void()>& after_hidden = {}) {
     Ctx& c = *k.ctx;
     Plane3 h = X;
     Plane3 lg;
@@ -514,6 +527,7 @@ void run_forward(mtk_bank& k, const Plane3& X, int B, int head_all, int src_rows
             gemm_fwd(k, l, h, B, 0, B, k.H[l + 1], true);
             after_launch(c);
             h = k.H[l + 1];
+            if (l == k.L - 2 && after_hidden) after_hidden();
         } else if (head_all >= 0) {
             gemm_fwd(k, l + head_all, h, B, 0, B, lg, false);
             after_launch(c);
@@ -577,25 +591,21 @@ void train_step(mtk_bank& k, const mtk_step& s, double* loss_host, double* mmd_h
     };
 
     const Plane3 X = input_plane(k, s.X, B);
-    run_forward(k, X, B, two ? -1 : 0, src);
+    // Side stream (Ctx::fork/join): the MMD prep pass beside the head forward +
+    // CE; the bias updates and the skinny head dW beside the DW GEMMs.
+    const char* nse = getenv("MTK_NO_SIDE");  // A/B (read per call)
+    const bool side = !(nse && nse[0] == '1');
+    cudaEvent_t bias_done[3] = {nullptr, nullptr, nullptr};  // side: last reader of colsum[j % 3]
+    auto before_colsum_write = [&](int layer) {  // main: about to overwrite colsum[layer % 3]
+        cudaEvent_t& e = bias_done[layer % 3];
+        if (e) MTK_CUDA(cudaStreamWaitEvent(c.stream, e, 0));
+        e = nullptr;
+    };
 
-    Plane3* cur = &k.dZ[0];
-    Plane3* nxt = &k.dZ[1];
-    CeArgs ce{k.G,      B,          k.dims[L], two ? src : B, k.logits, s.y, s.w,
-              (float)(1.0 / d0), (float)(1.0 / (two ? d1 : d0)), cur->f, k.row_loss, k.loss,
-              c.d_flags, k.loss_part};
-    // the head's bias gradient comes out of the CE kernel as column partials
     static const bool no_colsum = getenv("MTK_NO_COLSUM") != nullptr;  // A/B diagnostics
-    ce.colsum = (!two && L - 1 >= s.frozen_layers && !no_colsum) ? k.colsum : nullptr;
-    {
-        PhaseScope ph(c, kPhCe, 2);
-        launch_ce(ce, c.stream);
-        after_launch(c, 2);
-    }
-
-    bool head_fused = false, head_fused_colsum = false;
+    MmdArgs a;
+    bool prep_on_side = false;
     if (use_mmd) {
-        MmdArgs a;
         a.G = k.G;
         a.m = src;
         a.n = B - src;
@@ -624,28 +634,14 @@ void train_step(mtk_bank& k, const mtk_step& s, double* loss_host, double* mmd_h
         if (a.tc && !two && !no_head_fuse && hl > 0 && hl > s.frozen_layers && !k.tc[k.layer_of(hl)] &&
             head_dx_ok(k.fan_in(hl), k.fan_out(hl))) {
             const int fi = k.fan_in(hl), fo = k.fan_out(hl);
-            a.hd_dz = cur->f;
+            a.hd_dz = k.dlog.f;
             a.hd_dz_gs = (long long)B * fo;
             a.hd_n = fo;
             a.hd_W = k.W[hl].f;
             a.hd_w_gs = (long long)fi * fo;
-            a.hd_out = nxt->f;
-            a.hd_colsum = (hl - 1 >= s.frozen_layers && !no_colsum) ? k.colsum : nullptr;
+            a.hd_out = k.dZ[1].f;
+            a.hd_colsum = (hl - 1 >= s.frozen_layers && !no_colsum) ? k.colsum[(hl - 1) % 3] : nullptr;
             if (!mmd_head_fusable(a)) a.hd_n = 0;
-        }
-        if (a.hd_n > 0) {
-            const int fo = a.hd_n;
-            head_fused = true;
-            head_fused_colsum = a.hd_colsum != nullptr;
-            // the head's bias update first: the fused DX overwrites k.colsum
-            PhaseScope ph(c, kPhBias, 1);
-            if (ce.colsum)
-                launch_bias_from_partials(k.G, (B + 31) / 32, fo, k.colsum, k.b[hl], lr, bias_adam(hl),
-                                          k.keep_grads ? k.gb[hl] : nullptr, c.d_flags, c.stream);
-            else
-                launch_bias_sgd(k.G, B, fo, cur->f, (long long)B * fo, k.b[hl], fo, lr, bias_adam(hl),
-                                k.keep_grads ? k.gb[hl] : nullptr, c.d_flags, c.stream);
-            after_launch(c, 1);
         }
         if (const char* t = getenv("MTK_MMD_TRACE"))  // diagnostics (tools/mmd_trace.py)
             a.trace = reinterpret_cast<unsigned long long*>(strtoull(t, nullptr, 0));
@@ -667,15 +663,47 @@ void train_step(mtk_bank& k, const mtk_step& s, double* loss_host, double* mmd_h
                 MTK_CUDA(cudaMalloc(&k.mmd_z, zb));
                 k.mmd_z_bytes = zb;
             }
+            prep_on_side = side;
+        }
+    }
+    // the prep pass only needs the last hidden layer: it forks off after that
+    // layer's forward GEMM and runs beside the head forward and CE
+    run_forward(k, X, B, two ? -1 : 0, src, prep_on_side ? [&] {
+        c.fork();
+        PhaseScope ph(c, kPhMmdBeta, 2, c.side);  // prep pass: tf32 planes, norms, beta
+        launch_mmd_tc(a, k.mmd_z, c.side, kMmdPrep);
+        after_launch(c, 2);
+    } : std::function<void()>());
+
+    Plane3* cur = &k.dlog;
+    Plane3* nxt = &k.dZ[1];
+    Plane3* spare = &k.dZ[0];  // becomes nxt after the head (dlogits keep their own buffer)
+    CeArgs ce{k.G,      B,          k.dims[L], two ? src : B, k.logits, s.y, s.w,
+              (float)(1.0 / d0), (float)(1.0 / (two ? d1 : d0)), cur->f, k.row_loss, k.loss,
+              c.d_flags, k.loss_part};
+    // the head's bias gradient comes out of the CE kernel as column partials
+    ce.colsum = (!two && L - 1 >= s.frozen_layers && !no_colsum) ? k.colsum[(L - 1) % 3] : nullptr;
+    {
+        PhaseScope ph(c, kPhCe, 2);
+        launch_ce(ce, c.stream);
+        after_launch(c, 2);
+    }
+
+    const bool head_fused = use_mmd && a.hd_n > 0;
+    const bool head_fused_colsum = head_fused && a.hd_colsum != nullptr;
+    if (use_mmd) {
+        if (a.tc && !prep_on_side) {
             PhaseScope ph(c, kPhMmdBeta, 2);  // prep pass: tf32 planes, norms, beta
             launch_mmd_tc(a, k.mmd_z, c.stream, kMmdPrep);
             after_launch(c, 2);
-        } else {
+        } else if (!a.tc) {
             double* sc = c.scratch(mmd_beta_scratch_bytes(a));
             PhaseScope ph(c, kPhMmdBeta, 2);
             launch_mmd_beta(a, k.beta, sc, c.stream);
             after_launch(c, 2);
         }
+        c.join();  // the prep pass
+        if (head_fused && a.hd_colsum) before_colsum_write(L - 2);
         {
             PhaseScope ph(c, kPhMmdPairs, 1);
             if (a.tc) launch_mmd_tc(a, k.mmd_z, c.stream, kMmdPairs);
@@ -691,24 +719,27 @@ void train_step(mtk_bank& k, const mtk_step& s, double* loss_host, double* mmd_h
 
     // backward sweep, layer L-1 down to 0.  A DX launch also reduces its
     // output's columns per 32-row block when the layer below is trainable,
-    // so that layer's bias update needs no second pass over dZ.
+    // so that layer's bias update needs no second pass over dZ.  Bias updates
+    // from those partials and the skinny head dW go to the side stream once
+    // the layer's DX is enqueued; they overlap the DW GEMMs.
     bool colsum_ready = ce.colsum != nullptr;
     for (int l = L - 1; l >= 0; --l) {
         const bool trainable = l >= s.frozen_layers;
         const bool need_dx = l > 0 && l > s.frozen_layers;
         const Plane3& in = l == 0 ? X : k.H[l];
         const float* add = (l == L - 1 && use_mmd) ? k.gH : nullptr;
-        // the DX output feeds layer l-1: only write its tf32 planes if that layer is tc
         const Plane3 out = *nxt;
         const bool split = (l == L - 1 && two);
+        const int fo = k.dims[l + 1];
         bool next_colsum = false;
-        const bool fused_here = head_fused && l == L - 1;  // bias + DX done with the MMD
+        const bool fused_here = head_fused && l == L - 1;  // DX done with the MMD
         if (fused_here) next_colsum = head_fused_colsum;
-        if (trainable && !fused_here) {  // bias first: the DX below overwrites k.colsum
-            const int fo = k.dims[l + 1];
+        // bias from column partials: deferred to the side stream (below)
+        const bool bias_side = side && trainable && colsum_ready && !split;
+        if (trainable && !bias_side) {
             PhaseScope ph(c, kPhBias, split ? 2 : 1);
             if (colsum_ready && !split) {
-                launch_bias_from_partials(k.G, (B + 31) / 32, fo, k.colsum, k.b[l], lr, bias_adam(l),
+                launch_bias_from_partials(k.G, (B + 31) / 32, fo, k.colsum[l % 3], k.b[l], lr, bias_adam(l),
                                           k.keep_grads ? k.gb[l] : nullptr, c.d_flags, c.stream);
             } else if (split) {
                 launch_bias_sgd(k.G, src, fo, cur->f, (long long)B * fo, k.b[l], fo, lr, bias_adam(l),
@@ -730,27 +761,50 @@ void train_step(mtk_bank& k, const mtk_step& s, double* loss_host, double* mmd_h
                 after_launch(c, 2);
             } else {
                 const bool below_trainable = l - 1 >= s.frozen_layers && !no_colsum;
+                if (below_trainable) before_colsum_write(l - 1);
                 const bool have = gemm_dx(k, l, *cur, B, 0, B, out, k.H[l].f, add,
-                                          below_trainable ? k.colsum : nullptr);
+                                          below_trainable ? k.colsum[(l - 1) % 3] : nullptr);
                 after_launch(c);
                 next_colsum = have;
             }
         }
-        if (trainable) {
-            {
-                PhaseScope ph(c, kPhDw, split ? 2 : 1);
-                if (split) {
-                    gemm_dw(k, l, in, *cur, B, 0, src, lr, adam);
-                    gemm_dw(k, l + 1, in, *cur, B, src, B - src, lr, adam);
-                } else {
-                    gemm_dw(k, l, in, *cur, B, 0, B, lr, adam);
-                }
-                after_launch(c, split ? 2 : 1);
+        // the head's dW reads only dlogits (own buffer), H and its own W: side stream
+        const bool dw_side = side && trainable && l == L - 1 && !split && !k.tc[k.layer_of(l)] &&
+                             (head_dw_ok(fo) || head_dw_ok(k.dims[l]));
+        if (bias_side || dw_side) {
+            c.fork();
+            if (bias_side) {
+                PhaseScope ph(c, kPhBias, 1, c.side);
+                launch_bias_from_partials(k.G, (B + 31) / 32, fo, k.colsum[l % 3], k.b[l], lr, bias_adam(l),
+                                          k.keep_grads ? k.gb[l] : nullptr, c.d_flags, c.side);
+                after_launch(c, 1);
+                bias_done[l % 3] = c.record(c.side);
+            }
+            if (dw_side) {
+                PhaseScope ph(c, kPhDw, 1, c.side);
+                gemm_dw(k, l, in, *cur, B, 0, B, lr, adam, c.side);
+                after_launch(c, 1);
             }
         }
+        if (trainable && !dw_side) {
+            PhaseScope ph(c, kPhDw, split ? 2 : 1);
+            if (split) {
+                gemm_dw(k, l, in, *cur, B, 0, src, lr, adam);
+                gemm_dw(k, l + 1, in, *cur, B, src, B - src, lr, adam);
+            } else {
+                gemm_dw(k, l, in, *cur, B, 0, B, lr, adam);
+            }
+            after_launch(c, split ? 2 : 1);
+        }
         colsum_ready = next_colsum;
-        std::swap(cur, nxt);
+        if (l == L - 1) {  // dlogits -> dZ[1] -> dZ[0] -> dZ[1] ...
+            cur = nxt;
+            nxt = spare;
+        } else {
+            std::swap(cur, nxt);
+        }
     }
+    c.join();  // every side-stream launch of this step
 
     if (loss_host || mmd_host) {
         double* h = static_cast<double*>(c.pinned_buf(2 * k.G * sizeof(double) + 64));
@@ -1257,7 +1311,8 @@ int mtk_bank_fingerprint(mtk_bank* k, uint64_t* out_host) {
         after_launch(c);
         auto* h = static_cast<unsigned long long*>(c.pinned_buf(sizeof(unsigned long long)));
         MTK_CUDA(cudaMemcpyAsync(h, d, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c.stream));
-        MTK_CUDA(cudaStreamSynchronize(c.stream));
+        c.join();
+            MTK_CUDA(cudaStreamSynchronize(c.stream));
         *out_host = *h;
     });
 }

@@ -70,6 +70,30 @@ void Ctx::check_flags() {
     }
 }
 
+cudaEvent_t Ctx::record(cudaStream_t s) {
+    cudaEvent_t& e = ev_ring[ev_next];
+    ev_next = (ev_next + 1) % 32;
+    if (!e) MTK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    MTK_CUDA(cudaEventRecord(e, s));  // a wait captures the state at call time: reuse is safe
+    return e;
+}
+
+void Ctx::fork() {
+    if (!side) {
+        int lo = 0, hi = 0;
+        MTK_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        MTK_CUDA(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, lo));  // lowest priority
+    }
+    MTK_CUDA(cudaStreamWaitEvent(side, record(stream), 0));
+    side_pending = true;
+}
+
+void Ctx::join() {
+    if (!side_pending) return;
+    MTK_CUDA(cudaStreamWaitEvent(stream, record(side), 0));
+    side_pending = false;
+}
+
 cudaEvent_t Ctx::take_event() {
     if (!event_pool.empty()) {
         cudaEvent_t e = event_pool.back();
@@ -94,17 +118,18 @@ void Ctx::collect_phases() {
     pending.clear();
 }
 
-PhaseScope::PhaseScope(Ctx& ctx, int phase, int launches) : c(ctx), ph(phase), n(launches) {
+PhaseScope::PhaseScope(Ctx& ctx, int phase, int launches, cudaStream_t s)
+    : c(ctx), ph(s && s != ctx.stream ? (int)kPhSide : phase), n(launches), st(s ? s : ctx.stream) {
     if (c.timing) {
         a = c.take_event();
-        MTK_CUDA(cudaEventRecord(a, c.stream));
+        MTK_CUDA(cudaEventRecord(a, st));
     }
 }
 
 PhaseScope::~PhaseScope() {
     if (!a) return;
     cudaEvent_t b = c.take_event();
-    cudaEventRecord(b, c.stream);
+    cudaEventRecord(b, st);
     c.pending.push_back({ph, {a, b}});
     c.phase_launches[ph] += n;
 }
@@ -149,6 +174,12 @@ int mtk_ctx_destroy(mtk_ctx* c) {
         if (c->pinned) cudaFreeHost(c->pinned);
         if (c->pinned_flags) cudaFreeHost(c->pinned_flags);
         if (c->own_stream) cudaStreamDestroy(c->stream);
+        if (c->side) {
+            cudaStreamSynchronize(c->side);
+            cudaStreamDestroy(c->side);
+        }
+        for (cudaEvent_t e : c->ev_ring)
+            if (e) cudaEventDestroy(e);
         delete c;
     });
 }

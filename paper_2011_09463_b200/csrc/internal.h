@@ -32,7 +32,7 @@ enum : int { kFlagNonFinite = 1, kFlagBadLabel = 2, kFlagBadIndex = 4 };
 
 // Phases of the bank step, for optional CUDA-event timing (mtk_ctx_set_timing).
 enum Phase : int { kPhFwd = 0, kPhCe, kPhMmdBeta, kPhMmdPairs, kPhDx, kPhDw, kPhBias, kPhOther,
-                   kNumPhases };
+                   kPhSide, kNumPhases };
 
 struct Ctx {
     int device = 0;
@@ -60,6 +60,17 @@ struct Ctx {
     size_t big_bytes = 0;
     void* pinned_buf(size_t bytes);
     void check_flags();               // synchronizes; throws on a set flag
+    // Side stream for short, latency-bound kernels that do not feed the next
+    // main-stream launch (bias updates, the skinny head dW, the MMD prep pass):
+    // they run beside the persistent GEMMs, on the SMs those leave idle in
+    // their last partial wave.  Ordering is by events only.
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_ring[32] = {};
+    int ev_next = 0;
+    bool side_pending = false;        // side work not yet joined into the main stream
+    cudaEvent_t record(cudaStream_t s);  // a fresh (no-timing) event recorded on s
+    void fork();                      // side waits for all main-stream work so far
+    void join();                      // main waits for all side-stream work so far
 };
 
 // RAII: records start/stop events around a launch group when timing is on.
@@ -67,8 +78,9 @@ struct PhaseScope {
     Ctx& c;
     int ph;
     int n;
+    cudaStream_t st;
     cudaEvent_t a = nullptr;
-    PhaseScope(Ctx& ctx, int phase, int launches = 1);
+    PhaseScope(Ctx& ctx, int phase, int launches = 1, cudaStream_t s = nullptr);  // s: side -> kPhSide
     ~PhaseScope();
 };
 
