@@ -261,8 +261,9 @@ namespace {
 
 // ---- GEMM dispatch over row range [r0, r0+rows) of every model -------------
 // FWD: out[r, n] = sum_k in[r, k] W[k, n] (+bias, ReLU)
-void gemm_fwd(mtk_bank& k, int mat, const Plane3& in, int B, int r0, int rows, const Plane3& out,
-              bool relu) {
+// returns true when `ce` (optional) was computed by the same launch (skinny head)
+bool gemm_fwd(mtk_bank& k, int mat, const Plane3& in, int B, int r0, int rows, const Plane3& out,
+              bool relu, const CeArgs* ce = nullptr) {
     Ctx& c = *k.ctx;
     const int fi = k.fan_in(mat), fo = k.fan_out(mat);
     if (k.tc[k.layer_of(mat)]) {
@@ -305,7 +306,9 @@ void gemm_fwd(mtk_bank& k, int mat, const Plane3& in, int B, int r0, int rows, c
         h.ldc = fo;
         h.relu = relu ? 1 : 0;
         h.flags = c.d_flags;
+        h.ce = (ce && r0 == 0 && rows == B && !relu) ? ce : nullptr;
         launch_head_fwd(h, c.stream);
+        return h.ce != nullptr;
     } else {
         Gemm g;
         g.G = k.G;
@@ -329,6 +332,7 @@ void gemm_fwd(mtk_bank& k, int mat, const Plane3& in, int B, int r0, int rows, c
         g.flags = c.d_flags;
         launch_gemm(g, c.stream);
     }
+    return false;
 }
 
 // DX: out[r, p] = (sum_j dz[r, j] W[p, j] + add[r, p]) * (mask[r, p] > 0)
@@ -515,8 +519,10 @@ Plane3 input_plane(mtk_bank& k, const float* X, int B) {
 }
 
 // after_hidden (optional) runs once the last hidden layer's forward is enqueued
-void run_forward(mtk_bank& k, const Plane3& X, int B, int head_all, int src_rows,
-                 const std::function<void()>& after_hidden = {}) {
+// returns true when the head launch also ran `ce` (optional, single head)
+bool run_forward(mtk_bank& k, const Plane3& X, int B, int head_all, int src_rows,
+                 const std::function<void()>& after_hidden = {}, const CeArgs* ce = nullptr) {
+    bool ce_done = false;
     Ctx& c = *k.ctx;
     Plane3 h = X;
     Plane3 lg;
@@ -529,7 +535,7 @@ void run_forward(mtk_bank& k, const Plane3& X, int B, int head_all, int src_rows
             h = k.H[l + 1];
             if (l == k.L - 2 && after_hidden) after_hidden();
         } else if (head_all >= 0) {
-            gemm_fwd(k, l + head_all, h, B, 0, B, lg, false);
+            ce_done = gemm_fwd(k, l + head_all, h, B, 0, B, lg, false, ce);
             after_launch(c);
         } else {  // two heads split by rows
             gemm_fwd(k, l, h, B, 0, src_rows, lg, false);
@@ -537,6 +543,7 @@ void run_forward(mtk_bank& k, const Plane3& X, int B, int head_all, int src_rows
             after_launch(c, 2);
         }
     }
+    return ce_done;
 }
 
 void train_step(mtk_bank& k, const mtk_step& s, double* loss_host, double* mmd_host) {
@@ -668,13 +675,6 @@ void train_step(mtk_bank& k, const mtk_step& s, double* loss_host, double* mmd_h
     }
     // the prep pass only needs the last hidden layer: it forks off after that
     // layer's forward GEMM and runs beside the head forward and CE
-    run_forward(k, X, B, two ? -1 : 0, src, prep_on_side ? [&] {
-        c.fork();
-        PhaseScope ph(c, kPhMmdBeta, 2, c.side);  // prep pass: tf32 planes, norms, beta
-        launch_mmd_tc(a, k.mmd_z, c.side, kMmdPrep);
-        after_launch(c, 2);
-    } : std::function<void()>());
-
     Plane3* cur = &k.dlog;
     Plane3* nxt = &k.dZ[1];
     Plane3* spare = &k.dZ[0];  // becomes nxt after the head (dlogits keep their own buffer)
@@ -683,7 +683,27 @@ void train_step(mtk_bank& k, const mtk_step& s, double* loss_host, double* mmd_h
               c.d_flags, k.loss_part};
     // the head's bias gradient comes out of the CE kernel as column partials
     ce.colsum = (!two && L - 1 >= s.frozen_layers && !no_colsum) ? k.colsum[(L - 1) % 3] : nullptr;
-    {
+    const char* nhc = getenv("MTK_NO_HEAD_CE");  // A/B (read per call)
+    const bool fuse_ce = side && !(nhc && nhc[0] == '1');
+    // the skinny head's forward also runs the CE rows (fuse_ce), and the MMD
+    // prep pass forks off after the last hidden layer to run beside them
+    const bool ce_done = run_forward(k, X, B, two ? -1 : 0, src, prep_on_side ? [&] {
+        c.fork();
+        PhaseScope ph(c, kPhMmdBeta, 2, c.side);  // prep pass: tf32 planes, norms, beta
+        launch_mmd_tc(a, k.mmd_z, c.side, kMmdPrep);
+        after_launch(c, 2);
+    } : std::function<void()>(), fuse_ce ? &ce : nullptr);
+    // the loss finish only feeds the host read-back: it joins the first side
+    // segment of the backward sweep (a fork here would make the MMD's join wait)
+    bool ce_loss_pending = ce_done;
+    auto launch_ce_loss_side = [&] {
+        if (!ce_loss_pending) return;
+        PhaseScope ph(c, kPhCe, 1, c.side);
+        launch_ce_loss(ce, c.side);
+        after_launch(c, 1);
+        ce_loss_pending = false;
+    };
+    if (!ce_done) {
         PhaseScope ph(c, kPhCe, 2);
         launch_ce(ce, c.stream);
         after_launch(c, 2);
@@ -773,6 +793,7 @@ void train_step(mtk_bank& k, const mtk_step& s, double* loss_host, double* mmd_h
                              (head_dw_ok(fo) || head_dw_ok(k.dims[l]));
         if (bias_side || dw_side) {
             c.fork();
+            launch_ce_loss_side();
             if (bias_side) {
                 PhaseScope ph(c, kPhBias, 1, c.side);
                 launch_bias_from_partials(k.G, (B + 31) / 32, fo, k.colsum[l % 3], k.b[l], lr, bias_adam(l),
@@ -803,6 +824,10 @@ void train_step(mtk_bank& k, const mtk_step& s, double* loss_host, double* mmd_h
         } else {
             std::swap(cur, nxt);
         }
+    }
+    if (ce_loss_pending) {
+        c.fork();
+        launch_ce_loss_side();
     }
     c.join();  // every side-stream launch of this step
 

@@ -216,6 +216,7 @@ struct UmmaGemm {
 void launch_umma(const UmmaGemm& u, cudaStream_t s);
 
 // Skinny layers (out width <= 32): k_head.cu
+struct CeArgs;
 struct HeadFwd {
     int G = 1, rows = 0, K = 0, N = 0;
     const float* A = nullptr;
@@ -228,6 +229,10 @@ struct HeadFwd {
     long long c_gs = 0, ldc = 0;
     int relu = 0;
     int* flags = nullptr;
+    // optional: softmax-CE of the finished logits rows in the same kernel
+    // (ce_kernel's per-row work and per-32-row partials; rows = ce->B, C = N);
+    // the loss finish (launch_ce_loss) stays a separate launch
+    const CeArgs* ce = nullptr;
 };
 struct HeadDw {
     int G = 1, rows = 0, K = 0, N = 0;
@@ -283,7 +288,8 @@ struct CeArgs {
     double* loss_part;      // [G][ceil(B/32)] scratch
     float* colsum = nullptr;  // optional [G][ceil(B/32)][C] dlogits column partials
 };
-void launch_ce(const CeArgs& a, cudaStream_t s);
+void launch_ce(const CeArgs& a, cudaStream_t s);       // rows + loss finish
+void launch_ce_loss(const CeArgs& a, cudaStream_t s);  // the loss finish alone
 
 // Column sums + SGD on a bias: db[g,n] = sum_{rows} dZ[g, r, n]; b -= lr*db
 // bias update from per-row-block column partials [G][nrb][N] (fixed order)

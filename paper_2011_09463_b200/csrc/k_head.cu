@@ -11,6 +11,7 @@
 #include <cmath>
 
 #include "internal.h"
+#include "ce_row.cuh"
 #include "sm100.cuh"
 
 namespace mtk {
@@ -21,10 +22,13 @@ constexpr int MAXN = 32;
 __device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
 
 // ---- forward: block = 64 rows x 2 k-halves (128 threads); thread owns one row
-// and all NP outputs; A and W staged through smem in 64-wide k chunks.
+// and all NP outputs; A and W staged through smem in 64-wide k chunks, the
+// next A chunk's loads in flight (registers) while the current one computes.
+// With do_ce the row-owning warps (one 32-row CE block each) go on to the
+// softmax-CE of their finished logits (ce_row.cuh, as ce_kernel).
 constexpr int FR = 64, FK = 64;
 template <int NP>
-__global__ void __launch_bounds__(128) head_fwd_kernel(HeadFwd p) {
+__global__ void __launch_bounds__(128) head_fwd_kernel(HeadFwd p, CeArgs ce, int do_ce) {
     __shared__ float sA[FR][FK + 1];
     __shared__ __align__(16) float sW[FK][NP];
     __shared__ float red[FR][NP + 1];
@@ -38,19 +42,24 @@ __global__ void __launch_bounds__(128) head_fwd_kernel(HeadFwd p) {
     float acc[NP];
 #pragma unroll
     for (int n = 0; n < NP; ++n) acc[n] = 0.f;
+    constexpr int PA = FR * FK / 4 / 128;
+    float4 v[PA];  // the next A chunk (vec path)
+    auto load_a = [&](int k0) {
+        const int kc = min(FK, p.K - k0);
+#pragma unroll
+        for (int i = 0; i < PA; ++i) {
+            const int e = t + 128 * i, rr = e / (FK / 4), c4 = e % (FK / 4);
+            v[i] = (r0 + rr < p.rows && 4 * c4 < kc) ? ldg4(A + (long long)(r0 + rr) * p.lda + k0 + 4 * c4)
+                                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    };
+    if (vec) load_a(0);
     for (int k0 = 0; k0 < p.K; k0 += FK) {
         const int kc = min(FK, p.K - k0);
         __syncthreads();
         if (vec) {
-            float4 v[FR * FK / 4 / 128];  // all loads in flight before the smem stores
 #pragma unroll
-            for (int i = 0; i < FR * FK / 4 / 128; ++i) {
-                const int e = t + 128 * i, rr = e / (FK / 4), c4 = e % (FK / 4);
-                v[i] = (r0 + rr < p.rows && 4 * c4 < kc) ? ldg4(A + (long long)(r0 + rr) * p.lda + k0 + 4 * c4)
-                                                         : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-#pragma unroll
-            for (int i = 0; i < FR * FK / 4 / 128; ++i) {
+            for (int i = 0; i < PA; ++i) {
                 const int e = t + 128 * i, rr = e / (FK / 4), c4 = e % (FK / 4);
                 sA[rr][4 * c4] = v[i].x;
                 sA[rr][4 * c4 + 1] = v[i].y;
@@ -78,6 +87,7 @@ __global__ void __launch_bounds__(128) head_fwd_kernel(HeadFwd p) {
             }
         }
         __syncthreads();
+        if (vec && k0 + FK < p.K) load_a(k0 + FK);  // in flight during this chunk's FMAs
 #pragma unroll 4
         for (int kk = half; kk < FK; kk += 2) {
             const float a = sA[row][kk];
@@ -95,19 +105,40 @@ __global__ void __launch_bounds__(128) head_fwd_kernel(HeadFwd p) {
 #pragma unroll
         for (int n = 0; n < NP; ++n) red[row][n] = acc[n];
     __syncthreads();
+    if (half == 1) return;  // warps 2, 3
     const int r = r0 + row;
-    if (half == 1 || r >= p.rows) return;
+    const bool active = r < p.rows;
     bool bad = false;
+    float x[NP];
     float* out = p.C + g * p.c_gs + (long long)r * p.ldc;
 #pragma unroll
     for (int n = 0; n < NP; ++n) {
-        if (n >= N) break;
-        float v = (acc[n] + red[row][n]) + p.bias[g * p.bias_gs + n];
-        bad |= !isfinite(v);
-        if (p.relu) v = v > 0.f ? v : 0.f;
-        out[n] = v;
+        float val = 0.f;
+        if (n < N) {
+            val = (acc[n] + red[row][n]) + p.bias[g * p.bias_gs + n];
+            bad |= active && !isfinite(val);
+            if (p.relu) val = val > 0.f ? val : 0.f;
+            if (active) out[n] = val;
+        }
+        x[n] = val;
     }
     if (bad && p.flags) atomicOr(p.flags, kFlagNonFinite);
+    if (do_ce) {  // rows r0 .. r0 + 63: two whole 32-row CE blocks (FR = 64)
+        float dx[NP];
+        double rl = 0.0;
+#pragma unroll
+        for (int n = 0; n < NP; ++n) dx[n] = 0.f;
+        const long long rr = (long long)g * ce.B + r;
+        if (active) {
+            rl = ce_row(ce, r, rr, x, dx);
+            float* d = ce.dlogits + rr * ce.C;
+#pragma unroll
+            for (int j = 0; j < NP; ++j)
+                if (j < ce.C) d[j] = dx[j];
+            ce.row_loss[rr] = rl;
+        }
+        ce_warp_partials(ce, g, r >> 5, row & 31, rl, dx);
+    }
 }
 
 // ---- dX: out[r, q] = (sum_j dz[r, j] W[q, j] + add[r, q]) * (mask[r, q] > 0).
@@ -338,7 +369,9 @@ void by_width(int N, const P& p, cudaStream_t s) {
 template <int NP>
 struct FwdLaunch {
     static void run(const HeadFwd& p, cudaStream_t s) {
-        head_fwd_kernel<NP><<<dim3((p.rows + FR - 1) / FR, p.G), 128, 0, s>>>(p);
+        CeArgs ce{};
+        if (p.ce) ce = *p.ce;
+        head_fwd_kernel<NP><<<dim3((p.rows + FR - 1) / FR, p.G), 128, 0, s>>>(p, ce, p.ce ? 1 : 0);
     }
 };
 template <int NP>
@@ -362,6 +395,9 @@ bool head_dw_ok(int N) { return N >= 1 && N <= MAXN; }
 
 void launch_head_fwd(const HeadFwd& p, cudaStream_t s) {
     if (p.rows <= 0) return;
+    if (p.ce && (p.ce->B != p.rows || p.ce->C != p.N || p.ce->logits != p.C || p.c_gs != (long long)p.rows * p.N ||
+                 p.ldc != p.N || p.relu))
+        fail(MTK_ERROR, "head_fwd: fused CE needs the [G][rows][N] logits of a linear head");
     by_width<FwdLaunch>(p.N, p, s);
     count_launch();
 }

@@ -12,6 +12,7 @@
 #include <cmath>
 
 #include "internal.h"
+#include "ce_row.cuh"
 #include "sm100.cuh"
 
 namespace mtk {
@@ -136,48 +137,24 @@ __global__ void __launch_bounds__(256) ce_kernel(CeArgs a) {
     const int g = blockIdx.y;
     const int i = blockIdx.x * 256 + threadIdx.x;  // row within the model
     const int lane = threadIdx.x & 31;
-    const int blk = i >> 5;                        // 32-row block
-    const int nblk = (a.B + 31) / 32;
     const bool active = i < a.B;
     const long long r = (long long)g * a.B + i;
     double rl = 0.0;
-    float dx[32];
+    float x[32], dx[32];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) dx[j] = 0.f;
+    for (int j = 0; j < 32; ++j) {
+        x[j] = (active && j < a.C) ? a.logits[r * a.C + j] : 0.f;
+        dx[j] = 0.f;
+    }
     if (active) {
-        const float* x = a.logits + r * a.C;
-        const int lab = a.y[r];
-        if (lab < 0 || lab >= a.C) {
-            atomicOr(a.flags, kFlagBadLabel);
-        } else {
-            float mx = x[0];
-            for (int j = 1; j < a.C; ++j) mx = fmaxf(mx, x[j]);
-            float z = 0.f;
-            for (int j = 0; j < a.C; ++j) z += expf(x[j] - mx);
-            const float lse = mx + logf(z);
-            const float inv = (i < a.src_rows) ? a.inv_denom0 : a.inv_denom1;
-            const float wi = (a.w ? a.w[r] : 1.f) * inv;
-            rl = (double)wi * ((double)lse - (double)x[lab]);
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-                if (j < a.C) dx[j] = wi * (expf(x[j] - lse) - (j == lab ? 1.f : 0.f));
-        }
+        rl = ce_row(a, i, r, x, dx);
         float* d = a.dlogits + r * a.C;
-        for (int j = 0; j < a.C; ++j) d[j] = dx[j];
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            if (j < a.C) d[j] = dx[j];
         a.row_loss[r] = rl;
     }
-    // warp partials (inactive rows contribute zeros)
-    for (int o = 16; o > 0; o >>= 1) rl += __shfl_xor_sync(0xffffffffu, rl, o);
-    if (lane == 0 && blk < nblk) a.loss_part[(long long)g * nblk + blk] = rl;
-    if (a.colsum) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-            if (j >= a.C) break;
-            float v = dx[j];
-            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            if (lane == 0 && blk < nblk) a.colsum[((long long)g * nblk + blk) * a.C + j] = v;
-        }
-    }
+    ce_warp_partials(a, g, i >> 5, lane, rl, dx);  // inactive rows contribute zeros
 }
 
 // loss[g] = sum of the 32-row partials in order
@@ -242,6 +219,10 @@ void launch_ce(const CeArgs& a, cudaStream_t s) {
     if (a.C > 32) fail(MTK_SHAPE_ERROR, "cross_entropy: more than 32 classes");
     ce_kernel<<<dim3((a.B + 255) / 256, a.G), 256, 0, s>>>(a);
     count_launch();
+    launch_ce_loss(a, s);
+}
+
+void launch_ce_loss(const CeArgs& a, cudaStream_t s) {
     ce_loss_kernel<<<(a.G + 127) / 128, 128, 0, s>>>(a.loss_part, a.G, (a.B + 31) / 32, a.loss, a.flags);
     count_launch();
 }

@@ -188,6 +188,37 @@ def test_head_dx_fused_into_mmd_gradient_gemm(ctx, monkeypatch, B, src, dims, fr
                 assert np.array_equal(g0[g][0][i], g1[g][0][i]), (g, i)  # the head's own dW
 
 
+@pytest.mark.parametrize("B,dims,lam,weighted", [
+    (300, [96, 64, 10], 0.0, True), (77, [40, 3], 0.0, False), (130, [64, 48, 20], 0.5, True),
+    (300, [96, 64, 10], 0.7, False), (1024, [1024, 512, 256, 10], 1.0, False), (96, [64, 32, 16], 0.6, True)])
+def test_head_forward_with_fused_ce_is_bit_identical(ctx, monkeypatch, B, dims, lam, weighted):
+    """The skinny head's forward kernel also runs the softmax-CE rows (same
+    ce_row code as ce_kernel, same per-32-row partial order): the step must be
+    bit-identical to the separate CE launch (MTK_NO_HEAD_CE=1), including
+    ragged 64-row blocks and label weights; one launch fewer."""
+    G = 3
+    X, y = inputs(G, B, dims[0], dims[-1], shift=0.3)
+    Xd, yd = to_dev(X, y)
+    wd = None
+    if weighted:
+        wd = torch.tensor(np.linspace(0.0, 2.0, G * B, dtype=np.float32).reshape(G, B), device="cuda")
+    res = []
+    for off in ("0", "1"):
+        monkeypatch.setenv("MTK_NO_HEAD_CE", off)
+        bank = make_bank(ctx, G, dims, seed=4)
+        torch.cuda.synchronize()
+        n0 = ctx.launches
+        loss, mmd = bank.train_step(Xd, yd, wd, lr=0.05, src_rows=B // 2 if lam else 0, mmd_lambda=lam)
+        res.append((loss.copy(), mmd.copy(), [bank.get_params(g) for g in range(G)], ctx.launches - n0))
+    (l0, m0, p0, n0), (l1, m1, p1, n1) = res
+    assert n0 == n1 - 1, (n0, n1)
+    assert np.array_equal(l0, l1) and np.array_equal(m0, m1)
+    for g in range(G):
+        for k in (0, 1):
+            for a, b in zip(p0[g][k], p1[g][k]):
+                assert np.array_equal(a, b), g
+
+
 def test_step_two_heads_parameter_based(ctx):
     dims = [784, 256, 10]
     bank = make_bank(ctx, 3, dims, n_heads=2)
