@@ -394,8 +394,11 @@ def mmd_gaussian(ctx: Context, Xs: torch.Tensor, Xt: torch.Tensor, mult=None, be
     n = Xt.shape[0]
     mu = _mult_arr(mult)
     v, bo = C.c_double(), C.c_double()
-    gs = torch.empty_like(Xs) if grads else None
-    gt = torch.empty_like(Xt) if grads else None
+    gs = gt = None
+    if grads:  # one [m + n, d] block: with Xs, Xt views of one block too, the
+        # library can take its materialised-kernel-matrix path
+        g = torch.empty((m + n, d), dtype=Xs.dtype, device=Xs.device)
+        gs, gt = g[:m], g[m:]
     errors.check(lib.mtk_mmd_gaussian(ctx.h, _ptr(Xs), m, _ptr(Xt), n, d, mu.ctypes.data_as(_dp),
                                       len(mu), beta, C.byref(v), C.byref(bo), _ptr(gs), _ptr(gt)),
                  "mmd_gaussian")

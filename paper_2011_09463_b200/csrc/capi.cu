@@ -231,6 +231,9 @@ static MmdArgs mmd_args(mtk_ctx* c, const float* Xs, int64_t m, const float* Xt,
     a.d = d;
     a.Xs = Xs;
     a.Xt = Xt;
+    // one group: the group strides are never stepped, but the materialised-W
+    // path checks that [Xs; Xt] (and the gradients) form one [m + n][d] block
+    a.xs_gs = a.xt_gs = a.gs_gs = a.gt_gs = (m + n) * (long long)d;
     if (nb > 0) {
         need(mult != nullptr, MTK_VALUE_ERROR, "mmd: null bandwidth multipliers");
         a.nb = nb;

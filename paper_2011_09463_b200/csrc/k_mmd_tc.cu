@@ -725,13 +725,17 @@ struct MmdWParams {
     int diag;                  // diagnostics (MTK_MMDW_DIAG): 1 = epilogue only arrives, 2 = no MMAs
 };
 
+// unordered tile pair p -> (I, J), I <= J, row-major over the upper triangle
+// (row I starts at S(I) = I*T - I*(I-1)/2): closed form + integer fix-up
 __device__ __forceinline__ void pair_of(int p, int T, int& I, int& J) {
-    I = 0;
-    while (p >= T - I) {
-        p -= T - I;
-        ++I;
-    }
-    J = I + p;
+    const double b = 2.0 * T + 1.0;
+    int i = (int)((b - sqrt(b * b - 8.0 * (double)p)) * 0.5);
+    i = max(0, min(i, T - 1));
+    auto start = [T](int r) { return (long long)r * T - (long long)r * (r - 1) / 2; };
+    while (i > 0 && start(i) > p) --i;
+    while (i + 1 < T && start(i + 1) <= p) ++i;
+    I = i;
+    J = i + (int)(p - start(i));
 }
 
 // 8 column values per lane (lane = row) -> the sum over the warp's 32 rows
@@ -909,7 +913,7 @@ __global__ void __launch_bounds__(W_THREADS, 1) mmd_w_kernel(const __grid_consta
             const float* nrm = p.norms + (long long)g * N;
             const float ni = row_ok ? nrm[gi] : 0.f;
             float* Wg = p.W + (long long)g * N * p.ldw;
-            const unsigned ldw = (unsigned)p.ldw;
+            const long long ldw = p.ldw;
             const int buf = lt & 1;
             mbar_wait(&acc_full[buf], (lt >> 1) & 1);
             tc_fence_after();
@@ -1041,7 +1045,7 @@ __global__ void __launch_bounds__(W_THREADS, 1) mmd_w_kernel(const __grid_consta
                 for (int c = 0; c < 8; ++c) tw[lane * W_TILE_LD + (ch - 4 * h) * 8 + c] = wv[c];
                 if (!diag) {
                     // (j, i): lanes are consecutive i -> one 128-B row segment per store
-                    float* dt = Wg + ((unsigned)jb * ldw + (unsigned)gi);
+                    float* dt = Wg + ((long long)jb * ldw + gi);
                     if (p.diag == 3 || p.diag == 4) {
                     } else if (row_ok && full8) {
 #pragma unroll
@@ -1067,7 +1071,7 @@ __global__ void __launch_bounds__(W_THREADS, 1) mmd_w_kernel(const __grid_consta
                 const int r0 = I * WT + 32 * q;
                 const int nr = min(32, (int)N - r0);
                 if (jc < N) {
-                    float* dst = Wg + ((unsigned)r0 * ldw + (unsigned)jc);
+                    float* dst = Wg + ((long long)r0 * ldw + jc);
 #pragma unroll 8
                     for (int rr = 0; rr < nr; ++rr) {
                         *dst = tw[rr * W_TILE_LD + lane];
@@ -1193,6 +1197,28 @@ __global__ void __launch_bounds__(WSUM_THREADS) mmd_wsum_kernel(const float* rpa
     if (threadIdx.x < 3) partial[((long long)g * T + I) * 3 + threadIdx.x] = total[threadIdx.x];
 }
 
+// g = scale * (z * Wsum - sum_c V_c), the chunk partials summed in ascending
+// chunk order in fp64 (the multi-chunk V = W.Z of the materialised-W path)
+__global__ void mmd_vchunk_finish_kernel(const float* __restrict__ vpart, int chunks, long long per,
+                                         const float* __restrict__ Z, long long z_gs,
+                                         const float* __restrict__ wsum, float* __restrict__ gout,
+                                         long long g_gs, int G, long long N, int d, float scale, int* flags) {
+    const long long total = (long long)G * per;  // per = N * d
+    bool bad = false;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int g = (int)(e / per);
+        const long long o = e % per, i = o / d;
+        double v = 0.0;
+        for (int c = 0; c < chunks; ++c) v += (double)vpart[(long long)c * total + e];
+        const double z = (double)Z[g * z_gs + o];
+        const float x = (float)((double)scale * (z * (double)wsum[(long long)g * N + i] - v));
+        bad |= !isfinite(x);
+        gout[g * g_gs + o] = x;
+    }
+    if (bad) atomicOr(flags, kFlagNonFinite);
+}
+
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                               const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                               const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -1243,6 +1269,9 @@ int mmd_tc_blocks_per_group(const MmdArgs& a) {
 // with gradients whose samples and gradients are each one contiguous
 // [G][m+n][d] block and whose W fits the budget; MTK_MMD_FUSED=1 forces the
 // fused kernel (A/B)
+// W budget: fixed (not free-memory dependent), so the path -- and with it the
+// rounding -- is the same on every box.  C4 (N = 73,728, one group) needs 21.7 GB.
+constexpr double kWBudget = 48.0 * 1024 * 1024 * 1024;
 static bool w_path(const MmdArgs& a) {
     const char* fe = getenv("MTK_MMD_FUSED");
     const bool fused = fe && fe[0] == '1';
@@ -1252,11 +1281,17 @@ static bool w_path(const MmdArgs& a) {
     if (a.d % 4 || a.d < 32 || N % 4) return false;
     if (a.Xt != a.Xs + a.m * a.d || a.xt_gs != a.xs_gs || a.xs_gs < N * a.d) return false;
     if (a.gXt != a.gXs + a.m * a.d || a.gt_gs != a.gs_gs || a.gs_gs != a.xs_gs) return false;
-    return (double)a.G * N * N * 4.0 <= 2.0 * 1024 * 1024 * 1024;
+    return (double)a.G * N * N * 4.0 <= kWBudget;
 }
 
+// V = W.Z accumulates in fp32 in TMEM; past kVChunk columns of W it runs as
+// kVChunk-deep GEMMs whose fp32 partials are summed in fp64 (the fused pair
+// kernel's V flush interval: 16 j tiles of 64)
+constexpr long long kVChunk = 1024;
+static int v_chunks(const MmdArgs& a) { return (int)((a.m + a.n + kVChunk - 1) / kVChunk); }
+
 static bool head_block(const MmdArgs& a) {
-    return a.hd_n > 0 && a.hd_n <= kHeadK && (a.m + a.n) % 32 == 0;
+    return a.hd_n > 0 && a.hd_n <= kHeadK && (a.m + a.n) % 32 == 0 && v_chunks(a) == 1;
 }
 
 bool mmd_head_fusable(const MmdArgs& a) { return w_path(a) && head_block(a); }
@@ -1264,6 +1299,7 @@ bool mmd_head_fusable(const MmdArgs& a) { return w_path(a) && head_block(a); }
 struct WLayout {
     long long ldw;  // row stride of W: N, or N + kHeadK with the head block
     float* bx;      // [G][kHeadK][d]: -W_head^T / lambda, zero rows past hd_n
+    float* vpart;   // [chunks][G][N][d] fp32 partials of V (more than one chunk)
     float* W;
     float* rpart;
     float* cpart;
@@ -1290,6 +1326,8 @@ static WLayout w_layout(const MmdArgs& a, uintptr_t base) {
     cur = (cur + (size_t)a.G * np * W_EPI_WARPS * 3 * 8 + 255) & ~uintptr_t(255);
     L.wsum = reinterpret_cast<float*>(cur);
     cur = (cur + (size_t)a.G * N * 4 + 255) & ~uintptr_t(255);
+    L.vpart = reinterpret_cast<float*>(cur);
+    if (v_chunks(a) > 1) cur = (cur + (size_t)v_chunks(a) * a.G * N * a.d * 4 + 255) & ~uintptr_t(255);
     L.bytes = cur - start + 256;
     return L;
 }
@@ -1437,6 +1475,29 @@ void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s, int stages) 
         u.rowvec = L.wsum;
         u.scale = a.grad_scale;
         u.flags = a.flags;
+        const int nch = v_chunks(a);
+        if (nch > 1) {  // kVChunk-deep GEMMs into fp32 partials, then the fp64 finish
+            const long long per = N * a.d;
+            for (int c = 0; c < nch; ++c) {
+                const long long k0 = (long long)c * kVChunk;
+                UmmaGemm v = u;
+                v.K = (int)std::min(kVChunk, N - k0);
+                v.a = L.W + k0;
+                v.b = a.Xs + k0 * a.d;
+                v.epi = Epi::kStore;
+                v.C = L.vpart + (long long)c * a.G * per;
+                v.c_gs = per;
+                v.add = nullptr;
+                v.rowvec = nullptr;
+                v.colsum = nullptr;
+                launch_umma(v, s);
+            }
+            const long long tot = (long long)a.G * per;
+            mmd_vchunk_finish_kernel<<<(unsigned)std::min<long long>((tot + 255) / 256, 148 * 16), 256, 0, s>>>(
+                L.vpart, nch, per, a.Xs, a.xs_gs, L.wsum, a.gXs, a.gs_gs, a.G, N, a.d, a.grad_scale, a.flags);
+            count_launch();
+            return;
+        }
         launch_umma(u, s);
         return;
     }

@@ -153,3 +153,33 @@ def test_mmd_tensor_core_vs_simt(ctx, monkeypatch, m, n, d):
     for v, g in out:
         assert rel(v, ov) <= TOL
         assert rel(g, og) <= TOL
+
+
+@pytest.mark.parametrize("m,n,d", [(3000, 1000, 64), (700, 332, 96), (600, 400, 128)])
+def test_mmd_api_materialised_w_path(ctx, monkeypatch, m, n, d):
+    """Xs, Xt given as views of one [m + n, d] block: the C-ABI call takes the
+    materialised-W path (each unordered 128x128 tile pair once, V = W.Z as a
+    GEMM).  It must agree with the fused pair kernel (MTK_MMD_FUSED=1) and the
+    f64 oracle.  N > 1024 runs V as 1024-deep GEMMs summed in fp64 (N = 4000,
+    1032); N = 1000 is one GEMM with the fused gradient epilogue."""
+    from paper_2011_09463_b200 import api
+
+    rng = np.random.default_rng(m + d)
+    Z = rng.standard_normal((m + n, d)).astype(np.float32)
+    Z[m:] += 0.2
+    Zd = torch.tensor(Z, device="cuda")
+    res = []
+    for fused in ("0", "1"):
+        monkeypatch.setenv("MTK_MMD_FUSED", fused)
+        torch.cuda.synchronize()
+        n0 = ctx.launches
+        v, beta, gs, gt = api.mmd_gaussian(ctx, Zd[:m], Zd[m:])
+        res.append((v, beta, gs.cpu().numpy(), gt.cpu().numpy(), ctx.launches - n0))
+    (v0, b0, gs0, gt0, n0), (v1, b1, gs1, gt1, n1) = res
+    assert n0 != n1  # different kernels ran
+    assert b0 == b1
+    assert abs(v0 - v1) <= 1e-5 * abs(v1)
+    assert rel(gs0, gs1) <= 2e-5 and rel(gt0, gt1) <= 2e-5
+    ov, ob, ogs, ogt = po.mmd_gaussian(Z[:m].astype(np.float64), Z[m:].astype(np.float64))
+    assert abs(v0 - ov) <= 1e-5 * abs(ov)
+    assert rel(gs0, ogs) <= 1e-5 and rel(gt0, ogt) <= 1e-5
