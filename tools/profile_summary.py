@@ -29,7 +29,12 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-3, "us": 
          "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
 
 
+SIDE = ("mmd_prep", "beta_finish", "bias_from_partials", "head_dw", "ce_loss")  # side-stream launches
+
+
 def phase_of(name, in_mmd=False):
+    if any(s in name for s in SIDE):
+        return "side_stream"  # overlapped with the main stream in the bench (serialised under ncu)
     if in_mmd or "mmd_w_kernel" in name or "mmd_wsum" in name:
         return "mmd_pairs"  # the materialised-W path: pass 1, Wsum, V = W.Z GEMM
     if "umma_kernel<0, 1" in name or "head_fwd" in name:
