@@ -331,11 +331,8 @@ def run_attack_arm(args, world, rank, local):
     rng = api.Rng(77)
     att.init_params(0, rng)
 
-    def step():
-        F = api.posterior_features(ctx, logits, 3)
-        out = att.forward(F.reshape(1, ATT_Q, 3))
-        score = api.posterior_column(ctx, out, 1)
-        return api.auc(ctx, score, labels)
+    def step():  # mtk_attack_auc: one streaming scoring kernel + the AUC sort / count
+        return api.attack_auc(att, logits, labels)
 
     for _ in range(max(args.warmup, 1)):
         step()
@@ -356,9 +353,10 @@ def run_attack_arm(args, world, rank, local):
     if rank != 0:
         return
     _, _, hbm, src = peaks()
-    # algorithmic bytes per query: logits 40 + features 12 (w) + 12 (r) + out 8 (w) + 8 (r)
-    # + score 4 (w) + AUC: score 4 + label 1 read, sorted pairs (4+4) written/read twice
-    bytes_q = 40 + 12 + 12 + 8 + 8 + 4 + 5 + 2 * 2 * 8
+    # algorithmic bytes per query: logits 40 + label 1 read, two AUC keys written (8);
+    # the sort reads and writes the 4-B keys (one pass counted), the count reads
+    # label + member key + ~1 probe (9)
+    bytes_q = 40 + 1 + 8 + 2 * 4 + 9
     qps = world * ATT_Q * args.steps / (ms / 1000.0)
     gbs = qps * bytes_q / world / 1e9
     line = {
@@ -370,7 +368,7 @@ def run_attack_arm(args, world, rank, local):
                                "features -> attack MLP 3-64-2 -> score -> AUC/accuracy per rank",
                    "queries_per_gpu": ATT_Q, "parallelism": f"shard{world}", "auc": auc,
                    "accuracy": acc},
-        "roofline": {"bound": "hbm", "kernel": "features + attack forward + AUC (whole stage)",
+        "roofline": {"bound": "hbm", "kernel": "attack_score + AUC sort/count (whole stage)",
                      "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm if hbm else None,
                      "traffic": None,
                      "peak_note": f"{src} HBM copy bandwidth; {bytes_q} algorithmic B/query"},

@@ -271,6 +271,17 @@ int mtk_posterior_column(mtk_ctx* ctx, const float* logits, int64_t rows, int C,
  * may be NULL).  labels: 1 = member.  Synchronizing.                        */
 int mtk_auc(mtk_ctx* ctx, const float* scores, const uint8_t* labels, int64_t n,
             double* auc_host, double* acc_host);
+/* The whole attack evaluation of `rows` queried posteriors in one call:
+ * softmax -> top-k sorted features (k = the attack bank's input width) ->
+ * attack model (model 0 of `attack`, linear head) -> member probability
+ * (softmax column 1) -> mid-rank AUC + accuracy at 0.5.  Same results as
+ * mtk_posterior_features + mtk_bank_forward + mtk_posterior_column + mtk_auc
+ * (bit-identical scores); the [3, 64, 2] attack model over <= 16 classes runs
+ * as one streaming kernel with the weights in constant memory.  scores_out
+ * (device, [rows]) may be NULL.  Synchronizing.  Stands in for the absent
+ * reference attack stage.                   */
+int mtk_attack_auc(mtk_bank* attack, const float* logits, int64_t rows, int C, const uint8_t* labels,
+                   double* auc_host, double* acc_host, float* scores_out);
 
 /* ---- diagnostics (tests / profiling): C[g] = A[g] * B[g] through the
  * tcgen05 3xTF32 tensor-core GEMM used by the bank.  a_mn: A stored

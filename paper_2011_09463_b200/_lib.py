@@ -108,6 +108,7 @@ SIGNATURES = {
     "mtk_posterior_features": (C.c_int, [_vp, _vp, C.c_int64, C.c_int, C.c_int, _vp, _vp]),
     "mtk_posterior_column": (C.c_int, [_vp, _vp, C.c_int64, C.c_int, C.c_int, _vp]),
     "mtk_auc": (C.c_int, [_vp, _vp, _vp, C.c_int64, _dp, _dp]),
+    "mtk_attack_auc": (C.c_int, [_vp, _vp, C.c_int64, C.c_int, _vp, _dp, _dp, _vp]),
     "mtk_diag_gemm_tf32x3": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                        _vp, _vp, _vp]),
 }

@@ -527,6 +527,18 @@ def auc(ctx: Context, scores: torch.Tensor, labels: torch.Tensor):
     return a.value, acc.value
 
 
+def attack_auc(attack: "Bank", logits: torch.Tensor, labels: torch.Tensor, scores: bool = False):
+    """The attack stage in one call: posteriors -> top-k features -> attack
+    model (model 0 of `attack`) -> member probability -> (AUC, accuracy[, scores]).
+    Same results as posterior_features + Bank.forward + posterior_column + auc."""
+    logits2 = logits.reshape(-1, logits.shape[-1])
+    a, acc = C.c_double(), C.c_double()
+    out = torch.empty(logits2.shape[0], device=logits.device, dtype=torch.float32) if scores else None
+    errors.check(lib.mtk_attack_auc(attack.h, _ptr(logits2), logits2.shape[0], logits2.shape[1],
+                                    _ptr(labels), C.byref(a), C.byref(acc), _ptr(out)), "attack_auc")
+    return (a.value, acc.value, out) if scores else (a.value, acc.value)
+
+
 def diag_gemm_tf32x3(ctx: Context, A: torch.Tensor, B: torch.Tensor, a_mn: bool, b_mn: bool):
     """Diagnostics: C = A @ B on the tcgen05 3xTF32 path.  A is [G,M,K] (or
     [G,K,M] if a_mn), B is [G,K,N] (or [G,N,K] if not b_mn); returns [G,M,N]."""

@@ -1012,6 +1012,43 @@ int mtk_bank_forward(mtk_bank* k, const float* X, int B, int head, float* logits
     });
 }
 
+int mtk_attack_auc(mtk_bank* k, const float* logits, int64_t rows, int C, const uint8_t* labels,
+                   double* auc_host, double* acc_host, float* scores_out) {
+    return guard([&] {
+        check_bank(k);
+        need(logits && labels, MTK_VALUE_ERROR, "attack_auc: null argument");
+        need(rows >= 1 && C >= 1, MTK_SHAPE_ERROR, "attack_auc: zero dimension");
+        need(k->G == 1 && k->n_heads == 1 && k->dims[k->L] >= 2, MTK_CONFIG_ERROR,
+             "attack_auc: one attack model (G = 1) with one head of >= 2 outputs");
+        const int kf = k->dims[0];
+        need(kf <= C, MTK_SHAPE_ERROR, "attack_auc: more features than classes");
+        Ctx& c = *k->ctx;
+        if (k->L == 2 && attack_fused_ok(C, kf, k->dims[1], k->dims[2])) {
+            attack_auc_fused(c, logits, rows, C, k->W[0].f, k->b[0], k->W[1].f, k->b[1], labels, scores_out,
+                             auc_host, acc_host);
+            c.check_flags();
+            return;
+        }
+        // any other attack-model shape: the four-call composition on the device
+        need(rows <= 0x7fffffffLL, MTK_SHAPE_ERROR, "attack_auc: too many rows");
+        const int O = k->dims[k->L];
+        auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+        const size_t fb = al((size_t)rows * kf * 4), ob = al((size_t)rows * O * 4), sb = al((size_t)rows * 4);
+        float* buf = nullptr;
+        MTK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf), fb + ob + sb, c.stream));
+        float* feats = buf;
+        float* out = reinterpret_cast<float*>(reinterpret_cast<char*>(buf) + fb);
+        float* sc = scores_out ? scores_out : reinterpret_cast<float*>(reinterpret_cast<char*>(buf) + fb + ob);
+        launch_features(logits, rows, C, kf, nullptr, feats, c.d_flags, c.stream);
+        const int e = mtk_bank_forward(k, feats, (int)rows, 0, out, nullptr);
+        if (e != MTK_OK) fail(e, last_error());
+        launch_column(out, rows, O, 1, sc, c.stream);
+        auc_device(c, sc, labels, rows, auc_host, acc_host);
+        MTK_CUDA(cudaFreeAsync(buf, c.stream));
+        c.check_flags();
+    });
+}
+
 int mtk_bank_train_step(mtk_bank* k, const mtk_step* s, double* loss_host, double* mmd_host) {
     return guard([&] {
         check_bank(k);

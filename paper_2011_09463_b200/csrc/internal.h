@@ -363,6 +363,11 @@ void launch_features(const float* logits, long long rows, int C, int k, const in
                      float* feats, int* flags, cudaStream_t s);
 void launch_column(const float* logits, long long rows, int C, int col, float* out,
                    cudaStream_t s);
+// fused attack scoring (k_attack.cu): the [3, 64, 2] attack model over <= 16 classes
+bool attack_fused_ok(int C, int K, int H, int O);
+void attack_auc_fused(Ctx& ctx, const float* logits, long long rows, int C, const float* W0, const float* b0,
+                      const float* W1, const float* b1, const uint8_t* labels, float* score_out, double* auc,
+                      double* acc);
 void auc_device(Ctx& ctx, const float* scores, const uint8_t* labels, long long n, double* auc,
                 double* acc);
 

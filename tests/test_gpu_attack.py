@@ -96,3 +96,34 @@ def test_gather_rows_matches_indexing(ctx):
     api.gather_rows(ctx, X, bad, out, row0=5)
     with pytest.raises(errors.ValueError):
         ctx.synchronize()
+
+
+@pytest.mark.parametrize("rows,C,dims,ties", [(65573, 10, [3, 64, 2], False), (4096, 10, [3, 64, 2], True),
+                                              (3001, 16, [3, 64, 2], False), (2000, 7, [4, 32, 2], False)])
+def test_attack_auc_in_one_call(ctx, rows, C, dims, ties):
+    """mtk_attack_auc (features -> attack model -> member probability -> AUC in
+    one call; the [3, 64, 2] model as one streaming kernel) must reproduce the
+    four-call composition bit for bit: scores, AUC and accuracy; other attack
+    shapes take the composition itself.  AUC and accuracy are also checked
+    against the oracle on the GPU scores."""
+    from paper_2011_09463_b200 import api
+
+    x = logits(rows, C, seed=rows)
+    if ties:
+        x = np.round(x)
+    r = po.Rng(rows + 1)
+    lab = np.array([r.below(2) for _ in range(rows)], dtype=np.uint8)
+    lab[0], lab[1] = 1, 0
+    xd, ld = torch.tensor(x, device="cuda"), torch.tensor(lab, device="cuda")
+    att = api.Bank(ctx, 1, dims)
+    att.init_params(0, api.Rng(5))
+    a1, acc1, s1 = api.attack_auc(att, xd, ld, scores=True)
+    F = api.posterior_features(ctx, xd, dims[0])
+    out = att.forward(F.reshape(1, rows, dims[0]))
+    s2 = api.posterior_column(ctx, out, 1)
+    a2, acc2 = api.auc(ctx, s2, ld)
+    assert torch.equal(s1, s2)
+    assert a1 == a2 and acc1 == acc2
+    sc = s1.cpu().numpy().astype(np.float64)
+    assert abs(a1 - po.auc(sc, lab)) <= 1e-12
+    assert abs(acc1 - po.accuracy(sc, lab, 0.5)) <= 1e-12
