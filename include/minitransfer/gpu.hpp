@@ -209,5 +209,14 @@ inline double auc(Context& ctx, const float* scores, const uint8_t* labels, int6
     return a;
 }
 
+// the attack evaluation in one call: device logits [rows, C] of the queried
+// models -> AUC (and accuracy at 0.5) of `attack` (model 0) as the scorer
+inline double attack_auc(Bank& attack, const float* logits, int64_t rows, int C, const uint8_t* labels,
+                         double* accuracy = nullptr, float* scores = nullptr) {
+    double a = 0.0;
+    check(mtk_attack_auc(attack.get(), logits, rows, C, labels, &a, accuracy, scores), "attack_auc");
+    return a;
+}
+
 }  // namespace gpu
 }  // namespace mt
