@@ -28,7 +28,7 @@ __device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpre
 // softmax-CE of their finished logits (ce_row.cuh, as ce_kernel).
 constexpr int FR = 64, FK = 64;
 template <int NP>
-__global__ void __launch_bounds__(128) head_fwd_kernel(HeadFwd p, CeArgs ce, int do_ce) {
+__global__ void __launch_bounds__(128, 5) head_fwd_kernel(HeadFwd p, CeArgs ce, int do_ce) {
     __shared__ float sA[FR][FK + 1];
     __shared__ __align__(16) float sW[FK][NP];
     __shared__ float red[FR][NP + 1];

@@ -620,10 +620,19 @@ __global__ void __launch_bounds__(256) mmd_prep_kernel(const float* Xs, long lon
         lo[i] = reinterpret_cast<float4*>(zlo + o);
         acc[i] = 0.0;
     }
-    for (int k = lane; k < d4; k += 32) {
-        float4 x[R];
+    // two k steps per trip: all 2R row loads in flight before any store
+    for (int k0 = lane; k0 < d4; k0 += 64) {
+        float4 xx[2][R];
 #pragma unroll
-        for (int i = 0; i < R; ++i) x[i] = ok[i] ? src[i][k] : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int i = 0; i < R; ++i)
+                xx[u][i] = (ok[i] && k0 + 32 * u < d4) ? src[i][k0 + 32 * u] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+        const int k = k0 + 32 * u;
+        if (k >= d4) break;
+        const float4 (&x)[R] = xx[u];
 #pragma unroll
         for (int i = 0; i < R; ++i) {
             if (!ok[i]) continue;
@@ -652,6 +661,7 @@ __global__ void __launch_bounds__(256) mmd_prep_kernel(const float* Xs, long lon
             cs[4 * k + 2] = c2;
             cs[4 * k + 3] = c3;
         }
+    }
     }
     double nacc = 0.0;
 #pragma unroll
