@@ -86,8 +86,10 @@ struct mtk_bank {
     double* loss_part = nullptr;  // [G][ceil(B/32)] CE loss partials
     double* mmd_part = nullptr;
     size_t mmd_part_bytes = 0;
-    float* head_scratch = nullptr;  // skinny dW partial sums
-    size_t head_scratch_bytes = 0;
+    // skinny dW partial sums: [0] for the main stream, [1] for the side stream
+    // (the head dW there can overlap a narrow-input layer's dW on the main stream)
+    float* head_scratch[2] = {nullptr, nullptr};
+    size_t head_scratch_bytes[2] = {0, 0};
     void* mmd_z = nullptr;     // tf32 planes + norms of the MMD sample (tc path)
     size_t mmd_z_bytes = 0;
     bool tc_mmd = true;
@@ -137,7 +139,8 @@ struct mtk_bank {
         cudaFree(beta);
         cudaFree(mmd_part);
         cudaFree(mmd_z);
-        cudaFree(head_scratch);
+        cudaFree(head_scratch[0]);
+        cudaFree(head_scratch[1]);
         cudaFree(Xs);
         cudaFree(ys);
         cudaFree(ws);
@@ -475,14 +478,15 @@ void gemm_dw(mtk_bank& k, int mat, const Plane3& in, const Plane3& dz, int B, in
         h.grad_out = k.keep_grads ? k.gW[mat] : nullptr;
         h.flags = c.d_flags;
         const size_t hb = head_dw_scratch_bytes(k.G, fi, fo);
-        if (hb > k.head_scratch_bytes) {
+        const int hs = st == c.stream ? 0 : 1;
+        if (hb > k.head_scratch_bytes[hs]) {
             MTK_CUDA(cudaStreamSynchronize(st));  // (the side stream's own prior work)
             MTK_CUDA(cudaStreamSynchronize(c.stream));
-            cudaFree(k.head_scratch);
-            MTK_CUDA(cudaMalloc(&k.head_scratch, hb));
-            k.head_scratch_bytes = hb;
+            cudaFree(k.head_scratch[hs]);
+            MTK_CUDA(cudaMalloc(&k.head_scratch[hs], hb));
+            k.head_scratch_bytes[hs] = hb;
         }
-        h.partial = k.head_scratch;
+        h.partial = k.head_scratch[hs];
         launch_head_dw(h, st);
     } else {
         Gemm g;
@@ -1067,6 +1071,42 @@ int mtk_bank_train_epoch(mtk_bank* k, const mtk_step* tmpl, const float* X_pool,
         k->ensure_stage(tmpl->B);
         Ctx& c = *k->ctx;
         const int B = tmpl->B, G = k->G;
+        // the attack model under SGD: every step of the epoch in one launch
+        const char* nse = getenv("MTK_NO_SMALL_EPOCH");  // A/B (read per call)
+        if (!(nse && nse[0] == '1') && k->L == 2 && k->n_heads == 1 &&
+            small2_epoch_ok(k->dims[0], k->dims[1], k->dims[2], B) && tmpl->optimizer == 0 &&
+            tmpl->frozen_layers == 0 && !(tmpl->mmd_lambda > 0.0) && !k->keep_grads && nsteps > 0) {
+            need(std::isfinite(tmpl->lr), MTK_VALUE_ERROR, "train_step: lr must be finite");
+            std::vector<double> den(nsteps);
+            for (int s = 0; s < nsteps; ++s) {
+                const double d = denom0 ? denom0[s] : tmpl->denom[0];
+                need(d >= 0 && !std::isnan(d), MTK_VALUE_ERROR, "cross_entropy: denominator must be positive");
+                den[s] = d > 0 ? d : (double)B;
+            }
+            double* dden = c.scratch((size_t)nsteps * sizeof(double));
+            MTK_CUDA(cudaMemcpyAsync(dden, den.data(), (size_t)nsteps * sizeof(double), cudaMemcpyHostToDevice,
+                                     c.stream));
+            SmallEpoch e;
+            e.G = G;
+            e.B = B;
+            e.nsteps = nsteps;
+            e.W0 = k->W[0].f;
+            e.b0 = k->b[0];
+            e.W1 = k->W[1].f;
+            e.b1 = k->b[1];
+            e.X = X_pool;
+            e.y = y_pool;
+            e.pool_rows = pool_rows;
+            e.idx = idx;
+            e.w = w;
+            e.denom = dden;
+            e.lr = (float)tmpl->lr;
+            e.flags = c.d_flags;
+            launch_small2_epoch(e, c.stream);
+            after_launch(c);
+            c.check_flags();  // also keeps the host denominators alive until the copy is done
+            return;
+        }
         for (int s = 0; s < nsteps; ++s) {
             const int64_t* ix = idx + (size_t)s * G * B;
             launch_gather_rows(reinterpret_cast<const uint32_t*>(X_pool), pool_rows, k->dims[0],

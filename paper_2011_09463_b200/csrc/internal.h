@@ -267,6 +267,21 @@ bool small2_forward_ok(int K, int H, int O);
 void launch_small2_forward(const float* X, int G, int rows, int K, int H, int O, const float* W0,
                            const float* b0, const float* W1, const float* b1, float* logits,
                            cudaStream_t s);
+// whole SGD epochs of the attack model (K=3 -> 64 -> 2, B <= 1024) in one launch
+struct SmallEpoch {
+    int G, B, nsteps;
+    float *W0, *b0, *W1, *b1;  // the bank's parameters (updated in place)
+    const float* X;            // pool [pool_rows][3]
+    const int32_t* y;          // pool labels
+    long long pool_rows;
+    const int64_t* idx;        // [nsteps][G][B]
+    const float* w;            // [nsteps][G][B] or null
+    const double* denom;       // [nsteps] device
+    float lr;
+    int* flags;
+};
+bool small2_epoch_ok(int K, int H, int O, int B);
+void launch_small2_epoch(const SmallEpoch& p, cudaStream_t s);
 bool head_dx_ok(int K, int N);
 void launch_head_dx(const HeadDx& p, cudaStream_t s);
 size_t head_dw_scratch_bytes(int G, int K, int N);

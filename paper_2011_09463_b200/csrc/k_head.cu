@@ -9,6 +9,7 @@
 // narrow operand (W row or dZ row) is read as broadcast float4.
 // Reductions run in a fixed order (bit-deterministic).
 #include <cmath>
+#include <utility>
 
 #include "internal.h"
 #include "ce_row.cuh"
@@ -420,6 +421,185 @@ void launch_small2_forward(const float* X, int G, int rows, int K, int H, int O,
     const size_t smem = (size_t)(K * H + H + H * O + O) * 4;
     small2_forward_kernel<<<dim3((rows + 256 * S2_R - 1) / (256 * S2_R), G), 256, smem, s>>>(
         X, rows, K, H, O, W0, b0, W1, b1, logits);
+    count_launch();
+}
+
+// ---- whole SGD epochs of the attack model (k -> 64 -> 2) in one launch: one
+// CTA per model keeps its 386 parameters in shared memory and runs every
+// step of the epoch -- gather, forward, softmax-CE, backward, update -- with
+// one thread per batch row (row sets of 256).  The per-step launch chain of the generic bank
+// step (about ten small kernels) is what bounds a model this small.
+// Arithmetic per row follows the generic kernels (small2_forward / ce_row /
+// head_dx); the gradient sums run in a fixed order: a butterfly over each
+// warp's 32 rows, then the warps in ascending order.
+constexpr int E_K = 3, E_H = 64, E_O = 2;
+constexpr int E_NP = E_K * E_H + E_H + E_H * E_O + E_O;  // 386 parameters
+constexpr int E_NG = (E_NP + 31) / 32;                    // 13 groups of 32 per butterfly
+constexpr int E_THREADS = 256;  // rows [rs * 256 + t] for row sets rs < ceil(B / 256)
+
+// value e of a row's gradient contribution (e is a compile-time index)
+template <int e>
+__device__ __forceinline__ float epoch_value(const float (&x)[E_K], const float (&hv)[E_H], const float (&dh)[E_H],
+                                             const float (&dlog)[E_O]) {
+    if constexpr (e < E_K * E_H) return x[e / E_H] * dh[e % E_H];
+    else if constexpr (e < E_K * E_H + E_H) return dh[e - E_K * E_H];
+    else if constexpr (e < E_K * E_H + E_H + E_H * E_O) return hv[(e - E_K * E_H - E_H) / E_O] * dlog[(e - E_K * E_H - E_H) % E_O];
+    else if constexpr (e < E_NP) return dlog[e - E_K * E_H - E_H - E_H * E_O];
+    else return 0.f;
+}
+template <int gi, int... c>
+__device__ __forceinline__ void epoch_group(float (&v)[32], const float (&x)[E_K], const float (&hv)[E_H],
+                                            const float (&dh)[E_H], const float (&dlog)[E_O],
+                                            std::integer_sequence<int, c...>) {
+    ((v[c] = epoch_value<gi * 32 + c>(x, hv, dh, dlog)), ...);
+}
+// the warp's 32 rows of gradient group gi -> lane l holds the sum of value gi * 32 + l
+template <int gi>
+__device__ __forceinline__ float epoch_reduce(int lane, const float (&x)[E_K], const float (&hv)[E_H],
+                                              const float (&dh)[E_H], const float (&dlog)[E_O]) {
+    float v[32];
+    epoch_group<gi>(v, x, hv, dh, dlog, std::make_integer_sequence<int, 32>{});
+#pragma unroll
+    for (int k = 16; k >= 1; k >>= 1) {
+        const bool up = (lane & k) != 0;
+#pragma unroll
+        for (int j = 0; j < k; ++j) {
+            const float send = up ? v[j] : v[j + k];
+            const float keep = up ? v[j + k] : v[j];
+            v[j] = keep + __shfl_xor_sync(0xffffffffu, send, k);
+        }
+    }
+    return v[0];
+}
+template <int... gi>
+__device__ __forceinline__ void epoch_reduce_all(float (&acc)[E_NG], int lane, const float (&x)[E_K],
+                                                 const float (&hv)[E_H], const float (&dh)[E_H],
+                                                 const float (&dlog)[E_O], std::integer_sequence<int, gi...>) {
+    ((acc[gi] += epoch_reduce<gi>(lane, x, hv, dh, dlog)), ...);
+}
+
+__global__ void __launch_bounds__(E_THREADS, 1) small2_epoch_kernel(SmallEpoch p) {
+    __shared__ float prm[E_NG * 32];                      // W0 [K][H], b0 [H], W1 [H][O], b1 [O]
+    __shared__ float part[E_THREADS / 32][E_NG * 32];     // warp partials
+    const int g = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    float* gW0 = p.W0 + (long long)g * E_K * E_H;
+    float* gb0 = p.b0 + (long long)g * E_H;
+    float* gW1 = p.W1 + (long long)g * E_H * E_O;
+    float* gb1 = p.b1 + (long long)g * E_O;
+    for (int e = t; e < E_NG * 32; e += E_THREADS) {
+        float v = 0.f;
+        if (e < E_K * E_H) v = gW0[e];
+        else if (e < E_K * E_H + E_H) v = gb0[e - E_K * E_H];
+        else if (e < E_K * E_H + E_H + E_H * E_O) v = gW1[e - E_K * E_H - E_H];
+        else if (e < E_NP) v = gb1[e - E_K * E_H - E_H - E_H * E_O];
+        prm[e] = v;
+    }
+    __syncthreads();
+    const float* W0 = prm;
+    const float* B0 = W0 + E_K * E_H;
+    const float* W1 = B0 + E_H;
+    const float* B1 = W1 + E_H * E_O;
+    const int nsets = (p.B + E_THREADS - 1) / E_THREADS;
+    bool bad = false;
+    for (int s = 0; s < p.nsteps; ++s) {
+        float acc[E_NG];
+#pragma unroll
+        for (int q = 0; q < E_NG; ++q) acc[q] = 0.f;
+        const float inv = (float)(1.0 / p.denom[s]);
+        for (int rs = 0; rs < nsets; ++rs) {
+            const int r = rs * E_THREADS + t;
+            float x[E_K], hv[E_H], dh[E_H], dlog[E_O];
+#pragma unroll
+            for (int k = 0; k < E_K; ++k) x[k] = 0.f;
+#pragma unroll
+            for (int h = 0; h < E_H; ++h) hv[h] = 0.f;
+#pragma unroll
+            for (int j = 0; j < E_O; ++j) dlog[j] = 0.f;
+            if (r < p.B) {
+                const long long q = ((long long)s * p.G + g) * p.B + r;
+                const long long row = p.idx[q];
+                if (row < 0 || row >= p.pool_rows) {
+                    atomicOr(p.flags, kFlagBadIndex);
+                } else {
+                    const int lab = p.y[row];
+#pragma unroll
+                    for (int k = 0; k < E_K; ++k) x[k] = p.X[row * E_K + k];
+                    // forward (small2_forward_kernel's order)
+#pragma unroll
+                    for (int h = 0; h < E_H; ++h) {
+                        float a = 0.f;
+#pragma unroll
+                        for (int k = 0; k < E_K; ++k) a = fmaf(x[k], W0[k * E_H + h], a);
+                        a = a + B0[h];
+                        hv[h] = a > 0.f ? a : 0.f;
+                    }
+                    float o[E_O];
+#pragma unroll
+                    for (int j = 0; j < E_O; ++j) o[j] = 0.f;
+#pragma unroll
+                    for (int h = 0; h < E_H; ++h)
+#pragma unroll
+                        for (int j = 0; j < E_O; ++j) o[j] = fmaf(hv[h], W1[h * E_O + j], o[j]);
+#pragma unroll
+                    for (int j = 0; j < E_O; ++j) o[j] = o[j] + B1[j];
+                    if (lab < 0 || lab >= E_O) {
+                        atomicOr(p.flags, kFlagBadLabel);
+                        for (int k = 0; k < E_K; ++k) x[k] = 0.f;
+                    } else {  // softmax-CE row (ce_row.cuh)
+                        float mx = o[0];
+#pragma unroll
+                        for (int j = 1; j < E_O; ++j) mx = fmaxf(mx, o[j]);
+                        float z = 0.f;
+#pragma unroll
+                        for (int j = 0; j < E_O; ++j) z += expf(o[j] - mx);
+                        const float lse = mx + logf(z);
+                        const float wi = (p.w ? p.w[q] : 1.f) * inv;
+#pragma unroll
+                        for (int j = 0; j < E_O; ++j)
+                            dlog[j] = wi * (expf(o[j] - lse) - (j == lab ? 1.f : 0.f));
+                    }
+                }
+            }
+            // backward through the ReLU (head_dx order: j ascending from 0)
+#pragma unroll
+            for (int h = 0; h < E_H; ++h) {
+                float a = 0.f;
+#pragma unroll
+                for (int j = 0; j < E_O; ++j) a = fmaf(dlog[j], W1[h * E_O + j], a);
+                dh[h] = hv[h] > 0.f ? a : 0.f;
+            }
+            epoch_reduce_all(acc, lane, x, hv, dh, dlog, std::make_integer_sequence<int, E_NG>{});
+        }
+#pragma unroll
+        for (int q = 0; q < E_NG; ++q) part[warp][q * 32 + lane] = acc[q];
+        __syncthreads();
+        // the warps in ascending order, then SGD (sgd_update, as every update site)
+        for (int e = t; e < E_NP; e += E_THREADS) {
+            float gsum = 0.f;
+#pragma unroll
+            for (int w2 = 0; w2 < E_THREADS / 32; ++w2) gsum += part[w2][e];
+            const float nv = sgd_update(prm[e], gsum, p.lr);
+            bad |= !isfinite(nv);
+            prm[e] = nv;
+        }
+        __syncthreads();
+    }
+    if (bad) atomicOr(p.flags, kFlagNonFinite);
+    for (int e = t; e < E_NP; e += E_THREADS) {
+        const float v = prm[e];
+        if (e < E_K * E_H) gW0[e] = v;
+        else if (e < E_K * E_H + E_H) gb0[e - E_K * E_H] = v;
+        else if (e < E_K * E_H + E_H + E_H * E_O) gW1[e - E_K * E_H - E_H] = v;
+        else gb1[e - E_K * E_H - E_H - E_H * E_O] = v;
+    }
+}
+
+bool small2_epoch_ok(int K, int H, int O, int B) { return K == E_K && H == E_H && O == E_O && B >= 1 && B <= 1024; }
+
+void launch_small2_epoch(const SmallEpoch& p, cudaStream_t s) {
+    if (!small2_epoch_ok(E_K, E_H, E_O, p.B)) fail(MTK_ERROR, "small2_epoch: unsupported shape");
+    if (p.nsteps <= 0 || p.G <= 0) return;
+    small2_epoch_kernel<<<p.G, E_THREADS, 0, s>>>(p);
     count_launch();
 }
 

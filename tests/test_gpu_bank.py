@@ -408,3 +408,47 @@ def test_async_host_pipeline_matches_sync(ctx):
         assert np.array_equal(l1, l2) and np.array_equal(m1, m2)
     for a, b in zip(b1.get_params(0)[0], b2.get_params(0)[0]):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("G,B,steps,weighted", [(1, 1024, 6, True), (2, 300, 5, False), (1, 77, 9, True)])
+def test_attack_model_epoch_in_one_launch(ctx, monkeypatch, G, B, steps, weighted):
+    """mtk_bank_train_epoch on the attack model (3 -> 64 -> 2, SGD) runs every
+    step of the epoch in one launch (small2_epoch_kernel: parameters in shared
+    memory, one thread per row).  Per row it follows the generic kernels;
+    the gradient sums run in another fixed order, so the epoch agrees with the
+    generic per-step path (MTK_NO_SMALL_EPOCH=1) to fp32 rounding, and it is
+    deterministic."""
+    from paper_2011_09463_b200 import api
+
+    dims = [3, 64, 2]
+    r = po.Rng(B + steps)
+    pool = 2000
+    X = r.normals(pool * 3).reshape(pool, 3).astype(np.float32)
+    y = np.array([r.below(2) for _ in range(pool)], dtype=np.int32)
+    idx = np.array([r.below(pool) for _ in range(steps * G * B)], dtype=np.int64).reshape(steps, G, B)
+    w = None
+    den = None
+    if weighted:
+        w = np.ones((steps, G, B), dtype=np.float32)
+        w[-1, :, B // 2:] = 0.0  # a padded last batch
+        den = w[:, 0, :].sum(axis=1).astype(np.float64)
+    Xd, yd, idd = torch.tensor(X, device="cuda"), torch.tensor(y, device="cuda"), torch.tensor(idx, device="cuda")
+    wd = None if w is None else torch.tensor(w, device="cuda")
+    res = []
+    for off in ("0", "0", "1", "1"):
+        monkeypatch.setenv("MTK_NO_SMALL_EPOCH", off)
+        bank = make_bank(ctx, G, dims, seed=3)
+        torch.cuda.synchronize()
+        n0 = ctx.launches
+        bank.train_epoch(Xd, yd, idd, wd, den, lr=0.1)
+        res.append(([bank.get_params(g) for g in range(G)], ctx.launches - n0))
+    (p0, n0), (p1, n1), (p2, n2), (p3, n3) = res
+    assert n0 == 1 and n2 > steps, (n0, n2)
+    for g in range(G):
+        for k in (0, 1):
+            for a, b, c, d in zip(p0[g][k], p1[g][k], p2[g][k], p3[g][k]):
+                assert np.array_equal(a, b)  # deterministic
+                # the generic path too: its side-stream head dW and the main
+                # stream's narrow-input dW have separate partial-sum scratch
+                assert np.array_equal(c, d)
+                assert rel(a, c) <= 1e-5, (g, k, rel(a, c))
