@@ -53,7 +53,7 @@ def peaks():
 
 
 class ClockSampler:
-    """SM clock + throttle reasons via NVML, polled every 5 ms in a thread, for
+    """SM clock + throttle reasons via NVML, polled every 1 ms in a thread, for
     the duration of the `with` block (the timed region)."""
 
     REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
@@ -81,7 +81,7 @@ class ClockSampler:
                              pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)))
                     except Exception:
                         pass
-                    time.sleep(0.005)
+                    time.sleep(0.001)
 
             self.t = threading.Thread(target=poll, daemon=True)
             self.t.start()
@@ -98,7 +98,7 @@ class ClockSampler:
         sm = [s for s, _ in self.samples]
         reasons = sorted({n for _, r in self.samples for n, bit in self.REASONS.items() if r & bit})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz,
-                "reasons": reasons, "samples": len(sm), "source": "nvml, 5 ms poll"}
+                "reasons": reasons, "samples": len(sm), "source": "nvml, 1 ms poll"}
 
 
 def dist_setup(n_gpus):
