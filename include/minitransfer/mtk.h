@@ -283,6 +283,26 @@ int mtk_auc(mtk_ctx* ctx, const float* scores, const uint8_t* labels, int64_t n,
 int mtk_attack_auc(mtk_bank* attack, const float* logits, int64_t rows, int C, const uint8_t* labels,
                    double* auc_host, double* acc_host, float* scores_out);
 
+/* ---- the path's one collective: shadow models shard
+ * across the GPUs of a box with no gradient exchange; after querying, the
+ * ranks' posterior features are all-gathered so every rank trains the attack
+ * model on all shadows.  NCCL (NVLink / NVSwitch) is loaded at run time
+ * (libnccl.so.2; an already-loaded copy, e.g. torch's, is reused).
+ * No reference counterpart: the reference is single-process. */
+typedef struct mtk_comm mtk_comm;
+/* a fresh NCCL unique id (128 bytes) on one rank; ship it to the others */
+int mtk_comm_unique_id(void* out128);
+/* collective over nranks processes (ncclCommInitRank), bound to the calling
+ * thread's current CUDA device; every rank calls it with the same id.       */
+int mtk_comm_init(int nranks, int rank, const void* nccl_id, mtk_comm** out);
+int mtk_comm_destroy(mtk_comm* comm);
+/* any pointer may be NULL; nccl_version as ncclGetVersion reports it        */
+int mtk_comm_info(mtk_comm* comm, int* nranks, int* rank, int* device, int* nccl_version);
+/* recv[r * bytes_per_rank ...] = rank r's `send` (device buffers), in rank
+ * order; stream-ordered on ctx's stream (asynchronous).  ctx and comm must
+ * be on the same device.                                                    */
+int mtk_allgather(mtk_comm* comm, mtk_ctx* ctx, const void* send, void* recv, size_t bytes_per_rank);
+
 /* ---- diagnostics (tests / profiling): C[g] = A[g] * B[g] through the
  * tcgen05 3xTF32 tensor-core GEMM used by the bank.  a_mn: A stored
  * [G][K][M] (1) or [G][M][K] (0); b_mn: B stored [G][K][N] (1) or [G][N][K]

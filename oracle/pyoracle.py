@@ -1,7 +1,7 @@
 """TEST INFRASTRUCTURE ONLY: numpy/ctypes front-end for the CPU oracle.
 
 Loads ``oracle/liboracle.so`` (the C restatement, oracle.c) and, when present,
-``oracle/_ref/libmtref.so`` (the shim over the UNMODIFIED reference headers,
+``oracle/_ref/libmtref_v{3,4}.so`` (the shim over the UNMODIFIED reference headers,
 ref_shim.cpp).  Only tests/, ``__graft_entry__.smoke()`` and bench.py's CPU
 legs import this module; the product package never does.
 """
@@ -15,7 +15,43 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 _ORC = os.path.join(HERE, "liboracle.so")
-_REF = os.path.join(HERE, "_ref", "libmtref.so")
+_REF_V = {v: os.path.join(HERE, "_ref", f"libmtref_{v}.so") for v in ("v3", "v4")}
+
+
+def host_isa() -> str:
+    """x86-64 micro-architecture level of this host: "v4" with AVX-512
+    (F/BW/CD/DQ/VL), else "v3" -- picks the libmtref build ("-march=native"
+    resolved on the box that runs it)."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            flags = next((ln.split(":", 1)[1].split() for ln in f if ln.startswith("flags")), [])
+    except OSError:
+        flags = []
+    return "v4" if {"avx512f", "avx512bw", "avx512cd", "avx512dq", "avx512vl"} <= set(flags) else "v3"
+
+
+def ref_path():
+    """the libmtref build for this host (None when never built)"""
+    for v in (host_isa(), "v3"):
+        if os.path.exists(_REF_V[v]):
+            return _REF_V[v]
+    return None
+
+
+def cpu_info() -> dict:
+    """CPU model / threads usable / ISA level, recorded beside CPU timings"""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            model = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), model)
+    except OSError:
+        pass
+    try:
+        threads = len(os.sched_getaffinity(0))
+    except Exception:  # noqa: BLE001
+        threads = os.cpu_count() or 1
+    return {"cpu_model": model, "nproc": os.cpu_count(), "threads_available": threads,
+            "isa": "x86-64-" + host_isa()}
 
 _dp = C.POINTER(C.c_double)
 _ip = C.POINTER(C.c_int)
@@ -52,7 +88,8 @@ def ref():
     """The reference-header shim, or None when it was never built here."""
     global _ref
     if _ref is None:
-        _ref = _load(_REF)
+        p = ref_path()
+        _ref = _load(p) if p else None
         if _ref is not None:
             _setup_ref(_ref)
     return _ref
@@ -122,6 +159,11 @@ def _setup_ref(L):
     L.ref_grad_check_mmd.restype = C.c_double
     L.ref_grad_check_mmd.argtypes = [C.c_int, C.c_int, _dp, C.c_int, _dp, C.c_int, _dp, _dp, _dp,
                                      C.c_int, C.c_double, C.c_double]
+    L.ref_bench_mmd.restype = C.c_double
+    L.ref_bench_mmd.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_int, C.c_int64, C.c_uint64, _dp, _dp]
+    L.ref_bench_attack.restype = C.c_double
+    L.ref_bench_attack.argtypes = [C.c_int, C.c_int64, C.c_int, C.c_uint64, _dp]
+    L.ref_build_info.restype = C.c_char_p
     L.ref_bench_train.restype = C.c_double
     L.ref_bench_train.argtypes = [C.c_int, C.c_int, _ip, C.c_int, C.c_int, C.c_int, C.c_double,
                                   C.c_uint64]

@@ -109,6 +109,11 @@ SIGNATURES = {
     "mtk_posterior_column": (C.c_int, [_vp, _vp, C.c_int64, C.c_int, C.c_int, _vp]),
     "mtk_auc": (C.c_int, [_vp, _vp, _vp, C.c_int64, _dp, _dp]),
     "mtk_attack_auc": (C.c_int, [_vp, _vp, C.c_int64, C.c_int, _vp, _dp, _dp, _vp]),
+    "mtk_comm_unique_id": (C.c_int, [_vp]),
+    "mtk_comm_init": (C.c_int, [C.c_int, C.c_int, _vp, C.POINTER(_vp)]),
+    "mtk_comm_destroy": (C.c_int, [_vp]),
+    "mtk_comm_info": (C.c_int, [_vp, _ip, _ip, _ip, _ip]),
+    "mtk_allgather": (C.c_int, [_vp, _vp, _vp, _vp, C.c_size_t]),
     "mtk_diag_gemm_tf32x3": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                        _vp, _vp, _vp]),
 }

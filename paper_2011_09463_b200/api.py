@@ -33,6 +33,30 @@ def _ptr(t):
     return C.c_void_p(int(t))
 
 
+def _need(t, name: str, dtype, shape=None, cuda=True, optional=False):
+    """Argument check before a C call: a wrong dtype / device / shape would
+    otherwise be read with the C side's element size and bounds (e.g. int32
+    indices read as int64 run past the buffer)."""
+    if t is None:
+        if optional:
+            return
+        raise errors.ValueError(f"{name}: required")
+    if not isinstance(t, torch.Tensor):
+        raise errors.ValueError(f"{name}: expected a torch.Tensor, got {type(t).__name__}")
+    if t.dtype != dtype:
+        raise errors.ValueError(f"{name}: expected {dtype}, got {t.dtype}")
+    if cuda and t.device.type != "cuda":
+        raise errors.ValueError(f"{name}: expected a CUDA tensor, got {t.device}")
+    if not cuda and t.device.type != "cpu":
+        raise errors.ValueError(f"{name}: expected a host tensor, got {t.device}")
+    if not t.is_contiguous():
+        raise errors.ShapeError(f"{name}: tensor must be contiguous")
+    if shape is not None:
+        if t.dim() != len(shape) or any(s is not None and a != s for a, s in zip(t.shape, shape)):
+            want = "[" + ", ".join("*" if s is None else str(s) for s in shape) + "]"
+            raise errors.ShapeError(f"{name}: expected shape {want}, got {list(t.shape)}")
+
+
 def _dvec(a):
     return (_dp * len(a))(*[x.ctypes.data_as(_dp) if x is not None else None for x in a])
 
@@ -237,6 +261,7 @@ class Bank:
         return out
 
     def forward(self, X: torch.Tensor, head: int = 0, hidden: bool = False):
+        _need(X, "forward: X", torch.float32, (self.G, None, self.dims[0]))
         B = X.shape[1]
         logits = torch.empty((self.G, B, self.dims[-1]), device=X.device, dtype=torch.float32)
         hid = (torch.empty((self.G, B, self.dims[-2]), device=X.device, dtype=torch.float32)
@@ -273,6 +298,7 @@ class Bank:
 
     def train_step(self, X, y, w=None, *, want_loss=True, **kw):
         """One SGD step of all G models; returns (loss[G], mmd[G]) or None."""
+        self._check_batch("train_step", X, y, w)
         B = X.shape[1]
         s = self.make_step(B, X=X, y=y, w=w, **kw)
         lp = self._loss.ctypes.data_as(_dp) if want_loss else None
@@ -280,8 +306,15 @@ class Bank:
         errors.check(lib.mtk_bank_train_step(self.h, C.byref(s), lp, mp), "train_step")
         return (self._loss.copy(), self._mmd.copy()) if want_loss else None
 
+    def _check_batch(self, what, X, y, w, cuda=True):
+        _need(X, f"{what}: X", torch.float32, (self.G, None, self.dims[0]), cuda=cuda)
+        B = X.shape[1]
+        _need(y, f"{what}: y", torch.int32, (self.G, B), cuda=cuda)
+        _need(w, f"{what}: w", torch.float32, (self.G, B), cuda=cuda, optional=True)
+
     def train_step_host(self, X_host, y_host, w_host=None, *, want_loss=True, **kw):
         """Same step from host (ideally pinned) buffers; copies inside the call."""
+        self._check_batch("train_step_host", X_host, y_host, w_host, cuda=False)
         B = X_host.shape[1]
         s = self.make_step(B, **kw)
         lp = self._loss.ctypes.data_as(_dp) if want_loss else None
@@ -299,6 +332,7 @@ class Bank:
     def train_step_host_async(self, X_host, y_host, w_host=None, **kw):
         """Enqueue a step from pinned host buffers (copy overlaps the previous
         step's compute); collect results with step_result()."""
+        self._check_batch("train_step_host_async", X_host, y_host, w_host, cuda=False)
         B = X_host.shape[1]
         s = self.make_step(B, **kw)
         errors.check(lib.mtk_bank_train_step_host_async(self.h, C.byref(s), _ptr(X_host),
@@ -315,9 +349,11 @@ class Bank:
         """idx.shape[0] steps, each gathering X_pool[idx[s]] / y_pool[idx[s]] on
         the device (idx int64 [steps, G, B]); w [steps, G, B] or None; denom0
         per-step head-0 denominators (host) or None (kw's denom)."""
+        _need(idx, "train_epoch: idx", torch.int64, (None, self.G, None))
         steps, G, B = idx.shape
-        if G != self.G:
-            raise errors.ShapeError(f"train_epoch: idx has {G} models, bank has {self.G}")
+        _need(X_pool, "train_epoch: X_pool", torch.float32, (None, self.dims[0]))
+        _need(y_pool, "train_epoch: y_pool", torch.int32, (X_pool.shape[0],))
+        _need(w, "train_epoch: w", torch.float32, (steps, G, B), optional=True)
         s = self.make_step(B, **kw)
         dn = None
         if denom0 is not None:
@@ -343,6 +379,7 @@ class Bank:
     def compute_grads(self, X, y, w=None, out: torch.Tensor = None, *, want_loss=True, **kw):
         """Forward + backward of this shard into a device gradient arena
         (parameters and optimizer state unchanged); returns (arena, loss, mmd)."""
+        self._check_batch("compute_grads", X, y, w)
         n = self.grad_size()
         if out is None:
             out = torch.empty(n, dtype=torch.float32, device=X.device)
@@ -444,13 +481,19 @@ def gather_rows(ctx: Context, src: torch.Tensor, idx: torch.Tensor, out: torch.T
     """out[g, row0 + r] = src[idx[g, r]] on the device (batch assembly).
     src [rows, d] (float32 or int32), idx int64 [G, nb]; out [G, out_rows, d]
     (allocated [G, nb, d] when None)."""
+    if not isinstance(src, torch.Tensor) or src.dtype not in (torch.float32, torch.int32):
+        raise errors.ValueError("gather_rows: src must be a float32 or int32 tensor")
+    _need(src, "gather_rows: src", src.dtype)
+    _need(idx, "gather_rows: idx", torch.int64, (None, None))
     src2 = src.reshape(src.shape[0], -1)
     G, nb = idx.shape
     d = src2.shape[1]
     if out is None:
         out = torch.empty((G, nb) + tuple(src.shape[1:]), device=src.device, dtype=src.dtype)
-    if src.element_size() != 4 or out.element_size() != 4:
-        raise errors.ShapeError("gather_rows: 4-byte elements only")
+    _need(out, "gather_rows: out", src.dtype)
+    if out.dim() < 2 or out.shape[0] != G or row0 < 0 or row0 + nb > out.shape[1] or \
+            out[0, 0].numel() != d:
+        raise errors.ShapeError(f"gather_rows: out must be [{G}, >= row0 + {nb}, {d}]")
     errors.check(lib.mtk_gather_rows(ctx.h, _ptr(src2), src2.shape[0], d, _ptr(idx), G, nb,
                                      _ptr(out), out.shape[1], row0), "gather_rows")
     return out
@@ -549,3 +592,59 @@ def diag_gemm_tf32x3(ctx: Context, A: torch.Tensor, B: torch.Tensor, a_mn: bool,
     errors.check(lib.mtk_diag_gemm_tf32x3(ctx.h, int(a_mn), int(b_mn), G, M, N, K, _ptr(A),
                                           _ptr(B), _ptr(C_)), "diag_gemm_tf32x3")
     return C_
+
+
+class Comm:
+    """NCCL communicator for the path's one collective, the feature all-gather
+    (mtk_comm_* / mtk_allgather).  The 128-byte NCCL id
+    is created on rank 0 and broadcast over the given torch.distributed group
+    (any backend); with no process group, a one-rank communicator."""
+
+    def __init__(self, ctx: Context, group=None):
+        import torch.distributed as dist
+
+        self.ctx = ctx
+        if dist.is_available() and dist.is_initialized():
+            self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        else:
+            self.rank, self.world = 0, 1
+        uid = (C.c_uint8 * 128)()
+        if self.rank == 0:
+            errors.check(lib.mtk_comm_unique_id(uid), "comm_unique_id")
+        if self.world > 1:
+            obj = [bytes(uid)]
+            dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group else 0,
+                                       group=group)
+            uid = (C.c_uint8 * 128).from_buffer_copy(obj[0])
+        torch.cuda.set_device(ctx.device)
+        h = C.c_void_p()
+        errors.check(lib.mtk_comm_init(self.world, self.rank, uid, C.byref(h)), "comm_init")
+        self.h = h
+
+    def nccl_version(self) -> int:
+        v = C.c_int()
+        errors.check(lib.mtk_comm_info(self.h, None, None, None, C.byref(v)), "comm_info")
+        return v.value
+
+    def all_gather(self, t: torch.Tensor, out: torch.Tensor = None) -> torch.Tensor:
+        """[world, *t.shape]: rank r's tensor at index r (stream-ordered on the ctx)."""
+        if t.device.type != "cuda" or not t.is_contiguous():
+            raise errors.ValueError("all_gather: a contiguous CUDA tensor is required")
+        if out is None:
+            out = torch.empty((self.world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+        if out.numel() != self.world * t.numel() or out.dtype != t.dtype or not out.is_contiguous():
+            raise errors.ShapeError("all_gather: out must hold world x the input")
+        errors.check(lib.mtk_allgather(self.h, self.ctx.h, _ptr(t), _ptr(out),
+                                       t.numel() * t.element_size()), "allgather")
+        return out
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib.mtk_comm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass

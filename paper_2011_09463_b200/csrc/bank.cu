@@ -19,6 +19,7 @@
 //   W[i]  [G, fan_in, fan_out];  b[i] [G, fan_out]
 //   H[l]  [G, B, dims[l]] post-ReLU activations (ReLU mask = H > 0)
 //   dZ    two ping-pong [G, B, max dim] gradient buffers
+#include <cerrno>
 #include <cmath>
 #include <functional>
 #include <cstdlib>
@@ -69,6 +70,7 @@ struct mtk_bank {
         return adam_g;
     }
     bool keep_grads = false;
+    bool no_update = false;  // compute_grads: store gradients, never write a parameter
     int capB = 0;
     std::vector<Plane3> H;    // H[l], l in [1, L)
     Plane3 dZ[2];
@@ -425,7 +427,8 @@ void gemm_dw(mtk_bank& k, int mat, const Plane3& in, const Plane3& dz, int B, in
         adam.v = k.vW[mat];
     }
     // Adam on the GEMM paths: the epilogue stores the gradient, adam_apply updates
-    const bool adam_gemm = adam.on && (k.tc[k.layer_of(mat)] || (!head_dw_ok(fo) && !head_dw_ok(fi)));
+    const bool adam_gemm = (adam.on || adam.store_only) &&
+                           (k.tc[k.layer_of(mat)] || (!head_dw_ok(fo) && !head_dw_ok(fi)));
     float* gbuf = nullptr;
     if (adam_gemm) {
         gbuf = k.keep_grads ? k.gW[mat] : k.adam_grad(mat);
@@ -452,7 +455,7 @@ void gemm_dw(mtk_bank& k, int mat, const Plane3& in, const Plane3& dz, int B, in
         u.grad_out = (!adam_gemm && k.keep_grads) ? k.gW[mat] : nullptr;
         u.flags = c.d_flags;
         launch_umma(u, st);
-        if (adam_gemm)
+        if (adam_gemm && !adam.store_only)
             launch_adam_apply(k.W[mat].f, gbuf, (long long)k.G * fi * fo, lr, adam, c.d_flags, st);
     } else if (head_dw_ok(fo) || head_dw_ok(fi)) {
         // narrow output (the heads): reduce over rows with the fo-wide dZ as the
@@ -510,7 +513,7 @@ void gemm_dw(mtk_bank& k, int mat, const Plane3& in, const Plane3& dz, int B, in
         g.grad_out = (!adam_gemm && k.keep_grads) ? k.gW[mat] : nullptr;
         g.flags = c.d_flags;
         launch_gemm(g, st);
-        if (adam_gemm)
+        if (adam_gemm && !adam.store_only)
             launch_adam_apply(k.W[mat].f, gbuf, (long long)k.G * fi * fo, lr, adam, c.d_flags, st);
     }
 }
@@ -591,6 +594,10 @@ void train_step(mtk_bank& k, const mtk_step& s, double* loss_host, double* mmd_h
         adam.eps = (float)eps;
         adam.bc1 = (float)(1.0 - std::pow(b1, (double)k.adam_t));
         adam.bc2 = (float)(1.0 - std::pow(b2, (double)k.adam_t));
+    }
+    if (k.no_update) {  // mtk_bank_compute_grads: gradients out, parameters untouched
+        adam = AdamArgs();
+        adam.store_only = 1;
     }
     auto bias_adam = [&](int mat) {
         AdamArgs a = adam;
@@ -868,7 +875,7 @@ extern "C" {
 
 int mtk_bank_create(mtk_ctx* c, int G, int n_layers, const int* dims, int n_heads,
                     mtk_bank** out) {
-    return guard([&] {
+    return guard_on(c, [&] {
         need(c && dims && out, MTK_VALUE_ERROR, "mtk_bank_create: null argument");
         need(G >= 1 && n_layers >= 1, MTK_SHAPE_ERROR, "mtk_bank_create: zero dimension");
         need(n_heads == 1 || n_heads == 2, MTK_CONFIG_ERROR, "mtk_bank_create: n_heads is 1 or 2");
@@ -876,7 +883,6 @@ int mtk_bank_create(mtk_ctx* c, int G, int n_layers, const int* dims, int n_head
              "mtk_bank_create: two heads need a shared trunk");
         for (int i = 0; i <= n_layers; ++i)
             need(dims[i] >= 1, MTK_SHAPE_ERROR, "mtk_bank_create: zero dimension in dims");
-        MTK_CUDA(cudaSetDevice(c->device));
         std::unique_ptr<mtk_bank> k(new mtk_bank());
         k->ctx = c;
         k->G = G;
@@ -909,7 +915,7 @@ int mtk_bank_create(mtk_ctx* c, int G, int n_layers, const int* dims, int n_head
 }
 
 int mtk_bank_destroy(mtk_bank* k) {
-    return guard([&] {
+    return guard_on(k ? k->ctx : nullptr, [&] {
         if (!k) return;
         cudaStreamSynchronize(k->ctx->stream);
         delete k;
@@ -917,7 +923,7 @@ int mtk_bank_destroy(mtk_bank* k) {
 }
 
 int mtk_bank_set_params(mtk_bank* k, int model, const double* const* W, const double* const* b) {
-    return guard([&] {
+    return guard_on(k ? k->ctx : nullptr, [&] {
         check_model(k, model);
         need(W && b, MTK_VALUE_ERROR, "set_params: null arrays");
         std::vector<float> tmp;
@@ -938,7 +944,7 @@ int mtk_bank_set_params(mtk_bank* k, int model, const double* const* W, const do
 }
 
 int mtk_bank_get_params(mtk_bank* k, int model, double* const* W, double* const* b) {
-    return guard([&] {
+    return guard_on(k ? k->ctx : nullptr, [&] {
         check_model(k, model);
         MTK_CUDA(cudaStreamSynchronize(k->ctx->stream));
         std::vector<float> tmp;
@@ -961,7 +967,7 @@ int mtk_bank_get_params(mtk_bank* k, int model, double* const* W, double* const*
 }
 
 int mtk_bank_init_params(mtk_bank* k, int model, mtk_rng* r) {
-    return guard([&] {
+    return guard_on(k ? k->ctx : nullptr, [&] {
         check_model(k, model);
         need(r != nullptr, MTK_VALUE_ERROR, "init_params: null rng");
         std::vector<std::vector<double>> W(k->n_mats), b(k->n_mats);
@@ -980,7 +986,7 @@ int mtk_bank_init_params(mtk_bank* k, int model, mtk_rng* r) {
 }
 
 int mtk_bank_param_device(mtk_bank* k, int mat, float** W, float** b) {
-    return guard([&] {
+    return guard_on(k ? k->ctx : nullptr, [&] {
         check_bank(k);
         need(mat >= 0 && mat < k->n_mats, MTK_VALUE_ERROR, "param_device: bad matrix index");
         if (W) *W = k->W[mat].f;
@@ -990,7 +996,7 @@ int mtk_bank_param_device(mtk_bank* k, int mat, float** W, float** b) {
 
 int mtk_bank_forward(mtk_bank* k, const float* X, int B, int head, float* logits,
                      float* hidden_last) {
-    return guard([&] {
+    return guard_on(k ? k->ctx : nullptr, [&] {
         check_bank(k);
         need(X && logits, MTK_VALUE_ERROR, "forward: null argument");
         need(B >= 1, MTK_SHAPE_ERROR, "forward: B must be >= 1");
@@ -1018,7 +1024,7 @@ int mtk_bank_forward(mtk_bank* k, const float* X, int B, int head, float* logits
 
 int mtk_attack_auc(mtk_bank* k, const float* logits, int64_t rows, int C, const uint8_t* labels,
                    double* auc_host, double* acc_host, float* scores_out) {
-    return guard([&] {
+    return guard_on(k ? k->ctx : nullptr, [&] {
         check_bank(k);
         need(logits && labels, MTK_VALUE_ERROR, "attack_auc: null argument");
         need(rows >= 1 && C >= 1, MTK_SHAPE_ERROR, "attack_auc: zero dimension");
@@ -1054,7 +1060,7 @@ int mtk_attack_auc(mtk_bank* k, const float* logits, int64_t rows, int C, const 
 }
 
 int mtk_bank_train_step(mtk_bank* k, const mtk_step* s, double* loss_host, double* mmd_host) {
-    return guard([&] {
+    return guard_on(k ? k->ctx : nullptr, [&] {
         check_bank(k);
         need(s != nullptr, MTK_VALUE_ERROR, "train_step: null step");
         train_step(*k, *s, loss_host, mmd_host);
@@ -1064,7 +1070,7 @@ int mtk_bank_train_step(mtk_bank* k, const mtk_step* s, double* loss_host, doubl
 int mtk_bank_train_epoch(mtk_bank* k, const mtk_step* tmpl, const float* X_pool, const int32_t* y_pool,
                          int64_t pool_rows, const int64_t* idx, const float* w, const double* denom0,
                          int nsteps) {
-    return guard([&] {
+    return guard_on(k ? k->ctx : nullptr, [&] {
         check_bank(k);
         need(tmpl && X_pool && y_pool && idx, MTK_VALUE_ERROR, "train_epoch: null argument");
         need(nsteps >= 0 && tmpl->B >= 1 && pool_rows >= 1, MTK_SHAPE_ERROR, "train_epoch: bad shape");
@@ -1130,7 +1136,7 @@ int mtk_bank_train_epoch(mtk_bank* k, const mtk_step* tmpl, const float* X_pool,
 int mtk_bank_train_step_host(mtk_bank* k, const mtk_step* s, const float* X_host,
                              const int32_t* y_host, const float* w_host, double* loss_host,
                              double* mmd_host) {
-    return guard([&] {
+    return guard_on(k ? k->ctx : nullptr, [&] {
         check_bank(k);
         need(s && X_host && y_host, MTK_VALUE_ERROR, "train_step_host: null argument");
         need(s->B >= 1, MTK_SHAPE_ERROR, "train_step_host: B must be >= 1");
@@ -1152,7 +1158,7 @@ int mtk_bank_train_step_host(mtk_bank* k, const mtk_step* s, const float* X_host
 
 int mtk_bank_train_step_host_async(mtk_bank* k, const mtk_step* s, const float* X_host,
                                    const int32_t* y_host, const float* w_host) {
-    return guard([&] {
+    return guard_on(k ? k->ctx : nullptr, [&] {
         check_bank(k);
         need(s && X_host && y_host, MTK_VALUE_ERROR, "train_step_host_async: null argument");
         need(s->B >= 1, MTK_SHAPE_ERROR, "train_step_host_async: B must be >= 1");
@@ -1188,7 +1194,7 @@ int mtk_bank_train_step_host_async(mtk_bank* k, const mtk_step* s, const float* 
 }
 
 int mtk_bank_step_result(mtk_bank* k, int which, double* loss_host, double* mmd_host) {
-    return guard([&] {
+    return guard_on(k ? k->ctx : nullptr, [&] {
         check_bank(k);
         need(k->last_slot >= 0, MTK_CONFIG_ERROR, "step_result: no asynchronous step enqueued");
         need(which == 0 || which == 1, MTK_VALUE_ERROR, "step_result: which is 0 (last) or 1");
@@ -1207,14 +1213,14 @@ int mtk_bank_step_result(mtk_bank* k, int which, double* loss_host, double* mmd_
 }
 
 int mtk_bank_reset_optimizer(mtk_bank* k) {
-    return guard([&] {
+    return guard_on(k ? k->ctx : nullptr, [&] {
         need(k != nullptr, MTK_VALUE_ERROR, "reset_optimizer: null bank");
         k->reset_adam();
     });
 }
 
 int mtk_bank_set_keep_grads(mtk_bank* k, int on) {
-    return guard([&] {
+    return guard_on(k ? k->ctx : nullptr, [&] {
         check_bank(k);
         k->keep_grads = on != 0;
         if (k->keep_grads && k->gW.empty()) {
@@ -1232,7 +1238,7 @@ int mtk_bank_set_keep_grads(mtk_bank* k, int on) {
 }
 
 int mtk_bank_get_grads(mtk_bank* k, int model, double* const* dW, double* const* db) {
-    return guard([&] {
+    return guard_on(k ? k->ctx : nullptr, [&] {
         check_model(k, model);
         need(!k->gW.empty(), MTK_CONFIG_ERROR, "get_grads: call mtk_bank_set_keep_grads first");
         MTK_CUDA(cudaStreamSynchronize(k->ctx->stream));
@@ -1312,7 +1318,7 @@ std::vector<DpSegments> segment_chunks(const std::vector<DpSegment>& v) {
 }  // namespace
 
 int mtk_bank_grad_size(mtk_bank* k, int64_t* n_floats) {
-    return guard([&] {
+    return guard_on(k ? k->ctx : nullptr, [&] {
         check_bank(k);
         need(n_floats != nullptr, MTK_VALUE_ERROR, "grad_size: null out");
         *n_floats = arena_floats(*k);
@@ -1321,16 +1327,16 @@ int mtk_bank_grad_size(mtk_bank* k, int64_t* n_floats) {
 
 int mtk_bank_compute_grads(mtk_bank* k, const mtk_step* s, float* grads, double* loss_host,
                            double* mmd_host) {
-    return guard([&] {
+    return guard_on(k ? k->ctx : nullptr, [&] {
         check_bank(k);
         need(s != nullptr && grads != nullptr, MTK_VALUE_ERROR, "compute_grads: null argument");
         need(((uintptr_t)grads & 127) == 0, MTK_VALUE_ERROR,
              "compute_grads: the gradient arena must be 128-byte aligned");
         need(s->frozen_layers >= 0 && s->frozen_layers <= k->L, MTK_CONFIG_ERROR,
              "train_step: frozen_layers out of range");
-        // the step's own forward/backward with lr = 0 under SGD: every update
-        // is w - 0*g = w (bit-identical parameters, no optimizer state
-        // touched) while the keep-grads outputs land in the caller's arena
+        // the step's own forward/backward in no-update mode: the epilogues
+        // store the gradients into the caller's arena and never write a
+        // parameter (so a non-finite gradient cannot corrupt the replica)
         const std::vector<DpSegment> segs = arena_segments(*k, s->frozen_layers, false);
         std::vector<float*> saved_w, saved_b;
         saved_w.swap(k->gW);
@@ -1341,6 +1347,7 @@ int mtk_bank_compute_grads(mtk_bank* k, const mtk_step* s, float* grads, double*
             k->gb.push_back(grads + segs[2 * i + 1].off);
         }
         k->keep_grads = true;
+        k->no_update = true;
         struct Restore {
             mtk_bank* k;
             std::vector<float*>& w;
@@ -1350,6 +1357,7 @@ int mtk_bank_compute_grads(mtk_bank* k, const mtk_step* s, float* grads, double*
                 k->gW.swap(w);
                 k->gb.swap(b);
                 k->keep_grads = keep;
+                k->no_update = false;
             }
         } restore{k, saved_w, saved_b, saved_keep};
         for (const DpSegment& sg : segs)  // frozen matrices report zero gradients
@@ -1364,7 +1372,7 @@ int mtk_bank_compute_grads(mtk_bank* k, const mtk_step* s, float* grads, double*
 
 int mtk_bank_dp_apply(mtk_bank* k, const mtk_step* s, const float* parts, int n_parts,
                       int64_t part_stride) {
-    return guard([&] {
+    return guard_on(k ? k->ctx : nullptr, [&] {
         check_bank(k);
         need(s != nullptr && parts != nullptr, MTK_VALUE_ERROR, "dp_apply: null argument");
         need(n_parts >= 1, MTK_CONFIG_ERROR, "dp_apply: n_workers must be >= 1");
@@ -1402,7 +1410,7 @@ int mtk_bank_dp_apply(mtk_bank* k, const mtk_step* s, const float* parts, int n_
 }
 
 int mtk_bank_fingerprint(mtk_bank* k, uint64_t* out_host) {
-    return guard([&] {
+    return guard_on(k ? k->ctx : nullptr, [&] {
         check_bank(k);
         need(out_host != nullptr, MTK_VALUE_ERROR, "fingerprint: null out");
         Ctx& c = *k->ctx;
@@ -1420,7 +1428,7 @@ int mtk_bank_fingerprint(mtk_bank* k, uint64_t* out_host) {
 }
 
 int mtk_bank_tc_layers(mtk_bank* k, int* out_host) {
-    return guard([&] {
+    return guard_on(k ? k->ctx : nullptr, [&] {
         check_bank(k);
         need(out_host != nullptr, MTK_VALUE_ERROR, "tc_layers: null out");
         for (int l = 0; l < k->L; ++l) out_host[l] = k->tc[l] ? 1 : 0;
@@ -1432,7 +1440,10 @@ int mtk_bank_tc_layers(mtk_bank* k, int* out_host) {
 // ---- checkpoint / resume ---------------------------------------------------
 namespace {
 
-constexpr int kCkptVersion = 1;
+// version 2: the SHA-256 covers the header's config lines (G, dims, heads,
+// Adam flag and step count) as well as the payload, so a corrupted step count
+// cannot silently change Adam's bias correction on resume
+constexpr int kCkptVersion = 2;
 const char kCkptMagic[] = "MTKBANK";
 
 std::string hex32(const uint8_t* d) {
@@ -1503,6 +1514,31 @@ struct Reader {
     }
 };
 
+// SHA-256 over the canonical header text (magic .. payload line, each line
+// '\n'-terminated) followed by the payload
+void digest_of(const std::string& hdr_core, const std::string& pay, uint8_t out[32]) {
+    std::string all;
+    all.reserve(hdr_core.size() + pay.size());
+    all += hdr_core;
+    all += pay;
+    sha256(all.data(), all.size(), out);
+}
+
+// strict decimal integer in [lo, hi]: the whole word, no sign tricks, no overflow
+long long parse_int(const std::string& w, long long lo, long long hi, const char* what) {
+    bool ok = !w.empty() && w.size() <= 19;
+    for (char ch : w) ok = ok && ch >= '0' && ch <= '9';
+    long long v = 0;
+    if (ok) {
+        errno = 0;
+        char* end = nullptr;
+        v = std::strtoll(w.c_str(), &end, 10);
+        ok = errno == 0 && end && *end == '\0' && v >= lo && v <= hi;
+    }
+    need(ok, MTK_CHECKPOINT_ERROR, std::string("checkpoint: malformed ") + what + " '" + w + "'");
+    return v;
+}
+
 std::vector<float> d2h(const float* d, size_t n, cudaStream_t s) {
     std::vector<float> h(n);
     MTK_CUDA(cudaMemcpyAsync(h.data(), d, n * 4, cudaMemcpyDeviceToHost, s));
@@ -1513,7 +1549,7 @@ std::vector<float> d2h(const float* d, size_t n, cudaStream_t s) {
 }  // namespace
 
 int mtk_bank_save(mtk_bank* k, const char* path) {
-    return guard([&] {
+    return guard_on(k ? k->ctx : nullptr, [&] {
         check_bank(k);
         need(path != nullptr, MTK_VALUE_ERROR, "save: null path");
         Ctx& c = *k->ctx;
@@ -1532,8 +1568,6 @@ int mtk_bank_save(mtk_bank* k, const char* path) {
                 put_tensor(pay, "vb" + n, {G, fo}, d2h(k->vb[i], G * fo, c.stream));
             }
         }
-        uint8_t dg[32];
-        sha256(pay.data(), pay.size(), dg);
         std::string hdr = std::string(kCkptMagic) + " " + std::to_string(kCkptVersion) + "\n";
         hdr += "G " + std::to_string(k->G) + "\n";
         hdr += "dims";
@@ -1541,6 +1575,8 @@ int mtk_bank_save(mtk_bank* k, const char* path) {
         hdr += "\nheads " + std::to_string(k->n_heads) + "\n";
         hdr += "adam " + std::to_string(adam ? 1 : 0) + " " + std::to_string(k->adam_t) + "\n";
         hdr += "payload " + std::to_string(pay.size()) + "\n";
+        uint8_t dg[32];
+        digest_of(hdr, pay, dg);  // the header lines so far + the payload
         hdr += "sha256 " + hex32(dg) + "\n\n";
         FILE* f = std::fopen(path, "wb");
         need(f != nullptr, MTK_DATA_ERROR, std::string("save: cannot open ") + path);
@@ -1552,7 +1588,7 @@ int mtk_bank_save(mtk_bank* k, const char* path) {
 }
 
 int mtk_bank_load(mtk_ctx* c, const char* path, mtk_bank** out) {
-    return guard([&] {
+    return guard_on(c, [&] {
         need(c && path && out, MTK_VALUE_ERROR, "load: null argument");
         *out = nullptr;
         FILE* f = std::fopen(path, "rb");
@@ -1584,37 +1620,41 @@ int mtk_bank_load(mtk_ctx* c, const char* path, mtk_bank** out) {
         need(!lines.empty(), MTK_CHECKPOINT_ERROR, "checkpoint: empty header");
         auto l0 = words(lines[0]);
         need(l0.size() == 2 && l0[0] == kCkptMagic, MTK_CHECKPOINT_ERROR, "checkpoint: not a bank checkpoint");
-        const int ver = std::atoi(l0[1].c_str());
+        const long long ver = parse_int(l0[1], 0, 1LL << 30, "format_version");
         need(ver == kCkptVersion, MTK_VERSION_ERROR,
              "checkpoint: format_version " + l0[1] + " in file, this library reads version " +
                  std::to_string(kCkptVersion));
-        int G = 0, heads = 0, adam = 0;
-        unsigned long long adam_t = 0, paybytes = 0;
-        std::vector<int> dims;
-        std::string digest;
-        for (size_t i = 1; i < lines.size(); ++i) {
-            auto w = words(lines[i]);
-            if (w.empty()) continue;
-            if (w[0] == "G" && w.size() == 2) G = std::atoi(w[1].c_str());
-            else if (w[0] == "dims")
-                for (size_t j = 1; j < w.size(); ++j) dims.push_back(std::atoi(w[j].c_str()));
-            else if (w[0] == "heads" && w.size() == 2) heads = std::atoi(w[1].c_str());
-            else if (w[0] == "adam" && w.size() == 3) {
-                adam = std::atoi(w[1].c_str());
-                adam_t = std::strtoull(w[2].c_str(), nullptr, 10);
-            } else if (w[0] == "payload" && w.size() == 2) paybytes = std::strtoull(w[1].c_str(), nullptr, 10);
-            else if (w[0] == "sha256" && w.size() == 2) digest = w[1];
+        // exactly: magic, G, dims, heads, adam, payload, sha256 -- in that order
+        const char* keys[] = {"G", "dims", "heads", "adam", "payload", "sha256"};
+        need(lines.size() == 7, MTK_CHECKPOINT_ERROR, "checkpoint: malformed header (line count)");
+        std::vector<std::vector<std::string>> hw;
+        for (size_t i = 1; i < 7; ++i) {
+            hw.push_back(words(lines[i]));
+            need(!hw.back().empty() && hw.back()[0] == keys[i - 1], MTK_CHECKPOINT_ERROR,
+                 std::string("checkpoint: malformed header (expected '") + keys[i - 1] + "')");
         }
-        need(G >= 1 && dims.size() >= 2 && (heads == 1 || heads == 2) && digest.size() == 64,
-             MTK_CHECKPOINT_ERROR, "checkpoint: malformed header");
+        need(hw[0].size() == 2 && hw[1].size() >= 3 && hw[2].size() == 2 && hw[3].size() == 3 &&
+                 hw[4].size() == 2 && hw[5].size() == 2 && hw[5][1].size() == 64,
+             MTK_CHECKPOINT_ERROR, "checkpoint: malformed header (field count)");
+        const int G = (int)parse_int(hw[0][1], 1, 1 << 20, "G");
+        std::vector<int> dims;
+        for (size_t j = 1; j < hw[1].size(); ++j) dims.push_back((int)parse_int(hw[1][j], 1, 1 << 24, "dims"));
+        const int heads = (int)parse_int(hw[2][1], 1, 2, "heads");
+        const int adam = (int)parse_int(hw[3][1], 0, 1, "adam flag");
+        const unsigned long long adam_t = (unsigned long long)parse_int(hw[3][2], 0, 1LL << 62, "adam step");
+        const unsigned long long paybytes = (unsigned long long)parse_int(hw[4][1], 0, 1LL << 62, "payload size");
+        const std::string digest = hw[5][1];
+        const size_t sha_at = all.rfind("\nsha256 ", he);
+        need(sha_at != std::string::npos, MTK_CHECKPOINT_ERROR, "checkpoint: malformed header (sha256)");
+        const std::string hdr_core = all.substr(0, sha_at + 1);
         const std::string pay = all.substr(he + 2);
         need(pay.size() >= paybytes, MTK_TRUNCATED_ERROR,
              "checkpoint: truncated payload (" + std::to_string(pay.size()) + " of " +
                  std::to_string(paybytes) + " bytes)");
         need(pay.size() == paybytes, MTK_CHECKPOINT_ERROR, "checkpoint: trailing bytes after the payload");
         uint8_t dg[32];
-        sha256(pay.data(), pay.size(), dg);
-        need(hex32(dg) == digest, MTK_DIGEST_ERROR, "checkpoint: payload SHA-256 mismatch");
+        digest_of(hdr_core, pay, dg);
+        need(hex32(dg) == digest, MTK_DIGEST_ERROR, "checkpoint: header/payload SHA-256 mismatch");
         mtk_bank* k = nullptr;
         const int st = mtk_bank_create(c, G, (int)dims.size() - 1, dims.data(), heads, &k);
         if (st != MTK_OK) fail(st, mtk_last_error());
@@ -1652,7 +1692,7 @@ int mtk_bank_load(mtk_ctx* c, const char* path, mtk_bank** out) {
 }
 
 int mtk_bank_info(mtk_bank* k, int* G, int* n_layers, int* dims_out, int* n_heads) {
-    return guard([&] {
+    return guard_on(k ? k->ctx : nullptr, [&] {
         check_bank(k);
         if (G) *G = k->G;
         if (n_layers) *n_layers = k->L;

@@ -5,6 +5,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -18,6 +20,48 @@ std::string& last_error() {
 unsigned long long& launch_counter() {
     static unsigned long long n = 0;
     return n;
+}
+
+namespace {
+constexpr int kMaxDevices = 64;
+std::mutex g_dev_mu;
+int g_sms[kMaxDevices] = {};
+std::set<std::pair<int, const void*>> g_smem_attr;  // (device, kernel) already raised
+}  // namespace
+
+int current_device() {
+    int dev = 0;
+    MTK_CUDA(cudaGetDevice(&dev));
+    return dev;
+}
+
+int device_sm_count(int device) {
+    need(device >= 0 && device < kMaxDevices, MTK_ERROR, "device index out of range");
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    if (!g_sms[device]) MTK_CUDA(cudaDeviceGetAttribute(&g_sms[device], cudaDevAttrMultiProcessorCount, device));
+    return g_sms[device];
+}
+
+void ensure_smem_attr(const void* func, int bytes) {
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    if (g_smem_attr.count({dev, func})) return;
+    MTK_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    g_smem_attr.insert({dev, func});
+}
+
+DeviceScope::DeviceScope(int device) {
+    if (device < 0) return;
+    int cur = -1;
+    MTK_CUDA(cudaGetDevice(&cur));
+    if (cur != device) {
+        MTK_CUDA(cudaSetDevice(device));
+        prev = cur;
+    }
+}
+
+DeviceScope::~DeviceScope() {
+    if (prev >= 0) cudaSetDevice(prev);
 }
 }  // namespace mtk
 
@@ -151,7 +195,7 @@ int mtk_ctx_create(int device, void* stream, mtk_ctx** out) {
         int n = 0;
         MTK_CUDA(cudaGetDeviceCount(&n));
         need(device >= 0 && device < n, MTK_VALUE_ERROR, "mtk_ctx_create: no such device");
-        MTK_CUDA(cudaSetDevice(device));
+        DeviceScope ds(device);
         std::unique_ptr<mtk_ctx> c(new mtk_ctx());
         c->device = device;
         // the context runs on exactly the stream it is given; NULL is the
@@ -165,7 +209,7 @@ int mtk_ctx_create(int device, void* stream, mtk_ctx** out) {
 }
 
 int mtk_ctx_destroy(mtk_ctx* c) {
-    return guard([&] {
+    return guard_on(c, [&] {
         if (!c) return;
         cudaStreamSynchronize(c->stream);
         cudaFree(c->d_flags);
@@ -185,21 +229,21 @@ int mtk_ctx_destroy(mtk_ctx* c) {
 }
 
 int mtk_ctx_synchronize(mtk_ctx* c) {
-    return guard([&] {
+    return guard_on(c, [&] {
         need(c != nullptr, MTK_VALUE_ERROR, "null ctx");
         c->check_flags();
     });
 }
 
 int mtk_ctx_launch_count(mtk_ctx* c, uint64_t* out) {
-    return guard([&] {
+    return guard_on(c, [&] {
         need(c && out, MTK_VALUE_ERROR, "null argument");
         *out = __atomic_load_n(&launch_counter(), __ATOMIC_RELAXED);
     });
 }
 
 int mtk_ctx_set_timing(mtk_ctx* c, int on) {
-    return guard([&] {
+    return guard_on(c, [&] {
         need(c != nullptr, MTK_VALUE_ERROR, "null ctx");
         c->collect_phases();
         c->timing = on != 0;
@@ -207,7 +251,7 @@ int mtk_ctx_set_timing(mtk_ctx* c, int on) {
 }
 
 int mtk_ctx_phase_times(mtk_ctx* c, double* ms_host, uint64_t* launches_host) {
-    return guard([&] {
+    return guard_on(c, [&] {
         need(c != nullptr, MTK_VALUE_ERROR, "null ctx");
         c->collect_phases();
         for (int i = 0; i < kNumPhases; ++i) {
@@ -252,7 +296,7 @@ static MmdArgs mmd_args(mtk_ctx* c, const float* Xs, int64_t m, const float* Xt,
 
 int mtk_mmd_beta(mtk_ctx* c, const float* Xs, int64_t m, const float* Xt, int64_t n, int d,
                  double* beta_host) {
-    return guard([&] {
+    return guard_on(c, [&] {
         MmdArgs a = mmd_args(c, Xs, m, Xt, n, d, nullptr, 0);
         const size_t part = mmd_beta_scratch_bytes(a);
         double* sc = c->scratch(part + 64);
@@ -310,7 +354,7 @@ static void mmd_run(mtk_ctx* c, MmdArgs& a, double beta, bool want_value, double
 int mtk_mmd_gaussian(mtk_ctx* c, const float* Xs, int64_t m, const float* Xt, int64_t n, int d,
                      const double* mult, int nb, double beta, double* value_host,
                      double* beta_host, float* gXs, float* gXt) {
-    return guard([&] {
+    return guard_on(c, [&] {
         MmdArgs a = mmd_args(c, Xs, m, Xt, n, d, mult, nb);
         need(value_host != nullptr, MTK_VALUE_ERROR, "mmd: null value");
         a.gXs = gXs;
@@ -322,7 +366,7 @@ int mtk_mmd_gaussian(mtk_ctx* c, const float* Xs, int64_t m, const float* Xt, in
 int mtk_mmd_gaussian_rows(mtk_ctx* c, const float* Xs, int64_t m, const float* Xt, int64_t n,
                           int d, const double* mult, int nb, double beta, int64_t row_begin,
                           int64_t row_end, double* partial_host, float* gXs, float* gXt) {
-    return guard([&] {
+    return guard_on(c, [&] {
         MmdArgs a = mmd_args(c, Xs, m, Xt, n, d, mult, nb);
         need(beta > 0, MTK_VALUE_ERROR, "mmd_rows: beta must be given (> 0)");
         need(partial_host != nullptr, MTK_VALUE_ERROR, "mmd_rows: null partial");
@@ -343,7 +387,7 @@ int mtk_mmd_gaussian_rows(mtk_ctx* c, const float* Xs, int64_t m, const float* X
 // ---- attack stage ----------------------------------------------------------
 int mtk_gather_rows(mtk_ctx* c, const void* src, int64_t src_rows, int d, const int64_t* idx, int G,
                     int nb, void* out, int out_rows, int row0) {
-    return guard([&] {
+    return guard_on(c, [&] {
         need(c && src && idx && out, MTK_VALUE_ERROR, "gather_rows: null argument");
         need(d >= 1 && G >= 0 && nb >= 0 && src_rows >= 1, MTK_SHAPE_ERROR, "gather_rows: bad shape");
         need(row0 >= 0 && row0 + nb <= out_rows, MTK_SHAPE_ERROR, "gather_rows: rows exceed out_rows");
@@ -356,7 +400,7 @@ int mtk_gather_rows(mtk_ctx* c, const void* src, int64_t src_rows, int d, const 
 
 int mtk_philox4x64_fill(mtk_ctx* c, uint64_t seed, uint64_t stream, uint64_t ctr0, uint64_t ctr1,
                         int64_t nblocks, uint64_t* out) {
-    return guard([&] {
+    return guard_on(c, [&] {
         need(c && (out || nblocks == 0), MTK_VALUE_ERROR, "philox: null argument");
         need(nblocks >= 0, MTK_SHAPE_ERROR, "philox: negative block count");
         launch_philox_fill(seed, stream, ctr0, ctr1, nblocks, out, c->stream);
@@ -366,7 +410,7 @@ int mtk_philox4x64_fill(mtk_ctx* c, uint64_t seed, uint64_t stream, uint64_t ctr
 
 int mtk_counter_normals(mtk_ctx* c, uint64_t seed, uint64_t stream, int64_t first, int64_t count,
                         float* out) {
-    return guard([&] {
+    return guard_on(c, [&] {
         need(c && (out || count == 0), MTK_VALUE_ERROR, "counter_normals: null argument");
         need(first >= 0 && count >= 0, MTK_SHAPE_ERROR, "counter_normals: negative range");
         launch_counter_normals(seed, stream, first, count, out, c->stream);
@@ -376,7 +420,7 @@ int mtk_counter_normals(mtk_ctx* c, uint64_t seed, uint64_t stream, int64_t firs
 
 int mtk_synth_counter(mtk_ctx* c, uint64_t seed, uint64_t stream, int C, int d, int64_t n,
                       const float* mu, const float* shift, float* X, int32_t* y) {
-    return guard([&] {
+    return guard_on(c, [&] {
         need(c && mu && X && y, MTK_VALUE_ERROR, "synth_counter: null argument");
         need(C >= 1 && d >= 1 && n >= 1, MTK_SHAPE_ERROR, "synth_counter: zero dimension");
         launch_synth_counter(seed, stream, C, d, n, mu, shift, X, y, c->stream);
@@ -385,7 +429,7 @@ int mtk_synth_counter(mtk_ctx* c, uint64_t seed, uint64_t stream, int C, int d, 
 }
 
 int mtk_softmax(mtk_ctx* c, const float* logits, int64_t rows, int C, float* probs) {
-    return guard([&] {
+    return guard_on(c, [&] {
         need(c && logits && probs, MTK_VALUE_ERROR, "softmax: null argument");
         need(rows >= 1 && C >= 1, MTK_SHAPE_ERROR, "softmax: zero dimension");
         launch_softmax(logits, rows, C, probs, c->stream);
@@ -395,7 +439,7 @@ int mtk_softmax(mtk_ctx* c, const float* logits, int64_t rows, int C, float* pro
 
 int mtk_posterior_features(mtk_ctx* c, const float* logits, int64_t rows, int C, int k,
                            const int32_t* labels, float* feats) {
-    return guard([&] {
+    return guard_on(c, [&] {
         need(c && logits && feats, MTK_VALUE_ERROR, "features: null argument");
         need(rows >= 1 && C >= 1, MTK_SHAPE_ERROR, "features: zero dimension");
         need(k >= 1 && k <= C, MTK_VALUE_ERROR, "features: k must be in [1, C]");
@@ -406,7 +450,7 @@ int mtk_posterior_features(mtk_ctx* c, const float* logits, int64_t rows, int C,
 
 int mtk_posterior_column(mtk_ctx* c, const float* logits, int64_t rows, int C, int col,
                          float* out) {
-    return guard([&] {
+    return guard_on(c, [&] {
         need(c && logits && out, MTK_VALUE_ERROR, "posterior_column: null argument");
         need(rows >= 1 && C >= 1, MTK_SHAPE_ERROR, "posterior_column: zero dimension");
         need(col >= 0 && col < C, MTK_VALUE_ERROR, "posterior_column: column out of range");
@@ -417,7 +461,7 @@ int mtk_posterior_column(mtk_ctx* c, const float* logits, int64_t rows, int C, i
 
 int mtk_auc(mtk_ctx* c, const float* scores, const uint8_t* labels, int64_t n, double* auc_host,
             double* acc_host) {
-    return guard([&] {
+    return guard_on(c, [&] {
         need(c && scores && labels, MTK_VALUE_ERROR, "auc: null argument");
         need(n >= 1, MTK_SHAPE_ERROR, "auc: zero rows");
         auc_device(*c, scores, labels, n, auc_host, acc_host);
@@ -427,7 +471,7 @@ int mtk_auc(mtk_ctx* c, const float* scores, const uint8_t* labels, int64_t n, d
 
 int mtk_diag_gemm_tf32x3(mtk_ctx* c, int a_mn, int b_mn, int G, int M, int N, int K,
                          const float* A, const float* B, float* Cm) {
-    return guard([&] {
+    return guard_on(c, [&] {
         need(c && A && B && Cm, MTK_VALUE_ERROR, "diag_gemm: null argument");
         need(G >= 1 && M >= 1 && N >= 1 && K >= 1, MTK_SHAPE_ERROR, "diag_gemm: zero dimension");
         UmmaGemm u;

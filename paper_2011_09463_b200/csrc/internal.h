@@ -94,6 +94,10 @@ struct PhaseScope {
 // bc2 = 1 - b2^t (fp32 here, f64 in the reference).
 struct AdamArgs {
     int on = 0;
+    // no parameter update at all (mtk_bank_compute_grads): the epilogues store
+    // the gradient only and every update site leaves w untouched, so a
+    // non-finite gradient cannot reach the parameters
+    int store_only = 0;
     float b1 = 0.9f, b2 = 0.999f, eps = 1e-8f, bc1 = 1.f, bc2 = 1.f;
     float* m = nullptr;
     float* v = nullptr;
@@ -109,6 +113,7 @@ struct AdamArgs {
 __device__ __forceinline__ float sgd_update(float w, float g, float lr) { return __fmaf_rn(-lr, g, w); }
 __device__ __forceinline__ float param_update(float w, float g, float lr, const AdamArgs& a,
                                               long long idx) {
+    if (a.store_only) return w;
     if (!a.on) return sgd_update(w, g, lr);
     const float m = a.b1 * a.m[idx] + (1.f - a.b1) * g;
     const float v = a.b2 * a.v[idx] + (1.f - a.b2) * g * g;
@@ -414,6 +419,38 @@ inline int guard(F&& f) {
         last_error() = e.what();
         return MTK_ERROR;
     }
+}
+
+// Per-DEVICE launch state.  cudaFuncSetAttribute(MaxDynamicSharedMemorySize)
+// is per device context and the SM count is per device, so neither may be a
+// process-wide static: one process may drive several devices from several
+// host threads (one ctx per (host thread, device), mtk.h).  Both are cached
+// per device under a mutex.
+int current_device();
+int device_sm_count(int device);
+// raise `func`'s dynamic shared-memory limit to `bytes` on the current device
+// (once per (device, func))
+void ensure_smem_attr(const void* func, int bytes);
+
+// Makes `device` current for the duration of one C-ABI call and restores the
+// caller's device afterwards, so a ctx-bound entry point always launches on
+// its ctx's device whatever the calling thread last selected.
+struct DeviceScope {
+    int prev = -1;
+    explicit DeviceScope(int device);
+    ~DeviceScope();
+    DeviceScope(const DeviceScope&) = delete;
+    DeviceScope& operator=(const DeviceScope&) = delete;
+};
+
+// guard() for entry points bound to a context: the ctx's device is current
+// inside f (c may be null; f then reports the null argument itself).
+template <class F>
+inline int guard_on(const Ctx* c, F&& f) {
+    return guard([&] {
+        DeviceScope ds(c ? c->device : -1);
+        f();
+    });
 }
 
 inline void need(bool ok, int status, const char* msg) {

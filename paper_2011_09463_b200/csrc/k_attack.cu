@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <mutex>
 
 #include "internal.h"
 
@@ -410,8 +411,7 @@ AucWork auc_work(Ctx& ctx, long long n) {
 void auc_finish(Ctx& ctx, AucWork& w, const uint8_t* labels, long long n, double* auc, double* acc) {
     cudaStream_t s = ctx.stream;
     MTK_CUDA(cub::DeviceRadixSort::SortKeys(w.tmp, w.tmp_bytes, w.kn, w.kn_sorted, (int)n, 0, 32, s));
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx.device);
+    const int sms = device_sm_count(ctx.device);
     const long long want = (n + AUC_THREADS - 1) / AUC_THREADS;
     auc_member_count<<<(unsigned)std::min<long long>(want, 3LL * sms), AUC_THREADS, 0, s>>>(w.kn_sorted, w.kp,
                                                                                           labels, n, w.cnt);
@@ -435,6 +435,18 @@ void auc_device(Ctx& ctx, const float* scores, const uint8_t* labels, long long 
     auc_finish(ctx, w, labels, n, auc, acc);
 }
 
+namespace {
+std::mutex& att_mutex() {
+    static std::mutex m;
+    return m;
+}
+cudaEvent_t& att_last_use(int device) {
+    static cudaEvent_t ev[64] = {};
+    if (device < 0 || device >= 64) fail(MTK_ERROR, "attack_auc: device index out of range");
+    return ev[device];
+}
+}  // namespace
+
 bool attack_fused_ok(int C, int K, int H, int O) { return C >= 1 && C <= 16 && K == ATT_K && H == ATT_H && O == 2; }
 
 void attack_auc_fused(Ctx& ctx, const float* logits, long long rows, int C, const float* W0, const float* b0,
@@ -442,6 +454,15 @@ void attack_auc_fused(Ctx& ctx, const float* logits, long long rows, int C, cons
                       double* acc) {
     if (!attack_fused_ok(C, ATT_K, ATT_H, 2)) fail(MTK_ERROR, "attack_auc: unsupported shape");
     cudaStream_t s = ctx.stream;
+    // c_att is one symbol per device, shared by every context on it: the copy
+    // of this call must not land while another context's scoring kernel still
+    // reads the previous weights (a different stream, so no implicit order).
+    // Per device, the stream waits on the event recorded after the last
+    // scoring launch, and records its own; the mutex orders the enqueues.
+    std::lock_guard<std::mutex> lk(att_mutex());
+    cudaEvent_t& last = att_last_use(ctx.device);
+    if (last) MTK_CUDA(cudaStreamWaitEvent(s, last, 0));
+    else MTK_CUDA(cudaEventCreateWithFlags(&last, cudaEventDisableTiming));
     // the attack model's weights -> constant memory (stream-ordered device copies)
     MTK_CUDA(cudaMemcpyToSymbolAsync(c_att, W0, ATT_K * ATT_H * 4, 0, cudaMemcpyDeviceToDevice, s));
     MTK_CUDA(cudaMemcpyToSymbolAsync(c_att, b0, ATT_H * 4, ATT_K * ATT_H * 4, cudaMemcpyDeviceToDevice, s));
@@ -453,6 +474,7 @@ void attack_auc_fused(Ctx& ctx, const float* logits, long long rows, int C, cons
     attack_score_kernel<16><<<nblocks(rows, 256), 256, 0, s>>>(logits, rows, C, labels, score_out, w.kn, w.kp,
                                                                w.cnt);
     count_launch();
+    MTK_CUDA(cudaEventRecord(last, s));
     auc_finish(ctx, w, labels, rows, auc, acc);
 }
 

@@ -292,12 +292,7 @@ void launch_mmd_pairs(const MmdArgs& a, cudaStream_t s) {
     const int nblk = mmd_blocks_per_group(a);
     if (nblk <= 0) return;
     const size_t smem = (size_t)((TI + TJ) * (a.d + 1) + TI * TJ) * sizeof(float);
-    static bool attr = false;
-    if (!attr) {
-        MTK_CUDA(cudaFuncSetAttribute(mmd_pairs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)((TI + TJ) * (MAXD + 1) + TI * TJ) * 4));
-        attr = true;
-    }
+    ensure_smem_attr(reinterpret_cast<const void*>(mmd_pairs_kernel), (int)((TI + TJ) * (MAXD + 1) + TI * TJ) * 4);
     mmd_pairs_kernel<<<dim3(nblk, a.G), NT, smem, s>>>(a, nblk);
     count_launch();
 }

@@ -1420,14 +1420,8 @@ void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s, int stages) 
         w.kpart = L.kpart;
         w.flags = a.flags;
         if (const char* e = getenv("MTK_MMDW_DIAG")) w.diag = atoi(e);
-        static bool wattr = false;
-        if (!wattr) {
-            MTK_CUDA(cudaFuncSetAttribute(mmd_w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          W_SMEM_BYTES));
-            wattr = true;
-        }
-        int sms = 148;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+        ensure_smem_attr(reinterpret_cast<const void*>(mmd_w_kernel), W_SMEM_BYTES);
+        const int sms = device_sm_count(current_device());
         const int items = a.G * np;
         mmd_w_kernel<<<std::min(items, sms), W_THREADS, W_SMEM_BYTES, s>>>(w);
         count_launch();
@@ -1544,14 +1538,8 @@ void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s, int stages) 
     p.flags = a.flags;
     p.vacc = vacc;
     p.trace = a.trace;
-    static bool attr = false;
-    if (!attr) {
-        MTK_CUDA(cudaFuncSetAttribute(mmd_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      Plan<true>::SMEM_BYTES));
-        MTK_CUDA(cudaFuncSetAttribute(mmd_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      Plan<false>::SMEM_BYTES));
-        attr = true;
-    }
+    ensure_smem_attr(reinterpret_cast<const void*>(mmd_tc_kernel<true>), Plan<true>::SMEM_BYTES);
+    ensure_smem_attr(reinterpret_cast<const void*>(mmd_tc_kernel<false>), Plan<false>::SMEM_BYTES);
     dim3 grid(p.nblk, (a.d + VD - 1) / VD, a.G);
     // the resident-Z_i-hi plan measured ~1.5% slower than the 4-stage ring
     // (GEMM1 is bound by operand reads, not by the TMA stream); opt-in only

@@ -580,18 +580,8 @@ bool disable_half_tiles() {
 
 template <int A_MN, int B_MN, bool PAIR>
 void launch_variant(UmmaParams p, int G, cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
-        MTK_CUDA(cudaFuncSetAttribute(umma_kernel<A_MN, B_MN, PAIR>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-        attr = true;
-    }
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        MTK_CUDA(cudaGetDevice(&dev));
-        MTK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    }
+    ensure_smem_attr(reinterpret_cast<const void*>(umma_kernel<A_MN, B_MN, PAIR>), SMEM_BYTES);
+    const int sms = device_sm_count(current_device());
     const long long ntiles = PAIR ? (long long)((p.M + 255) / 256) * ((p.N + 255) / 256) * G
                                   : (long long)((p.M + 127) / 128) * ((p.N + 127) / 128) * G;
     const long long ncl = std::min<long long>(ntiles, PAIR ? sms / 2 : sms);

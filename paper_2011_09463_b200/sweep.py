@@ -179,8 +179,9 @@ class GpuBackend:
                                       None if shift is None else torch.from_numpy(np.asarray(shift)))
 
     def _pool(self, X, y):
-        if isinstance(X, self.torch.Tensor):  # device-born pool (data_rng = "counter")
-            return X, y
+        if isinstance(X, self.torch.Tensor):  # device-resident pool (counter data, features)
+            return X, self.to_dev(np.ascontiguousarray(y, dtype=np.int32)
+                                  if not isinstance(y, self.torch.Tensor) else y)
         if not hasattr(self, "_pools"):
             self._pools = {}
         key = (id(X), id(y))
@@ -217,18 +218,26 @@ class GpuBackend:
                                **kw)
 
     def features(self, bank, X, head, k):
+        """[G, rows, k] top-k posteriors; stays on the device"""
         X = self.to_dev(X)
         logits = bank.forward(X, head=head)
-        return self.api.posterior_features(self.ctx, logits, k).cpu().numpy().reshape(
-            X.shape[0], X.shape[1], k)
+        return self.api.posterior_features(self.ctx, logits, k).reshape(X.shape[0], X.shape[1], k)
+
+    def all_gather(self, F):
+        """the feature all-gather over NCCL (mtk_allgather), device to device;
+        needs an initialised torch.distributed group (used for the NCCL id)"""
+        if getattr(self, "comm", None) is None:
+            self.comm = self.api.Comm(self.ctx)
+        return list(self.comm.all_gather(F.contiguous()).unbind(0))
 
     def attack_scores(self, bank, F):
-        logits = bank.forward(self.to_dev(F[None]), head=0)
-        return self.api.posterior_column(self.ctx, logits, 1).cpu().numpy()
+        logits = bank.forward(self.to_dev(F)[None].contiguous(), head=0)
+        return self.api.posterior_column(self.ctx, logits, 1)
 
     def auc(self, scores, labels):
-        return self.api.auc(self.ctx, self.to_dev(scores.astype(np.float32)),
-                            self.to_dev(labels.astype(np.uint8)))
+        torch = self.torch
+        sc = scores if isinstance(scores, torch.Tensor) else self.to_dev(scores.astype(np.float32))
+        return self.api.auc(self.ctx, sc, self.to_dev(np.ascontiguousarray(labels, dtype=np.uint8)))
 
 
 # --------------------------------------------------------------------------- training
@@ -320,31 +329,79 @@ def train_attack(be, cfg, F_train, lab_train, rng):
     return bank
 
 
+def _is_torch(x) -> bool:
+    return type(x).__module__.split(".")[0] == "torch"
+
+
+def _cat(parts):
+    if _is_torch(parts[0]):
+        import torch
+
+        return torch.cat(list(parts), 0)
+    return np.concatenate(parts, axis=0)
+
+
+def _f32(x):
+    if _is_torch(x):
+        import torch
+
+        return x.to(torch.float32).contiguous()
+    return np.ascontiguousarray(x, dtype=np.float32)
+
+
+def model_blocks(M: int, world: int):
+    """rank r trains the contiguous model block [r M / W, (r + 1) M / W)
+    (SURVEY.md 8(e)); every model's RNG stream is root.split(k + 1) whatever
+    the rank, so results do not depend on W"""
+    return [(r * M // world, (r + 1) * M // world) for r in range(world)]
+
+
+def gather_features(F, blocks, gather):
+    """Combine the ranks' feature blocks [G_r, Q, k] into [M, Q, k] in model
+    order with an EQUAL-size collective `gather` (an NCCL all-gather needs
+    equal buffers): each block is padded to the largest G_r, gathered, and
+    the padding trimmed again."""
+    gmax = max(hi - lo for lo, hi in blocks)
+    g = F.shape[0]
+    if g < gmax:
+        pad = (F[:1] * 0).repeat(gmax - g, 1, 1) if _is_torch(F) else np.zeros(
+            (gmax - g,) + F.shape[1:], dtype=F.dtype)
+        F = _cat([F, pad])
+    parts = gather(F)
+    if len(parts) != len(blocks):
+        raise RuntimeError(f"feature gather returned {len(parts)} blocks for {len(blocks)} ranks")
+    return _cat([p[:hi - lo] for p, (lo, hi) in zip(parts, blocks)])
+
+
 def run_sweep(cfg: SweepConfig, be=None, *, rank: int = 0, world: int = 1,
               all_gather=None) -> dict[str, Any]:
     """One paradigm: train target + shadows (sharded over ranks), attack, AUC.
 
     Models [0, 1 + n_shadows) are split into contiguous rank blocks; the
     per-rank feature blocks are combined with ``all_gather`` (a callable
-    taking this rank's array and returning the list over ranks, e.g. a
-    torch.distributed all_gather over NCCL); with one rank it is the identity.
+    taking this rank's block and returning the list over ranks), by default
+    the backend's own (the GPU backend: NCCL over NVLink through
+    mtk_allgather, device to device); with one rank it is the identity.
     """
     cfg.validate()
     be = be or GpuBackend()
     pop = Population(cfg, be.Rng, getattr(be, "synth_counter", None))
     M = 1 + cfg.n_shadows
     streams = pop.model_streams(M + 1)  # last stream drives the attack model
-    lo, hi = rank * M // world, (rank + 1) * M // world
+    blocks = model_blocks(M, world)
+    lo, hi = blocks[rank]
     models = list(range(lo, hi))
     bank, mem, non = train_bank(be, cfg, pop, streams, models)
     F, lab = query_features(be, cfg, pop, bank, mem, non)
-    parts = all_gather(F) if all_gather else [F]
-    F_all = np.concatenate(parts, axis=0)  # [M, 2*members, k] in model order
+    gather = all_gather or (getattr(be, "all_gather", None) if world > 1 else None)
+    if world > 1 and gather is None:
+        raise RuntimeError("run_sweep: world > 1 needs an all_gather")
+    F_all = gather_features(F, blocks, gather) if gather else F  # [M, 2*members, k], model order
     F_target, F_shadow = F_all[0], F_all[1:]
-    Ftr = F_shadow.reshape(-1, cfg.k).astype(np.float32)
+    Ftr = _f32(F_shadow.reshape(-1, cfg.k))
     ltr = np.tile(lab, cfg.n_shadows)
     attack = train_attack(be, cfg, Ftr, ltr, streams[M])
-    scores = be.attack_scores(attack, F_target.astype(np.float32))
+    scores = be.attack_scores(attack, _f32(F_target))
     auc, acc = be.auc(scores, lab)
     return {"paradigm": cfg.paradigm, "auc": auc, "accuracy": acc, "models": M,
             "rank_models": models, "n_queries": int(len(lab)),
@@ -478,9 +535,25 @@ def main(argv=None) -> int:
             if getattr(a, flag) is not None:  # flag > file > default
                 doc[key] = getattr(a, flag)
         cfg = resolve_config(doc)
+        # under torchrun: one rank per GPU, contiguous model blocks, the
+        # feature all-gather over NCCL (mtk_allgather); rank 0 reports
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        rank = int(os.environ.get("RANK", "0"))
+        kw = {}
+        if world > 1:
+            import torch
+            import torch.distributed as dist
+
+            local = int(os.environ.get("LOCAL_RANK", "0"))
+            torch.cuda.set_device(local)
+            if not dist.is_initialized():
+                dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            kw = dict(be=GpuBackend(local), rank=rank, world=world)
         t0 = time.perf_counter()
-        result = run_sweep(cfg)
+        result = run_sweep(cfg, **kw)
         report = metrics_report(cfg, result, time.perf_counter() - t0)
+        if rank != 0:
+            return EXIT_OK
         if a.output:
             os.makedirs(a.output, exist_ok=True)
             with open(os.path.join(a.output, "resolved_config.json"), "w") as f:

@@ -13,7 +13,9 @@ def pytest_configure(config):
 
 
 def has_ref():
-    return os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libmtref.so"))
+    import pyoracle
+
+    return pyoracle.ref_path() is not None
 
 
 @pytest.fixture(scope="session")

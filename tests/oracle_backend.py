@@ -26,6 +26,19 @@ class OracleBank:
         self.adam = [None] * G  # po.Adam per model, created on the first Adam step
 
 
+def _pmap(fn, n):
+    """fn(g) for g < n on host threads (ctypes releases the GIL, so the oracle's
+    C loops run in parallel; each model's arithmetic is unchanged)"""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+
+    workers = min(n, len(os.sched_getaffinity(0)))
+    if workers <= 1:
+        return [fn(g) for g in range(n)]
+    with ThreadPoolExecutor(workers) as ex:
+        return list(ex.map(fn, range(n)))
+
+
 class OracleBackend:
     Rng = OracleRng
 
@@ -46,40 +59,43 @@ class OracleBackend:
     def step(self, bank, X, y, w, *, lr, src_rows=0, frozen_layers=0, mmd_lambda=0.0,
              denom=(0.0, 0.0), optimizer="sgd"):
         X = np.asarray(X, dtype=np.float64)
-        for g in range(bank.G):
-            W, b = bank.params[g]
-            dH = None
-            if mmd_lambda > 0:
-                _, H = po.mlp_forward(bank.dims, W, b, X[g])
-                _, _, gs, gt = po.mmd_gaussian(H[:src_rows], H[src_rows:])
-                dH = mmd_lambda * np.concatenate([gs, gt])
-            B = X.shape[1]
-            if bank.n_heads == 2:
-                den = [denom[0] or src_rows, denom[1] or B - src_rows]
-            else:
-                den = [denom[0] or B]
-            if optimizer == "sgd":
-                po.mlp_train_step(bank.dims, W, b, X[g], y[g], n_heads=bank.n_heads,
-                                  frozen=frozen_layers, src_rows=src_rows, w=w[g], denoms=den,
-                                  lr=lr, dH=dH)
-                continue
-            # Adam: gradients of the same Tape composition (lr = 0), then
-            # optimizer_step over every parameter (frozen ones get zero grads,
-            # which leaves them and their moments unchanged)
-            _, gW, gb = po.mlp_train_step(bank.dims, W, b, X[g], y[g], n_heads=bank.n_heads,
-                                          frozen=frozen_layers, src_rows=src_rows, w=w[g],
-                                          denoms=den, lr=0.0, dH=dH, want_grads=True)
-            if bank.adam[g] is None:
-                bank.adam[g] = po.Adam(W + b, lr)
-            bank.adam[g].update(W + b, gW + gb)
+        _pmap(lambda g: self._step_one(bank, g, X, y, w, lr, src_rows, frozen_layers, mmd_lambda,
+                                       denom, optimizer), bank.G)
+
+    def _step_one(self, bank, g, X, y, w, lr, src_rows, frozen_layers, mmd_lambda, denom, optimizer):
+        W, b = bank.params[g]
+        dH = None
+        if mmd_lambda > 0:
+            _, H = po.mlp_forward(bank.dims, W, b, X[g])
+            _, _, gs, gt = po.mmd_gaussian(H[:src_rows], H[src_rows:])
+            dH = mmd_lambda * np.concatenate([gs, gt])
+        B = X.shape[1]
+        if bank.n_heads == 2:
+            den = [denom[0] or src_rows, denom[1] or B - src_rows]
+        else:
+            den = [denom[0] or B]
+        if optimizer == "sgd":
+            po.mlp_train_step(bank.dims, W, b, X[g], y[g], n_heads=bank.n_heads,
+                              frozen=frozen_layers, src_rows=src_rows, w=w[g], denoms=den,
+                              lr=lr, dH=dH)
+            return
+        # Adam: gradients of the same Tape composition (lr = 0), then
+        # optimizer_step over every parameter (frozen ones get zero grads,
+        # which leaves them and their moments unchanged)
+        _, gW, gb = po.mlp_train_step(bank.dims, W, b, X[g], y[g], n_heads=bank.n_heads,
+                                      frozen=frozen_layers, src_rows=src_rows, w=w[g],
+                                      denoms=den, lr=0.0, dH=dH, want_grads=True)
+        if bank.adam[g] is None:
+            bank.adam[g] = po.Adam(W + b, lr)
+        bank.adam[g].update(W + b, gW + gb)
 
     def features(self, bank, X, head, k):
-        out = []
-        for g in range(bank.G):
+        def one(g):
             W, b = bank.params[g]
             logits, _ = po.mlp_forward(bank.dims, W, b, np.asarray(X[g], dtype=np.float64), head)
-            out.append(po.posterior_features(logits, k))
-        return np.stack(out)
+            return po.posterior_features(logits, k)
+
+        return np.stack(_pmap(one, bank.G))
 
     def attack_scores(self, bank, F):
         W, b = bank.params[0]
@@ -159,3 +175,27 @@ class OracleReplica:
         for Wi, bi in zip(self.W, self.b):
             out += [self._torch.from_numpy(Wi), self._torch.from_numpy(bi)]
         return out
+
+
+class TorchFeatureOracleBackend(OracleBackend):
+    """TEST INFRASTRUCTURE: the oracle's arithmetic, but the posterior features
+    travel the way the GPU backend's do -- as tensors, combined across ranks
+    by an EQUAL-size tensor all-gather (dist.all_gather over the default
+    group: gloo in the CPU tests, NCCL / mtk_allgather on GPUs) -- so the
+    sweep's padding / trimming / rank-order logic runs without a GPU."""
+
+    def features(self, bank, X, head, k):
+        import torch
+
+        return torch.from_numpy(super().features(bank, X, head, k))
+
+    def all_gather(self, F):
+        import torch
+        import torch.distributed as dist
+
+        parts = [torch.empty_like(F) for _ in range(dist.get_world_size())]
+        dist.all_gather(parts, F.contiguous())
+        return parts
+
+    def attack_scores(self, bank, F):
+        return super().attack_scores(bank, np.asarray(F))

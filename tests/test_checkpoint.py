@@ -89,8 +89,8 @@ def test_load_errors(ctx, tmp_path):
         api.Bank.load(ctx, p2)
     # a future format_version -> version error naming both versions
     p3 = os.path.join(tmp_path, "version.ckpt")
-    open(p3, "wb").write(raw.replace(b"MTKBANK 1\n", b"MTKBANK 2\n", 1))
-    with pytest.raises(errors.VersionError, match="2.*1"):
+    open(p3, "wb").write(raw.replace(b"MTKBANK 2\n", b"MTKBANK 3\n", 1))
+    with pytest.raises(errors.VersionError, match="3.*2"):
         api.Bank.load(ctx, p3)
     # truncated payload -> truncation error (a CheckpointError and a DataError)
     p4 = os.path.join(tmp_path, "trunc.ckpt")
@@ -99,3 +99,29 @@ def test_load_errors(ctx, tmp_path):
         api.Bank.load(ctx, p4)
     assert issubclass(errors.TruncatedError, errors.CheckpointError)
     assert issubclass(errors.CheckpointError, errors.DataError)
+
+
+@pytest.mark.gpu
+def test_header_is_digested_and_strictly_parsed(ctx, tmp_path):
+    """The SHA-256 covers the config lines too (a corrupted Adam step count
+    would change the bias correction on resume); integers parse strictly."""
+    from paper_2011_09463_b200 import api, errors
+
+    a = _bank(ctx, [16, 12, 4], G=2)
+    X, y = _data(2, 20, 16, 4)
+    a.train_step(X, y, lr=0.01, optimizer="adam", want_loss=False)
+    path = os.path.join(tmp_path, "bank.ckpt")
+    a.save(path)
+    raw = open(path, "rb").read()
+    assert b"\nadam 1 1\n" in raw
+    cases = {"step": (b"\nadam 1 1\n", b"\nadam 1 2\n", errors.DigestError),
+             "garbage": (b"\nG 2\n", b"\nG 2x\n", errors.CheckpointError),
+             "negative": (b"\nheads 1\n", b"\nheads -1\n", errors.CheckpointError),
+             "missing": (b"\nheads 1\n", b"\n", errors.CheckpointError)}
+    for name, (old, new, exc) in cases.items():
+        p = os.path.join(tmp_path, name + ".ckpt")
+        open(p, "wb").write(raw.replace(old, new, 1))
+        with pytest.raises(exc):
+            api.Bank.load(ctx, p)
+    b = api.Bank.load(ctx, path)  # the untouched file still loads
+    assert b.dims == [16, 12, 4]

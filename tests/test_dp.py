@@ -313,3 +313,48 @@ def test_gpu_dataparallel_single_rank_step():
         assert torch.equal(p, q)
     with pytest.raises(errors.ConfigError):
         par.step(X, y, lr=0.05, mmd_lambda=1.0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dims", [(64, 128, 10), (40, 96, 64, 10), (24, 12, 4)])
+def test_gpu_compute_grads_never_writes_parameters(dims):
+    """compute_grads stores gradients only (no lr = 0 update): a non-finite
+    shard raises mt::Error but leaves the replica bit-identical (-0 * inf
+    would have made the parameters NaN)."""
+    from paper_2011_09463_b200 import errors
+
+    _, bank = _gpu_bank(dims, 11)
+    X, y = _gpu_batch(2, 64, dims[0], dims[-1], 4)
+    X[1, 3, 0] = float("inf")
+    before = _params(bank)
+    fp = bank.fingerprint()
+    with pytest.raises(errors.Error):
+        bank.compute_grads(X, y, want_loss=True)
+    assert all(torch.equal(p, q) for p, q in zip(before, _params(bank)))
+    assert bank.fingerprint() == fp
+
+
+@pytest.mark.gpu
+def test_gpu_api_rejects_wrong_dtypes_before_the_c_call():
+    """int32 indices / float64 pools / wrong shapes raise before libmtk reads them"""
+    from paper_2011_09463_b200 import errors
+
+    dims = (16, 12, 4)
+    _, bank = _gpu_bank(dims, 1)
+    X, y = _gpu_batch(2, 8, dims[0], dims[-1], 5)
+    pool = torch.randn(32, 16, device="cuda")
+    ypool = torch.zeros(32, dtype=torch.int32, device="cuda")
+    idx = torch.zeros((3, 2, 8), dtype=torch.int64, device="cuda")
+    with pytest.raises(errors.ValueError):
+        bank.train_epoch(pool, ypool, idx.int(), lr=0.1)
+    with pytest.raises(errors.ValueError):
+        bank.train_epoch(pool.double(), ypool, idx, lr=0.1)
+    with pytest.raises(errors.ShapeError):
+        bank.train_epoch(pool, ypool, idx, torch.ones((3, 2, 7), device="cuda"), lr=0.1)
+    with pytest.raises(errors.ValueError):
+        bank.train_step(X, y.long(), lr=0.1)
+    with pytest.raises(errors.ShapeError):
+        bank.train_step(X[:, :, :8].contiguous(), y, lr=0.1)
+    with pytest.raises(errors.ValueError):
+        bank.compute_grads(X.cpu(), y, want_loss=False)
+    bank.train_epoch(pool, ypool, idx, lr=0.1)  # the well-formed call still runs

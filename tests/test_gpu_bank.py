@@ -452,3 +452,62 @@ def test_attack_model_epoch_in_one_launch(ctx, monkeypatch, G, B, steps, weighte
                 # stream's narrow-input dW have separate partial-sum scratch
                 assert np.array_equal(c, d)
                 assert rel(a, c) <= 1e-5, (g, k, rel(a, c))
+
+
+def test_step_bench_shape_c2_models_of_the_32_model_bank(ctx):
+    """The bench's own step (bench.py: 1024-512-256-10, 512 src + 512 tgt,
+    5-bandwidth MMD lambda = 1 on the 256-d hidden layer, SGD lr 0.01) on the
+    bench's 32-model bank; models 0, 17 and 31 against the f64 oracle.
+
+    Per kernel, on identical inputs (north_star 1e-5):
+      * logits and the MMD sample h (forward chain, 3 GEMMs);
+      * MMD^2 value and its gradient dH on the GPU's own h;
+      * every dW / db of the step, with the oracle's backward fed the GPU's
+        own injected gradient lambda * dH (the injection of tape.hpp:153-171).
+    Chained (the oracle's own h, its own MMD gradient): the same bound."""
+    from paper_2011_09463_b200 import api
+
+    dims = [1024, 512, 256, 10]
+    G, B, src = 32, 1024, 512
+    bank = make_bank(ctx, G, dims, seed=20110946)
+    X, y = inputs(G, B, dims[0], dims[-1], seed=1000, shift=0.5)
+    Xd, yd = to_dev(X, y)
+    logits, H = bank.forward(Xd, hidden=True)
+    before = {g: bank.get_params(g) for g in (0, 17, 31)}
+    bank.keep_grads(True)
+    loss, mmd = bank.train_step(Xd, yd, lr=0.01, src_rows=src, mmd_lambda=1.0)
+    worst = {}
+    for g, (W, b) in before.items():
+        Xg = X[g].astype(np.float64)
+        lo, Ho = po.mlp_forward(dims, W, b, Xg)
+        worst["logits"] = max(worst.get("logits", 0), rel(logits[g].cpu().numpy(), lo))
+        worst["h"] = max(worst.get("h", 0), rel(H[g].cpu().numpy(), Ho))
+        Hg = H[g].double().cpu().numpy()
+        v, _, ogs, ogt = po.mmd_gaussian(Hg[:src], Hg[src:])
+        gv, _, ggs, ggt = api.mmd_gaussian(ctx, H[g, :src].contiguous(), H[g, src:].contiguous())
+        worst["mmd_value"] = max(worst.get("mmd_value", 0), rel(mmd[g], v), rel(gv, v))
+        dH_gpu = np.concatenate([ggs.cpu().numpy(), ggt.cpu().numpy()]).astype(np.float64)
+        worst["dH"] = max(worst.get("dH", 0), rel(dH_gpu, np.concatenate([ogs, ogt])))
+        # identical inputs: the oracle's backward with the GPU's injected gradient
+        Wc, bc = [x.copy() for x in W], [x.copy() for x in b]
+        lo_, gW, gb = po.mlp_train_step(dims, Wc, bc, Xg, y[g], src_rows=src, lr=0.01, dH=dH_gpu,
+                                        want_grads=True)
+        worst["loss"] = max(worst.get("loss", 0), rel(loss[g], lo_))
+        dW, db = bank.get_grads(g)
+        Wn, bn = bank.get_params(g)
+        for i in range(3):
+            worst[f"dW{i}"] = max(worst.get(f"dW{i}", 0), rel(dW[i], gW[i]))
+            worst[f"db{i}"] = max(worst.get(f"db{i}", 0), rel(db[i], gb[i]))
+            worst[f"W{i}"] = max(worst.get(f"W{i}", 0), rel(Wn[i], Wc[i]))
+        # chained: the oracle's own h and MMD gradient
+        _, _, cgs, cgt = po.mmd_gaussian(Ho[:src], Ho[src:])
+        Wc2, bc2 = [x.copy() for x in W], [x.copy() for x in b]
+        _, cW, cb = po.mlp_train_step(dims, Wc2, bc2, Xg, y[g], src_rows=src, lr=0.01,
+                                      dH=np.concatenate([cgs, cgt]), want_grads=True)
+        for i in range(3):
+            worst[f"chained_dW{i}"] = max(worst.get(f"chained_dW{i}", 0), rel(dW[i], cW[i]),
+                                          rel(db[i], cb[i]))
+    print("bench-shape C2 parity (max |d| / max |ref| per tensor):",
+          {k: f"{v:.2e}" for k, v in worst.items()})
+    for k, v in worst.items():
+        assert v <= TOL, (k, v, worst)

@@ -87,6 +87,50 @@ def test_sweep_two_ranks_gloo_matches_one(paradigm):
     assert out[0][2] + out[1][2] == list(range(1 + TINY["n_shadows"]))
 
 
+def _tensor_worker(rank, world, port, paradigm, out):
+    import torch.distributed as dist
+
+    from oracle_backend import TorchFeatureOracleBackend
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = SweepConfig(paradigm=paradigm, **dict(TINY, n_shadows=4))
+    r = run_sweep(cfg, TorchFeatureOracleBackend(), rank=rank, world=world)  # backend's own gather
+    out[rank] = (r["auc"], r["accuracy"], r["rank_models"])
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("paradigm", ["model", "mapping"])
+def test_sweep_tensor_feature_gather_two_ranks_matches_one(paradigm):
+    """Features as tensors through an equal-size all-gather (5 models over 2
+    ranks: blocks of 2 and 3, so the smaller block is padded and trimmed)
+    reproduce the one-rank numpy sweep bit for bit."""
+    import torch.multiprocessing as mp
+
+    from paper_2011_09463_b200.sweep import gather_features, model_blocks
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    out = mp.Manager().dict()
+    mp.spawn(_tensor_worker, args=(2, port, paradigm, out), nprocs=2, join=True)
+    single = run_sweep(SweepConfig(paradigm=paradigm, **dict(TINY, n_shadows=4)), OracleBackend())
+    assert out[0][:2] == out[1][:2] == (single["auc"], single["accuracy"])
+    assert out[0][2] == [0, 1] and out[1][2] == [2, 3, 4]
+    # the padding helper alone: unequal blocks round-trip in model order
+    blocks = model_blocks(7, 3)
+    full = np.arange(7 * 2 * 3, dtype=np.float32).reshape(7, 2, 3)
+    padded = []
+
+    def fake_gather(F):
+        padded.append(F.shape[0])
+        return [np.pad(full[lo:hi], ((0, 3 - (hi - lo)), (0, 0), (0, 0))) for lo, hi in blocks]
+
+    assert np.array_equal(gather_features(full[0:2], blocks, fake_gather), full)
+    assert padded == [3]
+
+
 MID = dict(dims=(64, 32, 10), n_shadows=4, pool=2048, members=512, source_pool=4096,
            source_per_model=1024, batch=64, epochs=6, pretrain_epochs=1, mu_scale=0.15,
            attack_epochs=20, attack_batch=256)
@@ -184,3 +228,24 @@ def test_sweep_main_exit_codes(tmp_path, monkeypatch):
     r1.pop("wall_clock_seconds"), r2.pop("wall_clock_seconds")
     assert r1 == r2 and 0.0 <= r1["auc"] <= 1.0
     assert _json.loads((out / "resolved_config.json").read_text())["paradigm"] == "model"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("paradigm", ["model", "mapping", "parameter"])
+def test_sweep_c1_parity_config_gpu_matches_oracle(paradigm):
+    """BASELINE.md C1, the parity config, end to end: SweepConfig() defaults
+    = MLP 784-256-10, 1 target + 4 shadows, 2048 members + 2048 non-members
+    per model from an 8192 pool, B = 128, E = 10, SGD lr 0.05, attack MLP
+    3-64-2 over 2^13 target queries.  GPU vs the f64 oracle backend: AUC and
+    accuracy within +-0.01 (north_star)."""
+    from paper_2011_09463_b200.sweep import GpuBackend
+
+    cfg = SweepConfig(paradigm=paradigm)
+    assert (cfg.dims, cfg.n_shadows, cfg.members, cfg.pool, cfg.batch, cfg.epochs) == \
+        ((784, 256, 10), 4, 2048, 8192, 128, 10)
+    g = run_sweep(cfg, GpuBackend())
+    o = run_sweep(SweepConfig(paradigm=paradigm), OracleBackend())
+    print(f"C1 {paradigm}: gpu auc {g['auc']:.5f} acc {g['accuracy']:.5f} | "
+          f"oracle auc {o['auc']:.5f} acc {o['accuracy']:.5f}")
+    assert abs(g["auc"] - o["auc"]) <= 0.01, (g["auc"], o["auc"])
+    assert abs(g["accuracy"] - o["accuracy"]) <= 0.01, (g["accuracy"], o["accuracy"])

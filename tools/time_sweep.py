@@ -31,12 +31,12 @@ t2 = time.perf_counter()
 F, lab = sweep.query_features(be, cfg, pop, bank, mem, non)
 t3 = time.perf_counter()
 import numpy as np  # noqa: E402
-Ftr = F[1:].reshape(-1, cfg.k).astype(np.float32)
+Ftr = F[1:].reshape(-1, cfg.k).float().contiguous()
 ltr = np.tile(lab, cfg.n_shadows)
 att = sweep.train_attack(be, cfg, Ftr, ltr, streams[M])
 torch.cuda.synchronize()
 t4 = time.perf_counter()
-scores = be.attack_scores(att, F[0].astype(np.float32))
+scores = be.attack_scores(att, F[0].float().contiguous())
 auc, acc = be.auc(scores, lab)
 t5 = time.perf_counter()
 print(f"{par} [{drng}, pool {pool}]: models {M}: data {t1-t0:.2f}s train {t2-t1:.2f}s query {t3-t2:.2f}s "
