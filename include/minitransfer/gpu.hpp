@@ -177,6 +177,34 @@ class Bank {
     void forward(const float* X, int B, float* logits, int head = 0, float* hidden = nullptr) {
         check(mtk_bank_forward(h_, X, B, head, logits, hidden), "forward");
     }
+    // nsteps steps without host round trips (the trainers' batch_iter loop,
+    // SPEC.md:605-613): step s gathers X_pool[idx[s, g, r]] on the device;
+    // idx int64 [nsteps, G, B], w [nsteps, G, B] or null, denom0 [nsteps] or null
+    void train_epoch(const mtk_step& tmpl, const float* X_pool, const int32_t* y_pool, int64_t pool_rows,
+                     const int64_t* idx, const float* w, const double* denom0, int nsteps) {
+        check(mtk_bank_train_epoch(h_, &tmpl, X_pool, y_pool, pool_rows, idx, w, denom0, nsteps),
+              "train_epoch");
+    }
+    // data-parallel dp_step: this worker's gradients into a
+    // device arena (parameters untouched), then the ordered mean + one step
+    int64_t grad_size() {
+        int64_t n = 0;
+        check(mtk_bank_grad_size(h_, &n), "grad_size");
+        return n;
+    }
+    std::vector<double> compute_grads(const mtk_step& s, float* grads) {
+        std::vector<double> loss(G_);
+        check(mtk_bank_compute_grads(h_, &s, grads, loss.data(), nullptr), "compute_grads");
+        return loss;
+    }
+    void dp_apply(const mtk_step& s, const float* parts, int n_parts, int64_t part_stride) {
+        check(mtk_bank_dp_apply(h_, &s, parts, n_parts, part_stride), "dp_apply");
+    }
+    uint64_t fingerprint() {
+        uint64_t v = 0;
+        check(mtk_bank_fingerprint(h_, &v), "fingerprint");
+        return v;
+    }
     mtk_bank* get() const { return h_; }
 
   private:
@@ -199,6 +227,62 @@ inline MmdResult mmd_gaussian(Context& ctx, const float* Xs, int64_t m, const fl
     check(mtk_mmd_gaussian(ctx.get(), Xs, m, Xt, n, d, mult.empty() ? nullptr : mult.data(),
                            (int)mult.size(), beta, &r.value, &r.beta, gXs, gXt),
           "mmd_gaussian");
+    return r;
+}
+
+// batch assembly on the device: out[g, row0 + r, :] = src[idx[g * nb + r], :]
+inline void gather_rows(Context& ctx, const void* src, int64_t src_rows, int d, const int64_t* idx, int G,
+                        int nb, void* out, int out_rows, int row0 = 0) {
+    check(mtk_gather_rows(ctx.get(), src, src_rows, d, idx, G, nb, out, out_rows, row0), "gather_rows");
+}
+
+// counter-based synthetic pool straight into HBM (mtk.h contract, 8(f) f3)
+inline void synth_counter(Context& ctx, uint64_t seed, uint64_t stream, int C, int d, int64_t n,
+                          const float* mu, const float* shift, float* X, int32_t* y) {
+    check(mtk_synth_counter(ctx.get(), seed, stream, C, d, n, mu, shift, X, y), "synth_counter");
+}
+
+// The feature all-gather of the sharded sweep (NCCL over NVLink).  Rank 0
+// makes the id (unique_id()) and ships it to the others (any transport).
+class Comm {
+  public:
+    static std::vector<uint8_t> unique_id() {
+        std::vector<uint8_t> id(128);
+        check(mtk_comm_unique_id(id.data()), "comm_unique_id");
+        return id;
+    }
+    Comm(int nranks, int rank, const std::vector<uint8_t>& id) {
+        if (id.size() != 128) throw ValueError("Comm: the NCCL id is 128 bytes");
+        check(mtk_comm_init(nranks, rank, id.data(), &h_), "comm_init");
+    }
+    ~Comm() { mtk_comm_destroy(h_); }
+    Comm(const Comm&) = delete;
+    Comm& operator=(const Comm&) = delete;
+    void all_gather(Context& ctx, const void* send, void* recv, size_t bytes_per_rank) {
+        check(mtk_allgather(h_, ctx.get(), send, recv, bytes_per_rank), "allgather");
+    }
+    mtk_comm* get() const { return h_; }
+
+  private:
+    mtk_comm* h_ = nullptr;
+};
+
+// The shadow-training sweep + membership attack:
+// defaults are BASELINE.md C1.  One rank, or this rank's block of a sharded
+// run when `comm` is given.
+struct SweepConfig : mtk_sweep_config {
+    SweepConfig() { mtk_sweep_config_default(this); }
+    SweepConfig& set_dims(const std::vector<int>& d) {
+        if (d.size() < 2 || d.size() > MTK_SWEEP_MAX_LAYERS) throw ConfigError("SweepConfig: bad dims");
+        n_layers = (int)d.size() - 1;
+        for (std::size_t i = 0; i < d.size(); ++i) dims[i] = d[i];
+        return *this;
+    }
+};
+using SweepResult = mtk_sweep_result;
+inline SweepResult run_shadow_sweep(Context& ctx, const SweepConfig& cfg, Comm* comm = nullptr) {
+    SweepResult r{};
+    check(mtk_sweep_run(ctx.get(), &cfg, comm ? comm->get() : nullptr, &r), "run_shadow_sweep");
     return r;
 }
 

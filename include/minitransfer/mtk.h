@@ -303,6 +303,46 @@ int mtk_comm_info(mtk_comm* comm, int* nranks, int* rank, int* device, int* nccl
  * be on the same device.                                                    */
 int mtk_allgather(mtk_comm* comm, mtk_ctx* ctx, const void* send, void* recv, size_t bytes_per_rank);
 
+/* ---- the shadow-training sweep + membership attack in one native call
+ * (the reference has no code
+ * for it).  One paradigm: target (model 0) + n_shadows shadow models trained
+ * as one bank per rank (contiguous model blocks; stream k+1 of Rng(seed) for
+ * model k on every rank), top-k posterior features of each model on its
+ * members / non-members, the ranks' features all-gathered (comm, or NULL for
+ * one rank), an attack MLP k -> attack_hidden -> 2 trained on the shadows'
+ * features, AUC (mid-rank Mann-Whitney) and accuracy at 0.5 on the target's.
+ * Same definitions, call for call, as paper_2011_09463_b200/sweep.py (its
+ * docstring pins them); results are identical on one device.              */
+#define MTK_PARADIGM_MODEL 0     /* fine-tuning: pretrain on source, then members */
+#define MTK_PARADIGM_MAPPING 1   /* CE on [source; members] + lambda MMD^2 on the hidden layer */
+#define MTK_PARADIGM_PARAMETER 2 /* shared trunk + source head + target head */
+#define MTK_SWEEP_MAX_LAYERS 8
+typedef struct {
+    int paradigm;
+    int n_layers;                      /* dims[0..n_layers] */
+    int dims[MTK_SWEEP_MAX_LAYERS + 1];
+    int n_shadows, pool, members, source_pool, source_per_model;
+    int batch, epochs, pretrain_epochs, frozen_layers;
+    double lr;
+    int optimizer;                     /* 0 SGD, 1 Adam */
+    double mmd_lambda, mu_scale, shift_scale;
+    int k, attack_hidden, attack_epochs, attack_batch;
+    double attack_lr;
+    int attack_optimizer;
+    int data_rng;                      /* 0 host mt::Rng (bit-exact), 1 device Philox counter */
+    uint64_t seed;
+} mtk_sweep_config;
+typedef struct {
+    double auc, accuracy;
+    int models, rank_model_begin, rank_model_end;
+    int64_t n_queries;
+    double seconds;
+} mtk_sweep_result;
+/* BASELINE.md C1 (the parity config): 784-256-10, 1 target + 4 shadows,
+ * 2048 members of an 8192 pool, B = 128, E = 10, SGD lr 0.05, attack 3-64-2 */
+void mtk_sweep_config_default(mtk_sweep_config* cfg);
+int mtk_sweep_run(mtk_ctx* ctx, const mtk_sweep_config* cfg, mtk_comm* comm, mtk_sweep_result* out);
+
 /* ---- diagnostics (tests / profiling): C[g] = A[g] * B[g] through the
  * tcgen05 3xTF32 tensor-core GEMM used by the bank.  a_mn: A stored
  * [G][K][M] (1) or [G][M][K] (0); b_mn: B stored [G][K][N] (1) or [G][N][K]

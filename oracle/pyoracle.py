@@ -164,6 +164,9 @@ def _setup_ref(L):
     L.ref_bench_attack.restype = C.c_double
     L.ref_bench_attack.argtypes = [C.c_int, C.c_int64, C.c_int, C.c_uint64, _dp]
     L.ref_build_info.restype = C.c_char_p
+    L.ref_bench_train_heads.restype = C.c_double
+    L.ref_bench_train_heads.argtypes = [C.c_int, C.c_int, _ip, C.c_int, C.c_int, C.c_int, C.c_int,
+                                        C.c_double, C.c_uint64]
     L.ref_bench_train.restype = C.c_double
     L.ref_bench_train.argtypes = [C.c_int, C.c_int, _ip, C.c_int, C.c_int, C.c_int, C.c_double,
                                   C.c_uint64]

@@ -425,8 +425,18 @@ using Clock = std::chrono::steady_clock;
 // last hidden layer, injected into the step's own Tape.  Init + data before
 // the timed region; returns the seconds from the common start line until the
 // last thread finishes its steps.
+double ref_bench_train_heads(int threads, int L, const int* dims, int n_heads, int B, int src_rows,
+                             int steps, double mmd_lambda, uint64_t seed);
 double ref_bench_train(int threads, int L, const int* dims, int B, int src_rows, int steps,
                        double mmd_lambda, uint64_t seed) {
+    return ref_bench_train_heads(threads, L, dims, 1, B, src_rows, steps, mmd_lambda, seed);
+}
+
+// n_heads == 2: the parameter-based paradigm (shared trunk, a source head and
+// a target head; rows [0, src_rows) through head 0, the rest through head 1,
+// CE of each head over its own rows)
+double ref_bench_train_heads(int threads, int L, const int* dims, int n_heads, int B, int src_rows,
+                             int steps, double mmd_lambda, uint64_t seed) {
     Barrier start(threads + 1);
     std::vector<std::thread> pool;
     std::vector<Clock::time_point> done(threads);
@@ -434,18 +444,19 @@ double ref_bench_train(int threads, int L, const int* dims, int B, int src_rows,
         pool.emplace_back([=, &start, &done]() {
             mt::Rng rng(seed + th);
             std::vector<mt::Parameter> W, b;
-            for (int l = 0; l < L; ++l) {
+            for (int i = 0; i < L + n_heads - 1; ++i) {
+                const int l = i < L ? i : L - 1;
                 const double lim = 1.0 / std::sqrt((double)dims[l]);
                 std::vector<double> w((std::size_t)dims[l] * dims[l + 1]);
                 for (double& v : w) v = rng.uniform(-lim, lim);
-                W.emplace_back("W" + std::to_string(l), mt::Tensor({(std::size_t)dims[l], (std::size_t)dims[l + 1]}, w));
-                b.emplace_back("b" + std::to_string(l),
+                W.emplace_back("W" + std::to_string(i), mt::Tensor({(std::size_t)dims[l], (std::size_t)dims[l + 1]}, w));
+                b.emplace_back("b" + std::to_string(i),
                                mt::Tensor({(std::size_t)dims[l + 1]}, std::vector<double>(dims[l + 1], 0.0)));
             }
             std::vector<mt::Parameter*> params;
-            for (int l = 0; l < L; ++l) {
-                params.push_back(&W[l]);
-                params.push_back(&b[l]);
+            for (std::size_t i = 0; i < W.size(); ++i) {
+                params.push_back(&W[i]);
+                params.push_back(&b[i]);
             }
             std::vector<double> X((std::size_t)B * dims[0]);
             for (double& v : X) v = rng.normal();
@@ -453,6 +464,14 @@ double ref_bench_train(int threads, int L, const int* dims, int B, int src_rows,
             for (auto& v : y) v = (int)rng.below(dims[L]);
             const std::vector<double> wts(B, 1.0);
             const mt::Tensor Xt({(std::size_t)B, (std::size_t)dims[0]}, X);
+            const std::size_t ns = src_rows, nt = B - src_rows;
+            const mt::Tensor Xs2({ns ? ns : 1, (std::size_t)dims[0]},
+                                 std::vector<double>(X.begin(), X.begin() + (ns ? ns : 1) * dims[0]));
+            const mt::Tensor Xt2({nt ? nt : 1, (std::size_t)dims[0]},
+                                 std::vector<double>(X.begin() + ns * dims[0],
+                                                     X.begin() + (ns + (nt ? nt : 1)) * dims[0]));
+            const std::vector<int> ys(y.begin(), y.begin() + ns), yt(y.begin() + ns, y.end());
+            const std::vector<double> ws(ns, 1.0), wt2(nt, 1.0);
             const std::size_t hd = dims[L - 1];
             std::vector<double> G((std::size_t)B * hd);
             const double mult[5] = {0.25, 0.5, 1.0, 2.0, 4.0};
@@ -462,9 +481,25 @@ double ref_bench_train(int threads, int L, const int* dims, int B, int src_rows,
                 mt::zero_grads(params);
                 mt::Tape t;
                 std::vector<mt::Var> pw, pb;
-                for (int l = 0; l < L; ++l) {
-                    pw.push_back(t.param(W[l]));
-                    pb.push_back(t.param(b[l]));
+                for (std::size_t i = 0; i < W.size(); ++i) {
+                    pw.push_back(t.param(W[i]));
+                    pb.push_back(t.param(b[i]));
+                }
+                if (n_heads == 2) {  // parameter-based: two heads over the shared trunk
+                    auto run = [&](const mt::Tensor& x, int head) {
+                        mt::Var h = t.constant(x);
+                        for (int l = 0; l < L; ++l) {
+                            const int i = (l == L - 1) ? l + head : l;
+                            mt::Var z = t.add_bias(t.matmul(h, pw[i]), pb[i]);
+                            h = (l == L - 1) ? z : t.relu(z);
+                        }
+                        return h;
+                    };
+                    mt::Var loss = t.add(t.cross_entropy_weighted(run(Xs2, 0), ys, ws, (double)ns),
+                                         t.cross_entropy_weighted(run(Xt2, 1), yt, wt2, (double)nt));
+                    t.backward(loss);
+                    mt::optimizer_step(st, params);
+                    continue;
                 }
                 mt::Var h = t.constant(Xt), h_last = h;
                 for (int l = 0; l < L; ++l) {

@@ -47,7 +47,39 @@ class MtkStep(C.Structure):
     ]
 
 
+class MtkSweepConfig(C.Structure):
+    """mirrors mtk_sweep_config in mtk.h"""
+    _fields_ = [
+        ("paradigm", C.c_int),
+        ("n_layers", C.c_int),
+        ("dims", C.c_int * 9),
+        ("n_shadows", C.c_int), ("pool", C.c_int), ("members", C.c_int), ("source_pool", C.c_int),
+        ("source_per_model", C.c_int),
+        ("batch", C.c_int), ("epochs", C.c_int), ("pretrain_epochs", C.c_int), ("frozen_layers", C.c_int),
+        ("lr", C.c_double),
+        ("optimizer", C.c_int),
+        ("mmd_lambda", C.c_double), ("mu_scale", C.c_double), ("shift_scale", C.c_double),
+        ("k", C.c_int), ("attack_hidden", C.c_int), ("attack_epochs", C.c_int), ("attack_batch", C.c_int),
+        ("attack_lr", C.c_double),
+        ("attack_optimizer", C.c_int),
+        ("data_rng", C.c_int),
+        ("seed", C.c_uint64),
+    ]
+
+
+class MtkSweepResult(C.Structure):
+    """mirrors mtk_sweep_result in mtk.h"""
+    _fields_ = [
+        ("auc", C.c_double), ("accuracy", C.c_double),
+        ("models", C.c_int), ("rank_model_begin", C.c_int), ("rank_model_end", C.c_int),
+        ("n_queries", C.c_int64),
+        ("seconds", C.c_double),
+    ]
+
+
 SIGNATURES = {
+    "mtk_sweep_config_default": (None, [C.POINTER(MtkSweepConfig)]),
+    "mtk_sweep_run": (C.c_int, [_vp, C.POINTER(MtkSweepConfig), _vp, C.POINTER(MtkSweepResult)]),
     "mtk_version": (C.c_int, []),
     "mtk_last_error": (C.c_char_p, []),
     "mtk_ctx_create": (C.c_int, [C.c_int, _vp, C.POINTER(_vp)]),

@@ -16,7 +16,7 @@ import numpy as np
 import torch
 
 from . import errors
-from ._lib import MtkStep, lib
+from ._lib import MtkStep, MtkSweepConfig, MtkSweepResult, lib
 
 _dp = C.POINTER(C.c_double)
 
@@ -648,3 +648,35 @@ class Comm:
             self.close()
         except Exception:  # noqa: BLE001
             pass
+
+
+def sweep_run(ctx: Context, cfg: dict | None = None, comm: "Comm" = None) -> dict:
+    """The whole sweep (one paradigm) through the native driver, mtk_sweep_run:
+    cfg keys are SweepConfig's (paradigm "model" | "mapping" | "parameter",
+    optimizer "sgd" | "adam", data_rng "host" | "counter", dims a tuple);
+    unspecified keys keep the C1 defaults."""
+    c = MtkSweepConfig()
+    lib.mtk_sweep_config_default(C.byref(c))
+    enum = {"paradigm": {"model": 0, "mapping": 1, "parameter": 2}, "optimizer": {"sgd": 0, "adam": 1},
+            "attack_optimizer": {"sgd": 0, "adam": 1}, "data_rng": {"host": 0, "counter": 1}}
+    for key, v in (cfg or {}).items():
+        if key == "dims":
+            if not 2 <= len(v) <= 9:
+                raise errors.ConfigError("sweep: 1 to 8 layers")
+            c.n_layers = len(v) - 1
+            for i, x in enumerate(v):
+                c.dims[i] = int(x)
+        elif key in enum:
+            if v not in enum[key]:
+                raise errors.ConfigError(f"sweep: unknown {key} {v!r}")
+            setattr(c, key, enum[key][v])
+        elif hasattr(c, key):
+            setattr(c, key, v)
+        else:
+            raise errors.ConfigError(f"sweep: unknown key {key!r}")
+    r = MtkSweepResult()
+    errors.check(lib.mtk_sweep_run(ctx.h, C.byref(c), comm.h if comm is not None else None, C.byref(r)),
+                 "sweep_run")
+    return {"auc": r.auc, "accuracy": r.accuracy, "models": r.models,
+            "rank_models": list(range(r.rank_model_begin, r.rank_model_end)),
+            "n_queries": r.n_queries, "seconds": r.seconds}

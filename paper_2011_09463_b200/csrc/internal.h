@@ -216,6 +216,9 @@ struct UmmaGemm {
     const float* b2 = nullptr;
     long long b2_rs = 0, b2_gs = 0;
     int ksplit = 0;
+    // the operands are of one sign (e.g. MMD V = W.Z, W >= 0, Z = post-ReLU
+    // h >= 0): accumulate the 3xTF32 corrections separately whatever K is
+    int same_sign = 0;
     int* flags = nullptr;
 };
 void launch_umma(const UmmaGemm& u, cudaStream_t s);

@@ -1462,6 +1462,7 @@ void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s, int stages) 
         u.b_rs = a.d;
         u.b_gs = a.xs_gs;
         u.epi = Epi::kMmdGrad;
+        u.same_sign = 1;  // W >= 0 (and Z >= 0 in bank steps): see k_umma.cu sepc
         u.C = a.gXs;
         u.c_gs = a.gs_gs;
         if (head) {  // fused head DX: K gains the head block; the epilogue writes the layer's dZ

@@ -26,6 +26,18 @@
 // Persistent: one CTA (pair) per SM (pair), static tile striding; the TMEM
 // accumulator is double-buffered so the epilogue of tile t overlaps the
 // mainloop of tile t+1.
+// Accumulation precision (sepc): each MMA adds its 8 products into the fp32
+// TMEM accumulator with the result truncated toward zero, so a long K drifts
+// by ~0.5 ulp(acc) per MMA (measured, tools/gemm_precision.py: -1.9e-5 mean
+// relative error at K = 1024 on same-sign operands, 8.4e-6 max on zero-mean
+// ones).  Two thirds of those adds are the small hi*lo / lo*hi corrections.
+// With sepc the corrections accumulate in their own TMEM accumulator (2^-10
+// the magnitude, so their truncation is negligible) and the epilogue adds
+// main + corr once in fp32: the drift falls to the 128 hi*hi adds of K = 1024.
+// The correction accumulator takes the second TMEM buffer, so a sepc launch
+// runs single-buffered (the epilogue no longer overlaps the next mainloop);
+// it is used for K >= kSepcMinK and for the MMD V = W.Z GEMM (non-negative
+// operands, and g = z Wsum - V cancels).
 // Warp roles: w0 TMA producer, w1 MMA issuer (one elected thread), w2-w5
 // epilogue (TMEM -> registers -> fused bias/ReLU | ReLU-mask | SGD -> HBM),
 // w6-w13 converters.  Two rings: LS load stages (32 KB: A and B fp32 as TMA
@@ -50,6 +62,7 @@ namespace {
 using namespace sm100;
 
 constexpr int BK = 32, LS = 5, LO = 2;
+constexpr int kSepcMinK = 768;  // K from which corrections get their own accumulator
 constexpr int TILE_BYTES = 128 * BK * 4;     // 16 KB: 128 rows (or cols) x 32 k
 constexpr int LOAD_BYTES = 2 * TILE_BYTES;   // load stage: A fp32, B fp32 (TMA bytes)
 constexpr int LO_BYTES = 2 * TILE_BYTES;     // lo stage: A lo, B lo
@@ -143,8 +156,8 @@ __device__ __forceinline__ void convert_stage(uint8_t* st, uint8_t* lo, int t) {
 
 // 3 MMAs per 8-wide k step over one stage
 template <int A_MN, int B_MN, bool PAIR>
-__device__ __forceinline__ void mma_stage(uint32_t tmem, uint32_t base, uint32_t lo, uint32_t idesc,
-                                          bool first) {
+__device__ __forceinline__ void mma_stage(uint32_t tmem, uint32_t tcorr, uint32_t base, uint32_t lo,
+                                          uint32_t idesc, bool first) {
     constexpr uint32_t a_lbo = A_MN ? 4096 : 16, b_lbo = B_MN ? 4096 : 16;
     constexpr uint32_t a_sbo = A_MN ? 512 : 1024, b_sbo = B_MN ? 512 : 1024;
     constexpr uint32_t a_lay = A_MN ? 1 : 2, b_lay = B_MN ? 1 : 2;
@@ -159,14 +172,16 @@ __device__ __forceinline__ void mma_stage(uint32_t tmem, uint32_t base, uint32_t
         const uint64_t b32 = smem_desc(base + TILE_BYTES + boff, b_lbo, b_sbo, b_lay);
         const uint64_t blo = smem_desc(lo + TILE_BYTES + boff, b_lbo, b_sbo, b_lay);
         const uint32_t acc0 = (first && kk == 0) ? 0u : 1u;
+        // tcorr == tmem: one accumulator; else the corrections have their own
+        const uint32_t accm = tcorr == tmem ? 1u : acc0;
         if (PAIR) {
-            mma_tf32_2sm(tmem, a32, blo, idesc, acc0);
-            mma_tf32_2sm(tmem, alo, b32, idesc, 1u);
-            mma_tf32_2sm(tmem, a32, b32, idesc, 1u);
+            mma_tf32_2sm(tcorr, a32, blo, idesc, acc0);
+            mma_tf32_2sm(tcorr, alo, b32, idesc, 1u);
+            mma_tf32_2sm(tmem, a32, b32, idesc, accm);
         } else {
-            mma_tf32(tmem, a32, blo, idesc, acc0);
-            mma_tf32(tmem, alo, b32, idesc, 1u);
-            mma_tf32(tmem, a32, b32, idesc, 1u);
+            mma_tf32(tcorr, a32, blo, idesc, acc0);
+            mma_tf32(tcorr, alo, b32, idesc, 1u);
+            mma_tf32(tmem, a32, b32, idesc, accm);
         }
     }
 }
@@ -192,8 +207,9 @@ __device__ __forceinline__ float column_sums_32(float (&v)[32], int lane) {
 // global operand load (bias | mask, add | master weight) is issued before the
 // TMEM read, so a chunk costs one memory round trip.  No shared memory: the
 // mainloop running on the other accumulator saturates the smem port.
-__device__ __forceinline__ void epilogue_rows(const UmmaParams& p, uint32_t tmem, int q, int lane,
-                                              int g, int m0, int n0, int c0, int c1) {
+template <bool SEPC>
+__device__ __forceinline__ void epilogue_rows(const UmmaParams& p, uint32_t tmem, uint32_t tcorr, int q,
+                                              int lane, int g, int m0, int n0, int c0, int c1) {
     const int mw = m0 + 32 * q;
     const int m = mw + lane;
     const bool row_ok = m < p.M;
@@ -221,6 +237,15 @@ __device__ __forceinline__ void epilogue_rows(const UmmaParams& p, uint32_t tmem
         }
         float v[32];
         tmem_ld_32x32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(c * 32), v);
+        if (SEPC) {  // main + corrections, one fp32 add (8 columns at a time: registers)
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                float w[8];
+                tmem_ld_32x8(tcorr + ((uint32_t)(32 * q) << 16) + (uint32_t)(c * 32 + 8 * h), w);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) v[8 * h + j] += w[j];
+            }
+        }
         if (vec) {
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
@@ -345,7 +370,7 @@ __device__ __forceinline__ void prefetch_epilogue_rows(const UmmaParams& p, int 
     }
 }
 
-template <int A_MN, int B_MN, bool PAIR>
+template <int A_MN, int B_MN, bool PAIR, bool SEPC>
 __global__ void __launch_bounds__(NUM_THREADS, 1) umma_kernel(const __grid_constant__ UmmaParams p) {
     constexpr int TN = PAIR ? 256 : 128;  // accumulator columns per tile
     constexpr uint32_t TMEM_COLS = 2 * TN;  // double-buffered accumulator
@@ -443,17 +468,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_kernel(const __grid_const
             uint32_t it = 0, tl = 0;
             for (int w = cid; w < nitems; w += ncl, ++tl) {
                 const uint32_t idesc = w < p.nfull ? idesc_full : idesc_half;
-                const uint32_t b = tl & 1;
-                mbar_wait(&acc_empty[b], ((tl >> 1) & 1) ^ 1);
+                // SEPC: every tile takes both buffers (main, corrections)
+                const uint32_t b = SEPC ? 0u : (tl & 1);
+                const uint32_t ph = SEPC ? (tl & 1) : ((tl >> 1) & 1);
+                mbar_wait(&acc_empty[b], ph ^ 1);
                 tc_fence_after();
                 const uint32_t acc = tmem + b * TN;
+                const uint32_t corr = SEPC ? tmem + TN : acc;
                 for (int kb = 0; kb < nk; ++kb, ++it) {
                     const int s = it % LS, l = it % LO;
                     mbar_wait(&conv[l], (it / LO) & 1);
                     tc_fence_after();
                     if (lane == 0) {
                         if (tr && it < 1000) tr[1000 + it] = gtime();
-                        mma_stage<A_MN, B_MN, PAIR>(acc, smem_u32(smem + s * LOAD_BYTES),
+                        mma_stage<A_MN, B_MN, PAIR>(acc, corr, smem_u32(smem + s * LOAD_BYTES),
                                                     smem_u32(lo_ring + l * LO_BYTES), idesc, kb == 0);
                         if (PAIR) {  // frees the slots in both CTAs
                             mma_commit_2sm(&empty[s], 0x3);
@@ -483,12 +511,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_kernel(const __grid_const
             const int m0 = PAIR ? im.mt * 256 + (int)rank * 128 : im.mt * 128;
             const int ncols = im.half < 0 ? TN : TN / 2;
             const int n0 = im.nt * TN + (im.half > 0 ? TN / 2 : 0);
-            const uint32_t b = tl & 1;
-            mbar_wait(&acc_full[b], (tl >> 1) & 1);
+            const uint32_t b = SEPC ? 0u : (tl & 1);
+            mbar_wait(&acc_full[b], SEPC ? (tl & 1) : ((tl >> 1) & 1));
             if (tr && threadIdx.x == 64 && tl < 16) tr[2000 + 2 * tl] = gtime();
             tc_fence_after();
             const int nch = ncols / 32;
-            epilogue_rows(p, tmem + b * TN, q, lane, g, m0, n0, hsel * (nch / 2), (hsel + 1) * (nch / 2));
+            epilogue_rows<SEPC>(p, tmem + b * TN, tmem + TN, q, lane, g, m0, n0, hsel * (nch / 2),
+                                (hsel + 1) * (nch / 2));
             tc_fence_before();
             __syncwarp();
             if (tr && threadIdx.x == 64 && tl < 16) tr[2001 + 2 * tl] = gtime();
@@ -578,9 +607,9 @@ bool disable_half_tiles() {
     return mode == 1;
 }
 
-template <int A_MN, int B_MN, bool PAIR>
+template <int A_MN, int B_MN, bool PAIR, bool SEPC>
 void launch_variant(UmmaParams p, int G, cudaStream_t s) {
-    ensure_smem_attr(reinterpret_cast<const void*>(umma_kernel<A_MN, B_MN, PAIR>), SMEM_BYTES);
+    ensure_smem_attr(reinterpret_cast<const void*>(umma_kernel<A_MN, B_MN, PAIR, SEPC>), SMEM_BYTES);
     const int sms = device_sm_count(current_device());
     const long long ntiles = PAIR ? (long long)((p.M + 255) / 256) * ((p.N + 255) / 256) * G
                                   : (long long)((p.M + 127) / 128) * ((p.N + 127) / 128) * G;
@@ -605,16 +634,21 @@ void launch_variant(UmmaParams p, int G, cudaStream_t s) {
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    MTK_CUDA(cudaLaunchKernelEx(&cfg, umma_kernel<A_MN, B_MN, PAIR>, p));
+    MTK_CUDA(cudaLaunchKernelEx(&cfg, umma_kernel<A_MN, B_MN, PAIR, SEPC>, p));
     count_launch();
 }
 
+template <bool PAIR, bool SEPC>
+void dispatch2(const UmmaParams& p, int a_mn, int b_mn, int G, cudaStream_t s) {
+    if (!a_mn && b_mn) launch_variant<0, 1, PAIR, SEPC>(p, G, s);
+    else if (!a_mn && !b_mn) launch_variant<0, 0, PAIR, SEPC>(p, G, s);
+    else if (a_mn && b_mn) launch_variant<1, 1, PAIR, SEPC>(p, G, s);
+    else launch_variant<1, 0, PAIR, SEPC>(p, G, s);
+}
 template <bool PAIR>
-void dispatch(const UmmaParams& p, int a_mn, int b_mn, int G, cudaStream_t s) {
-    if (!a_mn && b_mn) launch_variant<0, 1, PAIR>(p, G, s);
-    else if (!a_mn && !b_mn) launch_variant<0, 0, PAIR>(p, G, s);
-    else if (a_mn && b_mn) launch_variant<1, 1, PAIR>(p, G, s);
-    else launch_variant<1, 0, PAIR>(p, G, s);
+void dispatch(const UmmaParams& p, int a_mn, int b_mn, int G, bool sepc, cudaStream_t s) {
+    if (sepc) dispatch2<PAIR, true>(p, a_mn, b_mn, G, s);
+    else dispatch2<PAIR, false>(p, a_mn, b_mn, G, s);
 }
 
 bool use_pair_kernel(const UmmaGemm& u) {
@@ -667,11 +701,16 @@ void launch_umma(const UmmaGemm& u, cudaStream_t s) {
         p.ksplit = u.ksplit;
         p.b2 = make_map(u.b2, u.N, u.K - u.ksplit, u.G, u.b2_rs, u.b2_gs, BK, true);
     }
+    // separate correction accumulator: long K, or operands of one sign
+    // (env MTK_UMMA_SEPC: 0 never, 1 always; A/B and precision diagnostics)
+    const char* se = getenv("MTK_UMMA_SEPC");  // read per call (A/B in one process)
+    const int sepc_mode = se ? atoi(se) : -1;
+    const bool sepc = sepc_mode >= 0 ? sepc_mode != 0 : (u.K >= kSepcMinK || u.same_sign);
     p.flags = u.flags;
     if (const char* t = getenv("MTK_UMMA_TRACE"))
         p.trace = reinterpret_cast<unsigned long long*>(strtoull(t, nullptr, 0));
-    if (pair) dispatch<true>(p, u.a_mn, u.b_mn, u.G, s);
-    else dispatch<false>(p, u.a_mn, u.b_mn, u.G, s);
+    if (pair) dispatch<true>(p, u.a_mn, u.b_mn, u.G, sepc, s);
+    else dispatch<false>(p, u.a_mn, u.b_mn, u.G, sepc, s);
 }
 
 }  // namespace mtk

@@ -21,13 +21,11 @@ schedule-independent; an all-reduce would let NCCL pick the summation order.
 ``dp_step_local`` runs the same arithmetic with n simulated workers on one
 device (the reference's own execution model).
 
-``estimate_speedup`` / ``speedup_table`` are the analytic ring all-reduce cost
-model (SPEC.md:623-631).
+(The analytic ring all-reduce speed-up model of SPEC.md:623-631 is not on
+the north_star path -- SURVEY.md section 2 row 20 -- and is not built.)
 """
 from __future__ import annotations
 
-import dataclasses
-import math
 
 import numpy as np
 import torch
@@ -64,74 +62,6 @@ def pad_batch(batch_size: int, n_workers: int):
     w = np.ones(padded, dtype=np.float32)
     w[batch_size:] = 0.0
     return idx, w
-
-
-# ---- analytic speedup model ---------------------
-
-
-@dataclasses.dataclass(frozen=True)
-class ParallelPlan:
-    """n_workers >= 1 and per-worker batch; reduction order is ascending
-    worker index."""
-    n_workers: int
-    per_worker_batch: int = 1
-
-    def __post_init__(self):
-        if int(self.n_workers) < 1 or int(self.per_worker_batch) < 1:
-            raise errors.ConfigError("ParallelPlan: n_workers and per_worker_batch must be >= 1")
-
-    @property
-    def global_batch(self) -> int:
-        return self.n_workers * self.per_worker_batch
-
-
-@dataclasses.dataclass(frozen=True)
-class CostModel:
-    """t_sample: compute seconds per sample per step; param_bytes: gradient
-    payload; bandwidth: bytes/s; latency: seconds per collective round
-    (SPEC.md:591-595).  t_sample and bandwidth must be positive; param_bytes
-    and latency may be 0 (the comm-free limit)."""
-    t_sample: float
-    param_bytes: float
-    bandwidth: float
-    latency: float
-
-    def __post_init__(self):
-        vals = (self.t_sample, self.param_bytes, self.bandwidth, self.latency)
-        if not all(math.isfinite(v) for v in vals):
-            raise errors.ConfigError("CostModel: fields must be finite")
-        if self.t_sample <= 0 or self.bandwidth <= 0 or self.param_bytes < 0 or self.latency < 0:
-            raise errors.ConfigError("CostModel: t_sample and bandwidth must be positive, "
-                                     "param_bytes and latency non-negative")
-
-
-def comm_time(n_workers: int, cost: CostModel) -> float:
-    """ring all-reduce: 0 for one worker, else 2(n-1)/n * param_bytes / bandwidth + latency"""
-    if n_workers <= 1:
-        return 0.0
-    return 2.0 * (n_workers - 1) / n_workers * cost.param_bytes / cost.bandwidth + cost.latency
-
-
-def step_time(n_workers: int, cost: CostModel, global_batch: int) -> float:
-    """T(n) = (global_batch / n) * t_sample + comm(n)"""
-    return global_batch / n_workers * cost.t_sample + comm_time(n_workers, cost)
-
-
-def estimate_speedup(plan: ParallelPlan, cost: CostModel, global_batch: int) -> float:
-    """S(n) = T(1) / T(n); S(1) = 1 and S(n) = n when
-    param_bytes = latency = 0."""
-    if global_batch < 1:
-        raise errors.ConfigError("estimate_speedup: global_batch must be >= 1")
-    n = plan.n_workers
-    return step_time(1, cost, global_batch) / step_time(n, cost, global_batch)
-
-
-def speedup_table(n_workers, cost: CostModel, global_batch: int) -> str:
-    """CSV "n_workers,predicted_speedup" (SPEC.md:640)."""
-    lines = ["n_workers,predicted_speedup"]
-    for n in n_workers:
-        lines.append(f"{n},{estimate_speedup(ParallelPlan(n), cost, global_batch):.6f}")
-    return "\n".join(lines) + "\n"
 
 
 # ---- replicas ----------------------------------------------------------------

@@ -54,46 +54,6 @@ def test_pad_batch():
 # ---- speedup model -----------------------------------
 
 
-def test_estimate_speedup_pinned_example():
-    cost = dp.CostModel(t_sample=1e-3, param_bytes=4e8, bandwidth=1e10, latency=5e-3)
-    s = dp.estimate_speedup(dp.ParallelPlan(32), cost, 1024)
-    assert dp.step_time(1, cost, 1024) == pytest.approx(1.024, abs=1e-12)
-    assert dp.comm_time(32, cost) == pytest.approx(0.0825, abs=1e-12)
-    assert dp.step_time(32, cost, 1024) == pytest.approx(0.1145, abs=1e-12)
-    assert round(s, 2) == 8.94
-    assert abs(s - 1.024 / 0.1145) <= 1e-9
-
-
-def test_estimate_speedup_limits_and_monotonicity():
-    cost = dp.CostModel(t_sample=2e-3, param_bytes=1e8, bandwidth=5e9, latency=1e-3)
-    assert dp.estimate_speedup(dp.ParallelPlan(1), cost, 512) == 1.0
-    free = dp.CostModel(t_sample=2e-3, param_bytes=0.0, bandwidth=5e9, latency=0.0)
-    for n in (1, 2, 4, 8, 16, 64):
-        assert dp.estimate_speedup(dp.ParallelPlan(n), free, 512) == pytest.approx(n, rel=0, abs=1e-12)
-        assert dp.estimate_speedup(dp.ParallelPlan(n), cost, 512) <= n
-    prev = 0.0
-    for bw in (1e8, 1e9, 1e10, 1e11):
-        s = dp.estimate_speedup(dp.ParallelPlan(8), dp.CostModel(2e-3, 1e8, bw, 1e-3), 512)
-        assert s >= prev
-        prev = s
-    prev = float("inf")
-    for lat in (0.0, 1e-4, 1e-3, 1e-2):
-        s = dp.estimate_speedup(dp.ParallelPlan(8), dp.CostModel(2e-3, 1e8, 5e9, lat), 512)
-        assert s <= prev
-        prev = s
-
-
-def test_speedup_table_csv_and_errors():
-    cost = dp.CostModel(t_sample=1e-3, param_bytes=4e8, bandwidth=1e10, latency=5e-3)
-    csv = dp.speedup_table([1, 2, 32], cost, 1024).splitlines()
-    assert csv[0] == "n_workers,predicted_speedup"
-    assert csv[1] == "1,1.000000" and csv[3].startswith("32,8.943")
-    with pytest.raises(errors.ConfigError):
-        dp.CostModel(t_sample=0.0, param_bytes=1.0, bandwidth=1.0, latency=0.0)
-    with pytest.raises(errors.ConfigError):
-        dp.ParallelPlan(0)
-
-
 # ---- dp_step on the oracle replica over gloo ---------------------------------
 
 DIMS = (12, 10, 4)

@@ -454,17 +454,39 @@ def test_attack_model_epoch_in_one_launch(ctx, monkeypatch, G, B, steps, weighte
                 assert rel(a, c) <= 1e-5, (g, k, rel(a, c))
 
 
+def _f64_backward(X, H1, H2, logits, y, W1, W2, dH_mmd, lam):
+    """TEST INFRASTRUCTURE: the reference backward of CE + lambda * MMD for a
+    3-layer MLP (tape.hpp:475-520 CE gradient, :349 strict ReLU mask,
+    :225-290 matmul backward, :153-171 injection) in numpy f64, evaluated on
+    the GPU's OWN forward activations -- so every dW / db kernel is checked on
+    identical inputs, ReLU masks included."""
+    B = X.shape[0]
+    z = logits - logits.max(1, keepdims=True)
+    P = np.exp(z) / np.exp(z).sum(1, keepdims=True)
+    dlog = P.copy()
+    dlog[np.arange(B), y] -= 1.0
+    dlog /= B
+    dZ2 = (dlog @ W2.T + lam * dH_mmd) * (H2 > 0)
+    dZ1 = (dZ2 @ W1.T) * (H1 > 0)
+    return [X.T @ dZ1, H1.T @ dZ2, H2.T @ dlog], [dZ1.sum(0), dZ2.sum(0), dlog.sum(0)]
+
+
 def test_step_bench_shape_c2_models_of_the_32_model_bank(ctx):
     """The bench's own step (bench.py: 1024-512-256-10, 512 src + 512 tgt,
     5-bandwidth MMD lambda = 1 on the 256-d hidden layer, SGD lr 0.01) on the
-    bench's 32-model bank; models 0, 17 and 31 against the f64 oracle.
+    bench's 32-model bank; models 0, 17 and 31 against f64.
 
-    Per kernel, on identical inputs (north_star 1e-5):
-      * logits and the MMD sample h (forward chain, 3 GEMMs);
-      * MMD^2 value and its gradient dH on the GPU's own h;
-      * every dW / db of the step, with the oracle's backward fed the GPU's
-        own injected gradient lambda * dH (the injection of tape.hpp:153-171).
-    Chained (the oracle's own h, its own MMD gradient): the same bound."""
+    Per kernel on identical inputs (north_star: 1e-5, max|d| / max|ref|):
+      * each forward GEMM on the GPU's own input activation: layer 0
+        (K = 1024), layer 1 (K = 512), the head (K = 256);
+      * MMD^2 value and gradient dH on the GPU's own h;
+      * every dW / db of the step against the f64 backward evaluated on the
+        GPU's own activations and injected MMD gradient.
+    Chained (the f64 oracle's own forward from the same X, W): reported, and
+    bounded looser, because the strict ReLU mask (tape.hpp:349) flips where
+    |z| is below the fp32-vs-f64 forward difference (~1e-6): each flipped
+    element moves one row's whole contribution to dW (the flip count is
+    printed)."""
     from paper_2011_09463_b200 import api
 
     dims = [1024, 512, 256, 10]
@@ -473,41 +495,62 @@ def test_step_bench_shape_c2_models_of_the_32_model_bank(ctx):
     X, y = inputs(G, B, dims[0], dims[-1], seed=1000, shift=0.5)
     Xd, yd = to_dev(X, y)
     logits, H = bank.forward(Xd, hidden=True)
-    before = {g: bank.get_params(g) for g in (0, 17, 31)}
+    picks = (0, 17, 31)
+    before = {g: bank.get_params(g) for g in picks}
+    # the first two layers as their own bank: its hidden output is H1 and its
+    # (linear) output is Z2, from the same tcgen05 GEMMs
+    trunk = api.Bank(ctx, G, dims[:3])
+    for g in range(G):
+        W, b = bank.get_params(g)
+        trunk.set_params(g, W[:2], b[:2])
+    Z2, H1 = trunk.forward(Xd, hidden=True)
     bank.keep_grads(True)
     loss, mmd = bank.train_step(Xd, yd, lr=0.01, src_rows=src, mmd_lambda=1.0)
-    worst = {}
+    worst, chained, flips = {}, {}, 0
+
+    def put(d, k, v):
+        d[k] = max(d.get(k, 0.0), v)
+
     for g, (W, b) in before.items():
         Xg = X[g].astype(np.float64)
-        lo, Ho = po.mlp_forward(dims, W, b, Xg)
-        worst["logits"] = max(worst.get("logits", 0), rel(logits[g].cpu().numpy(), lo))
-        worst["h"] = max(worst.get("h", 0), rel(H[g].cpu().numpy(), Ho))
-        Hg = H[g].double().cpu().numpy()
-        v, _, ogs, ogt = po.mmd_gaussian(Hg[:src], Hg[src:])
+        h1 = H1[g].double().cpu().numpy()
+        z2 = Z2[g].double().cpu().numpy()
+        h2 = H[g].double().cpu().numpy()
+        lg = logits[g].double().cpu().numpy()
+        put(worst, "fwd0 (K=1024)", rel(h1, np.maximum(Xg @ W[0] + b[0], 0.0)))
+        put(worst, "fwd1 (K=512)", rel(z2, h1 @ W[1] + b[1]))
+        put(worst, "fwd2 head (K=256)", rel(lg, h2 @ W[2] + b[2]))
+        v, _, ogs, ogt = po.mmd_gaussian(h2[:src], h2[src:])
         gv, _, ggs, ggt = api.mmd_gaussian(ctx, H[g, :src].contiguous(), H[g, src:].contiguous())
-        worst["mmd_value"] = max(worst.get("mmd_value", 0), rel(mmd[g], v), rel(gv, v))
+        put(worst, "mmd value", max(rel(mmd[g], v), rel(gv, v)))
         dH_gpu = np.concatenate([ggs.cpu().numpy(), ggt.cpu().numpy()]).astype(np.float64)
-        worst["dH"] = max(worst.get("dH", 0), rel(dH_gpu, np.concatenate([ogs, ogt])))
-        # identical inputs: the oracle's backward with the GPU's injected gradient
-        Wc, bc = [x.copy() for x in W], [x.copy() for x in b]
-        lo_, gW, gb = po.mlp_train_step(dims, Wc, bc, Xg, y[g], src_rows=src, lr=0.01, dH=dH_gpu,
-                                        want_grads=True)
-        worst["loss"] = max(worst.get("loss", 0), rel(loss[g], lo_))
+        put(worst, "mmd dH", rel(dH_gpu, np.concatenate([ogs, ogt])))
+        gW, gb = _f64_backward(Xg, h1, h2, lg, y[g], W[1], W[2], dH_gpu, 1.0)
         dW, db = bank.get_grads(g)
-        Wn, bn = bank.get_params(g)
         for i in range(3):
-            worst[f"dW{i}"] = max(worst.get(f"dW{i}", 0), rel(dW[i], gW[i]))
-            worst[f"db{i}"] = max(worst.get(f"db{i}", 0), rel(db[i], gb[i]))
-            worst[f"W{i}"] = max(worst.get(f"W{i}", 0), rel(Wn[i], Wc[i]))
-        # chained: the oracle's own h and MMD gradient
+            put(worst, f"dW{i}", rel(dW[i], gW[i]))
+            put(worst, f"db{i}", rel(db[i], gb[i]))
+        Wn, _ = bank.get_params(g)
+        for i in range(3):  # the SGD update itself: W - lr * dW (fp32 FMA)
+            put(worst, f"W{i} update", rel(Wn[i], W[i] - 0.01 * dW[i]))
+        # chained: the f64 oracle's own forward / MMD / backward from X, W
+        lo, Ho = po.mlp_forward(dims, W, b, Xg)
+        put(chained, "logits", rel(lg, lo))
+        put(chained, "h", rel(h2, Ho))
         _, _, cgs, cgt = po.mmd_gaussian(Ho[:src], Ho[src:])
-        Wc2, bc2 = [x.copy() for x in W], [x.copy() for x in b]
-        _, cW, cb = po.mlp_train_step(dims, Wc2, bc2, Xg, y[g], src_rows=src, lr=0.01,
-                                      dH=np.concatenate([cgs, cgt]), want_grads=True)
+        Wc, bc = [x.copy() for x in W], [x.copy() for x in b]
+        lo_, cW, cb = po.mlp_train_step(dims, Wc, bc, Xg, y[g], src_rows=src, lr=0.01,
+                                        dH=np.concatenate([cgs, cgt]), want_grads=True)
+        put(chained, "loss", rel(loss[g], lo_))
         for i in range(3):
-            worst[f"chained_dW{i}"] = max(worst.get(f"chained_dW{i}", 0), rel(dW[i], cW[i]),
-                                          rel(db[i], cb[i]))
-    print("bench-shape C2 parity (max |d| / max |ref| per tensor):",
-          {k: f"{v:.2e}" for k, v in worst.items()})
+            put(chained, f"dW{i}", rel(dW[i], cW[i]))
+            put(chained, f"db{i}", rel(db[i], cb[i]))
+        h1o = np.maximum(Xg @ W[0] + b[0], 0.0)
+        flips += int(((h1 > 0) != (h1o > 0)).sum() + ((h2 > 0) != (Ho > 0)).sum())
+    print("bench-shape C2, per kernel on identical inputs:", {k: f"{v:.2e}" for k, v in worst.items()})
+    print(f"bench-shape C2, chained vs the oracle's own forward ({flips} ReLU mask flips over "
+          f"{len(picks)} models):", {k: f"{v:.2e}" for k, v in chained.items()})
     for k, v in worst.items():
         assert v <= TOL, (k, v, worst)
+    assert chained["logits"] <= 2 * TOL and chained["h"] <= 2 * TOL and chained["loss"] <= TOL
+    assert max(v for k, v in chained.items() if k.startswith(("dW", "db"))) <= 1e-2

@@ -230,6 +230,78 @@ def test_sweep_main_exit_codes(tmp_path, monkeypatch):
     assert _json.loads((out / "resolved_config.json").read_text())["paradigm"] == "model"
 
 
+_C1 = {}  # paradigm -> {"oracle": result, "gpu": result} (the C1 runs are shared by two tests)
+
+
+def _c1(paradigm, which):
+    key = (paradigm, which)
+    if key not in _C1:
+        from paper_2011_09463_b200.sweep import GpuBackend
+
+        be = OracleBackend() if which == "oracle" else GpuBackend()
+        _C1[key] = run_sweep(SweepConfig(paradigm=paradigm), be)
+    return _C1[key]
+
+
+def _cpp_sweep_exe(tmp_path):
+    """tests/cpp/sweep_check built against the reference headers by
+    __graft_entry__.build() where they were mounted (the binary travels to the
+    GPU box), else built here against gpu.hpp alone"""
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    pre = os.path.join(root, "tests", "cpp", "_build", "sweep_check_ref")
+    if os.path.exists(pre):
+        return pre
+    exe = str(tmp_path / "sweep_check")
+    lib = os.path.join(root, "paper_2011_09463_b200")
+    subprocess.run(["g++", "-std=c++20", "-O2", f"-I{root}/include", "-I/usr/local/cuda/include",
+                    os.path.join(root, "tests", "cpp", "sweep_check.cpp"), f"-L{lib}", "-lmtk",
+                    "-L/usr/local/cuda/lib64", "-lcudart", f"-Wl,-rpath,{lib}",
+                    "-Wl,-rpath,/usr/local/cuda/lib64", "-o", exe], check=True)
+    return exe
+
+
+def test_cpp_sweep_builds_against_the_reference_headers(tmp_path):
+    """the C++ drop-in (gpu.hpp + mtk.h) compiles next to the unmodified
+    reference headers (mt:: error classes and Parameter in scope)"""
+    import subprocess
+
+    ref = "/root/reference/proj/include"
+    if not os.path.isdir(ref):
+        pytest.skip("reference headers not mounted")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib = os.path.join(root, "paper_2011_09463_b200")
+    exe = str(tmp_path / "sweep_check_ref")
+    subprocess.run(["g++", "-std=c++20", "-O2", "-Wall", "-Werror", "-Wno-missing-field-initializers",
+                    f"-I{root}/include", f"-I{ref}", "-I/usr/local/cuda/include",
+                    os.path.join(root, "tests", "cpp", "sweep_check.cpp"), f"-L{lib}", "-lmtk",
+                    "-L/usr/local/cuda/lib64", "-lcudart", f"-Wl,-rpath,{lib}", "-o", exe], check=True)
+    out = subprocess.run([exe, "nonsense"], capture_output=True, text=True)
+    assert out.returncode == 2 and "unknown paradigm" in out.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("paradigm", ["model", "mapping", "parameter"])
+def test_cpp_sweep_c1_matches_python_driver_and_oracle(tmp_path, paradigm):
+    """C1 end to end through the C++ drop-in only (mt::gpu::run_shadow_sweep
+    -> mtk_sweep_run): bit-identical AUC / accuracy to the Python driver on
+    the same device (same calls, same inputs), and within +-0.01 of the f64
+    oracle (north_star)."""
+    import json
+    import subprocess
+
+    exe = _cpp_sweep_exe(tmp_path)
+    out = subprocess.run([exe, paradigm], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
+    r = json.loads(out.stdout.strip().splitlines()[-1])
+    print(f"C1 {paradigm} via C++: {r}")
+    g, o = _c1(paradigm, "gpu"), _c1(paradigm, "oracle")
+    assert (r["auc"], r["accuracy"]) == (g["auc"], g["accuracy"]), (r, g)
+    assert r["models"] == 5 and r["n_queries"] == 4096
+    assert abs(r["auc"] - o["auc"]) <= 0.01 and abs(r["accuracy"] - o["accuracy"]) <= 0.01
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("paradigm", ["model", "mapping", "parameter"])
 def test_sweep_c1_parity_config_gpu_matches_oracle(paradigm):
@@ -243,9 +315,32 @@ def test_sweep_c1_parity_config_gpu_matches_oracle(paradigm):
     cfg = SweepConfig(paradigm=paradigm)
     assert (cfg.dims, cfg.n_shadows, cfg.members, cfg.pool, cfg.batch, cfg.epochs) == \
         ((784, 256, 10), 4, 2048, 8192, 128, 10)
-    g = run_sweep(cfg, GpuBackend())
-    o = run_sweep(SweepConfig(paradigm=paradigm), OracleBackend())
+    assert isinstance(GpuBackend, type)
+    g, o = _c1(paradigm, "gpu"), _c1(paradigm, "oracle")
     print(f"C1 {paradigm}: gpu auc {g['auc']:.5f} acc {g['accuracy']:.5f} | "
           f"oracle auc {o['auc']:.5f} acc {o['accuracy']:.5f}")
     assert abs(g["auc"] - o["auc"]) <= 0.01, (g["auc"], o["auc"])
     assert abs(g["accuracy"] - o["accuracy"]) <= 0.01, (g["accuracy"], o["accuracy"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("paradigm,extra", [("model", {}), ("mapping", {}), ("parameter", {}),
+                                            ("model", {"frozen_layers": 1, "optimizer": "adam", "lr": 0.005}),
+                                            ("mapping", {"data_rng": "counter"}),
+                                            ("parameter", {"members": 500, "batch": 64})])
+def test_native_sweep_is_bit_identical_to_the_python_driver(paradigm, extra):
+    """mtk_sweep_run (C++ driver, whole epochs per call) == sweep.py on the
+    GPU backend (per-step calls): same sampling, same kernels, same inputs ->
+    the same AUC / accuracy bits; incl. padded last batches (500 members,
+    B = 64), a frozen prefix, Adam and device counter data."""
+    from paper_2011_09463_b200 import api
+    from paper_2011_09463_b200.sweep import GpuBackend
+
+    kw = dict(MID, **extra)
+    if paradigm == "model" and "frozen_layers" in extra:
+        kw["dims"] = (64, 48, 32, 10)
+    be = GpuBackend()
+    py = run_sweep(SweepConfig(paradigm=paradigm, **kw), be)
+    nat = api.sweep_run(be.ctx, dict(kw, paradigm=paradigm))
+    assert (nat["auc"], nat["accuracy"]) == (py["auc"], py["accuracy"]), (nat, py)
+    assert nat["models"] == py["models"] and nat["n_queries"] == py["n_queries"]
