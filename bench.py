@@ -371,10 +371,13 @@ def kernel_traffic(phase, key="phases"):
 # ----------------------------------------------------------------------------- C4 MMD
 def measure_c4(args, world, rank, local, steps, warmup, cpu=True):
     """configs[3]: multi-bandwidth MMD^2 + gradient of Xs [65536, 512] vs Xt
-    [8192, 512].  One step = the full evaluation.  1 GPU: the materialised-W
-    path (each unordered 128x128 tile pair once, W = 21.7 GB, V = W.Z as a
-    GEMM).  N GPUs: pair rows sharded over the ranks (fused pair kernel),
-    raw sums combined in ascending rank order."""
+    [8192, 512].  One step = the full evaluation on the materialised-W path
+    (each unordered 128x128 tile pair once, W = 21.7 GB, V = W.Z as a GEMM).
+    N GPUs: rank r owns an equal range of 128-row tiles
+    (mtk_mmd_gaussian_tiles: the tile pairs touching its rows, its rows of W,
+    V and the gradient); the [T, 3] tile-row kernel sums are all-gathered
+    over NCCL inside the timed region and combined in ascending tile order --
+    the gradients and the value are bit-identical to one GPU's."""
     import torch
 
     from paper_2011_09463_b200 import api
@@ -388,15 +391,21 @@ def measure_c4(args, world, rank, local, steps, warmup, cpu=True):
     gZ = torch.empty_like(Z)
     gXs, gXt = gZ[:C4_M], gZ[C4_M:]
     beta = api.mmd_beta(ctx, Xs, Xt)
-    r0, r1 = rank * Nt // world, (rank + 1) * Nt // world
+    lo, hi = api.mmd_tile_ranges(C4_M, C4_N, world)[rank]
+    r0, r1 = lo * api.MMD_TILE, min(Nt, hi * api.MMD_TILE)
     full = world == 1
     out = {}
+    parts = torch.empty((world, -(-Nt // api.MMD_TILE), 3), dtype=torch.float64, device="cuda")
 
     def evaluate():
         if full:
             out["v"] = api.mmd_gaussian(ctx, Xs, Xt, beta=beta)[0]
         else:
-            api.mmd_gaussian_rows(ctx, Xs, Xt, beta, r0, r1, gXs=gXs, gXt=gXt)
+            import torch.distributed as dist
+
+            part = torch.from_numpy(api.mmd_gaussian_tiles(ctx, Z, C4_M, beta, lo, hi, gZ)).cuda()
+            dist.all_gather_into_tensor(parts, part)  # [world, T, 3], one owner per tile row
+            out["v"] = api.mmd_value_from_tiles(parts.sum(0).cpu().numpy(), C4_M, C4_N)
 
     for _ in range(warmup):
         evaluate()
@@ -416,7 +425,7 @@ def measure_c4(args, world, rank, local, steps, warmup, cpu=True):
             gh[:C4_M].copy_(gs, non_blocking=True)
             gh[C4_M:].copy_(gt, non_blocking=True)
         else:
-            api.mmd_gaussian_rows(ctx, Xs, Xt, beta, r0, r1, gXs=gXs, gXt=gXt)
+            evaluate()
             gh[r0:r1].copy_(gZ[r0:r1], non_blocking=True)
 
     e2e_step()
@@ -424,7 +433,7 @@ def measure_c4(args, world, rank, local, steps, warmup, cpu=True):
     e2e_steps = max(1, steps // 2)
     peak, bf16, src = fp32acc_peak()
     pairs_s = C4_PAIRS * steps / (ms / 1000.0)
-    achieved = pairs_s * 4 * C4_D / 1e12
+    achieved = pairs_s / world * 4 * C4_D / 1e12  # per GPU
     traffic, tsrc = kernel_traffic("c4", key="workloads")
     res = {
         "metric": "MMD kernel-pairs/s", "value": pairs_s, "unit": "pairs/s", "n_gpus": world,
@@ -432,15 +441,18 @@ def measure_c4(args, world, rank, local, steps, warmup, cpu=True):
         "scaling": "strong", "dtype": "f32",
         "config": {"workload": "C4 MMD stress: Xs 65536 x 512 vs Xt 8192 x 512 (N(0,1), N(0.1,1)), "
                                "5-bandwidth Gaussian MMD^2 + gradient"
-                               + ("" if full else ", pair rows sharded over ranks"),
-                   "unique_pairs": C4_PAIRS, "parallelism": f"rows{world}",
-                   "path": "materialised W (mmd_w + wsum + V GEMM)" if full else "fused pair kernel, row shards",
+                               + ("" if full else ", 128-row tiles sharded over ranks"),
+                   "unique_pairs": C4_PAIRS, "parallelism": f"tiles{world}", "value": out.get("v"),
+                   "path": "materialised W (mmd_w + wsum + V GEMM)" + (
+                       "" if full else f"; rank tiles [{lo}, {hi}): its tile pairs (cross-rank pairs on both "
+                       "ranks, each its own rows), its rows of V; [T,3] partials all-gathered (NCCL)"),
                    "l2": "inputs 151 MB + tf32 planes + 21.7 GB of W > 126 MB L2"},
-        "roofline": {"bound": "tensor", "kernel": "mmd_w + V GEMM (+prep)" if full else "mmd_tc_kernel",
+        "roofline": {"bound": "tensor", "kernel": "mmd_w + V GEMM (+prep)",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                      "traffic": traffic,
                      "peak_note": f"algorithmic 4d flop per unique pair; 3xTF32 peak = {src} bf16 {bf16} / 6"
-                                  + ("" if full else "; row shards evaluate ordered pairs (2x the work)"),
+                                  + ("" if full else f"; per rank {2 - 1 / world:.3f}x the ideal share of "
+                                     "pass-1 tile pairs (cross-rank pairs evaluated twice)"),
                      "traffic_note": f"DRAM bytes per evaluation, profiles/{tsrc}" if tsrc else
                      "no ncu capture of this workload committed"},
         "e2e": {"value": C4_PAIRS * e2e_steps / (e2e_ms / 1000.0), "unit": "pairs/s",

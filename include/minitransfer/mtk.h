@@ -256,6 +256,23 @@ int mtk_mmd_gaussian_rows(mtk_ctx* ctx, const float* Xs, int64_t m, const float*
                           int64_t row_end, double* partial_host, float* gXs, float* gXt);
 int mtk_mmd_beta(mtk_ctx* ctx, const float* Xs, int64_t m, const float* Xt, int64_t n, int d,
                  double* beta_host);
+/* Multi-GPU form on the materialised kernel matrix: the
+ * rank owning the 128-row tiles [tile_begin, tile_end) of [Xs; Xt] (Xs, Xt
+ * views of one [m + n, d] block, the gradients likewise) evaluates every
+ * tile pair touching its tiles -- pairs of two of its tiles once, pairs with
+ * another rank's tile by both ranks, each keeping only its own rows of W --
+ * and writes the gradients of its rows.  tile_partials_host [T][3] (T =
+ * ceil((m + n) / 128)) receives the kernel sums (ss, tt, st) of its tile
+ * rows (zeros elsewhere).  Per element the arithmetic is the one-rank
+ * call's, so gradients are bit-identical to mtk_mmd_gaussian, and so is the
+ * value from mtk_mmd_value_from_tile_partials over the ranks' partials
+ * (ascending tile rows, the one-rank finish's order).  Equal tile ranges
+ * balance the ranks (each does s T - s^2 / 2 tile pairs for s tiles).     */
+int mtk_mmd_gaussian_tiles(mtk_ctx* ctx, const float* Xs, int64_t m, const float* Xt, int64_t n, int d,
+                           const double* mult_host, int nb, double beta, int64_t tile_begin,
+                           int64_t tile_end, double* tile_partials_host, float* gXs, float* gXt);
+int mtk_mmd_value_from_tile_partials(const double* tile_partials_host, int64_t T, int64_t m, int64_t n,
+                                     double* value_host);
 
 /* ---- attack stage -------------------------------------------------------- */
 /* Tape::softmax semantics (tape.hpp:433-464), fp32 out */

@@ -141,6 +141,9 @@ SIGNATURES = {
     "mtk_posterior_column": (C.c_int, [_vp, _vp, C.c_int64, C.c_int, C.c_int, _vp]),
     "mtk_auc": (C.c_int, [_vp, _vp, _vp, C.c_int64, _dp, _dp]),
     "mtk_attack_auc": (C.c_int, [_vp, _vp, C.c_int64, C.c_int, _vp, _dp, _dp, _vp]),
+    "mtk_mmd_gaussian_tiles": (C.c_int, [_vp, _vp, C.c_int64, _vp, C.c_int64, C.c_int, _dp, C.c_int,
+                                         C.c_double, C.c_int64, C.c_int64, _dp, _vp, _vp]),
+    "mtk_mmd_value_from_tile_partials": (C.c_int, [_dp, C.c_int64, C.c_int64, C.c_int64, _dp]),
     "mtk_comm_unique_id": (C.c_int, [_vp]),
     "mtk_comm_init": (C.c_int, [C.c_int, C.c_int, _vp, C.POINTER(_vp)]),
     "mtk_comm_destroy": (C.c_int, [_vp]),

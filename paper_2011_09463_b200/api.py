@@ -456,6 +456,45 @@ def mmd_gaussian_rows(ctx: Context, Xs, Xt, beta: float, row_begin: int, row_end
     return part
 
 
+MMD_TILE = 128
+
+
+def mmd_tile_ranges(m: int, n: int, world: int):
+    """Equal 128-row tile ranges over [Xs; Xt], one per rank: with the
+    materialised-W sharding every rank then does s*T - s^2/2 tile pairs
+    (mtk_mmd_gaussian_tiles), i.e. the same work."""
+    T = -(-(m + n) // MMD_TILE)
+    return [(r * T // world, (r + 1) * T // world) for r in range(world)]
+
+
+def mmd_gaussian_tiles(ctx: Context, Z: torch.Tensor, m: int, beta: float, tile_begin: int, tile_end: int,
+                       gZ: torch.Tensor, mult=None) -> np.ndarray:
+    """This rank's share of the materialised-W MMD (mtk_mmd_gaussian_tiles):
+    Z = [Xs; Xt] one [m + n, d] block, gZ its gradient block (rows of tiles
+    [tile_begin, tile_end) written).  Returns the [T, 3] kernel-sum partials
+    (zeros outside the range); combine the ranks' with mmd_value_from_tiles."""
+    N, d = Z.shape
+    n = N - m
+    mu = _mult_arr(mult)
+    T = -(-N // MMD_TILE)
+    part = np.zeros((T, 3))
+    errors.check(lib.mtk_mmd_gaussian_tiles(ctx.h, _ptr(Z), m, C.c_void_p(Z.data_ptr() + m * d * 4), n, d,
+                                            mu.ctypes.data_as(_dp), len(mu), beta, tile_begin, tile_end,
+                                            part.ctypes.data_as(_dp), _ptr(gZ),
+                                            C.c_void_p(gZ.data_ptr() + m * d * 4)), "mmd_gaussian_tiles")
+    return part
+
+
+def mmd_value_from_tiles(partials: np.ndarray, m: int, n: int) -> float:
+    """MMD^2 from [T, 3] tile-row kernel sums (the ranks' partials added
+    elementwise: each tile row has one owner), in the one-rank finish order"""
+    p = np.ascontiguousarray(partials, dtype=np.float64)
+    v = C.c_double()
+    errors.check(lib.mtk_mmd_value_from_tile_partials(p.ctypes.data_as(_dp), p.shape[0], m, n, C.byref(v)),
+                 "mmd_value_from_tile_partials")
+    return v.value
+
+
 def mmd_beta(ctx: Context, Xs, Xt) -> float:
     m, d = Xs.shape
     out = C.c_double()

@@ -384,6 +384,53 @@ int mtk_mmd_gaussian_rows(mtk_ctx* c, const float* Xs, int64_t m, const float* X
     });
 }
 
+int mtk_mmd_gaussian_tiles(mtk_ctx* c, const float* Xs, int64_t m, const float* Xt, int64_t n, int d,
+                           const double* mult, int nb, double beta, int64_t tile_begin, int64_t tile_end,
+                           double* tile_partials_host, float* gXs, float* gXt) {
+    return guard_on(c, [&] {
+        MmdArgs a = mmd_args(c, Xs, m, Xt, n, d, mult, nb);
+        need(beta > 0, MTK_VALUE_ERROR, "mmd_tiles: beta must be given (> 0)");
+        need(tile_partials_host && gXs && gXt, MTK_VALUE_ERROR, "mmd_tiles: null argument");
+        const int64_t T = (m + n + kMmdTileRows - 1) / kMmdTileRows;
+        need(tile_begin >= 0 && tile_begin < tile_end && tile_end <= T, MTK_SHAPE_ERROR,
+             "mmd_tiles: tile range outside [0, ceil((m + n) / 128))");
+        a.gXs = gXs;
+        a.gXt = gXt;
+        a.tile_begin = tile_begin;
+        a.tile_end = tile_end;
+        need(a.tc && mmd_w_path(a), MTK_CONFIG_ERROR,
+             "mmd_tiles: needs the materialised-W path (Xs, Xt and the gradients each one [m + n, d] "
+             "block, d % 4 == 0, d >= 32)");
+        const size_t part = (size_t)T * 3 * sizeof(double);
+        double* sc = c->scratch(part + 64 * sizeof(double));
+        double* beta_d = sc;
+        double* part_d = sc + 64;
+        MTK_CUDA(cudaMemcpyAsync(beta_d, &beta, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        MTK_CUDA(cudaMemsetAsync(part_d, 0, part, c->stream));
+        a.beta = beta_d;
+        a.partial = part_d;
+        void* zs = c->big(mmd_tc_scratch_bytes(a));
+        launch_mmd_tc(a, zs, c->stream);
+        after_launch(*c, 1);
+        MTK_CUDA(cudaMemcpyAsync(tile_partials_host, part_d, part, cudaMemcpyDeviceToHost, c->stream));
+        c->check_flags();
+    });
+}
+
+int mtk_mmd_value_from_tile_partials(const double* partials, int64_t T, int64_t m, int64_t n,
+                                     double* value_host) {
+    return guard([&] {
+        need(partials && value_host && T >= 1 && m >= 1 && n >= 1, MTK_VALUE_ERROR, "mmd_value: bad argument");
+        // mmd_finish_kernel's order and formula, in fp64 (the host is built
+        // with -ffp-contract=off): ascending tile rows, then the V-statistic
+        double s[3] = {0.0, 0.0, 0.0};
+        for (int64_t b = 0; b < T; ++b)
+            for (int q = 0; q < 3; ++q) s[q] += partials[b * 3 + q];
+        const double md = (double)m, nd = (double)n;
+        *value_host = s[0] / (md * md) + s[1] / (nd * nd) - 2.0 * s[2] / (md * nd);
+    });
+}
+
 // ---- attack stage ----------------------------------------------------------
 int mtk_gather_rows(mtk_ctx* c, const void* src, int64_t src_rows, int d, const int64_t* idx, int G,
                     int nb, void* out, int out_rows, int row0) {

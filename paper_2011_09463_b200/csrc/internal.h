@@ -337,6 +337,9 @@ struct MmdArgs {
     const double* beta = nullptr;   // [G] device (detached)
     double* beta_out = nullptr;     // tc path: compute beta here (fused into the prep pass); == beta
     long long row_begin = 0, row_end = -1;  // concatenated-row range (all groups)
+    // materialised-W path, one group: this rank owns the 128-row tiles
+    // [tile_begin, tile_end) (-1: all); see mtk_mmd_gaussian_tiles
+    long long tile_begin = 0, tile_end = -1;
     double* partial = nullptr;      // [G, nblocks_per_group, 3] device
     float* gXs = nullptr;           // optional, layout as Xs, scaled by grad_scale
     long long gs_gs = 0;
@@ -365,6 +368,9 @@ size_t mmd_tc_scratch_bytes(const MmdArgs& a);
 // true when launch_mmd_tc fuses the head DX described by a.hd_* (materialised-W
 // path, hd_n <= 32, (m + n) % 32 == 0)
 bool mmd_head_fusable(const MmdArgs& a);
+// true when launch_mmd_tc takes the materialised-W path for these arguments
+bool mmd_w_path(const MmdArgs& a);
+constexpr int kMmdTileRows = 128;  // W-path tile (mtk_mmd_gaussian_tiles granularity)
 // stages: 1 = prep pass (tf32 planes, norms, fused beta), 2 = the pair kernel;
 // the same scratch must be passed to both.
 constexpr int kMmdPrep = 1, kMmdPairs = 2;

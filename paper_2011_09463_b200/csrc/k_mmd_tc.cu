@@ -726,7 +726,11 @@ struct MmdWParams {
     int d, nb, geo5;
     float mult[8];
     int T, npairs, G;
-    float* W;                  // [G][N][ldw]
+    // owned tile rows [ta, tb) (all: 0, T): the items are the tile pairs that
+    // touch them -- list A, pairs (I >= ta in range, J >= I), contiguous in the
+    // upper-triangle order from pair index pa; list B, pairs (I < ta, J in range)
+    int ta, tb, pa, nA, nB;
+    float* W;                  // [G][N][ldw] (rows outside [ta, tb) * WT never written)
     long long ldw;             // row stride of W (N, or N + 32 with the head block)
     float* rpart;              // [G][T][T][4][WT]: row sums of block (I, J), per column quarter
     float* cpart;              // [G][T][T][4][WT]: column sums of block (I, J) (I < J), per row quarter
@@ -737,6 +741,20 @@ struct MmdWParams {
 
 // unordered tile pair p -> (I, J), I <= J, row-major over the upper triangle
 // (row I starts at S(I) = I*T - I*(I-1)/2): closed form + integer fix-up
+__device__ __forceinline__ void pair_of(int p, int T, int& I, int& J);
+// work item of one group -> (I, J, pair index) over lists A then B (above)
+__device__ __forceinline__ void item_pair(const MmdWParams& p, int k, int& I, int& J, int& pidx) {
+    if (k < p.nA) {
+        pidx = p.pa + k;
+        pair_of(pidx, p.T, I, J);
+        return;
+    }
+    k -= p.nA;
+    const int w = p.tb - p.ta;
+    I = k / w;
+    J = p.ta + k % w;
+    pidx = (int)((long long)I * p.T - (long long)I * (I - 1) / 2) + (J - I);
+}
 __device__ __forceinline__ void pair_of(int p, int T, int& I, int& J) {
     const double b = 2.0 * T + 1.0;
     int i = (int)((b - sqrt(b * b - 8.0 * (double)p)) * 0.5);
@@ -791,7 +809,8 @@ __global__ void __launch_bounds__(W_THREADS, 1) mmd_w_kernel(const __grid_consta
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long N = p.m + p.n;
     const int nkc = (p.d + KC - 1) / KC;
-    const int total = p.G * p.npairs;
+    const int nloc = p.nA + p.nB;  // items per group
+    const int total = p.G * nloc;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&p.zk_hi);
@@ -820,9 +839,9 @@ __global__ void __launch_bounds__(W_THREADS, 1) mmd_w_kernel(const __grid_consta
         // ---------------- TMA producer ----------------
         int st = 0;
         for (int item = blockIdx.x; item < total; item += gridDim.x) {
-            const int g = item / p.npairs;
-            int I, J;
-            pair_of(item % p.npairs, p.T, I, J);
+            const int g = item / nloc;
+            int I, J, pidx_;
+            item_pair(p, item % nloc, I, J, pidx_);
             const int i0 = I * WT, j0 = J * WT;
             for (int kc = 0; kc < nkc; ++kc, ++st) {
                 const int s = st % W_STAGES;
@@ -893,11 +912,14 @@ __global__ void __launch_bounds__(W_THREADS, 1) mmd_w_kernel(const __grid_consta
         int lt = 0;
         bool bad = false;
         for (int item = blockIdx.x; item < total; item += gridDim.x, ++lt) {
-            const int g = item / p.npairs;
-            const int pidx = item % p.npairs;
-            int I, J;
-            pair_of(pidx, p.T, I, J);
+            const int g = item / nloc;
+            int I, J, pidx;
+            item_pair(p, item % nloc, I, J, pidx);
             const bool diag = I == J;
+            // a pair whose two tiles belong to different ranks is evaluated by
+            // both; each keeps only the half in its own rows (and only the
+            // owner of I counts its kernel sums)
+            const bool own_i = I >= p.ta && I < p.tb, own_j = J >= p.ta && J < p.tb;
             const int gi = I * WT + r;
             const bool row_ok = gi < N;
             const bool si = gi < p.m;
@@ -1053,7 +1075,7 @@ __global__ void __launch_bounds__(W_THREADS, 1) mmd_w_kernel(const __grid_consta
                 // as coalesced 128-B row segments after the last chunk
 #pragma unroll
                 for (int c = 0; c < 8; ++c) tw[lane * W_TILE_LD + (ch - 4 * h) * 8 + c] = wv[c];
-                if (!diag) {
+                if (!diag && own_j) {
                     // (j, i): lanes are consecutive i -> one 128-B row segment per store
                     float* dt = Wg + ((long long)jb * ldw + gi);
                     if (p.diag == 3 || p.diag == 4) {
@@ -1076,7 +1098,7 @@ __global__ void __launch_bounds__(W_THREADS, 1) mmd_w_kernel(const __grid_consta
             tc_fence_before();
             mbar_arrive(&acc_empty[buf]);
             __syncwarp();
-            if (p.diag != 3 && p.diag != 5) {
+            if (p.diag != 3 && p.diag != 5 && own_i) {
                 const int jc = J * WT + 32 * h + lane;
                 const int r0 = I * WT + 32 * q;
                 const int nr = min(32, (int)N - r0);
@@ -1091,6 +1113,7 @@ __global__ void __launch_bounds__(W_THREADS, 1) mmd_w_kernel(const __grid_consta
             }
             __syncwarp();
 
+            if (!own_i) continue;  // the (j, i) half, column sums: done above
             p.rpart[((((long long)g * p.T + I) * p.T + J) * 4 + h) * WT + r] = rowp;
             // this warp's kernel sums: fixed butterfly over the 32 rows, fp64
             double kd[3] = {(double)kss, (double)ktt, (double)kst};
@@ -1136,13 +1159,16 @@ struct WsumHead {  // the fused head DX's extra K block (hn = 0: none)
     long long ldw;
     float* bx;         // [G][kHeadK][d]
 };
+// Rows: the owned rows [r0, r0 + NR) of every group (all rows unless the
+// call is tile-sharded); tile rows: [ta, ta + NT) -> blocks of the kernel sums.
 __global__ void __launch_bounds__(WSUM_THREADS) mmd_wsum_kernel(const float* rpart, const float* cpart,
                                                                 const double* kpart, int G, long long N,
                                                                 int T, int npairs, float* wsum,
-                                                                double* partial, WsumHead h) {
+                                                                double* partial, WsumHead h, long long r0,
+                                                                long long NR, int ta, int NT) {
     __shared__ double jsum[3][WSUM_THREADS / 3 + 1];
-    const long long nbw = ((long long)G * N + WSUM_THREADS - 1) / WSUM_THREADS;
-    if (blockIdx.x >= nbw + (long long)G * T) {  // head block B rows: -W_head^T / lambda
+    const long long nbw = ((long long)G * NR + WSUM_THREADS - 1) / WSUM_THREADS;
+    if (blockIdx.x >= nbw + (long long)G * NT) {  // head block B rows: -W_head^T / lambda
         const long long e = (blockIdx.x - nbw - (long long)G * T) * WSUM_THREADS + threadIdx.x;
         const long long per = (long long)kHeadK * h.d;
         if (e >= G * per) return;
@@ -1151,10 +1177,11 @@ __global__ void __launch_bounds__(WSUM_THREADS) mmd_wsum_kernel(const float* rpa
         return;
     }
     if (blockIdx.x < nbw) {
-        const long long t = blockIdx.x * (long long)WSUM_THREADS + threadIdx.x;
-        if (t >= (long long)G * N) return;
-        const int g = (int)(t / N);
-        const long long i = t % N;
+        const long long tl = blockIdx.x * (long long)WSUM_THREADS + threadIdx.x;
+        if (tl >= (long long)G * NR) return;
+        const int g = (int)(tl / NR);
+        const long long i = r0 + tl % NR;
+        const long long t = (long long)g * N + i;
         if (h.hn) {  // head block A columns of row i: dZ_head[i, :], zero past hn
             const float* z = h.dz + g * h.dz_gs + i * h.hn;
             float4* dst = reinterpret_cast<float4*>(h.W + ((long long)g * N + i) * h.ldw + N);
@@ -1179,7 +1206,7 @@ __global__ void __launch_bounds__(WSUM_THREADS) mmd_wsum_kernel(const float* rpa
         wsum[t] = (float)s;
         return;
     }
-    const int gi = (int)(blockIdx.x - nbw), g = gi / T, I = gi % T;
+    const int gi = (int)(blockIdx.x - nbw), g = gi / NT, I = ta + gi % NT;
     int base = 0;
     for (int k = 0; k < I; ++k) base += T - k;
     const int nJ = T - I;
@@ -1288,6 +1315,8 @@ static bool w_path(const MmdArgs& a) {
     const long long N = a.m + a.n;
     if (fused || !a.gXs || !a.gXt || a.m <= 0 || a.n <= 0) return false;
     if (a.row_begin != 0 || (a.row_end >= 0 && a.row_end != N)) return false;
+    if (a.tile_end >= 0) return a.G == 1 && a.d % 4 == 0 && a.d >= 32 && N % 4 == 0 &&
+                                a.Xt == a.Xs + a.m * a.d && a.gXt == a.gXs + a.m * a.d;  // sharded: own rows of W
     if (a.d % 4 || a.d < 32 || N % 4) return false;
     if (a.Xt != a.Xs + a.m * a.d || a.xt_gs != a.xs_gs || a.xs_gs < N * a.d) return false;
     if (a.gXt != a.gXs + a.m * a.d || a.gt_gs != a.gs_gs || a.gs_gs != a.xs_gs) return false;
@@ -1301,10 +1330,27 @@ constexpr long long kVChunk = 1024;
 static int v_chunks(const MmdArgs& a) { return (int)((a.m + a.n + kVChunk - 1) / kVChunk); }
 
 static bool head_block(const MmdArgs& a) {
-    return a.hd_n > 0 && a.hd_n <= kHeadK && (a.m + a.n) % 32 == 0 && v_chunks(a) == 1;
+    return a.hd_n > 0 && a.hd_n <= kHeadK && (a.m + a.n) % 32 == 0 && v_chunks(a) == 1 && a.tile_end < 0;
+}
+
+// the owned tile rows [ta, tb) and rows [r0, r0 + NR) of a (tile-sharded) W path
+struct WRows {
+    int T, ta, tb;
+    long long r0, NR;
+};
+static WRows w_rows(const MmdArgs& a) {
+    const long long N = a.m + a.n;
+    WRows w;
+    w.T = (int)((N + WT - 1) / WT);
+    w.ta = a.tile_end < 0 ? 0 : (int)a.tile_begin;
+    w.tb = a.tile_end < 0 ? w.T : (int)a.tile_end;
+    w.r0 = (long long)w.ta * WT;
+    w.NR = std::min(N, (long long)w.tb * WT) - w.r0;
+    return w;
 }
 
 bool mmd_head_fusable(const MmdArgs& a) { return w_path(a) && head_block(a); }
+bool mmd_w_path(const MmdArgs& a) { return w_path(a); }
 
 struct WLayout {
     long long ldw;  // row stride of W: N, or N + kHeadK with the head block
@@ -1320,12 +1366,15 @@ struct WLayout {
 static WLayout w_layout(const MmdArgs& a, uintptr_t base) {
     const long long N = a.m + a.n;
     const int T = (int)((N + WT - 1) / WT), np = T * (T + 1) / 2;
+    const WRows wr = w_rows(a);
     WLayout L;
     uintptr_t cur = (base + 255) & ~uintptr_t(255);
     const uintptr_t start = cur;
     L.ldw = N + (head_block(a) ? kHeadK : 0);
-    L.W = reinterpret_cast<float*>(cur);
-    cur = (cur + (size_t)a.G * N * L.ldw * 4 + 255) & ~uintptr_t(255);
+    // only the owned rows of W exist (all rows unless tile-sharded, G = 1 then):
+    // L.W points at row 0 of the virtual [N][ldw] matrix
+    L.W = reinterpret_cast<float*>(cur) - (wr.NR < N ? wr.r0 * L.ldw : 0);
+    cur = (cur + (size_t)a.G * (wr.NR < N ? wr.NR : N) * L.ldw * 4 + 255) & ~uintptr_t(255);
     L.bx = reinterpret_cast<float*>(cur);
     if (head_block(a)) cur = (cur + (size_t)a.G * kHeadK * a.d * 4 + 255) & ~uintptr_t(255);
     L.rpart = reinterpret_cast<float*>(cur);
@@ -1337,7 +1386,7 @@ static WLayout w_layout(const MmdArgs& a, uintptr_t base) {
     L.wsum = reinterpret_cast<float*>(cur);
     cur = (cur + (size_t)a.G * N * 4 + 255) & ~uintptr_t(255);
     L.vpart = reinterpret_cast<float*>(cur);
-    if (v_chunks(a) > 1) cur = (cur + (size_t)v_chunks(a) * a.G * N * a.d * 4 + 255) & ~uintptr_t(255);
+    if (v_chunks(a) > 1) cur = (cur + (size_t)v_chunks(a) * a.G * wr.NR * a.d * 4 + 255) & ~uintptr_t(255);
     L.bytes = cur - start + 256;
     return L;
 }
@@ -1413,6 +1462,13 @@ void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s, int stages) 
         w.T = T;
         w.npairs = np;
         w.G = a.G;
+        const WRows wr = w_rows(a);
+        auto S = [T](long long I) { return I * T - I * (I - 1) / 2; };  // first pair of tile row I
+        w.ta = wr.ta;
+        w.tb = wr.tb;
+        w.pa = (int)S(wr.ta);
+        w.nA = (int)(S(wr.tb) - S(wr.ta));
+        w.nB = wr.ta * (wr.tb - wr.ta);
         w.W = L.W;
         w.ldw = L.ldw;
         w.rpart = L.rpart;
@@ -1422,10 +1478,11 @@ void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s, int stages) 
         if (const char* e = getenv("MTK_MMDW_DIAG")) w.diag = atoi(e);
         ensure_smem_attr(reinterpret_cast<const void*>(mmd_w_kernel), W_SMEM_BYTES);
         const int sms = device_sm_count(current_device());
-        const int items = a.G * np;
+        const int items = a.G * (w.nA + w.nB);
         mmd_w_kernel<<<std::min(items, sms), W_THREADS, W_SMEM_BYTES, s>>>(w);
         count_launch();
-        const long long nbw = ((long long)a.G * N + WSUM_THREADS - 1) / WSUM_THREADS;
+        const long long nbw = ((long long)a.G * wr.NR + WSUM_THREADS - 1) / WSUM_THREADS;
+        const int NT = wr.tb - wr.ta;
         const bool head = head_block(a);
         WsumHead h;
         std::memset(&h, 0, sizeof(h));
@@ -1445,16 +1502,18 @@ void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s, int stages) 
             h.bx = L.bx;
             nbx = ((long long)a.G * kHeadK * a.d + WSUM_THREADS - 1) / WSUM_THREADS;
         }
-        mmd_wsum_kernel<<<(unsigned)(nbw + (long long)a.G * T + nbx), WSUM_THREADS, 0, s>>>(
-            L.rpart, L.cpart, L.kpart, a.G, N, T, np, L.wsum, a.partial, h);
+        mmd_wsum_kernel<<<(unsigned)(nbw + (long long)a.G * NT + nbx), WSUM_THREADS, 0, s>>>(
+            L.rpart, L.cpart, L.kpart, a.G, N, T, np, L.wsum, a.partial, h, wr.r0, wr.NR, wr.ta, NT);
         count_launch();
+        // V = W.Z over the owned rows [r0, r0 + NR) (all rows unless sharded)
+        const long long r0 = wr.r0, NR = wr.NR;
         UmmaGemm u;
         u.G = a.G;
-        u.M = (int)N;
+        u.M = (int)NR;
         u.N = a.d;
         u.K = (int)N;
         u.a_mn = 0;
-        u.a = L.W;
+        u.a = L.W + r0 * L.ldw;
         u.a_rs = L.ldw;
         u.a_gs = N * L.ldw;
         u.b_mn = 1;
@@ -1463,7 +1522,7 @@ void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s, int stages) 
         u.b_gs = a.xs_gs;
         u.epi = Epi::kMmdGrad;
         u.same_sign = 1;  // W >= 0 (and Z >= 0 in bank steps): see k_umma.cu sepc
-        u.C = a.gXs;
+        u.C = a.gXs + r0 * a.d;
         u.c_gs = a.gs_gs;
         if (head) {  // fused head DX: K gains the head block; the epilogue writes the layer's dZ
             u.K = (int)N + kHeadK;
@@ -1476,18 +1535,18 @@ void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s, int stages) 
             u.colsum = a.hd_colsum;
         }
         u.ldc = a.d;
-        u.add = a.Xs;
-        u.rowvec = L.wsum;
+        u.add = a.Xs + r0 * a.d;
+        u.rowvec = L.wsum + r0;  // G = 1 when sharded (the epilogue indexes g * M + m)
         u.scale = a.grad_scale;
         u.flags = a.flags;
         const int nch = v_chunks(a);
         if (nch > 1) {  // kVChunk-deep GEMMs into fp32 partials, then the fp64 finish
-            const long long per = N * a.d;
+            const long long per = NR * a.d;
             for (int c = 0; c < nch; ++c) {
                 const long long k0 = (long long)c * kVChunk;
                 UmmaGemm v = u;
                 v.K = (int)std::min(kVChunk, N - k0);
-                v.a = L.W + k0;
+                v.a = L.W + r0 * L.ldw + k0;
                 v.b = a.Xs + k0 * a.d;
                 v.epi = Epi::kStore;
                 v.C = L.vpart + (long long)c * a.G * per;
@@ -1499,7 +1558,8 @@ void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s, int stages) 
             }
             const long long tot = (long long)a.G * per;
             mmd_vchunk_finish_kernel<<<(unsigned)std::min<long long>((tot + 255) / 256, 148 * 16), 256, 0, s>>>(
-                L.vpart, nch, per, a.Xs, a.xs_gs, L.wsum, a.gXs, a.gs_gs, a.G, N, a.d, a.grad_scale, a.flags);
+                L.vpart, nch, per, a.Xs + r0 * a.d, a.xs_gs, L.wsum + r0, a.gXs + r0 * a.d, a.gs_gs, a.G, NR, a.d,
+                a.grad_scale, a.flags);
             count_launch();
             return;
         }

@@ -43,3 +43,33 @@ def test_wrapper_gpu_step(tmp_path):
                          text=True)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "gpu checks ok" in out.stdout
+
+
+def _race_exe(tmp_path):
+    pre = os.path.join(ROOT, "tests", "cpp", "_build", "race_check_ref")
+    if os.path.exists(pre):
+        return pre
+    exe = str(tmp_path / "race_check")
+    lib = os.path.join(ROOT, "paper_2011_09463_b200")
+    subprocess.run(["g++", "-std=c++20", "-O2", f"-I{ROOT}/include", "-I/usr/local/cuda/include",
+                    os.path.join(ROOT, "tests", "cpp", "race_check.cpp"), f"-L{lib}", "-lmtk",
+                    "-L/usr/local/cuda/lib64", "-lcudart", f"-Wl,-rpath,{lib}",
+                    "-Wl,-rpath,/usr/local/cuda/lib64", "-o", exe], check=True)
+    return exe
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tool", ["racecheck", "synccheck"])
+def test_compute_sanitizer_bank_step_mmd_attack(tmp_path, tool):
+    """compute-sanitizer over one bank step with MMD (tcgen05 GEMMs, the
+    materialised-W MMD, the side stream), a fused-kernel MMD call and the
+    attack stage: no shared-memory hazards (racecheck), no barrier misuse
+    (synccheck).  Round 1 found a cross-stream scratch race only by chance."""
+    exe = _race_exe(tmp_path)
+    sanitizer = "/usr/local/cuda/bin/compute-sanitizer"
+    out = subprocess.run([sanitizer, "--tool", tool, "--error-exitcode", "9", exe], capture_output=True,
+                         text=True, timeout=900)
+    print(out.stdout[-3000:], out.stderr[-2000:])
+    assert out.returncode == 0, out.stdout[-4000:] + out.stderr[-2000:]
+    assert "race_check done" in out.stdout
+    assert "ERROR SUMMARY: 0 errors" in out.stdout + out.stderr

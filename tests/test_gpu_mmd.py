@@ -256,3 +256,28 @@ def test_mmd_c4_materialised_w_path_vs_fp64(ctx, monkeypatch):
     assert b1 == beta
     assert abs(v1 - v) <= TOL * abs(v)
     assert rel(Gw, G1) <= 2 * TOL
+
+
+@pytest.mark.parametrize("m,n,d,world", [(700, 324, 64, 2), (3000, 1000, 96, 3), (1500, 600, 128, 4)])
+def test_mmd_tile_sharding_is_bit_identical_to_one_rank(ctx, m, n, d, world):
+    """SURVEY.md 8(e) on the materialised-W path: `world` ranks each own an
+    equal range of 128-row tiles (simulated one after another on this GPU --
+    the ranks never wait on each other); the gradients of each rank's rows and
+    the MMD^2 value from the ascending-tile combination of the partials are
+    bit-identical to the one-rank evaluation (ragged last tiles, chunked V
+    for N > 1024)."""
+    from paper_2011_09463_b200 import api
+
+    rng = np.random.default_rng(m + world)
+    Z = torch.tensor(rng.standard_normal((m + n, d)).astype(np.float32), device="cuda")
+    Z[m:] += 0.2
+    v1, beta, gs, gt = api.mmd_gaussian(ctx, Z[:m], Z[m:])
+    g1 = torch.cat([gs, gt])
+    gZ = torch.full_like(Z, float("nan"))
+    tot = None
+    for lo, hi in api.mmd_tile_ranges(m, n, world):
+        part = api.mmd_gaussian_tiles(ctx, Z, m, beta, lo, hi, gZ)
+        assert not part[:lo].any() and not part[hi:].any()
+        tot = part if tot is None else tot + part  # one owner per tile row: exact
+    assert torch.equal(gZ, g1)
+    assert api.mmd_value_from_tiles(tot, m, n) == v1
