@@ -34,6 +34,9 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# NCCL's "NCCL version ..." banner goes to stdout, which must hold exactly one
+# JSON line (rank 0); keep NCCL at warnings (env NCCL_DEBUG_BENCH overrides)
+os.environ["NCCL_DEBUG"] = os.environ.get("NCCL_DEBUG_BENCH", "WARN")
 
 DIMS = [1024, 512, 256, 10]
 G = 32
