@@ -13,9 +13,11 @@ with its own roofline, clocks, e2e and cpu_baseline:
   "attack" -- the attack stage of configs[4] over 2^20 queries: queries/s.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
-  python bench.py --workload c4|attack|c3   # one workload as the whole line
+  python bench.py --workload c4|attack|c3|c5   # one workload as the whole line
       c3: configs[2], parameter-based 784-256-10, 8 shadows per GPU, with the
           NCCL feature all-gather inside the timed region
+      c5: configs[4], the full sweep (3 paradigms x 256 shadows, 2^20 attack
+          queries each) through the native driver
 
 --gpus N without torchrun re-launches itself under torch.distributed.run
 (one process per GPU).  Rank 0 prints ONE JSON line (contract in the task).
@@ -328,6 +330,8 @@ def run_reference_arm(args, world, rank):
         fn, unit, metric = (lambda: cpu_c4()), "pairs/s", "MMD kernel-pairs/s"
     elif wl == "attack":
         fn, unit, metric = (lambda: cpu_attack(reps=1)), "queries/s", "membership-attack queries/s"
+    elif wl == "c5":
+        fn, unit, metric = (lambda: cpu_c1_sample()), "samples/s", "shadow-model train samples/s"
     else:
         fn, unit, metric = (lambda: cpu_c3()), "samples/s", "shadow-model train samples/s"
     for _ in range(min(args.warmup, 1)):
@@ -347,7 +351,8 @@ def run_reference_arm(args, world, rank):
         "impl": "reference",
         "config": {"workload": {"c2": WORKLOAD, "c4": "C4 MMD stress 65536 x 8192 x 512",
                                 "attack": "attack stage, 2^20 queries",
-                                "c3": "C3 parameter-based 784-256-10"}[wl] + " (CPU, host threads)",
+                                "c3": "C3 parameter-based 784-256-10",
+                                "c5": "C5 sweep model 784-256-10 (sampled steps)"}[wl] + " (CPU, host threads)",
                    "parallelism": f"{rec['cores']} threads"},
         "cpu_baseline": dict(rec, value=value),
         "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -649,6 +654,98 @@ def measure_c3(args, world, rank, local, steps, warmup, cpu=True):
     return res
 
 
+# ----------------------------------------------------------------------------- C5
+def measure_c5(args, world, rank, local, steps, warmup, cpu=True):
+    """configs[4]: the full privacy sweep -- 3 transfer paradigms x 256 shadow
+    models (+ 1 target each), 2048 members + 2048 non-members per model, so
+    the attack model trains on 256 x 4096 = 2^20 member / non-member queries
+    per paradigm; AUC + accuracy on the target's 4096.  Each paradigm is one
+    mtk_sweep_run call (the native C++ driver: host mt::Rng sampling, device
+    pools, whole epochs per call, the ranks' features all-gathered over NCCL).
+    model / parameter: MLP 784-256-10; mapping: 1024-512-256-10 (configs[1]'s
+    model, lambda = 1 MMD).  One step = the whole sweep; timed on the host
+    clock (it includes host sampling), max over ranks."""
+    import torch
+
+    from paper_2011_09463_b200 import api
+
+    ctx = api.Context(local)
+    comm = api.Comm(ctx) if world > 1 else None
+    cfgs = [dict(paradigm="model", n_shadows=256), dict(paradigm="mapping", n_shadows=256, dims=(1024, 512, 256, 10)),
+            dict(paradigm="parameter", n_shadows=256)]
+
+    def sweep():
+        return [api.sweep_run(ctx, c, comm) for c in cfgs]
+
+    res = None
+    for _ in range(warmup):
+        res = sweep()
+    times = []
+    with ClockSampler(local) as clk:
+        for _ in range(steps):
+            barrier(world)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            res = sweep()
+            torch.cuda.synchronize()
+            times.append(max_over_ranks(time.perf_counter() - t0, world))
+    secs = statistics.median(times)
+    d = {"model": 784, "mapping": 1024, "parameter": 784}
+    # training rows per model: model = 2 pretrain epochs x 4096 source + 10 x 2048 members;
+    # mapping / parameter = 10 epochs x (2048 members + 2048 source rows riding along)
+    rows = {"model": 2 * 4096 + 10 * 2048, "mapping": 10 * 4096, "parameter": 10 * 4096}
+    samples = sum(257 * rows[c["paradigm"]] for c in cfgs)
+    flop = sum(257 * rows[c["paradigm"]] * (818_176 if c["paradigm"] != "mapping" else 2_898_944) for c in cfgs)
+    peak, bf16, src = fp32acc_peak()
+    achieved = flop / secs / world / 1e12
+    out = {
+        "metric": "shadow-model train samples/s", "value": samples / secs, "unit": "samples/s", "n_gpus": world,
+        "steps": steps, "warmup": warmup, "ms_per_step": 1000.0 * secs, "higher_is_better": True,
+        "scaling": "strong", "dtype": "f32",
+        "config": {"workload": "C5 full privacy sweep: 3 paradigms x (1 target + 256 shadows), 2048 members + "
+                               "2048 non-members each, 2^20 attack-training queries per paradigm, attack MLP "
+                               "3-64-2, AUC/accuracy on the target (native mtk_sweep_run, host-clock timed)",
+                   "paradigms": {c["paradigm"]: {"auc": r["auc"], "accuracy": r["accuracy"],
+                                                 "models": r["models"], "seconds": r["seconds"],
+                                                 "dims": list(c.get("dims", (784, 256, 10)))}
+                                 for c, r in zip(cfgs, res)},
+                   "train_samples_per_sweep": samples, "parallelism": f"models{world}",
+                   "timing": f"median of {steps} host-clock sweeps"},
+        "roofline": {"bound": "tensor", "kernel": "whole sweep (training dominates)", "achieved": achieved,
+                     "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                     "peak_note": f"algorithmic train flop per sample (818,176 / 2,898,944); 3xTF32 peak = "
+                                  f"{src} bf16 {bf16} / 6"},
+        "e2e": {"value": samples / secs, "unit": "samples/s", "h2d_bytes_per_step": None,
+                "d2h_bytes_per_step": None,
+                "note": "the sweep is end to end by construction: host sampling, pool upload and the AUC "
+                        "readback are inside each timed sweep"},
+        "gpu_launches": None,
+        "clocks": clk.summary(),
+        "cpu_baseline": None,
+    }
+    if comm is not None:
+        comm.close()
+    if rank == 0 and world == 1 and cpu:
+        v, rec = cpu_c1_sample()
+        rec["sample"] += f"; the full C5 sweep at this rate would take {samples / v / 3600:.2f} h"
+        out["cpu_baseline"] = rec
+    return out
+
+
+def cpu_c1_sample(threads=None, steps=8):
+    """784-256-10 SGD steps (B = 128), one model per thread (the C1/C5 model)"""
+    import ctypes as C
+
+    po, R = _ref()
+    if R is None:
+        return None, None
+    threads = threads or cpu_threads()
+    secs = R.ref_bench_train(threads, 2, (C.c_int * 3)(784, 256, 10), 128, 0, steps, 0.0, 5)
+    v = threads * steps * 128 / secs
+    sample = f"{threads} 784-256-10 models x {steps} SGD steps of 128 rows, one model per thread"
+    return v, _cpu_record(po, R, "reference", threads, sample, v, "samples/s", secs)
+
+
 # ----------------------------------------------------------------------------- C2 (headline)
 def measure_c2(args, world, rank, local):
     import torch
@@ -781,8 +878,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sub", action="store_true", help="C2 line without the c4 / attack sub-objects")
-    ap.add_argument("--workload", default="c2", choices=["c2", "c4", "attack", "c3"],
-                    help="c2 (default, the headline + c4 / attack sub-objects), c4, attack, c3")
+    ap.add_argument("--workload", default="c2", choices=["c2", "c4", "attack", "c3", "c5"],
+                    help="c2 (default, the headline + c4 / attack sub-objects), c4, attack, c3, c5")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args, int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")))
@@ -802,7 +899,7 @@ def main():
             if rank == 0 and world == 1 and cpu:
                 line["cpu_baseline"] = cpu_c2()[1]
         else:
-            fn = {"c4": measure_c4, "attack": measure_attack, "c3": measure_c3}[args.workload]
+            fn = {"c4": measure_c4, "attack": measure_attack, "c3": measure_c3, "c5": measure_c5}[args.workload]
             line = fn(args, world, rank, local, steps=args.steps, warmup=max(args.warmup, 3), cpu=cpu)
             line.update({"warmup": args.warmup, "vs_baseline": None, "data": "synthetic"})
         if rank == 0:
