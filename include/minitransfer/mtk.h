@@ -59,8 +59,8 @@ const char* mtk_last_error(void);
 int mtk_ctx_create(int device, void* cuda_stream, mtk_ctx** out);
 int mtk_ctx_destroy(mtk_ctx* ctx);
 int mtk_ctx_synchronize(mtk_ctx* ctx);
-/* number of kernels this library has launched in this process (its own
- * kernels; CUB's sort/scan internals in mtk_auc are not counted) */
+/* number of kernels this library has launched in this process (all of the
+ * path's kernels are the library's own; no library sort / scan is used)    */
 int mtk_ctx_launch_count(mtk_ctx* ctx, uint64_t* out);
 /* Optional CUDA-event timing of the bank step's phases, on the ctx stream.
  * mtk_ctx_phase_times synchronizes and returns (then resets) the summed

@@ -1,0 +1,268 @@
+// auc.cuh -- exact mid-rank (Mann-Whitney) AUC without sorting the scores
+// (AUC = (R_pos - npos (npos + 1) / 2) / (npos nneg),
+// mid-ranks for ties).  With U2 = sum over members of 2 #{non-members below}
+// + #{non-members equal}, AUC = (U2 / 2) / (npos nneg), all in exact integers.
+//
+// The scores are keyed by an order-preserving float -> uint32 map and the
+// rank sums come from key histograms instead of a sort:
+//   1. (fused into the kernel that produces the scores) the key of every
+//      query and a per-class histogram of the key's top 16 bits
+//      (warp-aggregated integer atomics);
+//   2. auc_scan_kernel, one CTA: in bucket order, every member contributes
+//      2 #{non-members in lower buckets} -- summed exactly -- and the
+//      buckets holding both classes ("mixed") get a slot in a compacted,
+//      bucket-ordered array;
+//   3. auc_scatter_kernel: the queries of mixed buckets go to their bucket's
+//      slot as (low 16 key bits << 1 | class);
+//   4. auc_bucket_kernel, one CTA per mixed bucket: within the bucket the
+//      members' 2 #{below} + #{equal} over the low 16 bits -- a shared-memory
+//      bitonic sort and a scan for buckets up to 8192 queries, a per-CTA
+//      65536-bin histogram of the non-members and its scan above that.
+// Integer sums are order-independent, so the AUC is deterministic and
+// bit-identical to the sort-based evaluation (and to oracle.c orc_auc's
+// ranks); no library sort on the path.
+#pragma once
+
+#include <cstdint>
+
+namespace mtk {
+namespace auc {
+
+constexpr int kBuckets = 65536;
+constexpr int kSmallMax = 8192;      // bitonic-sort path up to this many queries per bucket
+constexpr int kThreads = 1024;       // scan / bucket kernels
+constexpr uint32_t kNotMixed = 0xFFFFFFFFu;
+
+// order-preserving map float -> uint32 (ascending), -0.0 == +0.0
+__device__ __forceinline__ uint32_t key_of(float v) {
+    if (v == 0.f) v = 0.f;
+    const uint32_t u = __float_as_uint(v);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+// one query's key into the class histogram of the top 16 bits; all 32 lanes
+// of the warp must call it (valid = false for lanes without a query)
+__device__ __forceinline__ void hist_add(uint32_t* hist, uint32_t key, bool member, bool valid) {
+    const uint32_t tag = valid ? ((key >> 16) | (member ? 0x10000u : 0u)) : 0xFFFFFFFFu;
+    const unsigned peers = __match_any_sync(0xffffffffu, tag);
+    const int lane = threadIdx.x & 31;
+    if (valid && lane == __ffs(peers) - 1) atomicAdd(&hist[tag], (uint32_t)__popc(peers));
+}
+
+// block-wide exclusive scan of one u32 per thread (kThreads threads); returns
+// the thread's exclusive prefix, *total the block total
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* sh, uint32_t* total) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) sh[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        uint32_t s = sh[lane];
+        uint32_t t = s;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += y;
+        }
+        sh[lane] = t - s;  // exclusive warp offsets
+        if (lane == 31) sh[32] = t;
+    }
+    __syncthreads();
+    const uint32_t r = sh[w] + x - v;
+    *total = sh[32];
+    __syncthreads();
+    return r;
+}
+
+__device__ __forceinline__ unsigned long long block_sum_u64(unsigned long long v, unsigned long long* sh) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+    __syncthreads();
+    unsigned long long t = 0;
+    if (threadIdx.x == 0)
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += sh[i];
+    __syncthreads();
+    return t;  // valid on thread 0
+}
+
+struct Work {
+    uint32_t* key;        // [n]
+    uint32_t* hist;       // [2][kBuckets] class 0 (non-members), class 1 (members); zero on entry
+    uint32_t* cursor;     // [kBuckets]
+    uint32_t* packed;     // [n]
+    uint4* mixed;         // [kBuckets] (bucket, offset, size, non-members)
+    uint32_t* big;        // [grid][kBuckets] histogram scratch of the large-bucket path
+    unsigned long long* cnt;  // [0] members, [1] hits at 0.5, [2] U2, [3] mixed buckets
+};
+
+// 2. bucket order: exact cross-bucket U2 part, mixed-bucket slots, histogram reset
+__global__ void __launch_bounds__(kThreads) auc_scan_kernel(Work w) {
+    __shared__ uint32_t sh[33];
+    __shared__ unsigned long long shl[32];
+    constexpr int per = kBuckets / kThreads;  // 64 consecutive buckets per thread
+    const int b0 = threadIdx.x * per;
+    uint32_t n_neg = 0, n_mix = 0, n_slot = 0;
+    for (int i = 0; i < per; ++i) {
+        const uint32_t N = w.hist[b0 + i], P = w.hist[kBuckets + b0 + i];
+        n_neg += N;
+        const bool mixed = N && P;
+        n_mix += mixed;
+        n_slot += mixed ? N + P : 0;
+    }
+    uint32_t tot;
+    uint32_t below = block_excl_scan(n_neg, sh, &tot);
+    uint32_t mix = block_excl_scan(n_mix, sh, &tot);
+    const uint32_t nmixed = tot;
+    uint32_t off = block_excl_scan(n_slot, sh, &tot);
+    unsigned long long cross = 0;
+    for (int i = 0; i < per; ++i) {
+        const int b = b0 + i;
+        const uint32_t N = w.hist[b], P = w.hist[kBuckets + b];
+        cross += (unsigned long long)P * (2ull * below);
+        if (N && P) {
+            w.mixed[mix++] = make_uint4((uint32_t)b, off, N + P, N);
+            w.cursor[b] = off;
+            off += N + P;
+        } else {
+            w.cursor[b] = kNotMixed;
+        }
+        below += N;
+        w.hist[b] = 0;  // clean for the next call
+        w.hist[kBuckets + b] = 0;
+    }
+    cross = block_sum_u64(cross, shl);
+    if (threadIdx.x == 0) {
+        atomicAdd(&w.cnt[2], cross);
+        w.cnt[3] = nmixed;
+    }
+}
+
+// 3. the queries of mixed buckets into their bucket's slot (order inside a
+// bucket is immaterial: the bucket kernel sorts / counts it)
+__global__ void auc_scatter_kernel(Work w, const uint8_t* lab, long long n) {
+    for (long long i0 = blockIdx.x * (long long)blockDim.x; i0 < n; i0 += (long long)gridDim.x * blockDim.x) {
+        const long long i = i0 + threadIdx.x;
+        const bool valid = i < n;
+        const uint32_t k = valid ? w.key[i] : 0u;
+        const uint32_t b = k >> 16;
+        const bool mixed = valid && w.cursor[b] != kNotMixed;
+        const uint32_t tag = mixed ? b : 0xFFFFFFFFu;
+        const unsigned peers = __match_any_sync(0xffffffffu, tag);
+        const int lane = threadIdx.x & 31, leader = __ffs(peers) - 1;
+        uint32_t base = 0;
+        if (mixed && lane == leader) base = atomicAdd(&w.cursor[b], (uint32_t)__popc(peers));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (mixed) {
+            const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+            w.packed[base + rank] = ((k & 0xFFFFu) << 1) | (lab[i] ? 1u : 0u);
+        }
+    }
+}
+
+// 4. within-bucket ranks of the members against the non-members
+constexpr int kBucketSmem = 2 * kSmallMax * 4;  // dynamic: the sorted bucket + its prefix counts
+__global__ void __launch_bounds__(kThreads) auc_bucket_kernel(Work w) {
+    extern __shared__ uint32_t dsm[];
+    uint32_t* buf = dsm;
+    uint32_t* pre = dsm + kSmallMax;
+    __shared__ uint32_t sh[33];
+    __shared__ unsigned long long shl[32];
+    const uint32_t nmixed = (uint32_t)w.cnt[3];
+    unsigned long long acc = 0;
+    for (uint32_t t = blockIdx.x; t < nmixed; t += gridDim.x) {
+        const uint4 mb = w.mixed[t];
+        const uint32_t off = mb.y, s = mb.z, nneg = mb.w;
+        const uint32_t* src = w.packed + off;
+        if (s <= (uint32_t)kSmallMax) {
+            uint32_t P = 32;
+            while (P < s) P <<= 1;
+            for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) buf[i] = i < s ? src[i] : 0xFFFFFFFFu;
+            __syncthreads();
+            // bitonic sort, ascending: (value, class 0 before class 1)
+            for (uint32_t k = 2; k <= P; k <<= 1) {
+                for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+                    for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
+                        const uint32_t l = i ^ j;
+                        if (l > i) {
+                            const uint32_t a = buf[i], c = buf[l];
+                            const bool up = (i & k) == 0;
+                            if ((a > c) == up) {
+                                buf[i] = c;
+                                buf[l] = a;
+                            }
+                        }
+                    }
+                    __syncthreads();
+                }
+            }
+            // prefix count of non-members, P / blockDim elements per thread (consecutive)
+            const uint32_t per = (P + blockDim.x - 1) / blockDim.x;
+            const uint32_t e0 = threadIdx.x * per;
+            uint32_t loc = 0;
+            for (uint32_t e = e0; e < e0 + per && e < P; ++e) loc += (e < s && !(buf[e] & 1u));
+            uint32_t tot;
+            uint32_t run = block_excl_scan(loc, sh, &tot);
+            for (uint32_t e = e0; e < e0 + per && e < P; ++e) {
+                pre[e] = run;  // non-members before e
+                run += (e < s && !(buf[e] & 1u));
+            }
+            __syncthreads();
+            for (uint32_t e = threadIdx.x; e < s; e += blockDim.x) {
+                const uint32_t v = buf[e];
+                if (!(v & 1u)) continue;
+                // members sort after the non-members of their value: pre[e]
+                // counts below + equal; the value group's first element
+                // (lower bound of (value << 1) in the sorted bucket) gives below
+                const uint32_t first = v & ~1u;
+                uint32_t lo = 0, hi = e;
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (buf[mid] < first) lo = mid + 1;
+                    else hi = mid;
+                }
+                acc += (unsigned long long)pre[lo] + pre[e];
+            }
+            __syncthreads();
+        } else {
+            // large bucket: 65536-bin histogram of the non-members' low bits
+            uint32_t* h = w.big + (size_t)blockIdx.x * kBuckets;
+            for (int i = threadIdx.x; i < kBuckets; i += blockDim.x) h[i] = 0;
+            __syncthreads();
+            for (uint32_t e = threadIdx.x; e < s; e += blockDim.x) {
+                const uint32_t v = src[e];
+                if (!(v & 1u)) atomicAdd(&h[v >> 1], 1u);
+            }
+            __syncthreads();
+            constexpr int per = kBuckets / kThreads;
+            const int b0 = threadIdx.x * per;
+            uint32_t loc = 0;
+            for (int i = 0; i < per; ++i) loc += h[b0 + i];
+            uint32_t tot;
+            uint32_t run = block_excl_scan(loc, sh, &tot);
+            for (int i = 0; i < per; ++i) {
+                const uint32_t c = h[b0 + i];
+                h[b0 + i] = run;  // exclusive prefix: non-members below this value
+                run += c;
+            }
+            __syncthreads();
+            for (uint32_t e = threadIdx.x; e < s; e += blockDim.x) {
+                const uint32_t v = src[e];
+                if (!(v & 1u)) continue;
+                const uint32_t x = v >> 1;
+                const uint32_t below = h[x], upto = x + 1 < (uint32_t)kBuckets ? h[x + 1] : nneg;
+                acc += (unsigned long long)below + upto;  // 2 below + equal
+            }
+            __syncthreads();
+        }
+    }
+    acc = block_sum_u64(acc, shl);
+    if (threadIdx.x == 0 && acc) atomicAdd(&w.cnt[2], acc);
+}
+
+}  // namespace auc
+}  // namespace mtk

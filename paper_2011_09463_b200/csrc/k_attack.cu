@@ -5,12 +5,11 @@
 // (SURVEY.md section 8(a) row a18); definitions per SURVEY.md Appendix A and
 // oracle.c (orc_posterior_features, orc_auc).  These are streaming,
 // HBM-bound kernels: one thread per query row, coalesced row-major output.
-#include <cub/cub.cuh>
-
 #include <algorithm>
 #include <cmath>
 #include <mutex>
 
+#include "auc.cuh"
 #include "internal.h"
 
 namespace mtk {
@@ -137,18 +136,7 @@ __global__ void column_kernel(const float* logits, long long rows, int C, int co
     out[r] = expf(x[col] - mx) / z;
 }
 
-// ---- AUC -------------------------------------------------------------------
-// Exact mid-rank AUC without a tie pass: with the non-members' keys sorted,
-// each member contributes 2 * #{non-members below} + #{non-members equal}
-// (lower / upper bound); U2 = the sum (exact uint64) = 2 * (R_pos - npos (npos+1) / 2).
-// order-preserving map float -> uint32 (ascending), -0.0 == +0.0
-__device__ __forceinline__ uint32_t auc_key(float v) {
-    if (v == 0.f) v = 0.f;
-    const uint32_t u = __float_as_uint(v);
-    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-}
-constexpr uint32_t kSentinel = 0xFFFFFFFFu;  // a member's slot in the non-member key array
-
+// ---- AUC (auc.cuh: exact mid-rank AUC from key histograms, no sort) --------
 // block-aggregated integer atomics (exact, order-independent): cnt[0] += pos, cnt[1] += hit
 __device__ __forceinline__ void add_counts(unsigned long long pos, unsigned long long hit,
                                            unsigned long long* cnt) {
@@ -173,78 +161,23 @@ __device__ __forceinline__ void add_counts(unsigned long long pos, unsigned long
     }
 }
 
-// per query: kn = key (non-member) or the sentinel (member); kp = key (member)
-__global__ void auc_keys_kernel(const float* s, const uint8_t* lab, long long n, uint32_t* kn,
-                                uint32_t* kp, unsigned long long* counts) {
+// per query: the order-preserving key and the class histogram of its top
+// 16 bits (auc.cuh step 1), member and hit-at-0.5 counts
+__global__ void auc_keys_kernel(const float* s, const uint8_t* lab, long long n, auc::Work w) {
     const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     unsigned long long pos = 0, hit = 0;
-    if (i < n) {
-        const uint32_t u = auc_key(s[i]);
-        const bool l = lab[i] != 0;
-        kn[i] = l ? kSentinel : u;
-        kp[i] = u;
+    const bool valid = i < n;
+    uint32_t u = 0;
+    bool l = false;
+    if (valid) {
+        u = auc::key_of(s[i]);
+        l = lab[i] != 0;
+        w.key[i] = u;
         pos = l;
         hit = ((s[i] > 0.5f) == l);
     }
-    add_counts(pos, hit, counts);
-}
-
-// members: U2 += 2 * lower_bound + (upper_bound - lower_bound) over the sorted
-// non-member keys sorted[0, nneg) (nneg = n - cnt[0], read on the device).
-// A block keeps every step-th sorted key in shared memory (AUC_SAMPLES of
-// them), so a search touches global memory only inside one step-wide segment;
-// the upper bound gallops from the lower bound (ties are usually short).
-constexpr int AUC_SAMPLES = 8192, AUC_THREADS = 512;
-__global__ void __launch_bounds__(AUC_THREADS) auc_member_count(const uint32_t* sorted, const uint32_t* kp,
-                                                                const uint8_t* lab, long long n,
-                                                                unsigned long long* cnt) {
-    __shared__ uint32_t samp[AUC_SAMPLES];
-    __shared__ unsigned long long st[AUC_THREADS / 32];
-    const long long nneg = n - (long long)cnt[0];
-    const long long step = nneg > AUC_SAMPLES ? (nneg + AUC_SAMPLES - 1) / AUC_SAMPLES : 1;
-    const int ns = (int)((nneg + step - 1) / step);  // samp[s] = sorted[s * step]
-    for (int i = threadIdx.x; i < ns; i += blockDim.x) samp[i] = sorted[(long long)i * step];
-    __syncthreads();
-    unsigned long long t = 0;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x) {
-        if (!lab[i]) continue;
-        const uint32_t u = kp[i];
-        int a = 0, b = ns;  // first sample >= u
-        while (a < b) {
-            const int mid = (a + b) >> 1;
-            if (samp[mid] < u) a = mid + 1;
-            else b = mid;
-        }
-        // sorted[(a - 1) * step] < u <= sorted[a * step]: lower bound in ((a-1) step, a step]
-        long long lo = a > 0 ? (long long)(a - 1) * step + 1 : 0, hi = a < ns ? (long long)a * step : nneg;
-        while (lo < hi) {
-            const long long mid = (lo + hi) >> 1;
-            if (sorted[mid] < u) lo = mid + 1;
-            else hi = mid;
-        }
-        long long ub = lo, inc = 1;  // gallop: first index > u
-        while (ub < nneg && sorted[ub] <= u) {
-            ub += inc;
-            inc <<= 1;
-        }
-        long long glo = ub - (inc >> 1), ghi = ub < nneg ? ub : nneg;  // sorted[glo - 1] <= u (or glo = lo)
-        if (glo < lo) glo = lo;
-        while (glo < ghi) {
-            const long long mid = (glo + ghi) >> 1;
-            if (sorted[mid] <= u) glo = mid + 1;
-            else ghi = mid;
-        }
-        t += (unsigned long long)(lo + glo);  // 2 * below + equal
-    }
-    for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
-    if ((threadIdx.x & 31) == 0) st[threadIdx.x >> 5] = t;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long acc = 0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) acc += st[w];
-        if (acc) atomicAdd(&cnt[2], acc);
-    }
+    auc::hist_add(w.hist, u, l, valid);
+    add_counts(pos, hit, w.cnt);
 }
 
 // ---- fused attack scoring: posterior softmax -> top-KF sorted features ->
@@ -253,73 +186,103 @@ __global__ void __launch_bounds__(AUC_THREADS) auc_member_count(const uint32_t* 
 // small2_forward_kernel and column_kernel (bit-identical scores); the attack
 // model's weights sit in constant memory (warp-uniform operands).
 constexpr int ATT_K = 3, ATT_H = 64;
-__constant__ float c_att[ATT_K * ATT_H + ATT_H + ATT_H * 2 + 2];  // W0 [K][H], b0 [H], W1 [H][2], b1 [2]
+// Two queries per thread: the attack MLP runs on packed fp32x2 (FFMA2 /
+// FADD2: the same IEEE operations lane by lane, so the scores stay
+// bit-identical to the one-query kernel) with each weight stored twice in
+// constant memory (c_att2: (w, w) pairs, warp-uniform 64-bit operands).
+// EXACT: C == CC at compile time (the 10-class posteriors), no padding lanes.
+__constant__ float2 c_att2[ATT_K * ATT_H + ATT_H + ATT_H * 2 + 2];
 
-template <int CC>
-__global__ void __launch_bounds__(256) attack_score_kernel(const float* logits, long long rows, int C,
-                                                           const uint8_t* lab, float* score_out, uint32_t* kn,
-                                                           uint32_t* kp, unsigned long long* cnt) {
-    const long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    unsigned long long pos = 0, hit = 0;
-    if (r < rows) {
-        const float* x = logits + r * C;
-        float v[CC];
+template <int CC, bool EXACT>
+__device__ __forceinline__ void top3_of_row(const float* x, int C, float (&top)[ATT_K]) {
+    float v[CC];
 #pragma unroll
-        for (int j = 0; j < CC; ++j) v[j] = j < C ? __ldg(x + j) : -INFINITY;
-        float mx = v[0];
+    for (int j = 0; j < CC; ++j) v[j] = (EXACT || j < C) ? __ldg(x + j) : -INFINITY;
+    float mx = v[0];
 #pragma unroll
-        for (int j = 1; j < CC; ++j) mx = fmaxf(mx, v[j]);
-        float z = 0.f;
+    for (int j = 1; j < CC; ++j) mx = fmaxf(mx, v[j]);
+    float z = 0.f;
 #pragma unroll
-        for (int j = 0; j < CC; ++j) {
-            v[j] = j < C ? expf(v[j] - mx) : 0.f;
-            z += v[j];
-        }
-        const float inv = 1.f / z;
-        float top[ATT_K];
-#pragma unroll
-        for (int a = 0; a < ATT_K; ++a) top[a] = -1.f;
-#pragma unroll
-        for (int j = 0; j < CC; ++j) {
-            if (j >= C) break;
-            float t = v[j] * inv;
-#pragma unroll
-            for (int a = 0; a < ATT_K; ++a) {
-                const float hi = fmaxf(top[a], t), lo = fminf(top[a], t);
-                top[a] = hi;
-                t = lo;
-            }
-        }
-        const float* W0 = c_att;
-        const float* B0 = W0 + ATT_K * ATT_H;
-        const float* W1 = B0 + ATT_H;
-        const float* B1 = W1 + ATT_H * 2;
-        float o0 = 0.f, o1 = 0.f;
-#pragma unroll
-        for (int h = 0; h < ATT_H; ++h) {
-            float acc = 0.f;
-#pragma unroll
-            for (int k = 0; k < ATT_K; ++k) acc = fmaf(top[k], W0[k * ATT_H + h], acc);
-            float hv = acc + B0[h];
-            hv = hv > 0.f ? hv : 0.f;
-            o0 = fmaf(hv, W1[h * 2], o0);
-            o1 = fmaf(hv, W1[h * 2 + 1], o1);
-        }
-        o0 = o0 + B1[0];
-        o1 = o1 + B1[1];
-        // member posterior: column_kernel's softmax column 1
-        const float m2 = fmaxf(o0, o1);
-        const float z2 = expf(o0 - m2) + expf(o1 - m2);
-        const float sc = expf(o1 - m2) / z2;
-        if (score_out) score_out[r] = sc;
-        const uint32_t u = auc_key(sc);
-        const bool l = lab[r] != 0;
-        kn[r] = l ? kSentinel : u;
-        kp[r] = u;
-        pos = l;
-        hit = ((sc > 0.5f) == l);
+    for (int j = 0; j < CC; ++j) {
+        v[j] = (EXACT || j < C) ? expf(v[j] - mx) : 0.f;
+        z += v[j];
     }
-    add_counts(pos, hit, cnt);
+    const float inv = 1.f / z;
+#pragma unroll
+    for (int a = 0; a < ATT_K; ++a) top[a] = -1.f;
+#pragma unroll
+    for (int j = 0; j < CC; ++j) {
+        if (!EXACT && j >= C) break;
+        float t = v[j] * inv;
+#pragma unroll
+        for (int a = 0; a < ATT_K; ++a) {
+            const float hi = fmaxf(top[a], t), lo = fminf(top[a], t);
+            top[a] = hi;
+            t = lo;
+        }
+    }
+}
+
+template <int CC, bool EXACT>
+__global__ void __launch_bounds__(256) attack_score2_kernel(const float* logits, long long rows, int C,
+                                                            const uint8_t* lab, float* score_out, auc::Work w) {
+    const long long r0 = 2 * (blockIdx.x * (long long)blockDim.x + threadIdx.x);
+    float ta[ATT_K], tb[ATT_K];
+    const bool va = r0 < rows, vb = r0 + 1 < rows;
+    if (va) top3_of_row<CC, EXACT>(logits + r0 * C, C, ta);
+    else ta[0] = ta[1] = ta[2] = 0.f;
+    if (vb) top3_of_row<CC, EXACT>(logits + (r0 + 1) * C, C, tb);
+    else tb[0] = tb[1] = tb[2] = 0.f;
+    const float2* W0 = c_att2;
+    const float2* B0 = W0 + ATT_K * ATT_H;
+    const float2* W1 = B0 + ATT_H;
+    const float2* B1 = W1 + ATT_H * 2;
+    const float2 t0 = make_float2(ta[0], tb[0]), t1 = make_float2(ta[1], tb[1]), t2 = make_float2(ta[2], tb[2]);
+    float2 o0 = make_float2(0.f, 0.f), o1 = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int h = 0; h < ATT_H; ++h) {
+        float2 acc = __ffma2_rn(t0, W0[h], make_float2(0.f, 0.f));
+        acc = __ffma2_rn(t1, W0[ATT_H + h], acc);
+        acc = __ffma2_rn(t2, W0[2 * ATT_H + h], acc);
+        float2 hv = __fadd2_rn(acc, B0[h]);
+        hv.x = hv.x > 0.f ? hv.x : 0.f;
+        hv.y = hv.y > 0.f ? hv.y : 0.f;
+        o0 = __ffma2_rn(hv, W1[h * 2], o0);
+        o1 = __ffma2_rn(hv, W1[h * 2 + 1], o1);
+    }
+    o0 = __fadd2_rn(o0, B1[0]);
+    o1 = __fadd2_rn(o1, B1[1]);
+    unsigned long long pos = 0, hit = 0;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const long long r = r0 + q;
+        const bool valid = q ? vb : va;
+        const float p0 = q ? o0.y : o0.x, p1 = q ? o1.y : o1.x;
+        uint32_t u = 0;
+        bool l = false;
+        if (valid) {  // member posterior: column_kernel's softmax column 1
+            const float m2 = fmaxf(p0, p1);
+            const float z2 = expf(p0 - m2) + expf(p1 - m2);
+            const float sc = expf(p1 - m2) / z2;
+            if (score_out) score_out[r] = sc;
+            u = auc::key_of(sc);
+            l = lab[r] != 0;
+            w.key[r] = u;
+            pos += l;
+            hit += ((sc > 0.5f) == l);
+        }
+        auc::hist_add(w.hist, u, l, valid);
+    }
+    add_counts(pos, hit, w.cnt);
+}
+
+// (w, w) pairs of the attack weights for c_att2
+__global__ void att_dup_kernel(const float* W0, const float* b0, const float* W1, const float* b1, float2* out) {
+    const int i = threadIdx.x + blockIdx.x * blockDim.x;
+    constexpr int n0 = ATT_K * ATT_H, n1 = n0 + ATT_H, n2 = n1 + ATT_H * 2, n3 = n2 + 2;
+    if (i >= n3) return;
+    const float v = i < n0 ? W0[i] : i < n1 ? b0[i - n0] : i < n2 ? W1[i - n1] : b1[i - n2];
+    out[i] = make_float2(v, v);
 }
 
 inline unsigned nblocks(long long n, int t) { return (unsigned)((n + t - 1) / t); }
@@ -383,38 +346,40 @@ void launch_column(const float* logits, long long rows, int C, int col, float* o
 }
 
 namespace {
-struct AucWork {
-    uint32_t *kn, *kn_sorted, *kp;
-    unsigned long long* cnt;  // [0] members, [1] hits at 0.5, [2] U2
-    void* tmp;
-    size_t tmp_bytes;
-};
-AucWork auc_work(Ctx& ctx, long long n) {
+// grow-only workspace from ctx.big: keys, histograms, bucket slots, the
+// scattered mixed buckets, the large-bucket histograms, counters
+auc::Work auc_work(Ctx& ctx, long long n) {
     if (n > 0x7fffffffLL) fail(MTK_SHAPE_ERROR, "auc: more than 2^31 rows");
-    AucWork w;
-    w.tmp_bytes = 0;
-    cub::DeviceRadixSort::SortKeys(nullptr, w.tmp_bytes, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)n, 0, 32,
-                                   ctx.stream);
+    const int grid = device_sm_count(ctx.device);
     auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
-    char* p = static_cast<char*>(ctx.big(al(4 * n) * 3 + al(64) + al(w.tmp_bytes)));
+    const size_t hb = 2 * (size_t)auc::kBuckets * 4;
+    char* p = static_cast<char*>(ctx.big(al(4 * n) * 2 + al(hb) + al(4 * auc::kBuckets) +
+                                         al(16 * auc::kBuckets) + al((size_t)grid * auc::kBuckets * 4) + al(64)));
     auto take = [&](size_t b) { char* r = p; p += al(b); return r; };
-    w.kn = (uint32_t*)take(4 * n);
-    w.kn_sorted = (uint32_t*)take(4 * n);
-    w.kp = (uint32_t*)take(4 * n);
+    auc::Work w;
+    w.key = (uint32_t*)take(4 * n);
+    w.packed = (uint32_t*)take(4 * n);
+    w.hist = (uint32_t*)take(hb);
+    w.cursor = (uint32_t*)take(4 * auc::kBuckets);
+    w.mixed = (uint4*)take(16 * auc::kBuckets);
+    w.big = (uint32_t*)take((size_t)grid * auc::kBuckets * 4);
     w.cnt = (unsigned long long*)take(64);
-    w.tmp = take(w.tmp_bytes);
+    // hist is left zeroed by auc_scan_kernel, but the workspace may be new
+    MTK_CUDA(cudaMemsetAsync(w.hist, 0, hb, ctx.stream));
     MTK_CUDA(cudaMemsetAsync(w.cnt, 0, 64, ctx.stream));
     return w;
 }
-// keys written: sort the non-member keys (members' sentinels sort last), count
-// members against them, read back (synchronizes)
-void auc_finish(Ctx& ctx, AucWork& w, const uint8_t* labels, long long n, double* auc, double* acc) {
+// keys and histograms written: the cross-bucket pass, the scatter of the
+// mixed buckets, the within-bucket pass; read back (synchronizes)
+void auc_finish(Ctx& ctx, auc::Work& w, const uint8_t* labels, long long n, double* auc, double* acc) {
     cudaStream_t s = ctx.stream;
-    MTK_CUDA(cub::DeviceRadixSort::SortKeys(w.tmp, w.tmp_bytes, w.kn, w.kn_sorted, (int)n, 0, 32, s));
     const int sms = device_sm_count(ctx.device);
-    const long long want = (n + AUC_THREADS - 1) / AUC_THREADS;
-    auc_member_count<<<(unsigned)std::min<long long>(want, 3LL * sms), AUC_THREADS, 0, s>>>(w.kn_sorted, w.kp,
-                                                                                          labels, n, w.cnt);
+    auc::auc_scan_kernel<<<1, auc::kThreads, 0, s>>>(w);
+    auc::auc_scatter_kernel<<<(unsigned)std::min<long long>(nblocks(n, 256), 8LL * sms), 256, 0, s>>>(w, labels, n);
+    ensure_smem_attr(reinterpret_cast<const void*>(auc::auc_bucket_kernel), auc::kBucketSmem);
+    auc::auc_bucket_kernel<<<sms, auc::kThreads, auc::kBucketSmem, s>>>(w);
+    count_launch();
+    count_launch();
     count_launch();
     unsigned long long* h = static_cast<unsigned long long*>(ctx.pinned_buf(64));
     MTK_CUDA(cudaMemcpyAsync(h, w.cnt, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
@@ -429,8 +394,8 @@ void auc_finish(Ctx& ctx, AucWork& w, const uint8_t* labels, long long n, double
 
 void auc_device(Ctx& ctx, const float* scores, const uint8_t* labels, long long n, double* auc,
                 double* acc) {
-    AucWork w = auc_work(ctx, n);
-    auc_keys_kernel<<<nblocks(n, 256), 256, 0, ctx.stream>>>(scores, labels, n, w.kn, w.kp, w.cnt);
+    auc::Work w = auc_work(ctx, n);
+    auc_keys_kernel<<<nblocks(n, 256), 256, 0, ctx.stream>>>(scores, labels, n, w);
     count_launch();
     auc_finish(ctx, w, labels, n, auc, acc);
 }
@@ -454,7 +419,7 @@ void attack_auc_fused(Ctx& ctx, const float* logits, long long rows, int C, cons
                       double* acc) {
     if (!attack_fused_ok(C, ATT_K, ATT_H, 2)) fail(MTK_ERROR, "attack_auc: unsupported shape");
     cudaStream_t s = ctx.stream;
-    // c_att is one symbol per device, shared by every context on it: the copy
+    // c_att2 is one symbol per device, shared by every context on it: the copy
     // of this call must not land while another context's scoring kernel still
     // reads the previous weights (a different stream, so no implicit order).
     // Per device, the stream waits on the event recorded after the last
@@ -463,16 +428,19 @@ void attack_auc_fused(Ctx& ctx, const float* logits, long long rows, int C, cons
     cudaEvent_t& last = att_last_use(ctx.device);
     if (last) MTK_CUDA(cudaStreamWaitEvent(s, last, 0));
     else MTK_CUDA(cudaEventCreateWithFlags(&last, cudaEventDisableTiming));
-    // the attack model's weights -> constant memory (stream-ordered device copies)
-    MTK_CUDA(cudaMemcpyToSymbolAsync(c_att, W0, ATT_K * ATT_H * 4, 0, cudaMemcpyDeviceToDevice, s));
-    MTK_CUDA(cudaMemcpyToSymbolAsync(c_att, b0, ATT_H * 4, ATT_K * ATT_H * 4, cudaMemcpyDeviceToDevice, s));
-    MTK_CUDA(cudaMemcpyToSymbolAsync(c_att, W1, ATT_H * 2 * 4, (ATT_K * ATT_H + ATT_H) * 4,
-                                     cudaMemcpyDeviceToDevice, s));
-    MTK_CUDA(cudaMemcpyToSymbolAsync(c_att, b1, 2 * 4, (ATT_K * ATT_H + ATT_H + ATT_H * 2) * 4,
-                                     cudaMemcpyDeviceToDevice, s));
-    AucWork w = auc_work(ctx, rows);
-    attack_score_kernel<16><<<nblocks(rows, 256), 256, 0, s>>>(logits, rows, C, labels, score_out, w.kn, w.kp,
-                                                               w.cnt);
+    // the attack model's weights -> constant memory as (w, w) pairs
+    // (stream-ordered: a device-side duplication, then one device copy)
+    constexpr int nw = ATT_K * ATT_H + ATT_H + ATT_H * 2 + 2;
+    auc::Work w = auc_work(ctx, rows);
+    float2* dup = reinterpret_cast<float2*>(w.mixed);  // free until the AUC passes
+    att_dup_kernel<<<1, 512, 0, s>>>(W0, b0, W1, b1, dup);
+    count_launch();
+    MTK_CUDA(cudaMemcpyToSymbolAsync(c_att2, dup, nw * sizeof(float2), 0, cudaMemcpyDeviceToDevice, s));
+    const long long thr = (rows + 1) / 2;
+    if (C == 10)
+        attack_score2_kernel<10, true><<<nblocks(thr, 256), 256, 0, s>>>(logits, rows, C, labels, score_out, w);
+    else
+        attack_score2_kernel<16, false><<<nblocks(thr, 256), 256, 0, s>>>(logits, rows, C, labels, score_out, w);
     count_launch();
     MTK_CUDA(cudaEventRecord(last, s));
     auc_finish(ctx, w, labels, rows, auc, acc);

@@ -127,3 +127,50 @@ def test_attack_auc_in_one_call(ctx, rows, C, dims, ties):
     sc = s1.cpu().numpy().astype(np.float64)
     assert abs(a1 - po.auc(sc, lab)) <= 1e-12
     assert abs(acc1 - po.accuracy(sc, lab, 0.5)) <= 1e-12
+
+
+def _u2_numpy(s, lab):
+    """exact U2 = sum over members of 2 #{non-members below} + #{equal}
+    (integers; numpy sort + searchsorted on float64 scores)"""
+    neg = np.sort(s[lab == 0].astype(np.float64))
+    pos = s[lab == 1].astype(np.float64)
+    lo = np.searchsorted(neg, pos, side="left")
+    hi = np.searchsorted(neg, pos, side="right")
+    return int((2 * lo + (hi - lo)).sum()), int(lab.sum())
+
+
+@pytest.mark.parametrize("case", ["spread", "few_values", "one_value", "signed_zero", "narrow", "huge_bucket",
+                                  "tiny"])
+def test_auc_histogram_paths_exact(ctx, case):
+    """The sort-free AUC (auc.cuh): cross-bucket counts, small buckets
+    (shared-memory sort), large buckets (> 8192 queries: 65536-bin histogram),
+    all-equal scores, -0.0 == +0.0, negative scores -- the AUC equals the
+    exact integer U2 / 2 / (npos nneg) computed independently."""
+    from paper_2011_09463_b200 import api
+
+    rng = np.random.default_rng(hash(case) % 2**32)
+    n = 300_000
+    if case == "spread":
+        s = rng.standard_normal(n).astype(np.float32) * 1e3
+    elif case == "few_values":  # 37 distinct values: every bucket large, many ties
+        s = (rng.integers(0, 37, n) / 37.0).astype(np.float32)
+    elif case == "one_value":
+        s = np.full(n, 0.3, dtype=np.float32)
+    elif case == "signed_zero":
+        s = np.where(rng.random(n) < 0.5, np.float32(0.0), np.float32(-0.0)).astype(np.float32)
+        s[:1000] = rng.standard_normal(1000).astype(np.float32)
+    elif case == "narrow":  # scores in [0.5, 0.5 + 2^-8): a handful of hi-16 buckets
+        s = (0.5 + rng.random(n) / 256).astype(np.float32)
+    elif case == "huge_bucket":  # one bucket with ~all queries, distinct low bits
+        s = np.float32(0.75) + (rng.integers(0, 60000, n) * np.float32(2.0 ** -24)).astype(np.float32)
+    else:
+        n = 5
+        s = np.array([0.1, 0.4, 0.35, 0.8, 0.4], dtype=np.float32)
+    lab = (rng.random(n) < 0.4).astype(np.uint8)
+    lab[0], lab[-1] = 1, 0
+    a, acc = api.auc(ctx, torch.tensor(s, device="cuda"), torch.tensor(lab, device="cuda"))
+    u2, npos = _u2_numpy(s, lab)
+    nneg = n - npos
+    assert a == (0.5 * u2) / (npos * nneg), (a, u2)
+    assert abs(a - po.auc(s.astype(np.float64), lab)) <= 1e-12
+    assert acc == float(((s > 0.5) == (lab == 1)).sum()) / n
