@@ -8,16 +8,16 @@
 //   1. (fused into the kernel that produces the scores) the key of every
 //      query and a per-class histogram of the key's top 16 bits
 //      (warp-aggregated integer atomics);
-//   2. auc_scan_kernel, one CTA: in bucket order, every member contributes
-//      2 #{non-members in lower buckets} -- summed exactly -- and the
-//      buckets holding both classes ("mixed") get a slot in a compacted,
-//      bucket-ordered array;
+//   2. auc_scan_totals_kernel + auc_scan_kernel (64 blocks each): in bucket
+//      order, every member contributes 2 #{non-members in lower buckets} --
+//      summed exactly -- and the buckets holding both classes ("mixed") get
+//      a slot in a compacted, bucket-ordered array;
 //   3. auc_scatter_kernel: the queries of mixed buckets go to their bucket's
 //      slot as (low 16 key bits << 1 | class);
 //   4. auc_bucket_kernel, one CTA per mixed bucket: within the bucket the
 //      members' 2 #{below} + #{equal} over the low 16 bits -- a shared-memory
-//      bitonic sort and a scan for buckets up to 8192 queries, a per-CTA
-//      65536-bin histogram of the non-members and its scan above that.
+//      bitonic sort and a scan for buckets up to 8192 queries, above that a
+//      65536-bin histogram of the non-members' low bits and its scan.
 // Integer sums are order-independent, so the AUC is deterministic and
 // bit-identical to the sort-based evaluation (and to oracle.c orc_auc's
 // ranks); no library sort on the path.
@@ -96,49 +96,71 @@ struct Work {
     uint32_t* cursor;     // [kBuckets]
     uint32_t* packed;     // [n]
     uint4* mixed;         // [kBuckets] (bucket, offset, size, non-members)
+    uint4* totals;        // [kBuckets / kThreads] per-block totals of the scan
     uint32_t* big;        // [grid][kBuckets] histogram scratch of the large-bucket path
     unsigned long long* cnt;  // [0] members, [1] hits at 0.5, [2] U2, [3] mixed buckets
 };
 
-// 2. bucket order: exact cross-bucket U2 part, mixed-bucket slots, histogram reset
+// 2. bucket order in two fully parallel passes over kScanBlocks blocks of
+// kThreads buckets (one bucket per thread, coalesced):
+//   a. per block: non-members, mixed buckets, mixed-bucket queries (totals)
+//   b. per block: its offsets = the totals of the blocks before it (each
+//      block sums them itself), then per bucket: the exact cross-bucket U2
+//      part (every member: 2 #{non-members in lower buckets}), the mixed
+//      bucket's slot in the compacted array, and the histogram reset
+constexpr int kScanBlocks = kBuckets / kThreads;  // 64
+__device__ __forceinline__ void load_bucket(const uint32_t* hist, int b, uint32_t& N, uint32_t& P) {
+    N = hist[b];
+    P = hist[kBuckets + b];
+}
+__global__ void __launch_bounds__(kThreads) auc_scan_totals_kernel(Work w) {
+    __shared__ uint32_t sh[33];
+    const int b = blockIdx.x * kThreads + threadIdx.x;
+    uint32_t N, P;
+    load_bucket(w.hist, b, N, P);
+    const bool mixed = N && P;
+    uint32_t t0, t1, t2;
+    block_excl_scan(N, sh, &t0);
+    block_excl_scan(mixed ? 1u : 0u, sh, &t1);
+    block_excl_scan(mixed ? N + P : 0u, sh, &t2);
+    if (threadIdx.x == 0) w.totals[blockIdx.x] = make_uint4(t0, t1, t2, 0);
+}
 __global__ void __launch_bounds__(kThreads) auc_scan_kernel(Work w) {
     __shared__ uint32_t sh[33];
     __shared__ unsigned long long shl[32];
-    constexpr int per = kBuckets / kThreads;  // 64 consecutive buckets per thread
-    const int b0 = threadIdx.x * per;
-    uint32_t n_neg = 0, n_mix = 0, n_slot = 0;
-    for (int i = 0; i < per; ++i) {
-        const uint32_t N = w.hist[b0 + i], P = w.hist[kBuckets + b0 + i];
-        n_neg += N;
-        const bool mixed = N && P;
-        n_mix += mixed;
-        n_slot += mixed ? N + P : 0;
-    }
-    uint32_t tot;
-    uint32_t below = block_excl_scan(n_neg, sh, &tot);
-    uint32_t mix = block_excl_scan(n_mix, sh, &tot);
-    const uint32_t nmixed = tot;
-    uint32_t off = block_excl_scan(n_slot, sh, &tot);
-    unsigned long long cross = 0;
-    for (int i = 0; i < per; ++i) {
-        const int b = b0 + i;
-        const uint32_t N = w.hist[b], P = w.hist[kBuckets + b];
-        cross += (unsigned long long)P * (2ull * below);
-        if (N && P) {
-            w.mixed[mix++] = make_uint4((uint32_t)b, off, N + P, N);
-            w.cursor[b] = off;
-            off += N + P;
-        } else {
-            w.cursor[b] = kNotMixed;
+    __shared__ uint32_t base[3];
+    if (threadIdx.x < 3) {
+        uint32_t a = 0;
+        for (int k = 0; k < (int)blockIdx.x; ++k) {
+            const uint4 t = w.totals[k];
+            a += threadIdx.x == 0 ? t.x : threadIdx.x == 1 ? t.y : t.z;
         }
-        below += N;
-        w.hist[b] = 0;  // clean for the next call
-        w.hist[kBuckets + b] = 0;
+        base[threadIdx.x] = a;
     }
+    const int b = blockIdx.x * kThreads + threadIdx.x;
+    uint32_t N, P;
+    load_bucket(w.hist, b, N, P);
+    const bool mixed = N && P;
+    uint32_t tot;
+    const uint32_t eN = block_excl_scan(N, sh, &tot);
+    const uint32_t eM = block_excl_scan(mixed ? 1u : 0u, sh, &tot);
+    const uint32_t mtot = tot;
+    const uint32_t eS = block_excl_scan(mixed ? N + P : 0u, sh, &tot);  // (syncs: base visible)
+    const uint32_t below = base[0] + eN;
+    unsigned long long cross = (unsigned long long)P * (2ull * below);
+    if (mixed) {
+        const uint32_t off = base[2] + eS;
+        w.mixed[base[1] + eM] = make_uint4((uint32_t)b, off, N + P, N);
+        w.cursor[b] = off;
+    } else {
+        w.cursor[b] = kNotMixed;
+    }
+    w.hist[b] = 0;  // clean for the next call
+    w.hist[kBuckets + b] = 0;
     cross = block_sum_u64(cross, shl);
     if (threadIdx.x == 0) {
-        atomicAdd(&w.cnt[2], cross);
-        w.cnt[3] = nmixed;
+        if (cross) atomicAdd(&w.cnt[2], cross);
+        if (blockIdx.x == gridDim.x - 1) w.cnt[3] = base[1] + mtot;
     }
 }
 
@@ -164,12 +186,57 @@ __global__ void auc_scatter_kernel(Work w, const uint8_t* lab, long long n) {
     }
 }
 
+// In-place exclusive scan of kBuckets counters, block-wide and conflict-free:
+// warp w owns counters [w * 2048, (w + 1) * 2048) and walks them in chunks of
+// 32 consecutive counters (one per lane), carrying the running sum; the
+// warps' totals are then scanned and added.  T: uint16_t (shared memory) or
+// uint32_t (global memory).
+template <class T>
+__device__ __forceinline__ void excl_scan_buckets(T* h, uint32_t* sh) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    constexpr int span = kBuckets / (kThreads / 32);  // 2048
+    T* base = h + wid * span;
+    uint32_t carry = 0;
+    for (int c = 0; c < span; c += 32) {
+        const uint32_t v = base[c + lane];
+        uint32_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        base[c + lane] = (T)(carry + x - v);
+        carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+    if (lane == 0) sh[wid] = carry;
+    __syncthreads();
+    if (wid == 0) {
+        const uint32_t v = sh[lane];
+        uint32_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        sh[lane] = x - v;
+    }
+    __syncthreads();
+    const uint32_t add = sh[wid];
+    for (int c = 0; c < span; c += 32) base[c + lane] = (T)(base[c + lane] + add);
+    __syncthreads();
+}
+
 // 4. within-bucket ranks of the members against the non-members
-constexpr int kBucketSmem = 2 * kSmallMax * 4;  // dynamic: the sorted bucket + its prefix counts
+//    small (<= kSmallMax queries): bitonic sort in shared memory + scan;
+//    large, < 65536 non-members: 16-bit counters of the non-members' low key
+//      bits in shared memory (128 KB), scanned in place;
+//    larger still: the same with 32-bit counters in global scratch.
+constexpr int kBucketSmem = kBuckets * 2;  // 128 KB: the u16 histogram (the small path uses 64 KB of it)
 __global__ void __launch_bounds__(kThreads) auc_bucket_kernel(Work w) {
     extern __shared__ uint32_t dsm[];
     uint32_t* buf = dsm;
     uint32_t* pre = dsm + kSmallMax;
+    uint16_t* h16 = reinterpret_cast<uint16_t*>(dsm);
     __shared__ uint32_t sh[33];
     __shared__ unsigned long long shl[32];
     const uint32_t nmixed = (uint32_t)w.cnt[3];
@@ -228,8 +295,28 @@ __global__ void __launch_bounds__(kThreads) auc_bucket_kernel(Work w) {
                 acc += (unsigned long long)pre[lo] + pre[e];
             }
             __syncthreads();
+        } else if (nneg < 65536u) {
+            uint32_t* h32 = dsm;  // pairs of u16 counters
+            for (int i = threadIdx.x; i < kBuckets / 2; i += blockDim.x) h32[i] = 0;
+            __syncthreads();
+            for (uint32_t e = threadIdx.x; e < s; e += blockDim.x) {
+                const uint32_t v = src[e];
+                if (!(v & 1u)) {
+                    const uint32_t x = v >> 1;
+                    atomicAdd(&h32[x >> 1], 1u << ((x & 1u) * 16));  // counts < 65536: no carry
+                }
+            }
+            __syncthreads();
+            excl_scan_buckets(h16, sh);  // prefixes < 65536 fit 16 bits
+            for (uint32_t e = threadIdx.x; e < s; e += blockDim.x) {
+                const uint32_t v = src[e];
+                if (!(v & 1u)) continue;
+                const uint32_t x = v >> 1;
+                const uint32_t below = h16[x], upto = x + 1 < (uint32_t)kBuckets ? h16[x + 1] : nneg;
+                acc += (unsigned long long)below + upto;  // 2 below + equal
+            }
+            __syncthreads();
         } else {
-            // large bucket: 65536-bin histogram of the non-members' low bits
             uint32_t* h = w.big + (size_t)blockIdx.x * kBuckets;
             for (int i = threadIdx.x; i < kBuckets; i += blockDim.x) h[i] = 0;
             __syncthreads();
@@ -238,24 +325,13 @@ __global__ void __launch_bounds__(kThreads) auc_bucket_kernel(Work w) {
                 if (!(v & 1u)) atomicAdd(&h[v >> 1], 1u);
             }
             __syncthreads();
-            constexpr int per = kBuckets / kThreads;
-            const int b0 = threadIdx.x * per;
-            uint32_t loc = 0;
-            for (int i = 0; i < per; ++i) loc += h[b0 + i];
-            uint32_t tot;
-            uint32_t run = block_excl_scan(loc, sh, &tot);
-            for (int i = 0; i < per; ++i) {
-                const uint32_t c = h[b0 + i];
-                h[b0 + i] = run;  // exclusive prefix: non-members below this value
-                run += c;
-            }
-            __syncthreads();
+            excl_scan_buckets(h, sh);
             for (uint32_t e = threadIdx.x; e < s; e += blockDim.x) {
                 const uint32_t v = src[e];
                 if (!(v & 1u)) continue;
                 const uint32_t x = v >> 1;
                 const uint32_t below = h[x], upto = x + 1 < (uint32_t)kBuckets ? h[x + 1] : nneg;
-                acc += (unsigned long long)below + upto;  // 2 below + equal
+                acc += (unsigned long long)below + upto;
             }
             __syncthreads();
         }

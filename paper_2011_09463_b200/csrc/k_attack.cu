@@ -354,7 +354,7 @@ auc::Work auc_work(Ctx& ctx, long long n) {
     auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
     const size_t hb = 2 * (size_t)auc::kBuckets * 4;
     char* p = static_cast<char*>(ctx.big(al(4 * n) * 2 + al(hb) + al(4 * auc::kBuckets) +
-                                         al(16 * auc::kBuckets) + al((size_t)grid * auc::kBuckets * 4) + al(64)));
+                                         al(16 * auc::kBuckets) + al(16 * auc::kScanBlocks) + al((size_t)grid * auc::kBuckets * 4) + al(64)));
     auto take = [&](size_t b) { char* r = p; p += al(b); return r; };
     auc::Work w;
     w.key = (uint32_t*)take(4 * n);
@@ -362,6 +362,7 @@ auc::Work auc_work(Ctx& ctx, long long n) {
     w.hist = (uint32_t*)take(hb);
     w.cursor = (uint32_t*)take(4 * auc::kBuckets);
     w.mixed = (uint4*)take(16 * auc::kBuckets);
+    w.totals = (uint4*)take(16 * auc::kScanBlocks);
     w.big = (uint32_t*)take((size_t)grid * auc::kBuckets * 4);
     w.cnt = (unsigned long long*)take(64);
     // hist is left zeroed by auc_scan_kernel, but the workspace may be new
@@ -374,7 +375,9 @@ auc::Work auc_work(Ctx& ctx, long long n) {
 void auc_finish(Ctx& ctx, auc::Work& w, const uint8_t* labels, long long n, double* auc, double* acc) {
     cudaStream_t s = ctx.stream;
     const int sms = device_sm_count(ctx.device);
-    auc::auc_scan_kernel<<<1, auc::kThreads, 0, s>>>(w);
+    auc::auc_scan_totals_kernel<<<auc::kScanBlocks, auc::kThreads, 0, s>>>(w);
+    auc::auc_scan_kernel<<<auc::kScanBlocks, auc::kThreads, 0, s>>>(w);
+    count_launch();
     auc::auc_scatter_kernel<<<(unsigned)std::min<long long>(nblocks(n, 256), 8LL * sms), 256, 0, s>>>(w, labels, n);
     ensure_smem_attr(reinterpret_cast<const void*>(auc::auc_bucket_kernel), auc::kBucketSmem);
     auc::auc_bucket_kernel<<<sms, auc::kThreads, auc::kBucketSmem, s>>>(w);

@@ -25,6 +25,10 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <vector>
 
 #include "internal.h"
 #include "sm100.cuh"
@@ -730,6 +734,9 @@ struct MmdWParams {
     // touch them -- list A, pairs (I >= ta in range, J >= I), contiguous in the
     // upper-triangle order from pair index pa; list B, pairs (I < ta, J in range)
     int ta, tb, pa, nA, nB;
+    // optional explicit item order (I, J) of one group, nA entries (nB = 0):
+    // the L2-blocked raster of large problems (mmd_w_order)
+    const int2* order;
     float* W;                  // [G][N][ldw] (rows outside [ta, tb) * WT never written)
     long long ldw;             // row stride of W (N, or N + 32 with the head block)
     float* rpart;              // [G][T][T][4][WT]: row sums of block (I, J), per column quarter
@@ -744,6 +751,13 @@ struct MmdWParams {
 __device__ __forceinline__ void pair_of(int p, int T, int& I, int& J);
 // work item of one group -> (I, J, pair index) over lists A then B (above)
 __device__ __forceinline__ void item_pair(const MmdWParams& p, int k, int& I, int& J, int& pidx) {
+    if (p.order) {
+        const int2 ij = p.order[k];
+        I = ij.x;
+        J = ij.y;
+        pidx = (int)((long long)I * p.T - (long long)I * (I - 1) / 2) + (J - I);
+        return;
+    }
     if (k < p.nA) {
         pidx = p.pa + k;
         pair_of(pidx, p.T, I, J);
@@ -1234,6 +1248,40 @@ __global__ void __launch_bounds__(WSUM_THREADS) mmd_wsum_kernel(const float* rpa
     if (threadIdx.x < 3) partial[((long long)g * T + I) * 3 + threadIdx.x] = total[threadIdx.x];
 }
 
+// Item order for large tile triangles: the tile pairs in S x S blocks (block
+// rows ascending, block columns >= block row; row-major inside a block), so
+// the ~148 pairs in flight at a time share ~2S tiles of Z (S = 16: 16 MB of
+// tf32 planes) and Z stays in L2 while W streams out.  The row-major order
+// sweeps all J for each I instead; at C4 (T = 576, 302 MB of planes) that
+// re-read Z from DRAM (ncu r09: 84 GB of DRAM traffic for 21.7 GB of W).
+// Only pairs touching the owned tiles [ta, tb) are listed.  Cached per
+// (device, T, ta, tb); the order does not change any pair's arithmetic.
+constexpr int kRasterMinT = 32, kRasterS = 16;
+const int2* mmd_w_order(int T, int ta, int tb, int* count, cudaStream_t s) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, int, int, int>, std::pair<int2*, int>> cache;
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_tuple(dev, T, ta, tb);
+    auto it = cache.find(key);
+    if (it == cache.end()) {
+        std::vector<int2> v;
+        const int nb = (T + kRasterS - 1) / kRasterS;
+        for (int bi = 0; bi < nb; ++bi)
+            for (int bj = bi; bj < nb; ++bj)
+                for (int I = bi * kRasterS; I < std::min(T, (bi + 1) * kRasterS); ++I)
+                    for (int J = std::max(I, bj * kRasterS); J < std::min(T, (bj + 1) * kRasterS); ++J)
+                        if ((I >= ta && I < tb) || (J >= ta && J < tb)) v.push_back(make_int2(I, J));
+        int2* d = nullptr;
+        MTK_CUDA(cudaMalloc(&d, v.size() * sizeof(int2)));
+        MTK_CUDA(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(int2), cudaMemcpyHostToDevice, s));
+        MTK_CUDA(cudaStreamSynchronize(s));
+        it = cache.emplace(key, std::make_pair(d, (int)v.size())).first;
+    }
+    *count = it->second.second;
+    return it->second.first;
+}
+
 // g = scale * (z * Wsum - sum_c V_c), the chunk partials summed in ascending
 // chunk order in fp64 (the multi-chunk V = W.Z of the materialised-W path)
 __global__ void mmd_vchunk_finish_kernel(const float* __restrict__ vpart, int chunks, long long per,
@@ -1469,6 +1517,14 @@ void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s, int stages) 
         w.pa = (int)S(wr.ta);
         w.nA = (int)(S(wr.tb) - S(wr.ta));
         w.nB = wr.ta * (wr.tb - wr.ta);
+        const char* re = getenv("MTK_MMDW_ROWMAJOR");  // A/B (read per call)
+        if (T >= kRasterMinT && a.G == 1 && !(re && re[0] == '1')) {
+            int cnt = 0;
+            w.order = mmd_w_order(T, wr.ta, wr.tb, &cnt, s);
+            if (cnt != w.nA + w.nB) fail(MTK_ERROR, "mmd: tile-pair raster size mismatch");
+            w.nA = cnt;
+            w.nB = 0;
+        }
         w.W = L.W;
         w.ldw = L.ldw;
         w.rpart = L.rpart;
