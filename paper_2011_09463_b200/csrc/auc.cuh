@@ -12,12 +12,14 @@
 //      order, every member contributes 2 #{non-members in lower buckets} --
 //      summed exactly -- and the buckets holding both classes ("mixed") get
 //      a slot in a compacted, bucket-ordered array;
-//   3. auc_scatter_kernel: the queries of mixed buckets go to their bucket's
-//      slot as (low 16 key bits << 1 | class);
+//   3. auc_scatter_kernel: the queries of small mixed buckets (<= 8192) go
+//      to their bucket's slot as (low 16 key bits << 1 | class); those of
+//      large ones into per-bucket class histograms of the low 16 bits
+//      (level 2, global integer atomics over 65536 bins);
 //   4. auc_bucket_kernel, one CTA per mixed bucket: within the bucket the
 //      members' 2 #{below} + #{equal} over the low 16 bits -- a shared-memory
-//      bitonic sort and a scan for buckets up to 8192 queries, above that a
-//      65536-bin histogram of the non-members' low bits and its scan.
+//      bitonic sort and a scan for small buckets, a scan of the level-2
+//      histograms for large ones.
 // Integer sums are order-independent, so the AUC is deterministic and
 // bit-identical to the sort-based evaluation (and to oracle.c orc_auc's
 // ranks); no library sort on the path.
@@ -32,6 +34,7 @@ constexpr int kBuckets = 65536;
 constexpr int kSmallMax = 8192;      // bitonic-sort path up to this many queries per bucket
 constexpr int kThreads = 1024;       // scan / bucket kernels
 constexpr uint32_t kNotMixed = 0xFFFFFFFFu;
+constexpr uint32_t kLargeFlag = 0x80000000u;  // cursor / mixed-entry flag: level-2 histogram slot
 
 // order-preserving map float -> uint32 (ascending), -0.0 == +0.0
 __device__ __forceinline__ uint32_t key_of(float v) {
@@ -97,7 +100,8 @@ struct Work {
     uint32_t* packed;     // [n]
     uint4* mixed;         // [kBuckets] (bucket, offset, size, non-members)
     uint4* totals;        // [kBuckets / kThreads] per-block totals of the scan
-    uint32_t* big;        // [grid][kBuckets] histogram scratch of the large-bucket path
+    uint32_t* big;        // (unused)
+    uint32_t* l2;         // [large slots][2][kBuckets] level-2 class histograms; zero on entry and exit
     unsigned long long* cnt;  // [0] members, [1] hits at 0.5, [2] U2, [3] mixed buckets
 };
 
@@ -118,37 +122,43 @@ __global__ void __launch_bounds__(kThreads) auc_scan_totals_kernel(Work w) {
     const int b = blockIdx.x * kThreads + threadIdx.x;
     uint32_t N, P;
     load_bucket(w.hist, b, N, P);
-    const bool mixed = N && P;
-    uint32_t t0, t1, t2;
+    const bool mixed = N && P, large = mixed && N + P > (uint32_t)kSmallMax;
+    uint32_t t0, t1, t2, t3;
     block_excl_scan(N, sh, &t0);
     block_excl_scan(mixed ? 1u : 0u, sh, &t1);
-    block_excl_scan(mixed ? N + P : 0u, sh, &t2);
-    if (threadIdx.x == 0) w.totals[blockIdx.x] = make_uint4(t0, t1, t2, 0);
+    block_excl_scan(mixed && !large ? N + P : 0u, sh, &t2);
+    block_excl_scan(large ? 1u : 0u, sh, &t3);
+    if (threadIdx.x == 0) w.totals[blockIdx.x] = make_uint4(t0, t1, t2, t3);
 }
 __global__ void __launch_bounds__(kThreads) auc_scan_kernel(Work w) {
     __shared__ uint32_t sh[33];
     __shared__ unsigned long long shl[32];
-    __shared__ uint32_t base[3];
-    if (threadIdx.x < 3) {
+    __shared__ uint32_t base[4];
+    if (threadIdx.x < 4) {
         uint32_t a = 0;
         for (int k = 0; k < (int)blockIdx.x; ++k) {
             const uint4 t = w.totals[k];
-            a += threadIdx.x == 0 ? t.x : threadIdx.x == 1 ? t.y : t.z;
+            a += threadIdx.x == 0 ? t.x : threadIdx.x == 1 ? t.y : threadIdx.x == 2 ? t.z : t.w;
         }
         base[threadIdx.x] = a;
     }
     const int b = blockIdx.x * kThreads + threadIdx.x;
     uint32_t N, P;
     load_bucket(w.hist, b, N, P);
-    const bool mixed = N && P;
+    const bool mixed = N && P, large = mixed && N + P > (uint32_t)kSmallMax;
     uint32_t tot;
     const uint32_t eN = block_excl_scan(N, sh, &tot);
     const uint32_t eM = block_excl_scan(mixed ? 1u : 0u, sh, &tot);
     const uint32_t mtot = tot;
-    const uint32_t eS = block_excl_scan(mixed ? N + P : 0u, sh, &tot);  // (syncs: base visible)
+    const uint32_t eS = block_excl_scan(mixed && !large ? N + P : 0u, sh, &tot);  // (syncs: base visible)
+    const uint32_t eL = block_excl_scan(large ? 1u : 0u, sh, &tot);
     const uint32_t below = base[0] + eN;
     unsigned long long cross = (unsigned long long)P * (2ull * below);
-    if (mixed) {
+    if (large) {  // level-2 class histograms of the low key bits, slot L
+        const uint32_t L = base[3] + eL;
+        w.mixed[base[1] + eM] = make_uint4((uint32_t)b | kLargeFlag, L, N + P, N);
+        w.cursor[b] = kLargeFlag | L;
+    } else if (mixed) {  // packed slot for the shared-memory sort
         const uint32_t off = base[2] + eS;
         w.mixed[base[1] + eM] = make_uint4((uint32_t)b, off, N + P, N);
         w.cursor[b] = off;
@@ -172,7 +182,12 @@ __global__ void auc_scatter_kernel(Work w, const uint8_t* lab, long long n) {
         const bool valid = i < n;
         const uint32_t k = valid ? w.key[i] : 0u;
         const uint32_t b = k >> 16;
-        const bool mixed = valid && w.cursor[b] != kNotMixed;
+        const uint32_t cur = valid ? w.cursor[b] : kNotMixed;
+        if (cur != kNotMixed && (cur & kLargeFlag)) {  // large bucket: level-2 histogram
+            const uint32_t L = cur & ~kLargeFlag;
+            atomicAdd(&w.l2[((size_t)L * 2 + (lab[i] ? 1u : 0u)) * kBuckets + (k & 0xFFFFu)], 1u);
+        }
+        const bool mixed = cur != kNotMixed && !(cur & kLargeFlag);
         const uint32_t tag = mixed ? b : 0xFFFFFFFFu;
         const unsigned peers = __match_any_sync(0xffffffffu, tag);
         const int lane = threadIdx.x & 31, leader = __ffs(peers) - 1;
@@ -186,66 +201,23 @@ __global__ void auc_scatter_kernel(Work w, const uint8_t* lab, long long n) {
     }
 }
 
-// In-place exclusive scan of kBuckets counters, block-wide and conflict-free:
-// warp w owns counters [w * 2048, (w + 1) * 2048) and walks them in chunks of
-// 32 consecutive counters (one per lane), carrying the running sum; the
-// warps' totals are then scanned and added.  T: uint16_t (shared memory) or
-// uint32_t (global memory).
-template <class T>
-__device__ __forceinline__ void excl_scan_buckets(T* h, uint32_t* sh) {
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    constexpr int span = kBuckets / (kThreads / 32);  // 2048
-    T* base = h + wid * span;
-    uint32_t carry = 0;
-    for (int c = 0; c < span; c += 32) {
-        const uint32_t v = base[c + lane];
-        uint32_t x = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        base[c + lane] = (T)(carry + x - v);
-        carry += __shfl_sync(0xffffffffu, x, 31);
-    }
-    if (lane == 0) sh[wid] = carry;
-    __syncthreads();
-    if (wid == 0) {
-        const uint32_t v = sh[lane];
-        uint32_t x = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        sh[lane] = x - v;
-    }
-    __syncthreads();
-    const uint32_t add = sh[wid];
-    for (int c = 0; c < span; c += 32) base[c + lane] = (T)(base[c + lane] + add);
-    __syncthreads();
-}
-
 // 4. within-bucket ranks of the members against the non-members
 //    small (<= kSmallMax queries): bitonic sort in shared memory + scan;
-//    large, < 65536 non-members: 16-bit counters of the non-members' low key
-//      bits in shared memory (128 KB), scanned in place;
-//    larger still: the same with 32-bit counters in global scratch.
-constexpr int kBucketSmem = kBuckets * 2;  // 128 KB: the u16 histogram (the small path uses 64 KB of it)
+//    large: a scan of the level-2 class histograms the scatter pass built.
+constexpr int kBucketSmem = 2 * kSmallMax * 4;  // the sorted bucket + its prefix counts
 __global__ void __launch_bounds__(kThreads) auc_bucket_kernel(Work w) {
     extern __shared__ uint32_t dsm[];
     uint32_t* buf = dsm;
     uint32_t* pre = dsm + kSmallMax;
-    uint16_t* h16 = reinterpret_cast<uint16_t*>(dsm);
     __shared__ uint32_t sh[33];
     __shared__ unsigned long long shl[32];
     const uint32_t nmixed = (uint32_t)w.cnt[3];
     unsigned long long acc = 0;
     for (uint32_t t = blockIdx.x; t < nmixed; t += gridDim.x) {
         const uint4 mb = w.mixed[t];
-        const uint32_t off = mb.y, s = mb.z, nneg = mb.w;
+        const uint32_t off = mb.y, s = mb.z;
         const uint32_t* src = w.packed + off;
-        if (s <= (uint32_t)kSmallMax) {
+        if (!(mb.x & kLargeFlag)) {
             uint32_t P = 32;
             while (P < s) P <<= 1;
             for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) buf[i] = i < s ? src[i] : 0xFFFFFFFFu;
@@ -295,43 +267,45 @@ __global__ void __launch_bounds__(kThreads) auc_bucket_kernel(Work w) {
                 acc += (unsigned long long)pre[lo] + pre[e];
             }
             __syncthreads();
-        } else if (nneg < 65536u) {
-            uint32_t* h32 = dsm;  // pairs of u16 counters
-            for (int i = threadIdx.x; i < kBuckets / 2; i += blockDim.x) h32[i] = 0;
-            __syncthreads();
-            for (uint32_t e = threadIdx.x; e < s; e += blockDim.x) {
-                const uint32_t v = src[e];
-                if (!(v & 1u)) {
-                    const uint32_t x = v >> 1;
-                    atomicAdd(&h32[x >> 1], 1u << ((x & 1u) * 16));  // counts < 65536: no carry
-                }
-            }
-            __syncthreads();
-            excl_scan_buckets(h16, sh);  // prefixes < 65536 fit 16 bits
-            for (uint32_t e = threadIdx.x; e < s; e += blockDim.x) {
-                const uint32_t v = src[e];
-                if (!(v & 1u)) continue;
-                const uint32_t x = v >> 1;
-                const uint32_t below = h16[x], upto = x + 1 < (uint32_t)kBuckets ? h16[x + 1] : nneg;
-                acc += (unsigned long long)below + upto;  // 2 below + equal
-            }
-            __syncthreads();
         } else {
-            uint32_t* h = w.big + (size_t)blockIdx.x * kBuckets;
-            for (int i = threadIdx.x; i < kBuckets; i += blockDim.x) h[i] = 0;
+            // large bucket: the level-2 class histograms built by the scatter
+            // pass; members at value v add 2 #{non-members below v} + #{at v};
+            // the histograms are zeroed again for the next call
+            uint32_t* hn = w.l2 + (size_t)off * 2 * kBuckets;  // off = the level-2 slot
+            uint32_t* hp = hn + kBuckets;
+            const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+            constexpr int span = kBuckets / (kThreads / 32);
+            uint32_t carry = 0;
+            for (int c = 0; c < span; c += 32) carry += hn[wid * span + c + lane];
+            carry = __reduce_add_sync(0xffffffffu, carry);
+            if (lane == 0) sh[wid] = carry;
             __syncthreads();
-            for (uint32_t e = threadIdx.x; e < s; e += blockDim.x) {
-                const uint32_t v = src[e];
-                if (!(v & 1u)) atomicAdd(&h[v >> 1], 1u);
+            if (wid == 0) {
+                const uint32_t v = sh[lane];
+                uint32_t x = v;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= o) x += y;
+                }
+                sh[lane] = x - v;
             }
             __syncthreads();
-            excl_scan_buckets(h, sh);
-            for (uint32_t e = threadIdx.x; e < s; e += blockDim.x) {
-                const uint32_t v = src[e];
-                if (!(v & 1u)) continue;
-                const uint32_t x = v >> 1;
-                const uint32_t below = h[x], upto = x + 1 < (uint32_t)kBuckets ? h[x + 1] : nneg;
-                acc += (unsigned long long)below + upto;
+            uint32_t run = sh[wid];  // non-members below this warp's values
+            for (int c = 0; c < span; c += 32) {
+                const int v = wid * span + c + lane;
+                const uint32_t nv = hn[v], pv = hp[v];
+                uint32_t x = nv;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= o) x += y;
+                }
+                const uint32_t below = run + x - nv;
+                acc += (unsigned long long)pv * (2ull * below + nv);
+                run += __shfl_sync(0xffffffffu, x, 31);
+                if (nv) hn[v] = 0;
+                if (pv) hp[v] = 0;
             }
             __syncthreads();
         }

@@ -37,12 +37,18 @@ namespace {
 // one device fp32 array (kept as a struct so the layer plumbing stays typed)
 struct Plane3 {
     float* f = nullptr;
+    // post-ReLU activations only: the ReLU mask as bits, [G][rows][ceil(cols / 32)]
+    // words (bit j of word w = column 32 w + j > 0), written by the tcgen05
+    // FWD epilogue and read by the DX epilogue instead of the fp32 plane
+    uint32_t* bits = nullptr;
 };
 
 void free3(Plane3& p, bool own_f = true) {
     if (own_f) cudaFree(p.f);
+    cudaFree(p.bits);
     p = Plane3{};
 }
+inline int mask_words(int cols) { return (cols + 31) / 32; }
 
 void alloc3(Plane3& p, size_t n) { MTK_CUDA(cudaMalloc(&p.f, n * sizeof(float))); }
 
@@ -238,7 +244,13 @@ struct mtk_bank {
         free_acts();
         const size_t GB = (size_t)G * B;
         H.assign(L, Plane3{});
-        for (int l = 1; l < L; ++l) alloc3(H[l], GB * dims[l]);
+        for (int l = 1; l < L; ++l) {
+            alloc3(H[l], GB * dims[l]);
+            // the mask bits, when both the FWD producing H[l] and the DX reading it are tcgen05 GEMMs
+            const char* nb = getenv("MTK_NO_MASK_BITS");  // A/B at bank allocation
+            if (tc[l - 1] && tc[l] && !(nb && nb[0] == '1'))
+                MTK_CUDA(cudaMalloc(&H[l].bits, GB * mask_words(dims[l]) * sizeof(uint32_t)));
+        }
         for (auto& z : dZ) alloc3(z, GB * maxd());
         MTK_CUDA(cudaMalloc(&logits, GB * dims[L] * sizeof(float)));
         MTK_CUDA(cudaMalloc(&row_loss, GB * sizeof(double)));
@@ -291,6 +303,12 @@ bool gemm_fwd(mtk_bank& k, int mat, const Plane3& in, int B, int r0, int rows, c
         u.ldc = fo;
         u.bias = k.b[mat];
         u.bias_gs = fo;
+        if (relu && out.bits) {
+            const int wd = mask_words(fo);
+            u.mbits = out.bits + (size_t)r0 * wd;
+            u.mb_gs = (long long)B * wd;
+            u.mb_ld = wd;
+        }
         u.flags = c.d_flags;
         launch_umma(u, c.stream);
     } else if (head_fwd_ok(fi, fo)) {
@@ -344,7 +362,7 @@ bool gemm_fwd(mtk_bank& k, int mat, const Plane3& in, int B, int r0, int rows, c
 // returns true when `colsum` received the per-32-row-block column sums of out
 // (the next layer's bias gradient), false when the caller must reduce it
 bool gemm_dx(mtk_bank& k, int mat, const Plane3& dz, int B, int r0, int rows, const Plane3& out,
-             const float* mask, const float* add, float* colsum = nullptr) {
+             const float* mask, const float* add, float* colsum = nullptr, const uint32_t* mbits = nullptr) {
     Ctx& c = *k.ctx;
     const int fi = k.fan_in(mat), fo = k.fan_out(mat);
     if (k.tc[k.layer_of(mat)]) {
@@ -366,6 +384,12 @@ bool gemm_dx(mtk_bank& k, int mat, const Plane3& dz, int B, int r0, int rows, co
         u.c_gs = (long long)B * fi;
         u.ldc = fi;
         u.mask = mask + (size_t)r0 * fi;
+        if (mbits) {  // the mask as bits (written by the FWD epilogue of the layer below)
+            const int wd = mask_words(fi);
+            u.mbits = const_cast<uint32_t*>(mbits) + (size_t)r0 * wd;
+            u.mb_gs = (long long)B * wd;
+            u.mb_ld = wd;
+        }
         u.add = add ? add + (size_t)r0 * fi : nullptr;
         u.colsum = colsum;
         u.flags = c.d_flags;
@@ -787,14 +811,14 @@ void train_step(mtk_bank& k, const mtk_step& s, double* loss_host, double* mmd_h
         if (need_dx && !fused_here) {
             PhaseScope ph(c, kPhDx, split ? 2 : 1);
             if (split) {
-                gemm_dx(k, l, *cur, B, 0, src, out, k.H[l].f, nullptr);
-                gemm_dx(k, l + 1, *cur, B, src, B - src, out, k.H[l].f, nullptr);
+                gemm_dx(k, l, *cur, B, 0, src, out, k.H[l].f, nullptr, nullptr, k.H[l].bits);
+                gemm_dx(k, l + 1, *cur, B, src, B - src, out, k.H[l].f, nullptr, nullptr, k.H[l].bits);
                 after_launch(c, 2);
             } else {
                 const bool below_trainable = l - 1 >= s.frozen_layers && !no_colsum;
                 if (below_trainable) before_colsum_write(l - 1);
                 const bool have = gemm_dx(k, l, *cur, B, 0, B, out, k.H[l].f, add,
-                                          below_trainable ? k.colsum[(l - 1) % 3] : nullptr);
+                                          below_trainable ? k.colsum[(l - 1) % 3] : nullptr, k.H[l].bits);
                 after_launch(c);
                 next_colsum = have;
             }

@@ -89,6 +89,17 @@ void* Ctx::big(size_t bytes) {
     return d_big;
 }
 
+uint32_t* Ctx::auc_l2(size_t bytes) {
+    if (bytes > auc_l2_bytes) {
+        if (d_auc_l2) MTK_CUDA(cudaFree(d_auc_l2));  // synchronizes: in-flight users are done
+        d_auc_l2 = nullptr;
+        MTK_CUDA(cudaMalloc(&d_auc_l2, bytes));
+        MTK_CUDA(cudaMemsetAsync(d_auc_l2, 0, bytes, stream));
+        auc_l2_bytes = bytes;
+    }
+    return d_auc_l2;
+}
+
 void* Ctx::pinned_buf(size_t bytes) {
     if (bytes > pinned_bytes) {
         if (pinned) MTK_CUDA(cudaFreeHost(pinned));
@@ -215,6 +226,7 @@ int mtk_ctx_destroy(mtk_ctx* c) {
         cudaFree(c->d_flags);
         cudaFree(c->d_scratch);
         cudaFree(c->d_big);
+        cudaFree(c->d_auc_l2);
         if (c->pinned) cudaFreeHost(c->pinned);
         if (c->pinned_flags) cudaFreeHost(c->pinned_flags);
         if (c->own_stream) cudaStreamDestroy(c->stream);

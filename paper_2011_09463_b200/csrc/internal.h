@@ -59,6 +59,11 @@ struct Ctx {
     void* d_big = nullptr;
     size_t big_bytes = 0;
     void* pinned_buf(size_t bytes);
+    // AUC level-2 class histograms (auc.cuh): grow-only, zeroed when allocated
+    // and left zeroed by every call
+    uint32_t* auc_l2(size_t bytes);
+    uint32_t* d_auc_l2 = nullptr;
+    size_t auc_l2_bytes = 0;
     void check_flags();               // synchronizes; throws on a set flag
     // Side stream for short, latency-bound kernels that do not feed the next
     // main-stream launch (bias updates, the skinny head dW, the MMD prep pass):
@@ -219,6 +224,10 @@ struct UmmaGemm {
     // the operands are of one sign (e.g. MMD V = W.Z, W >= 0, Z = post-ReLU
     // h >= 0): accumulate the 3xTF32 corrections separately whatever K is
     int same_sign = 0;
+    // ReLU mask bits [G][M][mb_ld words], bit j of word w = column 32 w + j:
+    // kBiasRelu writes them (output > 0), kMask reads them instead of `mask`
+    uint32_t* mbits = nullptr;
+    long long mb_gs = 0, mb_ld = 0;
     int* flags = nullptr;
 };
 void launch_umma(const UmmaGemm& u, cudaStream_t s);

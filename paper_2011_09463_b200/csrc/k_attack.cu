@@ -223,41 +223,52 @@ __device__ __forceinline__ void top3_of_row(const float* x, int C, float (&top)[
     }
 }
 
-template <int CC, bool EXACT>
+template <int CC, bool EXACT, int QP>  // QP query pairs per thread
 __global__ void __launch_bounds__(256) attack_score2_kernel(const float* logits, long long rows, int C,
                                                             const uint8_t* lab, float* score_out, auc::Work w) {
-    const long long r0 = 2 * (blockIdx.x * (long long)blockDim.x + threadIdx.x);
-    float ta[ATT_K], tb[ATT_K];
-    const bool va = r0 < rows, vb = r0 + 1 < rows;
-    if (va) top3_of_row<CC, EXACT>(logits + r0 * C, C, ta);
-    else ta[0] = ta[1] = ta[2] = 0.f;
-    if (vb) top3_of_row<CC, EXACT>(logits + (r0 + 1) * C, C, tb);
-    else tb[0] = tb[1] = tb[2] = 0.f;
+    const long long r0 = 2LL * QP * (blockIdx.x * (long long)blockDim.x + threadIdx.x);
+    float2 t[QP][ATT_K];
+#pragma unroll
+    for (int q = 0; q < QP; ++q) {
+        float ta[ATT_K], tb[ATT_K];
+        const long long ra = r0 + 2 * q;
+        if (ra < rows) top3_of_row<CC, EXACT>(logits + ra * C, C, ta);
+        else ta[0] = ta[1] = ta[2] = 0.f;
+        if (ra + 1 < rows) top3_of_row<CC, EXACT>(logits + (ra + 1) * C, C, tb);
+        else tb[0] = tb[1] = tb[2] = 0.f;
+#pragma unroll
+        for (int a = 0; a < ATT_K; ++a) t[q][a] = make_float2(ta[a], tb[a]);
+    }
     const float2* W0 = c_att2;
     const float2* B0 = W0 + ATT_K * ATT_H;
     const float2* W1 = B0 + ATT_H;
     const float2* B1 = W1 + ATT_H * 2;
-    const float2 t0 = make_float2(ta[0], tb[0]), t1 = make_float2(ta[1], tb[1]), t2 = make_float2(ta[2], tb[2]);
-    float2 o0 = make_float2(0.f, 0.f), o1 = make_float2(0.f, 0.f);
+    float2 o0[QP], o1[QP];
 #pragma unroll
+    for (int q = 0; q < QP; ++q) o0[q] = o1[q] = make_float2(0.f, 0.f);
+#pragma unroll 8
     for (int h = 0; h < ATT_H; ++h) {
-        float2 acc = __ffma2_rn(t0, W0[h], make_float2(0.f, 0.f));
-        acc = __ffma2_rn(t1, W0[ATT_H + h], acc);
-        acc = __ffma2_rn(t2, W0[2 * ATT_H + h], acc);
-        float2 hv = __fadd2_rn(acc, B0[h]);
-        hv.x = hv.x > 0.f ? hv.x : 0.f;
-        hv.y = hv.y > 0.f ? hv.y : 0.f;
-        o0 = __ffma2_rn(hv, W1[h * 2], o0);
-        o1 = __ffma2_rn(hv, W1[h * 2 + 1], o1);
+        const float2 w0 = W0[h], w1 = W0[ATT_H + h], w2 = W0[2 * ATT_H + h], bb = B0[h];
+        const float2 v0 = W1[h * 2], v1 = W1[h * 2 + 1];
+#pragma unroll
+        for (int q = 0; q < QP; ++q) {
+            float2 acc = __ffma2_rn(t[q][0], w0, make_float2(0.f, 0.f));
+            acc = __ffma2_rn(t[q][1], w1, acc);
+            acc = __ffma2_rn(t[q][2], w2, acc);
+            float2 hv = __fadd2_rn(acc, bb);
+            hv.x = hv.x > 0.f ? hv.x : 0.f;
+            hv.y = hv.y > 0.f ? hv.y : 0.f;
+            o0[q] = __ffma2_rn(hv, v0, o0[q]);
+            o1[q] = __ffma2_rn(hv, v1, o1[q]);
+        }
     }
-    o0 = __fadd2_rn(o0, B1[0]);
-    o1 = __fadd2_rn(o1, B1[1]);
     unsigned long long pos = 0, hit = 0;
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < 2 * QP; ++q) {
         const long long r = r0 + q;
-        const bool valid = q ? vb : va;
-        const float p0 = q ? o0.y : o0.x, p1 = q ? o1.y : o1.x;
+        const bool valid = r < rows;
+        const float2 a = __fadd2_rn(o0[q / 2], B1[0]), b = __fadd2_rn(o1[q / 2], B1[1]);
+        const float p0 = (q & 1) ? a.y : a.x, p1 = (q & 1) ? b.y : b.x;
         uint32_t u = 0;
         bool l = false;
         if (valid) {  // member posterior: column_kernel's softmax column 1
@@ -350,11 +361,10 @@ namespace {
 // scattered mixed buckets, the large-bucket histograms, counters
 auc::Work auc_work(Ctx& ctx, long long n) {
     if (n > 0x7fffffffLL) fail(MTK_SHAPE_ERROR, "auc: more than 2^31 rows");
-    const int grid = device_sm_count(ctx.device);
     auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
     const size_t hb = 2 * (size_t)auc::kBuckets * 4;
     char* p = static_cast<char*>(ctx.big(al(4 * n) * 2 + al(hb) + al(4 * auc::kBuckets) +
-                                         al(16 * auc::kBuckets) + al(16 * auc::kScanBlocks) + al((size_t)grid * auc::kBuckets * 4) + al(64)));
+                                         al(16 * auc::kBuckets) + al(16 * auc::kScanBlocks) + al(64)));
     auto take = [&](size_t b) { char* r = p; p += al(b); return r; };
     auc::Work w;
     w.key = (uint32_t*)take(4 * n);
@@ -363,7 +373,9 @@ auc::Work auc_work(Ctx& ctx, long long n) {
     w.cursor = (uint32_t*)take(4 * auc::kBuckets);
     w.mixed = (uint4*)take(16 * auc::kBuckets);
     w.totals = (uint4*)take(16 * auc::kScanBlocks);
-    w.big = (uint32_t*)take((size_t)grid * auc::kBuckets * 4);
+    w.big = nullptr;
+    // at most n / kSmallMax buckets can be large: one level-2 slot each
+    w.l2 = ctx.auc_l2((size_t)(n / auc::kSmallMax + 1) * 2 * auc::kBuckets * 4);
     w.cnt = (unsigned long long*)take(64);
     // hist is left zeroed by auc_scan_kernel, but the workspace may be new
     MTK_CUDA(cudaMemsetAsync(w.hist, 0, hb, ctx.stream));
@@ -439,11 +451,12 @@ void attack_auc_fused(Ctx& ctx, const float* logits, long long rows, int C, cons
     att_dup_kernel<<<1, 512, 0, s>>>(W0, b0, W1, b1, dup);
     count_launch();
     MTK_CUDA(cudaMemcpyToSymbolAsync(c_att2, dup, nw * sizeof(float2), 0, cudaMemcpyDeviceToDevice, s));
-    const long long thr = (rows + 1) / 2;
+    constexpr int QP = 2;  // two query pairs per thread: weights loaded once per four queries
+    const long long thr = (rows + 2 * QP - 1) / (2 * QP);
     if (C == 10)
-        attack_score2_kernel<10, true><<<nblocks(thr, 256), 256, 0, s>>>(logits, rows, C, labels, score_out, w);
+        attack_score2_kernel<10, true, QP><<<nblocks(thr, 128), 128, 0, s>>>(logits, rows, C, labels, score_out, w);
     else
-        attack_score2_kernel<16, false><<<nblocks(thr, 256), 256, 0, s>>>(logits, rows, C, labels, score_out, w);
+        attack_score2_kernel<16, false, QP><<<nblocks(thr, 128), 128, 0, s>>>(logits, rows, C, labels, score_out, w);
     count_launch();
     MTK_CUDA(cudaEventRecord(last, s));
     auc_finish(ctx, w, labels, rows, auc, acc);

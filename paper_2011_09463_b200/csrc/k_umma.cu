@@ -92,6 +92,8 @@ struct UmmaParams {
     int zmask;            // kMmdGrad: C *= (add > 0) (the fused head DX)
     CUtensorMap b2;       // B rows k >= ksplit come from here (row k - ksplit); ksplit % 32 == 0
     int ksplit;           // K if there is no second B operand
+    uint32_t* mbits;      // ReLU mask bits (kBiasRelu writes, kMask reads), [G][M][mb_ld]
+    long long mb_gs, mb_ld;
     int* flags;
     unsigned long long* trace;  // diagnostics: timestamps of CTA (0,0,0)
 };
@@ -226,7 +228,10 @@ __device__ __forceinline__ void epilogue_rows(const UmmaParams& p, uint32_t tmem
             const float* s1 = nullptr;
             const float* s2 = nullptr;
             if (epi == (int)Epi::kBias || epi == (int)Epi::kBiasRelu) s1 = p.bias + g * p.bias_gs + nb;
-            else if (epi == (int)Epi::kMask) { s1 = p.mask + rowbase + nb; s2 = p.add ? p.add + rowbase + nb : nullptr; }
+            else if (epi == (int)Epi::kMask) {
+                s1 = p.mbits ? nullptr : p.mask + rowbase + nb;
+                s2 = p.add ? p.add + rowbase + nb : nullptr;
+            }
             else if (epi == (int)Epi::kSgd) s1 = p.C + rowbase + nb;
             else if (epi == (int)Epi::kMmdGrad) s1 = p.add + rowbase + nb;
 #pragma unroll
@@ -235,6 +240,9 @@ __device__ __forceinline__ void epilogue_rows(const UmmaParams& p, uint32_t tmem
                 o2[j] = s2 ? *reinterpret_cast<const float4*>(s2 + 4 * j) : make_float4(0.f, 0.f, 0.f, 0.f);
             }
         }
+        const uint32_t mword = (p.mbits && row_ok && epi == (int)Epi::kMask)
+                                   ? p.mbits[(long long)g * p.mb_gs + (long long)m * p.mb_ld + nb / 32]
+                                   : 0u;
         float v[32];
         tmem_ld_32x32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(c * 32), v);
         if (SEPC) {  // main + corrections, one fp32 add (8 columns at a time: registers)
@@ -270,10 +278,18 @@ __device__ __forceinline__ void epilogue_rows(const UmmaParams& p, uint32_t tmem
                         x.z = o2[j].z + x.z;
                         x.w = o2[j].w + x.w;
                     }
-                    x.x = o1[j].x > 0.f ? x.x : 0.f;
-                    x.y = o1[j].y > 0.f ? x.y : 0.f;
-                    x.z = o1[j].z > 0.f ? x.z : 0.f;
-                    x.w = o1[j].w > 0.f ? x.w : 0.f;
+                    if (p.mbits) {
+                        const uint32_t mb = mword >> (4 * j);
+                        x.x = (mb & 1u) ? x.x : 0.f;
+                        x.y = (mb & 2u) ? x.y : 0.f;
+                        x.z = (mb & 4u) ? x.z : 0.f;
+                        x.w = (mb & 8u) ? x.w : 0.f;
+                    } else {
+                        x.x = o1[j].x > 0.f ? x.x : 0.f;
+                        x.y = o1[j].y > 0.f ? x.y : 0.f;
+                        x.z = o1[j].z > 0.f ? x.z : 0.f;
+                        x.w = o1[j].w > 0.f ? x.w : 0.f;
+                    }
                 } else if (epi == (int)Epi::kMmdGrad) {  // o1 = z row, rowvec = Wsum
                     const float rv = p.rowvec[(long long)g * p.M + m];
                     x.x = p.scale * fmaf(o1[j].x, rv, -x.x);
@@ -314,7 +330,7 @@ __device__ __forceinline__ void epilogue_rows(const UmmaParams& p, uint32_t tmem
                         if (epi == (int)Epi::kBiasRelu) x = x > 0.f ? x : 0.f;
                     } else if (epi == (int)Epi::kMask) {
                         if (p.add) x = p.add[idx] + x;
-                        x = (p.mask[idx] > 0.f) ? x : 0.f;
+                        x = (p.mbits ? ((mword >> j) & 1u) != 0 : p.mask[idx] > 0.f) ? x : 0.f;
                     } else if (epi == (int)Epi::kMmdGrad) {
                         const float z = p.add[idx];
                         x = p.scale * fmaf(z, p.rowvec[(long long)g * p.M + m], -x);
@@ -331,6 +347,12 @@ __device__ __forceinline__ void epilogue_rows(const UmmaParams& p, uint32_t tmem
                 }
                 v[j] = x;
             }
+        }
+        if (epi == (int)Epi::kBiasRelu && p.mbits && row_ok) {  // the ReLU mask of this chunk as bits
+            uint32_t word = 0;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) word |= (v[j] > 0.f ? 1u : 0u) << j;
+            p.mbits[(long long)g * p.mb_gs + (long long)m * p.mb_ld + nb / 32] = word;
         }
         if (p.colsum && (epi == (int)Epi::kMask || epi == (int)Epi::kMmdGrad) && mw < p.M) {
             // per-32-row-block column sums of the stored values (next layer's db)
@@ -695,6 +717,12 @@ void launch_umma(const UmmaGemm& u, cudaStream_t s) {
     p.scale = u.scale;
     p.zmask = u.zmask;
     p.ksplit = u.K;
+    p.mbits = u.mbits;
+    p.mb_gs = u.mb_gs;
+    p.mb_ld = u.mb_ld;
+    if (u.mbits && (u.epi == Epi::kMask || u.epi == Epi::kBiasRelu) && u.mb_ld < (u.N + 31) / 32)
+        fail(MTK_ERROR, "umma: mask-bit rows shorter than ceil(N / 32) words");
+    if (u.epi != Epi::kMask && u.epi != Epi::kBiasRelu) p.mbits = nullptr;
     if (u.b2) {  // K = [0, ksplit) from b, [ksplit, K) from b2 (same major-ness)
         if (u.ksplit <= 0 || u.ksplit % BK || u.ksplit >= u.K || u.b_mn != 1)
             fail(MTK_ERROR, "umma: split B needs an N-major B and ksplit % 32 == 0 inside K");
