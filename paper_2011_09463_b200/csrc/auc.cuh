@@ -102,7 +102,8 @@ struct Work {
     uint4* totals;        // [kBuckets / kThreads] per-block totals of the scan
     uint32_t* big;        // (unused)
     uint32_t* l2;         // [large slots][2][kBuckets] level-2 class histograms; zero on entry and exit
-    unsigned long long* cnt;  // [0] members, [1] hits at 0.5, [2] U2, [3] mixed buckets
+    uint32_t* l2tot;      // [large slots][kBuckets / kThreads] block totals of the non-member counts
+    unsigned long long* cnt;  // [0] members, [1] hits at 0.5, [2] U2, [3] mixed, [4] large buckets
 };
 
 // 2. bucket order in two fully parallel passes over kScanBlocks blocks of
@@ -152,6 +153,7 @@ __global__ void __launch_bounds__(kThreads) auc_scan_kernel(Work w) {
     const uint32_t mtot = tot;
     const uint32_t eS = block_excl_scan(mixed && !large ? N + P : 0u, sh, &tot);  // (syncs: base visible)
     const uint32_t eL = block_excl_scan(large ? 1u : 0u, sh, &tot);
+    const uint32_t ltot = tot;
     const uint32_t below = base[0] + eN;
     unsigned long long cross = (unsigned long long)P * (2ull * below);
     if (large) {  // level-2 class histograms of the low key bits, slot L
@@ -170,7 +172,10 @@ __global__ void __launch_bounds__(kThreads) auc_scan_kernel(Work w) {
     cross = block_sum_u64(cross, shl);
     if (threadIdx.x == 0) {
         if (cross) atomicAdd(&w.cnt[2], cross);
-        if (blockIdx.x == gridDim.x - 1) w.cnt[3] = base[1] + mtot;
+        if (blockIdx.x == gridDim.x - 1) {
+            w.cnt[3] = base[1] + mtot;
+            w.cnt[4] = base[3] + ltot;
+        }
     }
 }
 
@@ -202,8 +207,9 @@ __global__ void auc_scatter_kernel(Work w, const uint8_t* lab, long long n) {
 }
 
 // 4. within-bucket ranks of the members against the non-members
-//    small (<= kSmallMax queries): bitonic sort in shared memory + scan;
-//    large: a scan of the level-2 class histograms the scatter pass built.
+//    small (<= kSmallMax queries): bitonic sort in shared memory + scan (here);
+//    large: a grid-wide scan of the level-2 class histograms the scatter pass
+//    built (auc_l2_totals_kernel, auc_l2_kernel: blocks of 1024 bins).
 constexpr int kBucketSmem = 2 * kSmallMax * 4;  // the sorted bucket + its prefix counts
 __global__ void __launch_bounds__(kThreads) auc_bucket_kernel(Work w) {
     extern __shared__ uint32_t dsm[];
@@ -267,48 +273,50 @@ __global__ void __launch_bounds__(kThreads) auc_bucket_kernel(Work w) {
                 acc += (unsigned long long)pre[lo] + pre[e];
             }
             __syncthreads();
-        } else {
-            // large bucket: the level-2 class histograms built by the scatter
-            // pass; members at value v add 2 #{non-members below v} + #{at v};
-            // the histograms are zeroed again for the next call
-            uint32_t* hn = w.l2 + (size_t)off * 2 * kBuckets;  // off = the level-2 slot
-            uint32_t* hp = hn + kBuckets;
-            const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-            constexpr int span = kBuckets / (kThreads / 32);
-            uint32_t carry = 0;
-            for (int c = 0; c < span; c += 32) carry += hn[wid * span + c + lane];
-            carry = __reduce_add_sync(0xffffffffu, carry);
-            if (lane == 0) sh[wid] = carry;
-            __syncthreads();
-            if (wid == 0) {
-                const uint32_t v = sh[lane];
-                uint32_t x = v;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-                    if (lane >= o) x += y;
-                }
-                sh[lane] = x - v;
-            }
-            __syncthreads();
-            uint32_t run = sh[wid];  // non-members below this warp's values
-            for (int c = 0; c < span; c += 32) {
-                const int v = wid * span + c + lane;
-                const uint32_t nv = hn[v], pv = hp[v];
-                uint32_t x = nv;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-                    if (lane >= o) x += y;
-                }
-                const uint32_t below = run + x - nv;
-                acc += (unsigned long long)pv * (2ull * below + nv);
-                run += __shfl_sync(0xffffffffu, x, 31);
-                if (nv) hn[v] = 0;
-                if (pv) hp[v] = 0;
-            }
-            __syncthreads();
         }
+    }
+    acc = block_sum_u64(acc, shl);
+    if (threadIdx.x == 0 && acc) atomicAdd(&w.cnt[2], acc);
+}
+
+// 5. large buckets: members at low bits v add 2 #{non-members below v} +
+// #{non-members at v}; work items (slot L, block j of kThreads bins), grid-
+// stride, in two passes (block totals of the non-members, then the scan with
+// the totals of the blocks before); the histograms are zeroed again
+constexpr int kL2Blocks = kBuckets / kThreads;  // 64 blocks of bins per slot
+__global__ void __launch_bounds__(kThreads) auc_l2_totals_kernel(Work w) {
+    __shared__ uint32_t sh[33];
+    const uint32_t items = (uint32_t)w.cnt[4] * kL2Blocks;
+    for (uint32_t it = blockIdx.x; it < items; it += gridDim.x) {
+        const uint32_t L = it / kL2Blocks, j = it % kL2Blocks;
+        const uint32_t nv = w.l2[(size_t)L * 2 * kBuckets + j * kThreads + threadIdx.x];
+        uint32_t tot;
+        block_excl_scan(nv, sh, &tot);
+        if (threadIdx.x == 0) w.l2tot[it] = tot;
+    }
+}
+__global__ void __launch_bounds__(kThreads) auc_l2_kernel(Work w) {
+    __shared__ uint32_t sh[33];
+    __shared__ unsigned long long shl[32];
+    __shared__ uint32_t base;
+    const uint32_t items = (uint32_t)w.cnt[4] * kL2Blocks;
+    unsigned long long acc = 0;
+    for (uint32_t it = blockIdx.x; it < items; it += gridDim.x) {
+        const uint32_t L = it / kL2Blocks, j = it % kL2Blocks;
+        if (threadIdx.x < 32) {
+            uint32_t a = 0;
+            for (uint32_t k = threadIdx.x; k < j; k += 32) a += w.l2tot[L * kL2Blocks + k];
+            a = __reduce_add_sync(0xffffffffu, a);
+            if (threadIdx.x == 0) base = a;
+        }
+        uint32_t* hn = w.l2 + (size_t)L * 2 * kBuckets + j * kThreads + threadIdx.x;
+        uint32_t* hp = hn + kBuckets;
+        const uint32_t nv = *hn, pv = *hp;
+        uint32_t tot;
+        const uint32_t e = block_excl_scan(nv, sh, &tot);  // (syncs: base visible)
+        acc += (unsigned long long)pv * (2ull * (base + e) + nv);
+        if (nv) *hn = 0;
+        if (pv) *hp = 0;
     }
     acc = block_sum_u64(acc, shl);
     if (threadIdx.x == 0 && acc) atomicAdd(&w.cnt[2], acc);
