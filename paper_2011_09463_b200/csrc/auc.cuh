@@ -31,7 +31,8 @@ namespace mtk {
 namespace auc {
 
 constexpr int kBuckets = 65536;
-constexpr int kSmallMax = 8192;      // bitonic-sort path up to this many queries per bucket
+constexpr int kSmallMax = 2048;      // bitonic-sort path up to this many queries per bucket
+constexpr int kBucketThreads = 256;  // small-bucket kernel: one CTA per bucket, 8 per SM
 constexpr int kThreads = 1024;       // scan / bucket kernels
 constexpr uint32_t kNotMixed = 0xFFFFFFFFu;
 constexpr uint32_t kLargeFlag = 0x80000000u;  // cursor / mixed-entry flag: level-2 histogram slot
@@ -52,7 +53,7 @@ __device__ __forceinline__ void hist_add(uint32_t* hist, uint32_t key, bool memb
     if (valid && lane == __ffs(peers) - 1) atomicAdd(&hist[tag], (uint32_t)__popc(peers));
 }
 
-// block-wide exclusive scan of one u32 per thread (kThreads threads); returns
+// block-wide exclusive scan of one u32 per thread (any multiple of 32 threads); returns
 // the thread's exclusive prefix, *total the block total
 __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* sh, uint32_t* total) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -65,7 +66,7 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* sh, ui
     if (lane == 31) sh[w] = x;
     __syncthreads();
     if (w == 0) {
-        uint32_t s = sh[lane];
+        uint32_t s = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0u;
         uint32_t t = s;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -211,7 +212,7 @@ __global__ void auc_scatter_kernel(Work w, const uint8_t* lab, long long n) {
 //    large: a grid-wide scan of the level-2 class histograms the scatter pass
 //    built (auc_l2_totals_kernel, auc_l2_kernel: blocks of 1024 bins).
 constexpr int kBucketSmem = 2 * kSmallMax * 4;  // the sorted bucket + its prefix counts
-__global__ void __launch_bounds__(kThreads) auc_bucket_kernel(Work w) {
+__global__ void __launch_bounds__(kBucketThreads) auc_bucket_kernel(Work w) {
     extern __shared__ uint32_t dsm[];
     uint32_t* buf = dsm;
     uint32_t* pre = dsm + kSmallMax;

@@ -395,7 +395,7 @@ void auc_finish(Ctx& ctx, auc::Work& w, const uint8_t* labels, long long n, doub
     count_launch();
     auc::auc_scatter_kernel<<<(unsigned)std::min<long long>(nblocks(n, 256), 8LL * sms), 256, 0, s>>>(w, labels, n);
     ensure_smem_attr(reinterpret_cast<const void*>(auc::auc_bucket_kernel), auc::kBucketSmem);
-    auc::auc_bucket_kernel<<<sms, auc::kThreads, auc::kBucketSmem, s>>>(w);
+    auc::auc_bucket_kernel<<<8 * sms, auc::kBucketThreads, auc::kBucketSmem, s>>>(w);
     auc::auc_l2_totals_kernel<<<2 * sms, auc::kThreads, 0, s>>>(w);
     auc::auc_l2_kernel<<<2 * sms, auc::kThreads, 0, s>>>(w);
     count_launch();
