@@ -18,8 +18,11 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <future>
 #include <memory>
 #include <string>
 #include <vector>
@@ -105,26 +108,30 @@ struct Bank {  // owning mtk_bank
     }
 };
 
-// batch_iter semantics: consecutive slices of the seeded
-// order; the short last batch is padded with weight-0 copies of its last row
-struct Batch {
-    std::vector<int64_t> idx;
-    std::vector<float> w;
-    double wsum;
+// batch_iter semantics over one seeded order: consecutive
+// slices; the short last batch is padded with weight-0 copies of its last row
+struct Batches {
+    std::vector<uint64_t> order;
+    int B;
+    int steps() const { return (int)((order.size() + B - 1) / B); }
+    int rows(int t) const { return (int)std::min<size_t>((size_t)B, order.size() - (size_t)t * B); }
+    int64_t idx(int t, int r) const { return (int64_t)order[(size_t)t * B + std::min(r, rows(t) - 1)]; }
+    float w(int t, int r) const { return r < rows(t) ? 1.f : 0.f; }
+    double wsum(int t) const { return (double)rows(t); }
 };
-std::vector<Batch> batches(const std::vector<uint64_t>& order, int B) {
-    std::vector<Batch> out;
-    for (size_t s = 0; s < order.size(); s += (size_t)B) {
-        Batch b;
-        const size_t n = std::min((size_t)B, order.size() - s);
-        for (size_t i = 0; i < (size_t)B; ++i) {
-            b.idx.push_back((int64_t)order[s + std::min(i, n - 1)]);
-            b.w.push_back(i < n ? 1.f : 0.f);
-        }
-        b.wsum = (double)n;
-        out.push_back(std::move(b));
+
+// Host-prepared work in order: item e + 1 is built on a worker thread while
+// item e runs (exceptions surface at get()).  The builders must only touch
+// state no consumer uses (here: the per-model RNG streams).
+template <class T, class F>
+void run_pipelined(std::vector<std::function<std::vector<T>()>>& items, F&& consume) {
+    if (items.empty()) return;
+    std::future<std::vector<T>> next = std::async(std::launch::async, items[0]);
+    for (size_t e = 0; e < items.size(); ++e) {
+        std::vector<T> cur = next.get();
+        if (e + 1 < items.size()) next = std::async(std::launch::async, items[e + 1]);
+        for (T& x : cur) consume(x);
     }
-    return out;
 }
 
 struct Pool {  // a device-resident population: X [rows, d] fp32, y [rows] int32
@@ -175,6 +182,13 @@ int mtk_sweep_run(mtk_ctx* ctx, const mtk_sweep_config* cfg, mtk_comm* comm, mtk
     return guard_on(ctx, [&] {
         need(ctx && cfg && out, MTK_VALUE_ERROR, "sweep: null argument");
         const auto t0 = std::chrono::steady_clock::now();
+        const char* trace_env = getenv("MTK_SWEEP_TRACE");  // phase wall times to stderr
+        auto trace = [&](const char* what) {
+            if (!trace_env) return;
+            MTK_CUDA(cudaStreamSynchronize(ctx->stream));
+            std::fprintf(stderr, "sweep %-14s %8.3f s\n", what,
+                         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+        };
         const mtk_sweep_config& c = *cfg;
         // ---- validation (sweep.py SweepConfig.validate) ----
         need(c.paradigm >= 0 && c.paradigm <= 2, MTK_CONFIG_ERROR, "sweep: unknown paradigm");
@@ -240,6 +254,7 @@ int mtk_sweep_run(mtk_ctx* ctx, const mtk_sweep_config* cfg, mtk_comm* comm, mtk
         MTK_CUDA(cudaMemcpyAsync(both.y.p, src.y.p, src.y.bytes, cudaMemcpyDeviceToDevice, st));
         MTK_CUDA(cudaMemcpyAsync(both.y.as<char>() + src.y.bytes, tgt.y.p, tgt.y.bytes, cudaMemcpyDeviceToDevice, st));
 
+        trace("population");
         const int M = 1 + c.n_shadows;
         std::vector<Rng> streams;
         for (int kk = 0; kk <= M; ++kk) streams.push_back(root.split((uint64_t)kk + 1));
@@ -263,91 +278,111 @@ int mtk_sweep_run(mtk_ctx* ctx, const mtk_sweep_config* cfg, mtk_comm* comm, mtk
         mtk_step tmpl{};
         tmpl.lr = c.lr;
         tmpl.optimizer = c.optimizer;
-        // one epoch: per model the batches of `orders`, row r of step t mapped
-        // through rowmap(g, t, idx) to pool rows; [nsteps][G][rows] on the device
-        auto run_epoch = [&](const Pool& pool, int rows, int nsteps,
+        // Each epoch becomes one or more train_epoch calls whose batch indices
+        // [nsteps][G][rows] are built on the host; a worker thread builds epoch
+        // e + 1 (the per-model streams advance in the same order as before)
+        // while the device trains epoch e.
+        struct Call {
+            const Pool* pool;
+            int rows, nsteps;
+            std::vector<int64_t> ix;
+            std::vector<float> w;
+            std::vector<double> den;
+            mtk_step s;
+        };
+        auto make_call = [&](const Pool& pool, int rows, int nsteps,
                              const std::function<void(int g, int t, int64_t* ix, float* w)>& fill,
-                             const std::vector<double>& denom0, mtk_step s) {
-            std::vector<int64_t> ix((size_t)nsteps * G * rows);
-            std::vector<float> w((size_t)nsteps * G * rows);
+                             std::vector<double> denom0, mtk_step s) {
+            Call cl{&pool, rows, nsteps, std::vector<int64_t>((size_t)nsteps * G * rows),
+                    std::vector<float>((size_t)nsteps * G * rows), std::move(denom0), s};
             for (int t = 0; t < nsteps; ++t)
                 for (int g = 0; g < G; ++g)
-                    fill(g, t, ix.data() + ((size_t)t * G + g) * rows, w.data() + ((size_t)t * G + g) * rows);
-            Dev dix = upload(ix, st), dw = upload(w, st);
-            s.B = rows;
-            ck(mtk_bank_train_epoch(bank.h, &s, pool.X.as<float>(), pool.y.as<int32_t>(), pool.rows,
-                                    dix.as<int64_t>(), dw.as<float>(), denom0.data(), nsteps),
-               "train_epoch");
+                    fill(g, t, cl.ix.data() + ((size_t)t * G + g) * rows, cl.w.data() + ((size_t)t * G + g) * rows);
+            cl.s.B = rows;
+            return cl;
         };
         auto model_orders = [&](uint64_t n) {
-            std::vector<std::vector<Batch>> o;
-            for (int g = 0; g < G; ++g) o.push_back(batches(streams[lo + g].permutation(n), B));
+            std::vector<Batches> o;
+            for (int g = 0; g < G; ++g) o.push_back(Batches{streams[lo + g].permutation(n), B});
             return o;
         };
-        if (c.paradigm == MTK_PARADIGM_MODEL && c.pretrain_epochs > 0) {
-            for (int e = 0; e < c.pretrain_epochs; ++e) {
-                auto orders = model_orders((uint64_t)c.source_per_model);
-                const int nsteps = (int)orders[0].size();
-                std::vector<double> den;
-                for (int t = 0; t < nsteps; ++t) den.push_back(orders[0][t].wsum);
-                run_epoch(src, B, nsteps, [&](int g, int t, int64_t* ix, float* w) {
-                    for (int r = 0; r < B; ++r) {
-                        ix[r] = (int64_t)srcs[g][orders[g][t].idx[r]];
-                        w[r] = orders[g][t].w[r];
-                    }
-                }, den, tmpl);
-            }
-        }
-        for (int e = 0; e < c.epochs; ++e) {
-            auto orders = model_orders((uint64_t)c.members);
-            const int nsteps = (int)orders[0].size();
-            if (c.paradigm == MTK_PARADIGM_MODEL) {
-                std::vector<double> den;
-                for (int t = 0; t < nsteps; ++t) den.push_back(orders[0][t].wsum);
-                mtk_step s = tmpl;
-                s.frozen_layers = c.frozen_layers;
-                run_epoch(tgt, B, nsteps, [&](int g, int t, int64_t* ix, float* w) {
-                    for (int r = 0; r < B; ++r) {
-                        ix[r] = (int64_t)mem[g][orders[g][t].idx[r]];
-                        w[r] = orders[g][t].w[r];
-                    }
-                }, den, s);
-                continue;
-            }
-            // co-training: a source batch rides along with every member batch
-            auto fill = [&](int g, int t, int64_t* ix, float* w) {
-                for (int r = 0; r < B; ++r) {
-                    ix[r] = (int64_t)srcs[g][((int64_t)t * B + r) % c.source_per_model];
-                    w[r] = 1.f;
-                    ix[B + r] = src.rows + (int64_t)mem[g][orders[g][t].idx[r]];
-                    w[B + r] = orders[g][t].w[r];
+        std::vector<std::function<std::vector<Call>()>> epochs;
+        if (c.paradigm == MTK_PARADIGM_MODEL)
+            for (int e = 0; e < c.pretrain_epochs; ++e)
+                epochs.push_back([&]() {
+                    auto orders = model_orders((uint64_t)c.source_per_model);
+                    const int nsteps = orders[0].steps();
+                    std::vector<double> den;
+                    for (int t = 0; t < nsteps; ++t) den.push_back(orders[0].wsum(t));
+                    std::vector<Call> v;
+                    v.push_back(make_call(src, B, nsteps, [&](int g, int t, int64_t* ix, float* w) {
+                        for (int r = 0; r < B; ++r) {
+                            ix[r] = (int64_t)srcs[g][orders[g].idx(t, r)];
+                            w[r] = orders[g].w(t, r);
+                        }
+                    }, den, tmpl));
+                    return v;
+                });
+        for (int e = 0; e < c.epochs; ++e)
+            epochs.push_back([&]() {
+                auto orders = model_orders((uint64_t)c.members);
+                const int nsteps = orders[0].steps();
+                std::vector<Call> v;
+                if (c.paradigm == MTK_PARADIGM_MODEL) {
+                    std::vector<double> den;
+                    for (int t = 0; t < nsteps; ++t) den.push_back(orders[0].wsum(t));
+                    mtk_step s = tmpl;
+                    s.frozen_layers = c.frozen_layers;
+                    v.push_back(make_call(tgt, B, nsteps, [&](int g, int t, int64_t* ix, float* w) {
+                        for (int r = 0; r < B; ++r) {
+                            ix[r] = (int64_t)mem[g][orders[g].idx(t, r)];
+                            w[r] = orders[g].w(t, r);
+                        }
+                    }, den, s));
+                    return v;
                 }
-            };
-            mtk_step s = tmpl;
-            s.src_rows = B;
-            if (c.paradigm == MTK_PARADIGM_MAPPING) {
-                s.mmd_lambda = c.mmd_lambda;
-                std::vector<double> den;
-                for (int t = 0; t < nsteps; ++t) den.push_back((double)B + orders[0][t].wsum);
-                run_epoch(both, 2 * B, nsteps, fill, den, s);
-            } else {
+                // co-training: a source batch rides along with every member batch
+                auto fill = [&](int g, int t, int64_t* ix, float* w) {
+                    for (int r = 0; r < B; ++r) {
+                        ix[r] = (int64_t)srcs[g][((int64_t)t * B + r) % c.source_per_model];
+                        w[r] = 1.f;
+                        ix[B + r] = src.rows + (int64_t)mem[g][orders[g].idx(t, r)];
+                        w[B + r] = orders[g].w(t, r);
+                    }
+                };
+                mtk_step s = tmpl;
+                s.src_rows = B;
+                if (c.paradigm == MTK_PARADIGM_MAPPING) {
+                    s.mmd_lambda = c.mmd_lambda;
+                    std::vector<double> den;
+                    for (int t = 0; t < nsteps; ++t) den.push_back((double)B + orders[0].wsum(t));
+                    v.push_back(make_call(both, 2 * B, nsteps, fill, den, s));
+                    return v;
+                }
                 // parameter-based: head denominators (B, member weight sum); the
                 // per-step override covers head 0 only, so runs of steps with
                 // equal member sums go in one call each
                 int t0 = 0;
                 while (t0 < nsteps) {
                     int t1 = t0 + 1;
-                    while (t1 < nsteps && orders[0][t1].wsum == orders[0][t0].wsum) ++t1;
+                    while (t1 < nsteps && orders[0].wsum(t1) == orders[0].wsum(t0)) ++t1;
                     mtk_step sp = s;
-                    sp.denom[1] = orders[0][t0].wsum;
-                    std::vector<double> den(t1 - t0, (double)B);
-                    run_epoch(both, 2 * B, t1 - t0,
-                              [&](int g, int t, int64_t* ix, float* w) { fill(g, t0 + t, ix, w); }, den, sp);
+                    sp.denom[1] = orders[0].wsum(t0);
+                    v.push_back(make_call(both, 2 * B, t1 - t0,
+                                          [&](int g, int t, int64_t* ix, float* w) { fill(g, t0 + t, ix, w); },
+                                          std::vector<double>(t1 - t0, (double)B), sp));
                     t0 = t1;
                 }
-            }
-        }
+                return v;
+            });
+        run_pipelined(epochs, [&](Call& cl) {
+            Dev dix = upload(cl.ix, st), dw = upload(cl.w, st);
+            ck(mtk_bank_train_epoch(bank.h, &cl.s, cl.pool->X.as<float>(), cl.pool->y.as<int32_t>(), cl.pool->rows,
+                                    dix.as<int64_t>(), dw.as<float>(), cl.den.data(), cl.nsteps),
+               "train_epoch");
+        });
 
+        trace("training");
         // ---- query_features: top-k posteriors of each model on its members
         // and non-members (the target-domain head) ----
         const int Q = 2 * c.members, kf = c.k;
@@ -383,6 +418,7 @@ int mtk_sweep_run(mtk_ctx* ctx, const mtk_sweep_config* cfg, mtk_comm* comm, mtk
             MTK_CUDA(cudaMemcpyAsync(Fall.p, F.p, Fall.bytes, cudaMemcpyDeviceToDevice, st));
         }
 
+        trace("features");
         // ---- train_attack on the shadows' features (member 1 / non-member 0) ----
         const int64_t ntr = (int64_t)c.n_shadows * Q;
         std::vector<int32_t> ltr((size_t)ntr);
@@ -393,27 +429,39 @@ int mtk_sweep_run(mtk_ctx* ctx, const mtk_sweep_config* cfg, mtk_comm* comm, mtk
         Rng& ar = streams[M];
         ck(mtk_bank_init_params(att.h, 0, ar.h), "init_params");
         const float* Ftr = Fall.as<float>() + (size_t)Q * kf;  // models 1 .. M-1
-        for (int e = 0; e < c.attack_epochs; ++e) {
-            std::vector<Batch> bl = batches(ar.permutation((uint64_t)ntr), c.attack_batch);
-            const int nb = (int)bl.size();
+        struct AttCall {
             std::vector<int64_t> ix;
             std::vector<float> w;
             std::vector<double> den;
-            for (auto& b : bl) {
-                ix.insert(ix.end(), b.idx.begin(), b.idx.end());
-                w.insert(w.end(), b.w.begin(), b.w.end());
-                den.push_back(b.wsum);
+        };
+        std::vector<std::function<std::vector<AttCall>()>> aep(c.attack_epochs, [&]() {
+            const Batches bl{ar.permutation((uint64_t)ntr), c.attack_batch};
+            const int nb = bl.steps();
+            AttCall a{std::vector<int64_t>((size_t)nb * c.attack_batch), std::vector<float>((size_t)nb * c.attack_batch),
+                      std::vector<double>(nb)};
+            for (int t = 0; t < nb; ++t) {
+                for (int r = 0; r < c.attack_batch; ++r) {
+                    a.ix[(size_t)t * c.attack_batch + r] = bl.idx(t, r);
+                    a.w[(size_t)t * c.attack_batch + r] = bl.w(t, r);
+                }
+                a.den[t] = bl.wsum(t);
             }
-            Dev dix = upload(ix, st), dw = upload(w, st);
+            std::vector<AttCall> v;
+            v.push_back(std::move(a));
+            return v;
+        });
+        run_pipelined(aep, [&](AttCall& a) {
+            Dev dix = upload(a.ix, st), dw = upload(a.w, st);
             mtk_step s{};
             s.B = c.attack_batch;
             s.lr = c.attack_lr;
             s.optimizer = c.attack_optimizer;
             ck(mtk_bank_train_epoch(att.h, &s, Ftr, dl.as<int32_t>(), ntr, dix.as<int64_t>(), dw.as<float>(),
-                                    den.data(), nb),
+                                    a.den.data(), (int)a.den.size()),
                "attack train_epoch");
-        }
+        });
 
+        trace("attack train");
         // ---- score the target's members / non-members: AUC + accuracy ----
         std::vector<uint8_t> lab((size_t)Q);
         for (int i = 0; i < Q; ++i) lab[(size_t)i] = i < c.members ? 1 : 0;
@@ -422,6 +470,7 @@ int mtk_sweep_run(mtk_ctx* ctx, const mtk_sweep_config* cfg, mtk_comm* comm, mtk
         ck(mtk_posterior_column(ctx, alog.as<float>(), Q, 2, 1, sc.as<float>()), "posterior_column");
         double auc = 0.0, acc = 0.0;
         ck(mtk_auc(ctx, sc.as<float>(), dlab.as<uint8_t>(), Q, &auc, &acc), "auc");
+        trace("attack score");
         out->auc = auc;
         out->accuracy = acc;
         out->models = M;
