@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmtk.so")
+LIB_PATH = os.environ.get("MTK_LIB_PATH") or os.path.join(_HERE, "libmtk.so")  # override: A/B diagnostics
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

@@ -58,3 +58,8 @@ ep = t[2000:2032]
 for i in range(16):
     if ep[2 * i] > 0:
         print("tile %d epilogue %.2f -> %.2f us" % (i, (ep[2 * i] - t0) / 1000, (ep[2 * i + 1] - t0) / 1000))
+for i in range(4):
+    row = t[2100 + 32 * i: 2100 + 32 * i + 16].reshape(4, 4)
+    if row[0, 0] > 0:
+        print("tile %d chunks (pre-ld, post-ld, post-store) us:" % i,
+              [[round((x - t0) / 1000, 2) for x in r[:3] if x > 0] for r in row])
