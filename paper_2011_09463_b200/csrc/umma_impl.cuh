@@ -87,8 +87,12 @@ constexpr int NUM_EPI_WARPS = 8;   // two per TMEM lane quarter, each half the c
 // MMD gradient: +20..50 us) -- those keep the thread-per-row path.
 template <int EPI>
 struct EpiPlan {
+#ifdef MTK_UMMA_COAL_ALL
+    static constexpr bool coal = MTK_UMMA_COAL && EPI >= 0;
+#else
     static constexpr bool coal = MTK_UMMA_COAL && (EPI == (int)Epi::kBias || EPI == (int)Epi::kBiasRelu ||
                                                    EPI == (int)Epi::kStore);
+#endif
     static constexpr int ls = coal ? 4 : 5;  // load stages
     static constexpr int tile_bytes = coal ? 32 * 32 * 4 : 0;
     static constexpr int roww_bytes = coal ? 32 * 4 : 0;
@@ -493,9 +497,7 @@ __device__ __forceinline__ void epilogue_coalesced(const UmmaParams& p, uint32_t
             continue;
         }
         const int ncol = nb + 4 * gq;  // this lane's first column
-        epi_prefetch<EPI>(p, lane, g, m0, n0, q, c, ops);
-        const uint32_t rw = ops.rw;
-        const float4 bias4 = ops.bias4;
+        const uint32_t rw = epi_rowword<EPI>(p, g, mw + lane, nb);
         if (etr && lane == 0) etr[4 * (c - c0)] = gtime();
         {
             float v[32];
@@ -524,6 +526,9 @@ __device__ __forceinline__ void epilogue_coalesced(const UmmaParams& p, uint32_t
             if (EPI == (int)Epi::kMask || EPI == (int)Epi::kMmdGrad) sts32(roww + 4u * lane, rw);
         }
         __syncwarp();
+        // the chunk's operands, issued once the accumulator registers are free
+        epi_prefetch<EPI>(p, lane, g, m0, n0, q, c, ops);
+        const float4 bias4 = ops.bias4;
         float4 cs = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
