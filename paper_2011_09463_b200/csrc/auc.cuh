@@ -4,9 +4,22 @@
 // + #{non-members equal}, AUC = (U2 / 2) / (npos nneg), all in exact integers.
 //
 // The scores are keyed by an order-preserving float -> uint32 map and the
-// rank sums come from key histograms instead of a sort:
-//   1. (fused into the kernel that produces the scores) the key of every
-//      query and a per-class histogram of the key's top 16 bits
+// rank sums come from key histograms instead of a sort.  The kernel that
+// produces the scores writes every query's key and the block-reduced key
+// range [kmin, kmax].
+//
+// Full-resolution path (kmax - kmin < 2^kFastBits: concentrated scores, the
+// attack stage's case -- bench data: a 2^20.1-key range):
+//   F1. auc_hist_kernel: per query one 64-bit atomic (1 << 32 | non-member)
+//       into bin key - kmin of a zero-invariant [2^kFastBits] arena (same-bin
+//       lanes of a warp aggregated by match.any);
+//   F2. auc_fast_scan_kernel: in bin (= key) order, every member adds
+//       2 #{non-members in lower bins} + #{non-members in its bin}: per block
+//       rounds of 1024 bins (block scan of the non-member counts), the
+//       blocks' partials combined in block order by the last block to finish;
+//       the bins are reset on the way.  Two launches after the scores.
+// General path (wider ranges), on the top 16 bits of the key:
+//   1. auc_hist_kernel: a per-class histogram of the key's top 16 bits
 //      (warp-aggregated integer atomics);
 //   2. auc_scan_totals_kernel + auc_scan_kernel (64 blocks each): in bucket
 //      order, every member contributes 2 #{non-members in lower buckets} --
@@ -30,6 +43,7 @@
 namespace mtk {
 namespace auc {
 
+constexpr int kFastBits = 23;  // full-resolution key histogram up to a 2^23-key range (64 MB arena)
 constexpr int kBuckets = 65536;
 constexpr int kSmallMax = 2048;      // bitonic-sort path up to this many queries per bucket
 constexpr int kBucketThreads = 256;  // small-bucket kernel: one CTA per bucket, 8 per SM
@@ -105,7 +119,213 @@ struct Work {
     uint32_t* l2;         // [large slots][2][kBuckets] level-2 class histograms; zero on entry and exit
     uint32_t* l2tot;      // [large slots][kBuckets / kThreads] block totals of the non-member counts
     unsigned long long* cnt;  // [0] members, [1] hits at 0.5, [2] U2, [3] mixed, [4] large buckets
+    uint32_t* mm;             // [0] max key, [1] max ~key (= ~min key), [2] a key outside the window; zero on entry
+    unsigned long long* cnt_next;  // the next call's counters (ping-pong): zeroed by this call's first kernel
+    uint32_t win_lo;          // speculative window [win_lo, win_lo + 2^kFastBits) of full-resolution bins
+    int win_on;               // 1: the score kernel adds every in-window key to fhist[key - win_lo]
+    unsigned long long* fhist;  // [2^kFastBits] (queries << 32 | non-members) per key; zero on entry and exit
+    unsigned long long* fpart;  // [blocks][3] per-block (non-members, members, U2) of auc_fast_scan_kernel
+    unsigned int* done;         // blocks finished in auc_fast_scan_kernel; zero on entry and exit
 };
+
+// the full-resolution path applies (the key range is known once the scores are)
+__device__ __forceinline__ bool fast_path(const Work& w) {
+    return w.win_on ? w.mm[2] == 0 : w.mm[0] - ~w.mm[1] < (1u << kFastBits);
+}
+
+// Speculative full-resolution binning inside the kernel that produces the
+// keys: the window is the previous call's key range, centred in 2^kFastBits
+// bins (host side).  Every in-window key is added to its bin right away; a
+// key outside sets mm[2], and the host re-runs the binning from the keys
+// (the bins written are cleared by auc_fast_scan_kernel).  All 32 lanes of
+// the warp call it.
+__device__ __forceinline__ void spec_add(const Work& w, uint32_t key, bool member, bool valid) {
+    const uint32_t b = key - w.win_lo;
+    const bool in = valid && b < (1u << kFastBits);
+    const uint32_t tag = in ? b : 0xFFFFFFFFu;
+    const unsigned peers = __match_any_sync(0xffffffffu, tag);
+    const unsigned nmp = __ballot_sync(0xffffffffu, in && !member) & peers;
+    const int lane = threadIdx.x & 31;
+    if (in && lane == __ffs(peers) - 1)
+        atomicAdd(&w.fhist[b], ((unsigned long long)__popc(peers) << 32) | (unsigned long long)__popc(nmp));
+    if (__any_sync(0xffffffffu, valid && !in) && lane == 0) atomicOr(&w.mm[2], 1u);
+}
+// the first kernel of a call zeroes the next call's counters (this call's were
+// zeroed by the previous call, whose host read-back has completed)
+__device__ __forceinline__ void zero_next_counters(const Work& w) {
+    if (blockIdx.x == 0 && threadIdx.x < 16) w.cnt_next[threadIdx.x] = 0ull;
+}
+
+// block-reduced key range, member and hit-at-0.5 counts -> the global counters
+// (integer atomics: exact and order-independent); every thread of the block calls it
+__device__ __forceinline__ void publish_counts(const Work& w, uint32_t kmax, uint32_t nkmin,
+                                               unsigned long long pos, unsigned long long hit) {
+    __shared__ uint32_t sa[32], sb[32];
+    __shared__ unsigned long long sp[32], sq[32];
+    kmax = __reduce_max_sync(0xffffffffu, kmax);
+    nkmin = __reduce_max_sync(0xffffffffu, nkmin);
+    for (int o = 16; o > 0; o >>= 1) {
+        pos += __shfl_down_sync(0xffffffffu, pos, o);
+        hit += __shfl_down_sync(0xffffffffu, hit, o);
+    }
+    const int wi = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        sa[wi] = kmax;
+        sb[wi] = nkmin;
+        sp[wi] = pos;
+        sq[wi] = hit;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t a = 0, b = 0;
+        unsigned long long c = 0, d = 0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+            a = max(a, sa[i]);
+            b = max(b, sb[i]);
+            c += sp[i];
+            d += sq[i];
+        }
+        if (a) atomicMax(&w.mm[0], a);
+        if (b) atomicMax(&w.mm[1], b);
+        if (c) atomicAdd(&w.cnt[0], c);
+        if (d) atomicAdd(&w.cnt[1], d);
+    }
+}
+
+// F1 / 1: per query, the full-resolution bin (fast path) or the top-16-bit
+// class histogram (general path).  Grid-stride over whole warps.
+__global__ void __launch_bounds__(256) auc_hist_kernel(Work w, const uint8_t* lab, long long n) {
+    const bool fast = fast_path(w);
+    const uint32_t kmin = ~w.mm[1];
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    const int lane = threadIdx.x & 31;
+    for (long long i0 = blockIdx.x * (long long)blockDim.x + (threadIdx.x & ~31); i0 < n; i0 += stride) {
+        const long long i = i0 + lane;
+        const bool valid = i < n;
+        const uint32_t k = valid ? w.key[i] : 0u;
+        const bool nm = valid && lab[i] == 0;
+        if (fast) {
+            const uint32_t b = valid ? k - kmin : 0xFFFFFFFFu;
+            const unsigned peers = __match_any_sync(0xffffffffu, b);
+            const unsigned nmp = __ballot_sync(0xffffffffu, nm) & peers;
+            if (valid && lane == __ffs(peers) - 1)
+                atomicAdd(&w.fhist[b], ((unsigned long long)__popc(peers) << 32) | (unsigned long long)__popc(nmp));
+        } else {
+            hist_add(w.hist, k, valid && !nm, valid);
+        }
+    }
+}
+
+// non-members in the first k0 blocks' bins (the combine loop's carry past 1024 blocks)
+__device__ __forceinline__ unsigned long long carry_blocks(const Work& w, unsigned k0) {
+    unsigned long long c = 0;
+    for (unsigned k = 0; k < k0; ++k) c += __ldcg(w.fpart + 3 * k);
+    return c;
+}
+
+// F2: U2 over the full-resolution bins [0, kmax - kmin]
+constexpr int kFastScanThreads = 1024;
+__global__ void __launch_bounds__(kFastScanThreads) auc_fast_scan_kernel(Work w) {
+    __shared__ uint32_t sh[33];
+    __shared__ unsigned long long shl[32];
+    __shared__ bool last;
+    const uint32_t kmin = ~w.mm[1], kmax = w.mm[0];
+    if (w.win_on && w.mm[2]) {  // a key fell outside the window: clear the in-window bins written
+        const uint32_t top = w.win_lo + ((1u << kFastBits) - 1u);
+        const long long lo = (long long)(max(kmin, w.win_lo) - w.win_lo);
+        const long long hi = (long long)(min(kmax, top) - w.win_lo);
+        if (kmax < w.win_lo || kmin > top) return;
+        for (long long b = lo + blockIdx.x * (long long)blockDim.x + threadIdx.x; b <= hi;
+             b += (long long)gridDim.x * blockDim.x)
+            if (w.fhist[b]) w.fhist[b] = 0ull;
+        return;
+    }
+    if (!fast_path(w)) return;
+    // bins [bin0, bin0 + nb) of fhist hold keys kmin .. kmax (bin0 aligned
+    // down to 8 bins in the window: the bins below kmin are empty)
+    const long long bin0 = w.win_on ? (long long)((kmin - w.win_lo) & ~7u) : 0;
+    const long long nb = (w.win_on ? (long long)(kmax - w.win_lo) : (long long)(kmax - kmin)) - bin0 + 1;
+    // blocks own ranges of whole 8-bin groups; a thread takes 8 consecutive
+    // bins per round (four 16-B loads in flight), one block scan per round
+    constexpr int kPer = 8, kRound = kPer * kFastScanThreads;
+    const long long groups = (nb + kPer - 1) / kPer;
+    const long long gper = (groups + gridDim.x - 1) / gridDim.x;
+    const long long b0 = blockIdx.x * gper * kPer, b1 = min(nb, b0 + gper * kPer);
+    unsigned long long* fh = w.fhist + bin0;
+    uint32_t carry = 0;  // non-members in this block's bins before the round
+    unsigned long long u2 = 0, pos = 0;
+    for (long long base = b0; base < b1; base += kRound) {  // block-uniform trip count
+        const long long t0 = base + (long long)threadIdx.x * kPer;
+        unsigned long long v[kPer];
+        if (t0 + kPer <= b1) {
+            const ulonglong2* src = reinterpret_cast<const ulonglong2*>(fh + t0);
+#pragma unroll
+            for (int j = 0; j < kPer / 2; ++j) {
+                const ulonglong2 x = src[j];
+                v[2 * j] = x.x;
+                v[2 * j + 1] = x.y;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < kPer; ++j) v[j] = t0 + j < b1 ? fh[t0 + j] : 0ull;
+        }
+        uint32_t nsum = 0;
+        unsigned long long any = 0;
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) {
+            nsum += (uint32_t)v[j];
+            any |= v[j];
+        }
+        uint32_t tot;
+        uint32_t below = carry + block_excl_scan(nsum, sh, &tot);
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) {
+            const uint32_t T = (uint32_t)(v[j] >> 32), N = (uint32_t)v[j], P = T - N;
+            u2 += (unsigned long long)P * (2ull * below + N);
+            pos += P;
+            below += N;
+        }
+        if (any) {  // zero-invariant arena
+            if (t0 + kPer <= b1) {
+                ulonglong2* dst = reinterpret_cast<ulonglong2*>(fh + t0);
+#pragma unroll
+                for (int j = 0; j < kPer / 2; ++j) dst[j] = make_ulonglong2(0ull, 0ull);
+            } else {
+                for (int j = 0; j < kPer && t0 + j < b1; ++j) fh[t0 + j] = 0ull;
+            }
+        }
+        carry += tot;
+    }
+    u2 = block_sum_u64(u2, shl);
+    pos = block_sum_u64(pos, shl);
+    if (threadIdx.x == 0) {
+        w.fpart[3 * blockIdx.x] = carry;
+        w.fpart[3 * blockIdx.x + 1] = pos;
+        w.fpart[3 * blockIdx.x + 2] = u2;
+        __threadfence();
+        last = atomicAdd(w.done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last) {  // combine in block order: + 2 #{non-members in earlier blocks} per member (one block per thread)
+        __threadfence();
+        unsigned long long t = 0;
+        for (unsigned k0 = 0; k0 < gridDim.x; k0 += kFastScanThreads) {  // (gridDim.x <= 1024 in practice)
+            const unsigned k = k0 + threadIdx.x;
+            const bool in = k < gridDim.x;
+            const uint32_t nk = in ? (uint32_t)__ldcg(w.fpart + 3 * k) : 0u;
+            const unsigned long long pk = in ? __ldcg(w.fpart + 3 * k + 1) : 0ull;
+            const unsigned long long uk = in ? __ldcg(w.fpart + 3 * k + 2) : 0ull;
+            uint32_t tot;
+            const uint32_t before = (uint32_t)carry_blocks(w, k0) + block_excl_scan(nk, sh, &tot);
+            t += uk + 2ull * before * pk;
+        }
+        t = block_sum_u64(t, shl);
+        if (threadIdx.x == 0) {
+            atomicAdd(&w.cnt[2], t);
+            *w.done = 0;
+        }
+    }
+}
 
 // 2. bucket order in two fully parallel passes over kScanBlocks blocks of
 // kThreads buckets (one bucket per thread, coalesced):
@@ -120,6 +340,7 @@ __device__ __forceinline__ void load_bucket(const uint32_t* hist, int b, uint32_
     P = hist[kBuckets + b];
 }
 __global__ void __launch_bounds__(kThreads) auc_scan_totals_kernel(Work w) {
+    if (fast_path(w)) return;  // the full-resolution path resolved the AUC
     __shared__ uint32_t sh[33];
     const int b = blockIdx.x * kThreads + threadIdx.x;
     uint32_t N, P;
@@ -133,6 +354,7 @@ __global__ void __launch_bounds__(kThreads) auc_scan_totals_kernel(Work w) {
     if (threadIdx.x == 0) w.totals[blockIdx.x] = make_uint4(t0, t1, t2, t3);
 }
 __global__ void __launch_bounds__(kThreads) auc_scan_kernel(Work w) {
+    if (fast_path(w)) return;  // the full-resolution path resolved the AUC
     __shared__ uint32_t sh[33];
     __shared__ unsigned long long shl[32];
     __shared__ uint32_t base[4];
@@ -183,6 +405,7 @@ __global__ void __launch_bounds__(kThreads) auc_scan_kernel(Work w) {
 // 3. the queries of mixed buckets into their bucket's slot (order inside a
 // bucket is immaterial: the bucket kernel sorts / counts it)
 __global__ void auc_scatter_kernel(Work w, const uint8_t* lab, long long n) {
+    if (fast_path(w)) return;  // the full-resolution path resolved the AUC
     for (long long i0 = blockIdx.x * (long long)blockDim.x; i0 < n; i0 += (long long)gridDim.x * blockDim.x) {
         const long long i = i0 + threadIdx.x;
         const bool valid = i < n;
@@ -213,6 +436,7 @@ __global__ void auc_scatter_kernel(Work w, const uint8_t* lab, long long n) {
 //    built (auc_l2_totals_kernel, auc_l2_kernel: blocks of 1024 bins).
 constexpr int kBucketSmem = 2 * kSmallMax * 4;  // the sorted bucket + its prefix counts
 __global__ void __launch_bounds__(kBucketThreads) auc_bucket_kernel(Work w) {
+    if (fast_path(w)) return;  // the full-resolution path resolved the AUC
     extern __shared__ uint32_t dsm[];
     uint32_t* buf = dsm;
     uint32_t* pre = dsm + kSmallMax;
@@ -286,6 +510,7 @@ __global__ void __launch_bounds__(kBucketThreads) auc_bucket_kernel(Work w) {
 // the totals of the blocks before); the histograms are zeroed again
 constexpr int kL2Blocks = kBuckets / kThreads;  // 64 blocks of bins per slot
 __global__ void __launch_bounds__(kThreads) auc_l2_totals_kernel(Work w) {
+    if (fast_path(w)) return;  // the full-resolution path resolved the AUC
     __shared__ uint32_t sh[33];
     const uint32_t items = (uint32_t)w.cnt[4] * kL2Blocks;
     for (uint32_t it = blockIdx.x; it < items; it += gridDim.x) {
@@ -297,6 +522,7 @@ __global__ void __launch_bounds__(kThreads) auc_l2_totals_kernel(Work w) {
     }
 }
 __global__ void __launch_bounds__(kThreads) auc_l2_kernel(Work w) {
+    if (fast_path(w)) return;  // the full-resolution path resolved the AUC
     __shared__ uint32_t sh[33];
     __shared__ unsigned long long shl[32];
     __shared__ uint32_t base;

@@ -63,6 +63,10 @@ struct Ctx {
     // and left zeroed by every call
     uint32_t* auc_l2(size_t bytes);
     uint32_t* d_auc_l2 = nullptr;
+    bool auc_fast_hint = true;        // the previous AUC took the full-resolution path (k_attack.cu)
+    bool auc_win_valid = false;       // speculative full-resolution window from the previous call's keys
+    uint32_t auc_win_lo = 0;
+    int auc_parity = 0;               // which of the two counter blocks this call uses
     size_t auc_l2_bytes = 0;
     void check_flags();               // synchronizes; throws on a set flag
     // Side stream for short, latency-bound kernels that do not feed the next

@@ -137,47 +137,25 @@ __global__ void column_kernel(const float* logits, long long rows, int C, int co
 }
 
 // ---- AUC (auc.cuh: exact mid-rank AUC from key histograms, no sort) --------
-// block-aggregated integer atomics (exact, order-independent): cnt[0] += pos, cnt[1] += hit
-__device__ __forceinline__ void add_counts(unsigned long long pos, unsigned long long hit,
-                                           unsigned long long* cnt) {
-    __shared__ unsigned long long sp[32], sh[32];
-    for (int o = 16; o > 0; o >>= 1) {
-        pos += __shfl_down_sync(0xffffffffu, pos, o);
-        hit += __shfl_down_sync(0xffffffffu, hit, o);
-    }
-    if ((threadIdx.x & 31) == 0) {
-        sp[threadIdx.x >> 5] = pos;
-        sh[threadIdx.x >> 5] = hit;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long a = 0, b = 0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-            a += sp[w];
-            b += sh[w];
-        }
-        if (a) atomicAdd(&cnt[0], a);
-        if (b) atomicAdd(&cnt[1], b);
-    }
-}
-
-// per query: the order-preserving key and the class histogram of its top
-// 16 bits (auc.cuh step 1), member and hit-at-0.5 counts
-__global__ void auc_keys_kernel(const float* s, const uint8_t* lab, long long n, auc::Work w) {
+// per query: the order-preserving key; per block: the key range, member and
+// hit-at-0.5 counts (auc.cuh)
+__global__ void __launch_bounds__(256) auc_keys_kernel(const float* s, const uint8_t* lab, long long n, auc::Work w) {
     const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     unsigned long long pos = 0, hit = 0;
-    const bool valid = i < n;
-    uint32_t u = 0;
+    uint32_t kmax = 0, nkmin = 0, u = 0;
     bool l = false;
-    if (valid) {
+    auc::zero_next_counters(w);
+    if (i < n) {
         u = auc::key_of(s[i]);
         l = lab[i] != 0;
         w.key[i] = u;
+        kmax = u;
+        nkmin = ~u;
         pos = l;
         hit = ((s[i] > 0.5f) == l);
     }
-    auc::hist_add(w.hist, u, l, valid);
-    add_counts(pos, hit, w.cnt);
+    if (w.win_on) auc::spec_add(w, u, l, i < n);
+    auc::publish_counts(w, kmax, nkmin, pos, hit);
 }
 
 // ---- fused attack scoring: posterior softmax -> top-KF sorted features ->
@@ -263,15 +241,16 @@ __global__ void __launch_bounds__(256) attack_score2_kernel(const float* logits,
         }
     }
     unsigned long long pos = 0, hit = 0;
+    uint32_t kmax = 0, nkmin = 0;
+    auc::zero_next_counters(w);
 #pragma unroll
     for (int q = 0; q < 2 * QP; ++q) {
         const long long r = r0 + q;
-        const bool valid = r < rows;
         const float2 a = __fadd2_rn(o0[q / 2], B1[0]), b = __fadd2_rn(o1[q / 2], B1[1]);
         const float p0 = (q & 1) ? a.y : a.x, p1 = (q & 1) ? b.y : b.x;
         uint32_t u = 0;
         bool l = false;
-        if (valid) {  // member posterior: column_kernel's softmax column 1
+        if (r < rows) {  // member posterior: column_kernel's softmax column 1
             const float m2 = fmaxf(p0, p1);
             const float z2 = expf(p0 - m2) + expf(p1 - m2);
             const float sc = expf(p1 - m2) / z2;
@@ -279,12 +258,14 @@ __global__ void __launch_bounds__(256) attack_score2_kernel(const float* logits,
             u = auc::key_of(sc);
             l = lab[r] != 0;
             w.key[r] = u;
+            kmax = max(kmax, u);
+            nkmin = max(nkmin, ~u);
             pos += l;
             hit += ((sc > 0.5f) == l);
         }
-        auc::hist_add(w.hist, u, l, valid);
+        if (w.win_on) auc::spec_add(w, u, l, r < rows);
     }
-    add_counts(pos, hit, w.cnt);
+    auc::publish_counts(w, kmax, nkmin, pos, hit);
 }
 
 // (w, w) pairs of the attack weights for c_att2
@@ -357,55 +338,114 @@ void launch_column(const float* logits, long long rows, int C, int col, float* o
 }
 
 namespace {
+int auc_fast_blocks(Ctx& ctx) { return device_sm_count(ctx.device); }
 // grow-only workspace from ctx.big: keys, histograms, bucket slots, the
 // scattered mixed buckets, the large-bucket histograms, counters
 auc::Work auc_work(Ctx& ctx, long long n) {
     if (n > 0x7fffffffLL) fail(MTK_SHAPE_ERROR, "auc: more than 2^31 rows");
     auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
     const size_t hb = 2 * (size_t)auc::kBuckets * 4;
-    char* p = static_cast<char*>(ctx.big(al(4 * n) * 2 + al(hb) + al(4 * auc::kBuckets) +
-                                         al(16 * auc::kBuckets) + al(16 * auc::kScanBlocks) + al(64) +
+    char* p = static_cast<char*>(ctx.big(al(4 * n) * 2 + al(4 * auc::kBuckets) +
+                                         al(16 * auc::kBuckets) + al(16 * auc::kScanBlocks) +
+                                         al(3 * 8 * (size_t)auc_fast_blocks(ctx)) +
                                          al((size_t)(n / auc::kSmallMax + 1) * auc::kL2Blocks * 4)));
     auto take = [&](size_t b) { char* r = p; p += al(b); return r; };
     auc::Work w;
     w.key = (uint32_t*)take(4 * n);
     w.packed = (uint32_t*)take(4 * n);
-    w.hist = (uint32_t*)take(hb);
     w.cursor = (uint32_t*)take(4 * auc::kBuckets);
     w.mixed = (uint4*)take(16 * auc::kBuckets);
     w.totals = (uint4*)take(16 * auc::kScanBlocks);
     w.big = nullptr;
     // at most n / kSmallMax buckets can be large: one level-2 slot each
     const size_t slots = (size_t)(n / auc::kSmallMax + 1);
-    w.l2 = ctx.auc_l2(slots * 2 * auc::kBuckets * 4);
     w.l2tot = (uint32_t*)take(slots * auc::kL2Blocks * 4);
-    w.cnt = (unsigned long long*)take(64);
-    // hist is left zeroed by auc_scan_kernel, but the workspace may be new
-    MTK_CUDA(cudaMemsetAsync(w.hist, 0, hb, ctx.stream));
-    MTK_CUDA(cudaMemsetAsync(w.cnt, 0, 64, ctx.stream));
+    w.fpart = (unsigned long long*)take(3 * 8 * (size_t)auc_fast_blocks(ctx));
+    // zero-invariant arena: the full-resolution bins, the block counter, the level-2 histograms
+    // (the top-16 histogram too: auc_scan_kernel leaves it zeroed)
+    const size_t fb = (size_t)8 << auc::kFastBits;
+    char* ar = reinterpret_cast<char*>(ctx.auc_l2(fb + 512 + al(hb) + slots * 2 * auc::kBuckets * 4));
+    w.fhist = reinterpret_cast<unsigned long long*>(ar);
+    w.done = reinterpret_cast<unsigned int*>(ar + fb);
+    // two counter blocks of 16 (counters, key range, window flag), used by
+    // alternate calls; each call's first kernel zeroes the other one
+    unsigned long long* cb = reinterpret_cast<unsigned long long*>(ar + fb + 256);
+    w.cnt = cb + 16 * ctx.auc_parity;
+    w.cnt_next = cb + 16 * (1 - ctx.auc_parity);
+    ctx.auc_parity ^= 1;
+    w.mm = reinterpret_cast<uint32_t*>(w.cnt + 8);
+    // the speculative window: the previous call's key range (auc_finish)
+    w.win_on = ctx.auc_win_valid ? 1 : 0;
+    w.win_lo = ctx.auc_win_lo;
+    w.hist = reinterpret_cast<uint32_t*>(ar + fb + 512);
+    w.l2 = reinterpret_cast<uint32_t*>(ar + fb + 512 + al(hb));
     return w;
 }
-// keys and histograms written: the cross-bucket pass, the scatter of the
-// mixed buckets, the within-bucket pass; read back (synchronizes)
-void auc_finish(Ctx& ctx, auc::Work& w, const uint8_t* labels, long long n, double* auc, double* acc) {
+// keys and key range written: the histogram pass, then the full-resolution
+// scan or (wide key ranges) the cross-bucket pass, the scatter of the mixed
+// buckets and the within-bucket passes -- the kernels of the path not taken
+// exit at once (device-side decision, no host round trip); read back (synchronizes)
+// the general path's kernels (each exits at once when the full-resolution path applies)
+void auc_general(Ctx& ctx, auc::Work& w, const uint8_t* labels, long long n) {
     cudaStream_t s = ctx.stream;
     const int sms = device_sm_count(ctx.device);
     auc::auc_scan_totals_kernel<<<auc::kScanBlocks, auc::kThreads, 0, s>>>(w);
     auc::auc_scan_kernel<<<auc::kScanBlocks, auc::kThreads, 0, s>>>(w);
-    count_launch();
     auc::auc_scatter_kernel<<<(unsigned)std::min<long long>(nblocks(n, 256), 8LL * sms), 256, 0, s>>>(w, labels, n);
     ensure_smem_attr(reinterpret_cast<const void*>(auc::auc_bucket_kernel), auc::kBucketSmem);
     auc::auc_bucket_kernel<<<8 * sms, auc::kBucketThreads, auc::kBucketSmem, s>>>(w);
     auc::auc_l2_totals_kernel<<<2 * sms, auc::kThreads, 0, s>>>(w);
     auc::auc_l2_kernel<<<2 * sms, auc::kThreads, 0, s>>>(w);
-    count_launch();
-    count_launch();
-    count_launch();
-    count_launch();
-    count_launch();
-    unsigned long long* h = static_cast<unsigned long long*>(ctx.pinned_buf(64));
-    MTK_CUDA(cudaMemcpyAsync(h, w.cnt, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-    MTK_CUDA(cudaStreamSynchronize(s));
+    for (int i = 0; i < 6; ++i) count_launch();
+}
+// keys and key range written: the histogram pass, then the full-resolution
+// scan or (wide key ranges) the general path.  Which one applies is known on
+// the device; the host predicts it from the context's previous call and
+// launches only that path's kernels -- on a misprediction to "full
+// resolution" the general kernels follow the read-back (one more round trip;
+// the result does not depend on the prediction).  Reads back (synchronizes).
+void auc_finish(Ctx& ctx, auc::Work& w, const uint8_t* labels, long long n, double* auc, double* acc) {
+    cudaStream_t s = ctx.stream;
+    const int sms = device_sm_count(ctx.device);
+    const unsigned hist_grid = (unsigned)std::min<long long>(nblocks(n, 256), 8LL * sms);
+    auto readback = [&](unsigned long long* h) {
+        MTK_CUDA(cudaMemcpyAsync(h, w.cnt, 10 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));  // counters, mm[0..2]
+        MTK_CUDA(cudaStreamSynchronize(s));
+    };
+    unsigned long long* h = static_cast<unsigned long long*>(ctx.pinned_buf(128));
+    const uint32_t* mm = reinterpret_cast<const uint32_t*>(h + 8);
+    bool spec_ok = false;
+    if (w.win_on) {  // the keys were binned speculatively in the window
+        auc::auc_fast_scan_kernel<<<auc_fast_blocks(ctx), auc::kFastScanThreads, 0, s>>>(w);
+        count_launch();
+        readback(h);
+        spec_ok = mm[2] == 0;
+        w.win_on = 0;  // a re-run bins from the keys
+    }
+    if (!spec_ok) {
+        auc::auc_hist_kernel<<<hist_grid, 256, 0, s>>>(w, labels, n);
+        auc::auc_fast_scan_kernel<<<auc_fast_blocks(ctx), auc::kFastScanThreads, 0, s>>>(w);
+        count_launch();
+        count_launch();
+        if (!ctx.auc_fast_hint) auc_general(ctx, w, labels, n);
+        readback(h);
+        const bool fast = mm[0] - ~mm[1] < (1u << auc::kFastBits);
+        if (ctx.auc_fast_hint && !fast) {
+            auc_general(ctx, w, labels, n);
+            readback(h);
+        }
+        ctx.auc_fast_hint = fast;
+    }
+    // the next call's window: this key range, centred in 2^kFastBits bins
+    const uint32_t kmin = ~mm[1], kmax = mm[0], range = kmax - kmin;
+    const uint32_t span = (1u << auc::kFastBits) - 1u;
+    ctx.auc_win_valid = range < span;
+    if (ctx.auc_win_valid) {
+        const uint32_t slack = (span - range) / 2;
+        uint32_t lo = kmin >= slack ? kmin - slack : 0u;
+        if (lo > 0xFFFFFFFFu - span) lo = 0xFFFFFFFFu - span;  // no wrap past the top key
+        ctx.auc_win_lo = lo;
+    }
     const double npos = (double)h[0], nneg = (double)n - npos;
     if (h[0] == 0 || npos == (double)n)
         fail(MTK_VALUE_ERROR, "auc: need at least one member and one non-member");

@@ -140,12 +140,16 @@ def _u2_numpy(s, lab):
 
 
 @pytest.mark.parametrize("case", ["spread", "few_values", "one_value", "signed_zero", "narrow", "huge_bucket",
-                                  "tiny"])
+                                  "tiny", "fast_edge", "general_edge", "fast_dense"])
 def test_auc_histogram_paths_exact(ctx, case):
-    """The sort-free AUC (auc.cuh): cross-bucket counts, small buckets
-    (shared-memory sort), large buckets (> 8192 queries: 65536-bin histogram),
-    all-equal scores, -0.0 == +0.0, negative scores -- the AUC equals the
-    exact integer U2 / 2 / (npos nneg) computed independently."""
+    """The sort-free AUC (auc.cuh) on both paths: the full-resolution key
+    histogram (key range < 2^23: one_value, narrow, huge_bucket, fast_edge =
+    a range of exactly 2^23 - 1 keys, fast_dense = 2^20 queries over a 2^20
+    range) and the top-16-bit buckets (wider: spread, few_values,
+    signed_zero, tiny, general_edge = a range of exactly 2^23): cross-bucket
+    counts, small buckets (shared-memory sort), large buckets (65536-bin
+    histogram), all-equal scores, -0.0 == +0.0, negative scores -- the AUC
+    equals the exact integer U2 / 2 / (npos nneg) computed independently."""
     from paper_2011_09463_b200 import api
 
     rng = np.random.default_rng(hash(case) % 2**32)
@@ -163,6 +167,14 @@ def test_auc_histogram_paths_exact(ctx, case):
         s = (0.5 + rng.random(n) / 256).astype(np.float32)
     elif case == "huge_bucket":  # one bucket with ~all queries, distinct low bits
         s = np.float32(0.75) + (rng.integers(0, 60000, n) * np.float32(2.0 ** -24)).astype(np.float32)
+    elif case in ("fast_edge", "general_edge"):  # floats in [1, 2] have consecutive keys
+        k = rng.integers(0, 1 << 23, n, dtype=np.int64)
+        k[1] = 0
+        k[2] = (1 << 23) - 1 if case == "fast_edge" else 1 << 23  # 2^23 - 1 / 2^23 keys of range
+        s = (np.uint32(0x3F800000) + k.astype(np.uint32)).view(np.float32)
+    elif case == "fast_dense":  # attack-score-like: 2^20 queries, ~2^20-key range, many ties
+        n = 1 << 20
+        s = np.float32(0.5) + (rng.integers(0, 1 << 20, n) * np.float32(2.0 ** -24)).astype(np.float32)
     else:
         n = 5
         s = np.array([0.1, 0.4, 0.35, 0.8, 0.4], dtype=np.float32)
