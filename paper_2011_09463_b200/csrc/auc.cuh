@@ -216,13 +216,6 @@ __global__ void __launch_bounds__(256) auc_hist_kernel(Work w, const uint8_t* la
     }
 }
 
-// non-members in the first k0 blocks' bins (the combine loop's carry past 1024 blocks)
-__device__ __forceinline__ unsigned long long carry_blocks(const Work& w, unsigned k0) {
-    unsigned long long c = 0;
-    for (unsigned k = 0; k < k0; ++k) c += __ldcg(w.fpart + 3 * k);
-    return c;
-}
-
 // F2: U2 over the full-resolution bins [0, kmax - kmin]
 constexpr int kFastScanThreads = 1024;
 __global__ void __launch_bounds__(kFastScanThreads) auc_fast_scan_kernel(Work w) {
@@ -308,16 +301,17 @@ __global__ void __launch_bounds__(kFastScanThreads) auc_fast_scan_kernel(Work w)
     __syncthreads();
     if (last) {  // combine in block order: + 2 #{non-members in earlier blocks} per member (one block per thread)
         __threadfence();
-        unsigned long long t = 0;
-        for (unsigned k0 = 0; k0 < gridDim.x; k0 += kFastScanThreads) {  // (gridDim.x <= 1024 in practice)
+        unsigned long long t = 0, carry_n = 0;
+        for (unsigned k0 = 0; k0 < gridDim.x; k0 += kFastScanThreads) {
             const unsigned k = k0 + threadIdx.x;
             const bool in = k < gridDim.x;
             const uint32_t nk = in ? (uint32_t)__ldcg(w.fpart + 3 * k) : 0u;
             const unsigned long long pk = in ? __ldcg(w.fpart + 3 * k + 1) : 0ull;
             const unsigned long long uk = in ? __ldcg(w.fpart + 3 * k + 2) : 0ull;
             uint32_t tot;
-            const uint32_t before = (uint32_t)carry_blocks(w, k0) + block_excl_scan(nk, sh, &tot);
+            const unsigned long long before = carry_n + block_excl_scan(nk, sh, &tot);
             t += uk + 2ull * before * pk;
+            carry_n += tot;
         }
         t = block_sum_u64(t, shl);
         if (threadIdx.x == 0) {
