@@ -75,7 +75,8 @@ void dispatch2(const UmmaParams& p, int a_mn, int b_mn, int G, cudaStream_t s) {
         else if (e == (int)Epi::kStore) launch_variant<0, 1, PAIR, SEPC, (int)Epi::kStore>(p, G, s);
         else launch_variant<0, 1, PAIR, SEPC, -1>(p, G, s);
     } else if (!a_mn && !b_mn) {
-        if (e == (int)Epi::kMask) launch_variant<0, 0, PAIR, SEPC, (int)Epi::kMask>(p, G, s);
+        if (e == (int)Epi::kMask && !p.add) launch_variant<0, 0, PAIR, SEPC, kEpiMaskNoAdd>(p, G, s);
+        else if (e == (int)Epi::kMask) launch_variant<0, 0, PAIR, SEPC, (int)Epi::kMask>(p, G, s);
         else launch_variant<0, 0, PAIR, SEPC, -1>(p, G, s);
     } else if (a_mn && b_mn) {
         if (e == (int)Epi::kSgd) launch_variant<1, 1, PAIR, SEPC, (int)Epi::kSgd>(p, G, s);

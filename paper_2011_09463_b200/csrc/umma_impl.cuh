@@ -85,13 +85,20 @@ constexpr int NUM_EPI_WARPS = 8;   // two per TMEM lane quarter, each half the c
 // operand (bias / bias + ReLU: FWD 239.8 -> 232 us per step) and slows the
 // others, whose preloaded operands spill at 128 registers (DX, DW + SGD,
 // MMD gradient: +20..50 us) -- those keep the thread-per-row path.
+// Template-only epilogue kind: the ReLU-mask DX without an addend (the bank's
+// DX launches).  Without the addend the coalesced epilogue preloads no
+// per-element operand, and so does not spill.
+constexpr int kEpiMaskNoAdd = 16;
+template <int EPI>
+constexpr int epi_kind() { return EPI == kEpiMaskNoAdd ? (int)Epi::kMask : EPI; }
+
 template <int EPI>
 struct EpiPlan {
 #ifdef MTK_UMMA_COAL_ALL
     static constexpr bool coal = MTK_UMMA_COAL && EPI >= 0;
 #else
     static constexpr bool coal = MTK_UMMA_COAL && (EPI == (int)Epi::kBias || EPI == (int)Epi::kBiasRelu ||
-                                                   EPI == (int)Epi::kStore);
+                                                   EPI == (int)Epi::kStore || EPI == kEpiMaskNoAdd);
 #endif
     static constexpr int ls = coal ? 4 : 5;  // load stages
     static constexpr int tile_bytes = coal ? 32 * 32 * 4 : 0;
@@ -250,7 +257,7 @@ __device__ __forceinline__ void epilogue_rows(const UmmaParams& p, uint32_t tmem
     const int m = mw + lane;
     const bool row_ok = m < p.M;
     const long long rowbase = (long long)g * p.c_gs + (long long)m * p.ldc;
-    const int epi = EPI >= 0 ? EPI : p.epi;  // compile-time for the specialised launches
+    const int epi = EPI >= 0 ? epi_kind<EPI>() : p.epi;  // compile-time for the specialised launches
     bool bad = false;
 #pragma unroll 1
     for (int c = c0; c < c1; ++c) {
@@ -426,7 +433,8 @@ template <int EPI>
 __device__ __forceinline__ float4 epi_operand(const UmmaParams& p, int g, int m, int ncol) {
     const long long idx = (long long)g * p.c_gs + (long long)m * p.ldc + ncol;
     if (m < p.M && p.ediag == 0) {
-        if (EPI == (int)Epi::kMask) {
+        if (EPI == kEpiMaskNoAdd) {
+        } else if (EPI == (int)Epi::kMask) {
             if (p.add) return *reinterpret_cast<const float4*>(p.add + idx);
         } else if (EPI == (int)Epi::kSgd) {
             return *reinterpret_cast<const float4*>(p.C + idx);
@@ -439,7 +447,7 @@ __device__ __forceinline__ float4 epi_operand(const UmmaParams& p, int g, int m,
 template <int EPI>
 __device__ __forceinline__ uint32_t epi_rowword(const UmmaParams& p, int g, int m, int nb) {
     if (m < p.M) {
-        if (EPI == (int)Epi::kMask && p.mbits) return p.mbits[(long long)g * p.mb_gs + (long long)m * p.mb_ld + nb / 32];
+        if (epi_kind<EPI>() == (int)Epi::kMask && p.mbits) return p.mbits[(long long)g * p.mb_gs + (long long)m * p.mb_ld + nb / 32];
         if (EPI == (int)Epi::kMmdGrad) return __float_as_uint(p.rowvec[(long long)g * p.M + m]);
     }
     return 0u;
@@ -481,7 +489,9 @@ template <bool SEPC, int EPI>
 __device__ __forceinline__ void epilogue_coalesced(const UmmaParams& p, uint32_t tmem, uint32_t tcorr, int q,
                                                    int lane, int g, int m0, int n0, int c0, int c1, uint32_t tile,
                                                    uint32_t roww, unsigned long long* etr = nullptr) {
-    constexpr bool kBiasE = EPI == (int)Epi::kBias || EPI == (int)Epi::kBiasRelu;
+    constexpr int E = epi_kind<EPI>();  // the arithmetic kind (kEpiMaskNoAdd: kMask without an addend)
+    constexpr bool kAdd = EPI != kEpiMaskNoAdd;
+    constexpr bool kBiasE = E == (int)Epi::kBias || E == (int)Epi::kBiasRelu;
     const int mw = m0 + 32 * q;
     const int gq = lane & 7, rsub = lane >> 3;
     const bool aligned = (p.c_gs % 4 == 0) && (p.ldc % 4 == 0);
@@ -493,7 +503,7 @@ __device__ __forceinline__ void epilogue_coalesced(const UmmaParams& p, uint32_t
         const int nb = n0 + c * 32;
         if (nb >= p.N) break;  // warp-uniform
         if (!aligned || nb + 32 > p.N) {
-            epilogue_rows_cold<SEPC, EPI>(p, tmem, tcorr, q, lane, g, m0, n0, c);
+            epilogue_rows_cold<SEPC, EPI>(p, tmem, tcorr, q, lane, g, m0, n0, c);  // (maps EPI itself)
             continue;
         }
         const int ncol = nb + 4 * gq;  // this lane's first column
@@ -523,7 +533,7 @@ __device__ __forceinline__ void epilogue_coalesced(const UmmaParams& p, uint32_t
                 bad |= t == 12345.f;
                 continue;
             }
-            if (EPI == (int)Epi::kMask || EPI == (int)Epi::kMmdGrad) sts32(roww + 4u * lane, rw);
+            if (E == (int)Epi::kMask || E == (int)Epi::kMmdGrad) sts32(roww + 4u * lane, rw);
         }
         __syncwarp();
         // the chunk's operands, issued once the accumulator registers are free
@@ -536,7 +546,7 @@ __device__ __forceinline__ void epilogue_coalesced(const UmmaParams& p, uint32_t
             const int m = mw + r;
             float4 x = lds128(tile + (uint32_t)(r * 128 + ((gq ^ (r & 7)) * 16)));
             const float4 op = ops.o[i];
-            const uint32_t rword = (EPI == (int)Epi::kMask || EPI == (int)Epi::kMmdGrad) ? lds32(roww + 4u * r) : 0u;
+            const uint32_t rword = (E == (int)Epi::kMask || E == (int)Epi::kMmdGrad) ? lds32(roww + 4u * r) : 0u;
             const bool ok = m < p.M && p.ediag != 2;
             const long long idx = (long long)g * p.c_gs + (long long)m * p.ldc + ncol;
             if (kBiasE) {
@@ -545,14 +555,14 @@ __device__ __forceinline__ void epilogue_coalesced(const UmmaParams& p, uint32_t
                 x.z += bias4.z;
                 x.w += bias4.w;
                 if (ok) bad |= !(isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w));
-                if (EPI == (int)Epi::kBiasRelu) {
+                if (E == (int)Epi::kBiasRelu) {
                     x.x = x.x > 0.f ? x.x : 0.f;
                     x.y = x.y > 0.f ? x.y : 0.f;
                     x.z = x.z > 0.f ? x.z : 0.f;
                     x.w = x.w > 0.f ? x.w : 0.f;
                 }
-            } else if (EPI == (int)Epi::kMask) {
-                if (p.add) {
+            } else if (E == (int)Epi::kMask) {
+                if (kAdd && p.add) {
                     x.x = op.x + x.x;
                     x.y = op.y + x.y;
                     x.z = op.z + x.z;
@@ -571,7 +581,7 @@ __device__ __forceinline__ void epilogue_coalesced(const UmmaParams& p, uint32_t
                     x.z = mk.z > 0.f ? x.z : 0.f;
                     x.w = mk.w > 0.f ? x.w : 0.f;
                 }
-            } else if (EPI == (int)Epi::kMmdGrad) {
+            } else if (E == (int)Epi::kMmdGrad) {
                 const float rv = __uint_as_float(rword);
                 x.x = p.scale * fmaf(op.x, rv, -x.x);
                 x.y = p.scale * fmaf(op.y, rv, -x.y);
@@ -584,7 +594,7 @@ __device__ __forceinline__ void epilogue_coalesced(const UmmaParams& p, uint32_t
                     x.z = op.z > 0.f ? x.z : 0.f;
                     x.w = op.w > 0.f ? x.w : 0.f;
                 }
-            } else if (EPI == (int)Epi::kSgd) {
+            } else if (E == (int)Epi::kSgd) {
                 if (ok && p.grad_out) *reinterpret_cast<float4*>(p.grad_out + idx) = x;
                 x.x = sgd_update(op.x, x.x, p.lr);
                 x.y = sgd_update(op.y, x.y, p.lr);
@@ -593,8 +603,8 @@ __device__ __forceinline__ void epilogue_coalesced(const UmmaParams& p, uint32_t
                 if (ok) bad |= !(isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w));
             }
             if (!ok) x = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (EPI != (int)Epi::kNone && ok) *reinterpret_cast<float4*>(p.C + idx) = x;
-            if (EPI == (int)Epi::kBiasRelu && p.mbits) {  // this chunk's ReLU mask bits of row r
+            if (E != (int)Epi::kNone && ok) *reinterpret_cast<float4*>(p.C + idx) = x;
+            if (E == (int)Epi::kBiasRelu && p.mbits) {  // this chunk's ReLU mask bits of row r
                 uint32_t nib = ((x.x > 0.f) ? 1u : 0u) | ((x.y > 0.f) ? 2u : 0u) | ((x.z > 0.f) ? 4u : 0u) |
                                ((x.w > 0.f) ? 8u : 0u);
                 nib <<= 4 * gq;
@@ -610,7 +620,7 @@ __device__ __forceinline__ void epilogue_coalesced(const UmmaParams& p, uint32_t
         }
         __syncwarp();  // the tile is rewritten by the next chunk
         if (etr && lane == 0) etr[4 * (c - c0) + 2] = gtime();
-        if (p.colsum && (EPI == (int)Epi::kMask || EPI == (int)Epi::kMmdGrad) && mw < p.M) {
+        if (p.colsum && (E == (int)Epi::kMask || E == (int)Epi::kMmdGrad) && mw < p.M) {
             // per-32-row-block column sums of the stored values (next layer's db)
 #pragma unroll
             for (int o = 8; o <= 16; o <<= 1) {

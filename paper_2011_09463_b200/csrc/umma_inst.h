@@ -24,6 +24,7 @@
 
 #define MTK_UMMA_PART_D(X) \
     MTK_UMMA_LV(X, 0, 0, (int)Epi::kMask) \
+    MTK_UMMA_LV(X, 0, 0, kEpiMaskNoAdd) \
     MTK_UMMA_LV(X, 1, 1, (int)Epi::kSgd) \
     MTK_UMMA_LV(X, 1, 1, (int)Epi::kStore)
 
