@@ -81,24 +81,26 @@ constexpr int NUM_EPI_WARPS = 8;   // two per TMEM lane quarter, each half the c
 // Epilogue plan per epilogue kind.  The smem-staged coalesced epilogue
 // (epilogue_coalesced) takes a 4 KB tile + 128 B of row words per epilogue
 // warp, paid for with one load stage (LS 5 -> 4).  Measured (same box, C2
-// step): it speeds up the launches whose epilogue preloads no per-element
-// operand (bias / bias + ReLU: FWD 239.8 -> 232 us per step) and slows the
-// others, whose preloaded operands spill at 128 registers (DX, DW + SGD,
-// MMD gradient: +20..50 us) -- those keep the thread-per-row path.
+// step, the thread-per-row path as the baseline): bias / bias + ReLU (FWD)
+// 239.8 -> 232 us, ReLU-mask DX without an addend 70.8 -> 62.8 us, SGD (DW,
+// operands loaded in groups of 4 passes) 238.8 -> 220.5 us; the MMD-gradient
+// epilogue (z and the row scale per element) spills and measured slower
+// (+20 us), so it and the DX with an addend keep the thread-per-row path.
+//
 // Template-only epilogue kind: the ReLU-mask DX without an addend (the bank's
-// DX launches).  Without the addend the coalesced epilogue preloads no
-// per-element operand, and so does not spill.
+// DX launches).  Without the addend the coalesced epilogue loads no
+// per-element operand.
 constexpr int kEpiMaskNoAdd = 16;
 template <int EPI>
 constexpr int epi_kind() { return EPI == kEpiMaskNoAdd ? (int)Epi::kMask : EPI; }
-
 template <int EPI>
 struct EpiPlan {
 #ifdef MTK_UMMA_COAL_ALL
     static constexpr bool coal = MTK_UMMA_COAL && EPI >= 0;
 #else
     static constexpr bool coal = MTK_UMMA_COAL && (EPI == (int)Epi::kBias || EPI == (int)Epi::kBiasRelu ||
-                                                   EPI == (int)Epi::kStore || EPI == kEpiMaskNoAdd);
+                                                   EPI == (int)Epi::kStore || EPI == kEpiMaskNoAdd ||
+                                                   EPI == (int)Epi::kSgd);
 #endif
     static constexpr int ls = coal ? 4 : 5;  // load stages
     static constexpr int tile_bytes = coal ? 32 * 32 * 4 : 0;
@@ -420,15 +422,10 @@ __device__ __noinline__ void epilogue_rows_cold(const UmmaParams& p, uint32_t tm
 
 // Operands of the coalesced epilogue (below): per pass i the float4 of row
 // mw + 4i + lane/8 at columns ncol..+3 (add | master weight | z), per row
-// (thread = row) the chunk's mask word or row scale, the bias columns.
-// They are issued before the chunk's TMEM read (one memory round trip per
-// chunk; loading chunk c + 1's during chunk c, or the first chunk's before
-// the accumulator wait, spilled at 128 registers and measured slower).
-struct EpiOps {
-    float4 o[8];
-    float4 bias4;
-    uint32_t rw;
-};
+// (thread = row) the chunk's mask word or row scale, the bias columns.  They
+// are loaded once the chunk's accumulator is staged, in groups of passes
+// (preloading a whole chunk, the next chunk's, or the first chunk's before
+// the accumulator wait spilled at 128 registers and measured slower).
 template <int EPI>
 __device__ __forceinline__ float4 epi_operand(const UmmaParams& p, int g, int m, int ncol) {
     const long long idx = (long long)g * p.c_gs + (long long)m * p.ldc + ncol;
@@ -461,19 +458,6 @@ __device__ __forceinline__ float4 epi_bias(const UmmaParams& p, int g, int ncol)
 __device__ __forceinline__ bool epi_fast_chunk(const UmmaParams& p, int nb) {
     return (p.c_gs % 4 == 0) && (p.ldc % 4 == 0) && nb + 32 <= p.N;
 }
-// chunk c's operands (no-op for a ragged chunk: the row path loads its own)
-template <int EPI>
-__device__ __forceinline__ void epi_prefetch(const UmmaParams& p, int lane, int g, int m0, int n0, int q, int c,
-                                             EpiOps& ops) {
-    const int nb = n0 + c * 32;
-    if (nb >= p.N || !epi_fast_chunk(p, nb)) return;
-    const int mw = m0 + 32 * q, ncol = nb + 4 * (lane & 7);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) ops.o[i] = epi_operand<EPI>(p, g, mw + 4 * i + (lane >> 3), ncol);
-    ops.bias4 = epi_bias<EPI>(p, g, ncol);
-    ops.rw = epi_rowword<EPI>(p, g, mw + lane, nb);
-}
-
 // The same epilogue through a 32 x 32 shared-memory tile per warp: the TMEM
 // rows (thread = row) are written to the tile, __syncwarp, and read back as
 // 8 passes of 4 rows x 32 columns (lane = row 4i + lane/8, columns 4 (lane%8)
@@ -497,7 +481,6 @@ __device__ __forceinline__ void epilogue_coalesced(const UmmaParams& p, uint32_t
     const bool aligned = (p.c_gs % 4 == 0) && (p.ldc % 4 == 0);
     const uint32_t wrow = tile + (uint32_t)lane * 128u;
     bool bad = false;
-    EpiOps ops;
 #pragma unroll 1
     for (int c = c0; c < c1; ++c) {
         const int nb = n0 + c * 32;
@@ -536,16 +519,23 @@ __device__ __forceinline__ void epilogue_coalesced(const UmmaParams& p, uint32_t
             if (E == (int)Epi::kMask || E == (int)Epi::kMmdGrad) sts32(roww + 4u * lane, rw);
         }
         __syncwarp();
-        // the chunk's operands, issued once the accumulator registers are free
-        epi_prefetch<EPI>(p, lane, g, m0, n0, q, c, ops);
-        const float4 bias4 = ops.bias4;
+        // the chunk's operands, issued once the accumulator registers are free,
+        // in groups of GS passes (8 preloaded float4s spilled at 128 registers)
+        const float4 bias4 = epi_bias<EPI>(p, g, ncol);
         float4 cs = make_float4(0.f, 0.f, 0.f, 0.f);
+        constexpr int GS = (E == (int)Epi::kMmdGrad || E == (int)Epi::kMask) ? 2 : 4;  // passes per operand group
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
+        for (int hp = 0; hp < 8 / GS; ++hp) {
+        float4 oh[GS];
+#pragma unroll
+        for (int ii = 0; ii < GS; ++ii) oh[ii] = epi_operand<EPI>(p, g, mw + 4 * (GS * hp + ii) + rsub, ncol);
+#pragma unroll
+        for (int ii = 0; ii < GS; ++ii) {
+            const int i = GS * hp + ii;
             const int r = 4 * i + rsub;
             const int m = mw + r;
             float4 x = lds128(tile + (uint32_t)(r * 128 + ((gq ^ (r & 7)) * 16)));
-            const float4 op = ops.o[i];
+            const float4 op = oh[ii];
             const uint32_t rword = (E == (int)Epi::kMask || E == (int)Epi::kMmdGrad) ? lds32(roww + 4u * r) : 0u;
             const bool ok = m < p.M && p.ediag != 2;
             const long long idx = (long long)g * p.c_gs + (long long)m * p.ldc + ncol;
@@ -618,6 +608,7 @@ __device__ __forceinline__ void epilogue_coalesced(const UmmaParams& p, uint32_t
             cs.z += x.z;
             cs.w += x.w;
         }
+        }  // halves
         __syncwarp();  // the tile is rewritten by the next chunk
         if (etr && lane == 0) etr[4 * (c - c0) + 2] = gtime();
         if (p.colsum && (E == (int)Epi::kMask || E == (int)Epi::kMmdGrad) && mw < p.M) {
