@@ -241,6 +241,20 @@ def test_step_ragged_shapes_and_weights(ctx):
     check_step(bank, X, y, w=w, lr=0.3)
 
 
+@pytest.mark.parametrize("lam", [0.0, 0.7])
+def test_step_staged_epilogue_ragged_chunks(ctx, lam):
+    """tcgen05 layers whose widths are not multiples of 32 and row counts not
+    multiples of the 128-row tile: the smem-staged epilogues (bias + ReLU,
+    ReLU-mask DX without an addend, SGD) take the thread-per-row path for the
+    last, ragged 32-column chunk and mask the rows past M; parity with the
+    oracle at the per-kernel tolerance (with and without the MMD)."""
+    dims = [100, 72, 44, 10]
+    bank = make_bank(ctx, 3, dims, seed=21)
+    assert bank.tc_layers()[:2] == [True, True], bank.tc_layers()
+    X, y = inputs(3, 300, dims[0], dims[-1], shift=0.3)
+    check_step(bank, X, y, src=140 if lam else 0, lam=lam, lr=0.1)
+
+
 def test_step_narrow_input_layer(ctx):
     """fan_in <= 32 < fan_out (the attack model's k -> 64 layer): dW runs as the
     transposed skinny reduction."""
