@@ -235,6 +235,9 @@ struct UmmaGemm {
     int* flags = nullptr;
 };
 void launch_umma(const UmmaGemm& u, cudaStream_t s);
+namespace umma {
+bool pdl_enabled();  // programmatic dependent launch of the tcgen05 kernels (MTK_PDL, default on)
+}
 
 // Skinny layers (out width <= 32): k_head.cu
 struct CeArgs;

@@ -840,6 +840,7 @@ __global__ void __launch_bounds__(W_THREADS, 1) mmd_w_kernel(const __grid_consta
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc<512>(tmem_slot);
+    pdl_wait();  // the predecessors' outputs (beta, norms, planes) are read from here on
     for (int g = threadIdx.x; g < p.G && g < W_MAX_G_TAB; g += blockDim.x) {
         const double beta = p.beta[g];
         gtab[g] = make_float2((float)(-1.4426950408889634 / beta), (float)(2.0 / beta));
@@ -1142,6 +1143,7 @@ __global__ void __launch_bounds__(W_THREADS, 1) mmd_w_kernel(const __grid_consta
         }
         if (bad && p.flags) atomicOr(p.flags, kFlagNonFinite);
     }
+    pdl_trigger();
     tc_fence_before();
     __syncthreads();
     if (warp == 1) {
@@ -1535,7 +1537,19 @@ void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s, int stages) 
         ensure_smem_attr(reinterpret_cast<const void*>(mmd_w_kernel), W_SMEM_BYTES);
         const int sms = device_sm_count(current_device());
         const int items = a.G * (w.nA + w.nB);
-        mmd_w_kernel<<<std::min(items, sms), W_THREADS, W_SMEM_BYTES, s>>>(w);
+        {
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3((unsigned)std::min(items, sms));
+            cfg.blockDim = dim3(W_THREADS);
+            cfg.dynamicSmemBytes = W_SMEM_BYTES;
+            cfg.stream = s;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (mmd_w calls pdl_wait)
+            at[0].val.programmaticStreamSerializationAllowed = umma::pdl_enabled() ? 1 : 0;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            MTK_CUDA(cudaLaunchKernelEx(&cfg, mmd_w_kernel, w));
+        }
         count_launch();
         const long long nbw = ((long long)a.G * wr.NR + WSUM_THREADS - 1) / WSUM_THREADS;
         const int NT = wr.tb - wr.ta;

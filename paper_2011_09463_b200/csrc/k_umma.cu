@@ -53,6 +53,16 @@ CUtensorMap make_map(const float* base, long long inner, long long outer, long l
     return m;
 }
 
+// programmatic dependent launch of the GEMM (and mmd_w) launches; MTK_PDL=0 disables (A/B)
+bool pdl_enabled() {
+    static int mode = -1;
+    if (mode < 0) {
+        const char* e = getenv("MTK_PDL");
+        mode = e ? atoi(e) : 1;
+    }
+    return mode != 0;
+}
+
 bool disable_half_tiles() {
     static int mode = -1;
     if (mode < 0) {

@@ -714,6 +714,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_kernel(const __grid_const
     else __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    // the prologue above overlapped the predecessor's tail (PDL launch); its
+    // outputs are read from here on
+    pdl_wait();
 
     // Producer and MMA warps run their loops converged (all lanes wait, lane 0
     // issues); see k_mmd_tc.cu for the divergent-lane stall this avoids.
@@ -843,6 +846,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_kernel(const __grid_const
             }
         }
     }
+    pdl_trigger();  // this CTA's work is issued: the next launch may start its prologue
     tc_fence_before();
     if (PAIR) cluster_sync();
     else __syncthreads();
@@ -858,6 +862,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_kernel(const __grid_const
 
 
 bool disable_half_tiles();
+bool pdl_enabled();
 
 template <int A_MN, int B_MN, bool PAIR, bool SEPC, int EPI>
 void launch_variant(UmmaParams p, int G, cudaStream_t s) {
@@ -879,13 +884,15 @@ void launch_variant(UmmaParams p, int G, cudaStream_t s) {
     cfg.blockDim = dim3(NUM_THREADS);
     cfg.dynamicSmemBytes = EpiPlan<EPI>::smem;
     cfg.stream = s;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = PAIR ? 2 : 1;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (the kernel calls pdl_wait)
+    at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     MTK_CUDA(cudaLaunchKernelEx(&cfg, umma_kernel<A_MN, B_MN, PAIR, SEPC, EPI>, p));
     count_launch();
 }
