@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "minitransfer/mtk.h"
@@ -236,8 +237,9 @@ struct UmmaGemm {
 };
 void launch_umma(const UmmaGemm& u, cudaStream_t s);
 namespace umma {
-bool pdl_enabled();  // programmatic dependent launch of the tcgen05 kernels (MTK_PDL, default on)
+bool pdl_enabled();  // programmatic dependent launch (MTK_PDL, default on)
 }
+
 
 // Skinny layers (out width <= 32): k_head.cu
 struct CeArgs;
