@@ -8,6 +8,8 @@
 // Register blocking keeps the shared-memory wavefront count per FMA low: the
 // narrow operand (W row or dZ row) is read as broadcast float4.
 // Reductions run in a fixed order (bit-deterministic).
+#include <cooperative_groups.h>
+
 #include <cmath>
 #include <utility>
 
@@ -478,10 +480,23 @@ __device__ __forceinline__ void epoch_reduce_all(float (&acc)[E_NG], int lane, c
     ((acc[gi] += epoch_reduce<gi>(lane, x, hv, dh, dlog)), ...);
 }
 
+// One thread-block cluster per model: CTA c of the cluster takes row set c
+// (rows c * 256 + t) of every step, so a 1024-row step runs on four SMs
+// instead of one (the kernel is latency-bound on its butterflies; one CTA
+// did 4 row sets in series).  The gradient sums keep the one-CTA order
+// exactly: per warp w, ((0 + B_0) + B_1) + ... over the row sets (B_c = the
+// warp's butterfly over row set c, read from CTA c's shared memory), then the
+// warps in ascending order -- so the parameters are bit-identical to the
+// one-CTA kernel.  Every CTA applies the update to its own copy; rank 0
+// writes the model back.
 __global__ void __launch_bounds__(E_THREADS, 1) small2_epoch_kernel(SmallEpoch p) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
     __shared__ float prm[E_NG * 32];                      // W0 [K][H], b0 [H], W1 [H][O], b1 [O]
-    __shared__ float part[E_THREADS / 32][E_NG * 32];     // warp partials
-    const int g = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    __shared__ float part[E_THREADS / 32][E_NG * 32];     // this CTA's warp partials
+    const int nsets = (int)cluster.num_blocks();          // = ceil(B / 256)
+    const int rs = (int)cluster.block_rank();
+    const int g = blockIdx.x / nsets, t = threadIdx.x, lane = t & 31, warp = t >> 5;
     float* gW0 = p.W0 + (long long)g * E_K * E_H;
     float* gb0 = p.b0 + (long long)g * E_H;
     float* gW1 = p.W1 + (long long)g * E_H * E_O;
@@ -494,19 +509,20 @@ __global__ void __launch_bounds__(E_THREADS, 1) small2_epoch_kernel(SmallEpoch p
         else if (e < E_NP) v = gb1[e - E_K * E_H - E_H - E_H * E_O];
         prm[e] = v;
     }
+    const float* rpart[4];  // the cluster's partial arrays (row set c in CTA c)
+    for (int c = 0; c < 4; ++c) rpart[c] = c < nsets ? cluster.map_shared_rank(&part[0][0], c) : nullptr;
     __syncthreads();
     const float* W0 = prm;
     const float* B0 = W0 + E_K * E_H;
     const float* W1 = B0 + E_H;
     const float* B1 = W1 + E_H * E_O;
-    const int nsets = (p.B + E_THREADS - 1) / E_THREADS;
     bool bad = false;
     for (int s = 0; s < p.nsteps; ++s) {
         float acc[E_NG];
 #pragma unroll
         for (int q = 0; q < E_NG; ++q) acc[q] = 0.f;
         const float inv = (float)(1.0 / p.denom[s]);
-        for (int rs = 0; rs < nsets; ++rs) {
+        {
             const int r = rs * E_THREADS + t;
             float x[E_K], hv[E_H], dh[E_H], dlog[E_O];
 #pragma unroll
@@ -572,26 +588,31 @@ __global__ void __launch_bounds__(E_THREADS, 1) small2_epoch_kernel(SmallEpoch p
         }
 #pragma unroll
         for (int q = 0; q < E_NG; ++q) part[warp][q * 32 + lane] = acc[q];
-        __syncthreads();
-        // the warps in ascending order, then SGD (sgd_update, as every update site)
+        cluster.sync();  // every row set's partials written
+        // per warp the row sets in order, then the warps in ascending order, then SGD
         for (int e = t; e < E_NP; e += E_THREADS) {
             float gsum = 0.f;
 #pragma unroll
-            for (int w2 = 0; w2 < E_THREADS / 32; ++w2) gsum += part[w2][e];
+            for (int w2 = 0; w2 < E_THREADS / 32; ++w2) {
+                float a = rpart[0][w2 * E_NG * 32 + e];
+                for (int c = 1; c < nsets; ++c) a += rpart[c][w2 * E_NG * 32 + e];
+                gsum += a;
+            }
             const float nv = sgd_update(prm[e], gsum, p.lr);
             bad |= !isfinite(nv);
             prm[e] = nv;
         }
-        __syncthreads();
+        cluster.sync();  // partials read everywhere (the next step rewrites them); prm updated
     }
     if (bad) atomicOr(p.flags, kFlagNonFinite);
-    for (int e = t; e < E_NP; e += E_THREADS) {
-        const float v = prm[e];
-        if (e < E_K * E_H) gW0[e] = v;
-        else if (e < E_K * E_H + E_H) gb0[e - E_K * E_H] = v;
-        else if (e < E_K * E_H + E_H + E_H * E_O) gW1[e - E_K * E_H - E_H] = v;
-        else gb1[e - E_K * E_H - E_H - E_H * E_O] = v;
-    }
+    if (rs == 0)
+        for (int e = t; e < E_NP; e += E_THREADS) {
+            const float v = prm[e];
+            if (e < E_K * E_H) gW0[e] = v;
+            else if (e < E_K * E_H + E_H) gb0[e - E_K * E_H] = v;
+            else if (e < E_K * E_H + E_H + E_H * E_O) gW1[e - E_K * E_H - E_H] = v;
+            else gb1[e - E_K * E_H - E_H - E_H * E_O] = v;
+        }
 }
 
 bool small2_epoch_ok(int K, int H, int O, int B) { return K == E_K && H == E_H && O == E_O && B >= 1 && B <= 1024; }
@@ -599,7 +620,19 @@ bool small2_epoch_ok(int K, int H, int O, int B) { return K == E_K && H == E_H &
 void launch_small2_epoch(const SmallEpoch& p, cudaStream_t s) {
     if (!small2_epoch_ok(E_K, E_H, E_O, p.B)) fail(MTK_ERROR, "small2_epoch: unsupported shape");
     if (p.nsteps <= 0 || p.G <= 0) return;
-    small2_epoch_kernel<<<p.G, E_THREADS, 0, s>>>(p);
+    const int nsets = (p.B + E_THREADS - 1) / E_THREADS;  // <= 4: the cluster size
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(p.G * nsets));
+    cfg.blockDim = dim3(E_THREADS);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)nsets;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    MTK_CUDA(cudaLaunchKernelEx(&cfg, small2_epoch_kernel, p));
     count_launch();
 }
 
