@@ -11,6 +11,8 @@
 #include <cstring>
 #include <random>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "minitransfer/mtk.h"
 
@@ -104,20 +106,89 @@ int mtk_rng_fill_normal(mtk_rng* r, double* out, uint64_t n) {
     return MTK_OK;
 }
 
+// The population draws are sequential (one mt19937_64 stream: a label by
+// rejection, then d Box-Muller normals whose pairs straddle rows), but the
+// transcendentals dominate (19.3 M normals for the sweep's default pools:
+// ~0.4 s on one core).  So: one sequential pass takes every raw draw -- the
+// labels, and each Box-Muller pair's two raw words -- in stream order; the
+// pairs' normals (the same expressions as gauss(), so bit-identical) and the
+// rows are then formed on all host cores.
 int mtk_synth(mtk_rng* r, int C, int d, uint64_t n, const double* mu, const double* shift,
               double* X64, float* X32, int32_t* y) {
     if (!r || !mu || !y) return set_err(MTK_VALUE_ERROR, "mtk_synth: null argument");
     if (C <= 0 || d <= 0) return set_err(MTK_SHAPE_ERROR, "mtk_synth: zero dimension");
+    const uint64_t total = n * static_cast<uint64_t>(d);  // gauss() calls, in stream order
+    // pass 1 (sequential): labels, and the raw words of every new pair
+    const bool cached0 = r->cached;
+    const double cache0 = r->cache;
+    std::vector<uint64_t> words;
+    words.reserve(static_cast<size_t>(total + 2));
+    bool cached = cached0;
     for (uint64_t i = 0; i < n; ++i) {
-        const int c = static_cast<int>(r->bounded(static_cast<uint64_t>(C)));
-        y[i] = c;
-        const double* mrow = mu + static_cast<size_t>(c) * d;
+        y[i] = static_cast<int32_t>(r->bounded(static_cast<uint64_t>(C)));
         for (int k = 0; k < d; ++k) {
-            double v = mrow[k] + r->gauss();
-            if (shift) v = v + shift[k];
-            if (X64) X64[i * d + k] = v;
-            if (X32) X32[i * d + k] = static_cast<float>(v);
+            if (cached) {
+                cached = false;
+            } else {
+                const uint64_t w1 = r->eng();
+                const uint64_t w2 = r->eng();
+                words.push_back(w1);
+                words.push_back(w2);
+                cached = true;
+            }
         }
+    }
+    const size_t npairs = words.size() / 2;
+    // pass 2 (parallel): pair p -> (cos, sin) values, exactly as gauss()
+    std::vector<double> gc(npairs), gs(npairs);
+    auto pairs = [&](size_t a, size_t b) {
+        for (size_t p = a; p < b; ++p) {
+            const double u1 = 1.0 - static_cast<double>(words[2 * p] >> 11) * 0x1.0p-53;
+            const double u2 = static_cast<double>(words[2 * p + 1] >> 11) * 0x1.0p-53;
+            const double rad = std::sqrt(-2.0 * std::log(u1));
+            const double theta = 6.28318530717958647692 * u2;
+            gs[p] = rad * std::sin(theta);
+            gc[p] = rad * std::cos(theta);
+        }
+    };
+    // gauss call j (0-based, stream order): with the cache full on entry, call
+    // 0 returns cache0 and call j >= 1 belongs to pair (j - 1) / 2 (cos if
+    // (j - 1) even); otherwise pair j / 2 (cos if j even)
+    const uint64_t off = cached0 ? 1 : 0;
+    auto gauss_at = [&](uint64_t j) -> double {
+        if (cached0 && j == 0) return cache0;
+        const uint64_t q = j - off;
+        return (q & 1) ? gs[q >> 1] : gc[q >> 1];
+    };
+    auto rows = [&](uint64_t a, uint64_t b) {
+        for (uint64_t i = a; i < b; ++i) {
+            const double* mrow = mu + static_cast<size_t>(y[i]) * d;
+            for (int k = 0; k < d; ++k) {
+                double v = mrow[k] + gauss_at(i * d + k);
+                if (shift) v = v + shift[k];
+                if (X64) X64[i * d + k] = v;
+                if (X32) X32[i * d + k] = static_cast<float>(v);
+            }
+        }
+    };
+    unsigned nt = std::thread::hardware_concurrency();
+    nt = nt == 0 ? 1 : (nt > 32 ? 32 : nt);
+    if (total < (1u << 16)) nt = 1;
+    auto parallel = [&](uint64_t count, auto&& fn) {
+        std::vector<std::thread> th;
+        for (unsigned t = 1; t < nt; ++t)
+            th.emplace_back([&, t] { fn(count * t / nt, count * (t + 1) / nt); });
+        fn(0, count / nt);
+        for (auto& x : th) x.join();
+    };
+    parallel(npairs, pairs);
+    parallel(n, rows);
+    // the generator's Box-Muller cache as the sequential loop leaves it
+    if (cached) {  // the last pair's sin value is pending
+        r->cached = true;
+        r->cache = cached0 && npairs == 0 ? cache0 : gs[npairs - 1];
+    } else {
+        r->cached = false;
     }
     return MTK_OK;
 }

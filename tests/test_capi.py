@@ -75,6 +75,30 @@ def test_host_rng_streams_and_synth_match_oracle():
     assert np.array_equal(X32, oX.astype(np.float32))
 
 
+@pytest.mark.parametrize("pre", [0, 1, 2])
+def test_parallel_synth_matches_sequential_stream(pre):
+    """mtk_synth draws the stream in one sequential pass and forms the normals
+    on all host cores: bit-identical to the oracle's sequential restatement for
+    a population past the threading threshold (odd d: Box-Muller pairs straddle
+    rows), entered with and without a cached normal, and the generator state it
+    leaves (the next normal, the next raw draw) is the sequential one."""
+    from paper_2011_09463_b200 import api
+
+    C_, d, n = 7, 37, 6001
+    mu = po.Rng(15).normals(C_ * d).reshape(C_, d)
+    sh = po.Rng(16).normals(d)
+    r, o = api.Rng(33), po.Rng(33)
+    for _ in range(pre):  # pre = 1: a cached normal on entry
+        assert r.normal() == o.normal()
+    X32, y, X64 = r.synth(C_, d, n, mu, sh, f64=True)
+    oX, oy = po.synth(o, C_, d, n, mu, sh)
+    assert np.array_equal(X64, oX) and np.array_equal(y, oy)
+    assert np.array_equal(X32, oX.astype(np.float32))
+    assert r.normal() == o.normal()
+    assert np.array_equal(r.normals(5), o.normals(5))
+    assert np.array_equal(r.permutation(100), o.permutation(100))
+
+
 def test_error_paths_without_gpu():
     """Argument validation reports the reference's error classes."""
     from paper_2011_09463_b200 import errors
