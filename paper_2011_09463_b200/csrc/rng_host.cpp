@@ -11,6 +11,7 @@
 #include <cstring>
 #include <random>
 #include <string>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -87,16 +88,79 @@ double mtk_rng_uniform(mtk_rng* r, double lo, double hi) { return r->range(lo, h
 double mtk_rng_normal(mtk_rng* r) { return r->gauss(); }
 uint64_t mtk_rng_below(mtk_rng* r, uint64_t n) { return r->bounded(n); }
 
-// rng.hpp:50-63: identity then Fisher-Yates swaps from the top
+// rng.hpp:50-63: identity then Fisher-Yates swaps from the top.  The swap
+// targets depend only on the stream (bounded(n), bounded(n - 1), ...), so
+// they are drawn first, in the same order; the swaps then run with the
+// random targets prefetched a few iterations ahead, on a 32-bit working
+// array when n < 2^32 (the attack sweep permutes 2^20 rows every epoch:
+// the swaps were bound by cache misses).  Same stream use, same result.
 int mtk_rng_permutation(mtk_rng* r, uint64_t n, uint64_t* out) {
     if (!r || (!out && n)) return set_err(MTK_VALUE_ERROR, "mtk_rng_permutation: null argument");
-    for (uint64_t i = 0; i < n; ++i) out[i] = i;
-    for (uint64_t top = n; top > 1; --top) {
-        const uint64_t j = r->bounded(top);
-        const uint64_t t = out[top - 1];
-        out[top - 1] = out[j];
-        out[j] = t;
+    if (n < 2 || n >= (1ull << 32)) {
+        for (uint64_t i = 0; i < n; ++i) out[i] = i;
+        for (uint64_t top = n; top > 1; --top) {
+            const uint64_t j = r->bounded(top);
+            const uint64_t t = out[top - 1];
+            out[top - 1] = out[j];
+            out[j] = t;
+        }
+        return MTK_OK;
     }
+    // working buffers reused across calls (fresh 16 MB per call cost ~6 ms of
+    // page faults); a concurrent caller takes its own
+    static std::mutex mu;
+    static std::vector<uint32_t> js_s, w_s;
+    static std::vector<uint64_t> raw_s;
+    std::unique_lock<std::mutex> lk(mu, std::try_to_lock);
+    std::vector<uint32_t> js_l, w_l;
+    std::vector<uint64_t> raw_l;
+    std::vector<uint32_t>& js = lk.owns_lock() ? js_s : js_l;
+    std::vector<uint32_t>& w = lk.owns_lock() ? w_s : w_l;
+    std::vector<uint64_t>& raw = lk.owns_lock() ? raw_s : raw_l;
+    if (js.size() < n - 1) js.resize(n - 1);
+    if (w.size() < n) w.resize(n);
+    if (raw.size() < n - 1) raw.resize(n - 1);
+    // the targets: raw words drawn in stream order, then the reductions
+    // (two 64-bit divisions each) on all cores.  A rejection (a word >= the
+    // cut: ~top / 2^64) would shift the stream: then the engine is restored
+    // and the targets drawn one by one, as bounded() does.
+    {
+        const std::mt19937_64 saved = r->eng;
+        for (uint64_t k = 0; k + 1 < n; ++k) raw[k] = r->eng();
+        unsigned nt = std::thread::hardware_concurrency();
+        nt = nt == 0 ? 1 : (nt > 16 ? 16 : nt);
+        if (n < (1u << 16)) nt = 1;
+        std::vector<char> rejected(nt, 0);
+        auto part = [&](unsigned t) {
+            const uint64_t a = (n - 1) * t / nt, b = (n - 1) * (t + 1) / nt;
+            for (uint64_t k = a; k < b; ++k) {
+                const uint64_t top = n - k, cut = UINT64_MAX - UINT64_MAX % top;
+                if (raw[k] >= cut) rejected[t] = 1;
+                js[k] = static_cast<uint32_t>(raw[k] % top);
+            }
+        };
+        std::vector<std::thread> th;
+        for (unsigned t = 1; t < nt; ++t) th.emplace_back(part, t);
+        part(0);
+        for (auto& x : th) x.join();
+        bool any = false;
+        for (char c : rejected) any |= c != 0;
+        if (any) {
+            r->eng = saved;
+            for (uint64_t k = 0, top = n; top > 1; --top, ++k) js[k] = static_cast<uint32_t>(r->bounded(top));
+        }
+    }
+    for (uint64_t i = 0; i < n; ++i) w[i] = static_cast<uint32_t>(i);
+    constexpr uint64_t kAhead = 16;
+    const uint64_t steps = n - 1;
+    for (uint64_t k = 0; k < steps; ++k) {
+        if (k + kAhead < steps) __builtin_prefetch(&w[js[k + kAhead]], 1, 0);
+        const uint64_t top = n - k, j = js[k];
+        const uint32_t t = w[top - 1];
+        w[top - 1] = w[j];
+        w[j] = t;
+    }
+    for (uint64_t i = 0; i < n; ++i) out[i] = w[i];
     return MTK_OK;
 }
 
