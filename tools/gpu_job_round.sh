@@ -10,3 +10,5 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 600 ncu --profile-from-start off --set full --clock-control none --import-source on -o gpurun_out/prof_$T -f python tools/profile_workload.py c2 > gpurun_out/ncu_c2_$T.log 2>&1; echo ncu c2 rc $?
 M="--metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none"
 timeout 600 ncu --profile-from-start off $M -o gpurun_out/attack_$T -f python tools/profile_workload.py attack > gpurun_out/ncu_attack_$T.log 2>&1; echo ncu attack rc $?
+timeout 900 python bench.py --workload c3 > gpurun_out/bench_c3_$T.log 2> gpurun_out/bench_c3_$T.err; echo c3 rc $?
+timeout 1200 python bench.py --workload c5 --steps 5 --warmup 1 > gpurun_out/bench_c5_$T.log 2> gpurun_out/bench_c5_$T.err; echo c5 rc $?
