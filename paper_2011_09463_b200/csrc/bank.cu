@@ -248,7 +248,8 @@ struct mtk_bank {
             alloc3(H[l], GB * dims[l]);
             // the mask bits, when both the FWD producing H[l] and the DX reading it are tcgen05 GEMMs
             const char* nb = getenv("MTK_NO_MASK_BITS");  // A/B at bank allocation
-            if (tc[l - 1] && tc[l] && !(nb && nb[0] == '1'))
+            // (and for the last hidden layer: the MMD gradient GEMM's fused head DX reads them)
+            if (tc[l - 1] && (tc[l] || l == L - 1) && !(nb && nb[0] == '1'))
                 MTK_CUDA(cudaMalloc(&H[l].bits, GB * mask_words(dims[l]) * sizeof(uint32_t)));
         }
         for (auto& z : dZ) alloc3(z, GB * maxd());
@@ -683,6 +684,11 @@ void train_step(mtk_bank& k, const mtk_step& s, double* loss_host, double* mmd_h
             a.hd_w_gs = (long long)fi * fo;
             a.hd_out = k.dZ[1].f;
             a.hd_colsum = (hl - 1 >= s.frozen_layers && !no_colsum) ? k.colsum[(hl - 1) % 3] : nullptr;
+            if (k.H[hl].bits) {
+                a.hd_zbits = k.H[hl].bits;
+                a.hd_zbits_ld = mask_words(fi);
+                a.hd_zbits_gs = (long long)B * a.hd_zbits_ld;
+            }
             if (!mmd_head_fusable(a)) a.hd_n = 0;
         }
         if (const char* t = getenv("MTK_MMD_TRACE"))  // diagnostics (tools/mmd_trace.py)

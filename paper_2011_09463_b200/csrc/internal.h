@@ -142,6 +142,7 @@ enum class Epi : int {
     kStore = 4,     // C = acc (diagnostics)
     kNone = 5,      // no output (diagnostics: epilogue without global traffic)
     kMmdGrad = 6,   // C = scale * (add[m,n] * rowvec[m] - acc)   (MMD gradient from V = W.Z)
+    kMmdGradW = 7,  // C = -scale * acc [* ReLU mask bits]         (V' = W'.Z, W' = W - diag(Wsum))
 };
 
 struct Gemm {
@@ -375,6 +376,10 @@ struct MmdArgs {
     int hd_n = 0;                   // <= 32
     float* hd_out = nullptr;
     float* hd_colsum = nullptr;
+    // optional: the ReLU mask of z (= Xs) as bits [G][m+n][hd_zbits_ld] (the FWD
+    // epilogue's); with it the fused head's mask comes from the bits (k_mmd_tc.cu)
+    const uint32_t* hd_zbits = nullptr;
+    long long hd_zbits_gs = 0, hd_zbits_ld = 0;
     int* flags = nullptr;
     bool tc = false;                // run on the tcgen05 path (k_mmd_tc.cu)
     unsigned long long* trace = nullptr;  // diagnostics (k_mmd_tc.cu)

@@ -1181,7 +1181,8 @@ __global__ void __launch_bounds__(WSUM_THREADS) mmd_wsum_kernel(const float* rpa
                                                                 const double* kpart, int G, long long N,
                                                                 int T, int npairs, float* wsum,
                                                                 double* partial, WsumHead h, long long r0,
-                                                                long long NR, int ta, int NT) {
+                                                                long long NR, int ta, int NT, float* wdiag,
+                                                                long long ldw) {
     __shared__ double jsum[3][WSUM_THREADS / 3 + 1];
     const long long nbw = ((long long)G * NR + WSUM_THREADS - 1) / WSUM_THREADS;
     if (blockIdx.x >= nbw + (long long)G * NT) {  // head block B rows: -W_head^T / lambda
@@ -1220,6 +1221,8 @@ __global__ void __launch_bounds__(WSUM_THREADS) mmd_wsum_kernel(const float* rpa
             s += (double)(((src[r] + src[WT + r]) + src[2 * WT + r]) + src[3 * WT + r]);
         }
         wsum[t] = (float)s;
+        // W' = W - diag(Wsum) (wdiag: the single-chunk V GEMM folds z * Wsum in)
+        if (wdiag) wdiag[((long long)g * N + i) * ldw + i] = -(float)s;
         return;
     }
     const int gi = (int)(blockIdx.x - nbw), g = gi / NT, I = ta + gi % NT;
@@ -1359,6 +1362,10 @@ int mmd_tc_blocks_per_group(const MmdArgs& a) {
 // W budget: fixed (not free-memory dependent), so the path -- and with it the
 // rounding -- is the same on every box.  C4 (N = 73,728, one group) needs 21.7 GB.
 constexpr double kWBudget = 48.0 * 1024 * 1024 * 1024;
+static bool getenv_flag(const char* name) {  // A/B switches, read per call
+    const char* e = getenv(name);
+    return e && e[0] == '1';
+}
 static bool w_path(const MmdArgs& a) {
     const char* fe = getenv("MTK_MMD_FUSED");
     const bool fused = fe && fe[0] == '1';
@@ -1572,8 +1579,13 @@ void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s, int stages) 
             h.bx = L.bx;
             nbx = ((long long)a.G * kHeadK * a.d + WSUM_THREADS - 1) / WSUM_THREADS;
         }
+        // single-chunk V GEMM: fold z * Wsum into it as a -Wsum diagonal of W, so
+        // its epilogue needs no z (only the fused head's ReLU mask, as bits)
+        const int nch = v_chunks(a);
+        const bool wdiag = nch == 1 && (!head || a.hd_zbits) && !getenv_flag("MTK_MMD_NO_WDIAG");
         mmd_wsum_kernel<<<(unsigned)(nbw + (long long)a.G * NT + nbx), WSUM_THREADS, 0, s>>>(
-            L.rpart, L.cpart, L.kpart, a.G, N, T, np, L.wsum, a.partial, h, wr.r0, wr.NR, wr.ta, NT);
+            L.rpart, L.cpart, L.kpart, a.G, N, T, np, L.wsum, a.partial, h, wr.r0, wr.NR, wr.ta, NT,
+            wdiag ? L.W : nullptr, L.ldw);
         count_launch();
         // V = W.Z over the owned rows [r0, r0 + NR) (all rows unless sharded)
         const long long r0 = wr.r0, NR = wr.NR;
@@ -1609,7 +1621,19 @@ void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s, int stages) 
         u.rowvec = L.wsum + r0;  // G = 1 when sharded (the epilogue indexes g * M + m)
         u.scale = a.grad_scale;
         u.flags = a.flags;
-        const int nch = v_chunks(a);
+        if (wdiag) {  // g = -scale * (W'.Z)[* mask]: no z, no Wsum in the epilogue
+            u.epi = Epi::kMmdGradW;
+            u.add = nullptr;
+            u.rowvec = nullptr;
+            // the corrections keep their own accumulator at any K: V' is a small
+            // difference of the off-diagonal sum and the diagonal term
+            u.same_sign = 1;
+            if (head) {
+                u.mbits = const_cast<uint32_t*>(a.hd_zbits) + r0 * a.hd_zbits_ld;
+                u.mb_gs = a.hd_zbits_gs;
+                u.mb_ld = a.hd_zbits_ld;
+            }
+        }
         if (nch > 1) {  // kVChunk-deep GEMMs into fp32 partials, then the fp64 finish
             const long long per = NR * a.d;
             for (int c = 0; c < nch; ++c) {

@@ -82,6 +82,7 @@ void dispatch2(const UmmaParams& p, int a_mn, int b_mn, int G, cudaStream_t s) {
         if (e == (int)Epi::kBias) launch_variant<0, 1, PAIR, SEPC, (int)Epi::kBias>(p, G, s);
         else if (e == (int)Epi::kBiasRelu) launch_variant<0, 1, PAIR, SEPC, (int)Epi::kBiasRelu>(p, G, s);
         else if (e == (int)Epi::kMmdGrad) launch_variant<0, 1, PAIR, SEPC, (int)Epi::kMmdGrad>(p, G, s);
+        else if (e == (int)Epi::kMmdGradW) launch_variant<0, 1, PAIR, SEPC, (int)Epi::kMmdGradW>(p, G, s);
         else if (e == (int)Epi::kStore) launch_variant<0, 1, PAIR, SEPC, (int)Epi::kStore>(p, G, s);
         else launch_variant<0, 1, PAIR, SEPC, -1>(p, G, s);
     } else if (!a_mn && !b_mn) {
@@ -156,9 +157,10 @@ void launch_umma(const UmmaGemm& u, cudaStream_t s) {
     p.mbits = u.mbits;
     p.mb_gs = u.mb_gs;
     p.mb_ld = u.mb_ld;
-    if (u.mbits && (u.epi == Epi::kMask || u.epi == Epi::kBiasRelu) && u.mb_ld < (u.N + 31) / 32)
+    const bool bits_epi = u.epi == Epi::kMask || u.epi == Epi::kBiasRelu || u.epi == Epi::kMmdGradW;
+    if (u.mbits && bits_epi && u.mb_ld < (u.N + 31) / 32)
         fail(MTK_ERROR, "umma: mask-bit rows shorter than ceil(N / 32) words");
-    if (u.epi != Epi::kMask && u.epi != Epi::kBiasRelu) p.mbits = nullptr;
+    if (!bits_epi) p.mbits = nullptr;
     if (u.b2) {  // K = [0, ksplit) from b, [ksplit, K) from b2 (same major-ness)
         if (u.ksplit <= 0 || u.ksplit % BK || u.ksplit >= u.K || u.b_mn != 1)
             fail(MTK_ERROR, "umma: split B needs an N-major B and ksplit % 32 == 0 inside K");

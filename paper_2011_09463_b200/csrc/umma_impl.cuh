@@ -100,7 +100,7 @@ struct EpiPlan {
 #else
     static constexpr bool coal = MTK_UMMA_COAL && (EPI == (int)Epi::kBias || EPI == (int)Epi::kBiasRelu ||
                                                    EPI == (int)Epi::kStore || EPI == kEpiMaskNoAdd ||
-                                                   EPI == (int)Epi::kSgd);
+                                                   EPI == (int)Epi::kSgd || EPI == (int)Epi::kMmdGradW);
 #endif
     static constexpr int ls = coal ? 4 : 5;  // load stages
     static constexpr int tile_bytes = coal ? 32 * 32 * 4 : 0;
@@ -283,7 +283,7 @@ __device__ __forceinline__ void epilogue_rows(const UmmaParams& p, uint32_t tmem
                 o2[j] = s2 ? *reinterpret_cast<const float4*>(s2 + 4 * j) : make_float4(0.f, 0.f, 0.f, 0.f);
             }
         }
-        const uint32_t mword = (p.mbits && row_ok && epi == (int)Epi::kMask)
+        const uint32_t mword = (p.mbits && row_ok && (epi == (int)Epi::kMask || epi == (int)Epi::kMmdGradW))
                                    ? p.mbits[(long long)g * p.mb_gs + (long long)m * p.mb_ld + nb / 32]
                                    : 0u;
         if (etr && lane == 0) etr[4 * (c - c0)] = gtime();
@@ -335,6 +335,19 @@ __device__ __forceinline__ void epilogue_rows(const UmmaParams& p, uint32_t tmem
                         x.z = o1[j].z > 0.f ? x.z : 0.f;
                         x.w = o1[j].w > 0.f ? x.w : 0.f;
                     }
+                } else if (epi == (int)Epi::kMmdGradW) {  // -scale * (W'.Z), the mask bits of z
+                    x.x = p.scale * -x.x;
+                    x.y = p.scale * -x.y;
+                    x.z = p.scale * -x.z;
+                    x.w = p.scale * -x.w;
+                    bad |= !(isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w));
+                    if (p.mbits) {
+                        const uint32_t mb = mword >> (4 * j);
+                        x.x = (mb & 1u) ? x.x : 0.f;
+                        x.y = (mb & 2u) ? x.y : 0.f;
+                        x.z = (mb & 4u) ? x.z : 0.f;
+                        x.w = (mb & 8u) ? x.w : 0.f;
+                    }
                 } else if (epi == (int)Epi::kMmdGrad) {  // o1 = z row, rowvec = Wsum
                     const float rv = p.rowvec[(long long)g * p.M + m];
                     x.x = p.scale * fmaf(o1[j].x, rv, -x.x);
@@ -376,6 +389,10 @@ __device__ __forceinline__ void epilogue_rows(const UmmaParams& p, uint32_t tmem
                     } else if (epi == (int)Epi::kMask) {
                         if (p.add) x = p.add[idx] + x;
                         x = (p.mbits ? ((mword >> j) & 1u) != 0 : p.mask[idx] > 0.f) ? x : 0.f;
+                    } else if (epi == (int)Epi::kMmdGradW) {
+                        x = p.scale * -x;
+                        bad |= !isfinite(x);
+                        if (p.mbits && !((mword >> j) & 1u)) x = 0.f;
                     } else if (epi == (int)Epi::kMmdGrad) {
                         const float z = p.add[idx];
                         x = p.scale * fmaf(z, p.rowvec[(long long)g * p.M + m], -x);
@@ -400,7 +417,8 @@ __device__ __forceinline__ void epilogue_rows(const UmmaParams& p, uint32_t tmem
             p.mbits[(long long)g * p.mb_gs + (long long)m * p.mb_ld + nb / 32] = word;
         }
         if (etr && lane == 0) etr[4 * (c - c0) + 2] = gtime();
-        if (p.colsum && (epi == (int)Epi::kMask || epi == (int)Epi::kMmdGrad) && mw < p.M) {
+        if (p.colsum && (epi == (int)Epi::kMask || epi == (int)Epi::kMmdGrad || epi == (int)Epi::kMmdGradW) &&
+            mw < p.M) {
             // per-32-row-block column sums of the stored values (next layer's db)
             const float cs = column_sums_32(v, lane);
             if (nb + lane < p.N) {
@@ -444,7 +462,7 @@ __device__ __forceinline__ float4 epi_operand(const UmmaParams& p, int g, int m,
 template <int EPI>
 __device__ __forceinline__ uint32_t epi_rowword(const UmmaParams& p, int g, int m, int nb) {
     if (m < p.M) {
-        if (epi_kind<EPI>() == (int)Epi::kMask && p.mbits) return p.mbits[(long long)g * p.mb_gs + (long long)m * p.mb_ld + nb / 32];
+        if ((epi_kind<EPI>() == (int)Epi::kMask || EPI == (int)Epi::kMmdGradW) && p.mbits) return p.mbits[(long long)g * p.mb_gs + (long long)m * p.mb_ld + nb / 32];
         if (EPI == (int)Epi::kMmdGrad) return __float_as_uint(p.rowvec[(long long)g * p.M + m]);
     }
     return 0u;
@@ -516,7 +534,7 @@ __device__ __forceinline__ void epilogue_coalesced(const UmmaParams& p, uint32_t
                 bad |= t == 12345.f;
                 continue;
             }
-            if (E == (int)Epi::kMask || E == (int)Epi::kMmdGrad) sts32(roww + 4u * lane, rw);
+            if (E == (int)Epi::kMask || E == (int)Epi::kMmdGrad || E == (int)Epi::kMmdGradW) sts32(roww + 4u * lane, rw);
         }
         __syncwarp();
         // the chunk's operands, issued once the accumulator registers are free,
@@ -536,7 +554,7 @@ __device__ __forceinline__ void epilogue_coalesced(const UmmaParams& p, uint32_t
             const int m = mw + r;
             float4 x = lds128(tile + (uint32_t)(r * 128 + ((gq ^ (r & 7)) * 16)));
             const float4 op = oh[ii];
-            const uint32_t rword = (E == (int)Epi::kMask || E == (int)Epi::kMmdGrad) ? lds32(roww + 4u * r) : 0u;
+            const uint32_t rword = (E == (int)Epi::kMask || E == (int)Epi::kMmdGrad || E == (int)Epi::kMmdGradW) ? lds32(roww + 4u * r) : 0u;
             const bool ok = m < p.M && p.ediag != 2;
             const long long idx = (long long)g * p.c_gs + (long long)m * p.ldc + ncol;
             if (kBiasE) {
@@ -570,6 +588,19 @@ __device__ __forceinline__ void epilogue_coalesced(const UmmaParams& p, uint32_t
                     x.y = mk.y > 0.f ? x.y : 0.f;
                     x.z = mk.z > 0.f ? x.z : 0.f;
                     x.w = mk.w > 0.f ? x.w : 0.f;
+                }
+            } else if (E == (int)Epi::kMmdGradW) {  // -scale * (W'.Z), the mask bits of z
+                x.x = p.scale * -x.x;
+                x.y = p.scale * -x.y;
+                x.z = p.scale * -x.z;
+                x.w = p.scale * -x.w;
+                if (ok) bad |= !(isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w));
+                if (p.mbits) {
+                    const uint32_t mb = rword >> (4 * gq);
+                    x.x = (mb & 1u) ? x.x : 0.f;
+                    x.y = (mb & 2u) ? x.y : 0.f;
+                    x.z = (mb & 4u) ? x.z : 0.f;
+                    x.w = (mb & 8u) ? x.w : 0.f;
                 }
             } else if (E == (int)Epi::kMmdGrad) {
                 const float rv = __uint_as_float(rword);
@@ -611,7 +642,7 @@ __device__ __forceinline__ void epilogue_coalesced(const UmmaParams& p, uint32_t
         }  // halves
         __syncwarp();  // the tile is rewritten by the next chunk
         if (etr && lane == 0) etr[4 * (c - c0) + 2] = gtime();
-        if (p.colsum && (E == (int)Epi::kMask || E == (int)Epi::kMmdGrad) && mw < p.M) {
+        if (p.colsum && (E == (int)Epi::kMask || E == (int)Epi::kMmdGrad || E == (int)Epi::kMmdGradW) && mw < p.M) {
             // per-32-row-block column sums of the stored values (next layer's db)
 #pragma unroll
             for (int o = 8; o <= 16; o <<= 1) {

@@ -20,6 +20,7 @@
 
 #define MTK_UMMA_PART_V(X) \
     MTK_UMMA_LV(X, 0, 1, (int)Epi::kMmdGrad) \
+    MTK_UMMA_LV(X, 0, 1, (int)Epi::kMmdGradW) \
     MTK_UMMA_LV(X, 0, 1, (int)Epi::kStore)
 
 #define MTK_UMMA_PART_D(X) \
