@@ -523,6 +523,27 @@ __device__ __forceinline__ void epilogue_coalesced(const UmmaParams& p, uint32_t
                     for (int j = 0; j < 8; ++j) v[8 * h + j] += w[j];
                 }
             }
+            if (kBiasE) {  // bias (+ ReLU) and the mask bits in the row layout: no shuffles
+                const float4* bp = reinterpret_cast<const float4*>(p.bias + g * p.bias_gs + nb);
+                const int m = mw + lane;
+                uint32_t word = 0;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const float4 b4 = bp[j];  // warp-uniform: broadcast
+                    v[4 * j] += b4.x;
+                    v[4 * j + 1] += b4.y;
+                    v[4 * j + 2] += b4.z;
+                    v[4 * j + 3] += b4.w;
+                }
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    if (m < p.M) bad |= !isfinite(v[j]);
+                    if (E == (int)Epi::kBiasRelu) v[j] = v[j] > 0.f ? v[j] : 0.f;
+                    word |= (v[j] > 0.f ? 1u : 0u) << j;
+                }
+                if (E == (int)Epi::kBiasRelu && p.mbits && m < p.M && p.ediag == 0)
+                    p.mbits[(long long)g * p.mb_gs + (long long)m * p.mb_ld + nb / 32] = word;
+            }
 #pragma unroll
             for (int j = 0; j < 8; ++j)
                 sts128(wrow + (uint32_t)((j ^ (lane & 7)) * 16),
@@ -539,7 +560,6 @@ __device__ __forceinline__ void epilogue_coalesced(const UmmaParams& p, uint32_t
         __syncwarp();
         // the chunk's operands, issued once the accumulator registers are free,
         // in groups of GS passes (8 preloaded float4s spilled at 128 registers)
-        const float4 bias4 = epi_bias<EPI>(p, g, ncol);
         float4 cs = make_float4(0.f, 0.f, 0.f, 0.f);
         constexpr int GS = (E == (int)Epi::kMmdGrad || E == (int)Epi::kMask) ? 2 : 4;  // passes per operand group
 #pragma unroll
@@ -557,18 +577,7 @@ __device__ __forceinline__ void epilogue_coalesced(const UmmaParams& p, uint32_t
             const uint32_t rword = (E == (int)Epi::kMask || E == (int)Epi::kMmdGrad || E == (int)Epi::kMmdGradW) ? lds32(roww + 4u * r) : 0u;
             const bool ok = m < p.M && p.ediag != 2;
             const long long idx = (long long)g * p.c_gs + (long long)m * p.ldc + ncol;
-            if (kBiasE) {
-                x.x += bias4.x;
-                x.y += bias4.y;
-                x.z += bias4.z;
-                x.w += bias4.w;
-                if (ok) bad |= !(isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w));
-                if (E == (int)Epi::kBiasRelu) {
-                    x.x = x.x > 0.f ? x.x : 0.f;
-                    x.y = x.y > 0.f ? x.y : 0.f;
-                    x.z = x.z > 0.f ? x.z : 0.f;
-                    x.w = x.w > 0.f ? x.w : 0.f;
-                }
+            if (kBiasE) {  // applied in the row layout above
             } else if (E == (int)Epi::kMask) {
                 if (kAdd && p.add) {
                     x.x = op.x + x.x;
@@ -625,15 +634,6 @@ __device__ __forceinline__ void epilogue_coalesced(const UmmaParams& p, uint32_t
             }
             if (!ok) x = make_float4(0.f, 0.f, 0.f, 0.f);
             if (E != (int)Epi::kNone && ok) *reinterpret_cast<float4*>(p.C + idx) = x;
-            if (E == (int)Epi::kBiasRelu && p.mbits) {  // this chunk's ReLU mask bits of row r
-                uint32_t nib = ((x.x > 0.f) ? 1u : 0u) | ((x.y > 0.f) ? 2u : 0u) | ((x.z > 0.f) ? 4u : 0u) |
-                               ((x.w > 0.f) ? 8u : 0u);
-                nib <<= 4 * gq;
-                nib |= __shfl_xor_sync(0xffffffffu, nib, 1);
-                nib |= __shfl_xor_sync(0xffffffffu, nib, 2);
-                nib |= __shfl_xor_sync(0xffffffffu, nib, 4);
-                if (ok && gq == 0) p.mbits[(long long)g * p.mb_gs + (long long)m * p.mb_ld + nb / 32] = nib;
-            }
             cs.x += x.x;
             cs.y += x.y;
             cs.z += x.z;

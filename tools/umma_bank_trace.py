@@ -23,7 +23,7 @@ for g in range(G):
 X = torch.randn((G, B, DIMS[0]), device="cuda")
 y = torch.randint(0, 10, (G, B), device="cuda", dtype=torch.int32)
 # (name, M, N, K, epi): kBias 0, kBiasRelu 1, kMask 2, kSgd 3, kStore 4, kMmdGrad 6
-SHAPES = [("fwd0", B, 512, 1024, 1), ("fwd1", B, 256, 512, 1), ("vgemm", B, 256, B + 32, 6),
+SHAPES = [("fwd0", B, 512, 1024, 1), ("fwd1", B, 256, 512, 1), ("vgemm", B, 256, B + 32, 7),
           ("dx1", B, 512, 256, 2), ("dw1", 512, 256, B, 3), ("dw0", 1024, 512, B, 3)]
 for name, M, N, K, e in SHAPES:
     os.environ["MTK_UMMA_TRACE_SHAPE"] = f"{M},{N},{K},{e}"
