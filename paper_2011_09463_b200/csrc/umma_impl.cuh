@@ -494,6 +494,8 @@ __device__ __forceinline__ void epilogue_coalesced(const UmmaParams& p, uint32_t
     constexpr int E = epi_kind<EPI>();  // the arithmetic kind (kEpiMaskNoAdd: kMask without an addend)
     constexpr bool kAdd = EPI != kEpiMaskNoAdd;
     constexpr bool kBiasE = E == (int)Epi::kBias || E == (int)Epi::kBiasRelu;
+    // the mask bits applied in the row layout (no addend to add first)
+    constexpr bool kRowMask = EPI == kEpiMaskNoAdd || E == (int)Epi::kMmdGradW;
     const int mw = m0 + 32 * q;
     const int gq = lane & 7, rsub = lane >> 3;
     const bool aligned = (p.c_gs % 4 == 0) && (p.ldc % 4 == 0);
@@ -544,6 +546,17 @@ __device__ __forceinline__ void epilogue_coalesced(const UmmaParams& p, uint32_t
                 if (E == (int)Epi::kBiasRelu && p.mbits && m < p.M && p.ediag == 0)
                     p.mbits[(long long)g * p.mb_gs + (long long)m * p.mb_ld + nb / 32] = word;
             }
+            if (kRowMask) {  // mask (and scale) in the row layout: the row's word is this thread's
+                const bool mrow = mw + lane < p.M;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    if (E == (int)Epi::kMmdGradW) {
+                        v[j] = p.scale * -v[j];
+                        if (mrow) bad |= !isfinite(v[j]);
+                    }
+                    if (p.mbits && !((rw >> j) & 1u)) v[j] = 0.f;
+                }
+            }
 #pragma unroll
             for (int j = 0; j < 8; ++j)
                 sts128(wrow + (uint32_t)((j ^ (lane & 7)) * 16),
@@ -555,7 +568,7 @@ __device__ __forceinline__ void epilogue_coalesced(const UmmaParams& p, uint32_t
                 bad |= t == 12345.f;
                 continue;
             }
-            if (E == (int)Epi::kMask || E == (int)Epi::kMmdGrad || E == (int)Epi::kMmdGradW) sts32(roww + 4u * lane, rw);
+            if ((E == (int)Epi::kMask || E == (int)Epi::kMmdGrad) && !kRowMask) sts32(roww + 4u * lane, rw);
         }
         __syncwarp();
         // the chunk's operands, issued once the accumulator registers are free,
@@ -574,10 +587,11 @@ __device__ __forceinline__ void epilogue_coalesced(const UmmaParams& p, uint32_t
             const int m = mw + r;
             float4 x = lds128(tile + (uint32_t)(r * 128 + ((gq ^ (r & 7)) * 16)));
             const float4 op = oh[ii];
-            const uint32_t rword = (E == (int)Epi::kMask || E == (int)Epi::kMmdGrad || E == (int)Epi::kMmdGradW) ? lds32(roww + 4u * r) : 0u;
+            const uint32_t rword = ((E == (int)Epi::kMask || E == (int)Epi::kMmdGrad) && !kRowMask) ? lds32(roww + 4u * r) : 0u;
             const bool ok = m < p.M && p.ediag != 2;
             const long long idx = (long long)g * p.c_gs + (long long)m * p.ldc + ncol;
             if (kBiasE) {  // applied in the row layout above
+            } else if (kRowMask) {  // applied in the row layout above
             } else if (E == (int)Epi::kMask) {
                 if (kAdd && p.add) {
                     x.x = op.x + x.x;
@@ -597,19 +611,6 @@ __device__ __forceinline__ void epilogue_coalesced(const UmmaParams& p, uint32_t
                     x.y = mk.y > 0.f ? x.y : 0.f;
                     x.z = mk.z > 0.f ? x.z : 0.f;
                     x.w = mk.w > 0.f ? x.w : 0.f;
-                }
-            } else if (E == (int)Epi::kMmdGradW) {  // -scale * (W'.Z), the mask bits of z
-                x.x = p.scale * -x.x;
-                x.y = p.scale * -x.y;
-                x.z = p.scale * -x.z;
-                x.w = p.scale * -x.w;
-                if (ok) bad |= !(isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w));
-                if (p.mbits) {
-                    const uint32_t mb = rword >> (4 * gq);
-                    x.x = (mb & 1u) ? x.x : 0.f;
-                    x.y = (mb & 2u) ? x.y : 0.f;
-                    x.z = (mb & 4u) ? x.z : 0.f;
-                    x.w = (mb & 8u) ? x.w : 0.f;
                 }
             } else if (E == (int)Epi::kMmdGrad) {
                 const float rv = __uint_as_float(rword);
