@@ -772,8 +772,11 @@ void train_step(mtk_bank& k, const mtk_step& s, double* loss_host, double* mmd_h
             after_launch(c, 1);
         }
         {
-            PhaseScope ph(c, kPhOther, 1);
-            launch_mmd_finish(a, k.mmd, nullptr, c.stream);
+            // the MMD value only feeds the host read-back: side stream (joined
+            // with the step's other side work)
+            if (side) c.fork();
+            PhaseScope ph(c, kPhOther, 1, side ? c.side : nullptr);
+            launch_mmd_finish(a, k.mmd, nullptr, side ? c.side : c.stream);
             after_launch(c, 1);
         }
     }
