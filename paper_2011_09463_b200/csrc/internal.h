@@ -230,6 +230,10 @@ struct UmmaGemm {
     // the operands are of one sign (e.g. MMD V = W.Z, W >= 0, Z = post-ReLU
     // h >= 0): accumulate the 3xTF32 corrections separately whatever K is
     int same_sign = 0;
+    // SEPC: at most this many leading k-blocks' corrections share the main
+    // accumulator while the previous tile's epilogue drains (0: none; the MMD
+    // gradient GEMM, whose result is a small difference)
+    int sepc_share = 6;
     // ReLU mask bits [G][M][mb_ld words], bit j of word w = column 32 w + j:
     // kBiasRelu writes them (output > 0), kMask reads them instead of `mask`
     uint32_t* mbits = nullptr;

@@ -1604,6 +1604,7 @@ void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s, int stages) 
         u.b_gs = a.xs_gs;
         u.epi = Epi::kMmdGrad;
         u.same_sign = 1;  // W >= 0 (and Z >= 0 in bank steps): see k_umma.cu sepc
+        u.sepc_share = 0;  // the gradient is a small difference: corrections separate from k = 0
         u.C = a.gXs + r0 * a.d;
         u.c_gs = a.gs_gs;
         if (head) {  // fused head DX: K gains the head block; the epilogue writes the layer's dZ

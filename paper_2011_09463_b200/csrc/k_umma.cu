@@ -3,6 +3,7 @@
 // pair, correction accumulator, epilogue kind) and launch_umma.
 #include <cuda.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -173,6 +174,17 @@ void launch_umma(const UmmaGemm& u, cudaStream_t s) {
     const int sepc_mode = se ? atoi(se) : -1;
     const bool sepc = sepc_mode >= 0 ? sepc_mode != 0 : (u.K >= kSepcMinK || u.same_sign);
     p.flags = u.flags;
+    // SEPC: the first kf k-blocks' corrections share the main accumulator while
+    // the previous tile's epilogue still reads the corrections' region (~the
+    // epilogue's duration: 6 stages of ~0.9 us; at most a fifth of K, so the
+    // shared part's drift stays that of a small partial sum); MTK_UMMA_SEPC_KF
+    // overrides
+    {
+        const int nk = (u.K + BK - 1) / BK;
+        int kf = std::min(u.sepc_share, nk / 5);  // <= a fifth of the k-blocks
+        if (const char* e = getenv("MTK_UMMA_SEPC_KF")) kf = std::min(atoi(e), nk);
+        p.sepc_kf = std::max(0, kf);
+    }
     if (const char* e = getenv("MTK_UMMA_EPI_DIAG")) p.ediag = atoi(e);
     if (const char* t = getenv("MTK_UMMA_TRACE")) {
         // diagnostics; MTK_UMMA_TRACE_SHAPE="M,N,K,epi" restricts it to matching launches

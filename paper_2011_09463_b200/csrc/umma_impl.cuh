@@ -138,6 +138,7 @@ struct UmmaParams {
     int* flags;
     unsigned long long* trace;  // diagnostics: timestamps of CTA (0,0,0)
     int ediag;                  // diagnostics (MTK_UMMA_EPI_DIAG): 1 = TMEM reads only, 2 = no global traffic
+    int sepc_kf;                // SEPC: k-blocks whose corrections share the main accumulator (see below)
 };
 
 __device__ __forceinline__ unsigned long long gtime() {
@@ -228,6 +229,58 @@ __device__ __forceinline__ void mma_stage(uint32_t tmem, uint32_t tcorr, uint32_
             mma_tf32(tmem, a32, b32, idesc, accm);
         }
     }
+}
+
+// SEPC, separate accumulators from k-block kf on: the corrections into tcorr
+// (the first of them initialising it when corr_first), the main product into
+// tmem (initialising it when main_first: kf = 0)
+template <int A_MN, int B_MN, bool PAIR>
+__device__ __forceinline__ void mma_stage_sep(uint32_t tmem, uint32_t tcorr, uint32_t base, uint32_t lo,
+                                              uint32_t idesc, bool corr_first, bool main_first) {
+    constexpr uint32_t a_lbo = A_MN ? 4096 : 16, b_lbo = B_MN ? 4096 : 16;
+    constexpr uint32_t a_sbo = A_MN ? 512 : 1024, b_sbo = B_MN ? 512 : 1024;
+    constexpr uint32_t a_lay = A_MN ? 1 : 2, b_lay = B_MN ? 1 : 2;
+#pragma unroll
+    for (int kk = 0; kk < BK / 8; ++kk) {
+        const uint32_t aoff = A_MN ? kk * 1024 : kk * 32;
+        const uint32_t boff = B_MN ? kk * 1024 : kk * 32;
+        const uint64_t a32 = smem_desc(base + aoff, a_lbo, a_sbo, a_lay);
+        const uint64_t alo = smem_desc(lo + aoff, a_lbo, a_sbo, a_lay);
+        const uint64_t b32 = smem_desc(base + TILE_BYTES + boff, b_lbo, b_sbo, b_lay);
+        const uint64_t blo = smem_desc(lo + TILE_BYTES + boff, b_lbo, b_sbo, b_lay);
+        const uint32_t accc = (corr_first && kk == 0) ? 0u : 1u;
+        const uint32_t accm = (main_first && kk == 0) ? 0u : 1u;
+        if (PAIR) {
+            mma_tf32_2sm(tcorr, a32, blo, idesc, accc);
+            mma_tf32_2sm(tcorr, alo, b32, idesc, 1u);
+            mma_tf32_2sm(tmem, a32, b32, idesc, accm);
+        } else {
+            mma_tf32(tcorr, a32, blo, idesc, accc);
+            mma_tf32(tcorr, alo, b32, idesc, 1u);
+            mma_tf32(tmem, a32, b32, idesc, accm);
+        }
+    }
+}
+
+// SEPC phase 1 of a tile's epilogue: this warp's chunks of main += corr, in
+// TMEM (the corrections' region is then free for the next tile's main)
+__device__ __forceinline__ void sepc_fold(uint32_t tmain, uint32_t tcorr, int q, int c0, int c1, int n0, int N) {
+#pragma unroll 1
+    for (int c = c0; c < c1; ++c) {
+        if (n0 + c * 32 >= N) break;  // warp-uniform
+        const uint32_t lq = (uint32_t)(32 * q) << 16;
+        float v[32];
+        tmem_ld_32x32(tmain + lq + (uint32_t)(c * 32), v);
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            float w[8];
+            tmem_ld_32x8(tcorr + lq + (uint32_t)(c * 32 + 8 * h), w);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[8 * h + j] += w[j];
+        }
+        tmem_st_32x32(tmain + lq + (uint32_t)(c * 32), v);
+    }
+    tmem_st_wait();
 }
 
 // 32 column values per lane (lane = row) -> lane j holds the sum over the
@@ -792,21 +845,35 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_kernel(const __grid_const
             uint32_t it = 0, tl = 0;
             for (int w = cid; w < nitems; w += ncl, ++tl) {
                 const uint32_t idesc = w < p.nfull ? idesc_full : idesc_half;
-                // SEPC: every tile takes both buffers (main, corrections)
-                const uint32_t b = SEPC ? 0u : (tl & 1);
-                const uint32_t ph = SEPC ? (tl & 1) : ((tl >> 1) & 1);
-                mbar_wait(&acc_empty[b], ph ^ 1);
-                tc_fence_after();
+                // Non-SEPC: double-buffered accumulator (region b = tile parity,
+                // freed every second tile).  SEPC: tile t's main accumulator is
+                // region t & 1, its corrections region (t & 1) ^ 1; each region is
+                // freed once per tile (the corrections' after the epilogue folds
+                // them into main, main after the epilogue proper), so tile t
+                // waits for t completions of each.  The first kf k-blocks'
+                // corrections go into main (the corrections' region is still being
+                // read by the previous tile's epilogue); their accumulation drift
+                // is that of a small partial sum.
+                const uint32_t b = tl & 1;
                 const uint32_t acc = tmem + b * TN;
-                const uint32_t corr = SEPC ? tmem + TN : acc;
+                const uint32_t corr = tmem + (b ^ 1) * TN;
+                const int kf = p.sepc_kf;
+                mbar_wait(&acc_empty[b], SEPC ? ((tl + 1) & 1) : (((tl >> 1) & 1) ^ 1));
+                tc_fence_after();
                 for (int kb = 0; kb < nk; ++kb, ++it) {
                     const int s = it % LS, l = it % LO;
                     mbar_wait(&conv[l], (it / LO) & 1);
+                    if (SEPC && kb == kf) mbar_wait(&acc_empty[b ^ 1], (tl + 1) & 1);  // corrections' region free
                     tc_fence_after();
                     if (lane == 0) {
                         if (tr && it < 1000) tr[1000 + it] = gtime();
-                        mma_stage<A_MN, B_MN, PAIR>(acc, corr, smem_u32(smem + s * LOAD_BYTES),
-                                                    smem_u32(lo_ring + l * LO_BYTES), idesc, kb == 0);
+                        if (!SEPC || kb < kf)
+                            mma_stage<A_MN, B_MN, PAIR>(acc, acc, smem_u32(smem + s * LOAD_BYTES),
+                                                        smem_u32(lo_ring + l * LO_BYTES), idesc, kb == 0);
+                        else
+                            mma_stage_sep<A_MN, B_MN, PAIR>(acc, corr, smem_u32(smem + s * LOAD_BYTES),
+                                                            smem_u32(lo_ring + l * LO_BYTES), idesc, kb == kf,
+                                                            kb == 0);
                         if (PAIR) {  // frees the slots in both CTAs
                             mma_commit_2sm(&empty[s], 0x3);
                             mma_commit_2sm(&lofree[l], 0x3);
@@ -835,21 +902,29 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_kernel(const __grid_const
             const int m0 = PAIR ? im.mt * 256 + (int)rank * 128 : im.mt * 128;
             const int ncols = im.half < 0 ? TN : TN / 2;
             const int n0 = im.nt * TN + (im.half > 0 ? TN / 2 : 0);
-            const uint32_t b = SEPC ? 0u : (tl & 1);
+            const uint32_t b = tl & 1;
             const int nch = ncols / 32;
-            mbar_wait(&acc_full[b], SEPC ? (tl & 1) : ((tl >> 1) & 1));
+            const int ec0 = hsel * (nch / 2), ec1 = (hsel + 1) * (nch / 2);
+            mbar_wait(&acc_full[b], (tl >> 1) & 1);
             if (tr && threadIdx.x == 64 && tl < 16) tr[2000 + 2 * tl] = gtime();
             tc_fence_after();
+            if (SEPC) {  // phase 1: fold the corrections into main, free their region
+                if (p.sepc_kf < nk) sepc_fold(tmem + b * TN, tmem + (b ^ 1) * TN, q, ec0, ec1, n0, p.N);
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if (PAIR) mbar_arrive_remote(&acc_empty[b ^ 1], 0);
+                    else mbar_arrive(&acc_empty[b ^ 1]);
+                }
+            }
             if constexpr (EpiPlan<EPI>::coal)
-                epilogue_coalesced<SEPC, EPI>(p, tmem + b * TN, tmem + TN, q, lane, g, m0, n0, hsel * (nch / 2),
-                                              (hsel + 1) * (nch / 2),
-                                              smem_u32(epi_tiles + (warp - EPI_W0) * EPI_TILE_BYTES),
-                                              smem_u32(epi_rowws + (warp - EPI_W0) * EPI_ROWW_BYTES),
-                                              (tr && threadIdx.x == 64 && tl < 4) ? tr + 2100 + 32 * tl : nullptr);
+                epilogue_coalesced<false, EPI>(p, tmem + b * TN, 0u, q, lane, g, m0, n0, ec0, ec1,
+                                               smem_u32(epi_tiles + (warp - EPI_W0) * EPI_TILE_BYTES),
+                                               smem_u32(epi_rowws + (warp - EPI_W0) * EPI_ROWW_BYTES),
+                                               (tr && threadIdx.x == 64 && tl < 4) ? tr + 2100 + 32 * tl : nullptr);
             else
-                epilogue_rows<SEPC, EPI>(p, tmem + b * TN, tmem + TN, q, lane, g, m0, n0, hsel * (nch / 2),
-                                         (hsel + 1) * (nch / 2),
-                                         (tr && threadIdx.x == 64 && tl < 4) ? tr + 2100 + 32 * tl : nullptr);
+                epilogue_rows<false, EPI>(p, tmem + b * TN, 0u, q, lane, g, m0, n0, ec0, ec1,
+                                          (tr && threadIdx.x == 64 && tl < 4) ? tr + 2100 + 32 * tl : nullptr);
             tc_fence_before();
             __syncwarp();
             if (tr && threadIdx.x == 64 && tl < 16) tr[2001 + 2 * tl] = gtime();
