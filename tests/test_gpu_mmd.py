@@ -247,6 +247,7 @@ def test_mmd_c4_materialised_w_path_vs_fp64(ctx, monkeypatch):
     ob = float((2.0 * N * (Zd * Zd).sum() - 2.0 * (Zd.sum(0) ** 2).sum()) / (N * N - N))
     assert abs(beta - ob) <= 1e-9 * ob
     assert abs(v - ref_v) <= TOL * abs(ref_v), (v, ref_v)
+    print(f"C4 W path: value {abs(v - ref_v) / abs(ref_v):.2e}, gradient rows {rel(Gw, ref_g):.2e} (bound {TOL})")
     assert rel(Gw, ref_g) <= TOL, rel(Gw, ref_g)
     for r, i in enumerate(rows):  # row by row too (each row's own scale)
         assert rel(Gw[r], ref_g[r]) <= 2 * TOL, (i, rel(Gw[r], ref_g[r]))
