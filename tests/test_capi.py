@@ -99,6 +99,19 @@ def test_parallel_synth_matches_sequential_stream(pre):
     assert np.array_equal(r.permutation(100), o.permutation(100))
 
 
+def test_parallel_permutation_matches_sequential_stream():
+    """mtk_rng_permutation draws the Fisher-Yates targets first and reduces
+    them on all host cores past 2^16 elements: bit-identical to the oracle's
+    sequential restatement, and the stream continues identically."""
+    from paper_2011_09463_b200 import api
+
+    r, o = api.Rng(77), po.Rng(77)
+    for n in (3, 70_000, 1 << 17, 1 << 16):
+        assert np.array_equal(r.permutation(n), o.permutation(n)), n
+    assert r.normal() == o.normal()
+    assert np.array_equal(r.permutation(1000), o.permutation(1000))
+
+
 def test_error_paths_without_gpu():
     """Argument validation reports the reference's error classes."""
     from paper_2011_09463_b200 import errors
