@@ -310,6 +310,7 @@ struct SmallEpoch {
     const double* denom;       // [nsteps] device
     float lr;
     int* flags;
+    unsigned long long* trace = nullptr;  // diagnostics (MTK_EPOCH_TRACE): phase stamps of CTA 0
 };
 bool small2_epoch_ok(int K, int H, int O, int B);
 void launch_small2_epoch(const SmallEpoch& p, cudaStream_t s);

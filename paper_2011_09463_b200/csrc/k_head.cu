@@ -11,6 +11,7 @@
 #include <cooperative_groups.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <utility>
 
 #include "internal.h"
@@ -510,20 +511,68 @@ __global__ void __launch_bounds__(E_THREADS, 1) small2_epoch_kernel(SmallEpoch p
         prm[e] = v;
     }
     const float* rpart[4];  // the cluster's partial arrays (row set c in CTA c)
-    for (int c = 0; c < 4; ++c) rpart[c] = c < nsets ? cluster.map_shared_rank(&part[0][0], c) : nullptr;
+    float* rprm[4];         // the cluster's parameter copies
+    for (int c = 0; c < 4; ++c) {
+        rpart[c] = c < nsets ? cluster.map_shared_rank(&part[0][0], c) : nullptr;
+        rprm[c] = c < nsets ? cluster.map_shared_rank(&prm[0], c) : nullptr;
+    }
+    const int per = (E_NP + nsets - 1) / nsets;  // this CTA's parameter slice
+    const int pe0 = rs * per, pe1 = min(E_NP, pe0 + per);
     __syncthreads();
     const float* W0 = prm;
     const float* B0 = W0 + E_K * E_H;
     const float* W1 = B0 + E_H;
     const float* B1 = W1 + E_H * E_O;
     bool bad = false;
+    unsigned long long* tr = (p.trace && blockIdx.x == 0 && t == 0) ? p.trace : nullptr;
+    auto stamp = [&](int s, int k) {
+        if (tr && s < 8) {
+            unsigned long long v;
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
+            tr[s * 8 + k] = v;
+        }
+    };
+    // this thread's row of step s (index, features, label, weight): loaded one
+    // step ahead (they do not depend on the parameters)
+    const int r = rs * E_THREADS + t;
+    struct RowIn {
+        int status;  // 0 no row, 1 row, 2 bad index
+        int lab;
+        float x[E_K];
+        float w;
+    };
+    auto load_row = [&](int s2) {
+        RowIn in;
+        in.status = 0;
+        in.lab = 0;
+        in.w = 1.f;
+#pragma unroll
+        for (int k = 0; k < E_K; ++k) in.x[k] = 0.f;
+        if (s2 < p.nsteps && r < p.B) {
+            const long long q = ((long long)s2 * p.G + g) * p.B + r;
+            const long long row = p.idx[q];
+            if (row < 0 || row >= p.pool_rows) {
+                in.status = 2;
+            } else {
+                in.status = 1;
+                in.lab = p.y[row];
+#pragma unroll
+                for (int k = 0; k < E_K; ++k) in.x[k] = p.X[row * E_K + k];
+                if (p.w) in.w = p.w[q];
+            }
+        }
+        return in;
+    };
+    RowIn nxt = load_row(0);
     for (int s = 0; s < p.nsteps; ++s) {
+        stamp(s, 0);
+        const RowIn cur = nxt;
+        nxt = load_row(s + 1);
         float acc[E_NG];
 #pragma unroll
         for (int q = 0; q < E_NG; ++q) acc[q] = 0.f;
         const float inv = (float)(1.0 / p.denom[s]);
         {
-            const int r = rs * E_THREADS + t;
             float x[E_K], hv[E_H], dh[E_H], dlog[E_O];
 #pragma unroll
             for (int k = 0; k < E_K; ++k) x[k] = 0.f;
@@ -531,15 +580,13 @@ __global__ void __launch_bounds__(E_THREADS, 1) small2_epoch_kernel(SmallEpoch p
             for (int h = 0; h < E_H; ++h) hv[h] = 0.f;
 #pragma unroll
             for (int j = 0; j < E_O; ++j) dlog[j] = 0.f;
-            if (r < p.B) {
-                const long long q = ((long long)s * p.G + g) * p.B + r;
-                const long long row = p.idx[q];
-                if (row < 0 || row >= p.pool_rows) {
+            if (cur.status != 0) {
+                if (cur.status == 2) {
                     atomicOr(p.flags, kFlagBadIndex);
                 } else {
-                    const int lab = p.y[row];
+                    const int lab = cur.lab;
 #pragma unroll
-                    for (int k = 0; k < E_K; ++k) x[k] = p.X[row * E_K + k];
+                    for (int k = 0; k < E_K; ++k) x[k] = cur.x[k];
                     // forward (small2_forward_kernel's order)
 #pragma unroll
                     for (int h = 0; h < E_H; ++h) {
@@ -569,13 +616,14 @@ __global__ void __launch_bounds__(E_THREADS, 1) small2_epoch_kernel(SmallEpoch p
 #pragma unroll
                         for (int j = 0; j < E_O; ++j) z += expf(o[j] - mx);
                         const float lse = mx + logf(z);
-                        const float wi = (p.w ? p.w[q] : 1.f) * inv;
+                        const float wi = cur.w * inv;
 #pragma unroll
                         for (int j = 0; j < E_O; ++j)
                             dlog[j] = wi * (expf(o[j] - lse) - (j == lab ? 1.f : 0.f));
                     }
                 }
             }
+            stamp(s, 1);
             // backward through the ReLU (head_dx order: j ascending from 0)
 #pragma unroll
             for (int h = 0; h < E_H; ++h) {
@@ -584,25 +632,42 @@ __global__ void __launch_bounds__(E_THREADS, 1) small2_epoch_kernel(SmallEpoch p
                 for (int j = 0; j < E_O; ++j) a = fmaf(dlog[j], W1[h * E_O + j], a);
                 dh[h] = hv[h] > 0.f ? a : 0.f;
             }
+            stamp(s, 2);
             epoch_reduce_all(acc, lane, x, hv, dh, dlog, std::make_integer_sequence<int, E_NG>{});
+            stamp(s, 3);
         }
 #pragma unroll
         for (int q = 0; q < E_NG; ++q) part[warp][q * 32 + lane] = acc[q];
         cluster.sync();  // every row set's partials written
-        // per warp the row sets in order, then the warps in ascending order, then SGD
-        for (int e = t; e < E_NP; e += E_THREADS) {
+        stamp(s, 4);
+        // per warp the row sets in order, then the warps in ascending order, then
+        // SGD; CTA c owns a slice of the parameters (one per thread, its
+        // 8 x nsets partial loads in flight together) and writes the update
+        // into every CTA's copy
+        for (int e = pe0 + t; e < pe1; e += E_THREADS) {
+            float v[E_THREADS / 32][4];
+#pragma unroll
+            for (int w2 = 0; w2 < E_THREADS / 32; ++w2)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) v[w2][c] = c < nsets ? rpart[c][w2 * E_NG * 32 + e] : 0.f;
             float gsum = 0.f;
 #pragma unroll
             for (int w2 = 0; w2 < E_THREADS / 32; ++w2) {
-                float a = rpart[0][w2 * E_NG * 32 + e];
-                for (int c = 1; c < nsets; ++c) a += rpart[c][w2 * E_NG * 32 + e];
+                float a = v[w2][0];
+#pragma unroll
+                for (int c = 1; c < 4; ++c)
+                    if (c < nsets) a += v[w2][c];
                 gsum += a;
             }
             const float nv = sgd_update(prm[e], gsum, p.lr);
             bad |= !isfinite(nv);
-            prm[e] = nv;
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                if (c < nsets) rprm[c][e] = nv;
         }
+        stamp(s, 5);
         cluster.sync();  // partials read everywhere (the next step rewrites them); prm updated
+        stamp(s, 6);
     }
     if (bad) atomicOr(p.flags, kFlagNonFinite);
     if (rs == 0)
@@ -621,6 +686,8 @@ void launch_small2_epoch(const SmallEpoch& p, cudaStream_t s) {
     if (!small2_epoch_ok(E_K, E_H, E_O, p.B)) fail(MTK_ERROR, "small2_epoch: unsupported shape");
     if (p.nsteps <= 0 || p.G <= 0) return;
     const int nsets = (p.B + E_THREADS - 1) / E_THREADS;  // <= 4: the cluster size
+    SmallEpoch q = p;
+    if (const char* t = getenv("MTK_EPOCH_TRACE")) q.trace = reinterpret_cast<unsigned long long*>(strtoull(t, nullptr, 0));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)(p.G * nsets));
     cfg.blockDim = dim3(E_THREADS);
@@ -632,7 +699,7 @@ void launch_small2_epoch(const SmallEpoch& p, cudaStream_t s) {
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    MTK_CUDA(cudaLaunchKernelEx(&cfg, small2_epoch_kernel, p));
+    MTK_CUDA(cudaLaunchKernelEx(&cfg, small2_epoch_kernel, q));
     count_launch();
 }
 
