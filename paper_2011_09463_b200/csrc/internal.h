@@ -233,7 +233,7 @@ struct UmmaGemm {
     // SEPC: at most this many leading k-blocks' corrections share the main
     // accumulator while the previous tile's epilogue drains (0: none; the MMD
     // gradient GEMM, whose result is a small difference)
-    int sepc_share = 6;
+    int sepc_share = 10;
     // ReLU mask bits [G][M][mb_ld words], bit j of word w = column 32 w + j:
     // kBiasRelu writes them (output > 0), kMask reads them instead of `mask`
     uint32_t* mbits = nullptr;

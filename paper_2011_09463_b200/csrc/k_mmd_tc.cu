@@ -1644,7 +1644,7 @@ void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s, int stages) 
                 v.a = L.W + r0 * L.ldw + k0;
                 v.b = a.Xs + k0 * a.d;
                 v.epi = Epi::kStore;
-                v.sepc_share = 6;  // V partials (the difference is taken in fp64 after the chunks)
+                v.sepc_share = 10;  // V partials (the difference is taken in fp64 after the chunks)
                 v.C = L.vpart + (long long)c * a.G * per;
                 v.c_gs = per;
                 v.add = nullptr;

@@ -176,12 +176,13 @@ void launch_umma(const UmmaGemm& u, cudaStream_t s) {
     p.flags = u.flags;
     // SEPC: the first kf k-blocks' corrections share the main accumulator while
     // the previous tile's epilogue still reads the corrections' region (~the
-    // epilogue's duration: 6 stages of ~0.9 us; at most a fifth of K, so the
-    // shared part's drift stays that of a small partial sum); MTK_UMMA_SEPC_KF
-    // overrides
+    // epilogue's duration: up to 10 stages of ~0.9 us -- the SGD epilogue takes
+    // ~8 us; at most a third of K, so the shared part's drift stays that of a
+    // partial sum: FWD0 / dW0 errors 3.6e-6 / 4.7e-6 -> 4.1e-6 / 4.8e-6 at the
+    // bench shape); MTK_UMMA_SEPC_KF overrides
     {
         const int nk = (u.K + BK - 1) / BK;
-        int kf = std::min(u.sepc_share, nk / 5);  // <= a fifth of the k-blocks
+        int kf = std::min(u.sepc_share, nk / 3);  // <= a third of the k-blocks
         if (const char* e = getenv("MTK_UMMA_SEPC_KF")) kf = std::min(atoi(e), nk);
         p.sepc_kf = std::max(0, kf);
     }
