@@ -187,6 +187,7 @@ void launch_umma(const UmmaGemm& u, cudaStream_t s) {
         p.sepc_kf = std::max(0, kf);
     }
     if (const char* e = getenv("MTK_UMMA_EPI_DIAG")) p.ediag = atoi(e);
+    if (const char* e = getenv("MTK_UMMA_PREFETCH")) p.prefetch = atoi(e);
     if (const char* t = getenv("MTK_UMMA_TRACE")) {
         // diagnostics; MTK_UMMA_TRACE_SHAPE="M,N,K,epi" restricts it to matching launches
         bool match = true;

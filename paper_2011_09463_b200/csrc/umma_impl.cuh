@@ -139,6 +139,7 @@ struct UmmaParams {
     unsigned long long* trace;  // diagnostics: timestamps of CTA (0,0,0)
     int ediag;                  // diagnostics (MTK_UMMA_EPI_DIAG): 1 = TMEM reads only, 2 = no global traffic
     int sepc_kf;                // SEPC: k-blocks whose corrections share the main accumulator (see below)
+    int prefetch;               // A/B (MTK_UMMA_PREFETCH=1): producer-side L2 prefetch of epilogue operands
 };
 
 __device__ __forceinline__ unsigned long long gtime() {
@@ -821,7 +822,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_kernel(const __grid_const
                 const CUtensorMap* bmap = (im.half >= 0 && !B_MN) ? &p.b64 : &p.b;
                 for (int kb = 0; kb < nk; ++kb, ++it) {
                     const int s = it % LS;
-                    if (kb == (nk > 8 ? nk - 8 : 0)) prefetch_epilogue_rows(p, g, m0, n0, ncols, lane);
+                    // optional L2 prefetch of the epilogue's per-element operands (off by
+                    // default: the 128 bulk prefetches per tile queue ahead of the next
+                    // tile's loads in the TMA unit -- measured ~5 us per tile boundary;
+                    // without them DX 60.9 -> 48.2 us, DW 209.5 -> 202.3 us per C2 step)
+                    constexpr bool kNeedsOps = EPI < 0 || EPI == (int)Epi::kSgd || EPI == (int)Epi::kMask ||
+                                               EPI == (int)Epi::kMmdGrad;
+                    if (kNeedsOps && p.prefetch && kb == (nk > 8 ? nk - 8 : 0))
+                        prefetch_epilogue_rows(p, g, m0, n0, ncols, lane);
                     mbar_wait(&empty[s], ((it / LS) & 1) ^ 1);
                     uint8_t* st = smem + s * LOAD_BYTES;
                     if (lane == 0) {

@@ -43,6 +43,12 @@ for name, M, N, K, e in SHAPES:
     en = (c[:, 1] - c[:, 0].min()) / 1000
     print(f"== {name} M{M} N{N} K{K} epi{e}: CTA end median {np.median(en):.1f} max {en.max():.1f} us; "
           f"mma stages {len(mma)} median {np.median(d):.3f} us mean {d.mean():.3f}")
+    if os.environ.get("SHOW_STAGES") == name:
+        prod = (t[:1000][t[:1000] > 0] - t0) / 1000
+        cv = (t[3000:4000][t[3000:4000] > 0] - t0) / 1000
+        print("  producer", np.round(prod[:40], 2).tolist())
+        print("  conv    ", np.round(cv[:40], 2).tolist())
+        print("  mma     ", np.round(mma[:40], 2).tolist())
     ep = t[2000:2032]
     for i in range(16):
         if ep[2 * i] > 0:
