@@ -723,7 +723,7 @@ __device__ __forceinline__ float ex2_approx(float x) {
 }
 
 struct MmdWParams {
-    CUtensorMap zk_hi, zk_lo;  // K-major (d, N, G), 64-row boxes
+    CUtensorMap zk_hi, zk_lo;  // K-major (d, N, G), 128-row boxes
     const float* norms;        // [G][N]
     const double* beta;        // [G]
     long long m, n;
@@ -865,14 +865,10 @@ __global__ void __launch_bounds__(W_THREADS, 1) mmd_w_kernel(const __grid_consta
                     uint8_t* b = smem + s * W_STAGE_BYTES;
                     const int k0 = kc * KC;
                     mbar_expect_tx(&full[s], W_STAGE_BYTES);
-                    tma_load_3d(b, &p.zk_hi, &full[s], k0, i0, g);
-                    tma_load_3d(b + 8192, &p.zk_hi, &full[s], k0, i0 + 64, g);
+                    tma_load_3d(b, &p.zk_hi, &full[s], k0, i0, g);  // 128-row boxes (16 KB each)
                     tma_load_3d(b + 16384, &p.zk_lo, &full[s], k0, i0, g);
-                    tma_load_3d(b + 24576, &p.zk_lo, &full[s], k0, i0 + 64, g);
                     tma_load_3d(b + 32768, &p.zk_lo, &full[s], k0, j0, g);
-                    tma_load_3d(b + 40960, &p.zk_lo, &full[s], k0, j0 + 64, g);
                     tma_load_3d(b + 49152, &p.zk_hi, &full[s], k0, j0, g);
-                    tma_load_3d(b + 57344, &p.zk_hi, &full[s], k0, j0 + 64, g);
                 }
                 __syncwarp();
             }
@@ -1505,8 +1501,8 @@ void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s, int stages) 
         const int T = (int)((N + WT - 1) / WT), np = T * (T + 1) / 2;
         MmdWParams w;
         std::memset(&w, 0, sizeof(w));
-        w.zk_hi = zmap(zhi, a.d, N, a.G, zgs, 64, false);
-        w.zk_lo = zmap(zlo, a.d, N, a.G, zgs, 64, false);
+        w.zk_hi = zmap(zhi, a.d, N, a.G, zgs, WT, false);  // whole 128-row tiles: 4 TMA ops per stage
+        w.zk_lo = zmap(zlo, a.d, N, a.G, zgs, WT, false);
         w.norms = norms;
         w.beta = a.beta;
         w.m = a.m;
