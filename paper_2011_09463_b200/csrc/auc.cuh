@@ -126,7 +126,23 @@ struct Work {
     unsigned long long* fhist;  // [2^kFastBits] (queries << 32 | non-members) per key; zero on entry and exit
     unsigned long long* fpart;  // [blocks][3] per-block (non-members, members, U2) of auc_fast_scan_kernel
     unsigned int* done;         // blocks finished in auc_fast_scan_kernel; zero on entry and exit
+    unsigned long long* mail;   // mapped host mailbox (or null): [0..2] counters, [8..9] key range
+                                // words, [10] 1 = U2 complete, [15] sequence number (written last)
+    unsigned long long seq;
 };
+
+// the counters (and whether U2 is complete) to the host mailbox, then the
+// sequence number (one thread; after the counters are final)
+__device__ __forceinline__ void post_mail(const Work& w, bool complete) {
+    if (!w.mail) return;
+    __threadfence();
+    for (int i = 0; i < 3; ++i) w.mail[i] = __ldcg(w.cnt + i);
+    w.mail[8] = __ldcg(w.cnt + 8);
+    w.mail[9] = __ldcg(w.cnt + 9);
+    w.mail[10] = complete ? 1ull : 0ull;
+    __threadfence_system();
+    w.mail[15] = w.seq;
+}
 
 // the full-resolution path applies (the key range is known once the scores are)
 __device__ __forceinline__ bool fast_path(const Work& w) {
@@ -223,6 +239,8 @@ __global__ void __launch_bounds__(kFastScanThreads) auc_fast_scan_kernel(Work w)
     __shared__ unsigned long long shl[32];
     __shared__ bool last;
     const uint32_t kmin = ~w.mm[1], kmax = w.mm[0];
+    if (blockIdx.x == 0 && threadIdx.x == 0 && ((w.win_on && w.mm[2]) || !fast_path(w)))
+        post_mail(w, false);  // the host continues (re-binning / the general path)
     if (w.win_on && w.mm[2]) {  // a key fell outside the window: clear the in-window bins written
         const uint32_t top = w.win_lo + ((1u << kFastBits) - 1u);
         const long long lo = (long long)(max(kmin, w.win_lo) - w.win_lo);
@@ -317,6 +335,7 @@ __global__ void __launch_bounds__(kFastScanThreads) auc_fast_scan_kernel(Work w)
         if (threadIdx.x == 0) {
             atomicAdd(&w.cnt[2], t);
             *w.done = 0;
+            post_mail(w, true);
         }
     }
 }

@@ -227,6 +227,7 @@ int mtk_ctx_destroy(mtk_ctx* c) {
         cudaFree(c->d_scratch);
         cudaFree(c->d_big);
         cudaFree(c->d_auc_l2);
+        if (c->auc_mail) cudaFreeHost(c->auc_mail);
         if (c->pinned) cudaFreeHost(c->pinned);
         if (c->pinned_flags) cudaFreeHost(c->pinned_flags);
         if (c->own_stream) cudaStreamDestroy(c->stream);

@@ -64,6 +64,12 @@ struct Ctx {
     // and left zeroed by every call
     uint32_t* auc_l2(size_t bytes);
     uint32_t* d_auc_l2 = nullptr;
+    // AUC mailbox: mapped pinned host memory the last AUC kernel writes its
+    // counters to, then a sequence number; the host spins on it instead of a
+    // D2H copy + stream synchronize (k_attack.cu)
+    unsigned long long* auc_mail = nullptr;      // host view, 16 words
+    unsigned long long* auc_mail_dev = nullptr;  // device view
+    unsigned long long auc_seq = 0;
     bool auc_fast_hint = true;        // the previous AUC took the full-resolution path (k_attack.cu)
     bool auc_win_valid = false;       // speculative full-resolution window from the previous call's keys
     uint32_t auc_win_lo = 0;

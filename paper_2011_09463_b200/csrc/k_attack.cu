@@ -6,6 +6,8 @@
 // oracle.c (orc_posterior_features, orc_auc).  These are streaming,
 // HBM-bound kernels: one thread per query row, coalesced row-major output.
 #include <algorithm>
+#include <atomic>
+#include <cstring>
 #include <cmath>
 #include <mutex>
 
@@ -377,6 +379,17 @@ auc::Work auc_work(Ctx& ctx, long long n) {
     // the speculative window: the previous call's key range (auc_finish)
     w.win_on = ctx.auc_win_valid ? 1 : 0;
     w.win_lo = ctx.auc_win_lo;
+    if (!ctx.auc_mail) {
+        void* hp = nullptr;
+        MTK_CUDA(cudaHostAlloc(&hp, 16 * sizeof(unsigned long long), cudaHostAllocMapped));
+        std::memset(hp, 0, 16 * sizeof(unsigned long long));
+        ctx.auc_mail = static_cast<unsigned long long*>(hp);
+        void* dp = nullptr;
+        MTK_CUDA(cudaHostGetDevicePointer(&dp, hp, 0));
+        ctx.auc_mail_dev = static_cast<unsigned long long*>(dp);
+    }
+    w.mail = ctx.auc_mail_dev;
+    w.seq = ++ctx.auc_seq;
     w.hist = reinterpret_cast<uint32_t*>(ar + fb + 512);
     w.l2 = reinterpret_cast<uint32_t*>(ar + fb + 512 + al(hb));
     return w;
@@ -412,15 +425,35 @@ void auc_finish(Ctx& ctx, auc::Work& w, const uint8_t* labels, long long n, doub
         MTK_CUDA(cudaMemcpyAsync(h, w.cnt, 10 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));  // counters, mm[0..2]
         MTK_CUDA(cudaStreamSynchronize(s));
     };
+    // the first read-back of a call: spin on the mailbox the fast scan kernel
+    // posts (counters + sequence number) once it is done, polling the stream
+    // now and then so an error or a missing post falls back to the copy +
+    // synchronize (either way the scan has finished when this returns)
+    auto mailbox = [&](unsigned long long* h) {
+        volatile unsigned long long* m = ctx.auc_mail;
+        for (unsigned spins = 1;; ++spins) {
+            if (m[15] == w.seq) {
+                std::atomic_thread_fence(std::memory_order_acquire);
+                for (int i = 0; i < 10; ++i) h[i] = m[i];
+                return;
+            }
+            if ((spins & 1023) == 0 && cudaStreamQuery(s) != cudaErrorNotReady) {
+                if (m[15] == w.seq) continue;  // posted just now
+                readback(h);                   // (raises a pending error)
+                return;
+            }
+        }
+    };
     unsigned long long* h = static_cast<unsigned long long*>(ctx.pinned_buf(128));
     const uint32_t* mm = reinterpret_cast<const uint32_t*>(h + 8);
     bool spec_ok = false;
     if (w.win_on) {  // the keys were binned speculatively in the window
         auc::auc_fast_scan_kernel<<<auc_fast_blocks(ctx), auc::kFastScanThreads, 0, s>>>(w);
         count_launch();
-        readback(h);
+        mailbox(h);
         spec_ok = mm[2] == 0;
         w.win_on = 0;  // a re-run bins from the keys
+        w.mail = nullptr;
     }
     if (!spec_ok) {
         auc::auc_hist_kernel<<<hist_grid, 256, 0, s>>>(w, labels, n);
