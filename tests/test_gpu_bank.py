@@ -344,6 +344,21 @@ def test_determinism(ctx):
         assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("env", [{"MTK_UMMA_SEPC_KF": "0"}, {"MTK_MMD_NO_WDIAG": "1"}, {"MTK_UMMA_PREFETCH": "1"},
+                                 {"MTK_UMMA_SEPC_KF": "0", "MTK_MMD_NO_WDIAG": "1", "MTK_UMMA_PREFETCH": "1"}])
+def test_ab_switches_keep_parity(ctx, monkeypatch, env):
+    """The A/B switches that restore earlier schedules (corrections shared by no
+    k-block, the z * Wsum MMD epilogue, the producer-side prefetch) stay
+    correct: a step with the MMD on tcgen05 shapes (K >= 768: SEPC launches)
+    against the oracle at the per-kernel tolerance."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    dims = [800, 256, 128, 10]
+    bank = make_bank(ctx, 2, dims, seed=17)
+    X, y = inputs(2, 512, dims[0], dims[-1], shift=0.3)
+    check_step(bank, X, y, src=256, lam=0.8, lr=0.05)
+
+
 def test_host_step_equals_device_step(ctx):
     dims = [64, 32, 10]
     X, y = inputs(2, 16, 64, 10)
