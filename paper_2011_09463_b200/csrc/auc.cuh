@@ -127,8 +127,10 @@ struct Work {
     unsigned long long* fpart;  // [blocks][3] per-block (non-members, members, U2) of auc_fast_scan_kernel
     unsigned int* done;         // blocks finished in auc_fast_scan_kernel; zero on entry and exit
     unsigned long long* mail;   // mapped host mailbox (or null): [0..2] counters, [8..9] key range
-                                // words, [10] 1 = U2 complete, [15] sequence number (written last)
+                                // words, [10] 1 = U2 complete, [11] the context's device flags,
+                                // [15] sequence number (written last)
     unsigned long long seq;
+    const int* flags;           // the context's device flags (posted with the counters)
 };
 
 // the counters (and whether U2 is complete) to the host mailbox, then the
@@ -140,6 +142,7 @@ __device__ __forceinline__ void post_mail(const Work& w, bool complete) {
     w.mail[8] = __ldcg(w.cnt + 8);
     w.mail[9] = __ldcg(w.cnt + 9);
     w.mail[10] = complete ? 1ull : 0ull;
+    w.mail[11] = w.flags ? (unsigned long long)(unsigned)__ldcg(w.flags) : 0ull;
     __threadfence_system();
     w.mail[15] = w.seq;
 }

@@ -1067,9 +1067,10 @@ int mtk_attack_auc(mtk_bank* k, const float* logits, int64_t rows, int C, const 
         need(kf <= C, MTK_SHAPE_ERROR, "attack_auc: more features than classes");
         Ctx& c = *k->ctx;
         if (k->L == 2 && attack_fused_ok(C, kf, k->dims[1], k->dims[2])) {
+            bool clear = false;
             attack_auc_fused(c, logits, rows, C, k->W[0].f, k->b[0], k->W[1].f, k->b[1], labels, scores_out,
-                             auc_host, acc_host);
-            c.check_flags();
+                             auc_host, acc_host, &clear);
+            if (!clear) c.check_flags();
             return;
         }
         // any other attack-model shape: the four-call composition on the device

@@ -524,8 +524,9 @@ int mtk_auc(mtk_ctx* c, const float* scores, const uint8_t* labels, int64_t n, d
     return guard_on(c, [&] {
         need(c && scores && labels, MTK_VALUE_ERROR, "auc: null argument");
         need(n >= 1, MTK_SHAPE_ERROR, "auc: zero rows");
-        auc_device(*c, scores, labels, n, auc_host, acc_host);
-        c->check_flags();
+        bool clear = false;
+        auc_device(*c, scores, labels, n, auc_host, acc_host, &clear);
+        if (!clear) c->check_flags();
     });
 }
 

@@ -430,9 +430,11 @@ void launch_column(const float* logits, long long rows, int C, int col, float* o
 bool attack_fused_ok(int C, int K, int H, int O);
 void attack_auc_fused(Ctx& ctx, const float* logits, long long rows, int C, const float* W0, const float* b0,
                       const float* W1, const float* b1, const uint8_t* labels, float* score_out, double* auc,
-                      double* acc);
+                      double* acc, bool* flags_clear = nullptr);
+// flags_clear (optional): set when the context's device flags came back clear
+// with the result (the mailbox path), so the caller can skip check_flags
 void auc_device(Ctx& ctx, const float* scores, const uint8_t* labels, long long n, double* auc,
-                double* acc);
+                double* acc, bool* flags_clear = nullptr);
 
 std::string& last_error();
 

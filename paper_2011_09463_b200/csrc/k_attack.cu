@@ -390,6 +390,7 @@ auc::Work auc_work(Ctx& ctx, long long n) {
     }
     w.mail = ctx.auc_mail_dev;
     w.seq = ++ctx.auc_seq;
+    w.flags = ctx.d_flags;
     w.hist = reinterpret_cast<uint32_t*>(ar + fb + 512);
     w.l2 = reinterpret_cast<uint32_t*>(ar + fb + 512 + al(hb));
     return w;
@@ -417,7 +418,11 @@ void auc_general(Ctx& ctx, auc::Work& w, const uint8_t* labels, long long n) {
 // launches only that path's kernels -- on a misprediction to "full
 // resolution" the general kernels follow the read-back (one more round trip;
 // the result does not depend on the prediction).  Reads back (synchronizes).
-void auc_finish(Ctx& ctx, auc::Work& w, const uint8_t* labels, long long n, double* auc, double* acc) {
+// flags_clear (optional): set when the result came through the mailbox with
+// the context's device flags clear -- the caller's check_flags round trip is
+// then redundant (every kernel of the call ran before the post)
+void auc_finish(Ctx& ctx, auc::Work& w, const uint8_t* labels, long long n, double* auc, double* acc,
+                bool* flags_clear = nullptr) {
     cudaStream_t s = ctx.stream;
     const int sms = device_sm_count(ctx.device);
     const unsigned hist_grid = (unsigned)std::min<long long>(nblocks(n, 256), 8LL * sms);
@@ -429,18 +434,18 @@ void auc_finish(Ctx& ctx, auc::Work& w, const uint8_t* labels, long long n, doub
     // posts (counters + sequence number) once it is done, polling the stream
     // now and then so an error or a missing post falls back to the copy +
     // synchronize (either way the scan has finished when this returns)
-    auto mailbox = [&](unsigned long long* h) {
+    auto mailbox = [&](unsigned long long* h) -> bool {
         volatile unsigned long long* m = ctx.auc_mail;
         for (unsigned spins = 1;; ++spins) {
             if (m[15] == w.seq) {
                 std::atomic_thread_fence(std::memory_order_acquire);
-                for (int i = 0; i < 10; ++i) h[i] = m[i];
-                return;
+                for (int i = 0; i < 12; ++i) h[i] = m[i];
+                return true;
             }
             if ((spins & 1023) == 0 && cudaStreamQuery(s) != cudaErrorNotReady) {
                 if (m[15] == w.seq) continue;  // posted just now
                 readback(h);                   // (raises a pending error)
-                return;
+                return false;
             }
         }
     };
@@ -450,8 +455,9 @@ void auc_finish(Ctx& ctx, auc::Work& w, const uint8_t* labels, long long n, doub
     if (w.win_on) {  // the keys were binned speculatively in the window
         auc::auc_fast_scan_kernel<<<auc_fast_blocks(ctx), auc::kFastScanThreads, 0, s>>>(w);
         count_launch();
-        mailbox(h);
+        const bool mailed = mailbox(h);
         spec_ok = mm[2] == 0;
+        if (flags_clear) *flags_clear = mailed && spec_ok && h[11] == 0;
         w.win_on = 0;  // a re-run bins from the keys
         w.mail = nullptr;
     }
@@ -488,11 +494,11 @@ void auc_finish(Ctx& ctx, auc::Work& w, const uint8_t* labels, long long n, doub
 }  // namespace
 
 void auc_device(Ctx& ctx, const float* scores, const uint8_t* labels, long long n, double* auc,
-                double* acc) {
+                double* acc, bool* flags_clear) {
     auc::Work w = auc_work(ctx, n);
     auc_keys_kernel<<<nblocks(n, 256), 256, 0, ctx.stream>>>(scores, labels, n, w);
     count_launch();
-    auc_finish(ctx, w, labels, n, auc, acc);
+    auc_finish(ctx, w, labels, n, auc, acc, flags_clear);
 }
 
 namespace {
@@ -511,7 +517,7 @@ bool attack_fused_ok(int C, int K, int H, int O) { return C >= 1 && C <= 16 && K
 
 void attack_auc_fused(Ctx& ctx, const float* logits, long long rows, int C, const float* W0, const float* b0,
                       const float* W1, const float* b1, const uint8_t* labels, float* score_out, double* auc,
-                      double* acc) {
+                      double* acc, bool* flags_clear) {
     if (!attack_fused_ok(C, ATT_K, ATT_H, 2)) fail(MTK_ERROR, "attack_auc: unsupported shape");
     cudaStream_t s = ctx.stream;
     // c_att2 is one symbol per device, shared by every context on it: the copy
@@ -539,7 +545,7 @@ void attack_auc_fused(Ctx& ctx, const float* logits, long long rows, int C, cons
         attack_score2_kernel<16, false, QP><<<nblocks(thr, 256), 256, 0, s>>>(logits, rows, C, labels, score_out, w);
     count_launch();
     MTK_CUDA(cudaEventRecord(last, s));
-    auc_finish(ctx, w, labels, rows, auc, acc);
+    auc_finish(ctx, w, labels, rows, auc, acc, flags_clear);
 }
 
 }  // namespace mtk

@@ -42,6 +42,16 @@ for Q in (1024, 1 << 20):
     for _ in range(200):
         lib.mtk_auc(ctx.h, ps, pl, Q, C.byref(a), C.byref(acc))
     print(f"Q={Q:8d} raw mtk_auc {(time.perf_counter() - t) / 200 * 1e6:7.1f} us/call")
+for Q in (1024, 1 << 20):
+    logits = torch.randn(Q, 10, device="cuda", generator=gen)
+    labels = (torch.rand(Q, device="cuda", generator=gen) < 0.5).to(torch.uint8)
+    pl, pb = C.c_void_p(logits.data_ptr()), C.c_void_p(labels.data_ptr())
+    for _ in range(20):
+        lib.mtk_attack_auc(att.h, pl, Q, 10, pb, C.byref(a), C.byref(acc), None)
+    t = time.perf_counter()
+    for _ in range(200):
+        lib.mtk_attack_auc(att.h, pl, Q, 10, pb, C.byref(a), C.byref(acc), None)
+    print(f"Q={Q:8d} raw mtk_attack_auc {(time.perf_counter() - t) / 200 * 1e6:7.1f} us/call")
 s = torch.cuda.current_stream()
 x = torch.empty(16, device="cuda")
 h = torch.empty(16, pin_memory=True)
