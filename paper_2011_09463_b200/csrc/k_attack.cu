@@ -168,16 +168,21 @@ __global__ void __launch_bounds__(256) auc_keys_kernel(const float* s, const uin
 constexpr int ATT_K = 3, ATT_H = 64;
 // Two queries per thread: the attack MLP runs on packed fp32x2 (FFMA2 /
 // FADD2: the same IEEE operations lane by lane, so the scores stay
-// bit-identical to the one-query kernel) with each weight stored twice in
-// constant memory (c_att2: (w, w) pairs, warp-uniform 64-bit operands).
+// bit-identical to the one-query kernel).  The weights sit in constant memory
+// grouped per hidden unit, so one 64-bit uniform load brings two of them and
+// FFMA2 broadcasts each from its uniform register (UR.F32 operand): three
+// LDCU per hidden unit instead of six.
 // EXACT: C == CC at compile time (the 10-class posteriors), no padding lanes.
-__constant__ float2 c_att2[ATT_K * ATT_H + ATT_H + ATT_H * 2 + 2];
+struct AttConst {
+    float4 a[ATT_H];  // (W0[0][h], W0[1][h], W0[2][h], b0[h])
+    float2 b[ATT_H];  // (W1[h][0], W1[h][1])
+    float2 c;         // (b1[0], b1[1])
+};
+static_assert(ATT_K == 3, "AttConst packs three input weights per hidden unit");
+__constant__ AttConst c_att;
 
 template <int CC, bool EXACT>
-__device__ __forceinline__ void top3_of_row(const float* x, int C, float (&top)[ATT_K]) {
-    float v[CC];
-#pragma unroll
-    for (int j = 0; j < CC; ++j) v[j] = (EXACT || j < C) ? __ldg(x + j) : -INFINITY;
+__device__ __forceinline__ void top3_of_vals(float (&v)[CC], int C, float (&top)[ATT_K]) {
     float mx = v[0];
 #pragma unroll
     for (int j = 1; j < CC; ++j) mx = fmaxf(mx, v[j]);
@@ -202,16 +207,38 @@ __device__ __forceinline__ void top3_of_row(const float* x, int C, float (&top)[
         }
     }
 }
+template <int CC, bool EXACT>
+__device__ __forceinline__ void top3_of_row(const float* x, int C, float (&top)[ATT_K]) {
+    float v[CC];
+#pragma unroll
+    for (int j = 0; j < CC; ++j) v[j] = (EXACT || j < C) ? __ldg(x + j) : -INFINITY;
+    top3_of_vals<CC, EXACT>(v, C, top);
+}
 
 template <int CC, bool EXACT, int QP>  // QP query pairs per thread
 __global__ void __launch_bounds__(256) attack_score2_kernel(const float* logits, long long rows, int C,
                                                             const uint8_t* lab, float* score_out, auc::Work w) {
     const long long r0 = 2LL * QP * (blockIdx.x * (long long)blockDim.x + threadIdx.x);
+    const bool vec = (reinterpret_cast<uintptr_t>(logits) & 15) == 0;
     float2 t[QP][ATT_K];
 #pragma unroll
     for (int q = 0; q < QP; ++q) {
         float ta[ATT_K], tb[ATT_K];
         const long long ra = r0 + 2 * q;
+        if (CC == 10 && EXACT && vec && ra + 1 < rows) {
+            // the pair's 20 posteriors are 80 contiguous, 16-B aligned bytes:
+            // five 128-bit loads instead of twenty scalar ones
+            const float4* p4 = reinterpret_cast<const float4*>(logits + ra * CC);
+            const float4 a0 = __ldg(p4), a1 = __ldg(p4 + 1), a2 = __ldg(p4 + 2), a3 = __ldg(p4 + 3),
+                         a4 = __ldg(p4 + 4);
+            float va[CC] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w, a2.x, a2.y};
+            float vb[CC] = {a2.z, a2.w, a3.x, a3.y, a3.z, a3.w, a4.x, a4.y, a4.z, a4.w};
+            top3_of_vals<CC, EXACT>(va, C, ta);
+            top3_of_vals<CC, EXACT>(vb, C, tb);
+#pragma unroll
+            for (int a = 0; a < ATT_K; ++a) t[q][a] = make_float2(ta[a], tb[a]);
+            continue;
+        }
         if (ra < rows) top3_of_row<CC, EXACT>(logits + ra * C, C, ta);
         else ta[0] = ta[1] = ta[2] = 0.f;
         if (ra + 1 < rows) top3_of_row<CC, EXACT>(logits + (ra + 1) * C, C, tb);
@@ -219,17 +246,16 @@ __global__ void __launch_bounds__(256) attack_score2_kernel(const float* logits,
 #pragma unroll
         for (int a = 0; a < ATT_K; ++a) t[q][a] = make_float2(ta[a], tb[a]);
     }
-    const float2* W0 = c_att2;
-    const float2* B0 = W0 + ATT_K * ATT_H;
-    const float2* W1 = B0 + ATT_H;
-    const float2* B1 = W1 + ATT_H * 2;
     float2 o0[QP], o1[QP];
 #pragma unroll
     for (int q = 0; q < QP; ++q) o0[q] = o1[q] = make_float2(0.f, 0.f);
 #pragma unroll 8
     for (int h = 0; h < ATT_H; ++h) {
-        const float2 w0 = W0[h], w1 = W0[ATT_H + h], w2 = W0[2 * ATT_H + h], bb = B0[h];
-        const float2 v0 = W1[h * 2], v1 = W1[h * 2 + 1];
+        const float4 a = c_att.a[h];
+        const float2 v = c_att.b[h];
+        const float2 w0 = make_float2(a.x, a.x), w1 = make_float2(a.y, a.y), w2 = make_float2(a.z, a.z),
+                     bb = make_float2(a.w, a.w);
+        const float2 v0 = make_float2(v.x, v.x), v1 = make_float2(v.y, v.y);
 #pragma unroll
         for (int q = 0; q < QP; ++q) {
             float2 acc = __ffma2_rn(t[q][0], w0, make_float2(0.f, 0.f));
@@ -248,7 +274,8 @@ __global__ void __launch_bounds__(256) attack_score2_kernel(const float* logits,
 #pragma unroll
     for (int q = 0; q < 2 * QP; ++q) {
         const long long r = r0 + q;
-        const float2 a = __fadd2_rn(o0[q / 2], B1[0]), b = __fadd2_rn(o1[q / 2], B1[1]);
+        const float2 a = __fadd2_rn(o0[q / 2], make_float2(c_att.c.x, c_att.c.x)),
+                     b = __fadd2_rn(o1[q / 2], make_float2(c_att.c.y, c_att.c.y));
         const float p0 = (q & 1) ? a.y : a.x, p1 = (q & 1) ? b.y : b.x;
         uint32_t u = 0;
         bool l = false;
@@ -270,13 +297,13 @@ __global__ void __launch_bounds__(256) attack_score2_kernel(const float* logits,
     auc::publish_counts(w, kmax, nkmin, pos, hit);
 }
 
-// (w, w) pairs of the attack weights for c_att2
-__global__ void att_dup_kernel(const float* W0, const float* b0, const float* W1, const float* b1, float2* out) {
-    const int i = threadIdx.x + blockIdx.x * blockDim.x;
-    constexpr int n0 = ATT_K * ATT_H, n1 = n0 + ATT_H, n2 = n1 + ATT_H * 2, n3 = n2 + 2;
-    if (i >= n3) return;
-    const float v = i < n0 ? W0[i] : i < n1 ? b0[i - n0] : i < n2 ? W1[i - n1] : b1[i - n2];
-    out[i] = make_float2(v, v);
+// the attack weights in c_att's layout (W0 is [ATT_K][ATT_H], W1 [ATT_H][2])
+__global__ void att_pack_kernel(const float* W0, const float* b0, const float* W1, const float* b1, AttConst* out) {
+    const int h = threadIdx.x;
+    if (h >= ATT_H) return;
+    out->a[h] = make_float4(W0[h], W0[ATT_H + h], W0[2 * ATT_H + h], b0[h]);
+    out->b[h] = make_float2(W1[2 * h], W1[2 * h + 1]);
+    if (h == 0) out->c = make_float2(b1[0], b1[1]);
 }
 
 inline unsigned nblocks(long long n, int t) { return (unsigned)((n + t - 1) / t); }
@@ -520,7 +547,7 @@ void attack_auc_fused(Ctx& ctx, const float* logits, long long rows, int C, cons
                       double* acc, bool* flags_clear) {
     if (!attack_fused_ok(C, ATT_K, ATT_H, 2)) fail(MTK_ERROR, "attack_auc: unsupported shape");
     cudaStream_t s = ctx.stream;
-    // c_att2 is one symbol per device, shared by every context on it: the copy
+    // c_att is one symbol per device, shared by every context on it: the copy
     // of this call must not land while another context's scoring kernel still
     // reads the previous weights (a different stream, so no implicit order).
     // Per device, the stream waits on the event recorded after the last
@@ -529,15 +556,14 @@ void attack_auc_fused(Ctx& ctx, const float* logits, long long rows, int C, cons
     cudaEvent_t& last = att_last_use(ctx.device);
     if (last) MTK_CUDA(cudaStreamWaitEvent(s, last, 0));
     else MTK_CUDA(cudaEventCreateWithFlags(&last, cudaEventDisableTiming));
-    // the attack model's weights -> constant memory as (w, w) pairs
-    // (stream-ordered: a device-side duplication, then one device copy)
-    constexpr int nw = ATT_K * ATT_H + ATT_H + ATT_H * 2 + 2;
+    // the attack model's weights -> constant memory, grouped per hidden unit
+    // (stream-ordered: a device-side pack, then one device copy)
     auc::Work w = auc_work(ctx, rows);
-    float2* dup = reinterpret_cast<float2*>(w.mixed);  // free until the AUC passes
-    att_dup_kernel<<<1, 512, 0, s>>>(W0, b0, W1, b1, dup);
+    AttConst* pk = reinterpret_cast<AttConst*>(w.mixed);  // free until the AUC passes
+    att_pack_kernel<<<1, ATT_H, 0, s>>>(W0, b0, W1, b1, pk);
     count_launch();
-    MTK_CUDA(cudaMemcpyToSymbolAsync(c_att2, dup, nw * sizeof(float2), 0, cudaMemcpyDeviceToDevice, s));
-    constexpr int QP = 1;  // one query pair per thread (QP = 2 measured slower: 44 vs 38 us)
+    MTK_CUDA(cudaMemcpyToSymbolAsync(c_att, pk, sizeof(AttConst), 0, cudaMemcpyDeviceToDevice, s));
+    constexpr int QP = 1;  // one query pair per thread (QP = 2: fewer instructions, but under one wave of threads -- not faster)
     const long long thr = (rows + 2 * QP - 1) / (2 * QP);
     if (C == 10)
         attack_score2_kernel<10, true, QP><<<nblocks(thr, 256), 256, 0, s>>>(logits, rows, C, labels, score_out, w);
