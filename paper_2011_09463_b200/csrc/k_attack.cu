@@ -9,7 +9,6 @@
 #include <atomic>
 #include <cstring>
 #include <cmath>
-#include <mutex>
 
 #include "auc.cuh"
 #include "internal.h"
@@ -163,23 +162,22 @@ __global__ void __launch_bounds__(256) auc_keys_kernel(const float* s, const uin
 // ---- fused attack scoring: posterior softmax -> top-KF sorted features ->
 // attack MLP KF -> H (ReLU) -> 2 -> member posterior -> AUC keys, one pass
 // over the logits.  Same arithmetic, in the same order, as features_small_kernel,
-// small2_forward_kernel and column_kernel (bit-identical scores); the attack
-// model's weights sit in constant memory (warp-uniform operands).
+// small2_forward_kernel and column_kernel (bit-identical scores); each CTA
+// stages the attack model's weights in shared memory (warp-uniform reads).
 constexpr int ATT_K = 3, ATT_H = 64;
 // Two queries per thread: the attack MLP runs on packed fp32x2 (FFMA2 /
 // FADD2: the same IEEE operations lane by lane, so the scores stay
-// bit-identical to the one-query kernel).  The weights sit in constant memory
-// grouped per hidden unit, so one 64-bit uniform load brings two of them and
-// FFMA2 broadcasts each from its uniform register (UR.F32 operand): three
-// LDCU per hidden unit instead of six.
+// bit-identical to the one-query kernel).  The weights are read straight from
+// the bank and staged per CTA, grouped per hidden unit: (W0[0][h], W0[1][h],
+// W0[2][h], b0[h]) and (W1[h][0], W1[h][1]) -- one 128-bit and one 64-bit
+// broadcast shared load per hidden unit, each weight broadcast into both
+// lanes by FFMA2 (R.F32 operand).  No per-call weight upload, no process-wide
+// symbol shared between contexts.
 // EXACT: C == CC at compile time (the 10-class posteriors), no padding lanes.
-struct AttConst {
-    float4 a[ATT_H];  // (W0[0][h], W0[1][h], W0[2][h], b0[h])
-    float2 b[ATT_H];  // (W1[h][0], W1[h][1])
-    float2 c;         // (b1[0], b1[1])
+static_assert(ATT_K == 3, "the per-hidden-unit record holds three input weights");
+struct AttW {
+    const float *W0, *b0, *W1, *b1;  // the bank's layer 0 ([ATT_K][ATT_H], [ATT_H]) and 1 ([ATT_H][2], [2])
 };
-static_assert(ATT_K == 3, "AttConst packs three input weights per hidden unit");
-__constant__ AttConst c_att;
 
 template <int CC, bool EXACT>
 __device__ __forceinline__ void top3_of_vals(float (&v)[CC], int C, float (&top)[ATT_K]) {
@@ -217,7 +215,18 @@ __device__ __forceinline__ void top3_of_row(const float* x, int C, float (&top)[
 
 template <int CC, bool EXACT, int QP>  // QP query pairs per thread
 __global__ void __launch_bounds__(256) attack_score2_kernel(const float* logits, long long rows, int C,
-                                                            const uint8_t* lab, float* score_out, auc::Work w) {
+                                                            const uint8_t* lab, float* score_out, auc::Work w,
+                                                            AttW aw) {
+    __shared__ float4 sa[ATT_H];  // (W0[0][h], W0[1][h], W0[2][h], b0[h])
+    __shared__ float2 sb[ATT_H];  // (W1[h][0], W1[h][1])
+    __shared__ float2 sc;         // (b1[0], b1[1])
+    if (threadIdx.x < ATT_H) {  // issued before the posterior loads; read after them
+        const int h = threadIdx.x;
+        sa[h] = make_float4(__ldg(aw.W0 + h), __ldg(aw.W0 + ATT_H + h), __ldg(aw.W0 + 2 * ATT_H + h),
+                            __ldg(aw.b0 + h));
+        sb[h] = make_float2(__ldg(aw.W1 + 2 * h), __ldg(aw.W1 + 2 * h + 1));
+        if (h == 0) sc = make_float2(__ldg(aw.b1), __ldg(aw.b1 + 1));
+    }
     const long long r0 = 2LL * QP * (blockIdx.x * (long long)blockDim.x + threadIdx.x);
     const bool vec = (reinterpret_cast<uintptr_t>(logits) & 15) == 0;
     float2 t[QP][ATT_K];
@@ -246,13 +255,14 @@ __global__ void __launch_bounds__(256) attack_score2_kernel(const float* logits,
 #pragma unroll
         for (int a = 0; a < ATT_K; ++a) t[q][a] = make_float2(ta[a], tb[a]);
     }
+    __syncthreads();  // the staged weights
     float2 o0[QP], o1[QP];
 #pragma unroll
     for (int q = 0; q < QP; ++q) o0[q] = o1[q] = make_float2(0.f, 0.f);
 #pragma unroll 8
     for (int h = 0; h < ATT_H; ++h) {
-        const float4 a = c_att.a[h];
-        const float2 v = c_att.b[h];
+        const float4 a = sa[h];
+        const float2 v = sb[h];
         const float2 w0 = make_float2(a.x, a.x), w1 = make_float2(a.y, a.y), w2 = make_float2(a.z, a.z),
                      bb = make_float2(a.w, a.w);
         const float2 v0 = make_float2(v.x, v.x), v1 = make_float2(v.y, v.y);
@@ -274,8 +284,8 @@ __global__ void __launch_bounds__(256) attack_score2_kernel(const float* logits,
 #pragma unroll
     for (int q = 0; q < 2 * QP; ++q) {
         const long long r = r0 + q;
-        const float2 a = __fadd2_rn(o0[q / 2], make_float2(c_att.c.x, c_att.c.x)),
-                     b = __fadd2_rn(o1[q / 2], make_float2(c_att.c.y, c_att.c.y));
+        const float2 a = __fadd2_rn(o0[q / 2], make_float2(sc.x, sc.x)),
+                     b = __fadd2_rn(o1[q / 2], make_float2(sc.y, sc.y));
         const float p0 = (q & 1) ? a.y : a.x, p1 = (q & 1) ? b.y : b.x;
         uint32_t u = 0;
         bool l = false;
@@ -297,14 +307,6 @@ __global__ void __launch_bounds__(256) attack_score2_kernel(const float* logits,
     auc::publish_counts(w, kmax, nkmin, pos, hit);
 }
 
-// the attack weights in c_att's layout (W0 is [ATT_K][ATT_H], W1 [ATT_H][2])
-__global__ void att_pack_kernel(const float* W0, const float* b0, const float* W1, const float* b1, AttConst* out) {
-    const int h = threadIdx.x;
-    if (h >= ATT_H) return;
-    out->a[h] = make_float4(W0[h], W0[ATT_H + h], W0[2 * ATT_H + h], b0[h]);
-    out->b[h] = make_float2(W1[2 * h], W1[2 * h + 1]);
-    if (h == 0) out->c = make_float2(b1[0], b1[1]);
-}
 
 inline unsigned nblocks(long long n, int t) { return (unsigned)((n + t - 1) / t); }
 
@@ -528,17 +530,6 @@ void auc_device(Ctx& ctx, const float* scores, const uint8_t* labels, long long 
     auc_finish(ctx, w, labels, n, auc, acc, flags_clear);
 }
 
-namespace {
-std::mutex& att_mutex() {
-    static std::mutex m;
-    return m;
-}
-cudaEvent_t& att_last_use(int device) {
-    static cudaEvent_t ev[64] = {};
-    if (device < 0 || device >= 64) fail(MTK_ERROR, "attack_auc: device index out of range");
-    return ev[device];
-}
-}  // namespace
 
 bool attack_fused_ok(int C, int K, int H, int O) { return C >= 1 && C <= 16 && K == ATT_K && H == ATT_H && O == 2; }
 
@@ -547,30 +538,17 @@ void attack_auc_fused(Ctx& ctx, const float* logits, long long rows, int C, cons
                       double* acc, bool* flags_clear) {
     if (!attack_fused_ok(C, ATT_K, ATT_H, 2)) fail(MTK_ERROR, "attack_auc: unsupported shape");
     cudaStream_t s = ctx.stream;
-    // c_att is one symbol per device, shared by every context on it: the copy
-    // of this call must not land while another context's scoring kernel still
-    // reads the previous weights (a different stream, so no implicit order).
-    // Per device, the stream waits on the event recorded after the last
-    // scoring launch, and records its own; the mutex orders the enqueues.
-    std::lock_guard<std::mutex> lk(att_mutex());
-    cudaEvent_t& last = att_last_use(ctx.device);
-    if (last) MTK_CUDA(cudaStreamWaitEvent(s, last, 0));
-    else MTK_CUDA(cudaEventCreateWithFlags(&last, cudaEventDisableTiming));
-    // the attack model's weights -> constant memory, grouped per hidden unit
-    // (stream-ordered: a device-side pack, then one device copy)
     auc::Work w = auc_work(ctx, rows);
-    AttConst* pk = reinterpret_cast<AttConst*>(w.mixed);  // free until the AUC passes
-    att_pack_kernel<<<1, ATT_H, 0, s>>>(W0, b0, W1, b1, pk);
-    count_launch();
-    MTK_CUDA(cudaMemcpyToSymbolAsync(c_att, pk, sizeof(AttConst), 0, cudaMemcpyDeviceToDevice, s));
+    const AttW aw{W0, b0, W1, b1};
     constexpr int QP = 1;  // one query pair per thread (QP = 2: fewer instructions, but under one wave of threads -- not faster)
     const long long thr = (rows + 2 * QP - 1) / (2 * QP);
     if (C == 10)
-        attack_score2_kernel<10, true, QP><<<nblocks(thr, 256), 256, 0, s>>>(logits, rows, C, labels, score_out, w);
+        attack_score2_kernel<10, true, QP><<<nblocks(thr, 256), 256, 0, s>>>(logits, rows, C, labels, score_out, w,
+                                                                             aw);
     else
-        attack_score2_kernel<16, false, QP><<<nblocks(thr, 256), 256, 0, s>>>(logits, rows, C, labels, score_out, w);
+        attack_score2_kernel<16, false, QP><<<nblocks(thr, 256), 256, 0, s>>>(logits, rows, C, labels, score_out, w,
+                                                                              aw);
     count_launch();
-    MTK_CUDA(cudaEventRecord(last, s));
     auc_finish(ctx, w, labels, rows, auc, acc, flags_clear);
 }
 
