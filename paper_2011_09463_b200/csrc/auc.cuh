@@ -235,12 +235,15 @@ __global__ void __launch_bounds__(256) auc_hist_kernel(Work w, const uint8_t* la
     }
 }
 
-// F2: U2 over the full-resolution bins [0, kmax - kmin]
+// F2: U2 over the full-resolution bins [0, kmax - kmin].  Launched right
+// behind the scoring (or keys) kernel as a programmatic dependent: its CTAs
+// take the SMs that kernel's last wave frees, and wait here for its results.
 constexpr int kFastScanThreads = 1024;
 __global__ void __launch_bounds__(kFastScanThreads) auc_fast_scan_kernel(Work w) {
     __shared__ uint32_t sh[33];
     __shared__ unsigned long long shl[32];
     __shared__ bool last;
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // (a no-op without the PDL launch attribute)
     const uint32_t kmin = ~w.mm[1], kmax = w.mm[0];
     if (blockIdx.x == 0 && threadIdx.x == 0 && ((w.win_on && w.mm[2]) || !fast_path(w)))
         post_mail(w, false);  // the host continues (re-binning / the general path)

@@ -141,6 +141,7 @@ __global__ void column_kernel(const float* logits, long long rows, int C, int co
 // per query: the order-preserving key; per block: the key range, member and
 // hit-at-0.5 counts (auc.cuh)
 __global__ void __launch_bounds__(256) auc_keys_kernel(const float* s, const uint8_t* lab, long long n, auc::Work w) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the scan kernel may launch
     const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     unsigned long long pos = 0, hit = 0;
     uint32_t kmax = 0, nkmin = 0, u = 0;
@@ -227,6 +228,7 @@ __global__ void __launch_bounds__(256) attack_score2_kernel(const float* logits,
         sb[h] = make_float2(__ldg(aw.W1 + 2 * h), __ldg(aw.W1 + 2 * h + 1));
         if (h == 0) sc = make_float2(__ldg(aw.b1), __ldg(aw.b1 + 1));
     }
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the scan kernel may launch
     const long long r0 = 2LL * QP * (blockIdx.x * (long long)blockDim.x + threadIdx.x);
     const bool vec = (reinterpret_cast<uintptr_t>(logits) & 15) == 0;
     float2 t[QP][ATT_K];
@@ -482,7 +484,17 @@ void auc_finish(Ctx& ctx, auc::Work& w, const uint8_t* labels, long long n, doub
     const uint32_t* mm = reinterpret_cast<const uint32_t*>(h + 8);
     bool spec_ok = false;
     if (w.win_on) {  // the keys were binned speculatively in the window
-        auc::auc_fast_scan_kernel<<<auc_fast_blocks(ctx), auc::kFastScanThreads, 0, s>>>(w);
+        // a programmatic dependent of the scoring / keys kernel just launched
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((unsigned)auc_fast_blocks(ctx));
+        cfg.blockDim = dim3(auc::kFastScanThreads);
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = umma::pdl_enabled() ? 1 : 0;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        MTK_CUDA(cudaLaunchKernelEx(&cfg, auc::auc_fast_scan_kernel, w));
         count_launch();
         const bool mailed = mailbox(h);
         spec_ok = mm[2] == 0;
