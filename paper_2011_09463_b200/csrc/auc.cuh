@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(256) auc_hist_kernel(Work w, const uint8_t* la
 // F2: U2 over the full-resolution bins [0, kmax - kmin].  Launched right
 // behind the scoring (or keys) kernel as a programmatic dependent: its CTAs
 // take the SMs that kernel's last wave frees, and wait here for its results.
-constexpr int kFastScanThreads = 1024;
+constexpr int kFastScanThreads = 512;
 __global__ void __launch_bounds__(kFastScanThreads) auc_fast_scan_kernel(Work w) {
     __shared__ uint32_t sh[33];
     __shared__ unsigned long long shl[32];

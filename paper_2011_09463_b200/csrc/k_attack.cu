@@ -371,7 +371,7 @@ void launch_column(const float* logits, long long rows, int C, int col, float* o
 }
 
 namespace {
-int auc_fast_blocks(Ctx& ctx) { return device_sm_count(ctx.device); }
+int auc_fast_blocks(Ctx& ctx) { return 2 * device_sm_count(ctx.device); }
 // grow-only workspace from ctx.big: keys, histograms, bucket slots, the
 // scattered mixed buckets, the large-bucket histograms, counters
 auc::Work auc_work(Ctx& ctx, long long n) {
