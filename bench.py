@@ -88,14 +88,15 @@ def fp32acc_peak():
 
 
 class ClockSampler:
-    """SM clock + throttle reasons via NVML, polled every 1 ms in a thread, for
-    the duration of the `with` block (the timed region)."""
+    """SM clock + throttle reasons via NVML, polled every `period` s (1 ms) in a
+    thread, for the duration of the `with` block (the timed region)."""
 
     REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
                "sw_power_cap": 0x4}
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period: float = 0.001):
         self.index = index
+        self.period = period
         self.samples = []
         self.max_mhz = None
         self._stop = threading.Event()
@@ -116,7 +117,7 @@ class ClockSampler:
                              pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)))
                     except Exception:
                         pass
-                    time.sleep(0.001)
+                    time.sleep(self.period)
 
             self.t = threading.Thread(target=poll, daemon=True)
             self.t.start()
@@ -133,7 +134,7 @@ class ClockSampler:
         sm = [s for s, _ in self.samples]
         reasons = sorted({n for _, r in self.samples for n, bit in self.REASONS.items() if r & bit})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz,
-                "reasons": reasons, "samples": len(sm), "source": "nvml, 1 ms poll"}
+                "reasons": reasons, "samples": len(sm), "source": f"nvml, {self.period * 1000:g} ms poll"}
 
 
 # ----------------------------------------------------------------------------- processes
@@ -681,7 +682,9 @@ def measure_c5(args, world, rank, local, steps, warmup, cpu=True):
     for _ in range(warmup):
         res = sweep()
     times = []
-    with ClockSampler(local) as clk:
+    # a 10 ms poll: the sweep's host phases use every core (a 1 ms poller
+    # thread straggles their parallel sections)
+    with ClockSampler(local, period=0.01) as clk:
         for _ in range(steps):
             barrier(world)
             torch.cuda.synchronize()

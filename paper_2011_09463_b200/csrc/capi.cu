@@ -89,6 +89,16 @@ void* Ctx::big(size_t bytes) {
     return d_big;
 }
 
+void* Ctx::sweep_buf(size_t bytes) {
+    if (bytes > sweep_bytes) {
+        if (d_sweep) MTK_CUDA(cudaFree(d_sweep));  // synchronizes: in-flight users are done
+        d_sweep = nullptr;
+        MTK_CUDA(cudaMalloc(&d_sweep, bytes));
+        sweep_bytes = bytes;
+    }
+    return d_sweep;
+}
+
 uint32_t* Ctx::auc_l2(size_t bytes) {
     if (bytes > auc_l2_bytes) {
         if (d_auc_l2) MTK_CUDA(cudaFree(d_auc_l2));  // synchronizes: in-flight users are done
@@ -123,6 +133,38 @@ void Ctx::check_flags() {
         if (f & kFlagBadIndex) fail(MTK_VALUE_ERROR, "gather_rows: index out of range");
         fail(MTK_ERROR, "non-finite values produced on the device");
     }
+}
+
+void* HostBlockPool::get(size_t bytes, size_t* cap) {
+    std::lock_guard<std::mutex> lk(mu_);
+    size_t best = free_.size();
+    for (size_t i = 0; i < free_.size(); ++i)
+        if (free_[i].second >= bytes && (best == free_.size() || free_[i].second < free_[best].second)) best = i;
+    if (best < free_.size()) {
+        void* p = free_[best].first;
+        *cap = free_[best].second;
+        free_.erase(free_.begin() + (long)best);
+        return p;
+    }
+    void* p = nullptr;
+    MTK_CUDA(cudaHostAlloc(&p, bytes, cudaHostAllocPortable));
+    all_.push_back(p);
+    *cap = bytes;
+    return p;
+}
+
+void HostBlockPool::put(void* p, size_t cap) {
+    std::lock_guard<std::mutex> lk(mu_);
+    free_.push_back({p, cap});
+}
+
+HostBlockPool::~HostBlockPool() {
+    for (void* p : all_) cudaFreeHost(p);
+}
+
+HostBlockPool& Ctx::host_pool() {
+    if (!host_blocks) host_blocks = new HostBlockPool();
+    return *host_blocks;
 }
 
 cudaEvent_t Ctx::record(cudaStream_t s) {
@@ -227,9 +269,11 @@ int mtk_ctx_destroy(mtk_ctx* c) {
         cudaFree(c->d_scratch);
         cudaFree(c->d_big);
         cudaFree(c->d_auc_l2);
+        cudaFree(c->d_sweep);
         if (c->auc_mail) cudaFreeHost(c->auc_mail);
         if (c->pinned) cudaFreeHost(c->pinned);
         if (c->pinned_flags) cudaFreeHost(c->pinned_flags);
+        delete c->host_blocks;
         if (c->own_stream) cudaStreamDestroy(c->stream);
         if (c->side) {
             cudaStreamSynchronize(c->side);

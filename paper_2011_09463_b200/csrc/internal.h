@@ -7,6 +7,7 @@
 #include <stdexcept>
 #include <string>
 #include <utility>
+#include <mutex>
 #include <vector>
 
 #include "minitransfer/mtk.h"
@@ -34,6 +35,24 @@ enum : int { kFlagNonFinite = 1, kFlagBadLabel = 2, kFlagBadIndex = 4 };
 // Phases of the bank step, for optional CUDA-event timing (mtk_ctx_set_timing).
 enum Phase : int { kPhFwd = 0, kPhCe, kPhMmdBeta, kPhMmdPairs, kPhDx, kPhDw, kPhBias, kPhOther,
                    kPhSide, kNumPhases };
+
+// Pinned host blocks, recycled (grow-only; thread-safe: the sweep's worker
+// thread takes blocks while the caller's thread returns them).  Portable, so
+// a thread with another device current may allocate.
+class HostBlockPool {
+    std::mutex mu_;
+    std::vector<std::pair<void*, size_t>> free_;
+    std::vector<void*> all_;
+
+public:
+    HostBlockPool() = default;
+    HostBlockPool(const HostBlockPool&) = delete;
+    HostBlockPool& operator=(const HostBlockPool&) = delete;
+    // the smallest free block of >= bytes, else a new one; *cap = its size
+    void* get(size_t bytes, size_t* cap);
+    void put(void* p, size_t cap);
+    ~HostBlockPool();
+};
 
 struct Ctx {
     int device = 0;
@@ -75,6 +94,13 @@ struct Ctx {
     uint32_t auc_win_lo = 0;
     int auc_parity = 0;               // which of the two counter blocks this call uses
     size_t auc_l2_bytes = 0;
+    HostBlockPool* host_blocks = nullptr;  // the native sweep's pinned staging (sweep.cpp)
+    HostBlockPool& host_pool();
+    // grow-only device workspace of the native sweep (the query rows of every
+    // model: G x Q x d floats, GBs at C5 -- allocated once per context)
+    void* sweep_buf(size_t bytes);
+    void* d_sweep = nullptr;
+    size_t sweep_bytes = 0;
     void check_flags();               // synchronizes; throws on a set flag
     // Side stream for short, latency-bound kernels that do not feed the next
     // main-stream launch (bias updates, the skinny head dW, the MMD prep pass):

@@ -24,6 +24,7 @@
 #include <functional>
 #include <future>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -60,6 +61,64 @@ struct Dev {  // owning device buffer
         return static_cast<T*>(p);
     }
 };
+
+// The per-epoch batch indices and weights are built straight into pinned
+// host blocks (the context's recycled pool, Ctx::host_pool) on the worker
+// thread and copied to persistent device buffers: no staging copy, no
+// synchronising pageable transfer, no per-epoch cudaMalloc / cudaFree
+// (cudaFree synchronises the device, which serialised the host and device
+// pipelines), and no pinning / unpinning per sweep.
+using PinnedPool = HostBlockPool;
+template <class T>
+struct PinnedVec {  // a fixed-size array in a pooled pinned block (bytes: the block's size)
+    PinnedPool* pool = nullptr;
+    T* p = nullptr;
+    size_t n = 0, bytes = 0;
+    PinnedVec() = default;
+    PinnedVec(PinnedPool& pl, size_t count) : pool(&pl), n(count) {
+        p = static_cast<T*>(pl.get(std::max<size_t>(count * sizeof(T), 1), &bytes));
+    }
+    PinnedVec(PinnedVec&& o) noexcept : pool(o.pool), p(o.p), n(o.n), bytes(o.bytes) { o.p = nullptr; }
+    PinnedVec& operator=(PinnedVec&& o) noexcept {
+        std::swap(pool, o.pool);
+        std::swap(p, o.p);
+        std::swap(n, o.n);
+        std::swap(bytes, o.bytes);
+        return *this;
+    }
+    PinnedVec(const PinnedVec&) = delete;
+    ~PinnedVec() {
+        if (p) pool->put(p, bytes);
+    }
+    T* data() const { return p; }
+    size_t size() const { return n; }
+    T& operator[](size_t i) const { return p[i]; }
+};
+// a grow-only device buffer
+struct DevBuf {
+    Dev d;
+    template <class T>
+    T* fit(size_t count) {
+        if (d.bytes < count * sizeof(T)) d = Dev(count * sizeof(T));
+        return d.as<T>();
+    }
+};
+// one epoch call's indices / weights -> device (stream-ordered; the caller's
+// train_epoch synchronises before the pinned blocks are recycled)
+template <class F>
+void with_uploaded(const PinnedVec<int64_t>& ix, const PinnedVec<float>& w, DevBuf& dix, DevBuf& dw,
+                   cudaStream_t st, F&& run) {
+    int64_t* di = dix.fit<int64_t>(ix.size());
+    float* dwp = dw.fit<float>(w.size());
+    MTK_CUDA(cudaMemcpyAsync(di, ix.data(), ix.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    MTK_CUDA(cudaMemcpyAsync(dwp, w.data(), w.size() * sizeof(float), cudaMemcpyHostToDevice, st));
+    try {
+        run(di, dwp);
+    } catch (...) {
+        cudaStreamSynchronize(st);  // the copies read the pinned blocks
+        throw;
+    }
+}
 
 template <class T>
 Dev upload(const std::vector<T>& h, cudaStream_t s) {
@@ -285,16 +344,18 @@ int mtk_sweep_run(mtk_ctx* ctx, const mtk_sweep_config* cfg, mtk_comm* comm, mtk
         struct Call {
             const Pool* pool;
             int rows, nsteps;
-            std::vector<int64_t> ix;
-            std::vector<float> w;
+            PinnedVec<int64_t> ix;
+            PinnedVec<float> w;
             std::vector<double> den;
             mtk_step s;
         };
+        PinnedPool& pinned = ctx->host_pool();
+        DevBuf dix_buf, dw_buf;
         auto make_call = [&](const Pool& pool, int rows, int nsteps,
                              const std::function<void(int g, int t, int64_t* ix, float* w)>& fill,
                              std::vector<double> denom0, mtk_step s) {
-            Call cl{&pool, rows, nsteps, std::vector<int64_t>((size_t)nsteps * G * rows),
-                    std::vector<float>((size_t)nsteps * G * rows), std::move(denom0), s};
+            Call cl{&pool, rows, nsteps, PinnedVec<int64_t>(pinned, (size_t)nsteps * G * rows),
+                    PinnedVec<float>(pinned, (size_t)nsteps * G * rows), std::move(denom0), s};
             for (int t = 0; t < nsteps; ++t)
                 for (int g = 0; g < G; ++g)
                     fill(g, t, cl.ix.data() + ((size_t)t * G + g) * rows, cl.w.data() + ((size_t)t * G + g) * rows);
@@ -376,17 +437,19 @@ int mtk_sweep_run(mtk_ctx* ctx, const mtk_sweep_config* cfg, mtk_comm* comm, mtk
                 return v;
             });
         run_pipelined(epochs, [&](Call& cl) {
-            Dev dix = upload(cl.ix, st), dw = upload(cl.w, st);
-            ck(mtk_bank_train_epoch(bank.h, &cl.s, cl.pool->X.as<float>(), cl.pool->y.as<int32_t>(), cl.pool->rows,
-                                    dix.as<int64_t>(), dw.as<float>(), cl.den.data(), cl.nsteps),
-               "train_epoch");
+            with_uploaded(cl.ix, cl.w, dix_buf, dw_buf, st, [&](const int64_t* dix, const float* dw) {
+                ck(mtk_bank_train_epoch(bank.h, &cl.s, cl.pool->X.as<float>(), cl.pool->y.as<int32_t>(),
+                                        cl.pool->rows, dix, dw, cl.den.data(), cl.nsteps),
+                   "train_epoch");
+            });
         });
 
         trace("training");
         // ---- query_features: top-k posteriors of each model on its members
         // and non-members (the target-domain head) ----
         const int Q = 2 * c.members, kf = c.k;
-        Dev Xq((size_t)G * Q * d * 4), lq((size_t)G * Q * C * 4);
+        float* Xq = static_cast<float*>(ctx->sweep_buf((size_t)G * Q * d * 4));  // reused across sweeps
+        Dev lq((size_t)G * Q * C * 4);
         {
             std::vector<int64_t> qi((size_t)G * Q);
             for (int g = 0; g < G; ++g) {
@@ -394,8 +457,8 @@ int mtk_sweep_run(mtk_ctx* ctx, const mtk_sweep_config* cfg, mtk_comm* comm, mtk
                 std::copy(non[g].begin(), non[g].end(), qi.begin() + (size_t)g * Q + c.members);
             }
             Dev dqi = upload(qi, st);
-            ck(mtk_gather_rows(ctx, tgt.X.p, tgt.rows, d, dqi.as<int64_t>(), G, Q, Xq.p, Q, 0), "gather_rows");
-            ck(mtk_bank_forward(bank.h, Xq.as<float>(), Q, two ? 1 : 0, lq.as<float>(), nullptr), "forward");
+            ck(mtk_gather_rows(ctx, tgt.X.p, tgt.rows, d, dqi.as<int64_t>(), G, Q, Xq, Q, 0), "gather_rows");
+            ck(mtk_bank_forward(bank.h, Xq, Q, two ? 1 : 0, lq.as<float>(), nullptr), "forward");
             MTK_CUDA(cudaStreamSynchronize(st));
         }
         const int gmax = (M + world - 1) / world;  // the largest rank block (padded for the all-gather)
@@ -430,15 +493,15 @@ int mtk_sweep_run(mtk_ctx* ctx, const mtk_sweep_config* cfg, mtk_comm* comm, mtk
         ck(mtk_bank_init_params(att.h, 0, ar.h), "init_params");
         const float* Ftr = Fall.as<float>() + (size_t)Q * kf;  // models 1 .. M-1
         struct AttCall {
-            std::vector<int64_t> ix;
-            std::vector<float> w;
+            PinnedVec<int64_t> ix;
+            PinnedVec<float> w;
             std::vector<double> den;
         };
         std::vector<std::function<std::vector<AttCall>()>> aep(c.attack_epochs, [&]() {
             const Batches bl{ar.permutation((uint64_t)ntr), c.attack_batch};
             const int nb = bl.steps();
-            AttCall a{std::vector<int64_t>((size_t)nb * c.attack_batch), std::vector<float>((size_t)nb * c.attack_batch),
-                      std::vector<double>(nb)};
+            AttCall a{PinnedVec<int64_t>(pinned, (size_t)nb * c.attack_batch),
+                      PinnedVec<float>(pinned, (size_t)nb * c.attack_batch), std::vector<double>(nb)};
             for (int t = 0; t < nb; ++t) {
                 for (int r = 0; r < c.attack_batch; ++r) {
                     a.ix[(size_t)t * c.attack_batch + r] = bl.idx(t, r);
@@ -451,14 +514,15 @@ int mtk_sweep_run(mtk_ctx* ctx, const mtk_sweep_config* cfg, mtk_comm* comm, mtk
             return v;
         });
         run_pipelined(aep, [&](AttCall& a) {
-            Dev dix = upload(a.ix, st), dw = upload(a.w, st);
             mtk_step s{};
             s.B = c.attack_batch;
             s.lr = c.attack_lr;
             s.optimizer = c.attack_optimizer;
-            ck(mtk_bank_train_epoch(att.h, &s, Ftr, dl.as<int32_t>(), ntr, dix.as<int64_t>(), dw.as<float>(),
-                                    a.den.data(), (int)a.den.size()),
-               "attack train_epoch");
+            with_uploaded(a.ix, a.w, dix_buf, dw_buf, st, [&](const int64_t* dix, const float* dw) {
+                ck(mtk_bank_train_epoch(att.h, &s, Ftr, dl.as<int32_t>(), ntr, dix, dw, a.den.data(),
+                                        (int)a.den.size()),
+                   "attack train_epoch");
+            });
         });
 
         trace("attack train");
