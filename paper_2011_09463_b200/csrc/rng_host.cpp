@@ -6,6 +6,7 @@
 // weight initialisation is bit-identical to the reference.  Compiled with
 // -ffp-contract=off (rng.hpp:22 changes bits
 // under FMA contraction).  Sampling never runs on the device.
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -173,87 +174,118 @@ int mtk_rng_fill_normal(mtk_rng* r, double* out, uint64_t n) {
 // The population draws are sequential (one mt19937_64 stream: a label by
 // rejection, then d Box-Muller normals whose pairs straddle rows), but the
 // transcendentals dominate (19.3 M normals for the sweep's default pools:
-// ~0.4 s on one core).  So: one sequential pass takes every raw draw -- the
-// labels, and each Box-Muller pair's two raw words -- in stream order; the
-// pairs' normals (the same expressions as gauss(), so bit-identical) and the
-// rows are then formed on all host cores.
+// ~0.4 s on one core).  So the rows go in blocks: the calling thread takes
+// every raw draw of block b + 1 -- the labels, and each Box-Muller pair's two
+// raw words -- in stream order, while the other host cores turn block b's
+// pairs into normals (the same expressions as gauss(), so bit-identical) and
+// rows.  Two block-sized word buffers, no whole-stream intermediate arrays.
+namespace {
+struct SynthBlock {
+    uint64_t row0 = 0, rows = 0;
+    bool cached_in = false;  // the block's first normal is the pending sin value `carry`
+    double carry = 0.0;
+    std::vector<uint64_t> words;  // two per new Box-Muller pair, stream order
+};
+inline void box_muller(uint64_t w1, uint64_t w2, double& c, double& s) {  // gauss(), rng.hpp:24-37
+    const double u1 = 1.0 - static_cast<double>(w1 >> 11) * 0x1.0p-53;
+    const double u2 = static_cast<double>(w2 >> 11) * 0x1.0p-53;
+    const double rad = std::sqrt(-2.0 * std::log(u1));
+    const double theta = 6.28318530717958647692 * u2;
+    s = rad * std::sin(theta);
+    c = rad * std::cos(theta);
+}
+}  // namespace
+
 int mtk_synth(mtk_rng* r, int C, int d, uint64_t n, const double* mu, const double* shift,
               double* X64, float* X32, int32_t* y) {
     if (!r || !mu || !y) return set_err(MTK_VALUE_ERROR, "mtk_synth: null argument");
     if (C <= 0 || d <= 0) return set_err(MTK_SHAPE_ERROR, "mtk_synth: zero dimension");
-    const uint64_t total = n * static_cast<uint64_t>(d);  // gauss() calls, in stream order
-    // pass 1 (sequential): labels, and the raw words of every new pair
-    const bool cached0 = r->cached;
-    const double cache0 = r->cache;
-    std::vector<uint64_t> words;
-    words.reserve(static_cast<size_t>(total + 2));
-    bool cached = cached0;
-    for (uint64_t i = 0; i < n; ++i) {
-        y[i] = static_cast<int32_t>(r->bounded(static_cast<uint64_t>(C)));
-        for (int k = 0; k < d; ++k) {
-            if (cached) {
-                cached = false;
-            } else {
-                const uint64_t w1 = r->eng();
-                const uint64_t w2 = r->eng();
-                words.push_back(w1);
-                words.push_back(w2);
-                cached = true;
-            }
-        }
-    }
-    const size_t npairs = words.size() / 2;
-    // pass 2 (parallel): pair p -> (cos, sin) values, exactly as gauss()
-    std::vector<double> gc(npairs), gs(npairs);
-    auto pairs = [&](size_t a, size_t b) {
-        for (size_t p = a; p < b; ++p) {
-            const double u1 = 1.0 - static_cast<double>(words[2 * p] >> 11) * 0x1.0p-53;
-            const double u2 = static_cast<double>(words[2 * p + 1] >> 11) * 0x1.0p-53;
-            const double rad = std::sqrt(-2.0 * std::log(u1));
-            const double theta = 6.28318530717958647692 * u2;
-            gs[p] = rad * std::sin(theta);
-            gc[p] = rad * std::cos(theta);
-        }
-    };
-    // gauss call j (0-based, stream order): with the cache full on entry, call
-    // 0 returns cache0 and call j >= 1 belongs to pair (j - 1) / 2 (cos if
-    // (j - 1) even); otherwise pair j / 2 (cos if j even)
-    const uint64_t off = cached0 ? 1 : 0;
-    auto gauss_at = [&](uint64_t j) -> double {
-        if (cached0 && j == 0) return cache0;
-        const uint64_t q = j - off;
-        return (q & 1) ? gs[q >> 1] : gc[q >> 1];
-    };
-    auto rows = [&](uint64_t a, uint64_t b) {
-        for (uint64_t i = a; i < b; ++i) {
-            const double* mrow = mu + static_cast<size_t>(y[i]) * d;
-            for (int k = 0; k < d; ++k) {
-                double v = mrow[k] + gauss_at(i * d + k);
-                if (shift) v = v + shift[k];
-                if (X64) X64[i * d + k] = v;
-                if (X32) X32[i * d + k] = static_cast<float>(v);
-            }
-        }
-    };
+    const uint64_t total = n * static_cast<uint64_t>(d);
     unsigned nt = std::thread::hardware_concurrency();
     nt = nt == 0 ? 1 : (nt > 32 ? 32 : nt);
     if (total < (1u << 16)) nt = 1;
-    auto parallel = [&](uint64_t count, auto&& fn) {
+    const uint64_t R = std::max<uint64_t>(1, (uint64_t(1) << 20) / static_cast<uint64_t>(d));  // rows per block
+    bool cached = r->cached;
+    double pending = r->cache;  // the value a cached gauss() call returns
+    // sequential: block b's labels and pair words; leaves the cache state
+    auto draw = [&](SynthBlock& B, uint64_t row0) {
+        B.row0 = row0;
+        B.rows = std::min<uint64_t>(R, n - row0);
+        B.cached_in = cached;
+        B.carry = pending;
+        B.words.clear();
+        for (uint64_t i = row0; i < row0 + B.rows; ++i) {
+            y[i] = static_cast<int32_t>(r->bounded(static_cast<uint64_t>(C)));
+            for (int k = 0; k < d; ++k) {
+                if (cached) {
+                    cached = false;
+                } else {
+                    B.words.push_back(r->eng());
+                    B.words.push_back(r->eng());
+                    cached = true;
+                }
+            }
+        }
+        if (cached && !B.words.empty()) {  // the block's last pair leaves its sin value pending
+            double c, sv;
+            const size_t m = B.words.size();
+            box_muller(B.words[m - 2], B.words[m - 1], c, sv);
+            pending = sv;
+        }
+    };
+    // parallel: block element e (stream order) -> X[row0 + e / d][e % d]
+    auto put = [&](const SynthBlock& B, uint64_t e, double g) {
+        const uint64_t i = B.row0 + e / static_cast<uint64_t>(d);
+        const int k = static_cast<int>(e % static_cast<uint64_t>(d));
+        double v = mu[static_cast<size_t>(y[i]) * d + k] + g;
+        if (shift) v = v + shift[k];
+        if (X64) X64[i * d + k] = v;
+        if (X32) X32[i * d + k] = static_cast<float>(v);
+    };
+    auto form = [&](const SynthBlock& B, size_t pa, size_t pb) {  // pairs [pa, pb) of the block
+        const uint64_t elems = B.rows * static_cast<uint64_t>(d);
+        const uint64_t off = B.cached_in ? 1 : 0;
+        if (pa == 0 && B.cached_in) put(B, 0, B.carry);
+        for (size_t p = pa; p < pb; ++p) {
+            double c, sv;
+            box_muller(B.words[2 * p], B.words[2 * p + 1], c, sv);
+            const uint64_t e = off + 2 * p;
+            put(B, e, c);
+            if (e + 1 < elems) put(B, e + 1, sv);  // else: pending for the next block
+        }
+    };
+    auto form_all = [&](const SynthBlock& B, unsigned threads) {
+        const size_t np = B.words.size() / 2;
+        if (threads <= 1 || np < 4096) {
+            form(B, 0, np);
+            return;
+        }
         std::vector<std::thread> th;
-        for (unsigned t = 1; t < nt; ++t)
-            th.emplace_back([&, t] { fn(count * t / nt, count * (t + 1) / nt); });
-        fn(0, count / nt);
+        for (unsigned t = 1; t < threads; ++t)
+            th.emplace_back([&, t] { form(B, np * t / threads, np * (t + 1) / threads); });
+        form(B, 0, np / threads);
         for (auto& x : th) x.join();
     };
-    parallel(npairs, pairs);
-    parallel(n, rows);
-    // the generator's Box-Muller cache as the sequential loop leaves it
-    if (cached) {  // the last pair's sin value is pending
-        r->cached = true;
-        r->cache = cached0 && npairs == 0 ? cache0 : gs[npairs - 1];
-    } else {
-        r->cached = false;
+    SynthBlock blk[2];
+    if (n == 0) return MTK_OK;
+    draw(blk[0], 0);
+    int cur = 0;
+    for (uint64_t row0 = 0; row0 < n; row0 += R) {
+        const uint64_t next = row0 + R;
+        if (next < n && nt > 1) {
+            // the other cores form block `cur` while this thread draws the next one
+            std::thread former([&, cur] { form_all(blk[cur], nt - 1); });
+            draw(blk[cur ^ 1], next);
+            former.join();
+        } else {
+            form_all(blk[cur], nt);
+            if (next < n) draw(blk[cur ^ 1], next);
+        }
+        cur ^= 1;
     }
+    // the generator's Box-Muller cache as the sequential draws leave it
+    r->cached = cached;
+    r->cache = cached ? pending : r->cache;
     return MTK_OK;
 }
 

@@ -75,16 +75,18 @@ def test_host_rng_streams_and_synth_match_oracle():
     assert np.array_equal(X32, oX.astype(np.float32))
 
 
-@pytest.mark.parametrize("pre", [0, 1, 2])
-def test_parallel_synth_matches_sequential_stream(pre):
-    """mtk_synth draws the stream in one sequential pass and forms the normals
-    on all host cores: bit-identical to the oracle's sequential restatement for
-    a population past the threading threshold (odd d: Box-Muller pairs straddle
-    rows), entered with and without a cached normal, and the generator state it
-    leaves (the next normal, the next raw draw) is the sequential one."""
+@pytest.mark.parametrize("pre,n", [(0, 6001), (1, 6001), (2, 6001), (0, 57_452), (1, 57_452)])
+def test_parallel_synth_matches_sequential_stream(pre, n):
+    """mtk_synth draws the stream block by block on the calling thread while
+    the other host cores form the previous block's normals and rows:
+    bit-identical to the oracle's sequential restatement for a population past
+    the threading threshold (odd d: Box-Muller pairs straddle rows, and with
+    57,452 rows of 37 -- three blocks of 2^20 / 37 rows -- the block
+    boundaries), entered with and without a cached normal, and the generator
+    state it leaves (the next normal, the next raw draw) is the sequential one."""
     from paper_2011_09463_b200 import api
 
-    C_, d, n = 7, 37, 6001
+    C_, d = 7, 37
     mu = po.Rng(15).normals(C_ * d).reshape(C_, d)
     sh = po.Rng(16).normals(d)
     r, o = api.Rng(33), po.Rng(33)
