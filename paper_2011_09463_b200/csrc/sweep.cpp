@@ -26,6 +26,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "internal.h"
@@ -324,14 +325,51 @@ int mtk_sweep_run(mtk_ctx* ctx, const mtk_sweep_config* cfg, mtk_comm* comm, mtk
         const bool two = c.paradigm == MTK_PARADIGM_PARAMETER;
         Bank bank(ctx, G, dims, two ? 2 : 1);
         std::vector<std::vector<uint64_t>> mem(G), non(G), srcs(G);
-        for (int g = 0; g < G; ++g) {
-            Rng& r = streams[lo + g];
-            std::vector<uint64_t> perm = r.permutation((uint64_t)c.pool);
-            mem[g].assign(perm.begin(), perm.begin() + c.members);
-            non[g].assign(perm.begin() + c.members, perm.begin() + 2 * (size_t)c.members);
-            ck(mtk_bank_init_params(bank.h, g, r.h), "init_params");
-            std::vector<uint64_t> sp = r.permutation((uint64_t)c.source_pool);
-            srcs[g].assign(sp.begin(), sp.begin() + c.source_per_model);
+        // Each model's stream draws its member split, its weights (exactly as
+        // mtk_bank_init_params: uniform(-1/sqrt(fan_in), +) per matrix, zero
+        // biases) and its source subset, in that order.  The streams are
+        // independent, so the models are drawn on all host cores (up to 0.7 s
+        // on one core for 257 models of 1024-512-256-10) into one pinned
+        // [matrix][model] block, uploaded with one copy per matrix.
+        PinnedPool& pinned = ctx->host_pool();
+        const int L = (int)dims.size() - 1, n_mats = L + (two ? 1 : 0);
+        auto fan = [&](int i, int io) { return dims[(i < L ? i : L - 1) + io]; };
+        std::vector<size_t> mat_off(n_mats + 1, 0);  // floats of matrices 0..i-1, all models
+        for (int i = 0; i < n_mats; ++i) mat_off[i + 1] = mat_off[i] + (size_t)G * fan(i, 0) * fan(i, 1);
+        {
+            PinnedVec<float> hw(pinned, mat_off[n_mats]);
+            auto draw_models = [&](int g0, int g1) {
+                for (int g = g0; g < g1; ++g) {
+                    Rng& r = streams[lo + g];
+                    std::vector<uint64_t> perm = r.permutation((uint64_t)c.pool);
+                    mem[g].assign(perm.begin(), perm.begin() + c.members);
+                    non[g].assign(perm.begin() + c.members, perm.begin() + 2 * (size_t)c.members);
+                    for (int i = 0; i < n_mats; ++i) {
+                        const size_t nw = (size_t)fan(i, 0) * fan(i, 1);
+                        const double lim = 1.0 / std::sqrt((double)fan(i, 0));
+                        float* w = hw.data() + mat_off[i] + (size_t)g * nw;
+                        for (size_t j = 0; j < nw; ++j) w[j] = (float)mtk_rng_uniform(r.h, -lim, lim);
+                    }
+                    std::vector<uint64_t> sp = r.permutation((uint64_t)c.source_pool);
+                    srcs[g].assign(sp.begin(), sp.begin() + c.source_per_model);
+                }
+            };
+            unsigned nt = std::thread::hardware_concurrency();
+            nt = std::max(1u, std::min({nt, 32u, (unsigned)G}));
+            std::vector<std::future<void>> parts;
+            for (unsigned t = 1; t < nt; ++t)
+                parts.push_back(std::async(std::launch::async, draw_models, (int)((long long)G * t / nt),
+                                           (int)((long long)G * (t + 1) / nt)));
+            draw_models(0, (int)((long long)G / nt));
+            for (auto& f : parts) f.get();  // (rethrows a worker's failure)
+            for (int i = 0; i < n_mats; ++i) {
+                float *Wd = nullptr, *bd = nullptr;
+                ck(mtk_bank_param_device(bank.h, i, &Wd, &bd), "param_device");
+                MTK_CUDA(cudaMemcpyAsync(Wd, hw.data() + mat_off[i], (mat_off[i + 1] - mat_off[i]) * 4,
+                                         cudaMemcpyHostToDevice, st));
+                MTK_CUDA(cudaMemsetAsync(bd, 0, (size_t)G * fan(i, 1) * 4, st));
+            }
+            MTK_CUDA(cudaStreamSynchronize(st));  // before the pinned block is recycled
         }
         const int B = c.batch;
         mtk_step tmpl{};
@@ -349,7 +387,6 @@ int mtk_sweep_run(mtk_ctx* ctx, const mtk_sweep_config* cfg, mtk_comm* comm, mtk
             std::vector<double> den;
             mtk_step s;
         };
-        PinnedPool& pinned = ctx->host_pool();
         DevBuf dix_buf, dw_buf;
         auto make_call = [&](const Pool& pool, int rows, int nsteps,
                              const std::function<void(int g, int t, int64_t* ix, float* w)>& fill,
