@@ -96,8 +96,8 @@ struct Ctx {
     size_t auc_l2_bytes = 0;
     HostBlockPool* host_blocks = nullptr;  // the native sweep's pinned staging (sweep.cpp)
     HostBlockPool& host_pool();
-    // grow-only device workspace of the native sweep (the query rows of every
-    // model: G x Q x d floats, GBs at C5 -- allocated once per context)
+    // grow-only device workspace of the native sweep (one chunk of query rows
+    // of every model: G x rows x d floats -- allocated once per context)
     void* sweep_buf(size_t bytes);
     void* d_sweep = nullptr;
     size_t sweep_bytes = 0;

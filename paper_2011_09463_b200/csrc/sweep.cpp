@@ -485,17 +485,33 @@ int mtk_sweep_run(mtk_ctx* ctx, const mtk_sweep_config* cfg, mtk_comm* comm, mtk
         // ---- query_features: top-k posteriors of each model on its members
         // and non-members (the target-domain head) ----
         const int Q = 2 * c.members, kf = c.k;
-        float* Xq = static_cast<float*>(ctx->sweep_buf((size_t)G * Q * d * 4));  // reused across sweeps
-        Dev lq((size_t)G * Q * C * 4);
+        // in chunks of the training batch's rows: the bank's activation
+        // buffers (sized by training) are reused; a whole-Q forward would
+        // allocate them for 4096 rows x 257 models (GBs, per sweep)
+        const int qb = std::min(Q, c.paradigm == MTK_PARADIGM_MODEL ? B : 2 * B);
+        const int nchunk = (Q + qb - 1) / qb;
+        Dev lq((size_t)G * Q * C * 4), lc((size_t)G * qb * C * 4);
         {
+            // chunk-major indices: chunk k holds [G][rows of the chunk]
             std::vector<int64_t> qi((size_t)G * Q);
-            for (int g = 0; g < G; ++g) {
-                std::copy(mem[g].begin(), mem[g].end(), qi.begin() + (size_t)g * Q);
-                std::copy(non[g].begin(), non[g].end(), qi.begin() + (size_t)g * Q + c.members);
+            size_t o = 0;
+            for (int k = 0; k < nchunk; ++k) {
+                const int q0 = k * qb, nq = std::min(qb, Q - q0);
+                for (int g = 0; g < G; ++g)
+                    for (int q = q0; q < q0 + nq; ++q)
+                        qi[o++] = (int64_t)(q < c.members ? mem[g][q] : non[g][q - c.members]);
             }
             Dev dqi = upload(qi, st);
-            ck(mtk_gather_rows(ctx, tgt.X.p, tgt.rows, d, dqi.as<int64_t>(), G, Q, Xq, Q, 0), "gather_rows");
-            ck(mtk_bank_forward(bank.h, Xq, Q, two ? 1 : 0, lq.as<float>(), nullptr), "forward");
+            float* Xc = static_cast<float*>(ctx->sweep_buf((size_t)G * qb * d * 4));  // reused across sweeps
+            for (int k = 0; k < nchunk; ++k) {
+                const int q0 = k * qb, nq = std::min(qb, Q - q0);
+                ck(mtk_gather_rows(ctx, tgt.X.p, tgt.rows, d, dqi.as<int64_t>() + (size_t)G * q0, G, nq, Xc, nq, 0),
+                   "gather_rows");
+                ck(mtk_bank_forward(bank.h, Xc, nq, two ? 1 : 0, lc.as<float>(), nullptr), "forward");
+                MTK_CUDA(cudaMemcpy2DAsync(lq.as<float>() + (size_t)q0 * C, (size_t)Q * C * 4, lc.p,
+                                           (size_t)nq * C * 4, (size_t)nq * C * 4, G, cudaMemcpyDeviceToDevice,
+                                           st));
+            }
             MTK_CUDA(cudaStreamSynchronize(st));
         }
         const int gmax = (M + world - 1) / world;  // the largest rank block (padded for the all-gather)
