@@ -194,6 +194,27 @@ void run_pipelined(std::vector<std::function<std::vector<T>()>>& items, F&& cons
     }
 }
 
+// f(i) for i in [0, n) on all host cores (contiguous ranges; f must only
+// touch state of its own i -- here: model g's stream, rows of step t)
+template <class F>
+void parallel_for(int n, F&& f) {
+    unsigned nt = std::thread::hardware_concurrency();
+    nt = std::max(1u, std::min({nt, 16u, (unsigned)std::max(n, 1)}));
+    if (nt == 1 || n < 8) {
+        for (int i = 0; i < n; ++i) f(i);
+        return;
+    }
+    auto range = [&](int a, int b) {
+        for (int i = a; i < b; ++i) f(i);
+    };
+    std::vector<std::future<void>> parts;
+    for (unsigned t = 1; t < nt; ++t)
+        parts.push_back(std::async(std::launch::async, range, (int)((long long)n * t / nt),
+                                   (int)((long long)n * (t + 1) / nt)));
+    range(0, (int)((long long)n / nt));
+    for (auto& p : parts) p.get();
+}
+
 struct Pool {  // a device-resident population: X [rows, d] fp32, y [rows] int32
     Dev X, y;
     int64_t rows = 0;
@@ -393,15 +414,16 @@ int mtk_sweep_run(mtk_ctx* ctx, const mtk_sweep_config* cfg, mtk_comm* comm, mtk
                              std::vector<double> denom0, mtk_step s) {
             Call cl{&pool, rows, nsteps, PinnedVec<int64_t>(pinned, (size_t)nsteps * G * rows),
                     PinnedVec<float>(pinned, (size_t)nsteps * G * rows), std::move(denom0), s};
-            for (int t = 0; t < nsteps; ++t)
-                for (int g = 0; g < G; ++g)
+            parallel_for(G, [&](int g) {  // the fills read model g's state only
+                for (int t = 0; t < nsteps; ++t)
                     fill(g, t, cl.ix.data() + ((size_t)t * G + g) * rows, cl.w.data() + ((size_t)t * G + g) * rows);
+            });
             cl.s.B = rows;
             return cl;
         };
-        auto model_orders = [&](uint64_t n) {
-            std::vector<Batches> o;
-            for (int g = 0; g < G; ++g) o.push_back(Batches{streams[lo + g].permutation(n), B});
+        auto model_orders = [&](uint64_t n) {  // one permutation per model stream (independent)
+            std::vector<Batches> o(G, Batches{{}, B});
+            parallel_for(G, [&](int g) { o[g].order = streams[lo + g].permutation(n); });
             return o;
         };
         std::vector<std::function<std::vector<Call>()>> epochs;
@@ -555,13 +577,13 @@ int mtk_sweep_run(mtk_ctx* ctx, const mtk_sweep_config* cfg, mtk_comm* comm, mtk
             const int nb = bl.steps();
             AttCall a{PinnedVec<int64_t>(pinned, (size_t)nb * c.attack_batch),
                       PinnedVec<float>(pinned, (size_t)nb * c.attack_batch), std::vector<double>(nb)};
-            for (int t = 0; t < nb; ++t) {
+            parallel_for(nb, [&](int t) {
                 for (int r = 0; r < c.attack_batch; ++r) {
                     a.ix[(size_t)t * c.attack_batch + r] = bl.idx(t, r);
                     a.w[(size_t)t * c.attack_batch + r] = bl.w(t, r);
                 }
                 a.den[t] = bl.wsum(t);
-            }
+            });
             std::vector<AttCall> v;
             v.push_back(std::move(a));
             return v;
