@@ -499,6 +499,11 @@ inline int guard(F&& f) {
 // per device under a mutex.
 int current_device();
 int device_sm_count(int device);
+// permutation(n) of mt::Rng (rng.hpp:48-56, rng_host.cpp) in two stages, so
+// a caller can pipeline them: the Fisher-Yates targets (the stream's draws,
+// js[n - 1], raw[n - 1] scratch), then the swaps (w[n] scratch)
+void rng_permutation_targets(mtk_rng* r, uint64_t n, uint32_t* js, uint64_t* raw);
+void permutation_apply(uint64_t n, const uint32_t* js, uint32_t* w, uint64_t* out);
 // raise `func`'s dynamic shared-memory limit to `bytes` on the current device
 // (once per (device, func))
 void ensure_smem_attr(const void* func, int bytes);

@@ -95,6 +95,60 @@ uint64_t mtk_rng_below(mtk_rng* r, uint64_t n) { return r->bounded(n); }
 // random targets prefetched a few iterations ahead, on a 32-bit working
 // array when n < 2^32 (the attack sweep permutes 2^20 rows every epoch:
 // the swaps were bound by cache misses).  Same stream use, same result.
+}  // extern "C"
+
+namespace mtk {
+// the Fisher-Yates targets of permutation(n) (n >= 2, n < 2^32): js[k] =
+// bounded(n - k), k = 0 .. n - 2, drawn in stream order -- the raw words in
+// one sequential pass, the reductions (two 64-bit divisions each) on all
+// cores.  A rejection (a word >= the cut: ~top / 2^64) would shift the
+// stream: then the engine is restored and the targets drawn one by one, as
+// bounded() does.
+void rng_permutation_targets(mtk_rng* r, uint64_t n, uint32_t* js, uint64_t* raw) {
+    const std::mt19937_64 saved = r->eng;
+    for (uint64_t k = 0; k + 1 < n; ++k) raw[k] = r->eng();
+    unsigned nt = std::thread::hardware_concurrency();
+    nt = nt == 0 ? 1 : (nt > 16 ? 16 : nt);
+    if (n < (1u << 16)) nt = 1;
+    std::vector<char> rejected(nt, 0);
+    auto part = [&](unsigned t) {
+        const uint64_t a = (n - 1) * t / nt, b = (n - 1) * (t + 1) / nt;
+        for (uint64_t k = a; k < b; ++k) {
+            const uint64_t top = n - k, cut = UINT64_MAX - UINT64_MAX % top;
+            if (raw[k] >= cut) rejected[t] = 1;
+            js[k] = static_cast<uint32_t>(raw[k] % top);
+        }
+    };
+    std::vector<std::thread> th;
+    for (unsigned t = 1; t < nt; ++t) th.emplace_back(part, t);
+    part(0);
+    for (auto& x : th) x.join();
+    bool any = false;
+    for (char c : rejected) any |= c != 0;
+    if (any) {
+        r->eng = saved;
+        for (uint64_t k = 0, top = n; top > 1; --top, ++k) js[k] = static_cast<uint32_t>(r->bounded(top));
+    }
+}
+
+// the swaps of permutation(n) for targets js, top down (w: n words of scratch)
+void permutation_apply(uint64_t n, const uint32_t* js, uint32_t* w, uint64_t* out) {
+    for (uint64_t i = 0; i < n; ++i) w[i] = static_cast<uint32_t>(i);
+    constexpr uint64_t kAhead = 16;
+    const uint64_t steps = n - 1;
+    for (uint64_t k = 0; k < steps; ++k) {
+        if (k + kAhead < steps) __builtin_prefetch(&w[js[k + kAhead]], 1, 0);
+        const uint64_t top = n - k, j = js[k];
+        const uint32_t t = w[top - 1];
+        w[top - 1] = w[j];
+        w[j] = t;
+    }
+    for (uint64_t i = 0; i < n; ++i) out[i] = w[i];
+}
+}  // namespace mtk
+
+extern "C" {
+
 int mtk_rng_permutation(mtk_rng* r, uint64_t n, uint64_t* out) {
     if (!r || (!out && n)) return set_err(MTK_VALUE_ERROR, "mtk_rng_permutation: null argument");
     if (n < 2 || n >= (1ull << 32)) {
@@ -121,47 +175,8 @@ int mtk_rng_permutation(mtk_rng* r, uint64_t n, uint64_t* out) {
     if (js.size() < n - 1) js.resize(n - 1);
     if (w.size() < n) w.resize(n);
     if (raw.size() < n - 1) raw.resize(n - 1);
-    // the targets: raw words drawn in stream order, then the reductions
-    // (two 64-bit divisions each) on all cores.  A rejection (a word >= the
-    // cut: ~top / 2^64) would shift the stream: then the engine is restored
-    // and the targets drawn one by one, as bounded() does.
-    {
-        const std::mt19937_64 saved = r->eng;
-        for (uint64_t k = 0; k + 1 < n; ++k) raw[k] = r->eng();
-        unsigned nt = std::thread::hardware_concurrency();
-        nt = nt == 0 ? 1 : (nt > 16 ? 16 : nt);
-        if (n < (1u << 16)) nt = 1;
-        std::vector<char> rejected(nt, 0);
-        auto part = [&](unsigned t) {
-            const uint64_t a = (n - 1) * t / nt, b = (n - 1) * (t + 1) / nt;
-            for (uint64_t k = a; k < b; ++k) {
-                const uint64_t top = n - k, cut = UINT64_MAX - UINT64_MAX % top;
-                if (raw[k] >= cut) rejected[t] = 1;
-                js[k] = static_cast<uint32_t>(raw[k] % top);
-            }
-        };
-        std::vector<std::thread> th;
-        for (unsigned t = 1; t < nt; ++t) th.emplace_back(part, t);
-        part(0);
-        for (auto& x : th) x.join();
-        bool any = false;
-        for (char c : rejected) any |= c != 0;
-        if (any) {
-            r->eng = saved;
-            for (uint64_t k = 0, top = n; top > 1; --top, ++k) js[k] = static_cast<uint32_t>(r->bounded(top));
-        }
-    }
-    for (uint64_t i = 0; i < n; ++i) w[i] = static_cast<uint32_t>(i);
-    constexpr uint64_t kAhead = 16;
-    const uint64_t steps = n - 1;
-    for (uint64_t k = 0; k < steps; ++k) {
-        if (k + kAhead < steps) __builtin_prefetch(&w[js[k + kAhead]], 1, 0);
-        const uint64_t top = n - k, j = js[k];
-        const uint32_t t = w[top - 1];
-        w[top - 1] = w[j];
-        w[j] = t;
-    }
-    for (uint64_t i = 0; i < n; ++i) out[i] = w[i];
+    mtk::rng_permutation_targets(r, n, js.data(), raw.data());
+    mtk::permutation_apply(n, js.data(), w.data(), out);
     return MTK_OK;
 }
 

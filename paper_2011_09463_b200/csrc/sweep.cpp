@@ -20,7 +20,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <condition_variable>
 #include <cstring>
+#include <deque>
 #include <functional>
 #include <future>
 #include <memory>
@@ -507,6 +509,7 @@ int mtk_sweep_run(mtk_ctx* ctx, const mtk_sweep_config* cfg, mtk_comm* comm, mtk
         // ---- query_features: top-k posteriors of each model on its members
         // and non-members (the target-domain head) ----
         const int Q = 2 * c.members, kf = c.k;
+        trace("features: start");
         // in chunks of the training batch's rows: the bank's activation
         // buffers (sized by training) are reused; a whole-Q forward would
         // allocate them for 4096 rows x 257 models (GBs, per sweep)
@@ -536,6 +539,7 @@ int mtk_sweep_run(mtk_ctx* ctx, const mtk_sweep_config* cfg, mtk_comm* comm, mtk
             }
             MTK_CUDA(cudaStreamSynchronize(st));
         }
+        trace("features: posteriors");
         const int gmax = (M + world - 1) / world;  // the largest rank block (padded for the all-gather)
         const size_t blk = (size_t)gmax * Q * kf;
         Dev F(blk * 4);
@@ -572,8 +576,61 @@ int mtk_sweep_run(mtk_ctx* ctx, const mtk_sweep_config* cfg, mtk_comm* comm, mtk
             PinnedVec<float> w;
             std::vector<double> den;
         };
+        // Three stages: a thread draws each epoch's Fisher-Yates targets from
+        // the attack stream (sequential, up to two epochs ahead); the epoch
+        // builder applies the swaps and fills the batch indices; the caller
+        // trains.  The permutations are the stream's own (rng_host.cpp).
+        const bool staged = ntr >= 2 && ntr < (int64_t(1) << 32);
+        std::mutex qm;
+        std::condition_variable qcv;
+        std::deque<std::vector<uint32_t>> tq;
+        bool tstop = false;
+        std::thread tthread;
+        if (staged)
+            tthread = std::thread([&] {
+                std::vector<uint64_t> raw((size_t)ntr - 1);
+                for (int e = 0; e < c.attack_epochs; ++e) {
+                    std::vector<uint32_t> js((size_t)ntr - 1);
+                    rng_permutation_targets(ar.h, (uint64_t)ntr, js.data(), raw.data());
+                    std::unique_lock<std::mutex> lk(qm);
+                    qcv.wait(lk, [&] { return tq.size() < 2 || tstop; });
+                    if (tstop) return;
+                    tq.push_back(std::move(js));
+                    qcv.notify_all();
+                }
+            });
+        struct JoinTargets {  // on every exit path
+            std::thread& t;
+            std::mutex& m;
+            std::condition_variable& cv;
+            bool& stop;
+            ~JoinTargets() {
+                {
+                    std::lock_guard<std::mutex> lk(m);
+                    stop = true;
+                }
+                cv.notify_all();
+                if (t.joinable()) t.join();
+            }
+        } join_targets{tthread, qm, qcv, tstop};
+        std::vector<uint64_t> order_buf(staged ? (size_t)ntr : 0);
+        std::vector<uint32_t> swap_buf(staged ? (size_t)ntr : 0);
+        auto next_order = [&]() -> std::vector<uint64_t> {
+            if (!staged) return ar.permutation((uint64_t)ntr);
+            std::vector<uint32_t> js;
+            {
+                std::unique_lock<std::mutex> lk(qm);
+                qcv.wait(lk, [&] { return !tq.empty(); });
+                js = std::move(tq.front());
+                tq.pop_front();
+            }
+            qcv.notify_all();
+            order_buf.resize((size_t)ntr);
+            permutation_apply((uint64_t)ntr, js.data(), swap_buf.data(), order_buf.data());
+            return std::move(order_buf);  // (handed back after the fill)
+        };
         std::vector<std::function<std::vector<AttCall>()>> aep(c.attack_epochs, [&]() {
-            const Batches bl{ar.permutation((uint64_t)ntr), c.attack_batch};
+            Batches bl{next_order(), c.attack_batch};
             const int nb = bl.steps();
             AttCall a{PinnedVec<int64_t>(pinned, (size_t)nb * c.attack_batch),
                       PinnedVec<float>(pinned, (size_t)nb * c.attack_batch), std::vector<double>(nb)};
@@ -584,6 +641,7 @@ int mtk_sweep_run(mtk_ctx* ctx, const mtk_sweep_config* cfg, mtk_comm* comm, mtk
                 }
                 a.den[t] = bl.wsum(t);
             });
+            if (staged) order_buf = std::move(bl.order);  // the next epoch's swap output
             std::vector<AttCall> v;
             v.push_back(std::move(a));
             return v;
