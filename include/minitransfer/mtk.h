@@ -294,7 +294,8 @@ int mtk_auc(mtk_ctx* ctx, const float* scores, const uint8_t* labels, int64_t n,
  * (softmax column 1) -> mid-rank AUC + accuracy at 0.5.  Same results as
  * mtk_posterior_features + mtk_bank_forward + mtk_posterior_column + mtk_auc
  * (bit-identical scores); the [3, 64, 2] attack model over <= 16 classes runs
- * as one streaming kernel with the weights in constant memory.  scores_out
+ * as one streaming kernel, each CTA staging the weights from the bank in
+ * shared memory, then one scan kernel for the AUC.  scores_out
  * (device, [rows]) may be NULL.  Synchronizing.  Stands in for the absent
  * reference attack stage.                   */
 int mtk_attack_auc(mtk_bank* attack, const float* logits, int64_t rows, int C, const uint8_t* labels,
