@@ -744,6 +744,7 @@ struct MmdWParams {
     double* kpart;             // [G][npairs][W_EPI_WARPS][3]: kernel sums per epilogue warp
     int* flags;
     int diag;                  // diagnostics (MTK_MMDW_DIAG): 1 = epilogue only arrives, 2 = no MMAs
+    int no_diag_share;         // A/B (MTK_MMDW_NO_DIAG_SHARE): diagonal tiles load Z_J too
 };
 
 // unordered tile pair p -> (I, J), I <= J, row-major over the upper triangle
@@ -858,17 +859,20 @@ __global__ void __launch_bounds__(W_THREADS, 1) mmd_w_kernel(const __grid_consta
             int I, J, pidx_;
             item_pair(p, item % nloc, I, J, pidx_);
             const int i0 = I * WT, j0 = J * WT;
+            const bool dg = I == J && !p.no_diag_share;  // a diagonal tile: Z_J is Z_I, two planes only
             for (int kc = 0; kc < nkc; ++kc, ++st) {
                 const int s = st % W_STAGES;
                 mbar_wait(&empty[s], ((st / W_STAGES) & 1) ^ 1);
                 if (lane == 0) {
                     uint8_t* b = smem + s * W_STAGE_BYTES;
                     const int k0 = kc * KC;
-                    mbar_expect_tx(&full[s], W_STAGE_BYTES);
+                    mbar_expect_tx(&full[s], dg ? W_STAGE_BYTES / 2 : W_STAGE_BYTES);
                     tma_load_3d(b, &p.zk_hi, &full[s], k0, i0, g);  // 128-row boxes (16 KB each)
                     tma_load_3d(b + 16384, &p.zk_lo, &full[s], k0, i0, g);
-                    tma_load_3d(b + 32768, &p.zk_lo, &full[s], k0, j0, g);
-                    tma_load_3d(b + 49152, &p.zk_hi, &full[s], k0, j0, g);
+                    if (!dg) {
+                        tma_load_3d(b + 32768, &p.zk_lo, &full[s], k0, j0, g);
+                        tma_load_3d(b + 49152, &p.zk_hi, &full[s], k0, j0, g);
+                    }
                 }
                 __syncwarp();
             }
@@ -881,6 +885,13 @@ __global__ void __launch_bounds__(W_THREADS, 1) mmd_w_kernel(const __grid_consta
         for (int item = blockIdx.x; item < total; item += gridDim.x, ++lt) {
             const int buf = lt & 1;
             const uint32_t tS = tmem + buf * 256;
+            int I, J, pidx_;
+            item_pair(p, item % nloc, I, J, pidx_);
+            // a diagonal tile reads Z_I as both operands: B = [Z_I hi | Z_I lo] puts
+            // hi.hi (+ lo.hi, second MMA) in columns [0, 128) and hi.lo in
+            // [128, 256) -- the two blocks of an off-diagonal tile, swapped; the
+            // epilogue adds them (commutative: the same bits)
+            const bool dg = I == J && !p.no_diag_share;
             mbar_wait(&acc_empty[buf], ((lt >> 1) & 1) ^ 1);
             tc_fence_after();
             for (int kc = 0; kc < nkc; ++kc, ++st) {
@@ -894,10 +905,16 @@ __global__ void __launch_bounds__(W_THREADS, 1) mmd_w_kernel(const __grid_consta
                         if (p.diag == 2) break;
                         const uint64_t ahi = smem_desc(b + kk * 32, 16, 1024, 2);
                         const uint64_t alo = smem_desc(b + 16384 + kk * 32, 16, 1024, 2);
-                        const uint64_t blh = smem_desc(b + 32768 + kk * 32, 16, 1024, 2);  // lo 128 | hi 128
-                        const uint64_t bhi = smem_desc(b + 49152 + kk * 32, 16, 1024, 2);
-                        mma_tf32(tS, ahi, blh, idw, (kc | kk) ? 1u : 0u);
-                        mma_tf32(tS + WT, alo, bhi, idn, 1u);
+                        if (dg) {
+                            const uint64_t bhl = smem_desc(b + kk * 32, 16, 1024, 2);  // hi 128 | lo 128
+                            mma_tf32(tS, ahi, bhl, idw, (kc | kk) ? 1u : 0u);
+                            mma_tf32(tS, alo, ahi, idn, 1u);
+                        } else {
+                            const uint64_t blh = smem_desc(b + 32768 + kk * 32, 16, 1024, 2);  // lo 128 | hi 128
+                            const uint64_t bhi = smem_desc(b + 49152 + kk * 32, 16, 1024, 2);
+                            mma_tf32(tS, ahi, blh, idw, (kc | kk) ? 1u : 0u);
+                            mma_tf32(tS + WT, alo, bhi, idn, 1u);
+                        }
                     }
                     mma_commit(&empty[s]);
                 }
@@ -1537,6 +1554,7 @@ void launch_mmd_tc(const MmdArgs& a, void* scratch, cudaStream_t s, int stages) 
         w.kpart = L.kpart;
         w.flags = a.flags;
         if (const char* e = getenv("MTK_MMDW_DIAG")) w.diag = atoi(e);
+        w.no_diag_share = getenv_flag("MTK_MMDW_NO_DIAG_SHARE") ? 1 : 0;
         ensure_smem_attr(reinterpret_cast<const void*>(mmd_w_kernel), W_SMEM_BYTES);
         const int sms = device_sm_count(current_device());
         const int items = a.G * (w.nA + w.nB);

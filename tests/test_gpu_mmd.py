@@ -185,6 +185,28 @@ def test_mmd_api_materialised_w_path(ctx, monkeypatch, m, n, d):
     assert rel(gs0, ogs) <= 1e-5 and rel(gt0, ogt) <= 1e-5
 
 
+@pytest.mark.parametrize("m,n,d", [(512, 512, 256), (700, 324, 64)])
+def test_mmd_w_diagonal_tiles_share_operands_bit_identically(ctx, monkeypatch, m, n, d):
+    """mmd_w loads a diagonal tile pair's operand planes once and swaps the
+    two accumulator blocks (B = [Z_I hi | Z_I lo]); the epilogue's sum is
+    commutative, so value, bandwidth and gradients are bit-identical to
+    loading Z_J separately (MTK_MMDW_NO_DIAG_SHARE=1)."""
+    from paper_2011_09463_b200 import api
+
+    rng = np.random.default_rng(m + 3 * d)
+    Z = rng.standard_normal((m + n, d)).astype(np.float32)
+    Z[m:] += 0.25
+    Zd = torch.tensor(Z, device="cuda")
+    res = []
+    for off in ("0", "1"):
+        monkeypatch.setenv("MTK_MMDW_NO_DIAG_SHARE", off)
+        v, beta, gs, gt = api.mmd_gaussian(ctx, Zd[:m], Zd[m:])
+        res.append((v, beta, gs.cpu().numpy(), gt.cpu().numpy()))
+    (v0, b0, gs0, gt0), (v1, b1, gs1, gt1) = res
+    assert v0 == v1 and b0 == b1
+    assert np.array_equal(gs0, gs1) and np.array_equal(gt0, gt1)
+
+
 def _f64_mmd_reference(Z, m, beta, rows, mult=(0.25, 0.5, 1.0, 2.0, 4.0), tile=4096):
     """Independent fp64 evaluation on the GPU (torch float64, tiled): the
     V-statistic MMD^2 over ALL pairs and the gradient of the given rows, in
