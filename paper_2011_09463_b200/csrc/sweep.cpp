@@ -315,16 +315,28 @@ int mtk_sweep_run(mtk_ctx* ctx, const mtk_sweep_config* cfg, mtk_comm* comm, mtk
                                  src.y.as<int32_t>()), "synth_counter");
             MTK_CUDA(cudaStreamSynchronize(st));
         } else {
-            for (Pool* p : {&tgt, &src}) {
-                std::vector<float> X((size_t)p->rows * d);
-                std::vector<int32_t> y((size_t)p->rows);
-                ck(mtk_synth(data.h, C, d, (uint64_t)p->rows, mu.data(), p == &tgt ? shift.data() : nullptr,
-                             nullptr, X.data(), y.data()),
-                   "synth");
-                MTK_CUDA(cudaMemcpyAsync(p->X.p, X.data(), X.size() * 4, cudaMemcpyHostToDevice, st));
-                MTK_CUDA(cudaMemcpyAsync(p->y.p, y.data(), y.size() * 4, cudaMemcpyHostToDevice, st));
-                MTK_CUDA(cudaStreamSynchronize(st));
+            // drawn straight into recycled pinned blocks; each pool's upload
+            // overlaps the next pool's draws
+            PinnedPool& hp = ctx->host_pool();
+            PinnedVec<float> X[2];
+            PinnedVec<int32_t> y[2];
+            int i = 0;
+            try {
+                for (Pool* p : {&tgt, &src}) {
+                    X[i] = PinnedVec<float>(hp, (size_t)p->rows * d);
+                    y[i] = PinnedVec<int32_t>(hp, (size_t)p->rows);
+                    ck(mtk_synth(data.h, C, d, (uint64_t)p->rows, mu.data(), p == &tgt ? shift.data() : nullptr,
+                                 nullptr, X[i].data(), y[i].data()),
+                       "synth");
+                    MTK_CUDA(cudaMemcpyAsync(p->X.p, X[i].data(), X[i].size() * 4, cudaMemcpyHostToDevice, st));
+                    MTK_CUDA(cudaMemcpyAsync(p->y.p, y[i].data(), y[i].size() * 4, cudaMemcpyHostToDevice, st));
+                    ++i;
+                }
+            } catch (...) {
+                cudaStreamSynchronize(st);  // queued copies still read the blocks
+                throw;
             }
+            MTK_CUDA(cudaStreamSynchronize(st));  // before the blocks are recycled
         }
         // one combined pool [source; target] for the co-training paradigms'
         // epochs (a step's batch is source rows then member rows)
